@@ -1,0 +1,153 @@
+/* kdb.h -- C-ABI of the B200-native kNN-DBSCAN clustering stage.
+ *
+ * The stage (Alg. 1 "Parallel kNN-DBSCAN") takes a directed
+ * k-nearest-neighbour graph G_k of N points (k >= M) split into contiguous row
+ * ranges over p processes ("we partition points evenly into each
+ * process"), a radius eps and a minimum neighbourhood size M, and returns
+ *   - core flags            (Alg. 1 lines 3-8; Lemma 1(i)),
+ *   - the exact minimum spanning forest of the core-core candidate edges
+ *     (Alg. 2/3 Boruvka; Def. 10 / Thm. 2),
+ *   - canonical labels: the minimum core index of a point's component, -1 noise
+ *     (north_star; border rule = Lemma 1(ii), "ClusterBorder" PAPER.md:543).
+ *
+ * Graph convention (SURVEY.md §8(c) readings #1, #17-#19):
+ *   row i lists i's neighbours EXCLUDING i itself, weights non-decreasing fp32,
+ *   padding entries are (id -1, weight +inf) at the row tail.  core(i) is
+ *   D[i][M-1] <= eps, i.e. at least M other points within eps.
+ * Candidate edges: every stored entry (i, c) with J = nbr[i][c] >= 0, J != i,
+ *   core(i), core(J) and D[i][c] <= eps is the UNDIRECTED edge {i, J} with
+ *   weight w = D[i][c] (reading #3: all k columns; reading #4: undirected).
+ * Edge order O1 (reading #6): (mono(w), a = min(i,J), b = max(i,J)) where
+ *   mono(w) is the fp32 bit pattern with -0 canonicalised to +0.  The MSF under
+ *   this strict order is unique; kdb_mst returns exactly it.
+ *
+ * Conventions for every call:
+ *   - All array arguments are DEVICE pointers owned by the caller (the library
+ *     never allocates device memory outside `workspace` and keeps no global
+ *     device state).  Host pointers are marked "host".
+ *   - Work is ordered on `stream` (a cudaStream_t).  kdb_core_mark and kdb_label
+ *     are asynchronous; kdb_mst synchronises `stream` (one small read-back per
+ *     Boruvka round) and returns host scalars.
+ *   - Host-side argument validation runs before any launch; on failure nothing
+ *     is launched and KDB_EINVAL is returned.  kdb_last_error() gives a
+ *     thread-local message for the most recent non-OK status.
+ *   - Multi-GPU: every rank calls with the same N, M, eps and a communicator;
+ *     rank r passes its own rows [row_begin, row_begin + n_rows).  Outputs that
+ *     are documented as replicated are identical on every rank.
+ */
+#ifndef KDB_H_
+#define KDB_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  KDB_OK = 0,
+  KDB_EINVAL = 1,    /* invalid argument (see each call)                         */
+  KDB_ENOMEM = 2,    /* workspace smaller than kdb_mst_workspace_bytes()         */
+  KDB_ECUDA = 3,     /* CUDA runtime error; message in kdb_last_error()          */
+  KDB_ENCCL = 4,     /* NCCL error / NCCL library not loadable                   */
+  KDB_EINTERNAL = 5  /* internal invariant violated (a bug); message attached    */
+} kdb_status;
+
+typedef struct CUstream_st* kdb_stream_t; /* == cudaStream_t */
+
+/* Caller promise: the graph is an EXACT kNN graph of a point set under a
+ * symmetric distance (rows hold each point's k nearest other points; every
+ * weight is d(i,J) computed identically from both ends).  Under this promise
+ * an entry u->v that v's row does not mirror has w >= D[v][k-1],
+ * which lets kdb_mst skip building reverse-edge lists.  Without it kdb_mst
+ * materialises in-edge lists in the workspace (correct for ANY valid graph,
+ * e.g. the approximate graph of Fig. cycle). */
+#define KDB_GRAPH_EXACT 1u
+
+typedef struct {
+  int64_t n_total;     /* N = |I|, all ranks                                        */
+  int64_t row_begin;   /* first global row id held by this rank                     */
+  int64_t n_rows;      /* rows held by this rank; [row_begin, row_begin+n_rows) in [0,N) */
+  int32_t k_max;       /* row stride k, 1 <= k <= 65535                             */
+  const int32_t* nbr;  /* device [n_rows][k_max] global ids, -1 = padding; 16-B aligned */
+  const float* dist;   /* device [n_rows][k_max] fp32 >= 0, non-decreasing per row,
+                          +inf = padding; 16-B aligned                              */
+  uint32_t flags;      /* KDB_GRAPH_EXACT or 0                                       */
+} kdb_graph;
+
+/* ---- communicators ------------------------------------------------------ */
+typedef struct kdb_comm kdb_comm; /* NULL => single GPU, this process owns all rows */
+
+/* NCCL backend over NVLink/NVSwitch.  `nccl_unique_id` is the 128-byte
+ * ncclUniqueId produced by kdb_nccl_unique_id() on rank 0 and broadcast by the
+ * caller (e.g. torch.distributed).  Each rank must have selected its device.
+ * The NCCL shared library is dlopen()ed from $KDB_NCCL_LIBRARY, else
+ * "libnccl.so.2". */
+kdb_status kdb_nccl_unique_id(void* out_128_bytes /* host */);
+kdb_status kdb_comm_create_nccl(kdb_comm** out, const void* nccl_unique_id /* host, 128 B */,
+                                int rank, int nranks);
+/* Single-GPU simulation of `nranks` ranks (tests): the caller passes the FULL
+ * graph (row_begin 0, n_rows N); the library splits rows into nranks
+ * contiguous ranges, keeps per-virtual-rank partial results and reduces them
+ * exactly as the NCCL backend would.  Results must equal the NULL-comm run. */
+kdb_status kdb_comm_create_sim(kdb_comm** out, int nranks);
+void kdb_comm_destroy(kdb_comm* comm);
+
+/* ---- the three calls of Alg. 1 ------------------------------------------ */
+
+/* Alg. 1 lines 3-8, Lemma 1(i):
+ *   core(v) = dist[v][M-1] <= eps   for this rank's rows v.
+ * core_bits: device uint32[ceil(N/32)], bit (v & 31) of word v >> 5.  The call
+ * zeroes it, sets the bits of local rows and, with a communicator, combines all
+ * ranks' bits so every rank ends with all N flags (replicated).
+ * EINVAL: M < 1 or M > k_max, eps not in (0, +inf), null pointers, bad ranges. */
+kdb_status kdb_core_mark(const kdb_graph* g, int32_t M, float eps, uint32_t* core_bits,
+                         kdb_comm* comm, kdb_stream_t stream);
+
+/* Bytes of device workspace kdb_mst needs for this graph (depends on N,
+ * n_rows, k_max, flags and the communicator's rank count). */
+size_t kdb_mst_workspace_bytes(const kdb_graph* g, kdb_comm* comm);
+
+/* Alg. 1 lines 10-12: ParallelLocalMST + DistributedCutMST,
+ * realised as exact global Boruvka.
+ *   core_bits : device, replicated output of kdb_core_mark.
+ *   comp      : device int32[N] out, replicated: for core v the minimum core id of
+ *               v's component (the canonical label), -1 for non-core v.
+ *   mst_a/b/w : device [mst_cap] out: the MSF edges {a < b} with weight w, sorted
+ *               by (a, b); identical on every rank.  mst_cap >= #core - 1 suffices
+ *               (EINVAL if the forest does not fit).
+ *   mst_count : host out, number of MSF edges.
+ *   mst_weight: host out, the fp64 sum of the MSF weights, computed exactly and
+ *               rounded once (independent of summation order and of the rank count).
+ *   workspace : device, >= kdb_mst_workspace_bytes(g, comm) bytes, 256-B aligned.
+ * Synchronises `stream`. */
+kdb_status kdb_mst(const kdb_graph* g, float eps, const uint32_t* core_bits, int32_t* comp,
+                   uint32_t* mst_a, uint32_t* mst_b, float* mst_w, int64_t mst_cap,
+                   int64_t* mst_count, double* mst_weight, void* workspace, size_t ws_bytes,
+                   kdb_comm* comm, kdb_stream_t stream);
+
+/* Alg. 1 line 13 ClusterBorder (body omitted in the paper,
+ * SURVEY.md §8(c) reading #13, Lemma 1(ii)):
+ *   labels[i] (device int32[n_rows]) for local row v = row_begin + i:
+ *     core v     -> comp[v];
+ *     non-core v -> comp[J] of the FIRST entry in stored row order with J >= 0,
+ *                   core(J) and D <= eps (the scan stops at the first D > eps);
+ *                   -1 (noise) if none.
+ * Asynchronous. */
+kdb_status kdb_label(const kdb_graph* g, float eps, const uint32_t* core_bits, const int32_t* comp,
+                     int32_t* labels, kdb_stream_t stream);
+
+/* Per-phase device times (ms) and counters of the most recent kdb_mst call on
+ * this thread: out[0] = rounds, out[1] = init/sweep ms, out[2] = min-edge ms
+ * (offer + tie + exchange), out[3] = hook/jump/relabel ms, out[4] = finalize ms,
+ * out[5] = in-edge build ms, out[6] = stall (sweep) rounds. Returns entries written. */
+int kdb_last_mst_stats(double* out, int cap);
+
+const char* kdb_status_string(kdb_status s);
+const char* kdb_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KDB_H_ */
