@@ -1,0 +1,27 @@
+# Builds every native artefact in-tree (they travel to the GPU box with gpurun).
+NVCC      ?= nvcc
+ARCH      := -gencode arch=compute_100a,code=sm_100a
+NCCL_INC  := $(shell python -c "import os,nvidia.nccl as m; print(os.path.join(list(m.__path__)[0],'include'))" 2>/dev/null)
+NVFLAGS   := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -shared -Iinclude -I$(NCCL_INC) --expt-relaxed-constexpr
+
+KDB_SO    := paper_2009_04552_b200/lib/libkdb.so
+KNNG_SO   := datagen/lib/libknng.so
+ORACLE_SO := oracle/liboracle.so
+
+all: $(KDB_SO) $(ORACLE_SO) $(if $(wildcard datagen/csrc/knng.cu),$(KNNG_SO))
+
+$(KDB_SO): paper_2009_04552_b200/csrc/kdb.cu include/kdb.h
+	@mkdir -p $(dir $@)
+	$(NVCC) $(NVFLAGS) -o $@ $< -ldl
+
+$(KNNG_SO): datagen/csrc/knng.cu
+	@mkdir -p $(dir $@)
+	$(NVCC) $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -shared -o $@ $<
+
+$(ORACLE_SO): oracle/kdb_oracle.cpp
+	g++ -O2 -std=c++17 -shared -fPIC -o $@ $<
+
+clean:
+	rm -f $(KDB_SO) $(KNNG_SO) $(ORACLE_SO)
+
+.PHONY: all clean

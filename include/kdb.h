@@ -144,6 +144,17 @@ kdb_status kdb_label(const kdb_graph* g, float eps, const uint32_t* core_bits, c
  * out[5] = in-edge build ms, out[6] = stall (sweep) rounds. Returns entries written. */
 int kdb_last_mst_stats(double* out, int cap);
 
+/* Measurement hooks (bench.py).  kdb_launch_count(): kernels this library has
+ * launched so far (library-internal CUB scans/sorts are not counted).  With
+ * profiling enabled every kernel launch is bracketed by CUDA events on its
+ * stream; kdb_profile_read() returns, per kernel name, the summed device time
+ * (ms) and the launch count, names '\n'-separated in `names` (host buffers).
+ * Profiling makes kdb_core_mark / kdb_label synchronise their stream. */
+void kdb_profile_enable(int on);
+void kdb_profile_reset(void);
+long long kdb_launch_count(void);
+int kdb_profile_read(char* names, size_t names_len, double* ms, long long* counts, int cap);
+
 const char* kdb_status_string(kdb_status s);
 const char* kdb_last_error(void);
 

@@ -1,0 +1,1380 @@
+// kdb.cu -- B200-native (sm_100a) kNN-DBSCAN clustering stage behind the C-ABI
+// declared in include/kdb.h.
+//
+// Hot path, one CUDA kernel per step:
+//   a1 k_core_mark      core(v) = D[v][M-1] <= eps                 Alg. 1 l.4
+//   a2 k_init_*         dense component ids, head pointers L[i]    Alg. 2 l.2-3
+//   a3 k_offer_rows     per-vertex first leaving entry -> 64-bit   Alg. 2 l.6-10 + Alg. 3
+//                       packed key atomicMin into Kc[comp]          Findmin/pwrite (PAPER.md:562-567,
+//                                                                    609-633)
+//   a4 k_tie            b tie-break atomicMin into Bc[comp]        reading #6 (paper silent)
+//   a5 k_hook           break symmetry + MSF emit                  Alg. 2 l.13-18
+//   a6 k_jump/k_relabel pointer jumping, dense renumber, relabel   Alg. 2 l.19-33
+//   a7 head pointers    edges that became intra never revive       L[i]
+//   a8 termination      no component offers a leaving edge
+//   a9 k_canon          label = min core id of the component       north_star
+//   a10 k_label         border: first core entry within eps        ClusterBorder
+//   a11 k_wbuckets      exact fp64 MSF weight                       north_star
+//
+// Undirected semantics (reading #4): an entry u->v is an edge of v as well.
+//   * KDB_GRAPH_EXACT: an unmirrored in-edge of v weighs >= D[v][k-1] =: kth(v).
+//     A component C only hooks when its best row offer is strictly lighter than
+//     min_{z in C} kth'(z) (certificate); otherwise it abstains this round (a
+//     selected edge is then still the true minimum, so Boruvka stays exact).  If
+//     a round would make no progress, a full edge-centric "sweep round" offers
+//     every leaving entry to both endpoint components.
+//   * otherwise: in-edge lists (transpose of the local candidate entries) are
+//     materialised once and scanned alongside the rows every round.
+// Multi-GPU (§8(e)): rows are contiguous ranges; per-component arrays are
+// replicated; each round all-reduces Kc (u64 MIN) and Bc (u32 MIN) with NCCL,
+// then every rank runs hook / jump / relabel identically.
+//
+// THIS FILE SHARES NO CODE WITH oracle/ (the CPU checker) and never calls it.
+
+#include "kdb.h"
+
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+// ============================================================================
+// error plumbing
+// ============================================================================
+namespace {
+
+thread_local std::string g_err;
+thread_local double g_stats[8];
+
+kdb_status set_err(kdb_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return s;
+}
+
+#define KDB_CUDA(expr)                                                                   \
+  do {                                                                                   \
+    cudaError_t e_ = (expr);                                                             \
+    if (e_ != cudaSuccess)                                                               \
+      return set_err(KDB_ECUDA, "%s failed: %s (%s:%d)", #expr, cudaGetErrorString(e_), \
+                     __FILE__, __LINE__);                                                \
+  } while (0)
+
+#define KDB_TRY(expr)                 \
+  do {                                \
+    kdb_status s_ = (expr);           \
+    if (s_ != KDB_OK) return s_;      \
+  } while (0)
+
+constexpr uint64_t kSent = ~0ull;      // sentinel key (reading #11)
+constexpr uint32_t kSentB = ~0u;
+constexpr uint32_t kInfBits = 0x7f800000u;
+constexpr int kThreads = 256;
+
+inline int grid_for(int64_t n, int per_block = kThreads) {
+  int64_t g = (n + per_block - 1) / per_block;
+  if (g < 1) g = 1;
+  if (g > 148 * 16) g = 148 * 16;  // grid-stride beyond 16 CTAs per SM
+  return (int)g;
+}
+
+// ============================================================================
+// launch accounting + optional per-kernel device timing (bench.py's roofline)
+// ============================================================================
+struct ProfRec {
+  const char* name;
+  cudaEvent_t a, b;
+};
+struct Prof {
+  bool on = false;
+  long long launches = 0;
+  std::vector<ProfRec> pending;
+  std::vector<cudaEvent_t> pool;
+  std::vector<std::string> names;
+  std::vector<double> ms;
+  std::vector<long long> cnt;
+  cudaEvent_t get() {
+    if (!pool.empty()) {
+      cudaEvent_t e = pool.back();
+      pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+  }
+  void add(const char* n, double t) {
+    for (size_t i = 0; i < names.size(); ++i)
+      if (names[i] == n) { ms[i] += t; cnt[i] += 1; return; }
+    names.push_back(n);
+    ms.push_back(t);
+    cnt.push_back(1);
+  }
+  // resolve recorded pairs (caller synchronised the stream)
+  void drain() {
+    for (auto& r : pending) {
+      float t = 0;
+      cudaEventSynchronize(r.b);
+      cudaEventElapsedTime(&t, r.a, r.b);
+      add(r.name, t);
+      pool.push_back(r.a);
+      pool.push_back(r.b);
+    }
+    pending.clear();
+  }
+};
+Prof g_prof;
+
+struct LaunchScope {
+  const char* name;
+  cudaStream_t st;
+  cudaEvent_t a = nullptr, b = nullptr;
+  LaunchScope(const char* n, cudaStream_t s, bool count = true) : name(n), st(s) {
+    if (count) ++g_prof.launches;
+    if (g_prof.on) {
+      a = g_prof.get();
+      b = g_prof.get();
+      cudaEventRecord(a, st);
+    }
+  }
+  ~LaunchScope() {
+    if (g_prof.on) {
+      cudaEventRecord(b, st);
+      g_prof.pending.push_back({name, a, b});
+    }
+  }
+};
+// LAUNCH(kernel, grid, block, stream, args...) -- every kernel of the hot path
+#define LAUNCH(kern, grid, block, st, ...)             \
+  do {                                                 \
+    LaunchScope ls_(#kern, st);                        \
+    kern<<<(grid), (block), 0, (st)>>>(__VA_ARGS__);   \
+  } while (0)
+
+// ============================================================================
+// NCCL (dlopen, so libkdb.so loads without NCCL on the path)
+// ============================================================================
+struct NcclApi {
+  void* h = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+NcclApi g_nccl;
+
+kdb_status nccl_load() {
+  if (g_nccl.h) return KDB_OK;
+  const char* path = getenv("KDB_NCCL_LIBRARY");
+  void* h = dlopen(path && *path ? path : "libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
+  if (!h) return set_err(KDB_ENCCL, "cannot dlopen NCCL (%s): %s", path ? path : "libnccl.so.2", dlerror());
+  g_nccl.GetUniqueId = (decltype(g_nccl.GetUniqueId))dlsym(h, "ncclGetUniqueId");
+  g_nccl.CommInitRank = (decltype(g_nccl.CommInitRank))dlsym(h, "ncclCommInitRank");
+  g_nccl.AllReduce = (decltype(g_nccl.AllReduce))dlsym(h, "ncclAllReduce");
+  g_nccl.CommDestroy = (decltype(g_nccl.CommDestroy))dlsym(h, "ncclCommDestroy");
+  g_nccl.GetErrorString = (decltype(g_nccl.GetErrorString))dlsym(h, "ncclGetErrorString");
+  if (!g_nccl.GetUniqueId || !g_nccl.CommInitRank || !g_nccl.AllReduce || !g_nccl.CommDestroy)
+    return set_err(KDB_ENCCL, "NCCL library lacks required symbols");
+  g_nccl.h = h;
+  return KDB_OK;
+}
+
+}  // namespace
+
+struct kdb_comm {
+  int kind = 0;  // 1 = nccl, 2 = sim
+  int rank = 0, nranks = 1;
+  ncclComm_t nccl = nullptr;
+};
+
+namespace {
+
+kdb_status nccl_check(ncclResult_t r, const char* what) {
+  if (r == ncclSuccess) return KDB_OK;
+  return set_err(KDB_ENCCL, "%s: %s", what, g_nccl.GetErrorString ? g_nccl.GetErrorString(r) : "?");
+}
+
+// ============================================================================
+// device helpers
+// ============================================================================
+__device__ __forceinline__ uint32_t mono_bits(float w) {
+  uint32_t u = __float_as_uint(w);
+  return u == 0x80000000u ? 0u : u;  // -0 -> +0 (reading #6)
+}
+
+__device__ __forceinline__ bool is_core(const uint32_t* __restrict__ bits, int64_t v) {
+  return (__ldg(bits + (v >> 5)) >> (v & 31)) & 1u;
+}
+
+__device__ __forceinline__ uint64_t pack_key(uint32_t wbits, uint32_t a) {
+  return ((uint64_t)wbits << 32) | a;
+}
+
+// warp-aggregated slot reservation: every lane with `want` gets a unique slot
+__device__ __forceinline__ uint32_t warp_reserve(uint32_t* counter, bool want) {
+  const unsigned active = __activemask();
+  const unsigned m = __ballot_sync(active, want);
+  const int lane = threadIdx.x & 31;
+  uint32_t base = 0;
+  const int leader = __ffs(m) - 1;
+  if (m && lane == leader) base = atomicAdd(counter, (uint32_t)__popc(m));
+  base = __shfl_sync(active, base, leader < 0 ? 0 : leader);
+  return base + __popc(m & ((1u << lane) - 1u));
+}
+
+// ============================================================================
+// a1: core marking
+// ============================================================================
+__global__ void k_core_mark(const float* __restrict__ dist, int64_t n_rows, int32_t k, int32_t M,
+                            float eps, int64_t row_begin, uint32_t* __restrict__ bits) {
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n_rows;
+       base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = base + threadIdx.x;
+    const bool in = i < n_rows;
+    bool core = false;
+    if (in) core = __ldg(dist + i * k + (M - 1)) <= eps;
+    const int64_t v = row_begin + i;
+    const unsigned inmask = __ballot_sync(0xffffffffu, in);
+    if (in) {
+      const unsigned grp = __match_any_sync(inmask, (unsigned long long)(v >> 5));
+      const unsigned word = __reduce_or_sync(grp, core ? (1u << (v & 31)) : 0u);
+      if ((threadIdx.x & 31) == __ffs(grp) - 1 && word) atomicOr(bits + (v >> 5), word);
+    }
+  }
+}
+
+// ============================================================================
+// a2: initial state
+// ============================================================================
+__global__ void k_popc_words(const uint32_t* __restrict__ bits, int64_t nwords, uint32_t* out) {
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < nwords;
+       w += (int64_t)gridDim.x * blockDim.x)
+    out[w] = __popc(bits[w]);
+}
+
+// comp[v] = rank of v among core points (dense id) or -1; cmin[comp] = v
+__global__ void k_init_comp(const uint32_t* __restrict__ bits, const uint32_t* __restrict__ woff,
+                            int64_t N, int32_t* __restrict__ comp, int32_t* __restrict__ cmin) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < N;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t word = bits[v >> 5];
+    if ((word >> (v & 31)) & 1u) {
+      const int32_t c = (int32_t)(woff[v >> 5] + __popc(word & ((1u << (v & 31)) - 1u)));
+      comp[v] = c;
+      cmin[c] = (int32_t)v;
+    } else {
+      comp[v] = -1;
+    }
+  }
+}
+
+__global__ void k_fill_comp_arrays(int64_t C, uint64_t* __restrict__ Kc, uint32_t* __restrict__ Bc,
+                                   uint32_t* __restrict__ kmin) {
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < C;
+       c += (int64_t)gridDim.x * blockDim.x) {
+    Kc[c] = kSent;
+    Bc[c] = kSentB;
+    if (kmin) kmin[c] = kInfBits;
+  }
+}
+
+// local rows: head = 0, certificate bound kth'(v) into kmin[comp v], active list
+__global__ void k_init_rows(const float* __restrict__ dist, int64_t n_rows, int32_t k, float eps,
+                            int64_t row_begin, const uint32_t* __restrict__ bits,
+                            const int32_t* __restrict__ comp, uint16_t* __restrict__ head,
+                            uint32_t* __restrict__ kmin, int32_t* __restrict__ active,
+                            uint32_t* __restrict__ n_active) {
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n_rows;
+       base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = base + threadIdx.x;
+    bool want = false;
+    int64_t v = row_begin + i;
+    if (i < n_rows) {
+      head[i] = 0;
+      if (is_core(bits, v)) {
+        // a row whose first entry is already beyond eps offers nothing, ever
+        want = __ldg(dist + i * k) <= eps;
+        if (kmin) {
+          const float kth = __ldg(dist + i * k + (k - 1));
+          kmin[comp[v]] = (kth <= eps) ? mono_bits(kth) : kInfBits;
+        }
+      }
+    }
+    const uint32_t slot = warp_reserve(n_active, want);
+    if (want) active[slot] = (int32_t)v;
+  }
+}
+
+// ============================================================================
+// general mode: in-edge lists (transpose of local candidate entries)
+// ============================================================================
+__global__ void k_in_count(const int32_t* __restrict__ nbr, const float* __restrict__ dist,
+                           int64_t n_rows, int32_t k, float eps, int64_t row_begin, int64_t N,
+                           const uint32_t* __restrict__ bits, unsigned long long* __restrict__ cnt) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_rows;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = row_begin + i;
+    if (!is_core(bits, v)) continue;
+    for (int32_t c = 0; c < k; ++c) {
+      const float w = __ldg(dist + i * k + c);
+      if (!(w <= eps)) break;
+      const int64_t J = __ldg(nbr + i * k + c);
+      if (J < 0 || J >= N || J == v || !is_core(bits, J)) continue;
+      atomicAdd(cnt + J, 1ull);
+    }
+  }
+}
+
+__global__ void k_in_fill(const int32_t* __restrict__ nbr, const float* __restrict__ dist,
+                          int64_t n_rows, int32_t k, float eps, int64_t row_begin, int64_t N,
+                          const uint32_t* __restrict__ bits, unsigned long long* __restrict__ cursor,
+                          int32_t* __restrict__ in_src, float* __restrict__ in_w) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_rows;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = row_begin + i;
+    if (!is_core(bits, v)) continue;
+    for (int32_t c = 0; c < k; ++c) {
+      const float w = __ldg(dist + i * k + c);
+      if (!(w <= eps)) break;
+      const int64_t J = __ldg(nbr + i * k + c);
+      if (J < 0 || J >= N || J == v || !is_core(bits, J)) continue;
+      const unsigned long long s = atomicAdd(cursor + J, 1ull);
+      in_src[s] = (int32_t)v;
+      in_w[s] = w;
+    }
+  }
+}
+
+// in_len[t] = count, in-active list = targets with in-edges
+__global__ void k_in_finish(const unsigned long long* __restrict__ off, int64_t N,
+                            int32_t* __restrict__ in_len, int32_t* __restrict__ in_active,
+                            uint32_t* __restrict__ n_in_active) {
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < N;
+       base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = base + threadIdx.x;
+    bool want = false;
+    if (t < N) {
+      const int32_t len = (int32_t)(off[t + 1] - off[t]);
+      in_len[t] = len;
+      want = len > 0;
+    }
+    const uint32_t slot = warp_reserve(n_in_active, want);
+    if (want) in_active[slot] = (int32_t)t;
+  }
+}
+
+// ============================================================================
+// a3: per-vertex minimum leaving entry (rows)
+// ============================================================================
+// For vertex v the incident edges of its row are ordered, under O1 with v fixed,
+// by (mono(w), far id) (reading #6).  Rows are sorted by w, so the first entry
+// (after skipping permanently dead entries) whose far endpoint lies in another
+// component opens the minimum group; equal-weight entries after it may carry a
+// smaller far id and are scanned too.  The head pointer only passes entries
+// that can never become leaving again (non-candidates, intra-component).
+__global__ void k_offer_rows(const int32_t* __restrict__ nbr, const float* __restrict__ dist,
+                             int32_t k, float eps, int64_t row_begin, int64_t N,
+                             const uint32_t* __restrict__ bits, const int32_t* __restrict__ comp,
+                             const int32_t* __restrict__ act_in, uint32_t n_in,
+                             uint16_t* __restrict__ head, int32_t* __restrict__ act_out,
+                             uint32_t* __restrict__ n_out, int32_t* __restrict__ off_v,
+                             uint64_t* __restrict__ off_key, uint32_t* __restrict__ off_b,
+                             uint32_t* __restrict__ n_off, unsigned long long* __restrict__ Kc) {
+  for (uint32_t base = blockIdx.x * blockDim.x; base < n_in; base += gridDim.x * blockDim.x) {
+    const uint32_t s = base + threadIdx.x;
+    bool found = false;
+    uint64_t best = kSent;
+    uint32_t bestb = kSentB;
+    int32_t v = -1, cv = -1;
+    if (s < n_in) {
+      v = act_in[s];
+      const int64_t i = (int64_t)v - row_begin;
+      const int32_t* nr = nbr + i * k;
+      const float* dr = dist + i * k;
+      cv = comp[v];
+      int h = head[i];
+      while (h < k) {
+        const float w = __ldg(dr + h);
+        if (!(w <= eps)) { h = k; break; }
+        const int64_t J = __ldg(nr + h);
+        if (J < 0 || J >= N || J == v || !is_core(bits, J) || comp[J] == cv) { ++h; continue; }
+        const uint32_t wb = mono_bits(w);
+        best = pack_key(wb, (uint32_t)min((int64_t)v, J));
+        bestb = (uint32_t)max((int64_t)v, J);
+        for (int h2 = h + 1; h2 < k; ++h2) {
+          const float w2 = __ldg(dr + h2);
+          if (w2 != w) break;
+          const int64_t J2 = __ldg(nr + h2);
+          if (J2 < 0 || J2 >= N || J2 == v || !is_core(bits, J2) || comp[J2] == cv) continue;
+          const uint64_t k2 = pack_key(wb, (uint32_t)min((int64_t)v, J2));
+          const uint32_t b2 = (uint32_t)max((int64_t)v, J2);
+          if (k2 < best || (k2 == best && b2 < bestb)) { best = k2; bestb = b2; }
+        }
+        found = true;
+        break;
+      }
+      head[i] = (uint16_t)h;
+    }
+    const uint32_t a = warp_reserve(n_out, found);
+    if (found) act_out[a] = v;
+    const uint32_t o = warp_reserve(n_off, found);
+    if (found) {
+      off_v[o] = v;
+      off_key[o] = best;
+      off_b[o] = bestb;
+      atomicMin(Kc + cv, (unsigned long long)best);
+    }
+  }
+}
+
+// in-edge lists: scan the live in-entries of target t, drop intra entries
+// (swap-remove; they never revive), offer the minimum leaving one.
+__global__ void k_offer_in(const unsigned long long* __restrict__ in_off, int32_t* __restrict__ in_len,
+                           int32_t* __restrict__ in_src, float* __restrict__ in_w,
+                           const int32_t* __restrict__ comp, const int32_t* __restrict__ act_in,
+                           uint32_t n_in, int32_t* __restrict__ act_out, uint32_t* __restrict__ n_out,
+                           int32_t* __restrict__ off_v, uint64_t* __restrict__ off_key,
+                           uint32_t* __restrict__ off_b, uint32_t* __restrict__ n_off,
+                           unsigned long long* __restrict__ Kc) {
+  for (uint32_t base = blockIdx.x * blockDim.x; base < n_in; base += gridDim.x * blockDim.x) {
+    const uint32_t s = base + threadIdx.x;
+    bool found = false, keep = false;
+    uint64_t best = kSent;
+    uint32_t bestb = kSentB;
+    int32_t t = -1, ct = -1;
+    if (s < n_in) {
+      t = act_in[s];
+      ct = comp[t];
+      const unsigned long long o = in_off[t];
+      int32_t len = in_len[t];
+      int32_t e = 0;
+      while (e < len) {
+        const int32_t u = in_src[o + e];
+        if (comp[u] == ct) {  // intra for good: swap-remove
+          --len;
+          in_src[o + e] = in_src[o + len];
+          in_w[o + e] = in_w[o + len];
+          continue;
+        }
+        const uint64_t kk = pack_key(mono_bits(in_w[o + e]), (uint32_t)min(u, t));
+        const uint32_t bb = (uint32_t)max(u, t);
+        if (kk < best || (kk == best && bb < bestb)) { best = kk; bestb = bb; }
+        found = true;
+        ++e;
+      }
+      in_len[t] = len;
+      keep = len > 0;
+    }
+    const uint32_t a = warp_reserve(n_out, keep);
+    if (keep) act_out[a] = t;
+    const uint32_t o2 = warp_reserve(n_off, found);
+    if (found) {
+      off_v[o2] = t;
+      off_key[o2] = best;
+      off_b[o2] = bestb;
+      atomicMin(Kc + ct, (unsigned long long)best);
+    }
+  }
+}
+
+// ============================================================================
+// a4: tie pass (b of the minimum key)
+// ============================================================================
+__global__ void k_tie(const int32_t* __restrict__ off_v, const uint64_t* __restrict__ off_key,
+                      const uint32_t* __restrict__ off_b, uint32_t n_off,
+                      const int32_t* __restrict__ comp, const uint64_t* __restrict__ Kc,
+                      uint32_t* __restrict__ Bc) {
+  for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < n_off; s += gridDim.x * blockDim.x) {
+    const int32_t c = comp[off_v[s]];
+    if (off_key[s] == Kc[c]) atomicMin(Bc + c, off_b[s]);
+  }
+}
+
+// stall fallback (exact mode): offer EVERY live leaving entry to both sides
+__global__ void k_sweep(const int32_t* __restrict__ nbr, const float* __restrict__ dist,
+                        int64_t n_rows, int32_t k, float eps, int64_t row_begin, int64_t N,
+                        const uint32_t* __restrict__ bits, const int32_t* __restrict__ comp,
+                        const uint16_t* __restrict__ head, unsigned long long* __restrict__ Kc,
+                        uint32_t* __restrict__ Bc, int tie_phase) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_rows;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = row_begin + i;
+    if (!is_core(bits, v)) continue;
+    const int32_t cv = comp[v];
+    for (int32_t c = head[i]; c < k; ++c) {
+      const float w = __ldg(dist + i * k + c);
+      if (!(w <= eps)) break;
+      const int64_t J = __ldg(nbr + i * k + c);
+      if (J < 0 || J >= N || J == v || !is_core(bits, J)) continue;
+      const int32_t cj = comp[J];
+      if (cj == cv) continue;
+      const uint64_t kk = pack_key(mono_bits(w), (uint32_t)min(v, J));
+      const uint32_t bb = (uint32_t)max(v, J);
+      if (!tie_phase) {
+        atomicMin(Kc + cv, (unsigned long long)kk);
+        atomicMin(Kc + cj, (unsigned long long)kk);
+      } else {
+        if (kk == Kc[cv]) atomicMin(Bc + cv, bb);
+        if (kk == Kc[cj]) atomicMin(Bc + cj, bb);
+      }
+    }
+  }
+}
+
+// ============================================================================
+// sim backend: elementwise MIN of per-virtual-rank partials
+// ============================================================================
+
+__global__ void k_min_into_u64(uint64_t* __restrict__ d, const uint64_t* __restrict__ s, int64_t n) {
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n; c += (int64_t)gridDim.x * blockDim.x)
+    if (s[c] < d[c]) d[c] = s[c];
+}
+__global__ void k_min_into_u32(uint32_t* __restrict__ d, const uint32_t* __restrict__ s, int64_t n) {
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n; c += (int64_t)gridDim.x * blockDim.x)
+    if (s[c] < d[c]) d[c] = s[c];
+}
+
+// ============================================================================
+// a5: hook (break symmetry) + MSF emission
+// ============================================================================
+struct RoundCounters {
+  unsigned long long msf_count;  // edges emitted so far (all rounds)
+  uint32_t hooks;                // this round
+  uint32_t offered;              // components with a finite key
+  uint32_t uncertified;          // offered but abstaining (exact-mode certificate)
+  uint32_t n_roots;              // components after contraction
+  uint32_t n_act[2];             // per-rank scratch (row / in active counts), see host
+  uint32_t n_off;
+  uint32_t violation;            // a hook target's key exceeds the hooker's: the
+                                 // KDB_GRAPH_EXACT promise was false (or a bug)
+};
+
+__device__ __forceinline__ bool certified(uint64_t K, const uint32_t* kmin, int64_t c) {
+  return kmin == nullptr || (uint32_t)(K >> 32) < kmin[c];
+}
+
+__global__ void k_hook(int64_t C, const uint64_t* __restrict__ Kc, const uint32_t* __restrict__ Bc,
+                       const uint32_t* __restrict__ kmin /* null = all certified */,
+                       const int32_t* __restrict__ comp, int32_t* __restrict__ parent,
+                       uint64_t* __restrict__ e_key, float* __restrict__ e_w, int64_t e_cap,
+                       RoundCounters* __restrict__ ctr) {
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < C;
+       base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = base + threadIdx.x;
+    bool emit = false, offered = false, unc = false;
+    uint32_t a = 0, b = 0, wb = 0;
+    if (c < C) {
+      const uint64_t K = Kc[c];
+      int32_t p = (int32_t)c;
+      if (K != kSent) {
+        offered = true;
+        if (!certified(K, kmin, c)) {
+          unc = true;
+        } else {
+          a = (uint32_t)K;
+          b = Bc[c];
+          wb = (uint32_t)(K >> 32);
+          const int32_t x = (comp[a] == (int32_t)c) ? (int32_t)b : (int32_t)a;
+          const int32_t t = comp[x];
+          const uint64_t Kt = Kc[t];
+          const bool cert_t = Kt != kSent && certified(Kt, kmin, t);
+          const bool mutual = cert_t && Kt == K && Bc[t] == b;
+          // t's true minimum is <= the edge c selected (that edge is incident to
+          // t); a larger key means t's offer missed an incident edge.  Under a
+          // true EXACT promise this cannot happen; it is the only way a hook
+          // cycle longer than a mutual pair could form (Fig. cycle).
+          if (cert_t && (Kt > K || (Kt == K && Bc[t] > b))) ctr->violation = 1u;
+          if (!(mutual && c < t)) {
+            p = t;
+            emit = true;
+          }
+        }
+      }
+      parent[c] = p;
+    }
+    const unsigned m_off = __ballot_sync(0xffffffffu, offered);
+    const unsigned m_unc = __ballot_sync(0xffffffffu, unc);
+    if ((threadIdx.x & 31) == 0) {
+      if (m_off) atomicAdd(&ctr->offered, __popc(m_off));
+      if (m_unc) atomicAdd(&ctr->uncertified, __popc(m_unc));
+    }
+    const unsigned m_emit = __ballot_sync(0xffffffffu, emit);
+    unsigned long long base_slot = 0;
+    if ((threadIdx.x & 31) == 0 && m_emit) {
+      base_slot = atomicAdd(&ctr->msf_count, (unsigned long long)__popc(m_emit));
+      atomicAdd(&ctr->hooks, __popc(m_emit));
+    }
+    base_slot = __shfl_sync(0xffffffffu, base_slot, 0);
+    if (emit) {
+      const unsigned long long slot = base_slot + __popc(m_emit & ((1u << (threadIdx.x & 31)) - 1u));
+      if ((int64_t)slot < e_cap) {
+        e_key[slot] = ((uint64_t)a << 32) | b;
+        e_w[slot] = __uint_as_float(wb);
+      }
+    }
+  }
+}
+
+// ============================================================================
+// a6: pointer jumping, dense renumbering, relabel
+// ============================================================================
+// Path halving on the hook forest.  Concurrent writes only ever replace a
+// parent pointer by one of its ancestors, so every thread still reaches the
+// same root; stale reads are ancestors too, so the loop terminates.  The root
+// goes to a SEPARATE array: another thread's halving write may land on
+// parent[c] after c found its root, so parent[c] itself is not final.
+__global__ void k_jump(int64_t C, int32_t* parent, int32_t* __restrict__ rootof, RoundCounters* ctr) {
+  volatile int32_t* P = parent;
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < C;
+       c += (int64_t)gridDim.x * blockDim.x) {
+    int32_t x = (int32_t)c;
+    int64_t steps = 0;
+    while (true) {
+      const int32_t p = P[x];
+      if (p == x) break;
+      const int32_t gp = P[p];
+      if (gp == p) { x = p; break; }
+      P[x] = gp;
+      x = gp;
+      if (++steps > C) {  // defence in depth: never spin on a cycle
+        ctr->violation = 2u;
+        break;
+      }
+    }
+    rootof[c] = x;
+  }
+}
+
+__global__ void k_root_flags(int64_t C, const int32_t* __restrict__ rootof, int32_t* __restrict__ flag) {
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < C;
+       c += (int64_t)gridDim.x * blockDim.x)
+    flag[c] = rootof[c] == (int32_t)c;
+}
+
+// new per-component arrays: cmin/kmin are minima over the merged tree
+__global__ void k_merge(int64_t C, const int32_t* __restrict__ rootof, const int32_t* __restrict__ newid,
+                        const int32_t* __restrict__ cmin, const uint32_t* __restrict__ kmin,
+                        int32_t* __restrict__ cmin2, uint32_t* __restrict__ kmin2) {
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < C;
+       c += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t r = newid[rootof[c]];
+    atomicMin(cmin2 + r, cmin[c]);
+    if (kmin) atomicMin(kmin2 + r, kmin[c]);
+  }
+}
+
+__global__ void k_fill_i32(int32_t* __restrict__ p, int64_t n, int32_t val) {
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n;
+       c += (int64_t)gridDim.x * blockDim.x)
+    p[c] = val;
+}
+
+__global__ void k_relabel(int64_t N, int32_t* __restrict__ comp, const int32_t* __restrict__ rootof,
+                          const int32_t* __restrict__ newid) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < N;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t c = comp[v];
+    if (c >= 0) comp[v] = newid[rootof[c]];
+  }
+}
+
+// ============================================================================
+// a9 / a11: canonical labels, MSF output, exact weight
+// ============================================================================
+__global__ void k_canon(int64_t N, int32_t* __restrict__ comp, const int32_t* __restrict__ cmin) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < N;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t c = comp[v];
+    if (c >= 0) comp[v] = cmin[c];
+  }
+}
+
+__global__ void k_split_edges(int64_t m, const uint64_t* __restrict__ keys, uint32_t* __restrict__ a,
+                              uint32_t* __restrict__ b) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t x = keys[e];
+    a[e] = (uint32_t)(x >> 32);
+    b[e] = (uint32_t)x;
+  }
+}
+
+// exact sum: integer mantissas bucketed by biased exponent (order independent)
+__global__ void k_wbuckets(int64_t m, const float* __restrict__ w, unsigned long long* __restrict__ bk) {
+  __shared__ unsigned long long sb[256];
+  for (int t = threadIdx.x; t < 256; t += blockDim.x) sb[t] = 0;
+  __syncthreads();
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t u = __float_as_uint(w[e]) & 0x7fffffffu;
+    const uint32_t ex = u >> 23;
+    uint32_t man = u & 0x7fffffu;
+    if (ex) man |= 0x800000u;
+    if (man) atomicAdd(sb + ex, (unsigned long long)man);
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < 256; t += blockDim.x)
+    if (sb[t]) atomicAdd(bk + t, sb[t]);
+}
+
+// a10: labels of this rank's rows
+__global__ void k_label(const int32_t* __restrict__ nbr, const float* __restrict__ dist, int64_t n_rows,
+                        int32_t k, float eps, int64_t row_begin, int64_t N,
+                        const uint32_t* __restrict__ bits, const int32_t* __restrict__ comp,
+                        int32_t* __restrict__ labels) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_rows;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = row_begin + i;
+    int32_t lab = -1;
+    if (is_core(bits, v)) {
+      lab = comp[v];
+    } else {
+      for (int32_t c = 0; c < k; ++c) {
+        const float w = __ldg(dist + i * k + c);
+        if (!(w <= eps)) break;
+        const int64_t J = __ldg(nbr + i * k + c);
+        if (J < 0 || J >= N || !is_core(bits, J)) continue;
+        lab = comp[J];
+        break;
+      }
+    }
+    labels[i] = lab;
+  }
+}
+
+// ============================================================================
+// host side
+// ============================================================================
+// exact value of sum_e bk[e] * 2^(max(e,1) - 150), rounded once to double
+double exact_bucket_sum(const unsigned long long* bk) {
+  uint64_t L[7] = {0, 0, 0, 0, 0, 0, 0};  // little-endian limbs, value * 2^149
+  for (int e = 0; e < 256; ++e) {
+    if (!bk[e]) continue;
+    const int sh = (e ? e : 1) - 1;  // 2^(max(e,1)-150) = 2^(sh) * 2^-149
+    const int q = sh / 64, r = sh % 64;
+    unsigned __int128 add0 = (unsigned __int128)bk[e] << r;  // up to 128 bits
+    uint64_t parts[3] = {(uint64_t)add0, (uint64_t)(add0 >> 64), 0};
+    unsigned __int128 carry = 0;
+    for (int j = q; j < 7; ++j) {
+      unsigned __int128 s = (unsigned __int128)L[j] + carry + (j - q < 3 ? parts[j - q] : 0);
+      L[j] = (uint64_t)s;
+      carry = s >> 64;
+    }
+  }
+  int top = -1;
+  for (int j = 6; j >= 0; --j)
+    if (L[j]) { top = j * 64 + 63 - __builtin_clzll(L[j]); break; }
+  if (top < 0) return 0.0;
+  auto bit = [&](int p) -> int { return p < 0 ? 0 : (int)((L[p / 64] >> (p % 64)) & 1u); };
+  // 53-bit mantissa [top-52, top], round bit top-53, sticky below
+  uint64_t man = 0;
+  for (int p = top; p > top - 53; --p) man = (man << 1) | (uint64_t)bit(p);
+  const int rb = bit(top - 53);
+  bool sticky = false;
+  for (int p = top - 54; p >= 0 && !sticky; --p) sticky = bit(p);
+  if (rb && (sticky || (man & 1u))) ++man;  // round to nearest even
+  return ldexp((double)man, top - 52 - 149);
+}
+
+struct Carver {
+  char* base;
+  size_t off = 0, cap;
+  bool dry;
+  template <typename T>
+  T* take(size_t n) {
+    off = (off + 255) & ~size_t(255);
+    T* p = dry ? nullptr : reinterpret_cast<T*>(base + off);
+    off += n * sizeof(T);
+    return p;
+  }
+};
+
+struct RankState {
+  int64_t row_begin = 0, n_rows = 0;
+  const int32_t* nbr = nullptr;
+  const float* dist = nullptr;
+  uint16_t* head = nullptr;
+  int32_t* act[2] = {nullptr, nullptr};
+  uint32_t n_act = 0;
+  // offers
+  int32_t* off_v = nullptr;
+  uint64_t* off_key = nullptr;
+  uint32_t* off_b = nullptr;
+  uint32_t n_off = 0;
+  // per-rank partial Kc/Bc (sim ranks > 0) -- else alias the shared ones
+  uint64_t* Kc = nullptr;
+  uint32_t* Bc = nullptr;
+  // in-edge lists (general mode)
+  unsigned long long* in_off = nullptr;
+  int32_t* in_len = nullptr;
+  int32_t* in_src = nullptr;
+  float* in_w = nullptr;
+  int32_t* in_act[2] = {nullptr, nullptr};
+  uint32_t n_in_act = 0;
+  RoundCounters* ctr = nullptr;  // per-rank counters (act/off)
+};
+
+struct Layout {
+  // shared
+  uint32_t* woff;
+  int32_t *cmin, *cmin2, *parent, *rootof, *newid, *flag;
+  uint32_t *kmin, *kmin2;
+  uint64_t* Kc;
+  uint32_t* Bc;
+  uint64_t *e_key, *e_key_sorted;
+  float* e_w;
+  unsigned long long* buckets;
+  RoundCounters* ctr;
+  void* cub_tmp;
+  size_t cub_bytes;
+  std::vector<RankState> ranks;
+};
+
+size_t cub_tmp_bytes(int64_t N, int64_t cap_edges) {
+  size_t a = 0, b = 0, c = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, a, (const int32_t*)nullptr, (int32_t*)nullptr, (int)std::max<int64_t>(N + 1, 1));
+  cub::DeviceScan::ExclusiveSum(nullptr, b, (const unsigned long long*)nullptr,
+                                (unsigned long long*)nullptr, (int)std::max<int64_t>(N + 1, 1));
+  cub::DeviceRadixSort::SortPairs(nullptr, c, (const uint64_t*)nullptr, (uint64_t*)nullptr,
+                                  (const float*)nullptr, (float*)nullptr, (int)std::max<int64_t>(cap_edges, 1));
+  return std::max(a, std::max(b, c)) + 256;
+}
+
+// carve the workspace; returns bytes needed
+size_t carve(Layout& L, char* base, bool dry, int64_t N, int nr, const int64_t* rb, const int64_t* rn,
+             bool general, int32_t k) {
+  Carver cv{base, 0, 0, dry};
+  const int64_t nwords = (N + 31) / 32;
+  L.woff = cv.take<uint32_t>(nwords + 1);
+  L.cmin = cv.take<int32_t>(N + 1);
+  L.cmin2 = cv.take<int32_t>(N + 1);
+  L.parent = cv.take<int32_t>(N + 1);
+  L.rootof = cv.take<int32_t>(N + 1);
+  L.newid = cv.take<int32_t>(N + 1);
+  L.flag = cv.take<int32_t>(N + 1);
+  L.kmin = cv.take<uint32_t>(N + 1);
+  L.kmin2 = cv.take<uint32_t>(N + 1);
+  L.Kc = cv.take<uint64_t>(N + 1);
+  L.Bc = cv.take<uint32_t>(N + 1);
+  L.e_key = cv.take<uint64_t>(N + 1);
+  L.e_key_sorted = cv.take<uint64_t>(N + 1);
+  L.e_w = cv.take<float>(N + 1);
+  L.buckets = cv.take<unsigned long long>(256);
+  L.ctr = cv.take<RoundCounters>(1);
+  L.cub_bytes = cub_tmp_bytes(N, N + 1);
+  L.cub_tmp = cv.take<char>(L.cub_bytes);
+  L.ranks.assign(nr, RankState());
+  for (int r = 0; r < nr; ++r) {
+    RankState& R = L.ranks[r];
+    R.row_begin = rb[r];
+    R.n_rows = rn[r];
+    const int64_t n = std::max<int64_t>(rn[r], 1);
+    R.head = cv.take<uint16_t>(n);
+    R.act[0] = cv.take<int32_t>(n);
+    R.act[1] = cv.take<int32_t>(n);
+    const int64_t noff = general ? n + N : n;
+    R.off_v = cv.take<int32_t>(noff);
+    R.off_key = cv.take<uint64_t>(noff);
+    R.off_b = cv.take<uint32_t>(noff);
+    R.ctr = cv.take<RoundCounters>(1);
+    if (r > 0) {
+      R.Kc = cv.take<uint64_t>(N + 1);
+      R.Bc = cv.take<uint32_t>(N + 1);
+    } else {
+      R.Kc = L.Kc;
+      R.Bc = L.Bc;
+    }
+    if (general) {
+      R.in_off = cv.take<unsigned long long>(N + 1);
+      R.in_len = cv.take<int32_t>(N);
+      R.in_src = cv.take<int32_t>(n * (int64_t)k);
+      R.in_w = cv.take<float>(n * (int64_t)k);
+      R.in_act[0] = cv.take<int32_t>(N);
+      R.in_act[1] = cv.take<int32_t>(N);
+    }
+  }
+  return cv.off + 256;
+}
+
+kdb_status validate_graph(const kdb_graph* g) {
+  if (!g) return set_err(KDB_EINVAL, "graph is NULL");
+  if (g->n_total < 0 || g->n_total >= (int64_t)INT32_MAX)
+    return set_err(KDB_EINVAL, "n_total out of range [0, 2^31-1)");
+  if (g->k_max < 1 || g->k_max > 65535) return set_err(KDB_EINVAL, "k_max must be in [1, 65535]");
+  if (g->n_rows < 0 || g->row_begin < 0 || g->row_begin + g->n_rows > g->n_total)
+    return set_err(KDB_EINVAL, "rank row range outside [0, n_total)");
+  if (g->n_rows > 0 && (!g->nbr || !g->dist)) return set_err(KDB_EINVAL, "nbr/dist is NULL");
+  if (((uintptr_t)g->nbr & 15u) || ((uintptr_t)g->dist & 15u))
+    return set_err(KDB_EINVAL, "nbr/dist must be 16-byte aligned");
+  if (g->flags & ~KDB_GRAPH_EXACT) return set_err(KDB_EINVAL, "unknown graph flags");
+  return KDB_OK;
+}
+
+kdb_status validate_eps(float eps) {
+  if (!(eps > 0.0f) || !(eps < __builtin_inff())) return set_err(KDB_EINVAL, "eps must be in (0, +inf)");
+  return KDB_OK;
+}
+
+// rank ranges of the computation this process performs
+void rank_ranges(const kdb_graph* g, kdb_comm* comm, std::vector<int64_t>& rb, std::vector<int64_t>& rn) {
+  rb.clear();
+  rn.clear();
+  if (comm && comm->kind == 2) {
+    const int P = comm->nranks;
+    for (int r = 0; r < P; ++r) {
+      const int64_t b = g->n_rows * r / P, e = g->n_rows * (r + 1) / P;
+      rb.push_back(g->row_begin + b);
+      rn.push_back(e - b);
+    }
+  } else {
+    rb.push_back(g->row_begin);
+    rn.push_back(g->n_rows);
+  }
+}
+
+kdb_status allreduce_min_u64(kdb_comm* comm, uint64_t* p, int64_t n, cudaStream_t st) {
+  if (!comm || comm->kind != 1 || comm->nranks == 1 || n <= 0) return KDB_OK;
+  return nccl_check(g_nccl.AllReduce(p, p, (size_t)n, ncclUint64, ncclMin, comm->nccl, st), "ncclAllReduce(u64,min)");
+}
+kdb_status allreduce_min_u32(kdb_comm* comm, uint32_t* p, int64_t n, cudaStream_t st) {
+  if (!comm || comm->kind != 1 || comm->nranks == 1 || n <= 0) return KDB_OK;
+  return nccl_check(g_nccl.AllReduce(p, p, (size_t)n, ncclUint32, ncclMin, comm->nccl, st), "ncclAllReduce(u32,min)");
+}
+
+}  // namespace
+
+// ============================================================================
+// C-ABI
+// ============================================================================
+extern "C" {
+
+const char* kdb_status_string(kdb_status s) {
+  switch (s) {
+    case KDB_OK: return "KDB_OK";
+    case KDB_EINVAL: return "KDB_EINVAL";
+    case KDB_ENOMEM: return "KDB_ENOMEM";
+    case KDB_ECUDA: return "KDB_ECUDA";
+    case KDB_ENCCL: return "KDB_ENCCL";
+    case KDB_EINTERNAL: return "KDB_EINTERNAL";
+  }
+  return "KDB_?";
+}
+
+const char* kdb_last_error(void) { return g_err.c_str(); }
+
+int kdb_last_mst_stats(double* out, int cap) {
+  int n = std::min(cap, 8);
+  for (int i = 0; i < n; ++i) out[i] = g_stats[i];
+  return n;
+}
+
+void kdb_profile_enable(int on) { g_prof.on = on != 0; }
+
+void kdb_profile_reset(void) {
+  g_prof.drain();
+  g_prof.names.clear();
+  g_prof.ms.clear();
+  g_prof.cnt.clear();
+  g_prof.launches = 0;
+}
+
+long long kdb_launch_count(void) { return g_prof.launches; }
+
+int kdb_profile_read(char* names, size_t names_len, double* ms, long long* counts, int cap) {
+  g_prof.drain();
+  size_t off = 0;
+  int n = 0;
+  for (size_t i = 0; i < g_prof.names.size() && n < cap; ++i, ++n) {
+    ms[n] = g_prof.ms[i];
+    counts[n] = g_prof.cnt[i];
+    const std::string& nm = g_prof.names[i];
+    if (names && off + nm.size() + 1 < names_len) {
+      memcpy(names + off, nm.c_str(), nm.size());
+      off += nm.size();
+      names[off++] = '\n';
+      names[off] = 0;
+    }
+  }
+  return n;
+}
+
+kdb_status kdb_nccl_unique_id(void* out) {
+  if (!out) return set_err(KDB_EINVAL, "out is NULL");
+  KDB_TRY(nccl_load());
+  ncclUniqueId id;
+  KDB_TRY(nccl_check(g_nccl.GetUniqueId(&id), "ncclGetUniqueId"));
+  memcpy(out, &id, sizeof(id));
+  return KDB_OK;
+}
+
+kdb_status kdb_comm_create_nccl(kdb_comm** out, const void* uid, int rank, int nranks) {
+  if (!out || !uid || nranks < 1 || rank < 0 || rank >= nranks)
+    return set_err(KDB_EINVAL, "bad communicator arguments");
+  KDB_TRY(nccl_load());
+  ncclUniqueId id;
+  memcpy(&id, uid, sizeof(id));
+  kdb_comm* c = new kdb_comm();
+  c->kind = 1;
+  c->rank = rank;
+  c->nranks = nranks;
+  kdb_status s = nccl_check(g_nccl.CommInitRank(&c->nccl, nranks, id, rank), "ncclCommInitRank");
+  if (s != KDB_OK) {
+    delete c;
+    return s;
+  }
+  *out = c;
+  return KDB_OK;
+}
+
+kdb_status kdb_comm_create_sim(kdb_comm** out, int nranks) {
+  if (!out || nranks < 1 || nranks > 1024) return set_err(KDB_EINVAL, "bad sim rank count");
+  kdb_comm* c = new kdb_comm();
+  c->kind = 2;
+  c->rank = 0;
+  c->nranks = nranks;
+  *out = c;
+  return KDB_OK;
+}
+
+void kdb_comm_destroy(kdb_comm* c) {
+  if (!c) return;
+  if (c->kind == 1 && c->nccl && g_nccl.CommDestroy) g_nccl.CommDestroy(c->nccl);
+  delete c;
+}
+
+kdb_status kdb_core_mark(const kdb_graph* g, int32_t M, float eps, uint32_t* core_bits, kdb_comm* comm,
+                         kdb_stream_t stream) {
+  KDB_TRY(validate_graph(g));
+  KDB_TRY(validate_eps(eps));
+  if (M < 1 || M > g->k_max) return set_err(KDB_EINVAL, "M must be in [1, k_max]");
+  if (!core_bits && g->n_total > 0) return set_err(KDB_EINVAL, "core_bits is NULL");
+  if (comm && comm->kind == 2 && (g->row_begin != 0 || g->n_rows != g->n_total))
+    return set_err(KDB_EINVAL, "sim communicator needs the full graph");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t nwords = (g->n_total + 31) / 32;
+  if (nwords == 0) return KDB_OK;
+  KDB_CUDA(cudaMemsetAsync(core_bits, 0, nwords * sizeof(uint32_t), st));
+  std::vector<int64_t> rb, rn;
+  rank_ranges(g, comm, rb, rn);
+  for (size_t r = 0; r < rb.size(); ++r) {
+    if (rn[r] == 0) continue;
+    const int64_t off = (rb[r] - g->row_begin) * g->k_max;
+    LAUNCH(k_core_mark, grid_for(rn[r]), kThreads, st, g->dist + off, rn[r], g->k_max, M, eps, rb[r], core_bits);
+    KDB_CUDA(cudaGetLastError());
+  }
+  // ranks own disjoint bits: SUM == OR
+  if (comm && comm->kind == 1 && comm->nranks > 1)
+    KDB_TRY(nccl_check(g_nccl.AllReduce(core_bits, core_bits, (size_t)nwords, ncclUint32, ncclSum,
+                                        comm->nccl, st), "ncclAllReduce(core bits)"));
+  if (g_prof.on) {  // profiling mode only: resolve timings now (synchronises)
+    KDB_CUDA(cudaStreamSynchronize(st));
+    g_prof.drain();
+  }
+  return KDB_OK;
+}
+
+size_t kdb_mst_workspace_bytes(const kdb_graph* g, kdb_comm* comm) {
+  if (validate_graph(g) != KDB_OK) return 0;
+  std::vector<int64_t> rb, rn;
+  rank_ranges(g, comm, rb, rn);
+  Layout L;
+  return carve(L, nullptr, true, g->n_total, (int)rb.size(), rb.data(), rn.data(),
+               !(g->flags & KDB_GRAPH_EXACT), g->k_max);
+}
+
+kdb_status kdb_mst(const kdb_graph* g, float eps, const uint32_t* core_bits, int32_t* comp,
+                   uint32_t* mst_a, uint32_t* mst_b, float* mst_w, int64_t mst_cap, int64_t* mst_count,
+                   double* mst_weight, void* workspace, size_t ws_bytes, kdb_comm* comm,
+                   kdb_stream_t stream) {
+  KDB_TRY(validate_graph(g));
+  KDB_TRY(validate_eps(eps));
+  const int64_t N = g->n_total;
+  if (!mst_count || !mst_weight) return set_err(KDB_EINVAL, "mst_count/mst_weight is NULL");
+  if (N > 0 && (!core_bits || !comp || !workspace)) return set_err(KDB_EINVAL, "NULL device pointer");
+  if (mst_cap < 0 || (mst_cap > 0 && (!mst_a || !mst_b || !mst_w)))
+    return set_err(KDB_EINVAL, "bad MSF output arrays");
+  if (comm && comm->kind == 2 && (g->row_begin != 0 || g->n_rows != g->n_total))
+    return set_err(KDB_EINVAL, "sim communicator needs the full graph");
+  if ((uintptr_t)workspace & 255u) return set_err(KDB_EINVAL, "workspace must be 256-byte aligned");
+  const bool general = !(g->flags & KDB_GRAPH_EXACT);
+  const int32_t k = g->k_max;
+  std::vector<int64_t> rb, rn;
+  rank_ranges(g, comm, rb, rn);
+  Layout L;
+  const size_t need = carve(L, (char*)workspace, false, N, (int)rb.size(), rb.data(), rn.data(), general, k);
+  if (ws_bytes < need) return set_err(KDB_ENOMEM, "workspace %zu < required %zu bytes", ws_bytes, need);
+  *mst_count = 0;
+  *mst_weight = 0.0;
+  for (auto& s : g_stats) s = 0;
+  if (N == 0) return KDB_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  for (auto& R : L.ranks) {
+    R.nbr = g->nbr + (R.row_begin - g->row_begin) * k;
+    R.dist = g->dist + (R.row_begin - g->row_begin) * k;
+  }
+  cudaEvent_t ev[4];
+  for (auto& e : ev) KDB_CUDA(cudaEventCreate(&e));
+  struct EvGuard {
+    cudaEvent_t* e;
+    ~EvGuard() { for (int i = 0; i < 4; ++i) cudaEventDestroy(e[i]); }
+  } guard{ev};
+  float ms = 0;
+  KDB_CUDA(cudaEventRecord(ev[0], st));
+
+  // ---- a2: dense component ids -------------------------------------------------
+  const int64_t nwords = (N + 31) / 32;
+  uint32_t* popc = reinterpret_cast<uint32_t*>(L.flag);  // scratch, nwords + 1 <= N + 1
+  KDB_CUDA(cudaMemsetAsync(popc + nwords, 0, sizeof(uint32_t), st));
+  KDB_CUDA(cudaMemsetAsync(L.ctr, 0, sizeof(RoundCounters), st));
+  LAUNCH(k_popc_words, grid_for(nwords), kThreads, st, core_bits, nwords, popc);
+  KDB_CUDA(cudaGetLastError());
+  size_t cb = L.cub_bytes;
+  { LaunchScope ls_("cub::DeviceScan", st, false); KDB_CUDA(cub::DeviceScan::ExclusiveSum(L.cub_tmp, cb, popc, L.woff, (int)(nwords + 1), st)); }
+  uint32_t C32 = 0;  // woff[nwords] = number of core points
+  KDB_CUDA(cudaMemcpyAsync(&C32, L.woff + nwords, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+  KDB_CUDA(cudaStreamSynchronize(st));
+  int64_t C = C32;
+  LAUNCH(k_init_comp, grid_for(N), kThreads, st, core_bits, L.woff, N, comp, L.cmin);
+  LAUNCH(k_fill_comp_arrays, grid_for(C), kThreads, st, C, L.Kc, L.Bc, general ? nullptr : L.kmin);
+  for (size_t r = 1; r < L.ranks.size(); ++r)
+    LAUNCH(k_fill_comp_arrays, grid_for(C), kThreads, st, C, L.ranks[r].Kc, L.ranks[r].Bc, nullptr);
+  KDB_CUDA(cudaGetLastError());
+  for (auto& R : L.ranks) {
+    KDB_CUDA(cudaMemsetAsync(R.ctr, 0, sizeof(RoundCounters), st));
+    if (R.n_rows > 0)
+      LAUNCH(k_init_rows, grid_for(R.n_rows), kThreads, st, R.dist, R.n_rows, k, eps, R.row_begin, core_bits,
+                                                           comp, R.head, general ? nullptr : L.kmin,
+                                                           R.act[0], &R.ctr->n_act[0]);
+    KDB_CUDA(cudaGetLastError());
+  }
+  if (!general) KDB_TRY(allreduce_min_u32(comm, L.kmin, C, st));
+  KDB_CUDA(cudaEventRecord(ev[1], st));
+  // ---- general mode: in-edge lists --------------------------------------------
+  if (general) {
+    for (auto& R : L.ranks) {
+      // counts -> scan -> offsets; e_key (N+1 u64) is scratch for counts and cursors
+      unsigned long long* cursor = reinterpret_cast<unsigned long long*>(L.e_key);
+      KDB_CUDA(cudaMemsetAsync(cursor, 0, (N + 1) * sizeof(unsigned long long), st));
+      if (R.n_rows > 0)
+        LAUNCH(k_in_count, grid_for(R.n_rows), kThreads, st, R.nbr, R.dist, R.n_rows, k, eps, R.row_begin, N,
+                                                            core_bits, cursor);
+      cb = L.cub_bytes;
+      { LaunchScope ls_("cub::DeviceScan", st, false); KDB_CUDA(cub::DeviceScan::ExclusiveSum(L.cub_tmp, cb, cursor, R.in_off, (int)(N + 1), st)); }
+      KDB_CUDA(cudaMemcpyAsync(cursor, R.in_off, (N + 1) * sizeof(unsigned long long),
+                               cudaMemcpyDeviceToDevice, st));
+      if (R.n_rows > 0)
+        LAUNCH(k_in_fill, grid_for(R.n_rows), kThreads, st, R.nbr, R.dist, R.n_rows, k, eps, R.row_begin, N,
+                                                           core_bits, cursor, R.in_src, R.in_w);
+      LAUNCH(k_in_finish, grid_for(N), kThreads, st, R.in_off, N, R.in_len, R.in_act[0], &R.ctr->n_act[1]);
+      KDB_CUDA(cudaGetLastError());
+    }
+  }
+  for (auto& R : L.ranks) {
+    RoundCounters hc;
+    KDB_CUDA(cudaMemcpyAsync(&hc, R.ctr, sizeof(hc), cudaMemcpyDeviceToHost, st));
+    KDB_CUDA(cudaStreamSynchronize(st));
+    R.n_act = hc.n_act[0];
+    R.n_in_act = hc.n_act[1];
+  }
+  KDB_CUDA(cudaEventRecord(ev[2], st));
+  KDB_CUDA(cudaEventSynchronize(ev[2]));
+  KDB_CUDA(cudaEventElapsedTime(&ms, ev[0], ev[1]));
+  g_stats[1] = ms;
+  KDB_CUDA(cudaEventElapsedTime(&ms, ev[1], ev[2]));
+  g_stats[5] = ms;
+
+  // ---- Boruvka rounds -------------------------------------------------------------
+  int cur = 0;
+  int rounds = 0, stalls = 0;
+  const uint32_t* kmin_cert = general ? nullptr : L.kmin;
+  double t_min_edges = 0, t_contract = 0;
+  while (C > 0) {
+    ++rounds;
+    KDB_CUDA(cudaEventRecord(ev[0], st));
+    // a3: offers (rows, then in-lists), per rank, into that rank's Kc partial
+    for (auto& R : L.ranks) {
+      KDB_CUDA(cudaMemsetAsync(&R.ctr->n_act[0], 0, 3 * sizeof(uint32_t), st));  // n_act[0..1], n_off
+      if (R.n_act)
+        LAUNCH(k_offer_rows, grid_for(R.n_act), kThreads, st, 
+            R.nbr, R.dist, k, eps, R.row_begin, N, core_bits, comp, R.act[cur], R.n_act, R.head,
+            R.act[cur ^ 1], &R.ctr->n_act[0], R.off_v, R.off_key, R.off_b, &R.ctr->n_off,
+            (unsigned long long*)R.Kc);
+      if (general && R.n_in_act)
+        LAUNCH(k_offer_in, grid_for(R.n_in_act), kThreads, st, 
+            R.in_off, R.in_len, R.in_src, R.in_w, comp, R.in_act[cur], R.n_in_act, R.in_act[cur ^ 1],
+            &R.ctr->n_act[1], R.off_v, R.off_key, R.off_b, &R.ctr->n_off, (unsigned long long*)R.Kc);
+      KDB_CUDA(cudaGetLastError());
+    }
+    for (auto& R : L.ranks) {
+      RoundCounters hc;
+      KDB_CUDA(cudaMemcpyAsync(&hc, R.ctr, sizeof(hc), cudaMemcpyDeviceToHost, st));
+      KDB_CUDA(cudaStreamSynchronize(st));
+      R.n_act = hc.n_act[0];
+      R.n_in_act = hc.n_act[1];
+      R.n_off = hc.n_off;
+    }
+    // exchange: sim -> min over virtual ranks; nccl -> allreduce
+    for (size_t r = 1; r < L.ranks.size(); ++r)
+      LAUNCH(k_min_into_u64, grid_for(C), kThreads, st, L.Kc, L.ranks[r].Kc, C);
+    KDB_TRY(allreduce_min_u64(comm, L.Kc, C, st));
+    // a4: ties
+    for (auto& R : L.ranks) {
+      if (R.n_off)
+        LAUNCH(k_tie, grid_for(R.n_off), kThreads, st, R.off_v, R.off_key, R.off_b, R.n_off, comp, L.Kc, R.Bc);
+      KDB_CUDA(cudaGetLastError());
+    }
+    for (size_t r = 1; r < L.ranks.size(); ++r)
+      LAUNCH(k_min_into_u32, grid_for(C), kThreads, st, L.Bc, L.ranks[r].Bc, C);
+    KDB_TRY(allreduce_min_u32(comm, L.Bc, C, st));
+    KDB_CUDA(cudaEventRecord(ev[1], st));
+    // a5: hook + emit
+    KDB_CUDA(cudaMemsetAsync(&L.ctr->hooks, 0, 4 * sizeof(uint32_t), st));
+    LAUNCH(k_hook, grid_for(C), kThreads, st, C, L.Kc, L.Bc, kmin_cert, comp, L.parent, L.e_key, L.e_w, N,
+                                             L.ctr);
+    KDB_CUDA(cudaGetLastError());
+    RoundCounters hc;
+    KDB_CUDA(cudaMemcpyAsync(&hc, L.ctr, sizeof(hc), cudaMemcpyDeviceToHost, st));
+    KDB_CUDA(cudaStreamSynchronize(st));
+    if (hc.offered == 0) {  // a8: no component has a leaving edge
+      KDB_CUDA(cudaEventRecord(ev[2], st));
+      KDB_CUDA(cudaEventSynchronize(ev[2]));
+      KDB_CUDA(cudaEventElapsedTime(&ms, ev[0], ev[1]));
+      t_min_edges += ms;
+      break;
+    }
+    if (hc.hooks == 0) {
+      // every offering component abstained: one edge-centric sweep round gives
+      // every component its exact minimum (both endpoints see every entry)
+      ++stalls;
+      LAUNCH(k_fill_comp_arrays, grid_for(C), kThreads, st, C, L.Kc, L.Bc, nullptr);
+      for (size_t r = 1; r < L.ranks.size(); ++r)
+        LAUNCH(k_fill_comp_arrays, grid_for(C), kThreads, st, C, L.ranks[r].Kc, L.ranks[r].Bc, nullptr);
+      for (auto& R : L.ranks)
+        if (R.n_rows)
+          LAUNCH(k_sweep, grid_for(R.n_rows), kThreads, st, R.nbr, R.dist, R.n_rows, k, eps, R.row_begin, N,
+                                                           core_bits, comp, R.head,
+                                                           (unsigned long long*)R.Kc, R.Bc, 0);
+      for (size_t r = 1; r < L.ranks.size(); ++r)
+        LAUNCH(k_min_into_u64, grid_for(C), kThreads, st, L.Kc, L.ranks[r].Kc, C);
+      KDB_TRY(allreduce_min_u64(comm, L.Kc, C, st));
+      for (auto& R : L.ranks)
+        if (R.n_rows)
+          LAUNCH(k_sweep, grid_for(R.n_rows), kThreads, st, R.nbr, R.dist, R.n_rows, k, eps, R.row_begin, N,
+                                                           core_bits, comp, R.head,
+                                                           (unsigned long long*)L.Kc, R.Bc, 1);
+      for (size_t r = 1; r < L.ranks.size(); ++r)
+        LAUNCH(k_min_into_u32, grid_for(C), kThreads, st, L.Bc, L.ranks[r].Bc, C);
+      KDB_TRY(allreduce_min_u32(comm, L.Bc, C, st));
+      KDB_CUDA(cudaMemsetAsync(&L.ctr->hooks, 0, 4 * sizeof(uint32_t), st));
+      LAUNCH(k_hook, grid_for(C), kThreads, st, C, L.Kc, L.Bc, nullptr, comp, L.parent, L.e_key, L.e_w, N,
+                                               L.ctr);
+      KDB_CUDA(cudaGetLastError());
+      KDB_CUDA(cudaMemcpyAsync(&hc, L.ctr, sizeof(hc), cudaMemcpyDeviceToHost, st));
+      KDB_CUDA(cudaStreamSynchronize(st));
+      if (hc.hooks == 0) return set_err(KDB_EINTERNAL, "sweep round made no progress");
+      // vertices whose rows were exhausted stay out of the active list; rows
+      // that still hold leaving entries are in it (exhaustion is permanent)
+    }
+    if (hc.violation) return set_err(KDB_EINVAL, "graph violates the KDB_GRAPH_EXACT promise (a component's "
+                                     "minimum missed an incident edge)");
+    // a6: contract
+    LAUNCH(k_jump, grid_for(C), kThreads, st, C, L.parent, L.rootof, L.ctr);
+    LAUNCH(k_root_flags, grid_for(C), kThreads, st, C, L.rootof, L.flag);
+    cb = L.cub_bytes;
+    { LaunchScope ls_("cub::DeviceScan", st, false); KDB_CUDA(cub::DeviceScan::ExclusiveSum(L.cub_tmp, cb, L.flag, L.newid, (int)C, st)); }
+    uint32_t viol = 0;
+    KDB_CUDA(cudaMemcpyAsync(&viol, &L.ctr->violation, 4, cudaMemcpyDeviceToHost, st));
+    int32_t last[2];
+    KDB_CUDA(cudaMemcpyAsync(&last[0], L.newid + C - 1, 4, cudaMemcpyDeviceToHost, st));
+    KDB_CUDA(cudaMemcpyAsync(&last[1], L.flag + C - 1, 4, cudaMemcpyDeviceToHost, st));
+    KDB_CUDA(cudaStreamSynchronize(st));
+    if (viol) return set_err(KDB_EINTERNAL, "pointer jumping did not converge (hook cycle)");
+    const int64_t C2 = (int64_t)last[0] + last[1];
+    LAUNCH(k_fill_i32, grid_for(C2), kThreads, st, L.cmin2, C2, INT32_MAX);
+    if (!general) LAUNCH(k_fill_i32, grid_for(C2), kThreads, st, (int32_t*)L.kmin2, C2, (int32_t)kInfBits);
+    LAUNCH(k_merge, grid_for(C), kThreads, st, C, L.rootof, L.newid, L.cmin, general ? nullptr : L.kmin, L.cmin2,
+                                              L.kmin2);
+    LAUNCH(k_relabel, grid_for(N), kThreads, st, N, comp, L.rootof, L.newid);
+    LAUNCH(k_fill_comp_arrays, grid_for(C2), kThreads, st, C2, L.Kc, L.Bc, nullptr);
+    for (size_t r = 1; r < L.ranks.size(); ++r)
+      LAUNCH(k_fill_comp_arrays, grid_for(C2), kThreads, st, C2, L.ranks[r].Kc, L.ranks[r].Bc, nullptr);
+    KDB_CUDA(cudaGetLastError());
+    std::swap(L.cmin, L.cmin2);
+    std::swap(L.kmin, L.kmin2);
+    kmin_cert = general ? nullptr : L.kmin;
+    C = C2;
+    cur ^= 1;
+    KDB_CUDA(cudaEventRecord(ev[2], st));
+    KDB_CUDA(cudaEventSynchronize(ev[2]));
+    KDB_CUDA(cudaEventElapsedTime(&ms, ev[0], ev[1]));
+    t_min_edges += ms;
+    KDB_CUDA(cudaEventElapsedTime(&ms, ev[1], ev[2]));
+    t_contract += ms;
+  }
+  // ---- finalize ---------------------------------------------------------------------
+  KDB_CUDA(cudaEventRecord(ev[0], st));
+  RoundCounters hc;
+  KDB_CUDA(cudaMemcpyAsync(&hc, L.ctr, sizeof(hc), cudaMemcpyDeviceToHost, st));
+  KDB_CUDA(cudaStreamSynchronize(st));
+  const int64_t m = (int64_t)hc.msf_count;
+  if (m > N) return set_err(KDB_EINTERNAL, "MSF larger than N-1");
+  if (m > mst_cap) return set_err(KDB_EINVAL, "mst_cap %lld < MSF size %lld", (long long)mst_cap, (long long)m);
+  LAUNCH(k_canon, grid_for(N), kThreads, st, N, comp, L.cmin);
+  KDB_CUDA(cudaGetLastError());
+  unsigned long long bk[256];
+  if (m > 0) {
+    cb = L.cub_bytes;
+    { LaunchScope ls_("cub::DeviceRadixSort", st, false); KDB_CUDA(cub::DeviceRadixSort::SortPairs(L.cub_tmp, cb, L.e_key, L.e_key_sorted, L.e_w, mst_w, (int)m, 0, 64, st)); }
+    LAUNCH(k_split_edges, grid_for(m), kThreads, st, m, L.e_key_sorted, mst_a, mst_b);
+    KDB_CUDA(cudaMemsetAsync(L.buckets, 0, 256 * sizeof(unsigned long long), st));
+    LAUNCH(k_wbuckets, grid_for(m), kThreads, st, m, mst_w, L.buckets);
+    KDB_CUDA(cudaGetLastError());
+    KDB_CUDA(cudaMemcpyAsync(bk, L.buckets, sizeof(bk), cudaMemcpyDeviceToHost, st));
+  }
+  KDB_CUDA(cudaEventRecord(ev[1], st));
+  KDB_CUDA(cudaStreamSynchronize(st));
+  KDB_CUDA(cudaEventElapsedTime(&ms, ev[0], ev[1]));
+  if (g_prof.on) g_prof.drain();
+  *mst_count = m;
+  *mst_weight = m > 0 ? exact_bucket_sum(bk) : 0.0;
+  g_stats[0] = rounds;
+  g_stats[2] = t_min_edges;
+  g_stats[3] = t_contract;
+  g_stats[4] = ms;
+  g_stats[6] = stalls;
+  return KDB_OK;
+}
+
+kdb_status kdb_label(const kdb_graph* g, float eps, const uint32_t* core_bits, const int32_t* comp,
+                     int32_t* labels, kdb_stream_t stream) {
+  KDB_TRY(validate_graph(g));
+  KDB_TRY(validate_eps(eps));
+  if (g->n_rows > 0 && (!core_bits || !comp || !labels)) return set_err(KDB_EINVAL, "NULL device pointer");
+  if (g->n_rows == 0) return KDB_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  LAUNCH(k_label, grid_for(g->n_rows), kThreads, st, g->nbr, g->dist, g->n_rows, g->k_max, eps, g->row_begin,
+                                                    g->n_total, core_bits, comp, labels);
+  KDB_CUDA(cudaGetLastError());
+  if (g_prof.on) {
+    KDB_CUDA(cudaStreamSynchronize(st));
+    g_prof.drain();
+  }
+  return KDB_OK;
+}
+
+}  // extern "C"

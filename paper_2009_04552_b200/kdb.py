@@ -1,0 +1,268 @@
+"""Thin Python binding of libkdb.so (include/kdb.h) -- argument marshalling only.
+
+Every step of the clustering stage runs in the CUDA kernels of
+``csrc/kdb.cu``; this module passes ``tensor.data_ptr()`` and the current
+torch stream through ctypes.  There is NO CPU fallback: if the shared library
+is missing or fails to load, every call raises ``KdbError``.
+
+Names follow the paper (Alg. 1): ``core_mark`` (lines 3-8),
+``mst`` (ParallelLocalMST + DistributedCutMST, lines 10-12), ``label``
+(ClusterBorder, line 13).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libkdb.so")
+KDB_GRAPH_EXACT = 1
+
+
+class KdbError(RuntimeError):
+    pass
+
+
+_lib = None
+
+
+class _Graph(C.Structure):
+    _fields_ = [("n_total", C.c_int64), ("row_begin", C.c_int64), ("n_rows", C.c_int64),
+                ("k_max", C.c_int32), ("nbr", C.c_void_p), ("dist", C.c_void_p),
+                ("flags", C.c_uint32)]
+
+
+def lib():
+    """Load libkdb.so (raises KdbError if it is not built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise KdbError(f"libkdb.so not built ({LIB_PATH}); run `make` or __graft_entry__.build()")
+    L = C.CDLL(LIB_PATH)
+    P, i32, i64, f32, u32 = C.c_void_p, C.c_int32, C.c_int64, C.c_float, C.c_uint32
+    G = C.POINTER(_Graph)
+    L.kdb_status_string.restype = C.c_char_p
+    L.kdb_status_string.argtypes = [C.c_int]
+    L.kdb_last_error.restype = C.c_char_p
+    L.kdb_nccl_unique_id.argtypes = [P]
+    L.kdb_comm_create_nccl.argtypes = [C.POINTER(P), P, C.c_int, C.c_int]
+    L.kdb_comm_create_sim.argtypes = [C.POINTER(P), C.c_int]
+    L.kdb_comm_destroy.argtypes = [P]
+    L.kdb_comm_destroy.restype = None
+    L.kdb_core_mark.argtypes = [G, i32, f32, P, P, P]
+    L.kdb_mst_workspace_bytes.argtypes = [G, P]
+    L.kdb_mst_workspace_bytes.restype = C.c_size_t
+    L.kdb_mst.argtypes = [G, f32, P, P, P, P, P, i64, C.POINTER(i64), C.POINTER(C.c_double), P,
+                          C.c_size_t, P, P]
+    L.kdb_label.argtypes = [G, f32, P, P, P, P]
+    L.kdb_last_mst_stats.argtypes = [C.POINTER(C.c_double), C.c_int]
+    L.kdb_profile_enable.argtypes = [C.c_int]
+    L.kdb_profile_enable.restype = None
+    L.kdb_profile_reset.restype = None
+    L.kdb_launch_count.restype = C.c_longlong
+    L.kdb_profile_read.argtypes = [C.c_char_p, C.c_size_t, C.POINTER(C.c_double), C.POINTER(C.c_longlong), C.c_int]
+    _lib = L
+    return L
+
+
+# the symbols include/kdb.h declares (checked by the CPU test suite)
+EXPORTS = sorted(["kdb_nccl_unique_id", "kdb_comm_create_nccl", "kdb_comm_create_sim", "kdb_comm_destroy",
+                  "kdb_core_mark", "kdb_mst_workspace_bytes", "kdb_mst", "kdb_label", "kdb_last_mst_stats",
+                  "kdb_profile_enable", "kdb_profile_reset", "kdb_launch_count", "kdb_profile_read",
+                  "kdb_status_string", "kdb_last_error"])
+
+
+def _check(rc: int, what: str):
+    if rc != 0:
+        L = lib()
+        raise KdbError(f"{what}: {L.kdb_status_string(rc).decode()}: {L.kdb_last_error().decode()}")
+
+
+def _stream(stream):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+class Comm:
+    """A kdb communicator: ``Comm.sim(P)`` (P virtual ranks on one GPU) or
+    ``Comm.nccl(rank, nranks, group)`` (one rank per GPU; the 128-byte NCCL id
+    is created on rank 0 and broadcast with torch.distributed)."""
+
+    def __init__(self, handle, nranks: int, rank: int, kind: str):
+        self.handle, self.nranks, self.rank, self.kind = handle, nranks, rank, kind
+
+    @classmethod
+    def sim(cls, nranks: int) -> "Comm":
+        h = C.c_void_p()
+        _check(lib().kdb_comm_create_sim(C.byref(h), int(nranks)), "kdb_comm_create_sim")
+        return cls(h, nranks, 0, "sim")
+
+    @classmethod
+    def nccl(cls, rank: int, nranks: int, group=None) -> "Comm":
+        import torch.distributed as dist
+        buf = (C.c_ubyte * 128)()
+        if rank == 0:
+            _check(lib().kdb_nccl_unique_id(C.cast(buf, C.c_void_p)), "kdb_nccl_unique_id")
+        obj = [bytes(buf)]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        C.memmove(buf, obj[0], 128)
+        h = C.c_void_p()
+        _check(lib().kdb_comm_create_nccl(C.byref(h), C.cast(buf, C.c_void_p), int(rank), int(nranks)),
+               "kdb_comm_create_nccl")
+        return cls(h, nranks, rank, "nccl")
+
+    def close(self):
+        if self.handle is not None:
+            lib().kdb_comm_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+@dataclass
+class Graph:
+    """This rank's rows of the kNN graph (device tensors, [n_rows, k])."""
+    nbr: torch.Tensor
+    dist: torch.Tensor
+    n_total: int
+    row_begin: int = 0
+    exact: bool = False
+
+    def __post_init__(self):
+        if self.nbr.dtype != torch.int32 or self.dist.dtype != torch.float32:
+            raise KdbError("nbr must be int32 and dist float32")
+        if self.nbr.shape != self.dist.shape or self.nbr.dim() != 2:
+            raise KdbError("nbr/dist must be [n_rows, k] tensors of equal shape")
+        if not (self.nbr.is_cuda and self.dist.is_cuda):
+            raise KdbError("nbr/dist must be CUDA tensors (there is no CPU path)")
+        if not (self.nbr.is_contiguous() and self.dist.is_contiguous()):
+            raise KdbError("nbr/dist must be contiguous")
+
+    @property
+    def k(self) -> int:
+        return int(self.nbr.shape[1])
+
+    @property
+    def n_rows(self) -> int:
+        return int(self.nbr.shape[0])
+
+    def c(self) -> _Graph:
+        return _Graph(int(self.n_total), int(self.row_begin), self.n_rows, self.k,
+                      self.nbr.data_ptr(), self.dist.data_ptr(),
+                      KDB_GRAPH_EXACT if self.exact else 0)
+
+
+def _h(comm):
+    return comm.handle if comm is not None else None
+
+
+def core_mark(g: Graph, M: int, eps: float, comm: Comm | None = None, stream=None) -> torch.Tensor:
+    """kdb_core_mark: int32[ceil(N/32)] bit words (uint32 semantics), replicated."""
+    bits = torch.empty((g.n_total + 31) // 32, dtype=torch.int32, device=g.dist.device)
+    gc = g.c()
+    _check(lib().kdb_core_mark(C.byref(gc), int(M), float(eps), C.c_void_p(bits.data_ptr()),
+                               _h(comm), _stream(stream)), "kdb_core_mark")
+    return bits
+
+
+def workspace_bytes(g: Graph, comm: Comm | None = None) -> int:
+    gc = g.c()
+    return int(lib().kdb_mst_workspace_bytes(C.byref(gc), _h(comm)))
+
+
+class MstResult:
+    def __init__(self, comp, a, b, w, count, weight, stats):
+        self.comp, self.a, self.b, self.w = comp, a, b, w
+        self.count, self.weight, self.stats = count, weight, stats
+
+
+def mst(g: Graph, eps: float, core_bits: torch.Tensor, comm: Comm | None = None, stream=None,
+        workspace: torch.Tensor | None = None, out: dict | None = None) -> MstResult:
+    """kdb_mst: exact MSF of the core-core candidate edges + component labels."""
+    dev = g.dist.device
+    N = g.n_total
+    o = out or {}
+    comp = o.get("comp")
+    if comp is None:
+        comp = torch.empty(max(N, 1), dtype=torch.int32, device=dev)
+    cap = max(N - 1, 0)
+    a = o.get("a"); b = o.get("b"); w = o.get("w")
+    if a is None:
+        a = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
+        b = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
+        w = torch.empty(max(cap, 1), dtype=torch.float32, device=dev)
+    nws = workspace_bytes(g, comm)
+    if workspace is None or workspace.numel() < nws:
+        workspace = torch.empty(max(nws, 256), dtype=torch.uint8, device=dev)
+    cnt = C.c_int64(0)
+    tot = C.c_double(0.0)
+    gc = g.c()
+    _check(lib().kdb_mst(C.byref(gc), float(eps), C.c_void_p(core_bits.data_ptr()),
+                         C.c_void_p(comp.data_ptr()), C.c_void_p(a.data_ptr()), C.c_void_p(b.data_ptr()),
+                         C.c_void_p(w.data_ptr()), cap, C.byref(cnt), C.byref(tot),
+                         C.c_void_p(workspace.data_ptr()), workspace.numel(), _h(comm), _stream(stream)),
+           "kdb_mst")
+    st = (C.c_double * 8)()
+    lib().kdb_last_mst_stats(st, 8)
+    stats = dict(rounds=int(st[0]), init_ms=st[1], min_edges_ms=st[2], contract_ms=st[3],
+                 finalize_ms=st[4], inlist_ms=st[5], stall_rounds=int(st[6]))
+    m = cnt.value
+    return MstResult(comp[:N], a[:m], b[:m], w[:m], m, tot.value, stats)
+
+
+def label(g: Graph, eps: float, core_bits: torch.Tensor, comp: torch.Tensor, stream=None,
+          out: torch.Tensor | None = None) -> torch.Tensor:
+    """kdb_label: canonical labels of this rank's rows (-1 = noise)."""
+    labels = out if out is not None else torch.empty(max(g.n_rows, 1), dtype=torch.int32, device=g.dist.device)
+    gc = g.c()
+    _check(lib().kdb_label(C.byref(gc), float(eps), C.c_void_p(core_bits.data_ptr()),
+                           C.c_void_p(comp.data_ptr()), C.c_void_p(labels.data_ptr()), _stream(stream)),
+           "kdb_label")
+    return labels[:g.n_rows]
+
+
+def profile(on: bool = True):
+    """Enable/disable per-kernel event timing inside libkdb.so."""
+    lib().kdb_profile_enable(1 if on else 0)
+
+
+def profile_reset():
+    lib().kdb_profile_reset()
+
+
+def launch_count() -> int:
+    return int(lib().kdb_launch_count())
+
+
+def profile_read() -> dict:
+    """{kernel name: (total device ms, launches)} since the last reset."""
+    cap = 128
+    names = C.create_string_buffer(16384)
+    ms = (C.c_double * cap)()
+    cnt = (C.c_longlong * cap)()
+    n = lib().kdb_profile_read(names, 16384, ms, cnt, cap)
+    nm = names.value.decode().split("\n")
+    return {nm[i]: (ms[i], int(cnt[i])) for i in range(n)}
+
+
+def kdbscan(g: Graph, M: int, eps: float, comm: Comm | None = None, stream=None):
+    """The whole clustering stage (Alg. 1): returns (core_bits, MstResult, labels)."""
+    bits = core_mark(g, M, eps, comm, stream)
+    r = mst(g, eps, bits, comm, stream)
+    lab = label(g, eps, bits, r.comp, stream)
+    return bits, r, lab
+
+
+def unpack_core(bits: torch.Tensor, n: int) -> torch.Tensor:
+    """uint8[n] core flags from the packed words (host-side helper for tests)."""
+    b = bits.cpu().numpy().view("uint32")
+    import numpy as np
+    return torch.from_numpy(((b[np.arange(n) >> 5] >> (np.arange(n) & 31).astype(np.uint32)) & 1).astype(np.uint8))

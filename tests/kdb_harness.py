@@ -1,0 +1,45 @@
+"""Shared helpers for the GPU parity tests: run the CUDA path through the C-ABI
+binding and the oracle on the same seeded inputs, and compare element by element.
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+import oracle
+import paper_2009_04552_b200 as kdb
+
+
+def run_gpu(nbr: np.ndarray, dist: np.ndarray, M: int, eps, *, exact: bool = False,
+            comm: "kdb.Comm | None" = None, device: str = "cuda:0"):
+    g = kdb.Graph(torch.from_numpy(np.ascontiguousarray(nbr, np.int32)).to(device),
+                  torch.from_numpy(np.ascontiguousarray(dist, np.float32)).to(device),
+                  n_total=nbr.shape[0], exact=exact)
+    bits, r, lab = kdb.kdbscan(g, M, float(np.float32(eps)), comm=comm)
+    torch.cuda.synchronize()
+    n = nbr.shape[0]
+    return dict(core=kdb.unpack_core(bits, n).numpy(), comp=r.comp.cpu().numpy(),
+                msf_a=r.a.cpu().numpy().astype(np.uint32), msf_b=r.b.cpu().numpy().astype(np.uint32),
+                msf_w=r.w.cpu().numpy(), msf_weight=r.weight, labels=lab.cpu().numpy(), stats=r.stats)
+
+
+def assert_parity(got: dict, exp: dict, rel_tol: float = 1e-6):
+    """Bit-exact core flags, labels, MSF edge set and weights; fp64 total within
+    rel_tol (north_star: 'MST total weight within 1e-6 relative')."""
+    assert np.array_equal(got["core"], exp["core"]), "core flags differ"
+    core = exp["core"].astype(bool)
+    assert np.array_equal(got["comp"][core], exp["labels"][core]), "core component labels differ"
+    assert np.all(got["comp"][~core] == -1), "non-core comp must be -1"
+    assert np.array_equal(got["labels"], exp["labels"]), "labels differ"
+    assert len(got["msf_a"]) == len(exp["msf_a"]), "MSF size differs"
+    assert np.array_equal(got["msf_a"], exp["msf_a"]) and np.array_equal(got["msf_b"], exp["msf_b"]), \
+        "MSF edge set differs"
+    assert np.array_equal(got["msf_w"].view(np.uint32) & 0x7fffffff,
+                          exp["msf_w"].view(np.uint32) & 0x7fffffff), "MSF weights differ"
+    ew = exp["msf_weight"]
+    assert abs(got["msf_weight"] - ew) <= rel_tol * max(abs(ew), 1e-300), \
+        f"MSF weight {got['msf_weight']!r} vs {ew!r}"
+
+
+def oracle_run(nbr, dist, M, eps):
+    return oracle.kdbscan(nbr, dist, M, np.float32(eps))

@@ -1,0 +1,101 @@
+"""CPU-side checks of the C-ABI library (-m "not gpu"): it loads without a GPU,
+exports every symbol include/kdb.h declares, and rejects invalid arguments
+before launching anything (host-side validation, include/kdb.h conventions).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "kdb.h")
+
+
+def declared_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(kdb_[a-z_0-9]+)\s*\(", src)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    import paper_2009_04552_b200 as kdb
+    if not os.path.exists(kdb.LIB_PATH):
+        subprocess.check_call(["make", "-C", ROOT, os.path.relpath(kdb.LIB_PATH, ROOT)])
+    return kdb.lib()
+
+
+def test_header_declares_the_three_calls():
+    fns = declared_functions()
+    for f in ("kdb_core_mark", "kdb_mst", "kdb_label", "kdb_mst_workspace_bytes"):
+        assert f in fns
+
+
+def test_library_exports_every_declared_symbol(lib):
+    import paper_2009_04552_b200 as kdb
+    fns = declared_functions()
+    missing = [f for f in fns if not hasattr(lib, f)]
+    assert not missing, missing
+    assert sorted(kdb.EXPORTS) == fns
+    # nm agrees (dynamic symbol table)
+    out = subprocess.run(["nm", "-D", "--defined-only", kdb.LIB_PATH], capture_output=True, text=True).stdout
+    for f in fns:
+        assert re.search(rf"\bT {f}$", out, flags=re.M), f
+
+
+def _graph(n_total=10, row_begin=0, n_rows=10, k=4, nbr=0x1000, dist=0x2000, flags=0):
+    import paper_2009_04552_b200.kdb as K
+    return K._Graph(n_total, row_begin, n_rows, k, nbr, dist, flags)
+
+
+@pytest.mark.parametrize("kw,M,eps", [
+    (dict(), 5, 0.5),                      # M > k
+    (dict(), 0, 0.5),                      # M < 1
+    (dict(), 2, 0.0),                      # eps not > 0
+    (dict(), 2, float("inf")),             # eps not finite
+    (dict(), 2, float("nan")),
+    (dict(k=0), 1, 0.5),                   # k < 1
+    (dict(n_rows=11), 2, 0.5),             # rows beyond n_total
+    (dict(row_begin=-1), 2, 0.5),
+    (dict(nbr=0), 2, 0.5),                 # NULL
+    (dict(dist=0x2004), 2, 0.5),           # misaligned
+    (dict(flags=8), 2, 0.5),               # unknown flag
+])
+def test_core_mark_validation(lib, kw, M, eps):
+    g = _graph(**kw)
+    rc = lib.kdb_core_mark(C.byref(g), M, eps, C.c_void_p(0x3000), None, None)
+    assert rc == 1  # KDB_EINVAL, nothing launched
+    assert lib.kdb_last_error()
+
+
+def test_mst_validation_and_workspace(lib):
+    g = _graph()
+    assert lib.kdb_mst_workspace_bytes(C.byref(g), None) > 0
+    exact = _graph(flags=1)
+    # exact graphs need no in-edge lists
+    assert lib.kdb_mst_workspace_bytes(C.byref(exact), None) < lib.kdb_mst_workspace_bytes(C.byref(g), None)
+    cnt = C.c_int64(); tot = C.c_double()
+    P = C.c_void_p
+    # workspace too small -> ENOMEM before any launch
+    rc = lib.kdb_mst(C.byref(g), 0.5, P(0x100), P(0x200), P(0x300), P(0x400), P(0x500), 9,
+                     C.byref(cnt), C.byref(tot), P(0x1000), 16, None, None)
+    assert rc == 2
+    # NULL host outputs
+    rc = lib.kdb_mst(C.byref(g), 0.5, P(0x100), P(0x200), P(0x300), P(0x400), P(0x500), 9,
+                     None, None, P(0x1000), 1 << 40, None, None)
+    assert rc == 1
+    assert lib.kdb_status_string(2) == b"KDB_ENOMEM"
+
+
+def test_sim_comm_lifecycle(lib):
+    h = C.c_void_p()
+    assert lib.kdb_comm_create_sim(C.byref(h), 4) == 0 and h.value
+    g = _graph(n_total=10, row_begin=2, n_rows=8)
+    # sim needs the full graph
+    assert lib.kdb_core_mark(C.byref(g), 2, 0.5, C.c_void_p(0x3000), h, None) == 1
+    lib.kdb_comm_destroy(h)
+    assert lib.kdb_comm_create_sim(C.byref(h), 0) == 1

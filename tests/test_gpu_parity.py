@@ -1,0 +1,222 @@
+"""GPU <-> oracle parity through the C-ABI (pytest -m gpu).
+
+Bar (north_star): core flags, labels and MSF edge set bit-identical to the
+oracle; MSF total weight within 1e-6 relative (the GPU sums exactly and rounds
+once, the oracle sums in key order, so they agree far below that).
+"""
+from __future__ import annotations
+
+import json
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from datagen import eps_from_graph, gen_c1, knn_bruteforce, random_graph
+from tests.kdb_harness import assert_parity, oracle_run, run_gpu
+
+pytestmark = pytest.mark.gpu
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required for -m gpu tests")
+    import paper_2009_04552_b200 as kdb
+    kdb.lib()  # fail loudly if the extension is missing
+
+
+def _golden(name):
+    return json.load(open(os.path.join(GOLDEN, name)))
+
+
+def _golden_cases():
+    out = []
+    for f in ["w1_fig_cycle.json", "w2_fig_cut_mst.json", "w3_unit_square.json"]:
+        g = _golden(f)
+        for c in g["cases"]:
+            out.append((g["nbr"], g["dist"], c))
+        if "dup" in g:
+            for c in g["dup"]["cases"]:
+                out.append((g["dup"]["nbr"], g["dup"]["dist"], c))
+    return out
+
+
+@pytest.mark.parametrize("idx", range(7))
+@pytest.mark.parametrize("P", [0, 1, 2, 3, 4])
+def test_golden_examples(idx, P):
+    import paper_2009_04552_b200 as kdb
+    nbr, dist, case = _golden_cases()[idx]
+    nbr = np.array(nbr, np.int32); dist = np.array(dist, np.float32)
+    comm = kdb.Comm.sim(P) if P else None
+    got = run_gpu(nbr, dist, case["M"], case["eps"], exact=False, comm=comm)
+    assert got["core"].tolist() == case["core"]
+    assert sorted(zip(got["msf_a"].tolist(), got["msf_b"].tolist())) == sorted(map(tuple, case["msf"]))
+    assert got["msf_weight"] == case["msf_weight"]
+    assert got["labels"].tolist() == case["labels"]
+    assert_parity(got, oracle_run(nbr, dist, case["M"], case["eps"]))
+
+
+def test_w1_false_exact_promise_is_detected():
+    """Fig. cycle's graph is approximate.  Promising EXACT
+    for it makes the row-only offers of V2 miss its in-edge from V1, i.e. the
+    directed-scan 4-cycle the paper describes; kdb_mst must detect the broken
+    promise (a hook target with a larger key) instead of spinning or returning
+    a wrong forest."""
+    import paper_2009_04552_b200 as kdb
+    g = _golden("w1_fig_cycle.json")
+    with pytest.raises(kdb.KdbError, match="EXACT"):
+        run_gpu(np.array(g["nbr"], np.int32), np.array(g["dist"], np.float32), 1, 0.2, exact=True)
+
+
+def test_w3_exact_mode():
+    g = _golden("w3_unit_square.json")
+    for src in (g, g["dup"]):
+        for c in src["cases"]:
+            nbr = np.array(src["nbr"], np.int32); dist = np.array(src["dist"], np.float32)
+            got = run_gpu(nbr, dist, c["M"], c["eps"], exact=True)
+            assert_parity(got, oracle_run(nbr, dist, c["M"], c["eps"]))
+
+
+RANDOM_CASES = [
+    # n, k, M, seed, levels, symmetric, pad, zero, local, eps quantile
+    (1000, 4, 2, 0, 4, True, 0.0, 0.0, None, 0.6),
+    (2000, 8, 3, 1, 3, False, 0.1, 0.05, 30, 0.5),
+    (3001, 16, 8, 2, None, True, 0.2, 0.0, None, 0.7),
+    (4097, 8, 1, 3, 2, True, 0.0, 0.2, 20, 0.9),
+    (5000, 12, 6, 4, 16, False, 0.3, 0.0, 60, 0.4),
+    (777, 5, 5, 5, 5, True, 0.0, 0.1, 8, 0.95),
+]
+
+
+@pytest.mark.parametrize("case", RANDOM_CASES)
+def test_random_graphs_general(case):
+    n, k, M, seed, levels, sym, pad, zero, local, q = case
+    nbr, dist = random_graph(n, k, seed, levels=levels, symmetric=sym, pad_frac=pad, zero_frac=zero, local=local)
+    fin = dist[np.isfinite(dist)].astype(np.float64)
+    eps = np.float32(np.quantile(fin, q))
+    exp = oracle_run(nbr, dist, M, eps)
+    got = run_gpu(nbr, dist, M, eps, exact=False)
+    assert_parity(got, exp)
+
+
+@pytest.mark.parametrize("P", [2, 3, 4, 8])
+def test_sim_ranks_identical(P):
+    import paper_2009_04552_b200 as kdb
+    nbr, dist = random_graph(3000, 8, 7, levels=4, symmetric=False, pad_frac=0.1, local=40)
+    eps = np.float32(np.quantile(dist[np.isfinite(dist)].astype(np.float64), 0.6))
+    exp = oracle_run(nbr, dist, 3, eps)
+    got1 = run_gpu(nbr, dist, 3, eps)
+    gotP = run_gpu(nbr, dist, 3, eps, comm=kdb.Comm.sim(P))
+    assert_parity(got1, exp)
+    assert_parity(gotP, exp)
+    for key in ("core", "comp", "labels", "msf_a", "msf_b", "msf_w"):
+        assert np.array_equal(got1[key], gotP[key])
+    assert got1["msf_weight"] == gotP["msf_weight"]
+
+
+@pytest.fixture(scope="module")
+def c1_graph():
+    X, _ = gen_c1(0)
+    nbr, dist = knn_bruteforce(X, 16)
+    return X, nbr, dist
+
+
+@pytest.mark.parametrize("exact", [False, True])
+@pytest.mark.parametrize("P", [0, 4])
+def test_config_c1_full(c1_graph, exact, P):
+    """BASELINE.json configs[0] at full size: exact kNN graph k=16, M=8,
+    eps = 1.5 x median 8th-NN distance."""
+    import paper_2009_04552_b200 as kdb
+    X, nbr, dist = c1_graph
+    eps = eps_from_graph(dist, 8, 1.5)
+    exp = oracle_run(nbr, dist, 8, eps)
+    got = run_gpu(nbr, dist, 8, eps, exact=exact, comm=kdb.Comm.sim(P) if P else None)
+    assert_parity(got, exp)
+    assert got["stats"]["rounds"] >= 1
+
+
+@pytest.mark.parametrize("factor", [0.3, 0.8, 1.0, 2.5, 10.0])
+def test_c1_eps_sweep_exact(c1_graph, factor):
+    """One graph, many eps (Fig. eps_mnist protocol)."""
+    X, nbr, dist = c1_graph
+    eps = eps_from_graph(dist, 8, factor)
+    exp = oracle_run(nbr, dist, 8, eps)
+    assert_parity(run_gpu(nbr, dist, 8, eps, exact=True), exp)
+
+
+def test_points_exact_graphs_small_k():
+    rng = np.random.default_rng(3)
+    for t in range(4):
+        n = int(rng.integers(50, 2500))
+        X = (rng.standard_normal((n, 3)) * rng.uniform(0.1, 1.0)).astype(np.float32)
+        X[rng.integers(0, n, n // 20)] = X[rng.integers(0, n, n // 20)]  # duplicates -> w = 0
+        k = int(rng.integers(2, 20)); M = int(rng.integers(1, k + 1))
+        nbr, dist = knn_bruteforce(X, k)
+        eps = eps_from_graph(dist, M, float(rng.uniform(0.8, 3.0)))
+        exp = oracle_run(nbr, dist, M, eps)
+        assert_parity(run_gpu(nbr, dist, M, eps, exact=True), exp)
+        assert_parity(run_gpu(nbr, dist, M, eps, exact=False), exp)
+
+
+def test_k_full_graph():
+    """k = N-1 (the complete graph, Thm. 2(i))."""
+    rng = np.random.default_rng(11)
+    X = rng.uniform(size=(300, 2)).astype(np.float32)
+    nbr, dist = knn_bruteforce(X, 299)
+    eps = eps_from_graph(dist, 5, 1.0)
+    exp = oracle_run(nbr, dist, 5, eps)
+    assert_parity(run_gpu(nbr, dist, 5, eps, exact=True), exp)
+    assert_parity(run_gpu(nbr, dist, 5, eps, exact=False), exp)
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 33])
+def test_degenerate_sizes(n):
+    k = max(1, n - 1)
+    if n == 1:
+        nbr = np.full((1, 1), -1, np.int32); dist = np.full((1, 1), np.inf, np.float32)
+    else:
+        X = np.random.default_rng(n).uniform(size=(n, 2)).astype(np.float32)
+        nbr, dist = knn_bruteforce(X, k)
+    for eps in (1e-6, 0.3, 10.0):
+        exp = oracle_run(nbr, dist, 1, eps)
+        assert_parity(run_gpu(nbr, dist, 1, eps, exact=True), exp)
+        assert_parity(run_gpu(nbr, dist, 1, eps), exp)
+
+
+def test_all_noise_and_all_core():
+    nbr, dist = random_graph(500, 6, 1, levels=8)
+    exp = oracle_run(nbr, dist, 6, 1e-4)
+    got = run_gpu(nbr, dist, 6, 1e-4)
+    assert_parity(got, exp)
+    assert np.all(got["labels"] == -1) and len(got["msf_a"]) == 0
+    exp = oracle_run(nbr, dist, 1, 5.0)
+    assert_parity(run_gpu(nbr, dist, 1, 5.0), exp)
+
+
+def test_determinism_repeat():
+    nbr, dist = random_graph(4000, 8, 9, levels=3, symmetric=True, local=25)
+    eps = np.float32(0.7)
+    a = run_gpu(nbr, dist, 2, eps)
+    for _ in range(3):
+        b = run_gpu(nbr, dist, 2, eps)
+        for key in ("core", "comp", "labels", "msf_a", "msf_b", "msf_w"):
+            assert np.array_equal(a[key], b[key])
+        assert a["msf_weight"] == b["msf_weight"]
+
+
+def test_invalid_arguments_raise():
+    import paper_2009_04552_b200 as kdb
+    nbr, dist = random_graph(64, 4, 0)
+    g = kdb.Graph(torch.from_numpy(nbr).cuda(), torch.from_numpy(dist).cuda(), n_total=64)
+    with pytest.raises(kdb.KdbError):
+        kdb.core_mark(g, 5, 0.5)          # M > k
+    with pytest.raises(kdb.KdbError):
+        kdb.core_mark(g, 2, 0.0)          # eps not in (0, inf)
+    with pytest.raises(kdb.KdbError):
+        kdb.core_mark(g, 2, float("inf"))
+    bad = kdb.Graph(torch.from_numpy(nbr).cuda(), torch.from_numpy(dist).cuda(), n_total=10)
+    with pytest.raises(kdb.KdbError):
+        kdb.core_mark(bad, 2, 0.5)        # rows outside [0, N)
