@@ -343,7 +343,7 @@ def dominant_algo_bytes(name, N, k, world, launches_per_step, stats):
         return 4.0 * n_local + n_local / 8.0          # one fp32 per row + the bit words
     if name == "k_label":
         return 4.0 * n_local + 4.0 * n_local           # D[i][0..] of border rows ~ 1 fp32 + label
-    if name in ("k_offer_rows", "k_sweep", "k_in_count", "k_in_fill"):
+    if name.startswith(("k_offer_rows", "k_offer_warp", "k_offer_first", "k_sweep")):
         er = np.mean([s.get("entries_read", 0) for s in stats]) if stats else 0
         if er and launches_per_step:
             return 8.0 * er / launches_per_step

@@ -141,7 +141,8 @@ kdb_status kdb_label(const kdb_graph* g, float eps, const uint32_t* core_bits, c
 /* Per-phase device times (ms) and counters of the most recent kdb_mst call on
  * this thread: out[0] = rounds, out[1] = init/sweep ms, out[2] = min-edge ms
  * (offer + tie + exchange), out[3] = hook/jump/relabel ms, out[4] = finalize ms,
- * out[5] = in-edge build ms, out[6] = stall (sweep) rounds. Returns entries written. */
+ * out[5] = in-edge build ms, out[6] = stall (sweep) rounds, out[7] = graph entries
+ * read by the per-vertex offer kernel (all rounds).  Returns entries written. */
 int kdb_last_mst_stats(double* out, int cap);
 
 /* Measurement hooks (bench.py).  kdb_launch_count(): kernels this library has

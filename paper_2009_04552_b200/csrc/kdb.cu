@@ -39,8 +39,11 @@
 
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
+#include <cub/device/device_select.cuh>
+#include <thrust/iterator/transform_iterator.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -85,9 +88,13 @@ constexpr uint32_t kInfBits = 0x7f800000u;
 constexpr int kThreads = 256;
 
 inline int grid_for(int64_t n, int per_block = kThreads) {
+  (void)0;
   int64_t g = (n + per_block - 1) / per_block;
   if (g < 1) g = 1;
-  if (g > 148 * 16) g = 148 * 16;  // grid-stride beyond 16 CTAs per SM
+  // grid-stride kernels: at most one resident wave (8 x 256-thread CTAs per SM);
+  // a second wave would only start after the first finished ALL its strides
+  const int cap = getenv("KDB_GRIDCAP") ? atoi(getenv("KDB_GRIDCAP")) : 148 * 8;
+  if (g > cap) g = cap;
   return (int)g;
 }
 
@@ -137,6 +144,8 @@ struct Prof {
   }
 };
 Prof g_prof;
+const uint32_t g_chunk = getenv("KDB_CHUNK") ? (uint32_t)atoi(getenv("KDB_CHUNK")) : (1u << 30);
+const uint32_t g_chunk_w = getenv("KDB_CHUNKW") ? (uint32_t)atoi(getenv("KDB_CHUNKW")) : (1u << 30);
 
 struct LaunchScope {
   const char* name;
@@ -218,23 +227,64 @@ __device__ __forceinline__ uint32_t mono_bits(float w) {
 }
 
 __device__ __forceinline__ bool is_core(const uint32_t* __restrict__ bits, int64_t v) {
-  return (__ldg(bits + (v >> 5)) >> (v & 31)) & 1u;
+  return (__ldcg(bits + (v >> 5)) >> (v & 31)) & 1u;
 }
+
+// Random 4/8-byte gathers go through ld.global.cg (L2 only, 32-B sector
+// requests).  The read-only .nc path (LDG.CONSTANT) promoted each miss to a
+// whole 128-B line: 4x the L2/DRAM traffic for a 4-B gather.
+template <typename T>
+__device__ __forceinline__ T gat(const T* p) { return __ldcg(p); }
 
 __device__ __forceinline__ uint64_t pack_key(uint32_t wbits, uint32_t a) {
   return ((uint64_t)wbits << 32) | a;
 }
 
-// warp-aggregated slot reservation: every lane with `want` gets a unique slot
-__device__ __forceinline__ uint32_t warp_reserve(uint32_t* counter, bool want) {
-  const unsigned active = __activemask();
-  const unsigned m = __ballot_sync(active, want);
-  const int lane = threadIdx.x & 31;
-  uint32_t base = 0;
-  const int leader = __ffs(m) - 1;
-  if (m && lane == leader) base = atomicAdd(counter, (uint32_t)__popc(m));
-  base = __shfl_sync(active, base, leader < 0 ? 0 : leader);
-  return base + __popc(m & ((1u << lane) - 1u));
+struct RoundCounters {
+  uint32_t msf_count;            // edges emitted so far (all rounds)
+  uint32_t pad0;
+  uint32_t hooks;                // this round
+  uint32_t offered;              // components with a finite key
+  uint32_t uncertified;          // offered but abstaining (exact-mode certificate)
+  uint32_t n_roots;              // components after contraction
+  uint32_t n_act[2];             // per-rank scratch (row / in active counts), see host
+  uint32_t n_off;
+  uint32_t violation;            // a hook target's key exceeds the hooker's: the
+                                 // KDB_GRAPH_EXACT promise was false (or a bug)
+  uint32_t n_cont;               // rows continuing in the warp-per-row scan
+  uint32_t pad1;
+  unsigned long long entries;    // graph entries (id + weight) read by offer kernels
+};
+
+// block-aggregated slot reservation: ONE global atomic per block and call.
+// Must be reached by every thread of the block (block-uniform control flow).
+__device__ __forceinline__ uint32_t block_reserve(uint32_t* counter, bool want) {
+  __shared__ uint32_t s_cnt[33];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  const unsigned m = __ballot_sync(0xffffffffu, want);
+  if (lane == 0) s_cnt[warp] = __popc(m);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t tot = 0;
+    for (int w = 0; w < nw; ++w) { const uint32_t c = s_cnt[w]; s_cnt[w] = tot; tot += c; }
+    s_cnt[32] = tot ? atomicAdd(counter, tot) : 0u;
+  }
+  __syncthreads();
+  const uint32_t slot = s_cnt[32] + s_cnt[warp] + __popc(m & ((1u << lane) - 1u));
+  __syncthreads();
+  return slot;
+}
+
+// block-aggregated counter increment (block-uniform call)
+__device__ __forceinline__ void block_count(uint32_t* counter, bool pred) {
+  __shared__ uint32_t s_c;
+  if (threadIdx.x == 0) s_c = 0;
+  __syncthreads();
+  const unsigned m = __ballot_sync(0xffffffffu, pred);
+  if ((threadIdx.x & 31) == 0 && m) atomicAdd(&s_c, (uint32_t)__popc(m));
+  __syncthreads();
+  if (threadIdx.x == 0 && s_c) atomicAdd(counter, s_c);
+  __syncthreads();
 }
 
 // ============================================================================
@@ -247,7 +297,7 @@ __global__ void k_core_mark(const float* __restrict__ dist, int64_t n_rows, int3
     const int64_t i = base + threadIdx.x;
     const bool in = i < n_rows;
     bool core = false;
-    if (in) core = __ldg(dist + i * k + (M - 1)) <= eps;
+    if (in) core = __ldcs(dist + i * k + (M - 1)) <= eps;
     const int64_t v = row_begin + i;
     const unsigned inmask = __ballot_sync(0xffffffffu, in);
     if (in) {
@@ -293,30 +343,43 @@ __global__ void k_fill_comp_arrays(int64_t C, uint64_t* __restrict__ Kc, uint32_
   }
 }
 
-// local rows: head = 0, certificate bound kth'(v) into kmin[comp v], active list
+// ---------------------------------------------------------------------------
+// Active-row records.  The scan position L[i] travels with the
+// row id through the active lists, so a row's state arrives in one coalesced
+// 8-byte load instead of a chain of dependent gathers.
+struct Act {
+  int32_t v;  // global row id
+  int32_t h;  // head: every entry before it is dead for good
+};
+// continuation record: everything k_offer_warp needs, written by k_offer_rows_t
+struct Cont {
+  int32_t v, h, cv, s;  // row, head, its component, slot in the active list
+};
+
+// local rows: certificate bound kth'(v) into kmin[comp v], active list (v, head 0)
 __global__ void k_init_rows(const float* __restrict__ dist, int64_t n_rows, int32_t k, float eps,
                             int64_t row_begin, const uint32_t* __restrict__ bits,
-                            const int32_t* __restrict__ comp, uint16_t* __restrict__ head,
-                            uint32_t* __restrict__ kmin, int32_t* __restrict__ active,
-                            uint32_t* __restrict__ n_active) {
+                            const int32_t* __restrict__ comp, uint32_t* __restrict__ kmin,
+                            Act* __restrict__ active, uint8_t* __restrict__ flag) {
   for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n_rows;
        base += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = base + threadIdx.x;
     bool want = false;
     int64_t v = row_begin + i;
     if (i < n_rows) {
-      head[i] = 0;
       if (is_core(bits, v)) {
         // a row whose first entry is already beyond eps offers nothing, ever
-        want = __ldg(dist + i * k) <= eps;
+        want = __ldcs(dist + i * k) <= eps;
         if (kmin) {
-          const float kth = __ldg(dist + i * k + (k - 1));
+          const float kth = __ldcs(dist + i * k + (k - 1));
           kmin[comp[v]] = (kth <= eps) ? mono_bits(kth) : kInfBits;
         }
       }
     }
-    const uint32_t slot = warp_reserve(n_active, want);
-    if (want) active[slot] = (int32_t)v;
+    if (i < n_rows) {
+      active[i] = Act{(int32_t)v, 0};
+      flag[i] = want ? 1 : 0;
+    }
   }
 }
 
@@ -373,7 +436,7 @@ __global__ void k_in_finish(const unsigned long long* __restrict__ off, int64_t 
       in_len[t] = len;
       want = len > 0;
     }
-    const uint32_t slot = warp_reserve(n_in_active, want);
+    const uint32_t slot = block_reserve(n_in_active, want);
     if (want) in_active[slot] = (int32_t)t;
   }
 }
@@ -387,59 +450,267 @@ __global__ void k_in_finish(const unsigned long long* __restrict__ off, int64_t 
 // component opens the minimum group; equal-weight entries after it may carry a
 // smaller far id and are scanned too.  The head pointer only passes entries
 // that can never become leaving again (non-candidates, intra-component).
-__global__ void k_offer_rows(const int32_t* __restrict__ nbr, const float* __restrict__ dist,
-                             int32_t k, float eps, int64_t row_begin, int64_t N,
-                             const uint32_t* __restrict__ bits, const int32_t* __restrict__ comp,
-                             const int32_t* __restrict__ act_in, uint32_t n_in,
-                             uint16_t* __restrict__ head, int32_t* __restrict__ act_out,
-                             uint32_t* __restrict__ n_out, int32_t* __restrict__ off_v,
-                             uint64_t* __restrict__ off_key, uint32_t* __restrict__ off_b,
-                             uint32_t* __restrict__ n_off, unsigned long long* __restrict__ Kc) {
-  for (uint32_t base = blockIdx.x * blockDim.x; base < n_in; base += gridDim.x * blockDim.x) {
-    const uint32_t s = base + threadIdx.x;
+//
+__device__ __forceinline__ bool cand_entry(int64_t J, int64_t v, int64_t N, const uint32_t* bits, bool all_core) {
+  return J >= 0 && J < N && J != v && (all_core || is_core(bits, J));
+}
+
+// One thread per active row; each step takes an aligned 4-entry chunk (int4
+// ids + float4 weights when k % 4 == 0, loaded evict-first so the streamed
+// graph does not push comp[] out of L2) and issues its 4 component gathers
+// together.  A thread gives up after kQmax chunks of dead entries (the chunk
+// count per row varies 1..k/4 inside a warp); the row then continues in
+// k_offer_warp, 32 entries per step.
+constexpr int kQmax = 2;
+
+template <bool VEC>
+__device__ __forceinline__ void load_chunk(const int32_t* nr, const float* dr, int c0, int k, int32_t (&J)[4],
+                                           float (&w)[4]) {
+  if (VEC && c0 + 3 < k) {
+    const int4 j4 = __ldcs(reinterpret_cast<const int4*>(nr + c0));
+    const float4 w4 = __ldcs(reinterpret_cast<const float4*>(dr + c0));
+    J[0] = j4.x; J[1] = j4.y; J[2] = j4.z; J[3] = j4.w;
+    w[0] = w4.x; w[1] = w4.y; w[2] = w4.z; w[3] = w4.w;
+  } else {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const bool in = c0 + j < k;
+      J[j] = in ? __ldcs(nr + c0 + j) : -1;
+      w[j] = in ? __ldcs(dr + c0 + j) : __int_as_float(0x7f800000);
+    }
+  }
+}
+
+template <bool VEC>
+__global__ void __launch_bounds__(256) k_offer_rows_t(
+    const int32_t* __restrict__ nbr, const float* __restrict__ dist, int32_t k, float eps, int64_t row_begin,
+    int64_t N, const uint32_t* __restrict__ bits, int all_core, const int32_t* __restrict__ comp,
+    Act* __restrict__ act, uint32_t s_begin, uint32_t s_end, uint8_t* __restrict__ status,
+    uint64_t* __restrict__ off_key, uint32_t* __restrict__ off_b, Cont* __restrict__ cand,
+    unsigned long long* __restrict__ Kc, unsigned long long* __restrict__ n_entries) {
+  unsigned long long reads = 0;
+  for (uint32_t s = s_begin + blockIdx.x * blockDim.x + threadIdx.x; s < s_end; s += gridDim.x * blockDim.x) {
+    bool found = false, more = false;
+    uint64_t best = kSent;
+    uint32_t bestb = kSentB;
+    const int2 a = __ldcs(reinterpret_cast<const int2*>(act + s));
+    const int32_t v = a.x;
+    int h = a.y;
+    const int64_t i = (int64_t)v - row_begin;
+    const int32_t* nr = nbr + i * k;
+    const float* dr = dist + i * k;
+    const int32_t cv = gat(comp + v);
+    int c0 = h & ~3;
+    float wstar = 0.f;
+    bool done = false;
+    int steps = 0;
+    while (!done && c0 < k) {
+      if (!found && steps == kQmax) {  // hand the rest of the dead run to a warp
+        more = true;
+        break;
+      }
+      ++steps;
+      int32_t J[4];
+      float w[4];
+      load_chunk<VEC>(nr, dr, c0, k, J, w);
+      int32_t cj[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const bool ok = c0 + j >= h && w[j] <= eps && cand_entry(J[j], v, N, bits, all_core);
+        cj[j] = ok ? gat(comp + J[j]) : -2;  // -2: not a candidate (dead for good)
+      }
+      reads += (unsigned long long)(min(c0 + 4, k) - max(c0, h));
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int idx = c0 + j;
+        if (done || idx < h || idx >= k) continue;
+        if (!found) {
+          if (!(w[j] <= eps)) { h = k; done = true; continue; }  // sorted: nothing left
+          if (cj[j] == -2 || cj[j] == cv) { h = idx + 1; continue; }  // dead entry
+          found = true;  // first leaving entry opens the minimum group
+          h = idx;
+          wstar = w[j];
+          best = pack_key(mono_bits(w[j]), (uint32_t)min((int64_t)v, (int64_t)J[j]));
+          bestb = (uint32_t)max((int64_t)v, (int64_t)J[j]);
+        } else {
+          if (w[j] != wstar) { done = true; continue; }
+          if (cj[j] == -2 || cj[j] == cv) continue;
+          const uint64_t kk = pack_key(mono_bits(w[j]), (uint32_t)min((int64_t)v, (int64_t)J[j]));
+          const uint32_t bb = (uint32_t)max((int64_t)v, (int64_t)J[j]);
+          if (kk < best || (kk == best && bb < bestb)) { best = kk; bestb = bb; }
+        }
+      }
+      c0 += 4;
+    }
+    h = min(h, k);
+    act[s].h = h;
+    __stcs(status + s, (uint8_t)(found ? 1 : (more ? 2 : 0)));  // 1 offer, 2 continue, 0 exhausted
+    if (found) {
+      __stcs(reinterpret_cast<unsigned long long*>(off_key) + s, (unsigned long long)best);
+      __stcs(off_b + s, bestb);
+      atomicMin(Kc + cv, (unsigned long long)best);
+    } else if (more) {
+      __stcs(reinterpret_cast<int4*>(cand + s), make_int4(v, h, cv, (int)s));
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) reads += __shfl_xor_sync(0xffffffffu, reads, o);
+  if ((threadIdx.x & 31) == 0 && reads) atomicAdd(n_entries, reads);
+}
+
+// Continuation: one warp per row, 32 consecutive entries per step (one 128-B
+// line of ids and one of weights, 32 component gathers in flight); a ballot
+// finds the first leaving entry, a warp reduction the minimum of its
+// equal-weight group.  The record of the warp's next row is prefetched.
+__global__ void __launch_bounds__(256) k_offer_warp(
+    const int32_t* __restrict__ nbr, const float* __restrict__ dist, int32_t k, float eps, int64_t row_begin,
+    int64_t N, const uint32_t* __restrict__ bits, int all_core, const int32_t* __restrict__ comp,
+    const Cont* __restrict__ cont, const uint32_t* __restrict__ n_cont_p, uint32_t q_begin, uint32_t q_end,
+    Act* __restrict__ act, uint8_t* __restrict__ status, uint64_t* __restrict__ off_key,
+    uint32_t* __restrict__ off_b, unsigned long long* __restrict__ Kc, unsigned long long* __restrict__ n_entries) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t n_cont = min(*n_cont_p, q_end);
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  unsigned long long reads = 0;
+  uint32_t q = q_begin + ((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  int4 rec = make_int4(0, 0, 0, 0);
+  if (q < n_cont) rec = __ldcs(reinterpret_cast<const int4*>(cont + q));
+  for (; q < n_cont; q += nwarps) {
+    const int32_t v = rec.x, cv = rec.z, s = rec.w;
+    int h = rec.y;
+    if (q + nwarps < n_cont) rec = __ldcs(reinterpret_cast<const int4*>(cont + q + nwarps));
+    const int64_t i = (int64_t)v - row_begin;
+    const int32_t* nr = nbr + i * k;
+    const float* dr = dist + i * k;
     bool found = false;
     uint64_t best = kSent;
     uint32_t bestb = kSentB;
-    int32_t v = -1, cv = -1;
-    if (s < n_in) {
-      v = act_in[s];
-      const int64_t i = (int64_t)v - row_begin;
-      const int32_t* nr = nbr + i * k;
-      const float* dr = dist + i * k;
-      cv = comp[v];
-      int h = head[i];
-      while (h < k) {
-        const float w = __ldg(dr + h);
-        if (!(w <= eps)) { h = k; break; }
-        const int64_t J = __ldg(nr + h);
-        if (J < 0 || J >= N || J == v || !is_core(bits, J) || comp[J] == cv) { ++h; continue; }
-        const uint32_t wb = mono_bits(w);
-        best = pack_key(wb, (uint32_t)min((int64_t)v, J));
-        bestb = (uint32_t)max((int64_t)v, J);
-        for (int h2 = h + 1; h2 < k; ++h2) {
-          const float w2 = __ldg(dr + h2);
-          if (w2 != w) break;
-          const int64_t J2 = __ldg(nr + h2);
-          if (J2 < 0 || J2 >= N || J2 == v || !is_core(bits, J2) || comp[J2] == cv) continue;
-          const uint64_t k2 = pack_key(wb, (uint32_t)min((int64_t)v, J2));
-          const uint32_t b2 = (uint32_t)max((int64_t)v, J2);
-          if (k2 < best || (k2 == best && b2 < bestb)) { best = k2; bestb = b2; }
-        }
-        found = true;
-        break;
+    float wstar = 0.f;
+    for (int c0 = h & ~31; c0 < k; c0 += 32) {
+      const int idx = c0 + lane;
+      const bool in = idx >= h && idx < k;
+      float w = __int_as_float(0x7f800000);
+      int32_t J = -1;
+      if (in) {
+        w = __ldcs(dr + idx);
+        J = __ldcs(nr + idx);
       }
-      head[i] = (uint16_t)h;
+      if (lane == 0) reads += (unsigned long long)(min(c0 + 32, k) - max(c0, h));
+      const bool beyond = in && !(w <= eps);
+      bool leaving = false;
+      if (in && !beyond && cand_entry(J, v, N, bits, all_core)) leaving = gat(comp + J) != cv;
+      const unsigned mb = __ballot_sync(0xffffffffu, beyond);
+      const unsigned ml = __ballot_sync(0xffffffffu, leaving);
+      const int fb = mb ? __ffs(mb) - 1 : 32;
+      if (!found) {
+        const int fl = ml ? __ffs(ml) - 1 : 32;
+        if (fl < fb) {
+          found = true;
+          h = c0 + fl;
+          wstar = __shfl_sync(0xffffffffu, w, fl);
+        } else if (fb < 32) {
+          h = k;
+          break;
+        } else {
+          h = c0 + 32;
+          continue;
+        }
+      }
+      uint64_t kk = kSent;
+      uint32_t bb = kSentB;
+      if (leaving && w == wstar) {
+        kk = pack_key(mono_bits(w), (uint32_t)min((int64_t)v, (int64_t)J));
+        bb = (uint32_t)max((int64_t)v, (int64_t)J);
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        const uint64_t k2 = __shfl_xor_sync(0xffffffffu, kk, o);
+        const uint32_t b2 = __shfl_xor_sync(0xffffffffu, bb, o);
+        if (k2 < kk || (k2 == kk && b2 < bb)) { kk = k2; bb = b2; }
+      }
+      if (kk < best || (kk == best && bb < bestb)) { best = kk; bestb = bb; }
+      if (!__shfl_sync(0xffffffffu, in && w == wstar, 31)) break;  // group ends in this line
     }
-    const uint32_t a = warp_reserve(n_out, found);
-    if (found) act_out[a] = v;
-    const uint32_t o = warp_reserve(n_off, found);
-    if (found) {
-      off_v[o] = v;
-      off_key[o] = best;
-      off_b[o] = bestb;
-      atomicMin(Kc + cv, (unsigned long long)best);
+    if (lane == 0) {
+      act[s].h = min(h, k);
+      status[s] = found ? 1 : 0;
+      if (found) {
+        off_key[s] = best;
+        off_b[s] = bestb;
+        atomicMin(Kc + cv, (unsigned long long)best);
+      }
     }
   }
+  for (int o = 16; o > 0; o >>= 1) reads += __shfl_xor_sync(0xffffffffu, reads, o);
+  if (lane == 0 && reads) atomicAdd(n_entries, reads);
+}
+
+struct IsTwo {
+  __host__ __device__ bool operator()(const uint8_t& x) const { return x == 2; }
+};
+
+// tie pass over per-slot row offers (status 1)
+__global__ void k_tie_slots(const Act* __restrict__ act, const uint8_t* __restrict__ status,
+                            const uint64_t* __restrict__ off_key, const uint32_t* __restrict__ off_b, uint32_t n,
+                            const int32_t* __restrict__ comp, const uint64_t* __restrict__ Kc,
+                            uint32_t* __restrict__ Bc) {
+  for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < n; s += gridDim.x * blockDim.x) {
+    if (status[s] != 1) continue;
+    const int32_t c = gat(comp + act[s].v);
+    if (off_key[s] == gat(Kc + c)) atomicMin(Bc + c, off_b[s]);
+  }
+}
+
+// Round 1 with singleton components (exact mode): comp(J) != comp(v) for every
+// candidate J, so the first candidate group of the row IS the minimum; no
+// component gathers, no atomics, no tie pass -- the owner writes Kc/Bc and the
+// hook target directly.
+__global__ void k_offer_first(const int32_t* __restrict__ nbr, const float* __restrict__ dist, int32_t k,
+                              float eps, int64_t row_begin, int64_t N, const uint32_t* __restrict__ bits,
+                              int all_core, const int32_t* __restrict__ comp, Act* __restrict__ act, uint32_t n_in,
+                              uint8_t* __restrict__ status, uint64_t* __restrict__ Kc, uint32_t* __restrict__ Bc,
+                              int32_t* __restrict__ tgt, unsigned long long* __restrict__ n_entries) {
+  unsigned long long reads = 0;
+  for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < n_in; s += gridDim.x * blockDim.x) {
+    bool found = false;
+    const int32_t v = act[s].v;
+    const int64_t i = (int64_t)v - row_begin;
+    const int32_t* nr = nbr + i * k;
+    const float* dr = dist + i * k;
+    uint64_t best = kSent;
+    uint32_t bestb = kSentB;
+    int64_t bestJ = -1;
+    int h = 0;
+    float wstar = 0.f;
+    for (; h < k; ++h) {
+      const float w = __ldcs(dr + h);
+      ++reads;
+      if (!(w <= eps)) { h = k; break; }
+      const int64_t J = __ldcs(nr + h);
+      if (!cand_entry(J, v, N, bits, all_core)) continue;
+      wstar = w;
+      found = true;
+      break;
+    }
+    if (found) {
+      for (int h2 = h; h2 < k; ++h2) {
+        const float w = h2 == h ? wstar : __ldg(dr + h2);
+        if (h2 != h) ++reads;
+        if (w != wstar) break;
+        const int64_t J = __ldg(nr + h2);
+        if (!cand_entry(J, v, N, bits, all_core)) continue;
+        const uint64_t kk = pack_key(mono_bits(w), (uint32_t)min((int64_t)v, J));
+        const uint32_t bb = (uint32_t)max((int64_t)v, J);
+        if (kk < best || (kk == best && bb < bestb)) { best = kk; bestb = bb; bestJ = J; }
+      }
+      const int32_t cv = gat(comp + v);
+      Kc[cv] = best;
+      Bc[cv] = bestb;
+      tgt[cv] = gat(comp + bestJ);
+    }
+    act[s].h = min(h, k);
+    status[s] = found ? 1 : 0;
+  }
+  for (int o = 16; o > 0; o >>= 1) reads += __shfl_xor_sync(0xffffffffu, reads, o);
+  if ((threadIdx.x & 31) == 0 && reads) atomicAdd(n_entries, reads);
 }
 
 // in-edge lists: scan the live in-entries of target t, drop intra entries
@@ -480,9 +751,9 @@ __global__ void k_offer_in(const unsigned long long* __restrict__ in_off, int32_
       in_len[t] = len;
       keep = len > 0;
     }
-    const uint32_t a = warp_reserve(n_out, keep);
+    const uint32_t a = block_reserve(n_out, keep);
     if (keep) act_out[a] = t;
-    const uint32_t o2 = warp_reserve(n_off, found);
+    const uint32_t o2 = block_reserve(n_off, found);
     if (found) {
       off_v[o2] = t;
       off_key[o2] = best;
@@ -505,18 +776,17 @@ __global__ void k_tie(const int32_t* __restrict__ off_v, const uint64_t* __restr
   }
 }
 
-// stall fallback (exact mode): offer EVERY live leaving entry to both sides
-__global__ void k_sweep(const int32_t* __restrict__ nbr, const float* __restrict__ dist,
-                        int64_t n_rows, int32_t k, float eps, int64_t row_begin, int64_t N,
-                        const uint32_t* __restrict__ bits, const int32_t* __restrict__ comp,
-                        const uint16_t* __restrict__ head, unsigned long long* __restrict__ Kc,
-                        uint32_t* __restrict__ Bc, int tie_phase) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_rows;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t v = row_begin + i;
-    if (!is_core(bits, v)) continue;
+// stall fallback (exact mode): offer EVERY live leaving entry of the active
+// rows to both endpoint components (rows outside the active list have none)
+__global__ void k_sweep(const int32_t* __restrict__ nbr, const float* __restrict__ dist, int32_t k, float eps,
+                        int64_t row_begin, int64_t N, const uint32_t* __restrict__ bits,
+                        const int32_t* __restrict__ comp, const Act* __restrict__ act, uint32_t n_act,
+                        unsigned long long* __restrict__ Kc, uint32_t* __restrict__ Bc, int tie_phase) {
+  for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < n_act; s += gridDim.x * blockDim.x) {
+    const int64_t v = act[s].v;
+    const int64_t i = v - row_begin;
     const int32_t cv = comp[v];
-    for (int32_t c = head[i]; c < k; ++c) {
+    for (int32_t c = act[s].h; c < k; ++c) {
       const float w = __ldg(dist + i * k + c);
       if (!(w <= eps)) break;
       const int64_t J = __ldg(nbr + i * k + c);
@@ -552,24 +822,17 @@ __global__ void k_min_into_u32(uint32_t* __restrict__ d, const uint32_t* __restr
 // ============================================================================
 // a5: hook (break symmetry) + MSF emission
 // ============================================================================
-struct RoundCounters {
-  unsigned long long msf_count;  // edges emitted so far (all rounds)
-  uint32_t hooks;                // this round
-  uint32_t offered;              // components with a finite key
-  uint32_t uncertified;          // offered but abstaining (exact-mode certificate)
-  uint32_t n_roots;              // components after contraction
-  uint32_t n_act[2];             // per-rank scratch (row / in active counts), see host
-  uint32_t n_off;
-  uint32_t violation;            // a hook target's key exceeds the hooker's: the
-                                 // KDB_GRAPH_EXACT promise was false (or a bug)
-};
+
 
 __device__ __forceinline__ bool certified(uint64_t K, const uint32_t* kmin, int64_t c) {
-  return kmin == nullptr || (uint32_t)(K >> 32) < kmin[c];
+  return kmin == nullptr || (uint32_t)(K >> 32) < gat(kmin + c);
 }
 
+// tgt != null: the hook target of every offering component is known (round 1,
+// written by its single offer), so t = tgt[c] and "mutual" is tgt[t] == c.
+// Otherwise t is found from the selected edge's endpoints.
 __global__ void k_hook(int64_t C, const uint64_t* __restrict__ Kc, const uint32_t* __restrict__ Bc,
-                       const uint32_t* __restrict__ kmin /* null = all certified */,
+                       const int32_t* __restrict__ tgt, const uint32_t* __restrict__ kmin /* null = all certified */,
                        const int32_t* __restrict__ comp, int32_t* __restrict__ parent,
                        uint64_t* __restrict__ e_key, float* __restrict__ e_w, int64_t e_cap,
                        RoundCounters* __restrict__ ctr) {
@@ -589,16 +852,28 @@ __global__ void k_hook(int64_t C, const uint64_t* __restrict__ Kc, const uint32_
           a = (uint32_t)K;
           b = Bc[c];
           wb = (uint32_t)(K >> 32);
-          const int32_t x = (comp[a] == (int32_t)c) ? (int32_t)b : (int32_t)a;
-          const int32_t t = comp[x];
-          const uint64_t Kt = Kc[t];
-          const bool cert_t = Kt != kSent && certified(Kt, kmin, t);
-          const bool mutual = cert_t && Kt == K && Bc[t] == b;
-          // t's true minimum is <= the edge c selected (that edge is incident to
-          // t); a larger key means t's offer missed an incident edge.  Under a
-          // true EXACT promise this cannot happen; it is the only way a hook
-          // cycle longer than a mutual pair could form (Fig. cycle).
-          if (cert_t && (Kt > K || (Kt == K && Bc[t] > b))) ctr->violation = 1u;
+          int32_t t;
+          if (tgt) {
+            t = tgt[c];
+          } else {
+            const int32_t x = (gat(comp + a) == (int32_t)c) ? (int32_t)b : (int32_t)a;
+            t = gat(comp + x);
+          }
+          bool mutual, cert_t = true;
+          if (kmin) {  // exact mode: t may abstain; also audit the promise
+            const uint64_t Kt = gat(Kc + t);
+            cert_t = Kt != kSent && certified(Kt, kmin, t);
+            // t's true minimum is <= the edge c selected (that edge is incident
+            // to t); a larger key means t's offer missed an incident edge --
+            // impossible under a true EXACT promise, and the only way a hook
+            // cycle longer than a mutual pair could form (Fig. cycle).
+            if (cert_t && (Kt > K || (Kt == K && gat(Bc + t) > b))) ctr->violation = 1u;
+            mutual = cert_t && Kt == K && gat(Bc + t) == b;
+          } else if (tgt) {
+            mutual = gat(tgt + t) == (int32_t)c;
+          } else {
+            mutual = gat(Kc + t) == K && gat(Bc + t) == b;
+          }
           if (!(mutual && c < t)) {
             p = t;
             emit = true;
@@ -607,21 +882,11 @@ __global__ void k_hook(int64_t C, const uint64_t* __restrict__ Kc, const uint32_
       }
       parent[c] = p;
     }
-    const unsigned m_off = __ballot_sync(0xffffffffu, offered);
-    const unsigned m_unc = __ballot_sync(0xffffffffu, unc);
-    if ((threadIdx.x & 31) == 0) {
-      if (m_off) atomicAdd(&ctr->offered, __popc(m_off));
-      if (m_unc) atomicAdd(&ctr->uncertified, __popc(m_unc));
-    }
-    const unsigned m_emit = __ballot_sync(0xffffffffu, emit);
-    unsigned long long base_slot = 0;
-    if ((threadIdx.x & 31) == 0 && m_emit) {
-      base_slot = atomicAdd(&ctr->msf_count, (unsigned long long)__popc(m_emit));
-      atomicAdd(&ctr->hooks, __popc(m_emit));
-    }
-    base_slot = __shfl_sync(0xffffffffu, base_slot, 0);
+    block_count(&ctr->offered, offered);
+    block_count(&ctr->uncertified, unc);
+    block_count(&ctr->hooks, emit);
+    const uint32_t slot = block_reserve(&ctr->msf_count, emit);
     if (emit) {
-      const unsigned long long slot = base_slot + __popc(m_emit & ((1u << (threadIdx.x & 31)) - 1u));
       if ((int64_t)slot < e_cap) {
         e_key[slot] = ((uint64_t)a << 32) | b;
         e_w[slot] = __uint_as_float(wb);
@@ -669,10 +934,11 @@ __global__ void k_root_flags(int64_t C, const int32_t* __restrict__ rootof, int3
 // new per-component arrays: cmin/kmin are minima over the merged tree
 __global__ void k_merge(int64_t C, const int32_t* __restrict__ rootof, const int32_t* __restrict__ newid,
                         const int32_t* __restrict__ cmin, const uint32_t* __restrict__ kmin,
-                        int32_t* __restrict__ cmin2, uint32_t* __restrict__ kmin2) {
+                        int32_t* __restrict__ cmin2, uint32_t* __restrict__ kmin2, int32_t* __restrict__ map) {
   for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < C;
        c += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t r = newid[rootof[c]];
+    const int32_t r = gat(newid + rootof[c]);
+    map[c] = r;
     atomicMin(cmin2 + r, cmin[c]);
     if (kmin) atomicMin(kmin2 + r, kmin[c]);
   }
@@ -684,12 +950,11 @@ __global__ void k_fill_i32(int32_t* __restrict__ p, int64_t n, int32_t val) {
     p[c] = val;
 }
 
-__global__ void k_relabel(int64_t N, int32_t* __restrict__ comp, const int32_t* __restrict__ rootof,
-                          const int32_t* __restrict__ newid) {
+__global__ void k_relabel(int64_t N, int32_t* __restrict__ comp, const int32_t* __restrict__ map) {
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < N;
        v += (int64_t)gridDim.x * blockDim.x) {
     const int32_t c = comp[v];
-    if (c >= 0) comp[v] = newid[rootof[c]];
+    if (c >= 0) comp[v] = gat(map + c);
   }
 }
 
@@ -700,7 +965,7 @@ __global__ void k_canon(int64_t N, int32_t* __restrict__ comp, const int32_t* __
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < N;
        v += (int64_t)gridDim.x * blockDim.x) {
     const int32_t c = comp[v];
-    if (c >= 0) comp[v] = cmin[c];
+    if (c >= 0) comp[v] = gat(cmin + c);
   }
 }
 
@@ -725,7 +990,10 @@ __global__ void k_wbuckets(int64_t m, const float* __restrict__ w, unsigned long
     const uint32_t ex = u >> 23;
     uint32_t man = u & 0x7fffffu;
     if (ex) man |= 0x800000u;
-    if (man) atomicAdd(sb + ex, (unsigned long long)man);
+    // lanes sharing an exponent pre-sum (32 x 2^24 < 2^32) -> one smem atomic each
+    const unsigned grp = __match_any_sync(__activemask(), ex);
+    const uint32_t sum = __reduce_add_sync(grp, man);
+    if ((threadIdx.x & 31) == __ffs(grp) - 1 && sum) atomicAdd(sb + ex, (unsigned long long)sum);
   }
   __syncthreads();
   for (int t = threadIdx.x; t < 256; t += blockDim.x)
@@ -808,17 +1076,22 @@ struct RankState {
   int64_t row_begin = 0, n_rows = 0;
   const int32_t* nbr = nullptr;
   const float* dist = nullptr;
-  uint16_t* head = nullptr;
-  int32_t* act[2] = {nullptr, nullptr};
+  Act* act[2] = {nullptr, nullptr};  // active rows (v, head), ping-pong
+  Cont* cand = nullptr;               // per-slot continuation records
+  Cont* cont = nullptr;               // compacted continuation list
+  uint8_t* status = nullptr;          // per slot: 0 exhausted, 1 offer, 2 continue
   uint32_t n_act = 0;
+  uint32_t n_slots = 0;  // offer slots written by this round's row kernels
   // offers
   int32_t* off_v = nullptr;
   uint64_t* off_key = nullptr;
   uint32_t* off_b = nullptr;
   uint32_t n_off = 0;
+  int64_t off_cap_rows = 0;  // offers [0, n_rows) from rows, [n_rows, n_rows + N) from in-lists
   // per-rank partial Kc/Bc (sim ranks > 0) -- else alias the shared ones
   uint64_t* Kc = nullptr;
   uint32_t* Bc = nullptr;
+  int32_t* tgt = nullptr;
   // in-edge lists (general mode)
   unsigned long long* in_off = nullptr;
   int32_t* in_len = nullptr;
@@ -836,6 +1109,8 @@ struct Layout {
   uint32_t *kmin, *kmin2;
   uint64_t* Kc;
   uint32_t* Bc;
+  int32_t* tgt;
+  int all_core = 0;
   uint64_t *e_key, *e_key_sorted;
   float* e_w;
   unsigned long long* buckets;
@@ -852,7 +1127,13 @@ size_t cub_tmp_bytes(int64_t N, int64_t cap_edges) {
                                 (unsigned long long*)nullptr, (int)std::max<int64_t>(N + 1, 1));
   cub::DeviceRadixSort::SortPairs(nullptr, c, (const uint64_t*)nullptr, (uint64_t*)nullptr,
                                   (const float*)nullptr, (float*)nullptr, (int)std::max<int64_t>(cap_edges, 1));
-  return std::max(a, std::max(b, c)) + 256;
+  size_t d = 0, e = 0;
+  const int n1 = (int)std::max<int64_t>(N + 1, 1);
+  thrust::transform_iterator<IsTwo, const uint8_t*, bool> two(nullptr, IsTwo{});
+  cub::DeviceSelect::Flagged(nullptr, d, (const Cont*)nullptr, two, (Cont*)nullptr, (uint32_t*)nullptr, n1);
+  cub::DeviceSelect::Flagged(nullptr, e, (const Act*)nullptr, (const uint8_t*)nullptr, (Act*)nullptr,
+                             (uint32_t*)nullptr, n1);
+  return std::max(std::max(a, std::max(b, c)), std::max(d, e)) + 256;
 }
 
 // carve the workspace; returns bytes needed
@@ -871,6 +1152,7 @@ size_t carve(Layout& L, char* base, bool dry, int64_t N, int nr, const int64_t* 
   L.kmin2 = cv.take<uint32_t>(N + 1);
   L.Kc = cv.take<uint64_t>(N + 1);
   L.Bc = cv.take<uint32_t>(N + 1);
+  L.tgt = cv.take<int32_t>(N + 1);
   L.e_key = cv.take<uint64_t>(N + 1);
   L.e_key_sorted = cv.take<uint64_t>(N + 1);
   L.e_w = cv.take<float>(N + 1);
@@ -884,10 +1166,13 @@ size_t carve(Layout& L, char* base, bool dry, int64_t N, int nr, const int64_t* 
     R.row_begin = rb[r];
     R.n_rows = rn[r];
     const int64_t n = std::max<int64_t>(rn[r], 1);
-    R.head = cv.take<uint16_t>(n);
-    R.act[0] = cv.take<int32_t>(n);
-    R.act[1] = cv.take<int32_t>(n);
+    R.act[0] = cv.take<Act>(n);
+    R.act[1] = cv.take<Act>(n);
+    R.cand = cv.take<Cont>(n);
+    R.cont = cv.take<Cont>(n);
+    R.status = cv.take<uint8_t>(n);
     const int64_t noff = general ? n + N : n;
+    R.off_cap_rows = n;
     R.off_v = cv.take<int32_t>(noff);
     R.off_key = cv.take<uint64_t>(noff);
     R.off_b = cv.take<uint32_t>(noff);
@@ -895,9 +1180,11 @@ size_t carve(Layout& L, char* base, bool dry, int64_t N, int nr, const int64_t* 
     if (r > 0) {
       R.Kc = cv.take<uint64_t>(N + 1);
       R.Bc = cv.take<uint32_t>(N + 1);
+      R.tgt = cv.take<int32_t>(N + 1);
     } else {
       R.Kc = L.Kc;
       R.Bc = L.Bc;
+      R.tgt = L.tgt;
     }
     if (general) {
       R.in_off = cv.take<unsigned long long>(N + 1);
@@ -1149,6 +1436,7 @@ kdb_status kdb_mst(const kdb_graph* g, float eps, const uint32_t* core_bits, int
   KDB_CUDA(cudaMemcpyAsync(&C32, L.woff + nwords, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
   KDB_CUDA(cudaStreamSynchronize(st));
   int64_t C = C32;
+  L.all_core = (C == N) ? 1 : 0;  // then no entry needs a core-bit gather
   LAUNCH(k_init_comp, grid_for(N), kThreads, st, core_bits, L.woff, N, comp, L.cmin);
   LAUNCH(k_fill_comp_arrays, grid_for(C), kThreads, st, C, L.Kc, L.Bc, general ? nullptr : L.kmin);
   for (size_t r = 1; r < L.ranks.size(); ++r)
@@ -1156,13 +1444,21 @@ kdb_status kdb_mst(const kdb_graph* g, float eps, const uint32_t* core_bits, int
   KDB_CUDA(cudaGetLastError());
   for (auto& R : L.ranks) {
     KDB_CUDA(cudaMemsetAsync(R.ctr, 0, sizeof(RoundCounters), st));
-    if (R.n_rows > 0)
-      LAUNCH(k_init_rows, grid_for(R.n_rows), kThreads, st, R.dist, R.n_rows, k, eps, R.row_begin, core_bits,
-                                                           comp, R.head, general ? nullptr : L.kmin,
-                                                           R.act[0], &R.ctr->n_act[0]);
+    if (R.n_rows > 0) {
+      // every row as (v, 0) + a flag, then a stable select: the active list is in row order
+      LAUNCH(k_init_rows, grid_for(R.n_rows), kThreads, st, R.dist, R.n_rows, k, eps, R.row_begin, core_bits, comp,
+             general ? nullptr : L.kmin, R.act[1], R.status);
+      cb = L.cub_bytes;
+      { LaunchScope ls_("cub::DeviceSelect", st, false);
+        KDB_CUDA(cub::DeviceSelect::Flagged(L.cub_tmp, cb, R.act[1], R.status, R.act[0], &R.ctr->n_act[0],
+                                            (int)R.n_rows, st)); }
+    }
     KDB_CUDA(cudaGetLastError());
   }
-  if (!general) KDB_TRY(allreduce_min_u32(comm, L.kmin, C, st));
+  if (!general) {
+    KDB_TRY(allreduce_min_u32(comm, L.kmin, C, st));
+    for (auto& R : L.ranks) LAUNCH(k_fill_i32, grid_for(C), kThreads, st, R.tgt, C, INT32_MAX);
+  }
   KDB_CUDA(cudaEventRecord(ev[1], st));
   // ---- general mode: in-edge lists --------------------------------------------
   if (general) {
@@ -1205,19 +1501,60 @@ kdb_status kdb_mst(const kdb_graph* g, float eps, const uint32_t* core_bits, int
   double t_min_edges = 0, t_contract = 0;
   while (C > 0) {
     ++rounds;
+    // round 1 of exact mode: singleton components, one offer each (no in-lists)
+    const bool direct = rounds == 1 && !general;
     KDB_CUDA(cudaEventRecord(ev[0], st));
     // a3: offers (rows, then in-lists), per rank, into that rank's Kc partial
     for (auto& R : L.ranks) {
       KDB_CUDA(cudaMemsetAsync(&R.ctr->n_act[0], 0, 3 * sizeof(uint32_t), st));  // n_act[0..1], n_off
-      if (R.n_act)
-        LAUNCH(k_offer_rows, grid_for(R.n_act), kThreads, st, 
-            R.nbr, R.dist, k, eps, R.row_begin, N, core_bits, comp, R.act[cur], R.n_act, R.head,
-            R.act[cur ^ 1], &R.ctr->n_act[0], R.off_v, R.off_key, R.off_b, &R.ctr->n_off,
-            (unsigned long long*)R.Kc);
+      R.n_slots = 0;
+      if (R.n_act) {
+        const uint32_t n_in = R.n_act;
+        if (direct) {
+          LAUNCH(k_offer_first, grid_for(n_in), kThreads, st, R.nbr, R.dist, k, eps, R.row_begin, N, core_bits,
+                 L.all_core, comp, R.act[cur], n_in, R.status, R.Kc, R.Bc, R.tgt, &L.ctr->entries);
+        } else {
+          // slot chunks: all threads finish a chunk before the next starts, which
+          // keeps the rows (and hence the comp[] window) in flight narrow
+          for (uint32_t s0 = 0; s0 < n_in; s0 += g_chunk) {
+            const uint32_t s1 = std::min<uint32_t>(s0 + g_chunk, n_in);
+            if ((k % 4) == 0)
+              LAUNCH(k_offer_rows_t<true>, grid_for(s1 - s0), kThreads, st, R.nbr, R.dist, k, eps, R.row_begin, N,
+                     core_bits, L.all_core, comp, R.act[cur], s0, s1, R.status, R.off_key, R.off_b, R.cand,
+                     (unsigned long long*)R.Kc, &L.ctr->entries);
+            else
+              LAUNCH(k_offer_rows_t<false>, grid_for(s1 - s0), kThreads, st, R.nbr, R.dist, k, eps, R.row_begin, N,
+                     core_bits, L.all_core, comp, R.act[cur], s0, s1, R.status, R.off_key, R.off_b, R.cand,
+                     (unsigned long long*)R.Kc, &L.ctr->entries);
+          }
+          // rows still skipping dead entries -> warp-per-row scan (stable order)
+          cb = L.cub_bytes;
+          {
+            LaunchScope ls_("cub::DeviceSelect", st, false);
+            thrust::transform_iterator<IsTwo, const uint8_t*, bool> two(R.status, IsTwo{});
+            KDB_CUDA(cub::DeviceSelect::Flagged(L.cub_tmp, cb, R.cand, two, R.cont, &R.ctr->n_cont, (int)n_in, st));
+          }
+          uint32_t ncont = 0;
+          KDB_CUDA(cudaMemcpyAsync(&ncont, &R.ctr->n_cont, 4, cudaMemcpyDeviceToHost, st));
+          KDB_CUDA(cudaStreamSynchronize(st));
+          for (uint32_t q0 = 0; q0 < ncont; q0 += g_chunk_w) {
+            const uint32_t q1 = std::min<uint32_t>(q0 + g_chunk_w, ncont);
+            LAUNCH(k_offer_warp, grid_for((int64_t)(q1 - q0) * 32), kThreads, st, R.nbr, R.dist, k, eps, R.row_begin,
+                   N, core_bits, L.all_core, comp, R.cont, &R.ctr->n_cont, q0, q1, R.act[cur], R.status, R.off_key,
+                   R.off_b, (unsigned long long*)R.Kc, &L.ctr->entries);
+          }
+        }
+        // next active list: rows that offered this round (order preserved)
+        cb = L.cub_bytes;
+        { LaunchScope ls_("cub::DeviceSelect", st, false);
+          KDB_CUDA(cub::DeviceSelect::Flagged(L.cub_tmp, cb, R.act[cur], R.status, R.act[cur ^ 1],
+                                              &R.ctr->n_act[0], (int)n_in, st)); }
+        R.n_slots = direct ? 0 : n_in;
+      }
       if (general && R.n_in_act)
-        LAUNCH(k_offer_in, grid_for(R.n_in_act), kThreads, st, 
-            R.in_off, R.in_len, R.in_src, R.in_w, comp, R.in_act[cur], R.n_in_act, R.in_act[cur ^ 1],
-            &R.ctr->n_act[1], R.off_v, R.off_key, R.off_b, &R.ctr->n_off, (unsigned long long*)R.Kc);
+        LAUNCH(k_offer_in, grid_for(R.n_in_act), kThreads, st, R.in_off, R.in_len, R.in_src, R.in_w, comp,
+               R.in_act[cur], R.n_in_act, R.in_act[cur ^ 1], &R.ctr->n_act[1], R.off_v + R.off_cap_rows,
+               R.off_key + R.off_cap_rows, R.off_b + R.off_cap_rows, &R.ctr->n_off, (unsigned long long*)R.Kc);
       KDB_CUDA(cudaGetLastError());
     }
     for (auto& R : L.ranks) {
@@ -1226,26 +1563,35 @@ kdb_status kdb_mst(const kdb_graph* g, float eps, const uint32_t* core_bits, int
       KDB_CUDA(cudaStreamSynchronize(st));
       R.n_act = hc.n_act[0];
       R.n_in_act = hc.n_act[1];
-      R.n_off = hc.n_off;
+      R.n_off = hc.n_off;  // in-list offers; row offers are the first n_act slots
     }
     // exchange: sim -> min over virtual ranks; nccl -> allreduce
     for (size_t r = 1; r < L.ranks.size(); ++r)
       LAUNCH(k_min_into_u64, grid_for(C), kThreads, st, L.Kc, L.ranks[r].Kc, C);
     KDB_TRY(allreduce_min_u64(comm, L.Kc, C, st));
-    // a4: ties
+    // a4: ties (the direct round already wrote Bc and the targets)
     for (auto& R : L.ranks) {
-      if (R.n_off)
-        LAUNCH(k_tie, grid_for(R.n_off), kThreads, st, R.off_v, R.off_key, R.off_b, R.n_off, comp, L.Kc, R.Bc);
+      if (R.n_slots && !direct)
+        LAUNCH(k_tie_slots, grid_for(R.n_slots), kThreads, st, R.act[cur], R.status, R.off_key, R.off_b,
+               R.n_slots, comp, L.Kc, R.Bc);
+      if (R.n_off && !direct)
+        LAUNCH(k_tie, grid_for(R.n_off), kThreads, st, R.off_v + R.off_cap_rows, R.off_key + R.off_cap_rows,
+               R.off_b + R.off_cap_rows, R.n_off, comp, L.Kc, R.Bc);
       KDB_CUDA(cudaGetLastError());
     }
     for (size_t r = 1; r < L.ranks.size(); ++r)
       LAUNCH(k_min_into_u32, grid_for(C), kThreads, st, L.Bc, L.ranks[r].Bc, C);
     KDB_TRY(allreduce_min_u32(comm, L.Bc, C, st));
+    if (direct) {
+      for (size_t r = 1; r < L.ranks.size(); ++r)
+        LAUNCH(k_min_into_u32, grid_for(C), kThreads, st, (uint32_t*)L.tgt, (const uint32_t*)L.ranks[r].tgt, C);
+      KDB_TRY(allreduce_min_u32(comm, (uint32_t*)L.tgt, C, st));  // non-owners hold INT32_MAX
+    }
     KDB_CUDA(cudaEventRecord(ev[1], st));
     // a5: hook + emit
     KDB_CUDA(cudaMemsetAsync(&L.ctr->hooks, 0, 4 * sizeof(uint32_t), st));
-    LAUNCH(k_hook, grid_for(C), kThreads, st, C, L.Kc, L.Bc, kmin_cert, comp, L.parent, L.e_key, L.e_w, N,
-                                             L.ctr);
+    LAUNCH(k_hook, grid_for(C), kThreads, st, C, L.Kc, L.Bc, direct ? L.tgt : nullptr, kmin_cert, comp, L.parent,
+           L.e_key, L.e_w, N, L.ctr);
     KDB_CUDA(cudaGetLastError());
     RoundCounters hc;
     KDB_CUDA(cudaMemcpyAsync(&hc, L.ctr, sizeof(hc), cudaMemcpyDeviceToHost, st));
@@ -1266,22 +1612,20 @@ kdb_status kdb_mst(const kdb_graph* g, float eps, const uint32_t* core_bits, int
         LAUNCH(k_fill_comp_arrays, grid_for(C), kThreads, st, C, L.ranks[r].Kc, L.ranks[r].Bc, nullptr);
       for (auto& R : L.ranks)
         if (R.n_rows)
-          LAUNCH(k_sweep, grid_for(R.n_rows), kThreads, st, R.nbr, R.dist, R.n_rows, k, eps, R.row_begin, N,
-                                                           core_bits, comp, R.head,
-                                                           (unsigned long long*)R.Kc, R.Bc, 0);
+          LAUNCH(k_sweep, grid_for(R.n_act), kThreads, st, R.nbr, R.dist, k, eps, R.row_begin, N, core_bits, comp,
+                 R.act[cur ^ 1], R.n_act, (unsigned long long*)R.Kc, R.Bc, 0);
       for (size_t r = 1; r < L.ranks.size(); ++r)
         LAUNCH(k_min_into_u64, grid_for(C), kThreads, st, L.Kc, L.ranks[r].Kc, C);
       KDB_TRY(allreduce_min_u64(comm, L.Kc, C, st));
       for (auto& R : L.ranks)
         if (R.n_rows)
-          LAUNCH(k_sweep, grid_for(R.n_rows), kThreads, st, R.nbr, R.dist, R.n_rows, k, eps, R.row_begin, N,
-                                                           core_bits, comp, R.head,
-                                                           (unsigned long long*)L.Kc, R.Bc, 1);
+          LAUNCH(k_sweep, grid_for(R.n_act), kThreads, st, R.nbr, R.dist, k, eps, R.row_begin, N, core_bits, comp,
+                 R.act[cur ^ 1], R.n_act, (unsigned long long*)L.Kc, R.Bc, 1);
       for (size_t r = 1; r < L.ranks.size(); ++r)
         LAUNCH(k_min_into_u32, grid_for(C), kThreads, st, L.Bc, L.ranks[r].Bc, C);
       KDB_TRY(allreduce_min_u32(comm, L.Bc, C, st));
       KDB_CUDA(cudaMemsetAsync(&L.ctr->hooks, 0, 4 * sizeof(uint32_t), st));
-      LAUNCH(k_hook, grid_for(C), kThreads, st, C, L.Kc, L.Bc, nullptr, comp, L.parent, L.e_key, L.e_w, N,
+      LAUNCH(k_hook, grid_for(C), kThreads, st, C, L.Kc, L.Bc, nullptr, nullptr, comp, L.parent, L.e_key, L.e_w, N,
                                                L.ctr);
       KDB_CUDA(cudaGetLastError());
       KDB_CUDA(cudaMemcpyAsync(&hc, L.ctr, sizeof(hc), cudaMemcpyDeviceToHost, st));
@@ -1307,9 +1651,10 @@ kdb_status kdb_mst(const kdb_graph* g, float eps, const uint32_t* core_bits, int
     const int64_t C2 = (int64_t)last[0] + last[1];
     LAUNCH(k_fill_i32, grid_for(C2), kThreads, st, L.cmin2, C2, INT32_MAX);
     if (!general) LAUNCH(k_fill_i32, grid_for(C2), kThreads, st, (int32_t*)L.kmin2, C2, (int32_t)kInfBits);
+    // map[c] = new dense id of c's tree (reuses `parent`, no longer needed)
     LAUNCH(k_merge, grid_for(C), kThreads, st, C, L.rootof, L.newid, L.cmin, general ? nullptr : L.kmin, L.cmin2,
-                                              L.kmin2);
-    LAUNCH(k_relabel, grid_for(N), kThreads, st, N, comp, L.rootof, L.newid);
+           L.kmin2, L.parent);
+    LAUNCH(k_relabel, grid_for(N), kThreads, st, N, comp, L.parent);
     LAUNCH(k_fill_comp_arrays, grid_for(C2), kThreads, st, C2, L.Kc, L.Bc, nullptr);
     for (size_t r = 1; r < L.ranks.size(); ++r)
       LAUNCH(k_fill_comp_arrays, grid_for(C2), kThreads, st, C2, L.ranks[r].Kc, L.ranks[r].Bc, nullptr);
@@ -1357,6 +1702,7 @@ kdb_status kdb_mst(const kdb_graph* g, float eps, const uint32_t* core_bits, int
   g_stats[3] = t_contract;
   g_stats[4] = ms;
   g_stats[6] = stalls;
+  g_stats[7] = (double)hc.entries;
   return KDB_OK;
 }
 

@@ -213,7 +213,7 @@ def mst(g: Graph, eps: float, core_bits: torch.Tensor, comm: Comm | None = None,
     st = (C.c_double * 8)()
     lib().kdb_last_mst_stats(st, 8)
     stats = dict(rounds=int(st[0]), init_ms=st[1], min_edges_ms=st[2], contract_ms=st[3],
-                 finalize_ms=st[4], inlist_ms=st[5], stall_rounds=int(st[6]))
+                 finalize_ms=st[4], inlist_ms=st[5], stall_rounds=int(st[6]), entries_read=int(st[7]))
     m = cnt.value
     return MstResult(comp[:N], a[:m], b[:m], w[:m], m, tot.value, stats)
 
