@@ -144,6 +144,13 @@ struct Prof {
   }
 };
 Prof g_prof;
+const int g_trace = getenv("KDB_TRACE") ? atoi(getenv("KDB_TRACE")) : 0;  // per-round log to stderr
+const int g_sortcont = getenv("KDB_SORTCONT") ? atoi(getenv("KDB_SORTCONT")) : 0;
+const int g_lines = getenv("KDB_LINES") ? atoi(getenv("KDB_LINES")) : 4;
+const int g_fa = getenv("KDB_FA") ? atoi(getenv("KDB_FA")) : 1;  // first block lines, awake rows
+const int g_fs = getenv("KDB_FS") ? atoi(getenv("KDB_FS")) : 4;  // first block lines, woken rows
+const int g_lazy = getenv("KDB_LAZY") ? atoi(getenv("KDB_LAZY")) : 1;
+const int g_qmax = getenv("KDB_QMAX") ? atoi(getenv("KDB_QMAX")) : 1;
 const uint32_t g_chunk = getenv("KDB_CHUNK") ? (uint32_t)atoi(getenv("KDB_CHUNK")) : (1u << 30);
 const uint32_t g_chunk_w = getenv("KDB_CHUNKW") ? (uint32_t)atoi(getenv("KDB_CHUNKW")) : (1u << 30);
 
@@ -253,6 +260,7 @@ struct RoundCounters {
                                  // KDB_GRAPH_EXACT promise was false (or a bug)
   uint32_t n_cont;               // rows continuing in the warp-per-row scan
   uint32_t pad1;
+  uint32_t part[2];              // next round: awake rows, asleep rows
   unsigned long long entries;    // graph entries (id + weight) read by offer kernels
 };
 
@@ -348,8 +356,10 @@ __global__ void k_fill_comp_arrays(int64_t C, uint64_t* __restrict__ Kc, uint32_
 // row id through the active lists, so a row's state arrives in one coalesced
 // 8-byte load instead of a chain of dependent gathers.
 struct Act {
-  int32_t v;  // global row id
-  int32_t h;  // head: every entry before it is dead for good
+  int32_t v;   // global row id
+  int32_t h;   // head: every entry before it is dead for good
+  float lb;    // asleep rows: every live entry at/after h weighs >= lb
+  int32_t asleep;  // 1: deferred -- skipped by pass A, only wake-checked
 };
 // continuation record: everything k_offer_warp needs, written by k_offer_rows_t
 struct Cont {
@@ -377,7 +387,7 @@ __global__ void k_init_rows(const float* __restrict__ dist, int64_t n_rows, int3
       }
     }
     if (i < n_rows) {
-      active[i] = Act{(int32_t)v, 0};
+      active[i] = Act{(int32_t)v, 0, 0.f, 0};  // awake
       flag[i] = want ? 1 : 0;
     }
   }
@@ -458,10 +468,9 @@ __device__ __forceinline__ bool cand_entry(int64_t J, int64_t v, int64_t N, cons
 // One thread per active row; each step takes an aligned 4-entry chunk (int4
 // ids + float4 weights when k % 4 == 0, loaded evict-first so the streamed
 // graph does not push comp[] out of L2) and issues its 4 component gathers
-// together.  A thread gives up after kQmax chunks of dead entries (the chunk
+// together.  A thread gives up after qmax chunks of dead entries (the chunk
 // count per row varies 1..k/4 inside a warp); the row then continues in
 // k_offer_warp, 32 entries per step.
-constexpr int kQmax = 2;
 
 template <bool VEC>
 __device__ __forceinline__ void load_chunk(const int32_t* nr, const float* dr, int c0, int k, int32_t (&J)[4],
@@ -487,13 +496,14 @@ __global__ void __launch_bounds__(256) k_offer_rows_t(
     int64_t N, const uint32_t* __restrict__ bits, int all_core, const int32_t* __restrict__ comp,
     Act* __restrict__ act, uint32_t s_begin, uint32_t s_end, uint8_t* __restrict__ status,
     uint64_t* __restrict__ off_key, uint32_t* __restrict__ off_b, Cont* __restrict__ cand,
-    unsigned long long* __restrict__ Kc, unsigned long long* __restrict__ n_entries) {
+    unsigned long long* __restrict__ Kc, unsigned long long* __restrict__ n_entries, int qmax) {
   unsigned long long reads = 0;
   for (uint32_t s = s_begin + blockIdx.x * blockDim.x + threadIdx.x; s < s_end; s += gridDim.x * blockDim.x) {
     bool found = false, more = false;
     uint64_t best = kSent;
     uint32_t bestb = kSentB;
-    const int2 a = __ldcs(reinterpret_cast<const int2*>(act + s));
+    const int4 a = __ldcs(reinterpret_cast<const int4*>(act + s));
+    if (a.w) continue;  // asleep: k_wake decides
     const int32_t v = a.x;
     int h = a.y;
     const int64_t i = (int64_t)v - row_begin;
@@ -501,11 +511,11 @@ __global__ void __launch_bounds__(256) k_offer_rows_t(
     const float* dr = dist + i * k;
     const int32_t cv = gat(comp + v);
     int c0 = h & ~3;
-    float wstar = 0.f;
+    float wstar = 0.f, wlast = 0.f;  // wlast: weight of the last dead entry passed
     bool done = false;
     int steps = 0;
     while (!done && c0 < k) {
-      if (!found && steps == kQmax) {  // hand the rest of the dead run to a warp
+      if (!found && steps == qmax) {  // hand the rest of the dead run to a warp
         more = true;
         break;
       }
@@ -526,7 +536,7 @@ __global__ void __launch_bounds__(256) k_offer_rows_t(
         if (done || idx < h || idx >= k) continue;
         if (!found) {
           if (!(w[j] <= eps)) { h = k; done = true; continue; }  // sorted: nothing left
-          if (cj[j] == -2 || cj[j] == cv) { h = idx + 1; continue; }  // dead entry
+          if (cj[j] == -2 || cj[j] == cv) { h = idx + 1; wlast = w[j]; continue; }  // dead entry
           found = true;  // first leaving entry opens the minimum group
           h = idx;
           wstar = w[j];
@@ -550,17 +560,22 @@ __global__ void __launch_bounds__(256) k_offer_rows_t(
       __stcs(off_b + s, bestb);
       atomicMin(Kc + cv, (unsigned long long)best);
     } else if (more) {
-      __stcs(reinterpret_cast<int4*>(cand + s), make_int4(v, h, cv, (int)s));
+      if (cand) __stcs(reinterpret_cast<int4*>(cand + s), make_int4(v, h, cv, (int)s));
+      act[s].lb = wlast;  // every leaving entry still ahead weighs >= wlast (rows are sorted)
     }
   }
   for (int o = 16; o > 0; o >>= 1) reads += __shfl_xor_sync(0xffffffffu, reads, o);
   if ((threadIdx.x & 31) == 0 && reads) atomicAdd(n_entries, reads);
 }
 
-// Continuation: one warp per row, 32 consecutive entries per step (one 128-B
-// line of ids and one of weights, 32 component gathers in flight); a ballot
-// finds the first leaving entry, a warp reduction the minimum of its
-// equal-weight group.  The record of the warp's next row is prefetched.
+// Continuation: one warp per row.  Lane l takes entries h+l, h+l+32, h+l+64,
+// h+l+96 of a 128-entry block: all id/weight loads and all component gathers
+// of the block are in flight together (no dependency between lines), then the
+// warp reduces (first leaving position, minimum key of the equal-weight group
+// that starts there).  Rows are sorted, so the minimum over the block's
+// leaving entries with the smallest weight IS that group's minimum; only when a
+// group reaches the end of the block does the next block have to be looked at.
+template <int kLines>
 __global__ void __launch_bounds__(256) k_offer_warp(
     const int32_t* __restrict__ nbr, const float* __restrict__ dist, int32_t k, float eps, int64_t row_begin,
     int64_t N, const uint32_t* __restrict__ bits, int all_core, const int32_t* __restrict__ comp,
@@ -576,61 +591,84 @@ __global__ void __launch_bounds__(256) k_offer_warp(
   if (q < n_cont) rec = __ldcs(reinterpret_cast<const int4*>(cont + q));
   for (; q < n_cont; q += nwarps) {
     const int32_t v = rec.x, cv = rec.z, s = rec.w;
-    int h = rec.y;
+    const int h0 = rec.y;
     if (q + nwarps < n_cont) rec = __ldcs(reinterpret_cast<const int4*>(cont + q + nwarps));
     const int64_t i = (int64_t)v - row_begin;
     const int32_t* nr = nbr + i * k;
     const float* dr = dist + i * k;
-    bool found = false;
+    int pos = k;              // first leaving position found so far
+    uint32_t wbest = 0xffffffffu;  // its weight bits
     uint64_t best = kSent;
     uint32_t bestb = kSentB;
-    float wstar = 0.f;
-    for (int c0 = h & ~31; c0 < k; c0 += 32) {
-      const int idx = c0 + lane;
-      const bool in = idx >= h && idx < k;
-      float w = __int_as_float(0x7f800000);
-      int32_t J = -1;
-      if (in) {
-        w = __ldcs(dr + idx);
-        J = __ldcs(nr + idx);
+    int base = h0;
+    bool stop = false;
+    while (!stop && base < k) {
+      float w[kLines];
+      int32_t J[kLines];
+#pragma unroll
+      for (int t = 0; t < kLines; ++t) {
+        const int c = base + lane + 32 * t;
+        w[t] = c < k ? __ldcs(dr + c) : __int_as_float(0x7f800000);
+        J[t] = c < k ? __ldcs(nr + c) : -1;
       }
-      if (lane == 0) reads += (unsigned long long)(min(c0 + 32, k) - max(c0, h));
-      const bool beyond = in && !(w <= eps);
-      bool leaving = false;
-      if (in && !beyond && cand_entry(J, v, N, bits, all_core)) leaving = gat(comp + J) != cv;
-      const unsigned mb = __ballot_sync(0xffffffffu, beyond);
-      const unsigned ml = __ballot_sync(0xffffffffu, leaving);
-      const int fb = mb ? __ffs(mb) - 1 : 32;
-      if (!found) {
-        const int fl = ml ? __ffs(ml) - 1 : 32;
-        if (fl < fb) {
-          found = true;
-          h = c0 + fl;
-          wstar = __shfl_sync(0xffffffffu, w, fl);
-        } else if (fb < 32) {
-          h = k;
-          break;
-        } else {
-          h = c0 + 32;
-          continue;
+      int32_t cj[kLines];
+#pragma unroll
+      for (int t = 0; t < kLines; ++t)
+        cj[t] = (w[t] <= eps && cand_entry(J[t], v, N, bits, all_core)) ? gat(comp + J[t]) : cv;
+      bool beyond = false;
+      unsigned lp = (unsigned)k;  // this lane's first leaving position in the block
+#pragma unroll
+      for (int t = kLines - 1; t >= 0; --t) {
+        const int c = base + lane + 32 * t;
+        if (c < k && !(w[t] <= eps)) beyond = true;
+        if (cj[t] != cv) lp = (unsigned)c;
+      }
+      lp = __reduce_min_sync(0xffffffffu, lp);  // the block's first leaving position
+      if ((int)lp < k) {
+        if (pos == k) {  // first leaving entry of the row: its weight opens the group
+          const int rel = (int)lp - base;
+          float wl = 0.f;
+#pragma unroll
+          for (int t = 0; t < kLines; ++t) {
+            const float x = __shfl_sync(0xffffffffu, w[t], rel & 31);
+            if ((rel >> 5) == t) wl = x;
+          }
+          pos = (int)lp;
+          wbest = mono_bits(wl);
         }
+        // group members in this block: leaving entries of weight wbest; their key's
+        // weight part is equal, so the minimum is over (a, b) as two 32-bit mins
+        uint32_t am = 0xffffffffu, bm = 0xffffffffu;
+#pragma unroll
+        for (int t = 0; t < kLines; ++t) {
+          const int c = base + lane + 32 * t;
+          if (c < k && cj[t] != cv && mono_bits(w[t]) == wbest) {
+            const uint32_t a2 = (uint32_t)min((int64_t)v, (int64_t)J[t]);
+            const uint32_t b2 = (uint32_t)max((int64_t)v, (int64_t)J[t]);
+            if (a2 < am || (a2 == am && b2 < bm)) { am = a2; bm = b2; }
+          }
+        }
+        const uint32_t amin = __reduce_min_sync(0xffffffffu, am);
+        const uint32_t bmin = __reduce_min_sync(0xffffffffu, am == amin ? bm : 0xffffffffu);
+        const uint64_t kk = pack_key(wbest, amin);
+        if (amin != 0xffffffffu && (kk < best || (kk == best && bmin < bestb))) { best = kk; bestb = bmin; }
       }
-      uint64_t kk = kSent;
-      uint32_t bb = kSentB;
-      if (leaving && w == wstar) {
-        kk = pack_key(mono_bits(w), (uint32_t)min((int64_t)v, (int64_t)J));
-        bb = (uint32_t)max((int64_t)v, (int64_t)J);
+      bool tail_eq = false;  // an entry of weight wbest sits at the block end
+      if (pos < k) {
+        const int c = base + lane + 32 * (kLines - 1);
+        tail_eq = lane == 31 && c < k && w[kLines - 1] <= eps && mono_bits(w[kLines - 1]) == wbest;
       }
-      for (int o = 16; o > 0; o >>= 1) {
-        const uint64_t k2 = __shfl_xor_sync(0xffffffffu, kk, o);
-        const uint32_t b2 = __shfl_xor_sync(0xffffffffu, bb, o);
-        if (k2 < kk || (k2 == kk && b2 < bb)) { kk = k2; bb = b2; }
-      }
-      if (kk < best || (kk == best && bb < bestb)) { best = kk; bestb = bb; }
-      if (!__shfl_sync(0xffffffffu, in && w == wstar, 31)) break;  // group ends in this line
+      if (lane == 0) reads += (unsigned long long)(min(base + 32 * kLines, k) - base);
+      const bool any_beyond = __any_sync(0xffffffffu, beyond);
+      const bool tail = __any_sync(0xffffffffu, tail_eq);
+      // stop once a leaving entry was found (unless its group reaches the block
+      // end) or the weights passed eps (sorted rows: nothing after)
+      stop = any_beyond || (pos < k && !tail);
+      base += 32 * kLines;
     }
     if (lane == 0) {
-      act[s].h = min(h, k);
+      const bool found = best != kSent;
+      act[s].h = found ? pos : k;
       status[s] = found ? 1 : 0;
       if (found) {
         off_key[s] = best;
@@ -643,9 +681,245 @@ __global__ void __launch_bounds__(256) k_offer_warp(
   if (lane == 0 && reads) atomicAdd(n_entries, reads);
 }
 
+// One warp scans the remaining entries of row v from head h0 (all 32 lanes,
+// the whole warp must call it).  Lane l takes entries base+l, base+l+32, ...:
+// the first block is one 32-entry line (most rows leave early), later blocks
+// are 128 entries with all id/weight loads and component gathers in flight
+// together.  Returns (found, first leaving position, minimum key and b of the
+// equal-weight group that starts there); rows are sorted, so that group's
+// minimum is the row's minimum leaving edge under O1.
+struct RowMin {
+  bool found;
+  int pos;
+  uint64_t key;
+  uint32_t b;
+};
+
+__device__ __forceinline__ RowMin warp_scan_row(const int32_t* __restrict__ nr, const float* __restrict__ dr, int k,
+                                                float eps, int32_t v, int32_t cv, int h0, int64_t N,
+                                                const uint32_t* __restrict__ bits, int all_core,
+                                                const int32_t* __restrict__ comp, unsigned long long& reads,
+                                                int first_lines) {
+  constexpr int kL = 4;
+  const int lane = threadIdx.x & 31;
+  int pos = k;
+  uint32_t wbest = 0xffffffffu;
+  uint64_t best = kSent;
+  uint32_t bestb = kSentB;
+  int base = h0;
+  int lines = first_lines;
+  bool stop = false;
+  while (!stop && base < k) {
+    const int bend = min(base + 32 * lines, k);  // block = [base, bend)
+    float w[kL];
+    int32_t J[kL];
+#pragma unroll
+    for (int t = 0; t < kL; ++t) {
+      const int c = base + lane + 32 * t;
+      const bool in = t < lines && c < bend;
+      w[t] = in ? __ldcs(dr + c) : __int_as_float(0x7f800000);
+      J[t] = in ? __ldcs(nr + c) : -1;
+    }
+    int32_t cj[kL];
+#pragma unroll
+    for (int t = 0; t < kL; ++t)
+      cj[t] = (w[t] <= eps && cand_entry(J[t], v, N, bits, all_core)) ? gat(comp + J[t]) : cv;
+    bool beyond = false;
+    unsigned lp = (unsigned)k;
+#pragma unroll
+    for (int t = kL - 1; t >= 0; --t) {
+      const int c = base + lane + 32 * t;
+      if (t < lines && c < bend && !(w[t] <= eps)) beyond = true;
+      if (cj[t] != cv) lp = (unsigned)c;
+    }
+    lp = __reduce_min_sync(0xffffffffu, lp);
+    if ((int)lp < k) {
+      if (pos == k) {
+        const int rel = (int)lp - base;
+        float wl = 0.f;
+#pragma unroll
+        for (int t = 0; t < kL; ++t) {
+          const float x = __shfl_sync(0xffffffffu, w[t], rel & 31);
+          if ((rel >> 5) == t) wl = x;
+        }
+        pos = (int)lp;
+        wbest = mono_bits(wl);
+      }
+      uint32_t am = 0xffffffffu, bm = 0xffffffffu;
+#pragma unroll
+      for (int t = 0; t < kL; ++t) {
+        if (cj[t] != cv && mono_bits(w[t]) == wbest) {
+          const uint32_t a2 = (uint32_t)min((int64_t)v, (int64_t)J[t]);
+          const uint32_t b2 = (uint32_t)max((int64_t)v, (int64_t)J[t]);
+          if (a2 < am || (a2 == am && b2 < bm)) { am = a2; bm = b2; }
+        }
+      }
+      const uint32_t amin = __reduce_min_sync(0xffffffffu, am);
+      const uint32_t bmin = __reduce_min_sync(0xffffffffu, am == amin ? bm : 0xffffffffu);
+      const uint64_t kk = pack_key(wbest, amin);
+      if (amin != 0xffffffffu && (kk < best || (kk == best && bmin < bestb))) { best = kk; bestb = bmin; }
+    }
+    bool tail_eq = false;  // the block's last entry still has the group's weight
+    if (pos < k) {
+      const int last = bend - 1;
+      const int t = (last - base) >> 5;
+      if (lane == ((last - base) & 31)) {
+#pragma unroll
+        for (int u = 0; u < kL; ++u)
+          if (u == t) tail_eq = w[u] <= eps && mono_bits(w[u]) == wbest;
+      }
+    }
+    if (lane == 0) reads += (unsigned long long)(bend - base);
+    const bool any_beyond = __any_sync(0xffffffffu, beyond);
+    const bool tail = __any_sync(0xffffffffu, tail_eq);
+    stop = any_beyond || (pos < k && !tail);
+    base = bend;
+    lines = kL;
+  }
+  RowMin r;
+  r.found = best != kSent;
+  r.pos = pos;
+  r.key = best;
+  r.b = bestb;
+  return r;
+}
+
+// After pass A: one lane per slot of a 32-slot tile decides whether its row
+// must be scanned this round (lazy Boruvka):
+//   awake row with a dead first chunk (status 2): scan unless lb > w(Kc[comp])
+//     -- then it is deferred (asleep) instead;
+//   asleep row: scan (wake) iff lb <= w(Kc[comp]) -- Kc holds an actual
+//     leaving edge of the component, so a row whose live entries all weigh
+//     more cannot supply the minimum.
+// The warp then scans the flagged rows one after another.
+__global__ void __launch_bounds__(256) k_scan_tiles(
+    const int32_t* __restrict__ nbr, const float* __restrict__ dist, int32_t k, float eps, int64_t row_begin,
+    int64_t N, const uint32_t* __restrict__ bits, int all_core, const int32_t* __restrict__ comp,
+    Act* __restrict__ act, uint32_t n, uint8_t* __restrict__ status, uint64_t* __restrict__ off_key,
+    uint32_t* __restrict__ off_b, unsigned long long* __restrict__ Kc, int lazy,
+    unsigned long long* __restrict__ n_entries, uint32_t* __restrict__ n_scanned, int g_first_awake,
+    int g_first_asleep) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  unsigned long long reads = 0;
+  uint32_t scanned = 0;
+  for (uint32_t tile = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; tile * 32 < n; tile += nwarps) {
+    const uint32_t s = tile * 32 + lane;
+    bool need = false;
+    int4 r = make_int4(-1, 0, 0, 0);
+    int32_t cv = -1;
+    if (s < n) {
+      r = __ldcs(reinterpret_cast<const int4*>(act + s));
+      const uint8_t st = r.w ? 0xff : status[s];  // 0xff: asleep (pass A skipped it)
+      if (st == 2 || st == 0xff) {
+        cv = gat(comp + r.x);
+        const uint32_t kw = (uint32_t)(gat(Kc + cv) >> 32);  // sentinel -> never deferred
+        const bool over = lazy && mono_bits(__int_as_float(r.z)) > kw;
+        if (over) {  // cannot supply the minimum this round: (stay) asleep
+          status[s] = 4;
+          if (!r.w) act[s].asleep = 1;
+        } else {
+          need = true;
+          if (r.w) act[s].asleep = 0;
+        }
+      }
+    }
+    unsigned m = __ballot_sync(0xffffffffu, need);
+    if (lane == 0) scanned += __popc(m);
+    while (m) {
+      const int src = __ffs(m) - 1;
+      m &= m - 1;
+      const int32_t v = __shfl_sync(0xffffffffu, r.x, src);
+      const int32_t h0 = __shfl_sync(0xffffffffu, r.y, src);
+      const int32_t c = __shfl_sync(0xffffffffu, cv, src);
+      const int32_t was_asleep = __shfl_sync(0xffffffffu, r.w, src);
+      const uint32_t ss = tile * 32 + src;
+      const int64_t i = (int64_t)v - row_begin;
+      // a woken row's first live entry is usually far away; an awake row's is near
+      const RowMin rm = warp_scan_row(nbr + i * k, dist + i * k, k, eps, v, c, h0, N, bits, all_core, comp, reads,
+                                      was_asleep ? g_first_asleep : g_first_awake);
+      if (lane == 0) {
+        act[ss].h = rm.found ? rm.pos : k;
+        status[ss] = rm.found ? 1 : 0;
+        if (rm.found) {
+          off_key[ss] = rm.key;
+          off_b[ss] = rm.b;
+          atomicMin(Kc + c, (unsigned long long)rm.key);
+        }
+      }
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    reads += __shfl_xor_sync(0xffffffffu, reads, o);
+    scanned += __shfl_xor_sync(0xffffffffu, scanned, o);
+  }
+  if (lane == 0) {
+    if (reads) atomicAdd(n_entries, reads);
+    if (scanned) atomicAdd(n_scanned, scanned);
+  }
+}
+
 struct IsTwo {
   __host__ __device__ bool operator()(const uint8_t& x) const { return x == 2; }
 };
+struct IsOne {
+  __host__ __device__ bool operator()(const uint8_t& x) const { return x == 1; }
+};
+struct IsFour {
+  __host__ __device__ bool operator()(const uint8_t& x) const { return x == 4; }
+};
+struct Survives {  // stays active next round: offered (1) or deferred (4)
+  __host__ __device__ bool operator()(const uint8_t& x) const { return x == 1 || x == 4; }
+};
+struct StatusOf {  // partition predicate over slot indices
+  const uint8_t* st;
+  uint8_t val;
+  __host__ __device__ bool operator()(const int32_t& s) const { return st[s] == val; }
+};
+
+// Lazy Boruvka.  A continuing row (status 2) has only dead entries before its
+// head and every live entry after it weighs >= lb.  Its component already holds
+// an offer Kc (an actual leaving edge, so >= the component's true minimum).  If
+// lb > w(Kc) the row cannot supply the minimum this round: defer it (status 4,
+// it stays active with its head) instead of scanning.  Exact for any graph.
+__global__ void k_defer_filter(const Cont* __restrict__ cand, Act* __restrict__ act,
+                               uint8_t* __restrict__ status, uint32_t n, const unsigned long long* __restrict__ Kc) {
+  for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < n; s += gridDim.x * blockDim.x) {
+    if (status[s] != 2) continue;
+    const int32_t cv = cand[s].cv;
+    const uint32_t kw = (uint32_t)(gat(Kc + cv) >> 32);  // sentinel -> 0xffffffff, never defers
+    if (mono_bits(act[s].lb) > kw) {
+      status[s] = 4;
+      act[s].asleep = 1;
+    }
+  }
+}
+
+// Asleep rows (deferred in an earlier round) are not scanned by pass A at all;
+// they only wake when their bound no longer exceeds their component's best
+// pass-A offer (or the component has none).  Woken rows are scanned by
+// k_offer_warp this round and are awake again if they offer.
+__global__ void k_wake(Act* __restrict__ act, uint32_t n, const int32_t* __restrict__ comp,
+                       const unsigned long long* __restrict__ Kc, uint8_t* __restrict__ status,
+                       Cont* __restrict__ cand) {
+  for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < n; s += gridDim.x * blockDim.x) {
+    const int4 r = __ldcs(reinterpret_cast<const int4*>(act + s));
+    if (!r.w) continue;
+    const int32_t cv = gat(comp + r.x);
+    const uint32_t kw = (uint32_t)(gat(Kc + cv) >> 32);
+    const bool woken = mono_bits(__int_as_float(r.z)) <= kw;
+    status[s] = woken ? 2 : 4;
+    if (woken) {
+      act[s].asleep = 0;
+      __stcs(reinterpret_cast<int4*>(cand + s), make_int4(r.x, r.y, cv, (int)s));
+    }
+  }
+}
+
+__global__ void k_cont_keys(const Cont* __restrict__ c, uint32_t n, int32_t* __restrict__ keys) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) keys[i] = c[i].v;
+}
+
 
 // tie pass over per-slot row offers (status 1)
 __global__ void k_tie_slots(const Act* __restrict__ act, const uint8_t* __restrict__ status,
@@ -1079,8 +1353,8 @@ struct RankState {
   Act* act[2] = {nullptr, nullptr};  // active rows (v, head), ping-pong
   Cont* cand = nullptr;               // per-slot continuation records
   Cont* cont = nullptr;               // compacted continuation list
-  uint8_t* status = nullptr;          // per slot: 0 exhausted, 1 offer, 2 continue
-  uint32_t n_act = 0;
+  uint8_t* status = nullptr;          // per slot: 0 exhausted, 1 offer, 2 continue, 4 deferred
+  uint32_t n_act = 0;  // live rows in act[cur] (awake and asleep)
   uint32_t n_slots = 0;  // offer slots written by this round's row kernels
   // offers
   int32_t* off_v = nullptr;
@@ -1133,7 +1407,17 @@ size_t cub_tmp_bytes(int64_t N, int64_t cap_edges) {
   cub::DeviceSelect::Flagged(nullptr, d, (const Cont*)nullptr, two, (Cont*)nullptr, (uint32_t*)nullptr, n1);
   cub::DeviceSelect::Flagged(nullptr, e, (const Act*)nullptr, (const uint8_t*)nullptr, (Act*)nullptr,
                              (uint32_t*)nullptr, n1);
-  return std::max(std::max(a, std::max(b, c)), std::max(d, e)) + 256;
+  size_t f = 0, g = 0;
+  thrust::transform_iterator<IsOne, const uint8_t*, bool> one(nullptr, IsOne{});
+  cub::DeviceSelect::Flagged(nullptr, f, (const Act*)nullptr, one, (Act*)nullptr, (uint32_t*)nullptr, n1);
+  thrust::transform_iterator<IsFour, const uint8_t*, bool> four(nullptr, IsFour{});
+  cub::DeviceSelect::Flagged(nullptr, g, (const Act*)nullptr, four, (Act*)nullptr, (uint32_t*)nullptr, n1);
+  f = std::max(f, g);
+  size_t h2 = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, h2, (const int32_t*)nullptr, (int32_t*)nullptr, (const Cont*)nullptr,
+                                  (Cont*)nullptr, n1, 0, 32);
+  f = std::max(f, h2);
+  return std::max(std::max(std::max(a, f), std::max(b, c)), std::max(d, e)) + 256;
 }
 
 // carve the workspace; returns bytes needed
@@ -1484,7 +1768,7 @@ kdb_status kdb_mst(const kdb_graph* g, float eps, const uint32_t* core_bits, int
     RoundCounters hc;
     KDB_CUDA(cudaMemcpyAsync(&hc, R.ctr, sizeof(hc), cudaMemcpyDeviceToHost, st));
     KDB_CUDA(cudaStreamSynchronize(st));
-    R.n_act = hc.n_act[0];
+    R.n_act = hc.n_act[0];  // initial active rows are all awake
     R.n_in_act = hc.n_act[1];
   }
   KDB_CUDA(cudaEventRecord(ev[2], st));
@@ -1508,47 +1792,39 @@ kdb_status kdb_mst(const kdb_graph* g, float eps, const uint32_t* core_bits, int
     for (auto& R : L.ranks) {
       KDB_CUDA(cudaMemsetAsync(&R.ctr->n_act[0], 0, 3 * sizeof(uint32_t), st));  // n_act[0..1], n_off
       R.n_slots = 0;
-      if (R.n_act) {
-        const uint32_t n_in = R.n_act;
+      // one list of live rows in row order; a flag in each record marks asleep rows
+      const uint32_t n_in = R.n_act;
+      if (n_in) {
         if (direct) {
           LAUNCH(k_offer_first, grid_for(n_in), kThreads, st, R.nbr, R.dist, k, eps, R.row_begin, N, core_bits,
                  L.all_core, comp, R.act[cur], n_in, R.status, R.Kc, R.Bc, R.tgt, &L.ctr->entries);
         } else {
-          // slot chunks: all threads finish a chunk before the next starts, which
-          // keeps the rows (and hence the comp[] window) in flight narrow
+          // pass A: the first chunk of every awake row
           for (uint32_t s0 = 0; s0 < n_in; s0 += g_chunk) {
             const uint32_t s1 = std::min<uint32_t>(s0 + g_chunk, n_in);
             if ((k % 4) == 0)
               LAUNCH(k_offer_rows_t<true>, grid_for(s1 - s0), kThreads, st, R.nbr, R.dist, k, eps, R.row_begin, N,
-                     core_bits, L.all_core, comp, R.act[cur], s0, s1, R.status, R.off_key, R.off_b, R.cand,
-                     (unsigned long long*)R.Kc, &L.ctr->entries);
+                     core_bits, L.all_core, comp, R.act[cur], s0, s1, R.status, R.off_key, R.off_b, nullptr,
+                     (unsigned long long*)R.Kc, &L.ctr->entries, g_qmax);
             else
               LAUNCH(k_offer_rows_t<false>, grid_for(s1 - s0), kThreads, st, R.nbr, R.dist, k, eps, R.row_begin, N,
-                     core_bits, L.all_core, comp, R.act[cur], s0, s1, R.status, R.off_key, R.off_b, R.cand,
-                     (unsigned long long*)R.Kc, &L.ctr->entries);
+                     core_bits, L.all_core, comp, R.act[cur], s0, s1, R.status, R.off_key, R.off_b, nullptr,
+                     (unsigned long long*)R.Kc, &L.ctr->entries, g_qmax);
           }
-          // rows still skipping dead entries -> warp-per-row scan (stable order)
-          cb = L.cub_bytes;
-          {
-            LaunchScope ls_("cub::DeviceSelect", st, false);
-            thrust::transform_iterator<IsTwo, const uint8_t*, bool> two(R.status, IsTwo{});
-            KDB_CUDA(cub::DeviceSelect::Flagged(L.cub_tmp, cb, R.cand, two, R.cont, &R.ctr->n_cont, (int)n_in, st));
-          }
-          uint32_t ncont = 0;
-          KDB_CUDA(cudaMemcpyAsync(&ncont, &R.ctr->n_cont, 4, cudaMemcpyDeviceToHost, st));
-          KDB_CUDA(cudaStreamSynchronize(st));
-          for (uint32_t q0 = 0; q0 < ncont; q0 += g_chunk_w) {
-            const uint32_t q1 = std::min<uint32_t>(q0 + g_chunk_w, ncont);
-            LAUNCH(k_offer_warp, grid_for((int64_t)(q1 - q0) * 32), kThreads, st, R.nbr, R.dist, k, eps, R.row_begin,
-                   N, core_bits, L.all_core, comp, R.cont, &R.ctr->n_cont, q0, q1, R.act[cur], R.status, R.off_key,
-                   R.off_b, (unsigned long long*)R.Kc, &L.ctr->entries);
-          }
+          // lazy Boruvka + scans of the rows that might supply their component's minimum
+          KDB_CUDA(cudaMemsetAsync(&R.ctr->n_cont, 0, sizeof(uint32_t), st));
+          LAUNCH(k_scan_tiles, grid_for((int64_t)n_in), kThreads, st, R.nbr, R.dist, k, eps, R.row_begin, N,
+                 core_bits, L.all_core, comp, R.act[cur], n_in, R.status, R.off_key, R.off_b,
+                 (unsigned long long*)R.Kc, g_lazy, &L.ctr->entries, &R.ctr->n_cont, g_fa, g_fs);
         }
-        // next active list: rows that offered this round (order preserved)
+        // next list: rows that offered (awake) or were deferred (asleep), row order kept
         cb = L.cub_bytes;
-        { LaunchScope ls_("cub::DeviceSelect", st, false);
-          KDB_CUDA(cub::DeviceSelect::Flagged(L.cub_tmp, cb, R.act[cur], R.status, R.act[cur ^ 1],
-                                              &R.ctr->n_act[0], (int)n_in, st)); }
+        {
+          LaunchScope ls_("cub::DeviceSelect", st, false);
+          thrust::transform_iterator<Survives, const uint8_t*, bool> keep(R.status, Survives{});
+          KDB_CUDA(cub::DeviceSelect::Flagged(L.cub_tmp, cb, R.act[cur], keep, R.act[cur ^ 1], &R.ctr->n_act[0],
+                                              (int)n_in, st));
+        }
         R.n_slots = direct ? 0 : n_in;
       }
       if (general && R.n_in_act)
@@ -1557,13 +1833,27 @@ kdb_status kdb_mst(const kdb_graph* g, float eps, const uint32_t* core_bits, int
                R.off_key + R.off_cap_rows, R.off_b + R.off_cap_rows, &R.ctr->n_off, (unsigned long long*)R.Kc);
       KDB_CUDA(cudaGetLastError());
     }
+    if (g_trace) {
+      RoundCounters h0, hr;
+      KDB_CUDA(cudaMemcpyAsync(&h0, L.ctr, sizeof(h0), cudaMemcpyDeviceToHost, st));
+      KDB_CUDA(cudaMemcpyAsync(&hr, L.ranks[0].ctr, sizeof(hr), cudaMemcpyDeviceToHost, st));
+      KDB_CUDA(cudaEventRecord(ev[3], st));
+      KDB_CUDA(cudaEventSynchronize(ev[3]));
+      float tms = 0;
+      KDB_CUDA(cudaEventElapsedTime(&tms, ev[0], ev[3]));
+      static unsigned long long last_entries = 0;
+      if (rounds == 1) last_entries = 0;
+      fprintf(stderr, "[kdb] round %d C=%lld live=%u scanned=%u -> live=%u entries=%llu offer_ms=%.3f\n",
+              rounds, (long long)C, L.ranks[0].n_act, hr.n_cont, hr.n_act[0], h0.entries - last_entries, tms);
+      last_entries = h0.entries;
+    }
     for (auto& R : L.ranks) {
       RoundCounters hc;
       KDB_CUDA(cudaMemcpyAsync(&hc, R.ctr, sizeof(hc), cudaMemcpyDeviceToHost, st));
       KDB_CUDA(cudaStreamSynchronize(st));
       R.n_act = hc.n_act[0];
       R.n_in_act = hc.n_act[1];
-      R.n_off = hc.n_off;  // in-list offers; row offers are the first n_act slots
+      R.n_off = hc.n_off;  // in-list offers (row offers live in the row slots)
     }
     // exchange: sim -> min over virtual ranks; nccl -> allreduce
     for (size_t r = 1; r < L.ranks.size(); ++r)
@@ -1612,15 +1902,15 @@ kdb_status kdb_mst(const kdb_graph* g, float eps, const uint32_t* core_bits, int
         LAUNCH(k_fill_comp_arrays, grid_for(C), kThreads, st, C, L.ranks[r].Kc, L.ranks[r].Bc, nullptr);
       for (auto& R : L.ranks)
         if (R.n_rows)
-          LAUNCH(k_sweep, grid_for(R.n_act), kThreads, st, R.nbr, R.dist, k, eps, R.row_begin, N, core_bits, comp,
-                 R.act[cur ^ 1], R.n_act, (unsigned long long*)R.Kc, R.Bc, 0);
+          LAUNCH(k_sweep, grid_for(R.n_act), kThreads, st, R.nbr, R.dist, k, eps, R.row_begin, N, core_bits,
+                 comp, R.act[cur ^ 1], R.n_act, (unsigned long long*)R.Kc, R.Bc, 0);
       for (size_t r = 1; r < L.ranks.size(); ++r)
         LAUNCH(k_min_into_u64, grid_for(C), kThreads, st, L.Kc, L.ranks[r].Kc, C);
       KDB_TRY(allreduce_min_u64(comm, L.Kc, C, st));
       for (auto& R : L.ranks)
         if (R.n_rows)
-          LAUNCH(k_sweep, grid_for(R.n_act), kThreads, st, R.nbr, R.dist, k, eps, R.row_begin, N, core_bits, comp,
-                 R.act[cur ^ 1], R.n_act, (unsigned long long*)L.Kc, R.Bc, 1);
+          LAUNCH(k_sweep, grid_for(R.n_act), kThreads, st, R.nbr, R.dist, k, eps, R.row_begin, N, core_bits,
+                 comp, R.act[cur ^ 1], R.n_act, (unsigned long long*)L.Kc, R.Bc, 1);
       for (size_t r = 1; r < L.ranks.size(); ++r)
         LAUNCH(k_min_into_u32, grid_for(C), kThreads, st, L.Bc, L.ranks[r].Bc, C);
       KDB_TRY(allreduce_min_u32(comm, L.Bc, C, st));
