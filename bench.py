@@ -326,7 +326,10 @@ def run_ours(args):
                 "mst": {"edges": msf_count, "weight": msf_weight, "clusters": n_clusters,
                         "rounds": stats[-1]["rounds"], "stall_rounds": stats[-1]["stall_rounds"],
                         "phase_ms": {k_: stats[-1][k_] for k_ in
-                                     ("init_ms", "min_edges_ms", "contract_ms", "finalize_ms")}}}
+                                     ("init_ms", "min_edges_ms", "contract_ms", "filter_ms", "heavy_ms",
+                                      "finalize_ms")},
+                        "filter": {k_: stats[-1][k_] for k_ in
+                                   ("tau", "light_components", "survivors", "heavy_rounds", "fallback")}}}
         emit(line, args)
     if comm is not None:
         comm.close()

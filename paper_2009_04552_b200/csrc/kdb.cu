@@ -56,7 +56,7 @@
 namespace {
 
 thread_local std::string g_err;
-thread_local double g_stats[8];
+thread_local double g_stats[16];
 
 kdb_status set_err(kdb_status s, const char* fmt, ...) {
   char buf[512];
@@ -145,14 +145,11 @@ struct Prof {
 };
 Prof g_prof;
 const int g_trace = getenv("KDB_TRACE") ? atoi(getenv("KDB_TRACE")) : 0;  // per-round log to stderr
-const int g_sortcont = getenv("KDB_SORTCONT") ? atoi(getenv("KDB_SORTCONT")) : 0;
-const int g_lines = getenv("KDB_LINES") ? atoi(getenv("KDB_LINES")) : 4;
 const int g_fa = getenv("KDB_FA") ? atoi(getenv("KDB_FA")) : 1;  // first block lines, awake rows
 const int g_fs = getenv("KDB_FS") ? atoi(getenv("KDB_FS")) : 4;  // first block lines, woken rows
 const int g_lazy = getenv("KDB_LAZY") ? atoi(getenv("KDB_LAZY")) : 1;
 const int g_qmax = getenv("KDB_QMAX") ? atoi(getenv("KDB_QMAX")) : 1;
 const uint32_t g_chunk = getenv("KDB_CHUNK") ? (uint32_t)atoi(getenv("KDB_CHUNK")) : (1u << 30);
-const uint32_t g_chunk_w = getenv("KDB_CHUNKW") ? (uint32_t)atoi(getenv("KDB_CHUNKW")) : (1u << 30);
 
 struct LaunchScope {
   const char* name;
@@ -352,44 +349,43 @@ __global__ void k_fill_comp_arrays(int64_t C, uint64_t* __restrict__ Kc, uint32_
 }
 
 // ---------------------------------------------------------------------------
-// Active-row records.  The scan position L[i] travels with the
-// row id through the active lists, so a row's state arrives in one coalesced
-// 8-byte load instead of a chain of dependent gathers.
-struct Act {
-  int32_t v;   // global row id
-  int32_t h;   // head: every entry before it is dead for good
-  float lb;    // asleep rows: every live entry at/after h weighs >= lb
-  int32_t asleep;  // 1: deferred -- skipped by pass A, only wake-checked
+// ---------------------------------------------------------------------------
+// Active rows and offers.  The scan position L[i] travels with
+// the row id: one coalesced 8-byte record per live row.  Every entry before h is
+// dead for good -- not a candidate, or intra-component (components only merge).
+struct Rec {
+  int32_t v;  // global row id
+  int32_t h;  // head
 };
-// continuation record: everything k_offer_warp needs, written by k_offer_rows_t
-struct Cont {
-  int32_t v, h, cv, s;  // row, head, its component, slot in the active list
+// one row's (or in-list's) minimum leaving edge: its component, the key's b, the key
+struct Offer {
+  int32_t c;
+  uint32_t b;
+  uint64_t key;
 };
 
-// local rows: certificate bound kth'(v) into kmin[comp v], active list (v, head 0)
+// local rows: certificate bound kth'(v) into kmin[comp v] (exact mode); the
+// active list holds the core rows whose first entry is within eps (a row
+// starting beyond it offers nothing, ever).  comp[v] >= 0 <=> v is core.
 __global__ void k_init_rows(const float* __restrict__ dist, int64_t n_rows, int32_t k, float eps,
-                            int64_t row_begin, const uint32_t* __restrict__ bits,
-                            const int32_t* __restrict__ comp, uint32_t* __restrict__ kmin,
-                            Act* __restrict__ active, uint8_t* __restrict__ flag) {
-  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n_rows;
-       base += (int64_t)gridDim.x * blockDim.x) {
+                            int64_t row_begin, const int32_t* __restrict__ comp, uint32_t* __restrict__ kmin,
+                            Rec* __restrict__ act, uint32_t* __restrict__ n_act) {
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n_rows; base += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = base + threadIdx.x;
+    const int64_t v = row_begin + i;
     bool want = false;
-    int64_t v = row_begin + i;
     if (i < n_rows) {
-      if (is_core(bits, v)) {
-        // a row whose first entry is already beyond eps offers nothing, ever
+      const int32_t cv = comp[v];
+      if (cv >= 0) {
         want = __ldcs(dist + i * k) <= eps;
         if (kmin) {
           const float kth = __ldcs(dist + i * k + (k - 1));
-          kmin[comp[v]] = (kth <= eps) ? mono_bits(kth) : kInfBits;
+          kmin[cv] = (kth <= eps) ? mono_bits(kth) : kInfBits;
         }
       }
     }
-    if (i < n_rows) {
-      active[i] = Act{(int32_t)v, 0, 0.f, 0};  // awake
-      flag[i] = want ? 1 : 0;
-    }
+    const uint32_t slot = block_reserve(n_act, want);
+    if (want) act[slot] = Rec{(int32_t)v, 0};
   }
 }
 
@@ -451,31 +447,20 @@ __global__ void k_in_finish(const unsigned long long* __restrict__ off, int64_t 
   }
 }
 
+
 // ============================================================================
 // a3: per-vertex minimum leaving entry (rows)
 // ============================================================================
 // For vertex v the incident edges of its row are ordered, under O1 with v fixed,
 // by (mono(w), far id) (reading #6).  Rows are sorted by w, so the first entry
-// (after skipping permanently dead entries) whose far endpoint lies in another
-// component opens the minimum group; equal-weight entries after it may carry a
-// smaller far id and are scanned too.  The head pointer only passes entries
-// that can never become leaving again (non-candidates, intra-component).
-//
-__device__ __forceinline__ bool cand_entry(int64_t J, int64_t v, int64_t N, const uint32_t* bits, bool all_core) {
-  return J >= 0 && J < N && J != v && (all_core || is_core(bits, J));
-}
-
-// One thread per active row; each step takes an aligned 4-entry chunk (int4
-// ids + float4 weights when k % 4 == 0, loaded evict-first so the streamed
-// graph does not push comp[] out of L2) and issues its 4 component gathers
-// together.  A thread gives up after qmax chunks of dead entries (the chunk
-// count per row varies 1..k/4 inside a warp); the row then continues in
-// k_offer_warp, 32 entries per step.
-
+// at/after the head whose far endpoint lies in another component opens the
+// minimum group; equal-weight entries after it may carry a smaller far id and
+// are examined too.  The head only passes entries that can never leave again.
+// comp[J] < 0 marks non-core J (not a candidate); J == v gives comp[J] == comp[v].
 template <bool VEC>
 __device__ __forceinline__ void load_chunk(const int32_t* nr, const float* dr, int c0, int k, int32_t (&J)[4],
                                            float (&w)[4]) {
-  if (VEC && c0 + 3 < k) {
+  if (VEC) {  // k % 4 == 0: an aligned 4-chunk never straddles the row end
     const int4 j4 = __ldcs(reinterpret_cast<const int4*>(nr + c0));
     const float4 w4 = __ldcs(reinterpret_cast<const float4*>(dr + c0));
     J[0] = j4.x; J[1] = j4.y; J[2] = j4.z; J[3] = j4.w;
@@ -490,498 +475,329 @@ __device__ __forceinline__ void load_chunk(const int32_t* nr, const float* dr, i
   }
 }
 
-template <bool VEC>
-__global__ void __launch_bounds__(256) k_offer_rows_t(
-    const int32_t* __restrict__ nbr, const float* __restrict__ dist, int32_t k, float eps, int64_t row_begin,
-    int64_t N, const uint32_t* __restrict__ bits, int all_core, const int32_t* __restrict__ comp,
-    Act* __restrict__ act, uint32_t s_begin, uint32_t s_end, uint8_t* __restrict__ status,
-    uint64_t* __restrict__ off_key, uint32_t* __restrict__ off_b, Cont* __restrict__ cand,
-    unsigned long long* __restrict__ Kc, unsigned long long* __restrict__ n_entries, int qmax) {
-  unsigned long long reads = 0;
-  for (uint32_t s = s_begin + blockIdx.x * blockDim.x + threadIdx.x; s < s_end; s += gridDim.x * blockDim.x) {
-    bool found = false, more = false;
-    uint64_t best = kSent;
-    uint32_t bestb = kSentB;
-    const int4 a = __ldcs(reinterpret_cast<const int4*>(act + s));
-    if (a.w) continue;  // asleep: k_wake decides
-    const int32_t v = a.x;
-    int h = a.y;
-    const int64_t i = (int64_t)v - row_begin;
-    const int32_t* nr = nbr + i * k;
-    const float* dr = dist + i * k;
-    const int32_t cv = gat(comp + v);
-    int c0 = h & ~3;
-    float wstar = 0.f, wlast = 0.f;  // wlast: weight of the last dead entry passed
-    bool done = false;
-    int steps = 0;
-    while (!done && c0 < k) {
-      if (!found && steps == qmax) {  // hand the rest of the dead run to a warp
-        more = true;
-        break;
-      }
-      ++steps;
-      int32_t J[4];
-      float w[4];
-      load_chunk<VEC>(nr, dr, c0, k, J, w);
-      int32_t cj[4];
+struct RowScan {
+  bool found;
+  int h;          // new head: the first leaving entry, or k when exhausted
+  uint64_t best;  // minimum key of the group
+  uint32_t bestb;
+  int32_t bestc;  // component of the best entry's far endpoint
+};
+
+// Scan row (nr, dr) of vertex v (component cv) from head h.  direct: singleton
+// components (round 1, exact mode) -- every candidate leaves; with all_core the
+// dense component id of a vertex is the vertex itself (no gathers at all).
+template <bool VEC, bool DIRECT>
+__device__ __forceinline__ RowScan scan_row(const int32_t* __restrict__ nr, const float* __restrict__ dr, int k,
+                                            float eps, int32_t v, int32_t cv, int h, int64_t N,
+                                            const int32_t* __restrict__ comp, int all_core,
+                                            unsigned long long& reads) {
+  RowScan r{false, k, kSent, kSentB, -1};
+  float wstar = 0.f;
+  int c0 = h & ~3;
+  bool done = false;
+  while (!done && c0 < k) {
+    int32_t J[4];
+    float w[4];
+    load_chunk<VEC>(nr, dr, c0, k, J, w);
+    int32_t cj[4];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const bool ok = c0 + j >= h && w[j] <= eps && cand_entry(J[j], v, N, bits, all_core);
-        cj[j] = ok ? gat(comp + J[j]) : -2;  // -2: not a candidate (dead for good)
-      }
-      reads += (unsigned long long)(min(c0 + 4, k) - max(c0, h));
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int idx = c0 + j;
-        if (done || idx < h || idx >= k) continue;
-        if (!found) {
-          if (!(w[j] <= eps)) { h = k; done = true; continue; }  // sorted: nothing left
-          if (cj[j] == -2 || cj[j] == cv) { h = idx + 1; wlast = w[j]; continue; }  // dead entry
-          found = true;  // first leaving entry opens the minimum group
-          h = idx;
-          wstar = w[j];
-          best = pack_key(mono_bits(w[j]), (uint32_t)min((int64_t)v, (int64_t)J[j]));
-          bestb = (uint32_t)max((int64_t)v, (int64_t)J[j]);
-        } else {
-          if (w[j] != wstar) { done = true; continue; }
-          if (cj[j] == -2 || cj[j] == cv) continue;
-          const uint64_t kk = pack_key(mono_bits(w[j]), (uint32_t)min((int64_t)v, (int64_t)J[j]));
-          const uint32_t bb = (uint32_t)max((int64_t)v, (int64_t)J[j]);
-          if (kk < best || (kk == best && bb < bestb)) { best = kk; bestb = bb; }
-        }
-      }
-      c0 += 4;
+    for (int j = 0; j < 4; ++j) {
+      const int idx = c0 + j;
+      const bool cand = idx >= h && idx < k && w[j] <= eps && J[j] >= 0 && J[j] < N && J[j] != v;
+      cj[j] = cand ? ((DIRECT && all_core) ? J[j] : gat(comp + J[j])) : -1;
     }
-    h = min(h, k);
-    act[s].h = h;
-    __stcs(status + s, (uint8_t)(found ? 1 : (more ? 2 : 0)));  // 1 offer, 2 continue, 0 exhausted
-    if (found) {
-      __stcs(reinterpret_cast<unsigned long long*>(off_key) + s, (unsigned long long)best);
-      __stcs(off_b + s, bestb);
-      atomicMin(Kc + cv, (unsigned long long)best);
-    } else if (more) {
-      if (cand) __stcs(reinterpret_cast<int4*>(cand + s), make_int4(v, h, cv, (int)s));
-      act[s].lb = wlast;  // every leaving entry still ahead weighs >= wlast (rows are sorted)
+    reads += (unsigned long long)(min(c0 + 4, k) - max(c0, h));
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int idx = c0 + j;
+      if (done || idx < h || idx >= k) continue;
+      const bool leaving = cj[j] >= 0 && (DIRECT || cj[j] != cv);
+      if (!r.found) {
+        if (!(w[j] <= eps)) { r.h = k; done = true; continue; }  // sorted: nothing left
+        if (!leaving) { h = idx + 1; continue; }                   // dead entry
+        r.found = true;
+        r.h = idx;
+        wstar = w[j];
+        r.best = pack_key(mono_bits(w[j]), (uint32_t)min(v, J[j]));
+        r.bestb = (uint32_t)max(v, J[j]);
+        r.bestc = cj[j];
+      } else {
+        if (w[j] != wstar) { done = true; continue; }
+        if (!leaving) continue;
+        const uint64_t kk = pack_key(mono_bits(w[j]), (uint32_t)min(v, J[j]));
+        const uint32_t bb = (uint32_t)max(v, J[j]);
+        if (kk < r.best || (kk == r.best && bb < r.bestb)) { r.best = kk; r.bestb = bb; r.bestc = cj[j]; }
+      }
+    }
+    c0 += 4;
+  }
+  if (!r.found) r.h = k;
+  return r;
+}
+
+// Round 1 with singleton components (exact mode): the row's first candidate
+// group IS its component's minimum -- no atomics and no tie pass; the owner
+// writes Kc, Bc and the hook target directly.  Rows that offered stay active.
+template <bool VEC>
+__global__ void __launch_bounds__(256) k_offer_first(const int32_t* __restrict__ nbr, const float* __restrict__ dist,
+                                                     int32_t k, float eps, int64_t row_begin, int64_t N,
+                                                     const int32_t* __restrict__ comp, int all_core,
+                                                     const Rec* __restrict__ act, uint32_t n_in,
+                                                     Rec* __restrict__ act_out, uint32_t* __restrict__ n_out,
+                                                     uint64_t* __restrict__ Kc, uint32_t* __restrict__ Bc,
+                                                     int32_t* __restrict__ tgt, unsigned long long* __restrict__ n_entries) {
+  unsigned long long reads = 0;
+  for (uint32_t base = blockIdx.x * blockDim.x; base < n_in; base += gridDim.x * blockDim.x) {
+    const uint32_t s = base + threadIdx.x;
+    RowScan r{false, 0, kSent, kSentB, -1};
+    int32_t v = -1;
+    if (s < n_in) {
+      const int2 a2 = __ldcs(reinterpret_cast<const int2*>(act + s));
+      const Rec a{a2.x, a2.y};
+      v = a.v;
+      const int64_t i = (int64_t)v - row_begin;
+      r = scan_row<VEC, true>(nbr + i * k, dist + i * k, k, eps, v, -1, a.h, N, comp, all_core, reads);
+      if (r.found) {
+        const int32_t cv = all_core ? v : gat(comp + v);
+        Kc[cv] = r.best;
+        Bc[cv] = r.bestb;
+        tgt[cv] = r.bestc;
+      }
+    }
+    const uint32_t slot = block_reserve(n_out, r.found);
+    if (r.found) act_out[slot] = Rec{v, r.h};
+  }
+  for (int o = 16; o > 0; o >>= 1) reads += __shfl_xor_sync(0xffffffffu, reads, o);
+  if ((threadIdx.x & 31) == 0 && reads) atomicAdd(n_entries, reads);
+}
+
+// Later rounds: one thread per live row; the offer goes to Kc[comp v] by a
+// 64-bit atomicMin (Alg. 3 pwrite, reading #7) and, with the
+// row's next record, to the same slot of the offer list (for the tie pass).
+template <bool VEC>
+__global__ void __launch_bounds__(256) k_offer_round(const int32_t* __restrict__ nbr, const float* __restrict__ dist,
+                                                     int32_t k, float eps, int64_t row_begin, int64_t N,
+                                                     const int32_t* __restrict__ comp, const Rec* __restrict__ act,
+                                                     uint32_t n_in, Rec* __restrict__ act_out,
+                                                     uint32_t* __restrict__ n_out, Offer* __restrict__ offers,
+                                                     unsigned long long* __restrict__ Kc,
+                                                     unsigned long long* __restrict__ n_entries) {
+  unsigned long long reads = 0;
+  for (uint32_t base = blockIdx.x * blockDim.x; base < n_in; base += gridDim.x * blockDim.x) {
+    const uint32_t s = base + threadIdx.x;
+    RowScan r{false, 0, kSent, kSentB, -1};
+    int32_t v = -1, cv = -1;
+    if (s < n_in) {
+      const int2 a2 = __ldcs(reinterpret_cast<const int2*>(act + s));
+      const Rec a{a2.x, a2.y};
+      v = a.v;
+      cv = gat(comp + v);
+      const int64_t i = (int64_t)v - row_begin;
+      r = scan_row<VEC, false>(nbr + i * k, dist + i * k, k, eps, v, cv, a.h, N, comp, 0, reads);
+      if (r.found) atomicMin(Kc + cv, (unsigned long long)r.best);
+    }
+    const uint32_t slot = block_reserve(n_out, r.found);
+    if (r.found) {
+      act_out[slot] = Rec{v, r.h};
+      offers[slot] = Offer{cv, r.bestb, r.best};
     }
   }
   for (int o = 16; o > 0; o >>= 1) reads += __shfl_xor_sync(0xffffffffu, reads, o);
   if ((threadIdx.x & 31) == 0 && reads) atomicAdd(n_entries, reads);
 }
 
-// Continuation: one warp per row.  Lane l takes entries h+l, h+l+32, h+l+64,
-// h+l+96 of a 128-entry block: all id/weight loads and all component gathers
-// of the block are in flight together (no dependency between lines), then the
-// warp reduces (first leaving position, minimum key of the equal-weight group
-// that starts there).  Rows are sorted, so the minimum over the block's
-// leaving entries with the smallest weight IS that group's minimum; only when a
-// group reaches the end of the block does the next block have to be looked at.
-template <int kLines>
-__global__ void __launch_bounds__(256) k_offer_warp(
-    const int32_t* __restrict__ nbr, const float* __restrict__ dist, int32_t k, float eps, int64_t row_begin,
-    int64_t N, const uint32_t* __restrict__ bits, int all_core, const int32_t* __restrict__ comp,
-    const Cont* __restrict__ cont, const uint32_t* __restrict__ n_cont_p, uint32_t q_begin, uint32_t q_end,
-    Act* __restrict__ act, uint8_t* __restrict__ status, uint64_t* __restrict__ off_key,
-    uint32_t* __restrict__ off_b, unsigned long long* __restrict__ Kc, unsigned long long* __restrict__ n_entries) {
-  const int lane = threadIdx.x & 31;
-  const uint32_t n_cont = min(*n_cont_p, q_end);
-  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
-  unsigned long long reads = 0;
-  uint32_t q = q_begin + ((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
-  int4 rec = make_int4(0, 0, 0, 0);
-  if (q < n_cont) rec = __ldcs(reinterpret_cast<const int4*>(cont + q));
-  for (; q < n_cont; q += nwarps) {
-    const int32_t v = rec.x, cv = rec.z, s = rec.w;
-    const int h0 = rec.y;
-    if (q + nwarps < n_cont) rec = __ldcs(reinterpret_cast<const int4*>(cont + q + nwarps));
-    const int64_t i = (int64_t)v - row_begin;
-    const int32_t* nr = nbr + i * k;
-    const float* dr = dist + i * k;
-    int pos = k;              // first leaving position found so far
-    uint32_t wbest = 0xffffffffu;  // its weight bits
-    uint64_t best = kSent;
-    uint32_t bestb = kSentB;
-    int base = h0;
-    bool stop = false;
-    while (!stop && base < k) {
-      float w[kLines];
-      int32_t J[kLines];
+// ---------------------------------------------------------------------------
+// Light ELL.  A random visit of a 400-byte-strided graph row is expensive
+// (scattered sectors, HBM row activations), so the first kW columns of every
+// core row are copied ONCE into a dense, 128-byte-aligned ELL of (J, w bits)
+// pairs and every Boruvka round reads that instead.  Rows whose candidate
+// prefix (w <= eps_run) runs past column kW continue in the graph row itself.
+constexpr int kW = 16;
+
+// one thread per row: 4 x (int4 + float4) loads in flight, 8 x int4 stores;
+// exact mode also writes the certificate bound kth'(v) into kmin[comp v]
+template <bool VEC>
+__global__ void __launch_bounds__(256) k_light_ell(const int32_t* __restrict__ nbr, const float* __restrict__ dist,
+                                                   int64_t n_rows, int32_t k, float eps, int64_t row_begin,
+                                                   const int32_t* __restrict__ comp, uint32_t* __restrict__ kmin,
+                                                   int4* __restrict__ LE, Rec* __restrict__ act,
+                                                   uint32_t* __restrict__ n_act) {
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n_rows; base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = base + threadIdx.x;
+    bool want = false;
+    const int64_t v = row_begin + i;
+    if (i < n_rows) {
+      const int32_t cv = comp[v];
+      if (cv >= 0) {
+        const int32_t* nr = nbr + i * k;
+        const float* dr = dist + i * k;
+        int32_t J[kW];
+        float w[kW];
+        if (VEC && k >= kW) {
 #pragma unroll
-      for (int t = 0; t < kLines; ++t) {
-        const int c = base + lane + 32 * t;
-        w[t] = c < k ? __ldcs(dr + c) : __int_as_float(0x7f800000);
-        J[t] = c < k ? __ldcs(nr + c) : -1;
-      }
-      int32_t cj[kLines];
-#pragma unroll
-      for (int t = 0; t < kLines; ++t)
-        cj[t] = (w[t] <= eps && cand_entry(J[t], v, N, bits, all_core)) ? gat(comp + J[t]) : cv;
-      bool beyond = false;
-      unsigned lp = (unsigned)k;  // this lane's first leaving position in the block
-#pragma unroll
-      for (int t = kLines - 1; t >= 0; --t) {
-        const int c = base + lane + 32 * t;
-        if (c < k && !(w[t] <= eps)) beyond = true;
-        if (cj[t] != cv) lp = (unsigned)c;
-      }
-      lp = __reduce_min_sync(0xffffffffu, lp);  // the block's first leaving position
-      if ((int)lp < k) {
-        if (pos == k) {  // first leaving entry of the row: its weight opens the group
-          const int rel = (int)lp - base;
-          float wl = 0.f;
-#pragma unroll
-          for (int t = 0; t < kLines; ++t) {
-            const float x = __shfl_sync(0xffffffffu, w[t], rel & 31);
-            if ((rel >> 5) == t) wl = x;
+          for (int q = 0; q < kW / 4; ++q) {
+            const int4 j4 = __ldcs(reinterpret_cast<const int4*>(nr + 4 * q));
+            const float4 w4 = __ldcs(reinterpret_cast<const float4*>(dr + 4 * q));
+            J[4 * q] = j4.x; J[4 * q + 1] = j4.y; J[4 * q + 2] = j4.z; J[4 * q + 3] = j4.w;
+            w[4 * q] = w4.x; w[4 * q + 1] = w4.y; w[4 * q + 2] = w4.z; w[4 * q + 3] = w4.w;
           }
-          pos = (int)lp;
-          wbest = mono_bits(wl);
-        }
-        // group members in this block: leaving entries of weight wbest; their key's
-        // weight part is equal, so the minimum is over (a, b) as two 32-bit mins
-        uint32_t am = 0xffffffffu, bm = 0xffffffffu;
+        } else {
 #pragma unroll
-        for (int t = 0; t < kLines; ++t) {
-          const int c = base + lane + 32 * t;
-          if (c < k && cj[t] != cv && mono_bits(w[t]) == wbest) {
-            const uint32_t a2 = (uint32_t)min((int64_t)v, (int64_t)J[t]);
-            const uint32_t b2 = (uint32_t)max((int64_t)v, (int64_t)J[t]);
-            if (a2 < am || (a2 == am && b2 < bm)) { am = a2; bm = b2; }
+          for (int c = 0; c < kW; ++c) {
+            J[c] = c < k ? __ldcs(nr + c) : -1;
+            w[c] = c < k ? __ldcs(dr + c) : __int_as_float(0x7f800000);
           }
         }
-        const uint32_t amin = __reduce_min_sync(0xffffffffu, am);
-        const uint32_t bmin = __reduce_min_sync(0xffffffffu, am == amin ? bm : 0xffffffffu);
-        const uint64_t kk = pack_key(wbest, amin);
-        if (amin != 0xffffffffu && (kk < best || (kk == best && bmin < bestb))) { best = kk; bestb = bmin; }
-      }
-      bool tail_eq = false;  // an entry of weight wbest sits at the block end
-      if (pos < k) {
-        const int c = base + lane + 32 * (kLines - 1);
-        tail_eq = lane == 31 && c < k && w[kLines - 1] <= eps && mono_bits(w[kLines - 1]) == wbest;
-      }
-      if (lane == 0) reads += (unsigned long long)(min(base + 32 * kLines, k) - base);
-      const bool any_beyond = __any_sync(0xffffffffu, beyond);
-      const bool tail = __any_sync(0xffffffffu, tail_eq);
-      // stop once a leaving entry was found (unless its group reaches the block
-      // end) or the weights passed eps (sorted rows: nothing after)
-      stop = any_beyond || (pos < k && !tail);
-      base += 32 * kLines;
-    }
-    if (lane == 0) {
-      const bool found = best != kSent;
-      act[s].h = found ? pos : k;
-      status[s] = found ? 1 : 0;
-      if (found) {
-        off_key[s] = best;
-        off_b[s] = bestb;
-        atomicMin(Kc + cv, (unsigned long long)best);
+        if (kmin) {
+          const float kth = __ldcs(dr + (k - 1));
+          kmin[cv] = (kth <= eps) ? mono_bits(kth) : kInfBits;
+        }
+        want = w[0] <= eps;
+        int4* o = LE + i * (kW / 2);
+#pragma unroll
+        for (int q = 0; q < kW / 2; ++q)
+          __stcg(o + q, make_int4(J[2 * q], __float_as_int(w[2 * q]), J[2 * q + 1], __float_as_int(w[2 * q + 1])));
       }
     }
+    const uint32_t slot = block_reserve(n_act, want);
+    if (want) act[slot] = Rec{(int32_t)v, 0};
   }
-  for (int o = 16; o > 0; o >>= 1) reads += __shfl_xor_sync(0xffffffffu, reads, o);
-  if (lane == 0 && reads) atomicAdd(n_entries, reads);
 }
 
-// One warp scans the remaining entries of row v from head h0 (all 32 lanes,
-// the whole warp must call it).  Lane l takes entries base+l, base+l+32, ...:
-// the first block is one 32-entry line (most rows leave early), later blocks
-// are 128 entries with all id/weight loads and component gathers in flight
-// together.  Returns (found, first leaving position, minimum key and b of the
-// equal-weight group that starts there); rows are sorted, so that group's
-// minimum is the row's minimum leaving edge under O1.
-struct RowMin {
-  bool found;
-  int pos;
-  uint64_t key;
-  uint32_t b;
-};
-
-__device__ __forceinline__ RowMin warp_scan_row(const int32_t* __restrict__ nr, const float* __restrict__ dr, int k,
-                                                float eps, int32_t v, int32_t cv, int h0, int64_t N,
-                                                const uint32_t* __restrict__ bits, int all_core,
-                                                const int32_t* __restrict__ comp, unsigned long long& reads,
-                                                int first_lines) {
-  constexpr int kL = 4;
-  const int lane = threadIdx.x & 31;
-  int pos = k;
-  uint32_t wbest = 0xffffffffu;
-  uint64_t best = kSent;
-  uint32_t bestb = kSentB;
-  int base = h0;
-  int lines = first_lines;
-  bool stop = false;
-  while (!stop && base < k) {
-    const int bend = min(base + 32 * lines, k);  // block = [base, bend)
-    float w[kL];
-    int32_t J[kL];
+// Scan row v (component cv) from head h: columns < kW from the ELL row, the
+// rest (rare: a candidate prefix longer than kW) from the graph row.  DIRECT:
+// singleton components (round 1, exact mode), every candidate leaves; with
+// all_core a vertex's dense component id is the vertex itself (no gathers).
+template <bool DIRECT>
+__device__ __forceinline__ RowScan scan_ell(const int4* __restrict__ le, const int32_t* __restrict__ nr,
+                                            const float* __restrict__ dr, int k, float eps, int32_t v, int32_t cv,
+                                            int h, int64_t N, const int32_t* __restrict__ comp, int all_core,
+                                            unsigned long long& reads) {
+  RowScan r{false, k, kSent, kSentB, -1};
+  uint32_t wstar = 0;
+  const int kend = min(k, kW);
+  int c0 = h & ~3;
+  bool done = false;
+  while (!done && c0 < kend) {
+    const int4 p0 = __ldcg(le + (c0 >> 1));
+    const int4 p1 = __ldcg(le + (c0 >> 1) + 1);
+    const int32_t J[4] = {p0.x, p0.z, p1.x, p1.z};
+    const float w[4] = {__int_as_float(p0.y), __int_as_float(p0.w), __int_as_float(p1.y), __int_as_float(p1.w)};
+    int32_t cj[4];
 #pragma unroll
-    for (int t = 0; t < kL; ++t) {
-      const int c = base + lane + 32 * t;
-      const bool in = t < lines && c < bend;
-      w[t] = in ? __ldcs(dr + c) : __int_as_float(0x7f800000);
-      J[t] = in ? __ldcs(nr + c) : -1;
+    for (int j = 0; j < 4; ++j) {
+      const int idx = c0 + j;
+      const bool cand = idx >= h && idx < kend && w[j] <= eps && J[j] >= 0 && J[j] < N && J[j] != v;
+      cj[j] = cand ? ((DIRECT && all_core) ? J[j] : gat(comp + J[j])) : -1;
     }
-    int32_t cj[kL];
+    reads += (unsigned long long)(min(c0 + 4, kend) - max(c0, h));
 #pragma unroll
-    for (int t = 0; t < kL; ++t)
-      cj[t] = (w[t] <= eps && cand_entry(J[t], v, N, bits, all_core)) ? gat(comp + J[t]) : cv;
-    bool beyond = false;
-    unsigned lp = (unsigned)k;
-#pragma unroll
-    for (int t = kL - 1; t >= 0; --t) {
-      const int c = base + lane + 32 * t;
-      if (t < lines && c < bend && !(w[t] <= eps)) beyond = true;
-      if (cj[t] != cv) lp = (unsigned)c;
-    }
-    lp = __reduce_min_sync(0xffffffffu, lp);
-    if ((int)lp < k) {
-      if (pos == k) {
-        const int rel = (int)lp - base;
-        float wl = 0.f;
-#pragma unroll
-        for (int t = 0; t < kL; ++t) {
-          const float x = __shfl_sync(0xffffffffu, w[t], rel & 31);
-          if ((rel >> 5) == t) wl = x;
-        }
-        pos = (int)lp;
-        wbest = mono_bits(wl);
-      }
-      uint32_t am = 0xffffffffu, bm = 0xffffffffu;
-#pragma unroll
-      for (int t = 0; t < kL; ++t) {
-        if (cj[t] != cv && mono_bits(w[t]) == wbest) {
-          const uint32_t a2 = (uint32_t)min((int64_t)v, (int64_t)J[t]);
-          const uint32_t b2 = (uint32_t)max((int64_t)v, (int64_t)J[t]);
-          if (a2 < am || (a2 == am && b2 < bm)) { am = a2; bm = b2; }
-        }
-      }
-      const uint32_t amin = __reduce_min_sync(0xffffffffu, am);
-      const uint32_t bmin = __reduce_min_sync(0xffffffffu, am == amin ? bm : 0xffffffffu);
-      const uint64_t kk = pack_key(wbest, amin);
-      if (amin != 0xffffffffu && (kk < best || (kk == best && bmin < bestb))) { best = kk; bestb = bmin; }
-    }
-    bool tail_eq = false;  // the block's last entry still has the group's weight
-    if (pos < k) {
-      const int last = bend - 1;
-      const int t = (last - base) >> 5;
-      if (lane == ((last - base) & 31)) {
-#pragma unroll
-        for (int u = 0; u < kL; ++u)
-          if (u == t) tail_eq = w[u] <= eps && mono_bits(w[u]) == wbest;
+    for (int j = 0; j < 4; ++j) {
+      const int idx = c0 + j;
+      if (done || idx < h || idx >= kend) continue;
+      const bool leaving = cj[j] >= 0 && (DIRECT || cj[j] != cv);
+      const uint32_t wb = mono_bits(w[j]);
+      if (!r.found) {
+        if (!(w[j] <= eps)) { r.h = k; done = true; continue; }  // sorted: nothing left
+        if (!leaving) { h = idx + 1; continue; }                   // dead entry
+        r.found = true;
+        r.h = idx;
+        wstar = wb;
+        r.best = pack_key(wb, (uint32_t)min(v, J[j]));
+        r.bestb = (uint32_t)max(v, J[j]);
+        r.bestc = cj[j];
+      } else {
+        if (wb != wstar) { done = true; continue; }
+        if (!leaving) continue;
+        const uint64_t kk = pack_key(wb, (uint32_t)min(v, J[j]));
+        const uint32_t bb = (uint32_t)max(v, J[j]);
+        if (kk < r.best || (kk == r.best && bb < r.bestb)) { r.best = kk; r.bestb = bb; r.bestc = cj[j]; }
       }
     }
-    if (lane == 0) reads += (unsigned long long)(bend - base);
-    const bool any_beyond = __any_sync(0xffffffffu, beyond);
-    const bool tail = __any_sync(0xffffffffu, tail_eq);
-    stop = any_beyond || (pos < k && !tail);
-    base = bend;
-    lines = kL;
+    c0 += 4;
   }
-  RowMin r;
-  r.found = best != kSent;
-  r.pos = pos;
-  r.key = best;
-  r.b = bestb;
+  if (!done && k > kW) {
+    // the candidate prefix (or the minimum's tie group) runs past the ELL
+    if (!r.found) {
+      RowScan t = scan_row<false, DIRECT>(nr, dr, k, eps, v, cv, max(h, kW), N, comp, all_core, reads);
+      return t;
+    }
+    // continue the tie group of weight wstar in the graph row
+    for (int c = kW; c < k; ++c) {
+      const float wc = __ldcg(dr + c);
+      if (mono_bits(wc) != wstar || !(wc <= eps)) break;
+      const int32_t Jc = __ldcg(nr + c);
+      ++reads;
+      if (Jc < 0 || Jc >= N || Jc == v) continue;
+      const int32_t cc = (DIRECT && all_core) ? Jc : gat(comp + Jc);
+      if (cc < 0 || (!DIRECT && cc == cv)) continue;
+      const uint64_t kk = pack_key(wstar, (uint32_t)min(v, Jc));
+      const uint32_t bb = (uint32_t)max(v, Jc);
+      if (kk < r.best || (kk == r.best && bb < r.bestb)) { r.best = kk; r.bestb = bb; r.bestc = cc; }
+    }
+  }
+  if (!r.found) r.h = k;
   return r;
 }
 
-// After pass A: one lane per slot of a 32-slot tile decides whether its row
-// must be scanned this round (lazy Boruvka):
-//   awake row with a dead first chunk (status 2): scan unless lb > w(Kc[comp])
-//     -- then it is deferred (asleep) instead;
-//   asleep row: scan (wake) iff lb <= w(Kc[comp]) -- Kc holds an actual
-//     leaving edge of the component, so a row whose live entries all weigh
-//     more cannot supply the minimum.
-// The warp then scans the flagged rows one after another.
-__global__ void __launch_bounds__(256) k_scan_tiles(
-    const int32_t* __restrict__ nbr, const float* __restrict__ dist, int32_t k, float eps, int64_t row_begin,
-    int64_t N, const uint32_t* __restrict__ bits, int all_core, const int32_t* __restrict__ comp,
-    Act* __restrict__ act, uint32_t n, uint8_t* __restrict__ status, uint64_t* __restrict__ off_key,
-    uint32_t* __restrict__ off_b, unsigned long long* __restrict__ Kc, int lazy,
-    unsigned long long* __restrict__ n_entries, uint32_t* __restrict__ n_scanned, int g_first_awake,
-    int g_first_asleep) {
-  const int lane = threadIdx.x & 31;
-  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+// round 1 (exact mode, singletons) over the ELL; see k_offer_first
+__global__ void __launch_bounds__(256) k_light_first(const int4* __restrict__ LE, const int32_t* __restrict__ nbr,
+                                                     const float* __restrict__ dist, int32_t k, float eps,
+                                                     int64_t row_begin, int64_t N, const int32_t* __restrict__ comp,
+                                                     int all_core, const Rec* __restrict__ act, uint32_t n_in,
+                                                     Rec* __restrict__ act_out, uint32_t* __restrict__ n_out,
+                                                     uint64_t* __restrict__ Kc, uint32_t* __restrict__ Bc,
+                                                     int32_t* __restrict__ tgt, unsigned long long* __restrict__ n_entries) {
   unsigned long long reads = 0;
-  uint32_t scanned = 0;
-  for (uint32_t tile = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; tile * 32 < n; tile += nwarps) {
-    const uint32_t s = tile * 32 + lane;
-    bool need = false;
-    int4 r = make_int4(-1, 0, 0, 0);
-    int32_t cv = -1;
-    if (s < n) {
-      r = __ldcs(reinterpret_cast<const int4*>(act + s));
-      const uint8_t st = r.w ? 0xff : status[s];  // 0xff: asleep (pass A skipped it)
-      if (st == 2 || st == 0xff) {
-        cv = gat(comp + r.x);
-        const uint32_t kw = (uint32_t)(gat(Kc + cv) >> 32);  // sentinel -> never deferred
-        const bool over = lazy && mono_bits(__int_as_float(r.z)) > kw;
-        if (over) {  // cannot supply the minimum this round: (stay) asleep
-          status[s] = 4;
-          if (!r.w) act[s].asleep = 1;
-        } else {
-          need = true;
-          if (r.w) act[s].asleep = 0;
-        }
-      }
-    }
-    unsigned m = __ballot_sync(0xffffffffu, need);
-    if (lane == 0) scanned += __popc(m);
-    while (m) {
-      const int src = __ffs(m) - 1;
-      m &= m - 1;
-      const int32_t v = __shfl_sync(0xffffffffu, r.x, src);
-      const int32_t h0 = __shfl_sync(0xffffffffu, r.y, src);
-      const int32_t c = __shfl_sync(0xffffffffu, cv, src);
-      const int32_t was_asleep = __shfl_sync(0xffffffffu, r.w, src);
-      const uint32_t ss = tile * 32 + src;
+  for (uint32_t base = blockIdx.x * blockDim.x; base < n_in; base += gridDim.x * blockDim.x) {
+    const uint32_t s = base + threadIdx.x;
+    RowScan r{false, 0, kSent, kSentB, -1};
+    int32_t v = -1;
+    if (s < n_in) {
+      const int2 a = __ldcs(reinterpret_cast<const int2*>(act + s));
+      v = a.x;
       const int64_t i = (int64_t)v - row_begin;
-      // a woken row's first live entry is usually far away; an awake row's is near
-      const RowMin rm = warp_scan_row(nbr + i * k, dist + i * k, k, eps, v, c, h0, N, bits, all_core, comp, reads,
-                                      was_asleep ? g_first_asleep : g_first_awake);
-      if (lane == 0) {
-        act[ss].h = rm.found ? rm.pos : k;
-        status[ss] = rm.found ? 1 : 0;
-        if (rm.found) {
-          off_key[ss] = rm.key;
-          off_b[ss] = rm.b;
-          atomicMin(Kc + c, (unsigned long long)rm.key);
-        }
+      r = scan_ell<true>(LE + i * (kW / 2), nbr + i * k, dist + i * k, k, eps, v, -1, a.y, N, comp, all_core, reads);
+      if (r.found) {
+        const int32_t cv = all_core ? v : gat(comp + v);
+        Kc[cv] = r.best;
+        Bc[cv] = r.bestb;
+        tgt[cv] = r.bestc;
       }
     }
+    const uint32_t slot = block_reserve(n_out, r.found);
+    if (r.found) act_out[slot] = Rec{v, r.h};
   }
-  for (int o = 16; o > 0; o >>= 1) {
-    reads += __shfl_xor_sync(0xffffffffu, reads, o);
-    scanned += __shfl_xor_sync(0xffffffffu, scanned, o);
-  }
-  if (lane == 0) {
-    if (reads) atomicAdd(n_entries, reads);
-    if (scanned) atomicAdd(n_scanned, scanned);
-  }
+  for (int o = 16; o > 0; o >>= 1) reads += __shfl_xor_sync(0xffffffffu, reads, o);
+  if ((threadIdx.x & 31) == 0 && reads) atomicAdd(n_entries, reads);
 }
 
-struct IsTwo {
-  __host__ __device__ bool operator()(const uint8_t& x) const { return x == 2; }
-};
-struct IsOne {
-  __host__ __device__ bool operator()(const uint8_t& x) const { return x == 1; }
-};
-struct IsFour {
-  __host__ __device__ bool operator()(const uint8_t& x) const { return x == 4; }
-};
-struct Survives {  // stays active next round: offered (1) or deferred (4)
-  __host__ __device__ bool operator()(const uint8_t& x) const { return x == 1 || x == 4; }
-};
-struct StatusOf {  // partition predicate over slot indices
-  const uint8_t* st;
-  uint8_t val;
-  __host__ __device__ bool operator()(const int32_t& s) const { return st[s] == val; }
-};
-
-// Lazy Boruvka.  A continuing row (status 2) has only dead entries before its
-// head and every live entry after it weighs >= lb.  Its component already holds
-// an offer Kc (an actual leaving edge, so >= the component's true minimum).  If
-// lb > w(Kc) the row cannot supply the minimum this round: defer it (status 4,
-// it stays active with its head) instead of scanning.  Exact for any graph.
-__global__ void k_defer_filter(const Cont* __restrict__ cand, Act* __restrict__ act,
-                               uint8_t* __restrict__ status, uint32_t n, const unsigned long long* __restrict__ Kc) {
-  for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < n; s += gridDim.x * blockDim.x) {
-    if (status[s] != 2) continue;
-    const int32_t cv = cand[s].cv;
-    const uint32_t kw = (uint32_t)(gat(Kc + cv) >> 32);  // sentinel -> 0xffffffff, never defers
-    if (mono_bits(act[s].lb) > kw) {
-      status[s] = 4;
-      act[s].asleep = 1;
-    }
-  }
-}
-
-// Asleep rows (deferred in an earlier round) are not scanned by pass A at all;
-// they only wake when their bound no longer exceeds their component's best
-// pass-A offer (or the component has none).  Woken rows are scanned by
-// k_offer_warp this round and are awake again if they offer.
-__global__ void k_wake(Act* __restrict__ act, uint32_t n, const int32_t* __restrict__ comp,
-                       const unsigned long long* __restrict__ Kc, uint8_t* __restrict__ status,
-                       Cont* __restrict__ cand) {
-  for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < n; s += gridDim.x * blockDim.x) {
-    const int4 r = __ldcs(reinterpret_cast<const int4*>(act + s));
-    if (!r.w) continue;
-    const int32_t cv = gat(comp + r.x);
-    const uint32_t kw = (uint32_t)(gat(Kc + cv) >> 32);
-    const bool woken = mono_bits(__int_as_float(r.z)) <= kw;
-    status[s] = woken ? 2 : 4;
-    if (woken) {
-      act[s].asleep = 0;
-      __stcs(reinterpret_cast<int4*>(cand + s), make_int4(r.x, r.y, cv, (int)s));
-    }
-  }
-}
-
-__global__ void k_cont_keys(const Cont* __restrict__ c, uint32_t n, int32_t* __restrict__ keys) {
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) keys[i] = c[i].v;
-}
-
-
-// tie pass over per-slot row offers (status 1)
-__global__ void k_tie_slots(const Act* __restrict__ act, const uint8_t* __restrict__ status,
-                            const uint64_t* __restrict__ off_key, const uint32_t* __restrict__ off_b, uint32_t n,
-                            const int32_t* __restrict__ comp, const uint64_t* __restrict__ Kc,
-                            uint32_t* __restrict__ Bc) {
-  for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < n; s += gridDim.x * blockDim.x) {
-    if (status[s] != 1) continue;
-    const int32_t c = gat(comp + act[s].v);
-    if (off_key[s] == gat(Kc + c)) atomicMin(Bc + c, off_b[s]);
-  }
-}
-
-// Round 1 with singleton components (exact mode): comp(J) != comp(v) for every
-// candidate J, so the first candidate group of the row IS the minimum; no
-// component gathers, no atomics, no tie pass -- the owner writes Kc/Bc and the
-// hook target directly.
-__global__ void k_offer_first(const int32_t* __restrict__ nbr, const float* __restrict__ dist, int32_t k,
-                              float eps, int64_t row_begin, int64_t N, const uint32_t* __restrict__ bits,
-                              int all_core, const int32_t* __restrict__ comp, Act* __restrict__ act, uint32_t n_in,
-                              uint8_t* __restrict__ status, uint64_t* __restrict__ Kc, uint32_t* __restrict__ Bc,
-                              int32_t* __restrict__ tgt, unsigned long long* __restrict__ n_entries) {
+// later rounds over the ELL; see k_offer_round
+__global__ void __launch_bounds__(256) k_light_round(const int4* __restrict__ LE, const int32_t* __restrict__ nbr,
+                                                     const float* __restrict__ dist, int32_t k, float eps,
+                                                     int64_t row_begin, int64_t N, const int32_t* __restrict__ comp,
+                                                     const Rec* __restrict__ act, uint32_t n_in,
+                                                     Rec* __restrict__ act_out, uint32_t* __restrict__ n_out,
+                                                     Offer* __restrict__ offers, unsigned long long* __restrict__ Kc,
+                                                     unsigned long long* __restrict__ n_entries) {
   unsigned long long reads = 0;
-  for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < n_in; s += gridDim.x * blockDim.x) {
-    bool found = false;
-    const int32_t v = act[s].v;
-    const int64_t i = (int64_t)v - row_begin;
-    const int32_t* nr = nbr + i * k;
-    const float* dr = dist + i * k;
-    uint64_t best = kSent;
-    uint32_t bestb = kSentB;
-    int64_t bestJ = -1;
-    int h = 0;
-    float wstar = 0.f;
-    for (; h < k; ++h) {
-      const float w = __ldcs(dr + h);
-      ++reads;
-      if (!(w <= eps)) { h = k; break; }
-      const int64_t J = __ldcs(nr + h);
-      if (!cand_entry(J, v, N, bits, all_core)) continue;
-      wstar = w;
-      found = true;
-      break;
+  for (uint32_t base = blockIdx.x * blockDim.x; base < n_in; base += gridDim.x * blockDim.x) {
+    const uint32_t s = base + threadIdx.x;
+    RowScan r{false, 0, kSent, kSentB, -1};
+    int32_t v = -1, cv = -1;
+    if (s < n_in) {
+      const int2 a = __ldcs(reinterpret_cast<const int2*>(act + s));
+      v = a.x;
+      cv = gat(comp + v);
+      const int64_t i = (int64_t)v - row_begin;
+      r = scan_ell<false>(LE + i * (kW / 2), nbr + i * k, dist + i * k, k, eps, v, cv, a.y, N, comp, 0, reads);
+      if (r.found) atomicMin(Kc + cv, (unsigned long long)r.best);
     }
-    if (found) {
-      for (int h2 = h; h2 < k; ++h2) {
-        const float w = h2 == h ? wstar : __ldg(dr + h2);
-        if (h2 != h) ++reads;
-        if (w != wstar) break;
-        const int64_t J = __ldg(nr + h2);
-        if (!cand_entry(J, v, N, bits, all_core)) continue;
-        const uint64_t kk = pack_key(mono_bits(w), (uint32_t)min((int64_t)v, J));
-        const uint32_t bb = (uint32_t)max((int64_t)v, J);
-        if (kk < best || (kk == best && bb < bestb)) { best = kk; bestb = bb; bestJ = J; }
-      }
-      const int32_t cv = gat(comp + v);
-      Kc[cv] = best;
-      Bc[cv] = bestb;
-      tgt[cv] = gat(comp + bestJ);
+    const uint32_t slot = block_reserve(n_out, r.found);
+    if (r.found) {
+      act_out[slot] = Rec{v, r.h};
+      offers[slot] = Offer{cv, r.bestb, r.best};
     }
-    act[s].h = min(h, k);
-    status[s] = found ? 1 : 0;
   }
   for (int o = 16; o > 0; o >>= 1) reads += __shfl_xor_sync(0xffffffffu, reads, o);
   if ((threadIdx.x & 31) == 0 && reads) atomicAdd(n_entries, reads);
@@ -993,8 +809,7 @@ __global__ void k_offer_in(const unsigned long long* __restrict__ in_off, int32_
                            int32_t* __restrict__ in_src, float* __restrict__ in_w,
                            const int32_t* __restrict__ comp, const int32_t* __restrict__ act_in,
                            uint32_t n_in, int32_t* __restrict__ act_out, uint32_t* __restrict__ n_out,
-                           int32_t* __restrict__ off_v, uint64_t* __restrict__ off_key,
-                           uint32_t* __restrict__ off_b, uint32_t* __restrict__ n_off,
+                           Offer* __restrict__ offers, uint32_t* __restrict__ n_off,
                            unsigned long long* __restrict__ Kc) {
   for (uint32_t base = blockIdx.x * blockDim.x; base < n_in; base += gridDim.x * blockDim.x) {
     const uint32_t s = base + threadIdx.x;
@@ -1029,33 +844,30 @@ __global__ void k_offer_in(const unsigned long long* __restrict__ in_off, int32_
     if (keep) act_out[a] = t;
     const uint32_t o2 = block_reserve(n_off, found);
     if (found) {
-      off_v[o2] = t;
-      off_key[o2] = best;
-      off_b[o2] = bestb;
+      offers[o2] = Offer{ct, bestb, best};
       atomicMin(Kc + ct, (unsigned long long)best);
     }
   }
 }
 
 // ============================================================================
-// a4: tie pass (b of the minimum key)
+// a4: tie pass (b of the minimum key); the offer count is read on the device
 // ============================================================================
-__global__ void k_tie(const int32_t* __restrict__ off_v, const uint64_t* __restrict__ off_key,
-                      const uint32_t* __restrict__ off_b, uint32_t n_off,
-                      const int32_t* __restrict__ comp, const uint64_t* __restrict__ Kc,
-                      uint32_t* __restrict__ Bc) {
-  for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < n_off; s += gridDim.x * blockDim.x) {
-    const int32_t c = comp[off_v[s]];
-    if (off_key[s] == Kc[c]) atomicMin(Bc + c, off_b[s]);
+__global__ void k_tie(const Offer* __restrict__ offers, const uint32_t* __restrict__ n_p,
+                      const uint64_t* __restrict__ Kc, uint32_t* __restrict__ Bc) {
+  const uint32_t n = *n_p;
+  for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < n; s += gridDim.x * blockDim.x) {
+    const Offer o = offers[s];
+    if (o.key == gat(Kc + o.c)) atomicMin(Bc + o.c, o.b);
   }
 }
 
 // stall fallback (exact mode): offer EVERY live leaving entry of the active
 // rows to both endpoint components (rows outside the active list have none)
 __global__ void k_sweep(const int32_t* __restrict__ nbr, const float* __restrict__ dist, int32_t k, float eps,
-                        int64_t row_begin, int64_t N, const uint32_t* __restrict__ bits,
-                        const int32_t* __restrict__ comp, const Act* __restrict__ act, uint32_t n_act,
-                        unsigned long long* __restrict__ Kc, uint32_t* __restrict__ Bc, int tie_phase) {
+                        int64_t row_begin, int64_t N, const int32_t* __restrict__ comp,
+                        const Rec* __restrict__ act, uint32_t n_act, unsigned long long* __restrict__ Kc,
+                        uint32_t* __restrict__ Bc, int tie_phase) {
   for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < n_act; s += gridDim.x * blockDim.x) {
     const int64_t v = act[s].v;
     const int64_t i = v - row_begin;
@@ -1064,9 +876,9 @@ __global__ void k_sweep(const int32_t* __restrict__ nbr, const float* __restrict
       const float w = __ldg(dist + i * k + c);
       if (!(w <= eps)) break;
       const int64_t J = __ldg(nbr + i * k + c);
-      if (J < 0 || J >= N || J == v || !is_core(bits, J)) continue;
+      if (J < 0 || J >= N || J == v) continue;
       const int32_t cj = comp[J];
-      if (cj == cv) continue;
+      if (cj < 0 || cj == cv) continue;
       const uint64_t kk = pack_key(mono_bits(w), (uint32_t)min(v, J));
       const uint32_t bb = (uint32_t)max(v, J);
       if (!tie_phase) {
@@ -1300,6 +1112,212 @@ __global__ void k_label(const int32_t* __restrict__ nbr, const float* __restrict
 }
 
 // ============================================================================
+// Filter-Boruvka: light phase, filter, heavy phase
+// ============================================================================
+// The rounds above run first on the LIGHT candidate graph G_L = entries with
+// w <= tau (tau < eps, sampled so that G_L's components are large).  Every
+// light key is smaller than every heavy key (mono(w) is the major field of
+// O1), so by the cut and cycle properties
+//     MSF(G) = MSF(G_L)  U  MSF(G / comp_L restricted to heavy entries whose
+//                              endpoints lie in different light components).
+// k_filter streams the heavy entries once and keeps only those that cross
+// light components ("survivors"); the heavy phase runs edge-centric Boruvka on
+// the survivors in the contracted (component) space, where every survivor is
+// offered to both endpoint components -- undirected by construction, so it is
+// exact for ANY valid graph (no certificate, no in-edge lists).
+
+// tau sampling: column `col` of every stride-th local row
+__global__ void k_sample_col(const float* __restrict__ dist, int64_t n_rows, int32_t k, int32_t col, int64_t stride,
+                             int64_t n_out, float* __restrict__ out) {
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n_out; s += (int64_t)gridDim.x * blockDim.x)
+    out[s] = __ldg(dist + (s * stride) * k + col);
+}
+
+struct HEdge {     // a survivor: a heavy candidate entry that crosses light components
+  uint64_t key;    // (mono(w) << 32) | a
+  int32_t x, y;    // light-component ids of the row vertex and of the target J
+  uint32_t b;      // max endpoint
+  uint32_t pad;
+};
+static_assert(sizeof(HEdge) == 24, "HEdge layout");
+
+// One pass over this rank's rows, 4 entries (one int4 + one float4) per thread
+// and step when k % 4 == 0 (a 4-chunk never straddles rows), 1 otherwise.
+// Survivor iff tau < w <= eps, J a valid core id != v (comp[J] >= 0) and
+// comp[J] != comp[v] (v core).  comp is the light phase's dense component id.
+template <int VEC>
+__global__ void __launch_bounds__(256) k_filter(const int32_t* __restrict__ nbr, const float* __restrict__ dist,
+                                                int64_t n_rows, int32_t k, float tau, float eps, int64_t row_begin,
+                                                int64_t N, const int32_t* __restrict__ comp, HEdge* __restrict__ out,
+                                                uint32_t cap, uint32_t* __restrict__ n_out) {
+  const int64_t total = n_rows * (int64_t)k;
+  const int64_t nchunks = (total + VEC - 1) / VEC;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < nchunks; base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t q = base + threadIdx.x;
+    int32_t J[VEC];
+    float w[VEC];
+    int64_t row[VEC];
+#pragma unroll
+    for (int j = 0; j < VEC; ++j) { J[j] = -1; w[j] = 0.f; row[j] = 0; }
+    if (q < nchunks) {
+      const int64_t e0 = q * VEC;
+      if (VEC == 4) {
+        const int4 j4 = __ldcs(reinterpret_cast<const int4*>(nbr + e0));
+        const float4 w4 = __ldcs(reinterpret_cast<const float4*>(dist + e0));
+        J[0] = j4.x; J[1] = j4.y; J[2] = j4.z; J[3] = j4.w;
+        w[0] = w4.x; w[1] = w4.y; w[2] = w4.z; w[3] = w4.w;
+        const int64_t r = e0 / k;
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) row[j] = r;
+      } else {
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) {
+          const int64_t e = e0 + j;
+          if (e < total) { J[j] = __ldcs(nbr + e); w[j] = __ldcs(dist + e); row[j] = e / k; }
+        }
+      }
+    }
+    bool surv[VEC];
+    int32_t ci[VEC], cj[VEC];
+    int32_t cr = -1;
+    int64_t rlast = -1;
+#pragma unroll
+    for (int j = 0; j < VEC; ++j) {
+      surv[j] = false;
+      ci[j] = -1;
+      cj[j] = -1;
+      const int64_t v = row_begin + row[j];
+      if (J[j] >= 0 && J[j] < N && J[j] != v && w[j] > tau && w[j] <= eps) {
+        if (row[j] != rlast) { cr = gat(comp + v); rlast = row[j]; }
+        if (cr >= 0) {
+          const int32_t c2 = gat(comp + J[j]);
+          ci[j] = cr;
+          cj[j] = c2;
+          surv[j] = c2 >= 0 && c2 != cr;
+        }
+      }
+    }
+    int cnt = 0;
+#pragma unroll
+    for (int j = 0; j < VEC; ++j) cnt += surv[j];
+    // warp-aggregated slot reservation
+    const unsigned any = __ballot_sync(0xffffffffu, cnt > 0);
+    if (any) {
+      int incl = cnt;
+      const int lane = threadIdx.x & 31;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      const int tot = __shfl_sync(0xffffffffu, incl, 31);
+      uint32_t base_slot = 0;
+      if (lane == 31) base_slot = atomicAdd(n_out, (uint32_t)tot);
+      base_slot = __shfl_sync(0xffffffffu, base_slot, 31);
+      uint32_t slot = base_slot + (uint32_t)(incl - cnt);
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) {
+        if (!surv[j]) continue;
+        if (slot < cap) {
+          const int64_t v = row_begin + row[j];
+          HEdge h;
+          h.key = pack_key(mono_bits(w[j]), (uint32_t)min(v, (int64_t)J[j]));
+          h.b = (uint32_t)max(v, (int64_t)J[j]);
+          h.x = ci[j];
+          h.y = cj[j];
+          h.pad = 0;
+          out[slot] = h;
+        }
+        ++slot;
+      }
+    }
+  }
+}
+
+// heavy phase, per round: x = hcomp[e.x], y = hcomp[e.y]; intra -> dropped for
+// good; else offer the key to both components (undirected)
+__global__ void k_hedge_offer(const HEdge* __restrict__ E, uint32_t n, const int32_t* __restrict__ hcomp,
+                              unsigned long long* __restrict__ Kc, uint8_t* __restrict__ keep) {
+  for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < n; s += gridDim.x * blockDim.x) {
+    const HEdge e = E[s];
+    const int32_t x = gat(hcomp + e.x), y = gat(hcomp + e.y);
+    const bool live = x != y;
+    keep[s] = live;
+    if (live) {
+      atomicMin(Kc + x, (unsigned long long)e.key);
+      atomicMin(Kc + y, (unsigned long long)e.key);
+    }
+  }
+}
+
+__global__ void k_hedge_tie(const HEdge* __restrict__ E, uint32_t n, const int32_t* __restrict__ hcomp,
+                            const uint64_t* __restrict__ Kc, uint32_t* __restrict__ Bc) {
+  for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < n; s += gridDim.x * blockDim.x) {
+    const HEdge e = E[s];
+    const int32_t x = gat(hcomp + e.x), y = gat(hcomp + e.y);
+    if (e.key == gat(Kc + x)) atomicMin(Bc + x, e.b);
+    if (e.key == gat(Kc + y)) atomicMin(Bc + y, e.b);
+  }
+}
+
+// heavy-phase hook: the component of vertex u is hcomp[compL[u]]
+__global__ void k_hook_h(int64_t C, const uint64_t* __restrict__ Kc, const uint32_t* __restrict__ Bc,
+                         const int32_t* __restrict__ compL, const int32_t* __restrict__ hcomp,
+                         int32_t* __restrict__ parent, uint64_t* __restrict__ e_key, float* __restrict__ e_w,
+                         int64_t e_cap, RoundCounters* __restrict__ ctr) {
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < C; base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = base + threadIdx.x;
+    bool emit = false, offered = false;
+    uint32_t a = 0, b = 0, wb = 0;
+    if (c < C) {
+      const uint64_t K = Kc[c];
+      int32_t p = (int32_t)c;
+      if (K != kSent) {
+        offered = true;
+        a = (uint32_t)K;
+        b = Bc[c];
+        wb = (uint32_t)(K >> 32);
+        const int32_t ca = gat(hcomp + gat(compL + a));
+        const int32_t t = ca == (int32_t)c ? gat(hcomp + gat(compL + b)) : ca;
+        const bool mutual = gat(Kc + t) == K && gat(Bc + t) == b;
+        if (!(mutual && c < t)) {
+          p = t;
+          emit = true;
+        }
+      }
+      parent[c] = p;
+    }
+    block_count(&ctr->offered, offered);
+    block_count(&ctr->hooks, emit);
+    const uint32_t slot = block_reserve(&ctr->msf_count, emit);
+    if (emit && (int64_t)slot < e_cap) {
+      e_key[slot] = ((uint64_t)a << 32) | b;
+      e_w[slot] = __uint_as_float(wb);
+    }
+  }
+}
+
+__global__ void k_iota(int32_t* __restrict__ p, int64_t n) {
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n; c += (int64_t)gridDim.x * blockDim.x)
+    p[c] = (int32_t)c;
+}
+
+// hcomp[c] = map[hcomp[c]] over the light components
+__global__ void k_relabel_h(int64_t n, int32_t* __restrict__ hcomp, const int32_t* __restrict__ map) {
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n; c += (int64_t)gridDim.x * blockDim.x)
+    hcomp[c] = gat(map + hcomp[c]);
+}
+
+// final vertex labels after the heavy phase: comp[v] = cminH[hcomp[comp[v]]]
+__global__ void k_canon_h(int64_t N, int32_t* __restrict__ comp, const int32_t* __restrict__ hcomp,
+                          const int32_t* __restrict__ cminH) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < N; v += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t c = comp[v];
+    if (c >= 0) comp[v] = gat(cminH + gat(hcomp + c));
+  }
+}
+
+// ============================================================================
 // host side
 // ============================================================================
 // exact value of sum_e bk[e] * 2^(max(e,1) - 150), rounded once to double
@@ -1333,6 +1351,11 @@ double exact_bucket_sum(const unsigned long long* bk) {
   return ldexp((double)man, top - 52 - 149);
 }
 
+// heavy-phase survivor capacity per rank (edges); beyond it kdb_mst falls back
+// to plain rows-Boruvka over the whole candidate graph (still exact)
+constexpr int kTauSamples = 8192;
+inline int64_t survivor_cap(int64_t n_rows) { return n_rows / 4 + 65536; }
+
 struct Carver {
   char* base;
   size_t off = 0, cap;
@@ -1350,18 +1373,14 @@ struct RankState {
   int64_t row_begin = 0, n_rows = 0;
   const int32_t* nbr = nullptr;
   const float* dist = nullptr;
-  Act* act[2] = {nullptr, nullptr};  // active rows (v, head), ping-pong
-  Cont* cand = nullptr;               // per-slot continuation records
-  Cont* cont = nullptr;               // compacted continuation list
-  uint8_t* status = nullptr;          // per slot: 0 exhausted, 1 offer, 2 continue, 4 deferred
-  uint32_t n_act = 0;  // live rows in act[cur] (awake and asleep)
-  uint32_t n_slots = 0;  // offer slots written by this round's row kernels
-  // offers
-  int32_t* off_v = nullptr;
-  uint64_t* off_key = nullptr;
-  uint32_t* off_b = nullptr;
-  uint32_t n_off = 0;
-  int64_t off_cap_rows = 0;  // offers [0, n_rows) from rows, [n_rows, n_rows + N) from in-lists
+  Rec* act[2] = {nullptr, nullptr};  // active rows (v, head), ping-pong
+  uint32_t n_act = 0;                 // live rows in act[cur]
+  bool compact = false;               // rows phase reads the light ELL (else the graph rows)
+  int4* LE = nullptr;                 // light ELL [n_rows][kW] (J, w bits) pairs
+  // offers: [0, n_rows) from rows (same slot as the row's next record),
+  // [n_rows, n_rows + N) from in-lists (general mode)
+  Offer* offers = nullptr;
+  int64_t off_cap_rows = 0;
   // per-rank partial Kc/Bc (sim ranks > 0) -- else alias the shared ones
   uint64_t* Kc = nullptr;
   uint32_t* Bc = nullptr;
@@ -1374,6 +1393,11 @@ struct RankState {
   int32_t* in_act[2] = {nullptr, nullptr};
   uint32_t n_in_act = 0;
   RoundCounters* ctr = nullptr;  // per-rank counters (act/off)
+  // heavy phase: survivors (ping-pong) and their keep flags
+  HEdge* hs[2] = {nullptr, nullptr};
+  uint8_t* hkeep = nullptr;
+  uint32_t hs_cap = 0, n_hs = 0;
+  uint32_t* n_hs_dev = nullptr;  // [2]: filter count, compaction count
 };
 
 struct Layout {
@@ -1388,6 +1412,8 @@ struct Layout {
   uint64_t *e_key, *e_key_sorted;
   float* e_w;
   unsigned long long* buckets;
+  int32_t* hcomp;   // heavy phase: light component -> heavy component
+  float* tau_sample;
   RoundCounters* ctr;
   void* cub_tmp;
   size_t cub_bytes;
@@ -1401,23 +1427,12 @@ size_t cub_tmp_bytes(int64_t N, int64_t cap_edges) {
                                 (unsigned long long*)nullptr, (int)std::max<int64_t>(N + 1, 1));
   cub::DeviceRadixSort::SortPairs(nullptr, c, (const uint64_t*)nullptr, (uint64_t*)nullptr,
                                   (const float*)nullptr, (float*)nullptr, (int)std::max<int64_t>(cap_edges, 1));
-  size_t d = 0, e = 0;
-  const int n1 = (int)std::max<int64_t>(N + 1, 1);
-  thrust::transform_iterator<IsTwo, const uint8_t*, bool> two(nullptr, IsTwo{});
-  cub::DeviceSelect::Flagged(nullptr, d, (const Cont*)nullptr, two, (Cont*)nullptr, (uint32_t*)nullptr, n1);
-  cub::DeviceSelect::Flagged(nullptr, e, (const Act*)nullptr, (const uint8_t*)nullptr, (Act*)nullptr,
-                             (uint32_t*)nullptr, n1);
-  size_t f = 0, g = 0;
-  thrust::transform_iterator<IsOne, const uint8_t*, bool> one(nullptr, IsOne{});
-  cub::DeviceSelect::Flagged(nullptr, f, (const Act*)nullptr, one, (Act*)nullptr, (uint32_t*)nullptr, n1);
-  thrust::transform_iterator<IsFour, const uint8_t*, bool> four(nullptr, IsFour{});
-  cub::DeviceSelect::Flagged(nullptr, g, (const Act*)nullptr, four, (Act*)nullptr, (uint32_t*)nullptr, n1);
-  f = std::max(f, g);
-  size_t h2 = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, h2, (const int32_t*)nullptr, (int32_t*)nullptr, (const Cont*)nullptr,
-                                  (Cont*)nullptr, n1, 0, 32);
-  f = std::max(f, h2);
-  return std::max(std::max(std::max(a, f), std::max(b, c)), std::max(d, e)) + 256;
+  size_t f = 0;
+  size_t h3 = 0;
+  cub::DeviceSelect::Flagged(nullptr, h3, (const HEdge*)nullptr, (const uint8_t*)nullptr, (HEdge*)nullptr,
+                             (uint32_t*)nullptr, (int)std::min<int64_t>(survivor_cap(N) + 1, INT32_MAX));
+  f = std::max(f, h3);
+  return std::max(std::max(a, f), std::max(b, c)) + 256;
 }
 
 // carve the workspace; returns bytes needed
@@ -1441,6 +1456,8 @@ size_t carve(Layout& L, char* base, bool dry, int64_t N, int nr, const int64_t* 
   L.e_key_sorted = cv.take<uint64_t>(N + 1);
   L.e_w = cv.take<float>(N + 1);
   L.buckets = cv.take<unsigned long long>(256);
+  L.hcomp = cv.take<int32_t>(N + 1);
+  L.tau_sample = cv.take<float>(kTauSamples);
   L.ctr = cv.take<RoundCounters>(1);
   L.cub_bytes = cub_tmp_bytes(N, N + 1);
   L.cub_tmp = cv.take<char>(L.cub_bytes);
@@ -1450,16 +1467,11 @@ size_t carve(Layout& L, char* base, bool dry, int64_t N, int nr, const int64_t* 
     R.row_begin = rb[r];
     R.n_rows = rn[r];
     const int64_t n = std::max<int64_t>(rn[r], 1);
-    R.act[0] = cv.take<Act>(n);
-    R.act[1] = cv.take<Act>(n);
-    R.cand = cv.take<Cont>(n);
-    R.cont = cv.take<Cont>(n);
-    R.status = cv.take<uint8_t>(n);
-    const int64_t noff = general ? n + N : n;
+    R.act[0] = cv.take<Rec>(n);
+    R.act[1] = cv.take<Rec>(n);
+    R.LE = cv.take<int4>(n * (kW / 2));
     R.off_cap_rows = n;
-    R.off_v = cv.take<int32_t>(noff);
-    R.off_key = cv.take<uint64_t>(noff);
-    R.off_b = cv.take<uint32_t>(noff);
+    R.offers = cv.take<Offer>(general ? n + N : n);
     R.ctr = cv.take<RoundCounters>(1);
     if (r > 0) {
       R.Kc = cv.take<uint64_t>(N + 1);
@@ -1470,6 +1482,11 @@ size_t carve(Layout& L, char* base, bool dry, int64_t N, int nr, const int64_t* 
       R.Bc = L.Bc;
       R.tgt = L.tgt;
     }
+    R.hs_cap = (uint32_t)std::min<int64_t>(survivor_cap(n), (int64_t)UINT32_MAX - 1);
+    R.hs[0] = cv.take<HEdge>(R.hs_cap);
+    R.hs[1] = cv.take<HEdge>(R.hs_cap);
+    R.hkeep = cv.take<uint8_t>(R.hs_cap);
+    R.n_hs_dev = cv.take<uint32_t>(2);
     if (general) {
       R.in_off = cv.take<unsigned long long>(N + 1);
       R.in_len = cv.take<int32_t>(N);
@@ -1527,6 +1544,462 @@ kdb_status allreduce_min_u32(kdb_comm* comm, uint32_t* p, int64_t n, cudaStream_
   return nccl_check(g_nccl.AllReduce(p, p, (size_t)n, ncclUint32, ncclMin, comm->nccl, st), "ncclAllReduce(u32,min)");
 }
 
+kdb_status allreduce_max_u32(kdb_comm* comm, uint32_t* p, int64_t n, cudaStream_t st) {
+  if (!comm || comm->kind != 1 || comm->nranks == 1 || n <= 0) return KDB_OK;
+  return nccl_check(g_nccl.AllReduce(p, p, (size_t)n, ncclUint32, ncclMax, comm->nccl, st), "ncclAllReduce(u32,max)");
+}
+
+int env_int(const char* name, int dflt) {
+  const char* s = getenv(name);
+  return (s && *s) ? atoi(s) : dflt;
+}
+
+// One kdb_mst call: the workspace layout plus the phase bookkeeping.
+struct Mst {
+  Layout L;
+  const kdb_graph* g = nullptr;
+  kdb_comm* comm = nullptr;
+  cudaStream_t st = nullptr;
+  int64_t N = 0;
+  int32_t k = 0;
+  const uint32_t* bits = nullptr;
+  int32_t* comp = nullptr;
+  bool general = false;
+  int64_t C = 0;         // components after the rows phase (light components under the filter)
+  int64_t C_heavy = -1;  // components after the heavy phase (-1: no heavy phase ran)
+  int rounds = 0, stalls = 0, heavy_rounds = 0;
+  double t_init = 0, t_inlist = 0, t_min_edges = 0, t_contract = 0, t_filter = 0, t_heavy = 0;
+  unsigned long long entries = 0, survivors = 0;
+  float tau = 0.f;
+  int fallback = 0;
+  cudaEvent_t ev[4];
+};
+
+float elapsed(cudaEvent_t a, cudaEvent_t b) {
+  float ms = 0;
+  cudaEventSynchronize(b);
+  cudaEventElapsedTime(&ms, a, b);
+  return ms;
+}
+
+// Light threshold: the median of column m0-1 over sampled local rows, made
+// global with an all-reduce MIN (all ranks must filter with the same tau).
+kdb_status pick_tau(Mst& m, int m0, float* tau_out) {
+  const kdb_graph* g = m.g;
+  Layout& L = m.L;
+  const int64_t n = g->n_rows;
+  uint32_t tb = kInfBits;
+  if (n > 0) {
+    const int64_t S = std::min<int64_t>(n, kTauSamples);
+    const int64_t stride = n / S;
+    LAUNCH(k_sample_col, grid_for(S), kThreads, m.st, g->dist, n, m.k, m0 - 1, stride, S, L.tau_sample);
+    KDB_CUDA(cudaGetLastError());
+    std::vector<float> h(S);
+    KDB_CUDA(cudaMemcpyAsync(h.data(), L.tau_sample, S * sizeof(float), cudaMemcpyDeviceToHost, m.st));
+    KDB_CUDA(cudaStreamSynchronize(m.st));
+    std::nth_element(h.begin(), h.begin() + S / 2, h.end());
+    float t = h[S / 2];
+    if (!(t >= 0.f)) t = __builtin_inff();  // NaN guard
+    memcpy(&tb, &t, 4);
+    if (tb == 0x80000000u) tb = 0u;
+  }
+  if (m.comm && m.comm->kind == 1 && m.comm->nranks > 1) {
+    uint32_t* d = reinterpret_cast<uint32_t*>(L.tau_sample);
+    KDB_CUDA(cudaMemcpyAsync(d, &tb, 4, cudaMemcpyHostToDevice, m.st));
+    KDB_TRY(allreduce_min_u32(m.comm, d, 1, m.st));
+    KDB_CUDA(cudaMemcpyAsync(&tb, d, 4, cudaMemcpyDeviceToHost, m.st));
+    KDB_CUDA(cudaStreamSynchronize(m.st));
+  }
+  memcpy(tau_out, &tb, 4);
+  return KDB_OK;
+}
+
+// a2-a8: rows-Boruvka over the candidate entries with w <= eps_run (from
+// singletons).  Leaves comp[] = dense component ids (0..C-1), L.cmin = minimum
+// core id per component, m.C.  Resets the MSF counter.
+kdb_status rows_phase(Mst& m, float eps_run) {
+  Layout& L = m.L;
+  kdb_comm* comm = m.comm;
+  cudaStream_t st = m.st;
+  const int64_t N = m.N;
+  const int32_t k = m.k;
+  const uint32_t* core_bits = m.bits;
+  int32_t* comp = m.comp;
+  const bool general = m.general;
+  const bool vec = (k % 4) == 0;
+  cudaEvent_t* ev = m.ev;
+  KDB_CUDA(cudaEventRecord(ev[0], st));
+
+  // ---- a2: dense component ids -------------------------------------------------
+  const int64_t nwords = (N + 31) / 32;
+  uint32_t* popc = reinterpret_cast<uint32_t*>(L.flag);  // scratch, nwords + 1 <= N + 1
+  KDB_CUDA(cudaMemsetAsync(popc + nwords, 0, sizeof(uint32_t), st));
+  KDB_CUDA(cudaMemsetAsync(L.ctr, 0, sizeof(RoundCounters), st));
+  LAUNCH(k_popc_words, grid_for(nwords), kThreads, st, core_bits, nwords, popc);
+  KDB_CUDA(cudaGetLastError());
+  size_t cb = L.cub_bytes;
+  { LaunchScope ls_("cub::DeviceScan", st, false); KDB_CUDA(cub::DeviceScan::ExclusiveSum(L.cub_tmp, cb, popc, L.woff, (int)(nwords + 1), st)); }
+  uint32_t C32 = 0;  // woff[nwords] = number of core points
+  KDB_CUDA(cudaMemcpyAsync(&C32, L.woff + nwords, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+  KDB_CUDA(cudaStreamSynchronize(st));
+  int64_t C = C32;
+  L.all_core = (C == N) ? 1 : 0;  // then the dense id of a vertex is the vertex itself
+  LAUNCH(k_init_comp, grid_for(N), kThreads, st, core_bits, L.woff, N, comp, L.cmin);
+  LAUNCH(k_fill_comp_arrays, grid_for(C), kThreads, st, C, L.Kc, L.Bc, general ? nullptr : L.kmin);
+  for (size_t r = 1; r < L.ranks.size(); ++r)
+    LAUNCH(k_fill_comp_arrays, grid_for(C), kThreads, st, C, L.ranks[r].Kc, L.ranks[r].Bc, nullptr);
+  KDB_CUDA(cudaGetLastError());
+  const bool use_compact = env_int("KDB_COMPACT", 1) != 0;
+  for (auto& R : L.ranks) {
+    KDB_CUDA(cudaMemsetAsync(R.ctr, 0, sizeof(RoundCounters), st));
+    R.compact = false;
+    if (R.n_rows > 0 && use_compact) {
+      R.compact = true;
+      if (vec)
+        LAUNCH(k_light_ell<true>, grid_for(R.n_rows), kThreads, st, R.nbr, R.dist, R.n_rows, k, eps_run,
+               R.row_begin, comp, general ? nullptr : L.kmin, R.LE, R.act[0], &R.ctr->n_act[0]);
+      else
+        LAUNCH(k_light_ell<false>, grid_for(R.n_rows), kThreads, st, R.nbr, R.dist, R.n_rows, k, eps_run,
+               R.row_begin, comp, general ? nullptr : L.kmin, R.LE, R.act[0], &R.ctr->n_act[0]);
+    }
+    if (R.n_rows > 0 && !R.compact)
+      LAUNCH(k_init_rows, grid_for(R.n_rows), kThreads, st, R.dist, R.n_rows, k, eps_run, R.row_begin, comp,
+             general ? nullptr : L.kmin, R.act[0], &R.ctr->n_act[0]);
+    KDB_CUDA(cudaGetLastError());
+  }
+  if (!general) {
+    KDB_TRY(allreduce_min_u32(comm, L.kmin, C, st));
+    for (auto& R : L.ranks) LAUNCH(k_fill_i32, grid_for(C), kThreads, st, R.tgt, C, INT32_MAX);
+  }
+  KDB_CUDA(cudaEventRecord(ev[1], st));
+  // ---- general mode: in-edge lists --------------------------------------------
+  if (general) {
+    for (auto& R : L.ranks) {
+      // counts -> scan -> offsets; e_key (N+1 u64) is scratch for counts and cursors
+      unsigned long long* cursor = reinterpret_cast<unsigned long long*>(L.e_key);
+      KDB_CUDA(cudaMemsetAsync(cursor, 0, (N + 1) * sizeof(unsigned long long), st));
+      if (R.n_rows > 0)
+        LAUNCH(k_in_count, grid_for(R.n_rows), kThreads, st, R.nbr, R.dist, R.n_rows, k, eps_run, R.row_begin, N,
+               core_bits, cursor);
+      cb = L.cub_bytes;
+      { LaunchScope ls_("cub::DeviceScan", st, false); KDB_CUDA(cub::DeviceScan::ExclusiveSum(L.cub_tmp, cb, cursor, R.in_off, (int)(N + 1), st)); }
+      KDB_CUDA(cudaMemcpyAsync(cursor, R.in_off, (N + 1) * sizeof(unsigned long long),
+                               cudaMemcpyDeviceToDevice, st));
+      if (R.n_rows > 0)
+        LAUNCH(k_in_fill, grid_for(R.n_rows), kThreads, st, R.nbr, R.dist, R.n_rows, k, eps_run, R.row_begin, N,
+               core_bits, cursor, R.in_src, R.in_w);
+      LAUNCH(k_in_finish, grid_for(N), kThreads, st, R.in_off, N, R.in_len, R.in_act[0], &R.ctr->n_act[1]);
+      KDB_CUDA(cudaGetLastError());
+    }
+  }
+  for (auto& R : L.ranks) {
+    RoundCounters hc;
+    KDB_CUDA(cudaMemcpyAsync(&hc, R.ctr, sizeof(hc), cudaMemcpyDeviceToHost, st));
+    KDB_CUDA(cudaStreamSynchronize(st));
+    R.n_act = hc.n_act[0];
+    R.n_in_act = hc.n_act[1];
+  }
+  KDB_CUDA(cudaEventRecord(ev[2], st));
+  KDB_CUDA(cudaEventSynchronize(ev[2]));
+  m.t_init += elapsed(ev[0], ev[1]);
+  m.t_inlist += elapsed(ev[1], ev[2]);
+
+  // ---- Boruvka rounds -------------------------------------------------------------
+  int cur = 0;
+  int rounds = 0, stalls = 0;
+  const uint32_t* kmin_cert = general ? nullptr : L.kmin;
+  while (C > 0) {
+    ++rounds;
+    // round 1 of exact mode: singleton components, one offer each (no in-lists)
+    const bool direct = rounds == 1 && !general;
+    KDB_CUDA(cudaEventRecord(ev[0], st));
+    // a3: offers (rows, then in-lists), per rank, into that rank's Kc partial
+    for (auto& R : L.ranks) {
+      KDB_CUDA(cudaMemsetAsync(&R.ctr->n_act[0], 0, 3 * sizeof(uint32_t), st));  // n_act[0..1], n_off
+      if (R.n_act && R.compact) {
+        if (direct)
+          LAUNCH(k_light_first, grid_for(R.n_act), kThreads, st, R.LE, R.nbr, R.dist, k, eps_run, R.row_begin, N,
+                 comp, L.all_core, R.act[cur], R.n_act, R.act[cur ^ 1], &R.ctr->n_act[0], R.Kc, R.Bc, R.tgt,
+                 &L.ctr->entries);
+        else
+          LAUNCH(k_light_round, grid_for(R.n_act), kThreads, st, R.LE, R.nbr, R.dist, k, eps_run, R.row_begin, N,
+                 comp, R.act[cur], R.n_act, R.act[cur ^ 1], &R.ctr->n_act[0], R.offers,
+                 (unsigned long long*)R.Kc, &L.ctr->entries);
+      } else if (R.n_act) {
+        if (direct) {
+          if (vec)
+            LAUNCH(k_offer_first<true>, grid_for(R.n_act), kThreads, st, R.nbr, R.dist, k, eps_run, R.row_begin, N,
+                   comp, L.all_core, R.act[cur], R.n_act, R.act[cur ^ 1], &R.ctr->n_act[0], R.Kc, R.Bc, R.tgt,
+                   &L.ctr->entries);
+          else
+            LAUNCH(k_offer_first<false>, grid_for(R.n_act), kThreads, st, R.nbr, R.dist, k, eps_run, R.row_begin,
+                   N, comp, L.all_core, R.act[cur], R.n_act, R.act[cur ^ 1], &R.ctr->n_act[0], R.Kc, R.Bc, R.tgt,
+                   &L.ctr->entries);
+        } else {
+          if (vec)
+            LAUNCH(k_offer_round<true>, grid_for(R.n_act), kThreads, st, R.nbr, R.dist, k, eps_run, R.row_begin, N,
+                   comp, R.act[cur], R.n_act, R.act[cur ^ 1], &R.ctr->n_act[0], R.offers,
+                   (unsigned long long*)R.Kc, &L.ctr->entries);
+          else
+            LAUNCH(k_offer_round<false>, grid_for(R.n_act), kThreads, st, R.nbr, R.dist, k, eps_run, R.row_begin,
+                   N, comp, R.act[cur], R.n_act, R.act[cur ^ 1], &R.ctr->n_act[0], R.offers,
+                   (unsigned long long*)R.Kc, &L.ctr->entries);
+        }
+      }
+      if (general && R.n_in_act)
+        LAUNCH(k_offer_in, grid_for(R.n_in_act), kThreads, st, R.in_off, R.in_len, R.in_src, R.in_w, comp,
+               R.in_act[cur], R.n_in_act, R.in_act[cur ^ 1], &R.ctr->n_act[1], R.offers + R.off_cap_rows,
+               &R.ctr->n_off, (unsigned long long*)R.Kc);
+      KDB_CUDA(cudaGetLastError());
+    }
+    // exchange: sim -> min over virtual ranks; nccl -> allreduce
+    for (size_t r = 1; r < L.ranks.size(); ++r)
+      LAUNCH(k_min_into_u64, grid_for(C), kThreads, st, L.Kc, L.ranks[r].Kc, C);
+    KDB_TRY(allreduce_min_u64(comm, L.Kc, C, st));
+    // a4: ties (the direct round already wrote Bc and the targets)
+    if (!direct) {
+      for (auto& R : L.ranks) {
+        if (R.n_act) LAUNCH(k_tie, grid_for(R.n_act), kThreads, st, R.offers, &R.ctr->n_act[0], L.Kc, R.Bc);
+        if (general && R.n_in_act)
+          LAUNCH(k_tie, grid_for(R.n_in_act), kThreads, st, R.offers + R.off_cap_rows, &R.ctr->n_off, L.Kc, R.Bc);
+        KDB_CUDA(cudaGetLastError());
+      }
+    }
+    for (size_t r = 1; r < L.ranks.size(); ++r)
+      LAUNCH(k_min_into_u32, grid_for(C), kThreads, st, L.Bc, L.ranks[r].Bc, C);
+    KDB_TRY(allreduce_min_u32(comm, L.Bc, C, st));
+    if (direct) {
+      for (size_t r = 1; r < L.ranks.size(); ++r)
+        LAUNCH(k_min_into_u32, grid_for(C), kThreads, st, (uint32_t*)L.tgt, (const uint32_t*)L.ranks[r].tgt, C);
+      KDB_TRY(allreduce_min_u32(comm, (uint32_t*)L.tgt, C, st));  // non-owners hold INT32_MAX
+    }
+    KDB_CUDA(cudaEventRecord(ev[1], st));
+    // a5: hook + emit
+    KDB_CUDA(cudaMemsetAsync(&L.ctr->hooks, 0, 4 * sizeof(uint32_t), st));
+    LAUNCH(k_hook, grid_for(C), kThreads, st, C, L.Kc, L.Bc, direct ? L.tgt : nullptr, kmin_cert, comp, L.parent,
+           L.e_key, L.e_w, N, L.ctr);
+    KDB_CUDA(cudaGetLastError());
+    RoundCounters hc;
+    KDB_CUDA(cudaMemcpyAsync(&hc, L.ctr, sizeof(hc), cudaMemcpyDeviceToHost, st));
+    std::vector<RoundCounters> rc(L.ranks.size());
+    for (size_t r = 0; r < L.ranks.size(); ++r)
+      KDB_CUDA(cudaMemcpyAsync(&rc[r], L.ranks[r].ctr, sizeof(RoundCounters), cudaMemcpyDeviceToHost, st));
+    KDB_CUDA(cudaStreamSynchronize(st));
+    if (g_trace) {
+      static unsigned long long last_entries = 0;
+      if (rounds == 1) last_entries = 0;
+      fprintf(stderr, "[kdb] round %d eps=%.6g C=%lld live=%u -> %u entries=%llu offer_ms=%.3f hooks=%u\n",
+              rounds, (double)eps_run, (long long)C, L.ranks[0].n_act, rc[0].n_act[0],
+              hc.entries - last_entries, elapsed(ev[0], ev[1]), hc.hooks);
+      last_entries = hc.entries;
+    }
+    for (size_t r = 0; r < L.ranks.size(); ++r) {
+      L.ranks[r].n_act = rc[r].n_act[0];
+      L.ranks[r].n_in_act = rc[r].n_act[1];
+    }
+    if (hc.offered == 0) {  // a8: no component has a leaving edge
+      m.t_min_edges += elapsed(ev[0], ev[1]);
+      break;
+    }
+    if (hc.hooks == 0) {
+      // every offering component abstained: one edge-centric sweep round gives
+      // every component its exact minimum (both endpoints see every entry)
+      ++stalls;
+      LAUNCH(k_fill_comp_arrays, grid_for(C), kThreads, st, C, L.Kc, L.Bc, nullptr);
+      for (size_t r = 1; r < L.ranks.size(); ++r)
+        LAUNCH(k_fill_comp_arrays, grid_for(C), kThreads, st, C, L.ranks[r].Kc, L.ranks[r].Bc, nullptr);
+      for (auto& R : L.ranks)
+        if (R.n_act)
+          LAUNCH(k_sweep, grid_for(R.n_act), kThreads, st, R.nbr, R.dist, k, eps_run, R.row_begin, N, comp,
+                 R.act[cur ^ 1], R.n_act, (unsigned long long*)R.Kc, R.Bc, 0);
+      for (size_t r = 1; r < L.ranks.size(); ++r)
+        LAUNCH(k_min_into_u64, grid_for(C), kThreads, st, L.Kc, L.ranks[r].Kc, C);
+      KDB_TRY(allreduce_min_u64(comm, L.Kc, C, st));
+      for (auto& R : L.ranks)
+        if (R.n_act)
+          LAUNCH(k_sweep, grid_for(R.n_act), kThreads, st, R.nbr, R.dist, k, eps_run, R.row_begin, N, comp,
+                 R.act[cur ^ 1], R.n_act, (unsigned long long*)L.Kc, R.Bc, 1);
+      for (size_t r = 1; r < L.ranks.size(); ++r)
+        LAUNCH(k_min_into_u32, grid_for(C), kThreads, st, L.Bc, L.ranks[r].Bc, C);
+      KDB_TRY(allreduce_min_u32(comm, L.Bc, C, st));
+      KDB_CUDA(cudaMemsetAsync(&L.ctr->hooks, 0, 4 * sizeof(uint32_t), st));
+      LAUNCH(k_hook, grid_for(C), kThreads, st, C, L.Kc, L.Bc, nullptr, nullptr, comp, L.parent, L.e_key, L.e_w, N,
+             L.ctr);
+      KDB_CUDA(cudaGetLastError());
+      KDB_CUDA(cudaMemcpyAsync(&hc, L.ctr, sizeof(hc), cudaMemcpyDeviceToHost, st));
+      KDB_CUDA(cudaStreamSynchronize(st));
+      if (hc.hooks == 0) return set_err(KDB_EINTERNAL, "sweep round made no progress");
+      // rows whose scan found nothing are exhausted for good and stay out of the
+      // active list; rows that still hold leaving entries are in it
+    }
+    if (hc.violation) return set_err(KDB_EINVAL, "graph violates the KDB_GRAPH_EXACT promise (a component's "
+                                     "minimum missed an incident edge)");
+    // a6: contract
+    LAUNCH(k_jump, grid_for(C), kThreads, st, C, L.parent, L.rootof, L.ctr);
+    LAUNCH(k_root_flags, grid_for(C), kThreads, st, C, L.rootof, L.flag);
+    cb = L.cub_bytes;
+    { LaunchScope ls_("cub::DeviceScan", st, false); KDB_CUDA(cub::DeviceScan::ExclusiveSum(L.cub_tmp, cb, L.flag, L.newid, (int)C, st)); }
+    uint32_t viol = 0;
+    KDB_CUDA(cudaMemcpyAsync(&viol, &L.ctr->violation, 4, cudaMemcpyDeviceToHost, st));
+    int32_t last[2];
+    KDB_CUDA(cudaMemcpyAsync(&last[0], L.newid + C - 1, 4, cudaMemcpyDeviceToHost, st));
+    KDB_CUDA(cudaMemcpyAsync(&last[1], L.flag + C - 1, 4, cudaMemcpyDeviceToHost, st));
+    KDB_CUDA(cudaStreamSynchronize(st));
+    if (viol) return set_err(KDB_EINTERNAL, "pointer jumping did not converge (hook cycle)");
+    const int64_t C2 = (int64_t)last[0] + last[1];
+    LAUNCH(k_fill_i32, grid_for(C2), kThreads, st, L.cmin2, C2, INT32_MAX);
+    if (!general) LAUNCH(k_fill_i32, grid_for(C2), kThreads, st, (int32_t*)L.kmin2, C2, (int32_t)kInfBits);
+    // map[c] = new dense id of c's tree (reuses `parent`, no longer needed)
+    LAUNCH(k_merge, grid_for(C), kThreads, st, C, L.rootof, L.newid, L.cmin, general ? nullptr : L.kmin, L.cmin2,
+           L.kmin2, L.parent);
+    LAUNCH(k_relabel, grid_for(N), kThreads, st, N, comp, L.parent);
+    LAUNCH(k_fill_comp_arrays, grid_for(C2), kThreads, st, C2, L.Kc, L.Bc, nullptr);
+    for (size_t r = 1; r < L.ranks.size(); ++r)
+      LAUNCH(k_fill_comp_arrays, grid_for(C2), kThreads, st, C2, L.ranks[r].Kc, L.ranks[r].Bc, nullptr);
+    KDB_CUDA(cudaGetLastError());
+    std::swap(L.cmin, L.cmin2);
+    std::swap(L.kmin, L.kmin2);
+    kmin_cert = general ? nullptr : L.kmin;
+    C = C2;
+    cur ^= 1;
+    KDB_CUDA(cudaEventRecord(ev[2], st));
+    m.t_min_edges += elapsed(ev[0], ev[1]);
+    m.t_contract += elapsed(ev[1], ev[2]);
+  }
+  RoundCounters hc;
+  KDB_CUDA(cudaMemcpyAsync(&hc, L.ctr, sizeof(hc), cudaMemcpyDeviceToHost, st));
+  KDB_CUDA(cudaStreamSynchronize(st));
+  m.entries += hc.entries;
+  m.rounds += rounds;
+  m.stalls += stalls;
+  m.C = C;
+  return KDB_OK;
+}
+
+// Filter: every rank streams its rows once and keeps the heavy candidate
+// entries (tau < w <= eps) whose endpoints lie in different light components.
+kdb_status filter_phase(Mst& m, float eps, bool* overflow) {
+  Layout& L = m.L;
+  cudaStream_t st = m.st;
+  KDB_CUDA(cudaEventRecord(m.ev[0], st));
+  // KDB_SURVCAP (tests): a smaller survivor capacity, to exercise the fallback
+  const int64_t cap_env = env_int("KDB_SURVCAP", -1);
+  for (auto& R : L.ranks) {
+    KDB_CUDA(cudaMemsetAsync(R.n_hs_dev, 0, 2 * sizeof(uint32_t), st));
+    if (cap_env >= 0) R.hs_cap = (uint32_t)std::min<int64_t>(R.hs_cap, cap_env);
+    if (R.n_rows == 0) continue;
+    const int64_t total = R.n_rows * (int64_t)m.k;
+    if ((m.k % 4) == 0)
+      LAUNCH(k_filter<4>, grid_for(total / 4), kThreads, st, R.nbr, R.dist, R.n_rows, m.k, m.tau, eps, R.row_begin,
+             m.N, m.comp, R.hs[0], R.hs_cap, R.n_hs_dev);
+    else
+      LAUNCH(k_filter<1>, grid_for(total), kThreads, st, R.nbr, R.dist, R.n_rows, m.k, m.tau, eps, R.row_begin,
+             m.N, m.comp, R.hs[0], R.hs_cap, R.n_hs_dev);
+    KDB_CUDA(cudaGetLastError());
+  }
+  uint32_t over = 0;
+  unsigned long long tot = 0;
+  for (auto& R : L.ranks) {
+    uint32_t n = 0;
+    KDB_CUDA(cudaMemcpyAsync(&n, R.n_hs_dev, 4, cudaMemcpyDeviceToHost, st));
+    KDB_CUDA(cudaStreamSynchronize(st));
+    R.n_hs = n;
+    tot += n;
+    if (n > R.hs_cap) over = 1;
+  }
+  if (m.comm && m.comm->kind == 1 && m.comm->nranks > 1) {  // every rank must take the same branch
+    uint32_t* d = L.ranks[0].n_hs_dev + 1;
+    KDB_CUDA(cudaMemcpyAsync(d, &over, 4, cudaMemcpyHostToDevice, st));
+    KDB_TRY(allreduce_max_u32(m.comm, d, 1, st));
+    KDB_CUDA(cudaMemcpyAsync(&over, d, 4, cudaMemcpyDeviceToHost, st));
+    KDB_CUDA(cudaStreamSynchronize(st));
+  }
+  KDB_CUDA(cudaEventRecord(m.ev[1], st));
+  m.t_filter += elapsed(m.ev[0], m.ev[1]);
+  m.survivors = tot;
+  *overflow = over != 0;
+  return KDB_OK;
+}
+
+// Heavy phase: edge-centric Boruvka over the survivors in light-component
+// space.  hcomp maps light component -> current heavy component (replicated).
+kdb_status heavy_phase(Mst& m) {
+  Layout& L = m.L;
+  cudaStream_t st = m.st;
+  kdb_comm* comm = m.comm;
+  const int64_t CL = m.C;
+  int64_t C = CL;
+  KDB_CUDA(cudaEventRecord(m.ev[0], st));
+  LAUNCH(k_iota, grid_for(CL), kThreads, st, L.hcomp, CL);
+  std::vector<int> cur(L.ranks.size(), 0);
+  int rounds = 0;
+  while (C > 1) {
+    ++rounds;
+    LAUNCH(k_fill_comp_arrays, grid_for(C), kThreads, st, C, L.Kc, L.Bc, nullptr);
+    for (size_t r = 1; r < L.ranks.size(); ++r)
+      LAUNCH(k_fill_comp_arrays, grid_for(C), kThreads, st, C, L.ranks[r].Kc, L.ranks[r].Bc, nullptr);
+    for (size_t r = 0; r < L.ranks.size(); ++r) {
+      RankState& R = L.ranks[r];
+      if (R.n_hs == 0) continue;
+      LAUNCH(k_hedge_offer, grid_for(R.n_hs), kThreads, st, R.hs[cur[r]], R.n_hs, L.hcomp,
+             (unsigned long long*)R.Kc, R.hkeep);
+      size_t cb = L.cub_bytes;
+      { LaunchScope ls_("cub::DeviceSelect", st, false);
+        KDB_CUDA(cub::DeviceSelect::Flagged(L.cub_tmp, cb, R.hs[cur[r]], R.hkeep, R.hs[cur[r] ^ 1],
+                                            R.n_hs_dev + 1, (int)R.n_hs, st)); }
+      cur[r] ^= 1;
+      KDB_CUDA(cudaGetLastError());
+    }
+    for (auto& R : L.ranks) {
+      if (R.n_hs == 0) continue;
+      KDB_CUDA(cudaMemcpyAsync(&R.n_hs, R.n_hs_dev + 1, 4, cudaMemcpyDeviceToHost, st));
+    }
+    KDB_CUDA(cudaStreamSynchronize(st));
+    for (size_t r = 1; r < L.ranks.size(); ++r)
+      LAUNCH(k_min_into_u64, grid_for(C), kThreads, st, L.Kc, L.ranks[r].Kc, C);
+    KDB_TRY(allreduce_min_u64(comm, L.Kc, C, st));
+    for (size_t r = 0; r < L.ranks.size(); ++r) {
+      RankState& R = L.ranks[r];
+      if (R.n_hs)
+        LAUNCH(k_hedge_tie, grid_for(R.n_hs), kThreads, st, R.hs[cur[r]], R.n_hs, L.hcomp, L.Kc, R.Bc);
+    }
+    for (size_t r = 1; r < L.ranks.size(); ++r)
+      LAUNCH(k_min_into_u32, grid_for(C), kThreads, st, L.Bc, L.ranks[r].Bc, C);
+    KDB_TRY(allreduce_min_u32(comm, L.Bc, C, st));
+    KDB_CUDA(cudaMemsetAsync(&L.ctr->hooks, 0, 4 * sizeof(uint32_t), st));
+    LAUNCH(k_hook_h, grid_for(C), kThreads, st, C, L.Kc, L.Bc, m.comp, L.hcomp, L.parent, L.e_key, L.e_w, m.N, L.ctr);
+    KDB_CUDA(cudaGetLastError());
+    RoundCounters hc;
+    KDB_CUDA(cudaMemcpyAsync(&hc, L.ctr, sizeof(hc), cudaMemcpyDeviceToHost, st));
+    KDB_CUDA(cudaStreamSynchronize(st));
+    if (hc.offered == 0) break;
+    if (hc.hooks == 0) return set_err(KDB_EINTERNAL, "heavy phase made no progress");
+    LAUNCH(k_jump, grid_for(C), kThreads, st, C, L.parent, L.rootof, L.ctr);
+    LAUNCH(k_root_flags, grid_for(C), kThreads, st, C, L.rootof, L.flag);
+    size_t cb = L.cub_bytes;
+    { LaunchScope ls_("cub::DeviceScan", st, false); KDB_CUDA(cub::DeviceScan::ExclusiveSum(L.cub_tmp, cb, L.flag, L.newid, (int)C, st)); }
+    uint32_t viol = 0;
+    int32_t last[2];
+    KDB_CUDA(cudaMemcpyAsync(&viol, &L.ctr->violation, 4, cudaMemcpyDeviceToHost, st));
+    KDB_CUDA(cudaMemcpyAsync(&last[0], L.newid + C - 1, 4, cudaMemcpyDeviceToHost, st));
+    KDB_CUDA(cudaMemcpyAsync(&last[1], L.flag + C - 1, 4, cudaMemcpyDeviceToHost, st));
+    KDB_CUDA(cudaStreamSynchronize(st));
+    if (viol) return set_err(KDB_EINTERNAL, "heavy-phase pointer jumping did not converge");
+    const int64_t C2 = (int64_t)last[0] + last[1];
+    LAUNCH(k_fill_i32, grid_for(C2), kThreads, st, L.cmin2, C2, INT32_MAX);
+    LAUNCH(k_merge, grid_for(C), kThreads, st, C, L.rootof, L.newid, L.cmin, nullptr, L.cmin2, nullptr, L.parent);
+    LAUNCH(k_relabel_h, grid_for(CL), kThreads, st, CL, L.hcomp, L.parent);
+    KDB_CUDA(cudaGetLastError());
+    std::swap(L.cmin, L.cmin2);
+    C = C2;
+  }
+  KDB_CUDA(cudaEventRecord(m.ev[1], st));
+  m.t_heavy += elapsed(m.ev[0], m.ev[1]);
+  m.heavy_rounds = rounds;
+  m.C_heavy = C;
+  return KDB_OK;
+}
+
 }  // namespace
 
 // ============================================================================
@@ -1549,7 +2022,7 @@ const char* kdb_status_string(kdb_status s) {
 const char* kdb_last_error(void) { return g_err.c_str(); }
 
 int kdb_last_mst_stats(double* out, int cap) {
-  int n = std::min(cap, 8);
+  int n = std::min(cap, 16);
   for (int i = 0; i < n; ++i) out[i] = g_stats[i];
   return n;
 }
@@ -1682,317 +2155,102 @@ kdb_status kdb_mst(const kdb_graph* g, float eps, const uint32_t* core_bits, int
   if (comm && comm->kind == 2 && (g->row_begin != 0 || g->n_rows != g->n_total))
     return set_err(KDB_EINVAL, "sim communicator needs the full graph");
   if ((uintptr_t)workspace & 255u) return set_err(KDB_EINVAL, "workspace must be 256-byte aligned");
-  const bool general = !(g->flags & KDB_GRAPH_EXACT);
-  const int32_t k = g->k_max;
+  Mst m;
+  m.g = g;
+  m.comm = comm;
+  m.st = (cudaStream_t)stream;
+  m.N = N;
+  m.k = g->k_max;
+  m.bits = core_bits;
+  m.comp = comp;
+  m.general = !(g->flags & KDB_GRAPH_EXACT);
+  Layout& L = m.L;
   std::vector<int64_t> rb, rn;
   rank_ranges(g, comm, rb, rn);
-  Layout L;
-  const size_t need = carve(L, (char*)workspace, false, N, (int)rb.size(), rb.data(), rn.data(), general, k);
+  const size_t need = carve(L, (char*)workspace, false, N, (int)rb.size(), rb.data(), rn.data(), m.general, m.k);
   if (ws_bytes < need) return set_err(KDB_ENOMEM, "workspace %zu < required %zu bytes", ws_bytes, need);
   *mst_count = 0;
   *mst_weight = 0.0;
   for (auto& s : g_stats) s = 0;
   if (N == 0) return KDB_OK;
-  cudaStream_t st = (cudaStream_t)stream;
+  cudaStream_t st = m.st;
   for (auto& R : L.ranks) {
-    R.nbr = g->nbr + (R.row_begin - g->row_begin) * k;
-    R.dist = g->dist + (R.row_begin - g->row_begin) * k;
+    R.nbr = g->nbr + (R.row_begin - g->row_begin) * m.k;
+    R.dist = g->dist + (R.row_begin - g->row_begin) * m.k;
   }
-  cudaEvent_t ev[4];
-  for (auto& e : ev) KDB_CUDA(cudaEventCreate(&e));
+  for (auto& e : m.ev) KDB_CUDA(cudaEventCreate(&e));
   struct EvGuard {
     cudaEvent_t* e;
     ~EvGuard() { for (int i = 0; i < 4; ++i) cudaEventDestroy(e[i]); }
-  } guard{ev};
-  float ms = 0;
-  KDB_CUDA(cudaEventRecord(ev[0], st));
+  } guard{m.ev};
 
-  // ---- a2: dense component ids -------------------------------------------------
-  const int64_t nwords = (N + 31) / 32;
-  uint32_t* popc = reinterpret_cast<uint32_t*>(L.flag);  // scratch, nwords + 1 <= N + 1
-  KDB_CUDA(cudaMemsetAsync(popc + nwords, 0, sizeof(uint32_t), st));
-  KDB_CUDA(cudaMemsetAsync(L.ctr, 0, sizeof(RoundCounters), st));
-  LAUNCH(k_popc_words, grid_for(nwords), kThreads, st, core_bits, nwords, popc);
-  KDB_CUDA(cudaGetLastError());
-  size_t cb = L.cub_bytes;
-  { LaunchScope ls_("cub::DeviceScan", st, false); KDB_CUDA(cub::DeviceScan::ExclusiveSum(L.cub_tmp, cb, popc, L.woff, (int)(nwords + 1), st)); }
-  uint32_t C32 = 0;  // woff[nwords] = number of core points
-  KDB_CUDA(cudaMemcpyAsync(&C32, L.woff + nwords, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
-  KDB_CUDA(cudaStreamSynchronize(st));
-  int64_t C = C32;
-  L.all_core = (C == N) ? 1 : 0;  // then no entry needs a core-bit gather
-  LAUNCH(k_init_comp, grid_for(N), kThreads, st, core_bits, L.woff, N, comp, L.cmin);
-  LAUNCH(k_fill_comp_arrays, grid_for(C), kThreads, st, C, L.Kc, L.Bc, general ? nullptr : L.kmin);
-  for (size_t r = 1; r < L.ranks.size(); ++r)
-    LAUNCH(k_fill_comp_arrays, grid_for(C), kThreads, st, C, L.ranks[r].Kc, L.ranks[r].Bc, nullptr);
-  KDB_CUDA(cudaGetLastError());
-  for (auto& R : L.ranks) {
-    KDB_CUDA(cudaMemsetAsync(R.ctr, 0, sizeof(RoundCounters), st));
-    if (R.n_rows > 0) {
-      // every row as (v, 0) + a flag, then a stable select: the active list is in row order
-      LAUNCH(k_init_rows, grid_for(R.n_rows), kThreads, st, R.dist, R.n_rows, k, eps, R.row_begin, core_bits, comp,
-             general ? nullptr : L.kmin, R.act[1], R.status);
-      cb = L.cub_bytes;
-      { LaunchScope ls_("cub::DeviceSelect", st, false);
-        KDB_CUDA(cub::DeviceSelect::Flagged(L.cub_tmp, cb, R.act[1], R.status, R.act[0], &R.ctr->n_act[0],
-                                            (int)R.n_rows, st)); }
+  // Filter-Boruvka when a light threshold below eps exists;
+  // plain rows-Boruvka over the whole candidate graph otherwise.
+  const int light_m = env_int("KDB_LIGHT", 8);
+  bool filtered = false;
+  if (env_int("KDB_FILTER", 1) && light_m >= 1 && light_m < m.k) {
+    KDB_TRY(pick_tau(m, light_m, &m.tau));
+    filtered = m.tau < eps;
+  }
+  if (filtered) {
+    KDB_TRY(rows_phase(m, m.tau));
+    bool overflow = false;
+    KDB_TRY(filter_phase(m, eps, &overflow));
+    if (overflow) {  // too many crossing heavy entries for the survivor buffers
+      m.fallback = 1;
+      m.C_heavy = -1;
+      KDB_TRY(rows_phase(m, eps));
+    } else {
+      KDB_TRY(heavy_phase(m));
     }
-    KDB_CUDA(cudaGetLastError());
+  } else {
+    KDB_TRY(rows_phase(m, eps));
   }
-  if (!general) {
-    KDB_TRY(allreduce_min_u32(comm, L.kmin, C, st));
-    for (auto& R : L.ranks) LAUNCH(k_fill_i32, grid_for(C), kThreads, st, R.tgt, C, INT32_MAX);
-  }
-  KDB_CUDA(cudaEventRecord(ev[1], st));
-  // ---- general mode: in-edge lists --------------------------------------------
-  if (general) {
-    for (auto& R : L.ranks) {
-      // counts -> scan -> offsets; e_key (N+1 u64) is scratch for counts and cursors
-      unsigned long long* cursor = reinterpret_cast<unsigned long long*>(L.e_key);
-      KDB_CUDA(cudaMemsetAsync(cursor, 0, (N + 1) * sizeof(unsigned long long), st));
-      if (R.n_rows > 0)
-        LAUNCH(k_in_count, grid_for(R.n_rows), kThreads, st, R.nbr, R.dist, R.n_rows, k, eps, R.row_begin, N,
-                                                            core_bits, cursor);
-      cb = L.cub_bytes;
-      { LaunchScope ls_("cub::DeviceScan", st, false); KDB_CUDA(cub::DeviceScan::ExclusiveSum(L.cub_tmp, cb, cursor, R.in_off, (int)(N + 1), st)); }
-      KDB_CUDA(cudaMemcpyAsync(cursor, R.in_off, (N + 1) * sizeof(unsigned long long),
-                               cudaMemcpyDeviceToDevice, st));
-      if (R.n_rows > 0)
-        LAUNCH(k_in_fill, grid_for(R.n_rows), kThreads, st, R.nbr, R.dist, R.n_rows, k, eps, R.row_begin, N,
-                                                           core_bits, cursor, R.in_src, R.in_w);
-      LAUNCH(k_in_finish, grid_for(N), kThreads, st, R.in_off, N, R.in_len, R.in_act[0], &R.ctr->n_act[1]);
-      KDB_CUDA(cudaGetLastError());
-    }
-  }
-  for (auto& R : L.ranks) {
-    RoundCounters hc;
-    KDB_CUDA(cudaMemcpyAsync(&hc, R.ctr, sizeof(hc), cudaMemcpyDeviceToHost, st));
-    KDB_CUDA(cudaStreamSynchronize(st));
-    R.n_act = hc.n_act[0];  // initial active rows are all awake
-    R.n_in_act = hc.n_act[1];
-  }
-  KDB_CUDA(cudaEventRecord(ev[2], st));
-  KDB_CUDA(cudaEventSynchronize(ev[2]));
-  KDB_CUDA(cudaEventElapsedTime(&ms, ev[0], ev[1]));
-  g_stats[1] = ms;
-  KDB_CUDA(cudaEventElapsedTime(&ms, ev[1], ev[2]));
-  g_stats[5] = ms;
 
-  // ---- Boruvka rounds -------------------------------------------------------------
-  int cur = 0;
-  int rounds = 0, stalls = 0;
-  const uint32_t* kmin_cert = general ? nullptr : L.kmin;
-  double t_min_edges = 0, t_contract = 0;
-  while (C > 0) {
-    ++rounds;
-    // round 1 of exact mode: singleton components, one offer each (no in-lists)
-    const bool direct = rounds == 1 && !general;
-    KDB_CUDA(cudaEventRecord(ev[0], st));
-    // a3: offers (rows, then in-lists), per rank, into that rank's Kc partial
-    for (auto& R : L.ranks) {
-      KDB_CUDA(cudaMemsetAsync(&R.ctr->n_act[0], 0, 3 * sizeof(uint32_t), st));  // n_act[0..1], n_off
-      R.n_slots = 0;
-      // one list of live rows in row order; a flag in each record marks asleep rows
-      const uint32_t n_in = R.n_act;
-      if (n_in) {
-        if (direct) {
-          LAUNCH(k_offer_first, grid_for(n_in), kThreads, st, R.nbr, R.dist, k, eps, R.row_begin, N, core_bits,
-                 L.all_core, comp, R.act[cur], n_in, R.status, R.Kc, R.Bc, R.tgt, &L.ctr->entries);
-        } else {
-          // pass A: the first chunk of every awake row
-          for (uint32_t s0 = 0; s0 < n_in; s0 += g_chunk) {
-            const uint32_t s1 = std::min<uint32_t>(s0 + g_chunk, n_in);
-            if ((k % 4) == 0)
-              LAUNCH(k_offer_rows_t<true>, grid_for(s1 - s0), kThreads, st, R.nbr, R.dist, k, eps, R.row_begin, N,
-                     core_bits, L.all_core, comp, R.act[cur], s0, s1, R.status, R.off_key, R.off_b, nullptr,
-                     (unsigned long long*)R.Kc, &L.ctr->entries, g_qmax);
-            else
-              LAUNCH(k_offer_rows_t<false>, grid_for(s1 - s0), kThreads, st, R.nbr, R.dist, k, eps, R.row_begin, N,
-                     core_bits, L.all_core, comp, R.act[cur], s0, s1, R.status, R.off_key, R.off_b, nullptr,
-                     (unsigned long long*)R.Kc, &L.ctr->entries, g_qmax);
-          }
-          // lazy Boruvka + scans of the rows that might supply their component's minimum
-          KDB_CUDA(cudaMemsetAsync(&R.ctr->n_cont, 0, sizeof(uint32_t), st));
-          LAUNCH(k_scan_tiles, grid_for((int64_t)n_in), kThreads, st, R.nbr, R.dist, k, eps, R.row_begin, N,
-                 core_bits, L.all_core, comp, R.act[cur], n_in, R.status, R.off_key, R.off_b,
-                 (unsigned long long*)R.Kc, g_lazy, &L.ctr->entries, &R.ctr->n_cont, g_fa, g_fs);
-        }
-        // next list: rows that offered (awake) or were deferred (asleep), row order kept
-        cb = L.cub_bytes;
-        {
-          LaunchScope ls_("cub::DeviceSelect", st, false);
-          thrust::transform_iterator<Survives, const uint8_t*, bool> keep(R.status, Survives{});
-          KDB_CUDA(cub::DeviceSelect::Flagged(L.cub_tmp, cb, R.act[cur], keep, R.act[cur ^ 1], &R.ctr->n_act[0],
-                                              (int)n_in, st));
-        }
-        R.n_slots = direct ? 0 : n_in;
-      }
-      if (general && R.n_in_act)
-        LAUNCH(k_offer_in, grid_for(R.n_in_act), kThreads, st, R.in_off, R.in_len, R.in_src, R.in_w, comp,
-               R.in_act[cur], R.n_in_act, R.in_act[cur ^ 1], &R.ctr->n_act[1], R.off_v + R.off_cap_rows,
-               R.off_key + R.off_cap_rows, R.off_b + R.off_cap_rows, &R.ctr->n_off, (unsigned long long*)R.Kc);
-      KDB_CUDA(cudaGetLastError());
-    }
-    if (g_trace) {
-      RoundCounters h0, hr;
-      KDB_CUDA(cudaMemcpyAsync(&h0, L.ctr, sizeof(h0), cudaMemcpyDeviceToHost, st));
-      KDB_CUDA(cudaMemcpyAsync(&hr, L.ranks[0].ctr, sizeof(hr), cudaMemcpyDeviceToHost, st));
-      KDB_CUDA(cudaEventRecord(ev[3], st));
-      KDB_CUDA(cudaEventSynchronize(ev[3]));
-      float tms = 0;
-      KDB_CUDA(cudaEventElapsedTime(&tms, ev[0], ev[3]));
-      static unsigned long long last_entries = 0;
-      if (rounds == 1) last_entries = 0;
-      fprintf(stderr, "[kdb] round %d C=%lld live=%u scanned=%u -> live=%u entries=%llu offer_ms=%.3f\n",
-              rounds, (long long)C, L.ranks[0].n_act, hr.n_cont, hr.n_act[0], h0.entries - last_entries, tms);
-      last_entries = h0.entries;
-    }
-    for (auto& R : L.ranks) {
-      RoundCounters hc;
-      KDB_CUDA(cudaMemcpyAsync(&hc, R.ctr, sizeof(hc), cudaMemcpyDeviceToHost, st));
-      KDB_CUDA(cudaStreamSynchronize(st));
-      R.n_act = hc.n_act[0];
-      R.n_in_act = hc.n_act[1];
-      R.n_off = hc.n_off;  // in-list offers (row offers live in the row slots)
-    }
-    // exchange: sim -> min over virtual ranks; nccl -> allreduce
-    for (size_t r = 1; r < L.ranks.size(); ++r)
-      LAUNCH(k_min_into_u64, grid_for(C), kThreads, st, L.Kc, L.ranks[r].Kc, C);
-    KDB_TRY(allreduce_min_u64(comm, L.Kc, C, st));
-    // a4: ties (the direct round already wrote Bc and the targets)
-    for (auto& R : L.ranks) {
-      if (R.n_slots && !direct)
-        LAUNCH(k_tie_slots, grid_for(R.n_slots), kThreads, st, R.act[cur], R.status, R.off_key, R.off_b,
-               R.n_slots, comp, L.Kc, R.Bc);
-      if (R.n_off && !direct)
-        LAUNCH(k_tie, grid_for(R.n_off), kThreads, st, R.off_v + R.off_cap_rows, R.off_key + R.off_cap_rows,
-               R.off_b + R.off_cap_rows, R.n_off, comp, L.Kc, R.Bc);
-      KDB_CUDA(cudaGetLastError());
-    }
-    for (size_t r = 1; r < L.ranks.size(); ++r)
-      LAUNCH(k_min_into_u32, grid_for(C), kThreads, st, L.Bc, L.ranks[r].Bc, C);
-    KDB_TRY(allreduce_min_u32(comm, L.Bc, C, st));
-    if (direct) {
-      for (size_t r = 1; r < L.ranks.size(); ++r)
-        LAUNCH(k_min_into_u32, grid_for(C), kThreads, st, (uint32_t*)L.tgt, (const uint32_t*)L.ranks[r].tgt, C);
-      KDB_TRY(allreduce_min_u32(comm, (uint32_t*)L.tgt, C, st));  // non-owners hold INT32_MAX
-    }
-    KDB_CUDA(cudaEventRecord(ev[1], st));
-    // a5: hook + emit
-    KDB_CUDA(cudaMemsetAsync(&L.ctr->hooks, 0, 4 * sizeof(uint32_t), st));
-    LAUNCH(k_hook, grid_for(C), kThreads, st, C, L.Kc, L.Bc, direct ? L.tgt : nullptr, kmin_cert, comp, L.parent,
-           L.e_key, L.e_w, N, L.ctr);
-    KDB_CUDA(cudaGetLastError());
-    RoundCounters hc;
-    KDB_CUDA(cudaMemcpyAsync(&hc, L.ctr, sizeof(hc), cudaMemcpyDeviceToHost, st));
-    KDB_CUDA(cudaStreamSynchronize(st));
-    if (hc.offered == 0) {  // a8: no component has a leaving edge
-      KDB_CUDA(cudaEventRecord(ev[2], st));
-      KDB_CUDA(cudaEventSynchronize(ev[2]));
-      KDB_CUDA(cudaEventElapsedTime(&ms, ev[0], ev[1]));
-      t_min_edges += ms;
-      break;
-    }
-    if (hc.hooks == 0) {
-      // every offering component abstained: one edge-centric sweep round gives
-      // every component its exact minimum (both endpoints see every entry)
-      ++stalls;
-      LAUNCH(k_fill_comp_arrays, grid_for(C), kThreads, st, C, L.Kc, L.Bc, nullptr);
-      for (size_t r = 1; r < L.ranks.size(); ++r)
-        LAUNCH(k_fill_comp_arrays, grid_for(C), kThreads, st, C, L.ranks[r].Kc, L.ranks[r].Bc, nullptr);
-      for (auto& R : L.ranks)
-        if (R.n_rows)
-          LAUNCH(k_sweep, grid_for(R.n_act), kThreads, st, R.nbr, R.dist, k, eps, R.row_begin, N, core_bits,
-                 comp, R.act[cur ^ 1], R.n_act, (unsigned long long*)R.Kc, R.Bc, 0);
-      for (size_t r = 1; r < L.ranks.size(); ++r)
-        LAUNCH(k_min_into_u64, grid_for(C), kThreads, st, L.Kc, L.ranks[r].Kc, C);
-      KDB_TRY(allreduce_min_u64(comm, L.Kc, C, st));
-      for (auto& R : L.ranks)
-        if (R.n_rows)
-          LAUNCH(k_sweep, grid_for(R.n_act), kThreads, st, R.nbr, R.dist, k, eps, R.row_begin, N, core_bits,
-                 comp, R.act[cur ^ 1], R.n_act, (unsigned long long*)L.Kc, R.Bc, 1);
-      for (size_t r = 1; r < L.ranks.size(); ++r)
-        LAUNCH(k_min_into_u32, grid_for(C), kThreads, st, L.Bc, L.ranks[r].Bc, C);
-      KDB_TRY(allreduce_min_u32(comm, L.Bc, C, st));
-      KDB_CUDA(cudaMemsetAsync(&L.ctr->hooks, 0, 4 * sizeof(uint32_t), st));
-      LAUNCH(k_hook, grid_for(C), kThreads, st, C, L.Kc, L.Bc, nullptr, nullptr, comp, L.parent, L.e_key, L.e_w, N,
-                                               L.ctr);
-      KDB_CUDA(cudaGetLastError());
-      KDB_CUDA(cudaMemcpyAsync(&hc, L.ctr, sizeof(hc), cudaMemcpyDeviceToHost, st));
-      KDB_CUDA(cudaStreamSynchronize(st));
-      if (hc.hooks == 0) return set_err(KDB_EINTERNAL, "sweep round made no progress");
-      // vertices whose rows were exhausted stay out of the active list; rows
-      // that still hold leaving entries are in it (exhaustion is permanent)
-    }
-    if (hc.violation) return set_err(KDB_EINVAL, "graph violates the KDB_GRAPH_EXACT promise (a component's "
-                                     "minimum missed an incident edge)");
-    // a6: contract
-    LAUNCH(k_jump, grid_for(C), kThreads, st, C, L.parent, L.rootof, L.ctr);
-    LAUNCH(k_root_flags, grid_for(C), kThreads, st, C, L.rootof, L.flag);
-    cb = L.cub_bytes;
-    { LaunchScope ls_("cub::DeviceScan", st, false); KDB_CUDA(cub::DeviceScan::ExclusiveSum(L.cub_tmp, cb, L.flag, L.newid, (int)C, st)); }
-    uint32_t viol = 0;
-    KDB_CUDA(cudaMemcpyAsync(&viol, &L.ctr->violation, 4, cudaMemcpyDeviceToHost, st));
-    int32_t last[2];
-    KDB_CUDA(cudaMemcpyAsync(&last[0], L.newid + C - 1, 4, cudaMemcpyDeviceToHost, st));
-    KDB_CUDA(cudaMemcpyAsync(&last[1], L.flag + C - 1, 4, cudaMemcpyDeviceToHost, st));
-    KDB_CUDA(cudaStreamSynchronize(st));
-    if (viol) return set_err(KDB_EINTERNAL, "pointer jumping did not converge (hook cycle)");
-    const int64_t C2 = (int64_t)last[0] + last[1];
-    LAUNCH(k_fill_i32, grid_for(C2), kThreads, st, L.cmin2, C2, INT32_MAX);
-    if (!general) LAUNCH(k_fill_i32, grid_for(C2), kThreads, st, (int32_t*)L.kmin2, C2, (int32_t)kInfBits);
-    // map[c] = new dense id of c's tree (reuses `parent`, no longer needed)
-    LAUNCH(k_merge, grid_for(C), kThreads, st, C, L.rootof, L.newid, L.cmin, general ? nullptr : L.kmin, L.cmin2,
-           L.kmin2, L.parent);
-    LAUNCH(k_relabel, grid_for(N), kThreads, st, N, comp, L.parent);
-    LAUNCH(k_fill_comp_arrays, grid_for(C2), kThreads, st, C2, L.Kc, L.Bc, nullptr);
-    for (size_t r = 1; r < L.ranks.size(); ++r)
-      LAUNCH(k_fill_comp_arrays, grid_for(C2), kThreads, st, C2, L.ranks[r].Kc, L.ranks[r].Bc, nullptr);
-    KDB_CUDA(cudaGetLastError());
-    std::swap(L.cmin, L.cmin2);
-    std::swap(L.kmin, L.kmin2);
-    kmin_cert = general ? nullptr : L.kmin;
-    C = C2;
-    cur ^= 1;
-    KDB_CUDA(cudaEventRecord(ev[2], st));
-    KDB_CUDA(cudaEventSynchronize(ev[2]));
-    KDB_CUDA(cudaEventElapsedTime(&ms, ev[0], ev[1]));
-    t_min_edges += ms;
-    KDB_CUDA(cudaEventElapsedTime(&ms, ev[1], ev[2]));
-    t_contract += ms;
-  }
   // ---- finalize ---------------------------------------------------------------------
-  KDB_CUDA(cudaEventRecord(ev[0], st));
+  KDB_CUDA(cudaEventRecord(m.ev[0], st));
   RoundCounters hc;
   KDB_CUDA(cudaMemcpyAsync(&hc, L.ctr, sizeof(hc), cudaMemcpyDeviceToHost, st));
   KDB_CUDA(cudaStreamSynchronize(st));
-  const int64_t m = (int64_t)hc.msf_count;
-  if (m > N) return set_err(KDB_EINTERNAL, "MSF larger than N-1");
-  if (m > mst_cap) return set_err(KDB_EINVAL, "mst_cap %lld < MSF size %lld", (long long)mst_cap, (long long)m);
-  LAUNCH(k_canon, grid_for(N), kThreads, st, N, comp, L.cmin);
+  const int64_t ne = (int64_t)hc.msf_count;
+  if (ne > N) return set_err(KDB_EINTERNAL, "MSF larger than N-1");
+  if (ne > mst_cap) return set_err(KDB_EINVAL, "mst_cap %lld < MSF size %lld", (long long)mst_cap, (long long)ne);
+  if (m.C_heavy >= 0)
+    LAUNCH(k_canon_h, grid_for(N), kThreads, st, N, comp, L.hcomp, L.cmin);
+  else
+    LAUNCH(k_canon, grid_for(N), kThreads, st, N, comp, L.cmin);
   KDB_CUDA(cudaGetLastError());
   unsigned long long bk[256];
-  if (m > 0) {
-    cb = L.cub_bytes;
-    { LaunchScope ls_("cub::DeviceRadixSort", st, false); KDB_CUDA(cub::DeviceRadixSort::SortPairs(L.cub_tmp, cb, L.e_key, L.e_key_sorted, L.e_w, mst_w, (int)m, 0, 64, st)); }
-    LAUNCH(k_split_edges, grid_for(m), kThreads, st, m, L.e_key_sorted, mst_a, mst_b);
+  if (ne > 0) {
+    size_t cb = L.cub_bytes;
+    { LaunchScope ls_("cub::DeviceRadixSort", st, false); KDB_CUDA(cub::DeviceRadixSort::SortPairs(L.cub_tmp, cb, L.e_key, L.e_key_sorted, L.e_w, mst_w, (int)ne, 0, 64, st)); }
+    LAUNCH(k_split_edges, grid_for(ne), kThreads, st, ne, L.e_key_sorted, mst_a, mst_b);
     KDB_CUDA(cudaMemsetAsync(L.buckets, 0, 256 * sizeof(unsigned long long), st));
-    LAUNCH(k_wbuckets, grid_for(m), kThreads, st, m, mst_w, L.buckets);
+    LAUNCH(k_wbuckets, grid_for(ne), kThreads, st, ne, mst_w, L.buckets);
     KDB_CUDA(cudaGetLastError());
     KDB_CUDA(cudaMemcpyAsync(bk, L.buckets, sizeof(bk), cudaMemcpyDeviceToHost, st));
   }
-  KDB_CUDA(cudaEventRecord(ev[1], st));
+  KDB_CUDA(cudaEventRecord(m.ev[1], st));
   KDB_CUDA(cudaStreamSynchronize(st));
-  KDB_CUDA(cudaEventElapsedTime(&ms, ev[0], ev[1]));
+  const double t_fin = elapsed(m.ev[0], m.ev[1]);
   if (g_prof.on) g_prof.drain();
-  *mst_count = m;
-  *mst_weight = m > 0 ? exact_bucket_sum(bk) : 0.0;
-  g_stats[0] = rounds;
-  g_stats[2] = t_min_edges;
-  g_stats[3] = t_contract;
-  g_stats[4] = ms;
-  g_stats[6] = stalls;
-  g_stats[7] = (double)hc.entries;
+  *mst_count = ne;
+  *mst_weight = ne > 0 ? exact_bucket_sum(bk) : 0.0;
+  g_stats[0] = m.rounds;
+  g_stats[1] = m.t_init;
+  g_stats[2] = m.t_min_edges;
+  g_stats[3] = m.t_contract;
+  g_stats[4] = t_fin;
+  g_stats[5] = m.t_inlist;
+  g_stats[6] = m.stalls;
+  g_stats[7] = (double)m.entries;
+  g_stats[8] = m.t_filter;
+  g_stats[9] = m.t_heavy;
+  g_stats[10] = (double)m.survivors;
+  g_stats[11] = m.heavy_rounds;
+  g_stats[12] = filtered ? (double)m.tau : -1.0;
+  g_stats[13] = (double)m.C;
+  g_stats[14] = m.fallback;
   return KDB_OK;
 }
 

@@ -220,3 +220,100 @@ def test_invalid_arguments_raise():
     bad = kdb.Graph(torch.from_numpy(nbr).cuda(), torch.from_numpy(dist).cuda(), n_total=10)
     with pytest.raises(kdb.KdbError):
         kdb.core_mark(bad, 2, 0.5)        # rows outside [0, N)
+
+
+# ---- Filter-Boruvka (light phase + filter + heavy phase) ---------
+@pytest.mark.parametrize("light", ["1", "2", "3", "6"])
+@pytest.mark.parametrize("case", RANDOM_CASES)
+def test_random_graphs_filter(case, light, monkeypatch):
+    """Light thresholds at several columns: the light MSF + filtered heavy MSF
+    must equal Kruskal's MSF of the whole candidate graph on adversarial graphs
+    (ties in random id order, asymmetric weights, padding, w = 0)."""
+    monkeypatch.setenv("KDB_LIGHT", light)
+    n, k, M, seed, levels, sym, pad, zero, local, q = case
+    if int(light) >= k:
+        pytest.skip("light column beyond k")
+    nbr, dist = random_graph(n, k, seed, levels=levels, symmetric=sym, pad_frac=pad, zero_frac=zero, local=local)
+    eps = np.float32(np.quantile(dist[np.isfinite(dist)].astype(np.float64), q))
+    got = run_gpu(nbr, dist, M, eps, exact=False)
+    assert_parity(got, oracle_run(nbr, dist, M, eps))
+
+
+@pytest.mark.parametrize("light", ["2", "4", "8"])
+@pytest.mark.parametrize("exact", [False, True])
+@pytest.mark.parametrize("P", [0, 3])
+def test_c1_filter(c1_graph, light, exact, P, monkeypatch):
+    import paper_2009_04552_b200 as kdb
+    monkeypatch.setenv("KDB_LIGHT", light)
+    X, nbr, dist = c1_graph
+    eps = eps_from_graph(dist, 8, 1.5)
+    got = run_gpu(nbr, dist, 8, eps, exact=exact, comm=kdb.Comm.sim(P) if P else None)
+    assert_parity(got, oracle_run(nbr, dist, 8, eps))
+    st = got["stats"]
+    assert st["tau"] >= 0 and st["fallback"] == 0, st  # the filter path really ran
+    assert st["light_components"] >= 1
+
+
+def test_filter_overflow_falls_back(c1_graph, monkeypatch):
+    """A survivor buffer too small for the crossing heavy entries: kdb_mst
+    reruns plain rows-Boruvka and the result is still exact."""
+    monkeypatch.setenv("KDB_LIGHT", "2")
+    monkeypatch.setenv("KDB_SURVCAP", "0")
+    X, nbr, dist = c1_graph
+    eps = eps_from_graph(dist, 8, 1.5)
+    got = run_gpu(nbr, dist, 8, eps, exact=True)
+    assert_parity(got, oracle_run(nbr, dist, 8, eps))
+    assert got["stats"]["fallback"] == 1 and got["stats"]["survivors"] > 0
+
+
+def test_filter_off_matches(c1_graph, monkeypatch):
+    monkeypatch.setenv("KDB_FILTER", "0")
+    X, nbr, dist = c1_graph
+    eps = eps_from_graph(dist, 8, 1.5)
+    got = run_gpu(nbr, dist, 8, eps, exact=True)
+    assert_parity(got, oracle_run(nbr, dist, 8, eps))
+    assert got["stats"]["tau"] == -1.0
+
+
+@pytest.mark.parametrize("light", ["1", "3", "10"])
+def test_points_filter_exact_graphs(light, monkeypatch):
+    monkeypatch.setenv("KDB_LIGHT", light)
+    rng = np.random.default_rng(int(light))
+    for t in range(3):
+        n = int(rng.integers(200, 3000))
+        X = (rng.standard_normal((n, 3)) * rng.uniform(0.1, 1.0)).astype(np.float32)
+        X[rng.integers(0, n, n // 20)] = X[rng.integers(0, n, n // 20)]
+        k = int(rng.integers(12, 24)); M = int(rng.integers(1, k + 1))
+        nbr, dist = knn_bruteforce(X, k)
+        eps = eps_from_graph(dist, M, float(rng.uniform(0.8, 3.0)))
+        exp = oracle_run(nbr, dist, M, eps)
+        for P in (0, 2):
+            import paper_2009_04552_b200 as kdb
+            comm = kdb.Comm.sim(P) if P else None
+            assert_parity(run_gpu(nbr, dist, M, eps, exact=True, comm=comm), exp)
+            assert_parity(run_gpu(nbr, dist, M, eps, exact=False, comm=comm), exp)
+
+
+@pytest.mark.parametrize("filt", ["0", "1"])
+@pytest.mark.parametrize("case", RANDOM_CASES)
+def test_inplace_rows_mode(case, filt, monkeypatch):
+    """KDB_COMPACT=0: the rows phase reads the graph rows in place instead of
+    the compact light lists (the path taken when the lists exceed capacity)."""
+    monkeypatch.setenv("KDB_COMPACT", "0")
+    monkeypatch.setenv("KDB_FILTER", filt)
+    monkeypatch.setenv("KDB_LIGHT", "2")
+    n, k, M, seed, levels, sym, pad, zero, local, q = case
+    nbr, dist = random_graph(n, k, seed, levels=levels, symmetric=sym, pad_frac=pad, zero_frac=zero, local=local)
+    eps = np.float32(np.quantile(dist[np.isfinite(dist)].astype(np.float64), q))
+    assert_parity(run_gpu(nbr, dist, M, eps, exact=False), oracle_run(nbr, dist, M, eps))
+
+
+@pytest.mark.parametrize("exact", [False, True])
+def test_c1_inplace_rows_mode(c1_graph, exact, monkeypatch):
+    monkeypatch.setenv("KDB_COMPACT", "0")
+    X, nbr, dist = c1_graph
+    eps = eps_from_graph(dist, 8, 1.5)
+    for P in (0, 2):
+        import paper_2009_04552_b200 as kdb
+        got = run_gpu(nbr, dist, 8, eps, exact=exact, comm=kdb.Comm.sim(P) if P else None)
+        assert_parity(got, oracle_run(nbr, dist, 8, eps))
