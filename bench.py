@@ -329,7 +329,8 @@ def run_ours(args):
                                      ("init_ms", "min_edges_ms", "contract_ms", "filter_ms", "heavy_ms",
                                       "finalize_ms")},
                         "filter": {k_: stats[-1][k_] for k_ in
-                                   ("tau", "light_components", "survivors", "heavy_rounds", "fallback")}}}
+                                   ("tau", "light_components", "survivors", "heavy_rounds", "fallback",
+                                    "filter_exceptions", "filter_slow_entries")}}}
         emit(line, args)
     if comm is not None:
         comm.close()

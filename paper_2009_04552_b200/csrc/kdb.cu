@@ -56,7 +56,7 @@
 namespace {
 
 thread_local std::string g_err;
-thread_local double g_stats[16];
+thread_local double g_stats[20];
 
 kdb_status set_err(kdb_status s, const char* fmt, ...) {
   char buf[512];
@@ -88,14 +88,31 @@ constexpr uint32_t kInfBits = 0x7f800000u;
 constexpr int kThreads = 256;
 
 inline int grid_for(int64_t n, int per_block = kThreads) {
-  (void)0;
   int64_t g = (n + per_block - 1) / per_block;
   if (g < 1) g = 1;
-  // grid-stride kernels: at most one resident wave (8 x 256-thread CTAs per SM);
-  // a second wave would only start after the first finished ALL its strides
-  const int cap = getenv("KDB_GRIDCAP") ? atoi(getenv("KDB_GRIDCAP")) : 148 * 8;
-  if (g > cap) g = cap;
+  if (g > (1 << 30)) g = 1 << 30;
   return (int)g;
+}
+
+// Grid-stride kernels run exactly one resident wave: min(requested, resident
+// CTAs per SM x SMs), from the occupancy calculator (cached per kernel).  A
+// second wave would only start after the first finished ALL its strides.
+int resident_cap(const void* kern, int block) {
+  static std::vector<std::pair<const void*, int>> cache;
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  for (auto& e : cache)
+    if (e.first == kern) return e.second;
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, block, 0) != cudaSuccess || per_sm < 1) per_sm = 1;
+  const int cap = per_sm * sms;
+  cache.emplace_back(kern, cap);
+  return cap;
 }
 
 // ============================================================================
@@ -171,10 +188,32 @@ struct LaunchScope {
   }
 };
 // LAUNCH(kernel, grid, block, stream, args...) -- every kernel of the hot path
-#define LAUNCH(kern, grid, block, st, ...)             \
-  do {                                                 \
-    LaunchScope ls_(#kern, st);                        \
-    kern<<<(grid), (block), 0, (st)>>>(__VA_ARGS__);   \
+#define LAUNCH(kern, grid, block, st, ...)                                          \
+  do {                                                                              \
+    LaunchScope ls_(#kern, st);                                                     \
+    const int g_ = std::min<int>((grid), resident_cap((const void*)(kern), (block))); \
+    kern<<<g_, (block), 0, (st)>>>(__VA_ARGS__);                                    \
+  } while (0)
+
+// LAUNCH_DYN: the same with dynamic shared memory (opt-in above 48 KB)
+int resident_cap_smem(const void* kern, int block, size_t smem) {
+  static std::vector<std::pair<const void*, int>> cache;
+  for (auto& e : cache)
+    if (e.first == kern) return e.second;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int sms = 148, dev = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, block, smem) != cudaSuccess || per_sm < 1)
+    per_sm = 1;
+  cache.emplace_back(kern, per_sm * sms);
+  return per_sm * sms;
+}
+#define LAUNCH_DYN(kern, grid, block, smem, st, ...)                                           \
+  do {                                                                                         \
+    LaunchScope ls_(#kern, st);                                                                \
+    const int g_ = std::min<int>((grid), resident_cap_smem((const void*)(kern), (block), (smem))); \
+    kern<<<g_, (block), (smem), (st)>>>(__VA_ARGS__);                                          \
   } while (0)
 
 // ============================================================================
@@ -257,7 +296,8 @@ struct RoundCounters {
                                  // KDB_GRAPH_EXACT promise was false (or a bug)
   uint32_t n_cont;               // rows continuing in the warp-per-row scan
   uint32_t pad1;
-  uint32_t part[2];              // next round: awake rows, asleep rows
+  uint32_t grab;                 // chunk cursor of the ordered row kernels (per rank)
+  uint32_t pad2;
   unsigned long long entries;    // graph entries (id + weight) read by offer kernels
 };
 
@@ -614,54 +654,105 @@ __global__ void __launch_bounds__(256) k_offer_round(const int32_t* __restrict__
 // prefix (w <= eps_run) runs past column kW continue in the graph row itself.
 constexpr int kW = 16;
 
-// one thread per row: 4 x (int4 + float4) loads in flight, 8 x int4 stores;
-// exact mode also writes the certificate bound kth'(v) into kmin[comp v]
+// records per chunk of the ordered row kernels (see k_light_first)
+constexpr int kChunk = 1024;
+// per-row filter metadata (written by the light pass): bits 0-14 light prefix
+// length (kW = "kW or more"), bit 15 = every entry of the row is within eps
+constexpr uint16_t kMetaAllIn = 0x8000u;
+constexpr uint16_t kMetaSkip = 0x7fffu;  // non-core row
+
+// one thread per row: 4 x (int4 + float4) loads in flight, 8 x int4 stores.
+// Exact mode also writes the certificate bound kth'(v) into kmin[comp v]; kth
+// is only loaded when the ELL row is entirely within eps (else kth > eps).
+// Rows are taken in ordered chunks; the initial list keeps row order.
 template <bool VEC>
 __global__ void __launch_bounds__(256) k_light_ell(const int32_t* __restrict__ nbr, const float* __restrict__ dist,
                                                    int64_t n_rows, int32_t k, float eps, int64_t row_begin,
                                                    const int32_t* __restrict__ comp, uint32_t* __restrict__ kmin,
                                                    int4* __restrict__ LE, Rec* __restrict__ act,
-                                                   uint32_t* __restrict__ n_act) {
-  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n_rows; base += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = base + threadIdx.x;
-    bool want = false;
-    const int64_t v = row_begin + i;
-    if (i < n_rows) {
+                                                   uint32_t* __restrict__ n_act, uint32_t* __restrict__ grab,
+                                                   uint16_t* __restrict__ meta, float eps_full) {
+  __shared__ Rec s_rec[kChunk];
+  __shared__ uint32_t s_n, s_chunk, s_base;
+  for (;;) {
+    if (threadIdx.x == 0) { s_chunk = atomicAdd(grab, 1u); s_n = 0; }
+    __syncthreads();
+    const int64_t base = (int64_t)s_chunk * kChunk;
+    if (base >= n_rows) break;
+    for (int t = 0; t < kChunk; t += 256) {
+      const int64_t i = base + t + threadIdx.x;
+      if (i >= n_rows) continue;
+      const int64_t v = row_begin + i;
       const int32_t cv = comp[v];
-      if (cv >= 0) {
-        const int32_t* nr = nbr + i * k;
-        const float* dr = dist + i * k;
-        int32_t J[kW];
-        float w[kW];
-        if (VEC && k >= kW) {
-#pragma unroll
-          for (int q = 0; q < kW / 4; ++q) {
-            const int4 j4 = __ldcs(reinterpret_cast<const int4*>(nr + 4 * q));
-            const float4 w4 = __ldcs(reinterpret_cast<const float4*>(dr + 4 * q));
-            J[4 * q] = j4.x; J[4 * q + 1] = j4.y; J[4 * q + 2] = j4.z; J[4 * q + 3] = j4.w;
-            w[4 * q] = w4.x; w[4 * q + 1] = w4.y; w[4 * q + 2] = w4.z; w[4 * q + 3] = w4.w;
-          }
-        } else {
-#pragma unroll
-          for (int c = 0; c < kW; ++c) {
-            J[c] = c < k ? __ldcs(nr + c) : -1;
-            w[c] = c < k ? __ldcs(dr + c) : __int_as_float(0x7f800000);
-          }
-        }
-        if (kmin) {
-          const float kth = __ldcs(dr + (k - 1));
-          kmin[cv] = (kth <= eps) ? mono_bits(kth) : kInfBits;
-        }
-        want = w[0] <= eps;
-        int4* o = LE + i * (kW / 2);
-#pragma unroll
-        for (int q = 0; q < kW / 2; ++q)
-          __stcg(o + q, make_int4(J[2 * q], __float_as_int(w[2 * q]), J[2 * q + 1], __float_as_int(w[2 * q + 1])));
+      if (cv < 0) {
+        if (meta) meta[i] = kMetaSkip;
+        continue;
       }
+      const int32_t* nr = nbr + i * k;
+      const float* dr = dist + i * k;
+      int32_t J[kW];
+      float w[kW];
+      if (VEC && k >= kW) {
+#pragma unroll
+        for (int q = 0; q < kW / 4; ++q) {
+          // L1-allocating loads: the two 16-B halves of a sector are separate
+          // instructions; the second must hit L1, not re-request the sector
+          const int4 j4 = __ldg(reinterpret_cast<const int4*>(nr + 4 * q));
+          const float4 w4 = __ldg(reinterpret_cast<const float4*>(dr + 4 * q));
+          J[4 * q] = j4.x; J[4 * q + 1] = j4.y; J[4 * q + 2] = j4.z; J[4 * q + 3] = j4.w;
+          w[4 * q] = w4.x; w[4 * q + 1] = w4.y; w[4 * q + 2] = w4.z; w[4 * q + 3] = w4.w;
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < kW; ++c) {
+          J[c] = c < k ? __ldg(nr + c) : -1;
+          w[c] = c < k ? __ldg(dr + c) : __int_as_float(0x7f800000);
+        }
+      }
+      // kth = D[v][k-1] >= D[v][kW-1]: only needed when that is within eps_run,
+      // or for the filter's per-row metadata
+      float kth = __int_as_float(0x7f800000);
+      if (meta || k <= kW || w[kW - 1] <= eps) kth = __ldcs(dr + (k - 1));
+      if (kmin) kmin[cv] = (kth <= eps) ? mono_bits(kth) : kInfBits;
+      if (meta) {
+        uint32_t pl = 0;
+#pragma unroll
+        for (int c = 0; c < kW; ++c) pl += (w[c] <= eps) ? 1u : 0u;  // sorted: the light prefix length
+        if (pl >= (uint32_t)kW && k > kW) pl = kW;                   // kW: ">= kW", the filter reads weights
+        meta[i] = (uint16_t)(pl | ((kth <= eps_full) ? kMetaAllIn : 0u));
+      }
+      int4* o = LE + i * (kW / 2);
+#pragma unroll
+      for (int q = 0; q < kW / 2; ++q)
+        __stcg(o + q, make_int4(J[2 * q], __float_as_int(w[2 * q]), J[2 * q + 1], __float_as_int(w[2 * q + 1])));
+      if (w[0] <= eps) s_rec[atomicAdd(&s_n, 1u)] = Rec{(int32_t)v, 0};
     }
-    const uint32_t slot = block_reserve(n_act, want);
-    if (want) act[slot] = Rec{(int32_t)v, 0};
+    __syncthreads();
+    if (threadIdx.x == 0) s_base = s_n ? atomicAdd(n_act, s_n) : 0u;
+    __syncthreads();
+    for (uint32_t j = threadIdx.x; j < s_n; j += blockDim.x) act[s_base + j] = s_rec[j];
+    __syncthreads();
   }
+}
+
+// filter metadata when the rows phase did not run over the ELL (in-place mode)
+__global__ void k_row_meta(const float* __restrict__ dist, int64_t n_rows, int32_t k, float tau, float eps,
+                           int64_t row_begin, const int32_t* __restrict__ comp, uint16_t* __restrict__ meta) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_rows; i += (int64_t)gridDim.x * blockDim.x) {
+    if (comp[row_begin + i] < 0) { meta[i] = kMetaSkip; continue; }
+    const float* dr = dist + i * k;
+    uint32_t pl = 0;
+    for (int c = 0; c < kW && c < k; ++c) pl += (__ldg(dr + c) <= tau) ? 1u : 0u;
+    if (pl >= (uint32_t)kW && k > kW) pl = kW;
+    meta[i] = (uint16_t)(pl | ((__ldg(dr + k - 1) <= eps) ? kMetaAllIn : 0u));
+  }
+}
+
+// one 32-byte load (sm_100: LDG.E.ENL2.256); p must be 32-byte aligned
+__device__ __forceinline__ void ld256(const int4* p, int4& a, int4& b) {
+  asm volatile("ld.global.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
+               : "l"(p));
 }
 
 // Scan row v (component cv) from head h: columns < kW from the ELL row, the
@@ -679,8 +770,8 @@ __device__ __forceinline__ RowScan scan_ell(const int4* __restrict__ le, const i
   int c0 = h & ~3;
   bool done = false;
   while (!done && c0 < kend) {
-    const int4 p0 = __ldcg(le + (c0 >> 1));
-    const int4 p1 = __ldcg(le + (c0 >> 1) + 1);
+    int4 p0, p1;
+    ld256(le + (c0 >> 1), p0, p1);
     const int32_t J[4] = {p0.x, p0.z, p1.x, p1.z};
     const float w[4] = {__int_as_float(p0.y), __int_as_float(p0.w), __int_as_float(p1.y), __int_as_float(p1.w)};
     int32_t cj[4];
@@ -740,33 +831,52 @@ __device__ __forceinline__ RowScan scan_ell(const int4* __restrict__ le, const i
   return r;
 }
 
+// The row kernels below take their input in ORDER: a block grabs the next
+// chunk of kChunk records from a cursor, so all SMs work on neighbouring rows
+// at any time and the component gathers of a cluster stay L2-resident (random
+// gathers run at ~2.9e11/s while their working set is below ~64 MB, at DRAM
+// rates beyond).  Outputs are staged in shared memory and written with ONE
+// global reservation per chunk, so the next list keeps the order too.
+
+
 // round 1 (exact mode, singletons) over the ELL; see k_offer_first
 __global__ void __launch_bounds__(256) k_light_first(const int4* __restrict__ LE, const int32_t* __restrict__ nbr,
                                                      const float* __restrict__ dist, int32_t k, float eps,
                                                      int64_t row_begin, int64_t N, const int32_t* __restrict__ comp,
                                                      int all_core, const Rec* __restrict__ act, uint32_t n_in,
                                                      Rec* __restrict__ act_out, uint32_t* __restrict__ n_out,
+                                                     uint32_t* __restrict__ grab,
                                                      uint64_t* __restrict__ Kc, uint32_t* __restrict__ Bc,
                                                      int32_t* __restrict__ tgt, unsigned long long* __restrict__ n_entries) {
+  __shared__ Rec s_rec[kChunk];
+  __shared__ uint32_t s_n, s_chunk, s_base;
   unsigned long long reads = 0;
-  for (uint32_t base = blockIdx.x * blockDim.x; base < n_in; base += gridDim.x * blockDim.x) {
-    const uint32_t s = base + threadIdx.x;
-    RowScan r{false, 0, kSent, kSentB, -1};
-    int32_t v = -1;
-    if (s < n_in) {
+  for (;;) {
+    if (threadIdx.x == 0) { s_chunk = atomicAdd(grab, 1u); s_n = 0; }
+    __syncthreads();
+    const uint64_t base = (uint64_t)s_chunk * kChunk;
+    if (base >= n_in) break;
+    for (int t = 0; t < kChunk; t += 256) {
+      const uint64_t s = base + t + threadIdx.x;
+      if (s >= n_in) continue;
       const int2 a = __ldcs(reinterpret_cast<const int2*>(act + s));
-      v = a.x;
+      const int32_t v = a.x;
       const int64_t i = (int64_t)v - row_begin;
-      r = scan_ell<true>(LE + i * (kW / 2), nbr + i * k, dist + i * k, k, eps, v, -1, a.y, N, comp, all_core, reads);
+      const RowScan r = scan_ell<true>(LE + i * (kW / 2), nbr + i * k, dist + i * k, k, eps, v, -1, a.y, N, comp,
+                                       all_core, reads);
       if (r.found) {
         const int32_t cv = all_core ? v : gat(comp + v);
         Kc[cv] = r.best;
         Bc[cv] = r.bestb;
         tgt[cv] = r.bestc;
+        s_rec[atomicAdd(&s_n, 1u)] = Rec{v, r.h};
       }
     }
-    const uint32_t slot = block_reserve(n_out, r.found);
-    if (r.found) act_out[slot] = Rec{v, r.h};
+    __syncthreads();
+    if (threadIdx.x == 0) s_base = s_n ? atomicAdd(n_out, s_n) : 0u;
+    __syncthreads();
+    for (uint32_t j = threadIdx.x; j < s_n; j += blockDim.x) act_out[s_base + j] = s_rec[j];
+    __syncthreads();
   }
   for (int o = 16; o > 0; o >>= 1) reads += __shfl_xor_sync(0xffffffffu, reads, o);
   if ((threadIdx.x & 31) == 0 && reads) atomicAdd(n_entries, reads);
@@ -778,26 +888,42 @@ __global__ void __launch_bounds__(256) k_light_round(const int4* __restrict__ LE
                                                      int64_t row_begin, int64_t N, const int32_t* __restrict__ comp,
                                                      const Rec* __restrict__ act, uint32_t n_in,
                                                      Rec* __restrict__ act_out, uint32_t* __restrict__ n_out,
-                                                     Offer* __restrict__ offers, unsigned long long* __restrict__ Kc,
+                                                     uint32_t* __restrict__ grab, Offer* __restrict__ offers,
+                                                     unsigned long long* __restrict__ Kc,
                                                      unsigned long long* __restrict__ n_entries) {
+  __shared__ Rec s_rec[kChunk];
+  __shared__ Offer s_off[kChunk];
+  __shared__ uint32_t s_n, s_chunk, s_base;
   unsigned long long reads = 0;
-  for (uint32_t base = blockIdx.x * blockDim.x; base < n_in; base += gridDim.x * blockDim.x) {
-    const uint32_t s = base + threadIdx.x;
-    RowScan r{false, 0, kSent, kSentB, -1};
-    int32_t v = -1, cv = -1;
-    if (s < n_in) {
+  for (;;) {
+    if (threadIdx.x == 0) { s_chunk = atomicAdd(grab, 1u); s_n = 0; }
+    __syncthreads();
+    const uint64_t base = (uint64_t)s_chunk * kChunk;
+    if (base >= n_in) break;
+    for (int t = 0; t < kChunk; t += 256) {
+      const uint64_t s = base + t + threadIdx.x;
+      if (s >= n_in) continue;
       const int2 a = __ldcs(reinterpret_cast<const int2*>(act + s));
-      v = a.x;
-      cv = gat(comp + v);
+      const int32_t v = a.x;
+      const int32_t cv = gat(comp + v);
       const int64_t i = (int64_t)v - row_begin;
-      r = scan_ell<false>(LE + i * (kW / 2), nbr + i * k, dist + i * k, k, eps, v, cv, a.y, N, comp, 0, reads);
-      if (r.found) atomicMin(Kc + cv, (unsigned long long)r.best);
+      const RowScan r = scan_ell<false>(LE + i * (kW / 2), nbr + i * k, dist + i * k, k, eps, v, cv, a.y, N, comp,
+                                        0, reads);
+      if (r.found) {
+        atomicMin(Kc + cv, (unsigned long long)r.best);
+        const uint32_t j = atomicAdd(&s_n, 1u);
+        s_rec[j] = Rec{v, r.h};
+        s_off[j] = Offer{cv, r.bestb, r.best};
+      }
     }
-    const uint32_t slot = block_reserve(n_out, r.found);
-    if (r.found) {
-      act_out[slot] = Rec{v, r.h};
-      offers[slot] = Offer{cv, r.bestb, r.best};
+    __syncthreads();
+    if (threadIdx.x == 0) s_base = s_n ? atomicAdd(n_out, s_n) : 0u;
+    __syncthreads();
+    for (uint32_t j = threadIdx.x; j < s_n; j += blockDim.x) {
+      act_out[s_base + j] = s_rec[j];
+      offers[s_base + j] = s_off[j];
     }
+    __syncthreads();
   }
   for (int o = 16; o > 0; o >>= 1) reads += __shfl_xor_sync(0xffffffffu, reads, o);
   if ((threadIdx.x & 31) == 0 && reads) atomicAdd(n_entries, reads);
@@ -1141,97 +1267,252 @@ struct HEdge {     // a survivor: a heavy candidate entry that crosses light com
 };
 static_assert(sizeof(HEdge) == 24, "HEdge layout");
 
-// One pass over this rank's rows, 4 entries (one int4 + one float4) per thread
-// and step when k % 4 == 0 (a 4-chunk never straddles rows), 1 otherwise.
-// Survivor iff tau < w <= eps, J a valid core id != v (comp[J] >= 0) and
-// comp[J] != comp[v] (v core).  comp is the light phase's dense component id.
+// ---------------------------------------------------------------------------
+// Filter fast path (exact).  Most heavy entries join two vertices of the same
+// light component, and ids are block-local (points of a cluster have nearby
+// ids), so the per-entry component gather is replaced by two shared-memory
+// probes:  id block J >> dom_shift has a dominant component dom[blk]; the
+// exceptions X = {x core : comp[x] != dom[x >> dom_shift]} go into a Bloom
+// filter (no false negatives).  If dom[J >> shift] == comp[v] and J is not
+// (possibly) in X, then comp[J] == comp[v] and the entry is intra -- skipped
+// without touching comp[].  Everything else takes the exact gather.
+constexpr int kDomMax = 16384;         // dom table entries (64 KB of shared memory)
+constexpr int kBloomBits = 1 << 20;    // 128 KB of shared memory
+constexpr int kFilterThreads = 1024;
+constexpr int kFilterUnroll = 4;
+constexpr size_t kFilterSmem = kBloomBits / 8;
+
+__device__ __forceinline__ uint32_t bloom_hash(uint32_t x) {
+  return (x * 0x9E3779B1u) >> (32 - 20);  // kBloomBits = 2^20
+}
+
+// dom[blk]: majority component among 32 sampled vertices of the id block (-1 if none is core)
+__global__ void k_dom(const int32_t* __restrict__ comp, int64_t N, int shift, int64_t nblk,
+                      int32_t* __restrict__ dom) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t blk = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; blk < nblk; blk += nw) {
+    const int64_t lo = blk << shift, len = min((int64_t)1 << shift, N - lo);
+    const int64_t x = lo + (len * lane) / 32;
+    const int32_t c = x < N ? comp[x] : -1;
+    const unsigned grp = __match_any_sync(0xffffffffu, c);
+    int cnt = c >= 0 ? __popc(grp) : 0;
+    int best = cnt, bc = c;
+    for (int o = 16; o > 0; o >>= 1) {
+      const int oc = __shfl_xor_sync(0xffffffffu, best, o);
+      const int ob = __shfl_xor_sync(0xffffffffu, bc, o);
+      if (oc > best || (oc == best && ob > bc)) { best = oc; bc = ob; }
+    }
+    if (lane == 0) dom[blk] = best > 0 ? bc : -1;
+  }
+}
+
+__global__ void k_bloom_build(const int32_t* __restrict__ comp, int64_t N, int shift, const int32_t* __restrict__ dom,
+                              uint32_t* __restrict__ bloom, uint32_t* __restrict__ n_exc) {
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < N; base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t x = base + threadIdx.x;
+    bool exc = false;
+    if (x < N) {
+      const int32_t c = comp[x];
+      exc = c >= 0 && c != dom[x >> shift];
+      if (exc) {
+        const uint32_t h = bloom_hash((uint32_t)x);
+        atomicOr(bloom + (h >> 5), 1u << (h & 31));
+      }
+    }
+    block_count(n_exc, exc);
+  }
+}
+
+// per-component id range [lo, hi) made of a contiguous run of id blocks whose
+// dominant component it is (else empty): rlo/rhi/rcnt are C-sized scratch
+__global__ void k_rng_acc(const int32_t* __restrict__ dom, int64_t nblk, int32_t* __restrict__ rlo,
+                          int32_t* __restrict__ rhi, int32_t* __restrict__ rcnt) {
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nblk; b += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t g = dom[b];
+    if (g < 0) continue;
+    atomicMin(rlo + g, (int32_t)b);
+    atomicMax(rhi + g, (int32_t)b);
+    atomicAdd(rcnt + g, 1);
+  }
+}
+__global__ void k_rng_fin(int64_t C, int64_t N, int shift, const int32_t* __restrict__ rlo,
+                          const int32_t* __restrict__ rhi, const int32_t* __restrict__ rcnt, int2* __restrict__ rng) {
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < C; c += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t n = rcnt[c], lo = rlo[c], hi = rhi[c];
+    if (n > 0 && n == hi - lo + 1)
+      rng[c] = make_int2((int32_t)((int64_t)lo << shift), (int32_t)min(((int64_t)hi + 1) << shift, N));
+    else
+      rng[c] = make_int2(1, 0);
+  }
+}
+
+// q / d by one multiply-high (d > 1: M = ceil(2^64 / d); exact for q < 2^64 / d)
+struct FastDiv {
+  uint64_t M;
+  uint64_t d;
+};
+__device__ __forceinline__ uint64_t fdiv(uint64_t q, const FastDiv& f) { return f.d == 1 ? q : __umul64hi(q, f.M); }
+
+// The filter: every rank streams its rows once, in tiles of kFilterThreads
+// rows.  Per tile, thread i stages row i's data in shared memory (metadata,
+// comp[v], the id range of comp[v]); then the tile's R*k entries are swept in
+// flat order, VEC per thread and step (VEC = 4: an int4 of ids, plus a float4
+// of weights only for rows whose metadata cannot classify entries without
+// them).  An entry is heavy if past the row's light prefix and within eps; a
+// heavy candidate survives iff comp[J] != comp[v].  Fast path: J inside the id
+// range of comp[v] and not in the Bloom filter of the exceptions => comp[J] ==
+// comp[v], no gather.
+struct FRow {
+  uint32_t meta;  // kMetaSkip, or light length | kMetaAllIn
+  int32_t cr;     // comp[v]
+  uint32_t lo;    // id range of comp[v]: [lo, lo + span)
+  uint32_t span;
+};
+
 template <int VEC>
-__global__ void __launch_bounds__(256) k_filter(const int32_t* __restrict__ nbr, const float* __restrict__ dist,
-                                                int64_t n_rows, int32_t k, float tau, float eps, int64_t row_begin,
-                                                int64_t N, const int32_t* __restrict__ comp, HEdge* __restrict__ out,
-                                                uint32_t cap, uint32_t* __restrict__ n_out) {
-  const int64_t total = n_rows * (int64_t)k;
-  const int64_t nchunks = (total + VEC - 1) / VEC;
-  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < nchunks; base += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t q = base + threadIdx.x;
-    int32_t J[VEC];
-    float w[VEC];
-    int64_t row[VEC];
-#pragma unroll
-    for (int j = 0; j < VEC; ++j) { J[j] = -1; w[j] = 0.f; row[j] = 0; }
-    if (q < nchunks) {
-      const int64_t e0 = q * VEC;
-      if (VEC == 4) {
-        const int4 j4 = __ldcs(reinterpret_cast<const int4*>(nbr + e0));
-        const float4 w4 = __ldcs(reinterpret_cast<const float4*>(dist + e0));
-        J[0] = j4.x; J[1] = j4.y; J[2] = j4.z; J[3] = j4.w;
-        w[0] = w4.x; w[1] = w4.y; w[2] = w4.z; w[3] = w4.w;
-        const int64_t r = e0 / k;
-#pragma unroll
-        for (int j = 0; j < VEC; ++j) row[j] = r;
-      } else {
-#pragma unroll
-        for (int j = 0; j < VEC; ++j) {
-          const int64_t e = e0 + j;
-          if (e < total) { J[j] = __ldcs(nbr + e); w[j] = __ldcs(dist + e); row[j] = e / k; }
+__global__ void __launch_bounds__(kFilterThreads) k_filter(
+    const int32_t* __restrict__ nbr, const float* __restrict__ dist, int64_t n_rows, int32_t k, float tau, float eps,
+    int64_t row_begin, int64_t N, const int32_t* __restrict__ comp, const uint16_t* __restrict__ meta,
+    const int2* __restrict__ rng, const uint32_t* __restrict__ bloom, int use_fast, FastDiv fd,
+    HEdge* __restrict__ out, uint32_t cap, uint32_t* __restrict__ n_out, unsigned long long* __restrict__ n_slow) {
+  extern __shared__ uint32_t s_bloom[];
+  __shared__ FRow s_row[kFilterThreads];
+  constexpr int R = kFilterThreads;
+  if (use_fast) {
+    for (int t = threadIdx.x; t < kBloomBits / 32; t += blockDim.x) s_bloom[t] = bloom[t];
+  }
+  const uint32_t Nu = (uint32_t)N;
+  const int64_t n_tiles = (n_rows + R - 1) / R;
+  uint32_t slow = 0;
+  for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    const int64_t r0 = tile * R;
+    const int nr = (int)((n_rows - r0) < R ? (n_rows - r0) : R);
+    __syncthreads();  // previous tile's readers are done with s_row (and the Bloom copy is complete)
+    if ((int)threadIdx.x < nr) {
+      const int64_t i = r0 + threadIdx.x;
+      FRow fr;
+      fr.meta = meta[i];
+      fr.cr = -1;
+      fr.lo = 0;
+      fr.span = 0;
+      if (fr.meta != kMetaSkip) {
+        fr.cr = __ldg(comp + row_begin + i);
+        if (use_fast) {
+          const int2 rg = __ldg(rng + fr.cr);
+          if (rg.y > rg.x) { fr.lo = (uint32_t)rg.x; fr.span = (uint32_t)(rg.y - rg.x); }
         }
       }
+      s_row[threadIdx.x] = fr;
     }
-    bool surv[VEC];
-    int32_t ci[VEC], cj[VEC];
-    int32_t cr = -1;
-    int64_t rlast = -1;
+    __syncthreads();
+    const int64_t e_base = r0 * k;
+    const uint32_t n_chunks = (uint32_t)(((int64_t)nr * k) / VEC);
+    // kFilterUnroll chunks per thread and step: all their id loads are in
+    // flight together (the sweep is bound by load latency x loads in flight)
+    for (uint32_t base = 0; base < n_chunks; base += blockDim.x * kFilterUnroll) {
+      int32_t J[kFilterUnroll][VEC];
+      float w[kFilterUnroll][VEC];
+      uint32_t lr[kFilterUnroll], col[kFilterUnroll];
+      bool act[kFilterUnroll], hw[kFilterUnroll];
 #pragma unroll
-    for (int j = 0; j < VEC; ++j) {
-      surv[j] = false;
-      ci[j] = -1;
-      cj[j] = -1;
-      const int64_t v = row_begin + row[j];
-      if (J[j] >= 0 && J[j] < N && J[j] != v && w[j] > tau && w[j] <= eps) {
-        if (row[j] != rlast) { cr = gat(comp + v); rlast = row[j]; }
-        if (cr >= 0) {
-          const int32_t c2 = gat(comp + J[j]);
-          ci[j] = cr;
-          cj[j] = c2;
-          surv[j] = c2 >= 0 && c2 != cr;
+      for (int t = 0; t < kFilterUnroll; ++t) {
+        const uint32_t u = base + t * blockDim.x + threadIdx.x;
+        act[t] = false;
+        hw[t] = false;
+        lr[t] = 0;
+        col[t] = 0;
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) { J[t][j] = -1; w[t][j] = 0.f; }
+        if (u < n_chunks) {
+          const uint32_t n = u * VEC;
+          lr[t] = (uint32_t)fdiv(n, fd);
+          col[t] = n - lr[t] * (uint32_t)k;
+          const uint32_t m = s_row[lr[t]].meta;
+          const uint32_t pl = m & 0x7fffu;
+          hw[t] = (m & kMetaAllIn) == 0 || pl >= (uint32_t)kW;
+          act[t] = m != kMetaSkip && (hw[t] || col[t] + VEC > pl);
+          if (act[t]) {
+            const int64_t e0 = e_base + n;
+            if (VEC == 4) {
+              const int4 j4 = __ldcs(reinterpret_cast<const int4*>(nbr + e0));
+              J[t][0] = j4.x; J[t][1] = j4.y; J[t][2] = j4.z; J[t][3] = j4.w;
+              if (hw[t]) {
+                const float4 w4 = __ldcs(reinterpret_cast<const float4*>(dist + e0));
+                w[t][0] = w4.x; w[t][1] = w4.y; w[t][2] = w4.z; w[t][3] = w4.w;
+              }
+            } else {
+              J[t][0] = __ldcs(nbr + e0);
+              if (hw[t]) w[t][0] = __ldcs(dist + e0);
+            }
+          }
         }
       }
-    }
-    int cnt = 0;
 #pragma unroll
-    for (int j = 0; j < VEC; ++j) cnt += surv[j];
-    // warp-aggregated slot reservation
-    const unsigned any = __ballot_sync(0xffffffffu, cnt > 0);
-    if (any) {
-      int incl = cnt;
-      const int lane = threadIdx.x & 31;
+      for (int t = 0; t < kFilterUnroll; ++t) {
+        bool surv[VEC];
+        int32_t cj[VEC];
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int t = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += t;
-      }
-      const int tot = __shfl_sync(0xffffffffu, incl, 31);
-      uint32_t base_slot = 0;
-      if (lane == 31) base_slot = atomicAdd(n_out, (uint32_t)tot);
-      base_slot = __shfl_sync(0xffffffffu, base_slot, 31);
-      uint32_t slot = base_slot + (uint32_t)(incl - cnt);
+        for (int j = 0; j < VEC; ++j) { surv[j] = false; cj[j] = -1; }
+        int32_t cr = -1;
+        if (act[t]) {
+          const FRow fr = s_row[lr[t]];
+          cr = fr.cr;
+          const uint32_t pl = fr.meta & 0x7fffu;
+          const uint32_t v = (uint32_t)(row_begin + r0 + lr[t]);
 #pragma unroll
-      for (int j = 0; j < VEC; ++j) {
-        if (!surv[j]) continue;
-        if (slot < cap) {
-          const int64_t v = row_begin + row[j];
-          HEdge h;
-          h.key = pack_key(mono_bits(w[j]), (uint32_t)min(v, (int64_t)J[j]));
-          h.b = (uint32_t)max(v, (int64_t)J[j]);
-          h.x = ci[j];
-          h.y = cj[j];
-          h.pad = 0;
-          out[slot] = h;
+          for (int j = 0; j < VEC; ++j) {
+            const uint32_t Jj = (uint32_t)J[t][j];
+            const bool heavy = hw[t] ? (w[t][j] > tau && w[t][j] <= eps) : (col[t] + j >= pl);
+            const bool cand = heavy && Jj < Nu && Jj != v;
+            const uint32_t h = bloom_hash(Jj);
+            const uint32_t word = use_fast ? s_bloom[h >> 5] : 0xffffffffu;
+            const bool fast = (Jj - fr.lo) < fr.span && !((word >> (h & 31)) & 1u);
+            const bool need = cand && !fast;
+            slow += need ? 1u : 0u;
+            cj[j] = need ? gat(comp + Jj) : -1;
+            surv[j] = cj[j] >= 0 && cj[j] != cr;
+          }
         }
-        ++slot;
+        int cnt = 0;
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) cnt += surv[j];
+        if (__any_sync(0xffffffffu, cnt > 0)) {
+          int incl = cnt;
+          const int lane = threadIdx.x & 31;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int x = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += x;
+          }
+          const int tot = __shfl_sync(0xffffffffu, incl, 31);
+          uint32_t base_slot = 0;
+          if (lane == 31) base_slot = atomicAdd(n_out, (uint32_t)tot);
+          base_slot = __shfl_sync(0xffffffffu, base_slot, 31);
+          uint32_t slot = base_slot + (uint32_t)(incl - cnt);
+#pragma unroll
+          for (int j = 0; j < VEC; ++j) {
+            if (!surv[j]) continue;
+            if (slot < cap) {
+              const int64_t v = row_begin + r0 + lr[t];
+              const int64_t e = e_base + (int64_t)(lr[t]) * k + col[t] + j;
+              const float wj = hw[t] ? w[t][j] : __ldg(dist + e);
+              HEdge hh;
+              hh.key = pack_key(mono_bits(wj), (uint32_t)min(v, (int64_t)J[t][j]));
+              hh.b = (uint32_t)max(v, (int64_t)J[t][j]);
+              hh.x = cr;
+              hh.y = cj[j];
+              hh.pad = 0;
+              out[slot] = hh;
+            }
+            ++slot;
+          }
+        }
       }
     }
   }
+  for (int o = 16; o > 0; o >>= 1) slow += __shfl_xor_sync(0xffffffffu, slow, o);
+  if ((threadIdx.x & 31) == 0 && slow) atomicAdd(n_slow, (unsigned long long)slow);
 }
 
 // heavy phase, per round: x = hcomp[e.x], y = hcomp[e.y]; intra -> dropped for
@@ -1377,6 +1658,8 @@ struct RankState {
   uint32_t n_act = 0;                 // live rows in act[cur]
   bool compact = false;               // rows phase reads the light ELL (else the graph rows)
   int4* LE = nullptr;                 // light ELL [n_rows][kW] (J, w bits) pairs
+  uint16_t* meta = nullptr;           // filter metadata per row (kMetaAllIn | light length)
+  bool meta_ok = false;
   // offers: [0, n_rows) from rows (same slot as the row's next record),
   // [n_rows, n_rows + N) from in-lists (general mode)
   Offer* offers = nullptr;
@@ -1413,6 +1696,9 @@ struct Layout {
   float* e_w;
   unsigned long long* buckets;
   int32_t* hcomp;   // heavy phase: light component -> heavy component
+  int32_t* dom;     // filter fast path: dominant component per id block
+  uint32_t* bloom;  // filter fast path: Bloom filter of the exceptions
+  unsigned long long* fcount;  // [0] exceptions, [1] slow-path entries
   float* tau_sample;
   RoundCounters* ctr;
   void* cub_tmp;
@@ -1457,6 +1743,9 @@ size_t carve(Layout& L, char* base, bool dry, int64_t N, int nr, const int64_t* 
   L.e_w = cv.take<float>(N + 1);
   L.buckets = cv.take<unsigned long long>(256);
   L.hcomp = cv.take<int32_t>(N + 1);
+  L.dom = cv.take<int32_t>(kDomMax);
+  L.bloom = cv.take<uint32_t>(kBloomBits / 32);
+  L.fcount = cv.take<unsigned long long>(2);
   L.tau_sample = cv.take<float>(kTauSamples);
   L.ctr = cv.take<RoundCounters>(1);
   L.cub_bytes = cub_tmp_bytes(N, N + 1);
@@ -1470,6 +1759,7 @@ size_t carve(Layout& L, char* base, bool dry, int64_t N, int nr, const int64_t* 
     R.act[0] = cv.take<Rec>(n);
     R.act[1] = cv.take<Rec>(n);
     R.LE = cv.take<int4>(n * (kW / 2));
+    R.meta = cv.take<uint16_t>(n);
     R.off_cap_rows = n;
     R.offers = cv.take<Offer>(general ? n + N : n);
     R.ctr = cv.take<RoundCounters>(1);
@@ -1569,8 +1859,10 @@ struct Mst {
   int64_t C_heavy = -1;  // components after the heavy phase (-1: no heavy phase ran)
   int rounds = 0, stalls = 0, heavy_rounds = 0;
   double t_init = 0, t_inlist = 0, t_min_edges = 0, t_contract = 0, t_filter = 0, t_heavy = 0;
-  unsigned long long entries = 0, survivors = 0;
+  unsigned long long entries = 0, survivors = 0, exceptions = 0, slow_entries = 0;
   float tau = 0.f;
+  float eps_full = 0.f;  // the call's eps (the rows phase may run at tau)
+  bool want_meta = false;
   int fallback = 0;
   cudaEvent_t ev[4];
 };
@@ -1653,14 +1945,18 @@ kdb_status rows_phase(Mst& m, float eps_run) {
   for (auto& R : L.ranks) {
     KDB_CUDA(cudaMemsetAsync(R.ctr, 0, sizeof(RoundCounters), st));
     R.compact = false;
+    R.meta_ok = false;
     if (R.n_rows > 0 && use_compact) {
       R.compact = true;
+      R.meta_ok = m.want_meta;
       if (vec)
         LAUNCH(k_light_ell<true>, grid_for(R.n_rows), kThreads, st, R.nbr, R.dist, R.n_rows, k, eps_run,
-               R.row_begin, comp, general ? nullptr : L.kmin, R.LE, R.act[0], &R.ctr->n_act[0]);
+               R.row_begin, comp, general ? nullptr : L.kmin, R.LE, R.act[0], &R.ctr->n_act[0], &R.ctr->grab,
+               m.want_meta ? R.meta : nullptr, m.eps_full);
       else
         LAUNCH(k_light_ell<false>, grid_for(R.n_rows), kThreads, st, R.nbr, R.dist, R.n_rows, k, eps_run,
-               R.row_begin, comp, general ? nullptr : L.kmin, R.LE, R.act[0], &R.ctr->n_act[0]);
+               R.row_begin, comp, general ? nullptr : L.kmin, R.LE, R.act[0], &R.ctr->n_act[0], &R.ctr->grab,
+               m.want_meta ? R.meta : nullptr, m.eps_full);
     }
     if (R.n_rows > 0 && !R.compact)
       LAUNCH(k_init_rows, grid_for(R.n_rows), kThreads, st, R.dist, R.n_rows, k, eps_run, R.row_begin, comp,
@@ -1716,14 +2012,15 @@ kdb_status rows_phase(Mst& m, float eps_run) {
     // a3: offers (rows, then in-lists), per rank, into that rank's Kc partial
     for (auto& R : L.ranks) {
       KDB_CUDA(cudaMemsetAsync(&R.ctr->n_act[0], 0, 3 * sizeof(uint32_t), st));  // n_act[0..1], n_off
+      KDB_CUDA(cudaMemsetAsync(&R.ctr->grab, 0, sizeof(uint32_t), st));
       if (R.n_act && R.compact) {
         if (direct)
           LAUNCH(k_light_first, grid_for(R.n_act), kThreads, st, R.LE, R.nbr, R.dist, k, eps_run, R.row_begin, N,
-                 comp, L.all_core, R.act[cur], R.n_act, R.act[cur ^ 1], &R.ctr->n_act[0], R.Kc, R.Bc, R.tgt,
-                 &L.ctr->entries);
+                 comp, L.all_core, R.act[cur], R.n_act, R.act[cur ^ 1], &R.ctr->n_act[0], &R.ctr->grab, R.Kc, R.Bc,
+                 R.tgt, &L.ctr->entries);
         else
           LAUNCH(k_light_round, grid_for(R.n_act), kThreads, st, R.LE, R.nbr, R.dist, k, eps_run, R.row_begin, N,
-                 comp, R.act[cur], R.n_act, R.act[cur ^ 1], &R.ctr->n_act[0], R.offers,
+                 comp, R.act[cur], R.n_act, R.act[cur ^ 1], &R.ctr->n_act[0], &R.ctr->grab, R.offers,
                  (unsigned long long*)R.Kc, &L.ctr->entries);
       } else if (R.n_act) {
         if (direct) {
@@ -1884,17 +2181,53 @@ kdb_status filter_phase(Mst& m, float eps, bool* overflow) {
   KDB_CUDA(cudaEventRecord(m.ev[0], st));
   // KDB_SURVCAP (tests): a smaller survivor capacity, to exercise the fallback
   const int64_t cap_env = env_int("KDB_SURVCAP", -1);
+  // fast-path tables (identical on every rank: comp is replicated)
+  int shift = 0;
+  while (((m.N + ((int64_t)1 << shift) - 1) >> shift) > kDomMax) ++shift;
+  const int64_t nblk = (m.N + ((int64_t)1 << shift) - 1) >> shift;
+  bool fast = env_int("KDB_FASTFILTER", 1) != 0;
+  unsigned long long fc[2] = {0, 0};
+  int2* rng = reinterpret_cast<int2*>(L.Kc);  // C_L entries; Kc is refilled by the heavy phase
+  KDB_CUDA(cudaMemsetAsync(L.fcount, 0, 2 * sizeof(unsigned long long), st));
+  if (fast) {
+    const int64_t C = m.C;
+    KDB_CUDA(cudaMemsetAsync(L.bloom, 0, kBloomBits / 8, st));
+    LAUNCH(k_dom, grid_for(nblk * 32), kThreads, st, m.comp, m.N, shift, nblk, L.dom);
+    LAUNCH(k_bloom_build, grid_for(m.N), kThreads, st, m.comp, m.N, shift, L.dom, L.bloom,
+           reinterpret_cast<uint32_t*>(L.fcount));
+    LAUNCH(k_fill_i32, grid_for(C), kThreads, st, L.parent, C, INT32_MAX);
+    LAUNCH(k_fill_i32, grid_for(C), kThreads, st, L.rootof, C, -1);
+    LAUNCH(k_fill_i32, grid_for(C), kThreads, st, L.newid, C, 0);
+    LAUNCH(k_rng_acc, grid_for(nblk), kThreads, st, L.dom, nblk, L.parent, L.rootof, L.newid);
+    LAUNCH(k_rng_fin, grid_for(C), kThreads, st, C, m.N, shift, L.parent, L.rootof, L.newid, rng);
+    KDB_CUDA(cudaGetLastError());
+    KDB_CUDA(cudaMemcpyAsync(fc, L.fcount, sizeof(fc), cudaMemcpyDeviceToHost, st));
+    KDB_CUDA(cudaStreamSynchronize(st));
+    fc[0] &= 0xffffffffull;  // block_count wrote the low 32-bit word
+    m.exceptions = fc[0];
+    // a saturated filter would send almost every entry down the slow path
+    if (fc[0] > (unsigned long long)kBloomBits / 4) fast = false;
+  }
   for (auto& R : L.ranks) {
     KDB_CUDA(cudaMemsetAsync(R.n_hs_dev, 0, 2 * sizeof(uint32_t), st));
     if (cap_env >= 0) R.hs_cap = (uint32_t)std::min<int64_t>(R.hs_cap, cap_env);
     if (R.n_rows == 0) continue;
-    const int64_t total = R.n_rows * (int64_t)m.k;
-    if ((m.k % 4) == 0)
-      LAUNCH(k_filter<4>, grid_for(total / 4), kThreads, st, R.nbr, R.dist, R.n_rows, m.k, m.tau, eps, R.row_begin,
-             m.N, m.comp, R.hs[0], R.hs_cap, R.n_hs_dev);
+    if (!R.meta_ok)
+      LAUNCH(k_row_meta, grid_for(R.n_rows), kThreads, st, R.dist, R.n_rows, m.k, m.tau, eps, R.row_begin, m.comp,
+             R.meta);
+    const int vec = (m.k % 4) == 0 ? 4 : 1;
+    FastDiv fd;  // entry index within a tile -> row within the tile
+    fd.d = (uint64_t)m.k;
+    fd.M = fd.d > 1 ? (~0ull / fd.d) + 1 : 0;
+    const int64_t ntiles = (R.n_rows + kFilterThreads - 1) / kFilterThreads;
+    if (vec == 4)
+      LAUNCH_DYN(k_filter<4>, (int)std::min<int64_t>(ntiles, 1 << 30), kFilterThreads, kFilterSmem, st, R.nbr, R.dist,
+                 R.n_rows, m.k, m.tau, eps, R.row_begin, m.N, m.comp, R.meta, rng, L.bloom, fast ? 1 : 0, fd,
+                 R.hs[0], R.hs_cap, R.n_hs_dev, L.fcount + 1);
     else
-      LAUNCH(k_filter<1>, grid_for(total), kThreads, st, R.nbr, R.dist, R.n_rows, m.k, m.tau, eps, R.row_begin,
-             m.N, m.comp, R.hs[0], R.hs_cap, R.n_hs_dev);
+      LAUNCH_DYN(k_filter<1>, (int)std::min<int64_t>(ntiles, 1 << 30), kFilterThreads, kFilterSmem, st, R.nbr, R.dist,
+                 R.n_rows, m.k, m.tau, eps, R.row_begin, m.N, m.comp, R.meta, rng, L.bloom, fast ? 1 : 0, fd,
+                 R.hs[0], R.hs_cap, R.n_hs_dev, L.fcount + 1);
     KDB_CUDA(cudaGetLastError());
   }
   uint32_t over = 0;
@@ -1914,6 +2247,9 @@ kdb_status filter_phase(Mst& m, float eps, bool* overflow) {
     KDB_CUDA(cudaMemcpyAsync(&over, d, 4, cudaMemcpyDeviceToHost, st));
     KDB_CUDA(cudaStreamSynchronize(st));
   }
+  KDB_CUDA(cudaMemcpyAsync(&fc[1], L.fcount + 1, 8, cudaMemcpyDeviceToHost, st));
+  KDB_CUDA(cudaStreamSynchronize(st));
+  m.slow_entries = fc[1];
   KDB_CUDA(cudaEventRecord(m.ev[1], st));
   m.t_filter += elapsed(m.ev[0], m.ev[1]);
   m.survivors = tot;
@@ -2022,7 +2358,7 @@ const char* kdb_status_string(kdb_status s) {
 const char* kdb_last_error(void) { return g_err.c_str(); }
 
 int kdb_last_mst_stats(double* out, int cap) {
-  int n = std::min(cap, 16);
+  int n = std::min(cap, 20);
   for (int i = 0; i < n; ++i) out[i] = g_stats[i];
   return n;
 }
@@ -2186,14 +2522,17 @@ kdb_status kdb_mst(const kdb_graph* g, float eps, const uint32_t* core_bits, int
 
   // Filter-Boruvka when a light threshold below eps exists;
   // plain rows-Boruvka over the whole candidate graph otherwise.
-  const int light_m = env_int("KDB_LIGHT", 8);
+  const int light_m = env_int("KDB_LIGHT", 10);
   bool filtered = false;
   if (env_int("KDB_FILTER", 1) && light_m >= 1 && light_m < m.k) {
     KDB_TRY(pick_tau(m, light_m, &m.tau));
     filtered = m.tau < eps;
   }
+  m.eps_full = eps;
   if (filtered) {
+    m.want_meta = true;
     KDB_TRY(rows_phase(m, m.tau));
+    m.want_meta = false;
     bool overflow = false;
     KDB_TRY(filter_phase(m, eps, &overflow));
     if (overflow) {  // too many crossing heavy entries for the survivor buffers
@@ -2251,6 +2590,8 @@ kdb_status kdb_mst(const kdb_graph* g, float eps, const uint32_t* core_bits, int
   g_stats[12] = filtered ? (double)m.tau : -1.0;
   g_stats[13] = (double)m.C;
   g_stats[14] = m.fallback;
+  g_stats[15] = (double)m.exceptions;
+  g_stats[16] = (double)m.slow_entries;
   return KDB_OK;
 }
 

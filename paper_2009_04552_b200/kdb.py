@@ -210,12 +210,13 @@ def mst(g: Graph, eps: float, core_bits: torch.Tensor, comm: Comm | None = None,
                          C.c_void_p(w.data_ptr()), cap, C.byref(cnt), C.byref(tot),
                          C.c_void_p(workspace.data_ptr()), workspace.numel(), _h(comm), _stream(stream)),
            "kdb_mst")
-    st = (C.c_double * 16)()
-    lib().kdb_last_mst_stats(st, 16)
+    st = (C.c_double * 20)()
+    lib().kdb_last_mst_stats(st, 20)
     stats = dict(rounds=int(st[0]), init_ms=st[1], min_edges_ms=st[2], contract_ms=st[3],
                  finalize_ms=st[4], inlist_ms=st[5], stall_rounds=int(st[6]), entries_read=int(st[7]),
                  filter_ms=st[8], heavy_ms=st[9], survivors=int(st[10]), heavy_rounds=int(st[11]),
-                 tau=st[12], light_components=int(st[13]), fallback=int(st[14]))
+                 tau=st[12], light_components=int(st[13]), fallback=int(st[14]),
+                 filter_exceptions=int(st[15]), filter_slow_entries=int(st[16]))
     m = cnt.value
     return MstResult(comp[:N], a[:m], b[:m], w[:m], m, tot.value, stats)
 

@@ -317,3 +317,25 @@ def test_c1_inplace_rows_mode(c1_graph, exact, monkeypatch):
         import paper_2009_04552_b200 as kdb
         got = run_gpu(nbr, dist, 8, eps, exact=exact, comm=kdb.Comm.sim(P) if P else None)
         assert_parity(got, oracle_run(nbr, dist, 8, eps))
+
+
+@pytest.mark.parametrize("fast", ["0", "1"])
+@pytest.mark.parametrize("light", ["2", "4"])
+def test_filter_fast_path_toggle(c1_graph, fast, light, monkeypatch):
+    """The filter's shared-memory fast path (dominant component per id block +
+    Bloom filter of the exceptions) must give the same survivors as the plain
+    per-entry gather; shuffled ids (no block locality) exercise its slow path."""
+    monkeypatch.setenv("KDB_FASTFILTER", fast)
+    monkeypatch.setenv("KDB_LIGHT", light)
+    X, nbr, dist = c1_graph
+    eps = eps_from_graph(dist, 8, 1.5)
+    got = run_gpu(nbr, dist, 8, eps, exact=True)
+    assert_parity(got, oracle_run(nbr, dist, 8, eps))
+    # the same point set under a random id permutation
+    n = len(X)
+    perm = np.random.default_rng(5).permutation(n)
+    Xp = X[perm]
+    nbr2, dist2 = knn_bruteforce(Xp, 16)
+    eps2 = eps_from_graph(dist2, 8, 1.5)
+    got2 = run_gpu(nbr2, dist2, 8, eps2, exact=True)
+    assert_parity(got2, oracle_run(nbr2, dist2, 8, eps2))
