@@ -1282,8 +1282,13 @@ constexpr int kFilterThreads = 1024;
 constexpr int kFilterUnroll = 4;
 constexpr size_t kFilterSmem = kBloomBits / 8;
 
-__device__ __forceinline__ uint32_t bloom_hash(uint32_t x) {
-  return (x * 0x9E3779B1u) >> (32 - 20);  // kBloomBits = 2^20
+// Blocked Bloom filter: key x selects ONE 32-bit word (top 15 bits of x*C1)
+// and sets 3 bits in it (three 5-bit fields of x*C2): a single shared-memory
+// probe per test, false-positive rate ~1e-4 at ~2e4 keys.
+__device__ __forceinline__ uint32_t bloom_word(uint32_t x) { return (x * 0x9E3779B1u) >> 17; }
+__device__ __forceinline__ uint32_t bloom_mask(uint32_t x) {
+  const uint32_t h = x * 0x85EBCA77u;
+  return (1u << (h >> 27)) | (1u << ((h >> 22) & 31u)) | (1u << ((h >> 17) & 31u));
 }
 
 // dom[blk]: majority component among 32 sampled vertices of the id block (-1 if none is core)
@@ -1315,10 +1320,7 @@ __global__ void k_bloom_build(const int32_t* __restrict__ comp, int64_t N, int s
     if (x < N) {
       const int32_t c = comp[x];
       exc = c >= 0 && c != dom[x >> shift];
-      if (exc) {
-        const uint32_t h = bloom_hash((uint32_t)x);
-        atomicOr(bloom + (h >> 5), 1u << (h & 31));
-      }
+      if (exc) atomicOr(bloom + bloom_word((uint32_t)x), bloom_mask((uint32_t)x));
     }
     block_count(n_exc, exc);
   }
@@ -1351,6 +1353,8 @@ __global__ void k_rng_fin(int64_t C, int64_t N, int shift, const int32_t* __rest
 struct FastDiv {
   uint64_t M;
   uint64_t d;
+  uint32_t m32;  // ceil(2^32 / d): n / d == umulhi(n, m32) for n < 2^32 / d
+  uint32_t pad;
 };
 __device__ __forceinline__ uint64_t fdiv(uint64_t q, const FastDiv& f) { return f.d == 1 ? q : __umul64hi(q, f.M); }
 
@@ -1370,16 +1374,17 @@ struct FRow {
   uint32_t span;
 };
 
-template <int VEC>
+template <int VEC, bool FAST>
 __global__ void __launch_bounds__(kFilterThreads) k_filter(
     const int32_t* __restrict__ nbr, const float* __restrict__ dist, int64_t n_rows, int32_t k, float tau, float eps,
     int64_t row_begin, int64_t N, const int32_t* __restrict__ comp, const uint16_t* __restrict__ meta,
-    const int2* __restrict__ rng, const uint32_t* __restrict__ bloom, int use_fast, FastDiv fd,
+    const int2* __restrict__ rng, const uint32_t* __restrict__ bloom, FastDiv fd,
     HEdge* __restrict__ out, uint32_t cap, uint32_t* __restrict__ n_out, unsigned long long* __restrict__ n_slow) {
   extern __shared__ uint32_t s_bloom[];
   __shared__ FRow s_row[kFilterThreads];
   constexpr int R = kFilterThreads;
-  if (use_fast) {
+  const uint32_t s_base = (uint32_t)__cvta_generic_to_shared(s_bloom);
+  if (FAST) {
     for (int t = threadIdx.x; t < kBloomBits / 32; t += blockDim.x) s_bloom[t] = bloom[t];
   }
   const uint32_t Nu = (uint32_t)N;
@@ -1398,7 +1403,7 @@ __global__ void __launch_bounds__(kFilterThreads) k_filter(
       fr.span = 0;
       if (fr.meta != kMetaSkip) {
         fr.cr = __ldg(comp + row_begin + i);
-        if (use_fast) {
+        if (FAST) {
           const int2 rg = __ldg(rng + fr.cr);
           if (rg.y > rg.x) { fr.lo = (uint32_t)rg.x; fr.span = (uint32_t)(rg.y - rg.x); }
         }
@@ -1406,78 +1411,78 @@ __global__ void __launch_bounds__(kFilterThreads) k_filter(
       s_row[threadIdx.x] = fr;
     }
     __syncthreads();
-    const int64_t e_base = r0 * k;
+    const int32_t* __restrict__ nt = nbr + r0 * k;  // this tile's ids (contiguous)
+    const float* __restrict__ dt = dist + r0 * k;
     const uint32_t n_chunks = (uint32_t)(((int64_t)nr * k) / VEC);
-    // kFilterUnroll chunks per thread and step: all their id loads are in
-    // flight together (the sweep is bound by load latency x loads in flight)
+    // kFilterUnroll chunks per thread and step: their id loads are issued
+    // together (the sweep is bound by load latency x loads in flight)
     for (uint32_t base = 0; base < n_chunks; base += blockDim.x * kFilterUnroll) {
       int32_t J[kFilterUnroll][VEC];
-      float w[kFilterUnroll][VEC];
-      uint32_t lr[kFilterUnroll], col[kFilterUnroll];
-      bool act[kFilterUnroll], hw[kFilterUnroll];
 #pragma unroll
       for (int t = 0; t < kFilterUnroll; ++t) {
         const uint32_t u = base + t * blockDim.x + threadIdx.x;
-        act[t] = false;
-        hw[t] = false;
-        lr[t] = 0;
-        col[t] = 0;
-#pragma unroll
-        for (int j = 0; j < VEC; ++j) { J[t][j] = -1; w[t][j] = 0.f; }
-        if (u < n_chunks) {
-          const uint32_t n = u * VEC;
-          lr[t] = (uint32_t)fdiv(n, fd);
-          col[t] = n - lr[t] * (uint32_t)k;
-          const uint32_t m = s_row[lr[t]].meta;
-          const uint32_t pl = m & 0x7fffu;
-          hw[t] = (m & kMetaAllIn) == 0 || pl >= (uint32_t)kW;
-          act[t] = m != kMetaSkip && (hw[t] || col[t] + VEC > pl);
-          if (act[t]) {
-            const int64_t e0 = e_base + n;
-            if (VEC == 4) {
-              const int4 j4 = __ldcs(reinterpret_cast<const int4*>(nbr + e0));
-              J[t][0] = j4.x; J[t][1] = j4.y; J[t][2] = j4.z; J[t][3] = j4.w;
-              if (hw[t]) {
-                const float4 w4 = __ldcs(reinterpret_cast<const float4*>(dist + e0));
-                w[t][0] = w4.x; w[t][1] = w4.y; w[t][2] = w4.z; w[t][3] = w4.w;
-              }
-            } else {
-              J[t][0] = __ldcs(nbr + e0);
-              if (hw[t]) w[t][0] = __ldcs(dist + e0);
-            }
-          }
+        if (VEC == 4) {
+          const int4 j4 = u < n_chunks ? __ldcs(reinterpret_cast<const int4*>(nt) + u) : make_int4(-1, -1, -1, -1);
+          J[t][0] = j4.x; J[t][1] = j4.y; J[t][2] = j4.z; J[t][3] = j4.w;
+        } else {
+          J[t][0] = u < n_chunks ? __ldcs(nt + u) : -1;
         }
       }
 #pragma unroll
       for (int t = 0; t < kFilterUnroll; ++t) {
-        bool surv[VEC];
-        int32_t cj[VEC];
-#pragma unroll
-        for (int j = 0; j < VEC; ++j) { surv[j] = false; cj[j] = -1; }
-        int32_t cr = -1;
-        if (act[t]) {
-          const FRow fr = s_row[lr[t]];
+        const uint32_t u = base + t * blockDim.x + threadIdx.x;
+        uint32_t survm = 0, lr = 0, col = 0;
+        int32_t cj[VEC], cr = -1;
+        float w[VEC];
+        if (u < n_chunks) {
+          const uint32_t n = u * VEC;
+          lr = (k > 1 && k < 2048) ? __umulhi(n, fd.m32) : (uint32_t)fdiv(n, fd);  // row within the tile
+          col = n - lr * (uint32_t)k;
+          const FRow fr = s_row[lr];
           cr = fr.cr;
-          const uint32_t pl = fr.meta & 0x7fffu;
-          const uint32_t v = (uint32_t)(row_begin + r0 + lr[t]);
+          // Fast test first: J in the id range of comp[v] and not a possible
+          // exception => comp[J] == comp[v].  That also settles light entries,
+          // entries beyond eps and J == v (none is a candidate leaving edge), so
+          // the full classification below only runs for the rare rest.
+          uint32_t slowm = 0;
 #pragma unroll
           for (int j = 0; j < VEC; ++j) {
-            const uint32_t Jj = (uint32_t)J[t][j];
-            const bool heavy = hw[t] ? (w[t][j] > tau && w[t][j] <= eps) : (col[t] + j >= pl);
-            const bool cand = heavy && Jj < Nu && Jj != v;
-            const uint32_t h = bloom_hash(Jj);
-            const uint32_t word = use_fast ? s_bloom[h >> 5] : 0xffffffffu;
-            const bool fast = (Jj - fr.lo) < fr.span && !((word >> (h & 31)) & 1u);
-            const bool need = cand && !fast;
-            slow += need ? 1u : 0u;
-            cj[j] = need ? gat(comp + Jj) : -1;
-            surv[j] = cj[j] >= 0 && cj[j] != cr;
+            uint32_t fast = 0;
+            if (FAST) {
+              const uint32_t Jj = (uint32_t)J[t][j];
+              uint32_t word;
+              asm("ld.shared.u32 %0, [%1];" : "=r"(word) : "r"(s_base + bloom_word(Jj) * 4u));
+              const uint32_t bm = bloom_mask(Jj);
+              fast = (uint32_t)((Jj - fr.lo) < fr.span) & (uint32_t)((word & bm) != bm);
+            }
+            slowm |= ((fast & 1u) ^ 1u) << j;
+          }
+          const uint32_t pl = fr.meta & 0x7fffu;
+          const bool hw = (fr.meta & kMetaAllIn) == 0 || pl >= (uint32_t)kW;  // weights needed to classify
+          if (fr.meta == kMetaSkip) slowm = 0;
+          if (slowm) {
+            const uint32_t v = (uint32_t)(row_begin + r0 + lr);
+            if (VEC == 4) {
+              const float4 w4 = __ldg(reinterpret_cast<const float4*>(dt) + u);
+              w[0] = w4.x; w[1] = w4.y; w[2] = w4.z; w[3] = w4.w;
+            } else {
+              w[0] = __ldg(dt + u);
+            }
+#pragma unroll
+            for (int j = 0; j < VEC; ++j) {
+              cj[j] = -1;
+              const uint32_t Jj = (uint32_t)J[t][j];
+              const bool heavy = hw ? (w[j] > tau && w[j] <= eps) : (col + j >= pl);
+              if (((slowm >> j) & 1u) && heavy && Jj < Nu && Jj != v) {
+                ++slow;
+                cj[j] = gat(comp + Jj);
+                if (cj[j] >= 0 && cj[j] != cr) survm |= 1u << j;
+              }
+            }
           }
         }
-        int cnt = 0;
-#pragma unroll
-        for (int j = 0; j < VEC; ++j) cnt += surv[j];
-        if (__any_sync(0xffffffffu, cnt > 0)) {
+        if (__any_sync(0xffffffffu, survm != 0)) {  // rare: warp-aggregated append
+          const int cnt = __popc(survm);
           int incl = cnt;
           const int lane = threadIdx.x & 31;
 #pragma unroll
@@ -1492,13 +1497,11 @@ __global__ void __launch_bounds__(kFilterThreads) k_filter(
           uint32_t slot = base_slot + (uint32_t)(incl - cnt);
 #pragma unroll
           for (int j = 0; j < VEC; ++j) {
-            if (!surv[j]) continue;
+            if (!((survm >> j) & 1u)) continue;
             if (slot < cap) {
-              const int64_t v = row_begin + r0 + lr[t];
-              const int64_t e = e_base + (int64_t)(lr[t]) * k + col[t] + j;
-              const float wj = hw[t] ? w[t][j] : __ldg(dist + e);
+              const int64_t v = row_begin + r0 + lr;
               HEdge hh;
-              hh.key = pack_key(mono_bits(wj), (uint32_t)min(v, (int64_t)J[t][j]));
+              hh.key = pack_key(mono_bits(w[j]), (uint32_t)min(v, (int64_t)J[t][j]));
               hh.b = (uint32_t)max(v, (int64_t)J[t][j]);
               hh.x = cr;
               hh.y = cj[j];
@@ -2219,15 +2222,18 @@ kdb_status filter_phase(Mst& m, float eps, bool* overflow) {
     FastDiv fd;  // entry index within a tile -> row within the tile
     fd.d = (uint64_t)m.k;
     fd.M = fd.d > 1 ? (~0ull / fd.d) + 1 : 0;
+    fd.m32 = fd.d > 1 ? (uint32_t)((0xffffffffull / fd.d) + 1) : 0;
+    fd.pad = 0;
     const int64_t ntiles = (R.n_rows + kFilterThreads - 1) / kFilterThreads;
-    if (vec == 4)
-      LAUNCH_DYN(k_filter<4>, (int)std::min<int64_t>(ntiles, 1 << 30), kFilterThreads, kFilterSmem, st, R.nbr, R.dist,
-                 R.n_rows, m.k, m.tau, eps, R.row_begin, m.N, m.comp, R.meta, rng, L.bloom, fast ? 1 : 0, fd,
-                 R.hs[0], R.hs_cap, R.n_hs_dev, L.fcount + 1);
-    else
-      LAUNCH_DYN(k_filter<1>, (int)std::min<int64_t>(ntiles, 1 << 30), kFilterThreads, kFilterSmem, st, R.nbr, R.dist,
-                 R.n_rows, m.k, m.tau, eps, R.row_begin, m.N, m.comp, R.meta, rng, L.bloom, fast ? 1 : 0, fd,
-                 R.hs[0], R.hs_cap, R.n_hs_dev, L.fcount + 1);
+    const int grid = (int)std::min<int64_t>(ntiles, 1 << 30);
+#define KDB_FILTER_LAUNCH(V, F)                                                                                  \
+  LAUNCH_DYN((k_filter<V, F>), grid, kFilterThreads, kFilterSmem, st, R.nbr, R.dist, R.n_rows, m.k, m.tau, eps,  \
+             R.row_begin, m.N, m.comp, R.meta, rng, L.bloom, fd, R.hs[0], R.hs_cap, R.n_hs_dev, L.fcount + 1)
+    if (vec == 4 && fast) KDB_FILTER_LAUNCH(4, true);
+    else if (vec == 4) KDB_FILTER_LAUNCH(4, false);
+    else if (fast) KDB_FILTER_LAUNCH(1, true);
+    else KDB_FILTER_LAUNCH(1, false);
+#undef KDB_FILTER_LAUNCH
     KDB_CUDA(cudaGetLastError());
   }
   uint32_t over = 0;
