@@ -1181,13 +1181,36 @@ __global__ void k_canon(int64_t N, int32_t* __restrict__ comp, const int32_t* __
   }
 }
 
-__global__ void k_split_edges(int64_t m, const uint64_t* __restrict__ keys, uint32_t* __restrict__ a,
-                              uint32_t* __restrict__ b) {
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m;
-       e += (int64_t)gridDim.x * blockDim.x) {
+// MSF output in (a, b) order: radix sort on the 32-bit a (only ceil(log2 N)
+// bits) carrying (b, w) as a 64-bit payload, then each run of equal a (tiny:
+// a vertex is the smaller endpoint of few MSF edges) is sorted by b in place.
+__global__ void k_msf_pack(int64_t m, const uint64_t* __restrict__ keys, const float* __restrict__ w,
+                           uint32_t* __restrict__ ka, unsigned long long* __restrict__ vb) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x) {
     const uint64_t x = keys[e];
-    a[e] = (uint32_t)(x >> 32);
-    b[e] = (uint32_t)x;
+    ka[e] = (uint32_t)(x >> 32);
+    vb[e] = (x << 32) | __float_as_uint(w[e]);
+  }
+}
+__global__ void k_msf_unpack(int64_t m, const uint32_t* __restrict__ ka, const unsigned long long* __restrict__ vb,
+                             uint32_t* __restrict__ a, uint32_t* __restrict__ b, float* __restrict__ w) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t ai = ka[i];
+    a[i] = ai;
+    if (i > 0 && ka[i - 1] == ai) continue;  // not the start of a run
+    int64_t j = i + 1;
+    while (j < m && ka[j] == ai) ++j;
+    for (int64_t p = i; p < j; ++p) {  // insertion sort of the run [i, j) by b
+      const unsigned long long x = vb[p];
+      int64_t q = p;
+      while (q > i && (uint32_t)(b[q - 1]) > (uint32_t)(x >> 32)) {
+        b[q] = b[q - 1];
+        w[q] = w[q - 1];
+        --q;
+      }
+      b[q] = (uint32_t)(x >> 32);
+      w[q] = __uint_as_float((uint32_t)x);
+    }
   }
 }
 
@@ -1695,7 +1718,7 @@ struct Layout {
   uint32_t* Bc;
   int32_t* tgt;
   int all_core = 0;
-  uint64_t *e_key, *e_key_sorted;
+  uint64_t* e_key;
   float* e_w;
   unsigned long long* buckets;
   int32_t* hcomp;   // heavy phase: light component -> heavy component
@@ -1714,8 +1737,9 @@ size_t cub_tmp_bytes(int64_t N, int64_t cap_edges) {
   cub::DeviceScan::ExclusiveSum(nullptr, a, (const int32_t*)nullptr, (int32_t*)nullptr, (int)std::max<int64_t>(N + 1, 1));
   cub::DeviceScan::ExclusiveSum(nullptr, b, (const unsigned long long*)nullptr,
                                 (unsigned long long*)nullptr, (int)std::max<int64_t>(N + 1, 1));
-  cub::DeviceRadixSort::SortPairs(nullptr, c, (const uint64_t*)nullptr, (uint64_t*)nullptr,
-                                  (const float*)nullptr, (float*)nullptr, (int)std::max<int64_t>(cap_edges, 1));
+  cub::DeviceRadixSort::SortPairs(nullptr, c, (const uint32_t*)nullptr, (uint32_t*)nullptr,
+                                  (const unsigned long long*)nullptr, (unsigned long long*)nullptr,
+                                  (int)std::max<int64_t>(cap_edges, 1));
   size_t f = 0;
   size_t h3 = 0;
   cub::DeviceSelect::Flagged(nullptr, h3, (const HEdge*)nullptr, (const uint8_t*)nullptr, (HEdge*)nullptr,
@@ -1742,7 +1766,6 @@ size_t carve(Layout& L, char* base, bool dry, int64_t N, int nr, const int64_t* 
   L.Bc = cv.take<uint32_t>(N + 1);
   L.tgt = cv.take<int32_t>(N + 1);
   L.e_key = cv.take<uint64_t>(N + 1);
-  L.e_key_sorted = cv.take<uint64_t>(N + 1);
   L.e_w = cv.take<float>(N + 1);
   L.buckets = cv.take<unsigned long long>(256);
   L.hcomp = cv.take<int32_t>(N + 1);
@@ -2568,8 +2591,18 @@ kdb_status kdb_mst(const kdb_graph* g, float eps, const uint32_t* core_bits, int
   unsigned long long bk[256];
   if (ne > 0) {
     size_t cb = L.cub_bytes;
-    { LaunchScope ls_("cub::DeviceRadixSort", st, false); KDB_CUDA(cub::DeviceRadixSort::SortPairs(L.cub_tmp, cb, L.e_key, L.e_key_sorted, L.e_w, mst_w, (int)ne, 0, 64, st)); }
-    LAUNCH(k_split_edges, grid_for(ne), kThreads, st, ne, L.e_key_sorted, mst_a, mst_b);
+    uint32_t* ka = reinterpret_cast<uint32_t*>(L.parent);  // N + 1 each, free now
+    uint32_t* ka2 = reinterpret_cast<uint32_t*>(L.rootof);
+    unsigned long long* vb = reinterpret_cast<unsigned long long*>(L.Kc);
+    unsigned long long* vb2 = reinterpret_cast<unsigned long long*>(L.e_key);
+    LAUNCH(k_msf_pack, grid_for(ne), kThreads, st, ne, L.e_key, L.e_w, ka, vb);
+    int abits = 1;
+    while (abits < 32 && ((int64_t)1 << abits) < N) ++abits;
+    {
+      LaunchScope ls_("cub::DeviceRadixSort", st, false);
+      KDB_CUDA(cub::DeviceRadixSort::SortPairs(L.cub_tmp, cb, ka, ka2, vb, vb2, (int)ne, 0, abits, st));
+    }
+    LAUNCH(k_msf_unpack, grid_for(ne), kThreads, st, ne, ka2, vb2, mst_a, mst_b, mst_w);
     KDB_CUDA(cudaMemsetAsync(L.buckets, 0, 256 * sizeof(unsigned long long), st));
     LAUNCH(k_wbuckets, grid_for(ne), kThreads, st, ne, mst_w, L.buckets);
     KDB_CUDA(cudaGetLastError());
