@@ -654,6 +654,13 @@ __global__ void __launch_bounds__(256) k_offer_round(const int32_t* __restrict__
 // prefix (w <= eps_run) runs past column kW continue in the graph row itself.
 constexpr int kW = 16;
 
+// one 32-byte load (sm_100: LDG.E.ENL2.256); p must be 32-byte aligned
+__device__ __forceinline__ void ld256(const int4* p, int4& a, int4& b) {
+  asm volatile("ld.global.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
+               : "l"(p));
+}
+
 // records per chunk of the ordered row kernels (see k_light_first)
 constexpr int kChunk = 1024;
 // per-row filter metadata (written by the light pass): bits 0-14 light prefix
@@ -665,7 +672,7 @@ constexpr uint16_t kMetaSkip = 0x7fffu;  // non-core row
 // Exact mode also writes the certificate bound kth'(v) into kmin[comp v]; kth
 // is only loaded when the ELL row is entirely within eps (else kth > eps).
 // Rows are taken in ordered chunks; the initial list keeps row order.
-template <bool VEC>
+template <bool VEC, bool A32>
 __global__ void __launch_bounds__(256) k_light_ell(const int32_t* __restrict__ nbr, const float* __restrict__ dist,
                                                    int64_t n_rows, int32_t k, float eps, int64_t row_begin,
                                                    const int32_t* __restrict__ comp, uint32_t* __restrict__ kmin,
@@ -692,7 +699,34 @@ __global__ void __launch_bounds__(256) k_light_ell(const int32_t* __restrict__ n
       const float* dr = dist + i * k;
       int32_t J[kW];
       float w[kW];
-      if (VEC && k >= kW) {
+      if (VEC && A32) {
+        // whole 32-byte sectors (LDG.256): a row starts at a 32-B boundary or
+        // 16 B past one (k % 8 == 4), so 2 or 3 sectors cover its first kW
+        // entries -- one request per sector instead of one per 16-B half
+        const int sh = (int)((i * k) & 7);  // 0 or 4
+        int4 a0, a1, a2, a3, a4, a5, b0, b1, b2, b3, b4, b5;
+        const int4* pj = reinterpret_cast<const int4*>(nr - sh);
+        const int4* pd = reinterpret_cast<const int4*>(dr - sh);
+        ld256(pj, a0, a1);
+        ld256(pj + 2, a2, a3);
+        ld256(pd, b0, b1);
+        ld256(pd + 2, b2, b3);
+        if (sh) {
+          ld256(pj + 4, a4, a5);
+          ld256(pd + 4, b4, b5);
+        } else {
+          a4 = a5 = b4 = b5 = make_int4(0, 0, 0, 0);
+        }
+        const int32_t SJ[24] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w, a2.x, a2.y, a2.z, a2.w,
+                                a3.x, a3.y, a3.z, a3.w, a4.x, a4.y, a4.z, a4.w, a5.x, a5.y, a5.z, a5.w};
+        const int32_t SW[24] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w, b2.x, b2.y, b2.z, b2.w,
+                                b3.x, b3.y, b3.z, b3.w, b4.x, b4.y, b4.z, b4.w, b5.x, b5.y, b5.z, b5.w};
+#pragma unroll
+        for (int c = 0; c < kW; ++c) {
+          J[c] = sh ? SJ[c + 4] : SJ[c];
+          w[c] = __int_as_float(sh ? SW[c + 4] : SW[c]);
+        }
+      } else if (VEC && k >= kW) {
 #pragma unroll
         for (int q = 0; q < kW / 4; ++q) {
           // L1-allocating loads: the two 16-B halves of a sector are separate
@@ -748,12 +782,6 @@ __global__ void k_row_meta(const float* __restrict__ dist, int64_t n_rows, int32
   }
 }
 
-// one 32-byte load (sm_100: LDG.E.ENL2.256); p must be 32-byte aligned
-__device__ __forceinline__ void ld256(const int4* p, int4& a, int4& b) {
-  asm volatile("ld.global.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-               : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
-               : "l"(p));
-}
 
 // Scan row v (component cv) from head h: columns < kW from the ELL row, the
 // rest (rare: a candidate prefix longer than kW) from the graph row.  DIRECT:
@@ -1162,24 +1190,39 @@ __global__ void k_fill_i32(int32_t* __restrict__ p, int64_t n, int32_t val) {
     p[c] = val;
 }
 
-__global__ void k_relabel(int64_t N, int32_t* __restrict__ comp, const int32_t* __restrict__ map) {
-  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < N;
+// comp[v] = m2[m1[comp[v]]] (m2 optional) for every comp[v] >= 0.  Each thread
+// takes 8 consecutive vertices per step (two int4 loads, 8 independent
+// gathers in flight): the loop is bound by gather latency otherwise.
+__global__ void k_relabel(int64_t N, int32_t* __restrict__ comp, const int32_t* __restrict__ m1,
+                          const int32_t* __restrict__ m2) {
+  const int64_t n8 = ((uintptr_t)comp & 15u) ? 0 : N / 8;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n8; q += (int64_t)gridDim.x * blockDim.x) {
+    int4* p = reinterpret_cast<int4*>(comp) + 2 * q;
+    int4 a = p[0], b = p[1];
+    int32_t c[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+    for (int j = 0; j < 8; ++j) c[j] = c[j] >= 0 ? gat(m1 + c[j]) : c[j];
+    if (m2) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) c[j] = c[j] >= 0 ? gat(m2 + c[j]) : c[j];
+    }
+    p[0] = make_int4(c[0], c[1], c[2], c[3]);
+    p[1] = make_int4(c[4], c[5], c[6], c[7]);
+  }
+  for (int64_t v = n8 * 8 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < N;
        v += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t c = comp[v];
-    if (c >= 0) comp[v] = gat(map + c);
+    int32_t c = comp[v];
+    if (c >= 0) {
+      c = gat(m1 + c);
+      if (m2) c = gat(m2 + c);
+      comp[v] = c;
+    }
   }
 }
 
 // ============================================================================
 // a9 / a11: canonical labels, MSF output, exact weight
 // ============================================================================
-__global__ void k_canon(int64_t N, int32_t* __restrict__ comp, const int32_t* __restrict__ cmin) {
-  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < N;
-       v += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t c = comp[v];
-    if (c >= 0) comp[v] = gat(cmin + c);
-  }
-}
 
 // MSF output in (a, b) order: radix sort on the 32-bit a (only ceil(log2 N)
 // bits) carrying (b, w) as a 64-bit payload, then each run of equal a (tiny:
@@ -1615,15 +1658,6 @@ __global__ void k_relabel_h(int64_t n, int32_t* __restrict__ hcomp, const int32_
     hcomp[c] = gat(map + hcomp[c]);
 }
 
-// final vertex labels after the heavy phase: comp[v] = cminH[hcomp[comp[v]]]
-__global__ void k_canon_h(int64_t N, int32_t* __restrict__ comp, const int32_t* __restrict__ hcomp,
-                          const int32_t* __restrict__ cminH) {
-  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < N; v += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t c = comp[v];
-    if (c >= 0) comp[v] = gat(cminH + gat(hcomp + c));
-  }
-}
-
 // ============================================================================
 // host side
 // ============================================================================
@@ -1975,14 +2009,17 @@ kdb_status rows_phase(Mst& m, float eps_run) {
     if (R.n_rows > 0 && use_compact) {
       R.compact = true;
       R.meta_ok = m.want_meta;
-      if (vec)
-        LAUNCH(k_light_ell<true>, grid_for(R.n_rows), kThreads, st, R.nbr, R.dist, R.n_rows, k, eps_run,
-               R.row_begin, comp, general ? nullptr : L.kmin, R.LE, R.act[0], &R.ctr->n_act[0], &R.ctr->grab,
-               m.want_meta ? R.meta : nullptr, m.eps_full);
-      else
-        LAUNCH(k_light_ell<false>, grid_for(R.n_rows), kThreads, st, R.nbr, R.dist, R.n_rows, k, eps_run,
-               R.row_begin, comp, general ? nullptr : L.kmin, R.LE, R.act[0], &R.ctr->n_act[0], &R.ctr->grab,
-               m.want_meta ? R.meta : nullptr, m.eps_full);
+      // 32-byte sector loads need 32-B aligned arrays, k % 8 in {0, 4} and rows
+      // long enough for the third sector (k >= 20)
+      const bool a32 = vec && k >= 20 && !(((uintptr_t)R.nbr | (uintptr_t)R.dist) & 31u);
+#define KDB_ELL_LAUNCH(V, A)                                                                                    \
+  LAUNCH((k_light_ell<V, A>), grid_for(R.n_rows), kThreads, st, R.nbr, R.dist, R.n_rows, k, eps_run, R.row_begin, \
+         comp, general ? nullptr : L.kmin, R.LE, R.act[0], &R.ctr->n_act[0], &R.ctr->grab,                     \
+         m.want_meta ? R.meta : nullptr, m.eps_full)
+      if (a32) KDB_ELL_LAUNCH(true, true);
+      else if (vec) KDB_ELL_LAUNCH(true, false);
+      else KDB_ELL_LAUNCH(false, false);
+#undef KDB_ELL_LAUNCH
     }
     if (R.n_rows > 0 && !R.compact)
       LAUNCH(k_init_rows, grid_for(R.n_rows), kThreads, st, R.dist, R.n_rows, k, eps_run, R.row_begin, comp,
@@ -2175,7 +2212,7 @@ kdb_status rows_phase(Mst& m, float eps_run) {
     // map[c] = new dense id of c's tree (reuses `parent`, no longer needed)
     LAUNCH(k_merge, grid_for(C), kThreads, st, C, L.rootof, L.newid, L.cmin, general ? nullptr : L.kmin, L.cmin2,
            L.kmin2, L.parent);
-    LAUNCH(k_relabel, grid_for(N), kThreads, st, N, comp, L.parent);
+    LAUNCH(k_relabel, grid_for(N / 8 + 1), kThreads, st, N, comp, L.parent, (const int32_t*)nullptr);
     LAUNCH(k_fill_comp_arrays, grid_for(C2), kThreads, st, C2, L.Kc, L.Bc, nullptr);
     for (size_t r = 1; r < L.ranks.size(); ++r)
       LAUNCH(k_fill_comp_arrays, grid_for(C2), kThreads, st, C2, L.ranks[r].Kc, L.ranks[r].Bc, nullptr);
@@ -2583,10 +2620,11 @@ kdb_status kdb_mst(const kdb_graph* g, float eps, const uint32_t* core_bits, int
   const int64_t ne = (int64_t)hc.msf_count;
   if (ne > N) return set_err(KDB_EINTERNAL, "MSF larger than N-1");
   if (ne > mst_cap) return set_err(KDB_EINVAL, "mst_cap %lld < MSF size %lld", (long long)mst_cap, (long long)ne);
+  // canonical labels: comp[v] = cmin[comp[v]] (through hcomp after a heavy phase)
   if (m.C_heavy >= 0)
-    LAUNCH(k_canon_h, grid_for(N), kThreads, st, N, comp, L.hcomp, L.cmin);
+    LAUNCH(k_relabel, grid_for(N / 8 + 1), kThreads, st, N, comp, L.hcomp, L.cmin);
   else
-    LAUNCH(k_canon, grid_for(N), kThreads, st, N, comp, L.cmin);
+    LAUNCH(k_relabel, grid_for(N / 8 + 1), kThreads, st, N, comp, L.cmin, (const int32_t*)nullptr);
   KDB_CUDA(cudaGetLastError());
   unsigned long long bk[256];
   if (ne > 0) {

@@ -339,3 +339,19 @@ def test_filter_fast_path_toggle(c1_graph, fast, light, monkeypatch):
     eps2 = eps_from_graph(dist2, 8, 1.5)
     got2 = run_gpu(nbr2, dist2, 8, eps2, exact=True)
     assert_parity(got2, oracle_run(nbr2, dist2, 8, eps2))
+
+
+@pytest.mark.parametrize("k", [20, 24, 28, 100])
+def test_wide_rows_exact(k):
+    """k % 4 == 0 and k >= 20: the light ELL is read with 32-byte sector loads
+    (rows start at a 32-B boundary or 16 B past one)."""
+    rng = np.random.default_rng(k)
+    n = 3000
+    X = np.concatenate([rng.standard_normal((n // 2, 3)) * 0.05, rng.standard_normal((n - n // 2, 3)) * 0.05 + 1.0])
+    X = X.astype(np.float32)
+    nbr, dist = knn_bruteforce(X, k)
+    for M, f in ((k // 2, 1.5), (5, 1.0)):
+        eps = eps_from_graph(dist, M, f)
+        exp = oracle_run(nbr, dist, M, eps)
+        assert_parity(run_gpu(nbr, dist, M, eps, exact=True), exp)
+        assert_parity(run_gpu(nbr, dist, M, eps, exact=False), exp)
