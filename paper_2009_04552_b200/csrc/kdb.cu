@@ -1071,67 +1071,88 @@ __device__ __forceinline__ bool certified(uint64_t K, const uint32_t* kmin, int6
 // tgt != null: the hook target of every offering component is known (round 1,
 // written by its single offer), so t = tgt[c] and "mutual" is tgt[t] == c.
 // Otherwise t is found from the selected edge's endpoints.
-__global__ void k_hook(int64_t C, const uint64_t* __restrict__ Kc, const uint32_t* __restrict__ Bc,
+// Components are taken in chunks of kHookChunk; a chunk's emitted MSF edges are
+// staged in shared memory and written with one reservation; the round counters
+// are summed in registers and flushed once per warp at the end.
+constexpr int kHookChunk = 1024;
+
+__global__ void __launch_bounds__(256) k_hook(int64_t C, const uint64_t* __restrict__ Kc, const uint32_t* __restrict__ Bc,
                        const int32_t* __restrict__ tgt, const uint32_t* __restrict__ kmin /* null = all certified */,
                        const int32_t* __restrict__ comp, int32_t* __restrict__ parent,
                        uint64_t* __restrict__ e_key, float* __restrict__ e_w, int64_t e_cap,
                        RoundCounters* __restrict__ ctr) {
-  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < C;
-       base += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t c = base + threadIdx.x;
-    bool emit = false, offered = false, unc = false;
-    uint32_t a = 0, b = 0, wb = 0;
-    if (c < C) {
+  __shared__ uint64_t s_key[kHookChunk];
+  __shared__ uint32_t s_w[kHookChunk];
+  __shared__ uint32_t s_n, s_base;
+  uint32_t n_off = 0, n_unc = 0, n_hook = 0;
+  for (int64_t chunk = blockIdx.x; chunk * kHookChunk < C; chunk += gridDim.x) {
+    if (threadIdx.x == 0) s_n = 0;
+    __syncthreads();
+    for (int t = 0; t < kHookChunk; t += blockDim.x) {
+      const int64_t c = chunk * kHookChunk + t + threadIdx.x;
+      if (c >= C) continue;
       const uint64_t K = Kc[c];
       int32_t p = (int32_t)c;
       if (K != kSent) {
-        offered = true;
+        ++n_off;
         if (!certified(K, kmin, c)) {
-          unc = true;
+          ++n_unc;
         } else {
-          a = (uint32_t)K;
-          b = Bc[c];
-          wb = (uint32_t)(K >> 32);
-          int32_t t;
+          const uint32_t a = (uint32_t)K;
+          const uint32_t b = Bc[c];
+          int32_t t2;
           if (tgt) {
-            t = tgt[c];
+            t2 = tgt[c];
           } else {
             const int32_t x = (gat(comp + a) == (int32_t)c) ? (int32_t)b : (int32_t)a;
-            t = gat(comp + x);
+            t2 = gat(comp + x);
           }
           bool mutual, cert_t = true;
           if (kmin) {  // exact mode: t may abstain; also audit the promise
-            const uint64_t Kt = gat(Kc + t);
-            cert_t = Kt != kSent && certified(Kt, kmin, t);
+            const uint64_t Kt = gat(Kc + t2);
+            cert_t = Kt != kSent && certified(Kt, kmin, t2);
             // t's true minimum is <= the edge c selected (that edge is incident
             // to t); a larger key means t's offer missed an incident edge --
             // impossible under a true EXACT promise, and the only way a hook
             // cycle longer than a mutual pair could form (Fig. cycle).
-            if (cert_t && (Kt > K || (Kt == K && gat(Bc + t) > b))) ctr->violation = 1u;
-            mutual = cert_t && Kt == K && gat(Bc + t) == b;
+            const uint32_t Bt = cert_t ? gat(Bc + t2) : 0u;
+            if (cert_t && (Kt > K || (Kt == K && Bt > b))) ctr->violation = 1u;
+            mutual = cert_t && Kt == K && Bt == b;
           } else if (tgt) {
-            mutual = gat(tgt + t) == (int32_t)c;
+            mutual = gat(tgt + t2) == (int32_t)c;
           } else {
-            mutual = gat(Kc + t) == K && gat(Bc + t) == b;
+            mutual = gat(Kc + t2) == K && gat(Bc + t2) == b;
           }
-          if (!(mutual && c < t)) {
-            p = t;
-            emit = true;
+          if (!(mutual && c < t2)) {
+            p = t2;
+            ++n_hook;
+            const uint32_t j = atomicAdd(&s_n, 1u);
+            s_key[j] = ((uint64_t)a << 32) | b;
+            s_w[j] = (uint32_t)(K >> 32);
           }
         }
       }
       parent[c] = p;
     }
-    block_count(&ctr->offered, offered);
-    block_count(&ctr->uncertified, unc);
-    block_count(&ctr->hooks, emit);
-    const uint32_t slot = block_reserve(&ctr->msf_count, emit);
-    if (emit) {
-      if ((int64_t)slot < e_cap) {
-        e_key[slot] = ((uint64_t)a << 32) | b;
-        e_w[slot] = __uint_as_float(wb);
+    __syncthreads();
+    if (threadIdx.x == 0) s_base = s_n ? atomicAdd(&ctr->msf_count, s_n) : 0u;
+    __syncthreads();
+    for (uint32_t j = threadIdx.x; j < s_n; j += blockDim.x) {
+      if ((int64_t)(s_base + j) < e_cap) {
+        e_key[s_base + j] = s_key[j];
+        e_w[s_base + j] = __uint_as_float(s_w[j]);
       }
     }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    n_off += __shfl_xor_sync(0xffffffffu, n_off, o);
+    n_unc += __shfl_xor_sync(0xffffffffu, n_unc, o);
+    n_hook += __shfl_xor_sync(0xffffffffu, n_hook, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (n_off) atomicAdd(&ctr->offered, n_off);
+    if (n_unc) atomicAdd(&ctr->uncertified, n_unc);
+    if (n_hook) atomicAdd(&ctr->hooks, n_hook);
   }
 }
 
@@ -1180,7 +1201,10 @@ __global__ void k_merge(int64_t C, const int32_t* __restrict__ rootof, const int
     const int32_t r = gat(newid + rootof[c]);
     map[c] = r;
     atomicMin(cmin2 + r, cmin[c]);
-    if (kmin) atomicMin(kmin2 + r, kmin[c]);
+    if (kmin) {
+      const uint32_t km = kmin[c];
+      if (km != kInfBits) atomicMin(kmin2 + r, km);  // kmin2 starts at +inf
+    }
   }
 }
 
@@ -1200,11 +1224,13 @@ __global__ void k_relabel(int64_t N, int32_t* __restrict__ comp, const int32_t* 
     int4* p = reinterpret_cast<int4*>(comp) + 2 * q;
     int4 a = p[0], b = p[1];
     int32_t c[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    // read-only maps through L1 (__ldg): when few components remain, 64M
+    // gathers hit a handful of lines, which would serialise on their L2 slices
 #pragma unroll
-    for (int j = 0; j < 8; ++j) c[j] = c[j] >= 0 ? gat(m1 + c[j]) : c[j];
+    for (int j = 0; j < 8; ++j) c[j] = c[j] >= 0 ? __ldg(m1 + c[j]) : c[j];
     if (m2) {
 #pragma unroll
-      for (int j = 0; j < 8; ++j) c[j] = c[j] >= 0 ? gat(m2 + c[j]) : c[j];
+      for (int j = 0; j < 8; ++j) c[j] = c[j] >= 0 ? __ldg(m2 + c[j]) : c[j];
     }
     p[0] = make_int4(c[0], c[1], c[2], c[3]);
     p[1] = make_int4(c[4], c[5], c[6], c[7]);
@@ -1213,8 +1239,8 @@ __global__ void k_relabel(int64_t N, int32_t* __restrict__ comp, const int32_t* 
        v += (int64_t)gridDim.x * blockDim.x) {
     int32_t c = comp[v];
     if (c >= 0) {
-      c = gat(m1 + c);
-      if (m2) c = gat(m2 + c);
+      c = __ldg(m1 + c);
+      if (m2) c = __ldg(m2 + c);
       comp[v] = c;
     }
   }
