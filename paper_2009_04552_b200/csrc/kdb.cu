@@ -335,21 +335,30 @@ __device__ __forceinline__ void block_count(uint32_t* counter, bool pred) {
 // ============================================================================
 // a1: core marking
 // ============================================================================
+// One thread per 32-bit word of core flags: 32 independent loads of
+// D[v][M-1] in flight, the word is stored whole (atomicOr only for the
+// partial words at this rank's range ends; the caller zeroed the bits).
 __global__ void k_core_mark(const float* __restrict__ dist, int64_t n_rows, int32_t k, int32_t M,
                             float eps, int64_t row_begin, uint32_t* __restrict__ bits) {
-  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n_rows;
-       base += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = base + threadIdx.x;
-    const bool in = i < n_rows;
-    bool core = false;
-    if (in) core = __ldcs(dist + i * k + (M - 1)) <= eps;
-    const int64_t v = row_begin + i;
-    const unsigned inmask = __ballot_sync(0xffffffffu, in);
-    if (in) {
-      const unsigned grp = __match_any_sync(inmask, (unsigned long long)(v >> 5));
-      const unsigned word = __reduce_or_sync(grp, core ? (1u << (v & 31)) : 0u);
-      if ((threadIdx.x & 31) == __ffs(grp) - 1 && word) atomicOr(bits + (v >> 5), word);
+  const int64_t r_end = row_begin + n_rows;
+  const int64_t w0 = row_begin >> 5, w1 = (r_end + 31) >> 5;
+  for (int64_t wd = w0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; wd < w1;
+       wd += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v0 = wd << 5;
+    float d[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const int64_t v = v0 + j;
+      d[j] = (v >= row_begin && v < r_end) ? __ldcs(dist + (v - row_begin) * k + (M - 1))
+                                            : __int_as_float(0x7f800000);
     }
+    uint32_t word = 0;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) word |= (d[j] <= eps ? 1u : 0u) << j;
+    if (v0 >= row_begin && v0 + 32 <= r_end)
+      bits[wd] = word;
+    else if (word)
+      atomicOr(bits + wd, word);
   }
 }
 
@@ -1380,7 +1389,8 @@ constexpr size_t kFilterSmem = kBloomBits / 8;
 __device__ __forceinline__ uint32_t bloom_word(uint32_t x) { return (x * 0x9E3779B1u) >> 17; }
 __device__ __forceinline__ uint32_t bloom_mask(uint32_t x) {
   const uint32_t h = x * 0x85EBCA77u;
-  return (1u << (h >> 27)) | (1u << ((h >> 22) & 31u)) | (1u << ((h >> 17) & 31u));
+  // 1 << (s & 31) as one funnel shift (SHF.L.W wraps the amount)
+  return __funnelshift_l(0u, 1u, h >> 27) | __funnelshift_l(0u, 1u, h >> 22) | __funnelshift_l(0u, 1u, h >> 17);
 }
 
 // dom[blk]: majority component among 32 sampled vertices of the id block (-1 if none is core)
@@ -2546,7 +2556,7 @@ kdb_status kdb_core_mark(const kdb_graph* g, int32_t M, float eps, uint32_t* cor
   for (size_t r = 0; r < rb.size(); ++r) {
     if (rn[r] == 0) continue;
     const int64_t off = (rb[r] - g->row_begin) * g->k_max;
-    LAUNCH(k_core_mark, grid_for(rn[r]), kThreads, st, g->dist + off, rn[r], g->k_max, M, eps, rb[r], core_bits);
+    LAUNCH(k_core_mark, grid_for(rn[r] / 32 + 2), kThreads, st, g->dist + off, rn[r], g->k_max, M, eps, rb[r], core_bits);
     KDB_CUDA(cudaGetLastError());
   }
   // ranks own disjoint bits: SUM == OR
