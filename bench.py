@@ -292,16 +292,23 @@ def run_ours(args):
     if dom:
         name, (tot_ms, nl) = dom
         per_launch_ms = tot_ms / nl
-        algo_bytes = dominant_algo_bytes(name, N, k, world, nl / args.steps, stats)
+        algo_bytes = algo_bytes_per_launch(name, N, k, world, nl / args.steps, stats)
         achieved = algo_bytes / (per_launch_ms * 1e-3) / 1e9 if algo_bytes else None
+        traffic = measured_traffic().get(base_name(name), {}).get("dram_bytes_per_launch")
         roof = {"kernel": name, "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": (achieved / peak) if achieved else None, "traffic": None,
+                "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                 "peak_source": peak_src, "launches_per_step": nl / args.steps,
                 "ms_per_launch": per_launch_ms, "share_of_step": tot_ms / args.steps / ms,
                 "algo_bytes_per_launch": algo_bytes}
     t_min_ms = (8.0 * N * k + 4.0 * N + N / 8.0) / (peak * 1e9) * 1e3 / world
-    kernels = {n: {"ms_per_step": v[0] / args.steps, "launches_per_step": v[1] / args.steps}
-               for n, v in sorted(prof.items(), key=lambda kv: -kv[1][0])}
+    kernels = {}
+    for n, v in sorted(prof.items(), key=lambda kv: -kv[1][0]):
+        e = {"ms_per_step": v[0] / args.steps, "launches_per_step": v[1] / args.steps}
+        ab = algo_bytes_per_launch(n, N, k, world, v[1] / args.steps, stats) if v[1] else None
+        if ab:
+            gbs = ab / (v[0] / v[1] * 1e-3) / 1e9
+            e.update(algo_gbs=gbs, frac_of_peak=gbs / peak)
+        kernels[n] = e
 
     # ---- cpu baseline (rank 0, N = 1 only) ------------------------------------------
     cpu = None
@@ -338,23 +345,46 @@ def run_ours(args):
         tdist.destroy_process_group()
 
 
-def dominant_algo_bytes(name, N, k, world, launches_per_step, stats):
-    """Algorithmic bytes per launch of kernel `name`:
-    8 B per kNN entry the launch must read, plus 4 B per vertex
-    for kernels whose unit is a vertex."""
+KW = 16  # light ELL width (csrc/kdb.cu kW)
+
+
+def base_name(name):
+    """'(k_filter<4, true>)' -> 'k_filter'"""
+    return name.strip("()").split("<")[0]
+
+
+def algo_bytes_per_launch(name, N, k, world, launches_per_step, stats):
+    """Algorithmic bytes per launch of kernel `name`: the graph
+    bytes the launch must read (8 B per (id, weight) entry, SURVEY.md 8(d);
+    4 B per entry where only the id is needed) plus 4 B per vertex for
+    vertex-unit kernels.  None for kernels without a graph-byte unit."""
     n_local = N / world
-    if name == "k_core_mark":
-        return 4.0 * n_local + n_local / 8.0          # one fp32 per row + the bit words
-    if name == "k_label":
-        return 4.0 * n_local + 4.0 * n_local           # D[i][0..] of border rows ~ 1 fp32 + label
-    if name.startswith(("k_offer_rows", "k_offer_warp", "k_offer_first", "k_sweep")):
-        er = np.mean([s.get("entries_read", 0) for s in stats]) if stats else 0
-        if er and launches_per_step:
-            return 8.0 * er / launches_per_step
-        return None
-    if name in ("k_relabel", "k_canon", "k_init_comp"):
+    bn = base_name(name)
+    mean = lambda key: float(np.mean([s.get(key, 0) for s in stats])) if stats else 0.0
+    if bn == "k_core_mark":
+        return 4.0 * n_local + n_local / 8.0            # D[v][M-1] per row + the flag words
+    if bn == "k_label":
+        return 4.0 * n_local + 4.0 * n_local            # first weight of each row + the label
+    if bn == "k_light_ell":
+        return n_local * (8.0 * KW + 4.0)               # the first kW entries + D[v][k-1] per row
+    if bn == "k_filter":
+        return n_local * (4.0 * k + 2.0)                # every id (weights only where needed) + row metadata
+    if bn in ("k_light_round", "k_light_first", "k_offer_round", "k_offer_first"):
+        er = mean("entries_read")                       # (J, w) entries scanned, all rounds
+        rounds = mean("rounds")
+        return 8.0 * er / rounds if er and rounds else None
+    if bn == "k_relabel":
         return 8.0 * N                                  # read + write one int32 per vertex
     return None
+
+
+def measured_traffic():
+    """Per-launch DRAM bytes (read + write) per kernel from the committed ncu
+    summary (profiles/ncu_traffic.json, written by tools/ncu_traffic.py)."""
+    try:
+        return json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+    except Exception:
+        return {}
 
 
 def run_e2e(args, kdb, W, N, k, M, eps, rb, re_, comm, ws, outs, dev, world):
