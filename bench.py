@@ -39,7 +39,7 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="C4", choices=["C1", "C4", "C5"])
+    ap.add_argument("--config", default="C4", choices=["C1", "C2", "C3", "C4", "C5"])
     ap.add_argument("--scale", type=float, default=1.0, help="shrink every cluster (tests only)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--seed", type=int, default=0)
@@ -128,12 +128,15 @@ def make_workload(cfg_name: str, scale: float, seed: int, device):
     """Points (numpy, seeded), exact kNN graph on the GPU, eps from the config rule."""
     import torch
     from datagen import CONFIGS, gen_config_points
-    from datagen.knng_gpu import build_knng_grid
+    from datagen.knng_gpu import build_knng_brute, build_knng_grid
     cfg = CONFIGS[cfg_name]
     t0 = time.time()
     X, truth = gen_config_points(cfg_name, seed, scale)
     t1 = time.time()
-    nbr, dist, info = build_knng_grid(X, cfg["k"], device=device)
+    if X.shape[1] <= 5:   # uniform-grid cell search (C1, C4, C5)
+        nbr, dist, info = build_knng_grid(X, cfg["k"], device=device)
+    else:                 # brute force with exact re-rank (C2 d=50, C3 d=10)
+        nbr, dist, info = build_knng_brute(X, cfg["k"], device=device)
     torch.cuda.synchronize()
     t2 = time.time()
     med = median_like_numpy(dist[:, cfg["M"] - 1])
@@ -149,7 +152,8 @@ def workload_desc(cfg_name, W, scale):
                         (f" scaled x{scale}" if scale != 1.0 else ""),
             "N": W["N"], "d": W["d"], "k": W["k"], "M": W["M"], "eps": W["eps"],
             "eps_rule": f"fp32({c['eps_factor']} x median D[:, M-1])",
-            "graph": "exact kNN, self-excluded, fp32 dist / int32 ids (datagen/csrc/knng.cu grid builder)",
+            "graph": "exact kNN, self-excluded, fp32 dist / int32 ids (datagen/csrc/knng.cu " +
+                     ("grid builder)" if W["d"] <= 5 else "brute-force builder, fp64 re-rank)"),
             "graph_bytes": int(W["N"]) * int(W["k"]) * 8,
             "l2": "no flush: the resident graph (>=1 GB) exceeds the 126 MB L2",
             "graph_build_s": round(W["graph_build_s"], 2)}

@@ -164,6 +164,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_cells(const float* __restrict__
   int* cid = reinterpret_cast<int*>(cx + kCandCap * D);
   __shared__ int64_t nb_start[256];
   __shared__ int nb_len[256];
+  __shared__ int nb_pre[256];
   __shared__ int ncand, nnb;
   constexpr int NB = D == 1 ? 3 : D == 2 ? 9 : D == 3 ? 27 : D == 4 ? 81 : 243;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -181,56 +182,65 @@ __global__ void __launch_bounds__(kWarps * 32) k_cells(const float* __restrict__
       nb_len[s] = (int)((j + 1 < ncell ? ustart[j + 1] : n) - ustart[j]);
     }
     __syncthreads();
-    // stage candidates (cooperative copy of every neighbour cell's points)
+    // neighbour cells' points are staged in chunks of kCandCap (5-D blocks of
+    // 3^5 cells often hold more); each warp accumulates its query's points
+    // within h' over all chunks
     if (threadIdx.x == 0) {
       int tot = 0;
-      for (int s = 0; s < nnb; ++s) tot += nb_len[s];
+      for (int s2 = 0; s2 < nnb; ++s2) { nb_pre[s2] = tot; tot += nb_len[s2]; }
       ncand = tot;
     }
     __syncthreads();
     const int64_t qbeg = ustart[c], qend = (c + 1 < ncell ? ustart[c + 1] : n);
-    if (ncand > kCandCap) {  // too dense: every query of this cell goes to the fallback
-      for (int64_t q = qbeg + threadIdx.x; q < qend; q += blockDim.x) fb[atomicAdd(nfb, 1u)] = sid[q];
-      __syncthreads();
-      continue;
-    }
-    {
-      int base = 0;
-      for (int s = 0; s < nnb; ++s) {
-        for (int t = threadIdx.x; t < nb_len[s]; t += blockDim.x) {
-          const int32_t p = sid[nb_start[s] + t];
-          cid[base + t] = p;
-          for (int u = 0; u < D; ++u) cx[(base + t) * D + u] = X[(int64_t)p * D + u];
+    const bool one_chunk = ncand <= kCandCap;
+    auto stage = [&](int cbase) {
+      const int cend = min(cbase + kCandCap, ncand);
+      for (int s2 = 0; s2 < nnb; ++s2) {
+        const int lo = max(nb_pre[s2], cbase), hi = min(nb_pre[s2] + nb_len[s2], cend);
+        for (int f = lo + (int)threadIdx.x; f < hi; f += blockDim.x) {
+          const int32_t p = sid[nb_start[s2] + (f - nb_pre[s2])];
+          cid[f - cbase] = p;
+          for (int u = 0; u < D; ++u) cx[(f - cbase) * D + u] = X[(int64_t)p * D + u];
         }
-        base += nb_len[s];
       }
-    }
+    };
+    if (one_chunk) stage(0);
     __syncthreads();
-    for (int64_t q = qbeg + warp; q < qend; q += kWarps) {
-      const int32_t qi = sid[q];
+    for (int64_t q0 = qbeg; q0 < qend; q0 += kWarps) {
+      const int64_t q = q0 + warp;
+      const bool active = q < qend;
+      const int32_t qi = active ? sid[q] : -1;
       float qx[D];
-      for (int u = 0; u < D; ++u) qx[u] = X[(int64_t)qi * D + u];
+      for (int u = 0; u < D; ++u) qx[u] = active ? X[(int64_t)qi * D + u] : 0.f;
       int cnt = 0;
-      bool over = false;
-      for (int b0 = 0; b0 < ncand; b0 += 32) {
-        const int t = b0 + lane;
-        bool take = false;
-        double dd = 0.0;
-        int pid = -1;
-        if (t < ncand) {
-          pid = cid[t];
-          if (pid != qi) {
-            dd = dist64(qx, cx + t * D, D);
-            take = dd <= hq;
-          }
+      for (int cbase = 0; cbase < ncand; cbase += kCandCap) {
+        if (!one_chunk) {
+          __syncthreads();
+          stage(cbase);
+          __syncthreads();
         }
-        const unsigned m = __ballot_sync(0xffffffffu, take);
-        const int pos = cnt + __popc(m & ((1u << lane) - 1u));
-        if (take && pos < kWarpBuf) { wd[warp][pos] = dd; wi[warp][pos] = pid; }
-        cnt += __popc(m);
+        const int cn = min(kCandCap, ncand - cbase);
+        if (!active) continue;
+        for (int b0 = 0; b0 < cn; b0 += 32) {
+          const int t = b0 + lane;
+          bool take = false;
+          double dd = 0.0;
+          int pid = -1;
+          if (t < cn) {
+            pid = cid[t];
+            if (pid != qi) {
+              dd = dist64(qx, cx + t * D, D);
+              take = dd <= hq;
+            }
+          }
+          const unsigned m = __ballot_sync(0xffffffffu, take);
+          const int pos = cnt + __popc(m & ((1u << lane) - 1u));
+          if (take && pos < kWarpBuf) { wd[warp][pos] = dd; wi[warp][pos] = pid; }
+          cnt += __popc(m);
+        }
       }
-      over = cnt > kWarpBuf;
-      if (cnt < k || over) {
+      if (!active) continue;
+      if (cnt < k || cnt > kWarpBuf) {
         if (lane == 0) fb[atomicAdd(nfb, 1u)] = qi;
         __syncwarp();
         continue;
@@ -381,6 +391,184 @@ __global__ void k_ladder(const float* __restrict__ X, int64_t n, int D, const in
   }
 }
 
+// ============================================================================
+// Any-d exact kNN by brute force (C2: d = 50, C3: d = 10) -- input
+// construction, not the hot path.  Pass 1 never materialises the N^2
+// distances: each thread owns one query, streams every candidate through a
+// shared-memory tile (rotated to start at the query's own id block, so the
+// threshold drops early on cluster-major ids), computes the fp32
+// difference-form squared distance and keeps the Kp smallest in a max-heap in
+// global scratch.  Pass 2 recomputes the Kp candidates exactly (fp64, dimension
+// order, no fusion -- the datagen/knn_cpu.py definition), sorts them by
+// (distance, index) and keeps k.  Certificate: the fp32 sum of d squared
+// differences is within a relative delta = (d + 3) 2^-24 of the real value, so
+// if heap_max (1 - delta) > A (1 + delta), A = the largest fp32 value among the
+// exact top-k, no point outside the heap can belong to the top-k.  Rows that
+// fail it are flagged and recomputed exactly over all points.
+constexpr int kBrT = 256;   // threads (= queries) per block
+constexpr int kBrTile = 128;
+
+__device__ __forceinline__ void heap_sift(float* hs, int32_t* hi, int n, int p) {
+  while (true) {
+    const int l = 2 * p + 1, r = l + 1;
+    int m = p;
+    if (l < n && hs[l] > hs[m]) m = l;
+    if (r < n && hs[r] > hs[m]) m = r;
+    if (m == p) return;
+    const float ts = hs[p]; hs[p] = hs[m]; hs[m] = ts;
+    const int32_t ti = hi[p]; hi[p] = hi[m]; hi[m] = ti;
+    p = m;
+  }
+}
+
+template <int DC>  // DC > 0: compile-time dimension; 0: runtime d (<= 64)
+__global__ void __launch_bounds__(kBrT) k_brute_cand(const float* __restrict__ X, int64_t n, int d_rt, int Kp,
+                                                       float* __restrict__ hs_all, int32_t* __restrict__ hi_all,
+                                                       int32_t* __restrict__ hcount) {
+  constexpr int DM = DC > 0 ? DC : 64;
+  const int D = DC > 0 ? DC : d_rt;
+  __shared__ __align__(16) float tile[DM * kBrTile];  // [dim][candidate]
+  const int64_t qi = (int64_t)blockIdx.x * kBrT + threadIdx.x;
+  const bool active = qi < n;
+  float q[DM];
+#pragma unroll
+  for (int t = 0; t < DM; ++t) q[t] = (active && t < D) ? X[qi * D + t] : 0.f;
+  float* hs = hs_all + (active ? qi : 0) * Kp;
+  int32_t* hi = hi_all + (active ? qi : 0) * Kp;
+  int h = 0;
+  float thr = __int_as_float(0x7f800000);
+  const int64_t ntiles = (n + kBrTile - 1) / kBrTile;
+  const int64_t t_start = ((int64_t)blockIdx.x * kBrT) / kBrTile;
+  for (int64_t tt = 0; tt < ntiles; ++tt) {
+    const int64_t tile_id = (t_start + tt) % ntiles;
+    const int64_t c0 = tile_id * kBrTile;
+    const int nc = (int)min((int64_t)kBrTile, n - c0);
+    __syncthreads();
+    for (int e = threadIdx.x; e < kBrTile * D; e += kBrT) {
+      const int c = e / D, t = e - c * D;
+      tile[t * kBrTile + c] = c < nc ? __ldg(X + (c0 + c) * D + t) : 0.f;
+    }
+    __syncthreads();
+    if (!active) continue;
+    for (int c = 0; c < nc; c += 4) {
+      float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+#pragma unroll
+      for (int t = 0; t < DM; ++t) {
+        if (DC == 0 && t >= D) break;
+        const float4 x = *reinterpret_cast<const float4*>(tile + t * kBrTile + c);
+        const float a0 = q[t] - x.x, a1 = q[t] - x.y, a2 = q[t] - x.z, a3 = q[t] - x.w;
+        s0 = fmaf(a0, a0, s0);
+        s1 = fmaf(a1, a1, s1);
+        s2 = fmaf(a2, a2, s2);
+        s3 = fmaf(a3, a3, s3);
+      }
+      const float sv[4] = {s0, s1, s2, s3};
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int64_t j = c0 + c + r;
+        if (c + r >= nc || j == qi || !(sv[r] < thr)) continue;
+        if (h < Kp) {
+          hs[h] = sv[r];
+          hi[h] = (int32_t)j;
+          if (++h == Kp) {
+            for (int p2 = Kp / 2 - 1; p2 >= 0; --p2) heap_sift(hs, hi, Kp, p2);
+            thr = hs[0];
+          }
+        } else {
+          hs[0] = sv[r];
+          hi[0] = (int32_t)j;
+          heap_sift(hs, hi, Kp, 0);
+          thr = hs[0];
+        }
+      }
+    }
+  }
+  if (active) hcount[qi] = h;
+}
+
+__device__ __forceinline__ double exact_d64(const float* __restrict__ a, const float* __restrict__ b, int D) {
+  double acc = 0.0;
+  for (int t = 0; t < D; ++t) {
+    const double df = __dsub_rn((double)a[t], (double)b[t]);
+    acc = __dadd_rn(acc, __dmul_rn(df, df));
+  }
+  return sqrt(acc);
+}
+
+// one warp per query: exact fp64 distances of the heap, bitonic sort by
+// (distance, index) in shared memory, top k out, certificate check
+constexpr int kRrWarps = 8;
+constexpr int kRrBuf = 256;  // Kp <= 256
+__global__ void __launch_bounds__(kRrWarps * 32) k_brute_rerank(const float* __restrict__ X, int64_t n, int D, int k,
+                                                                 int Kp, const float* __restrict__ hs_all,
+                                                                 const int32_t* __restrict__ hi_all,
+                                                                 const int32_t* __restrict__ hcount,
+                                                                 int32_t* __restrict__ nbr, float* __restrict__ dist,
+                                                                 int32_t* __restrict__ fail_rows,
+                                                                 unsigned int* __restrict__ n_fail) {
+  __shared__ double sd[kRrWarps][kRrBuf];
+  __shared__ int si[kRrWarps][kRrBuf];
+  __shared__ float ss[kRrWarps][kRrBuf];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const double delta = (D + 3) * 5.9604644775390625e-8;  // (d + 3) 2^-24
+  for (int64_t qi = (int64_t)blockIdx.x * kRrWarps + w; qi < n; qi += (int64_t)gridDim.x * kRrWarps) {
+    const int h = hcount[qi];
+    const float* hs = hs_all + qi * Kp;
+    const int32_t* hi = hi_all + qi * Kp;
+    float hmax = 0.f;
+    for (int e = lane; e < kRrBuf; e += 32) {
+      if (e < h) {
+        const int32_t j = hi[e];
+        sd[w][e] = exact_d64(X + qi * D, X + (int64_t)j * D, D);
+        si[w][e] = j;
+        ss[w][e] = hs[e];
+        hmax = fmaxf(hmax, hs[e]);
+      } else {
+        sd[w][e] = __longlong_as_double(0x7ff0000000000000ll);
+        si[w][e] = 0x7fffffff;
+        ss[w][e] = 0.f;
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) hmax = fmaxf(hmax, __shfl_xor_sync(0xffffffffu, hmax, o));
+    __syncwarp();
+    // bitonic sort of kRrBuf entries by (distance, index)
+    for (int size = 2; size <= kRrBuf; size <<= 1) {
+      for (int stride = size >> 1; stride > 0; stride >>= 1) {
+        for (int e = lane; e < kRrBuf / 2; e += 32) {
+          const int lo = 2 * e - (e & (stride - 1)), hi2 = lo + stride;
+          const bool up = (lo & size) == 0;
+          const double dl = sd[w][lo], dh = sd[w][hi2];
+          const int il = si[w][lo], ih = si[w][hi2];
+          const bool gt = dl > dh || (dl == dh && il > ih);
+          if (gt == up) {
+            sd[w][lo] = dh; sd[w][hi2] = dl;
+            si[w][lo] = ih; si[w][hi2] = il;
+            const float t = ss[w][lo]; ss[w][lo] = ss[w][hi2]; ss[w][hi2] = t;
+          }
+        }
+        __syncwarp();
+      }
+    }
+    float amax = 0.f;
+    for (int e = lane; e < k; e += 32) {
+      nbr[qi * k + e] = si[w][e];
+      dist[qi * k + e] = (float)sd[w][e];
+      amax = fmaxf(amax, ss[w][e]);
+    }
+    for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+    // a heap that never filled saw every other point: exact without a certificate
+    const bool ok = h < Kp || (double)hmax * (1.0 - delta) > (double)amax * (1.0 + delta);
+    if (!ok && lane == 0) fail_rows[atomicAdd(n_fail, 1u)] = (int32_t)qi;
+    __syncwarp();
+  }
+}
+
+// exact fp64 distances from query row q to every point (fallback rows)
+__global__ void k_exact_row(const float* __restrict__ X, int64_t n, int D, int64_t q, double* __restrict__ out) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x)
+    out[j] = j == q ? __longlong_as_double(0x7ff0000000000000ll) : exact_d64(X + q * D, X + j * D, D);
+}
+
 }  // namespace
 
 extern "C" {
@@ -496,6 +684,30 @@ int knng_grid(const float* X, int64_t n, int D, int k, double h, const double* l
     if (cudaStreamSynchronize(st) != cudaSuccess) return 1;
     if (hfail) return 3;
   }
+  return cudaGetLastError() == cudaSuccess ? 0 : 1;
+}
+
+// brute-force candidates + exact re-rank; rows failing the certificate are
+// written to fail_rows (count in *n_fail) for knng_exact_row.  scratch: n*Kp
+// floats + n*Kp ints + n ints.  Returns 0 ok, 1 cuda error, 4 bad args.
+int knng_brute(const float* X, int64_t n, int D, int k, int Kp, float* hs, int32_t* hi, int32_t* hcount,
+               int32_t* nbr, float* dist, int32_t* fail_rows, unsigned int* n_fail, cudaStream_t st) {
+  if (D < 1 || D > 64 || k < 1 || k > n - 1 || Kp < k || Kp > kRrBuf) return 4;
+  const int g = (int)((n + kBrT - 1) / kBrT);
+  if (D == 10)
+    k_brute_cand<10><<<g, kBrT, 0, st>>>(X, n, D, Kp, hs, hi, hcount);
+  else if (D == 50)
+    k_brute_cand<50><<<g, kBrT, 0, st>>>(X, n, D, Kp, hs, hi, hcount);
+  else
+    k_brute_cand<0><<<g, kBrT, 0, st>>>(X, n, D, Kp, hs, hi, hcount);
+  if (cudaGetLastError() != cudaSuccess) return 1;
+  cudaMemsetAsync(n_fail, 0, 4, st);
+  k_brute_rerank<<<148 * 16, kRrWarps * 32, 0, st>>>(X, n, D, k, Kp, hs, hi, hcount, nbr, dist, fail_rows, n_fail);
+  return cudaGetLastError() == cudaSuccess ? 0 : 1;
+}
+
+int knng_exact_row(const float* X, int64_t n, int D, int64_t q, double* out, cudaStream_t st) {
+  k_exact_row<<<148 * 4, 256, 0, st>>>(X, n, D, q, out);
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
 

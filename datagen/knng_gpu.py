@@ -29,6 +29,9 @@ def _load():
         L.knng_grid.argtypes = [C.c_void_p, C.c_int64, C.c_int, C.c_int, C.c_double, C.c_void_p, C.c_double,
                                 C.c_double, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p,
                                 C.POINTER(C.c_int64)]
+        L.knng_brute.argtypes = [C.c_void_p, C.c_int64, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p,
+                                 C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+        L.knng_exact_row.argtypes = [C.c_void_p, C.c_int64, C.c_int, C.c_int64, C.c_void_p, C.c_void_p]
         _lib = L
     return _lib
 
@@ -85,3 +88,42 @@ def build_knng_grid(X, k: int, h: float | None = None, device: str = "cuda"):
         raise RuntimeError(f"knng_grid failed rc={rc}")
     del ws
     return nbr, dist, dict(h=float(h), n_fallback=int(nfb.value))
+
+
+def build_knng_brute(X, k: int, margin: int = 32, device: str = "cuda"):
+    """Exact self-excluded kNN graph of X (float32 [n, d], any d <= 64) by GPU
+    brute force: fp32 candidate heaps of size k + margin, exact fp64 re-rank by
+    (distance, index), certificate-checked; failing rows are recomputed over all
+    points.  Same rows as ``knn_cpu.knn_bruteforce``.  Returns CUDA tensors
+    (nbr int32 [n,k], dist float32 [n,k], info dict)."""
+    Xd = torch.as_tensor(np.ascontiguousarray(X, np.float32) if isinstance(X, np.ndarray) else X)
+    Xd = Xd.to(device=device, dtype=torch.float32).contiguous()
+    n, d = Xd.shape
+    if not (1 <= d <= 64) or not (1 <= k <= n - 1):
+        raise ValueError("need d <= 64 and 1 <= k <= n-1")
+    Kp = min(n - 1, k + margin, 256)
+    L = _load()
+    hs = torch.empty(n * Kp, dtype=torch.float32, device=device)
+    hi = torch.empty(n * Kp, dtype=torch.int32, device=device)
+    hc = torch.empty(n, dtype=torch.int32, device=device)
+    nbr = torch.empty((n, k), dtype=torch.int32, device=device)
+    dist = torch.empty((n, k), dtype=torch.float32, device=device)
+    fail = torch.empty(n, dtype=torch.int32, device=device)
+    nfail = torch.zeros(1, dtype=torch.int32, device=device)
+    st = torch.cuda.current_stream().cuda_stream
+    rc = L.knng_brute(Xd.data_ptr(), n, d, k, Kp, hs.data_ptr(), hi.data_ptr(), hc.data_ptr(), nbr.data_ptr(),
+                      dist.data_ptr(), fail.data_ptr(), nfail.data_ptr(), st)
+    if rc:
+        raise RuntimeError(f"knng_brute failed rc={rc}")
+    del hs, hi, hc
+    nf = int(nfail.item())
+    if nf:
+        rows = fail[:nf].cpu().tolist()
+        buf = torch.empty(n, dtype=torch.float64, device=device)
+        for q in rows:
+            if L.knng_exact_row(Xd.data_ptr(), n, d, int(q), buf.data_ptr(), st):
+                raise RuntimeError("knng_exact_row failed")
+            order = torch.sort(buf, stable=True).indices[:k]   # stable: ties by ascending index
+            nbr[q] = order.to(torch.int32)
+            dist[q] = buf[order].to(torch.float32)
+    return nbr, dist, dict(candidates=Kp, certificate_failures=nf)

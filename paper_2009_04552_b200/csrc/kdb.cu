@@ -1731,7 +1731,9 @@ double exact_bucket_sum(const unsigned long long* bk) {
 // heavy-phase survivor capacity per rank (edges); beyond it kdb_mst falls back
 // to plain rows-Boruvka over the whole candidate graph (still exact)
 constexpr int kTauSamples = 8192;
-inline int64_t survivor_cap(int64_t n_rows) { return n_rows / 4 + 65536; }
+inline int64_t survivor_cap(int64_t n_rows, int64_t k) {
+  return std::max<int64_t>(n_rows / 4, std::min<int64_t>(n_rows * k / 4, (int64_t)1 << 24)) + 65536;
+}
 
 struct Carver {
   char* base;
@@ -1813,7 +1815,7 @@ size_t cub_tmp_bytes(int64_t N, int64_t cap_edges) {
   size_t f = 0;
   size_t h3 = 0;
   cub::DeviceSelect::Flagged(nullptr, h3, (const HEdge*)nullptr, (const uint8_t*)nullptr, (HEdge*)nullptr,
-                             (uint32_t*)nullptr, (int)std::min<int64_t>(survivor_cap(N) + 1, INT32_MAX));
+                             (uint32_t*)nullptr, (int)std::min<int64_t>(survivor_cap(N, 65535) + 1, INT32_MAX));
   f = std::max(f, h3);
   return std::max(std::max(a, f), std::max(b, c)) + 256;
 }
@@ -1868,7 +1870,7 @@ size_t carve(Layout& L, char* base, bool dry, int64_t N, int nr, const int64_t* 
       R.Bc = L.Bc;
       R.tgt = L.tgt;
     }
-    R.hs_cap = (uint32_t)std::min<int64_t>(survivor_cap(n), (int64_t)UINT32_MAX - 1);
+    R.hs_cap = (uint32_t)std::min<int64_t>(survivor_cap(n, k), (int64_t)UINT32_MAX - 1);
     R.hs[0] = cv.take<HEdge>(R.hs_cap);
     R.hs[1] = cv.take<HEdge>(R.hs_cap);
     R.hkeep = cv.take<uint8_t>(R.hs_cap);
