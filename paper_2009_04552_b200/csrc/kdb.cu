@@ -663,6 +663,14 @@ __global__ void __launch_bounds__(256) k_offer_round(const int32_t* __restrict__
 // prefix (w <= eps_run) runs past column kW continue in the graph row itself.
 constexpr int kW = 16;
 
+// one 32-byte streaming load (evict-first: LDG.E.EF.ENL2.256) -- a light-ELL
+// chunk is read once per round; keep L2 for the component gathers
+__device__ __forceinline__ void ld256cs(const int4* p, int4& a, int4& b) {
+  asm volatile("ld.global.cs.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
+               : "l"(p));
+}
+
 // one 32-byte load (sm_100: LDG.E.ENL2.256); p must be 32-byte aligned
 __device__ __forceinline__ void ld256(const int4* p, int4& a, int4& b) {
   asm volatile("ld.global.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
@@ -688,7 +696,7 @@ __global__ void __launch_bounds__(256) k_light_ell(const int32_t* __restrict__ n
                                                    int4* __restrict__ LE, Rec* __restrict__ act,
                                                    uint32_t* __restrict__ n_act, uint32_t* __restrict__ grab,
                                                    uint16_t* __restrict__ meta, float eps_full) {
-  __shared__ Rec s_rec[kChunk];
+  __shared__ __align__(16) Rec s_rec[kChunk];
   __shared__ uint32_t s_n, s_chunk, s_base;
   for (;;) {
     if (threadIdx.x == 0) { s_chunk = atomicAdd(grab, 1u); s_n = 0; }
@@ -767,7 +775,7 @@ __global__ void __launch_bounds__(256) k_light_ell(const int32_t* __restrict__ n
       int4* o = LE + i * (kW / 2);
 #pragma unroll
       for (int q = 0; q < kW / 2; ++q)
-        __stcg(o + q, make_int4(J[2 * q], __float_as_int(w[2 * q]), J[2 * q + 1], __float_as_int(w[2 * q + 1])));
+        __stcs(o + q, make_int4(J[2 * q], __float_as_int(w[2 * q]), J[2 * q + 1], __float_as_int(w[2 * q + 1])));
       if (w[0] <= eps) s_rec[atomicAdd(&s_n, 1u)] = Rec{(int32_t)v, 0};
     }
     __syncthreads();
@@ -808,7 +816,7 @@ __device__ __forceinline__ RowScan scan_ell(const int4* __restrict__ le, const i
   bool done = false;
   while (!done && c0 < kend) {
     int4 p0, p1;
-    ld256(le + (c0 >> 1), p0, p1);
+    ld256cs(le + (c0 >> 1), p0, p1);
     const int32_t J[4] = {p0.x, p0.z, p1.x, p1.z};
     const float w[4] = {__int_as_float(p0.y), __int_as_float(p0.w), __int_as_float(p1.y), __int_as_float(p1.w)};
     int32_t cj[4];
@@ -885,7 +893,7 @@ __global__ void __launch_bounds__(256) k_light_first(const int4* __restrict__ LE
                                                      uint32_t* __restrict__ grab,
                                                      uint64_t* __restrict__ Kc, uint32_t* __restrict__ Bc,
                                                      int32_t* __restrict__ tgt, unsigned long long* __restrict__ n_entries) {
-  __shared__ Rec s_rec[kChunk];
+  __shared__ __align__(16) Rec s_rec[kChunk];
   __shared__ uint32_t s_n, s_chunk, s_base;
   unsigned long long reads = 0;
   for (;;) {
@@ -912,7 +920,8 @@ __global__ void __launch_bounds__(256) k_light_first(const int4* __restrict__ LE
     __syncthreads();
     if (threadIdx.x == 0) s_base = s_n ? atomicAdd(n_out, s_n) : 0u;
     __syncthreads();
-    for (uint32_t j = threadIdx.x; j < s_n; j += blockDim.x) act_out[s_base + j] = s_rec[j];
+    for (uint32_t j = threadIdx.x; j < s_n; j += blockDim.x)
+      __stcs(reinterpret_cast<int2*>(act_out + s_base + j), *reinterpret_cast<const int2*>(s_rec + j));
     __syncthreads();
   }
   for (int o = 16; o > 0; o >>= 1) reads += __shfl_xor_sync(0xffffffffu, reads, o);
@@ -928,8 +937,8 @@ __global__ void __launch_bounds__(256) k_light_round(const int4* __restrict__ LE
                                                      uint32_t* __restrict__ grab, Offer* __restrict__ offers,
                                                      unsigned long long* __restrict__ Kc,
                                                      unsigned long long* __restrict__ n_entries) {
-  __shared__ Rec s_rec[kChunk];
-  __shared__ Offer s_off[kChunk];
+  __shared__ __align__(16) Rec s_rec[kChunk];
+  __shared__ __align__(16) Offer s_off[kChunk];
   __shared__ uint32_t s_n, s_chunk, s_base;
   unsigned long long reads = 0;
   for (;;) {
@@ -957,8 +966,8 @@ __global__ void __launch_bounds__(256) k_light_round(const int4* __restrict__ LE
     if (threadIdx.x == 0) s_base = s_n ? atomicAdd(n_out, s_n) : 0u;
     __syncthreads();
     for (uint32_t j = threadIdx.x; j < s_n; j += blockDim.x) {
-      act_out[s_base + j] = s_rec[j];
-      offers[s_base + j] = s_off[j];
+      __stcs(reinterpret_cast<int2*>(act_out + s_base + j), *reinterpret_cast<const int2*>(s_rec + j));
+      __stcs(reinterpret_cast<int4*>(offers + s_base + j), *reinterpret_cast<const int4*>(s_off + j));
     }
     __syncthreads();
   }
