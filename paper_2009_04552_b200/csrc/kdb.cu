@@ -680,10 +680,6 @@ __device__ __forceinline__ void ld256(const int4* p, int4& a, int4& b) {
 
 // records per chunk of the ordered row kernels (see k_light_first)
 constexpr int kChunk = 1024;
-// per-row filter metadata (written by the light pass): bits 0-14 light prefix
-// length (kW = "kW or more"), bit 15 = every entry of the row is within eps
-constexpr uint16_t kMetaAllIn = 0x8000u;
-constexpr uint16_t kMetaSkip = 0x7fffu;  // non-core row
 
 // one thread per row: 4 x (int4 + float4) loads in flight, 8 x int4 stores.
 // Exact mode also writes the certificate bound kth'(v) into kmin[comp v]; kth
@@ -694,8 +690,7 @@ __global__ void __launch_bounds__(256) k_light_ell(const int32_t* __restrict__ n
                                                    int64_t n_rows, int32_t k, float eps, int64_t row_begin,
                                                    const int32_t* __restrict__ comp, uint32_t* __restrict__ kmin,
                                                    int4* __restrict__ LE, Rec* __restrict__ act,
-                                                   uint32_t* __restrict__ n_act, uint32_t* __restrict__ grab,
-                                                   uint16_t* __restrict__ meta, float eps_full) {
+                                                   uint32_t* __restrict__ n_act, uint32_t* __restrict__ grab) {
   __shared__ __align__(16) Rec s_rec[kChunk];
   __shared__ uint32_t s_n, s_chunk, s_base;
   for (;;) {
@@ -708,10 +703,7 @@ __global__ void __launch_bounds__(256) k_light_ell(const int32_t* __restrict__ n
       if (i >= n_rows) continue;
       const int64_t v = row_begin + i;
       const int32_t cv = comp[v];
-      if (cv < 0) {
-        if (meta) meta[i] = kMetaSkip;
-        continue;
-      }
+      if (cv < 0) continue;
       const int32_t* nr = nbr + i * k;
       const float* dr = dist + i * k;
       int32_t J[kW];
@@ -760,17 +752,12 @@ __global__ void __launch_bounds__(256) k_light_ell(const int32_t* __restrict__ n
           w[c] = c < k ? __ldg(dr + c) : __int_as_float(0x7f800000);
         }
       }
-      // kth = D[v][k-1] >= D[v][kW-1]: only needed when that is within eps_run,
-      // or for the filter's per-row metadata
-      float kth = __int_as_float(0x7f800000);
-      if (meta || k <= kW || w[kW - 1] <= eps) kth = __ldcs(dr + (k - 1));
-      if (kmin) kmin[cv] = (kth <= eps) ? mono_bits(kth) : kInfBits;
-      if (meta) {
-        uint32_t pl = 0;
-#pragma unroll
-        for (int c = 0; c < kW; ++c) pl += (w[c] <= eps) ? 1u : 0u;  // sorted: the light prefix length
-        if (pl >= (uint32_t)kW && k > kW) pl = kW;                   // kW: ">= kW", the filter reads weights
-        meta[i] = (uint16_t)(pl | ((kth <= eps_full) ? kMetaAllIn : 0u));
+      // kth = D[v][k-1] >= D[v][kW-1]: only needed (exact-mode certificate) when
+      // that is within eps_run
+      if (kmin) {
+        float kth = __int_as_float(0x7f800000);
+        if (k <= kW || w[kW - 1] <= eps) kth = __ldcs(dr + (k - 1));
+        kmin[cv] = (kth <= eps) ? mono_bits(kth) : kInfBits;
       }
       int4* o = LE + i * (kW / 2);
 #pragma unroll
@@ -786,18 +773,6 @@ __global__ void __launch_bounds__(256) k_light_ell(const int32_t* __restrict__ n
   }
 }
 
-// filter metadata when the rows phase did not run over the ELL (in-place mode)
-__global__ void k_row_meta(const float* __restrict__ dist, int64_t n_rows, int32_t k, float tau, float eps,
-                           int64_t row_begin, const int32_t* __restrict__ comp, uint16_t* __restrict__ meta) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_rows; i += (int64_t)gridDim.x * blockDim.x) {
-    if (comp[row_begin + i] < 0) { meta[i] = kMetaSkip; continue; }
-    const float* dr = dist + i * k;
-    uint32_t pl = 0;
-    for (int c = 0; c < kW && c < k; ++c) pl += (__ldg(dr + c) <= tau) ? 1u : 0u;
-    if (pl >= (uint32_t)kW && k > kW) pl = kW;
-    meta[i] = (uint16_t)(pl | ((__ldg(dr + k - 1) <= eps) ? kMetaAllIn : 0u));
-  }
-}
 
 
 // Scan row v (component cv) from head h: columns < kW from the ELL row, the
@@ -1470,26 +1445,24 @@ struct FastDiv {
 __device__ __forceinline__ uint64_t fdiv(uint64_t q, const FastDiv& f) { return f.d == 1 ? q : __umul64hi(q, f.M); }
 
 // The filter: every rank streams its rows once, in tiles of kFilterThreads
-// rows.  Per tile, thread i stages row i's data in shared memory (metadata,
-// comp[v], the id range of comp[v]); then the tile's R*k entries are swept in
-// flat order, VEC per thread and step (VEC = 4: an int4 of ids, plus a float4
-// of weights only for rows whose metadata cannot classify entries without
-// them).  An entry is heavy if past the row's light prefix and within eps; a
-// heavy candidate survives iff comp[J] != comp[v].  Fast path: J inside the id
-// range of comp[v] and not in the Bloom filter of the exceptions => comp[J] ==
-// comp[v], no gather.
+// rows.  Per tile, thread i stages row i's data in shared memory (comp[v] and
+// the id range of comp[v]); then the tile's R*k ids are swept in flat order,
+// VEC per thread and step.  Fast path: J inside the id range of comp[v] and
+// not in the Bloom filter of the exceptions => comp[J] == comp[v]: the entry
+// is intra (or light, or beyond eps, or J == v -- none a candidate leaving
+// edge), decided from the id alone.  Otherwise the chunk's weights are loaded
+// and a heavy (tau < w <= eps) candidate survives iff comp[J] != comp[v].
 struct FRow {
-  uint32_t meta;  // kMetaSkip, or light length | kMetaAllIn
-  int32_t cr;     // comp[v]
+  int32_t cr;     // comp[v] (< 0: non-core row)
   uint32_t lo;    // id range of comp[v]: [lo, lo + span)
   uint32_t span;
+  uint32_t pad;
 };
 
 template <int VEC, bool FAST>
 __global__ void __launch_bounds__(kFilterThreads) k_filter(
     const int32_t* __restrict__ nbr, const float* __restrict__ dist, int64_t n_rows, int32_t k, float tau, float eps,
-    int64_t row_begin, int64_t N, const int32_t* __restrict__ comp, const uint16_t* __restrict__ meta,
-    const int2* __restrict__ rng, const uint32_t* __restrict__ bloom, FastDiv fd,
+    int64_t row_begin, int64_t N, const int32_t* __restrict__ comp, const int2* __restrict__ rng, const uint32_t* __restrict__ bloom, FastDiv fd,
     HEdge* __restrict__ out, uint32_t cap, uint32_t* __restrict__ n_out, unsigned long long* __restrict__ n_slow) {
   extern __shared__ uint32_t s_bloom[];
   __shared__ FRow s_row[kFilterThreads];
@@ -1508,16 +1481,12 @@ __global__ void __launch_bounds__(kFilterThreads) k_filter(
     if ((int)threadIdx.x < nr) {
       const int64_t i = r0 + threadIdx.x;
       FRow fr;
-      fr.meta = meta[i];
-      fr.cr = -1;
+      fr.cr = __ldg(comp + row_begin + i);
       fr.lo = 0;
       fr.span = 0;
-      if (fr.meta != kMetaSkip) {
-        fr.cr = __ldg(comp + row_begin + i);
-        if (FAST) {
-          const int2 rg = __ldg(rng + fr.cr);
-          if (rg.y > rg.x) { fr.lo = (uint32_t)rg.x; fr.span = (uint32_t)(rg.y - rg.x); }
-        }
+      if (FAST && fr.cr >= 0) {
+        const int2 rg = __ldg(rng + fr.cr);
+        if (rg.y > rg.x) { fr.lo = (uint32_t)rg.x; fr.span = (uint32_t)(rg.y - rg.x); }
       }
       s_row[threadIdx.x] = fr;
     }
@@ -1568,9 +1537,7 @@ __global__ void __launch_bounds__(kFilterThreads) k_filter(
             }
             slowm |= ((fast & 1u) ^ 1u) << j;
           }
-          const uint32_t pl = fr.meta & 0x7fffu;
-          const bool hw = (fr.meta & kMetaAllIn) == 0 || pl >= (uint32_t)kW;  // weights needed to classify
-          if (fr.meta == kMetaSkip) slowm = 0;
+          if (fr.cr < 0) slowm = 0;  // non-core row: no candidate entries
           if (slowm) {
             const uint32_t v = (uint32_t)(row_begin + r0 + lr);
             if (VEC == 4) {
@@ -1583,7 +1550,7 @@ __global__ void __launch_bounds__(kFilterThreads) k_filter(
             for (int j = 0; j < VEC; ++j) {
               cj[j] = -1;
               const uint32_t Jj = (uint32_t)J[t][j];
-              const bool heavy = hw ? (w[j] > tau && w[j] <= eps) : (col + j >= pl);
+              const bool heavy = w[j] > tau && w[j] <= eps;  // not light, and a candidate weight
               if (((slowm >> j) & 1u) && heavy && Jj < Nu && Jj != v) {
                 ++slow;
                 cj[j] = gat(comp + Jj);
@@ -1765,8 +1732,6 @@ struct RankState {
   uint32_t n_act = 0;                 // live rows in act[cur]
   bool compact = false;               // rows phase reads the light ELL (else the graph rows)
   int4* LE = nullptr;                 // light ELL [n_rows][kW] (J, w bits) pairs
-  uint16_t* meta = nullptr;           // filter metadata per row (kMetaAllIn | light length)
-  bool meta_ok = false;
   // offers: [0, n_rows) from rows (same slot as the row's next record),
   // [n_rows, n_rows + N) from in-lists (general mode)
   Offer* offers = nullptr;
@@ -1866,7 +1831,6 @@ size_t carve(Layout& L, char* base, bool dry, int64_t N, int nr, const int64_t* 
     R.act[0] = cv.take<Rec>(n);
     R.act[1] = cv.take<Rec>(n);
     R.LE = cv.take<int4>(n * (kW / 2));
-    R.meta = cv.take<uint16_t>(n);
     R.off_cap_rows = n;
     R.offers = cv.take<Offer>(general ? n + N : n);
     R.ctr = cv.take<RoundCounters>(1);
@@ -1968,8 +1932,6 @@ struct Mst {
   double t_init = 0, t_inlist = 0, t_min_edges = 0, t_contract = 0, t_filter = 0, t_heavy = 0;
   unsigned long long entries = 0, survivors = 0, exceptions = 0, slow_entries = 0;
   float tau = 0.f;
-  float eps_full = 0.f;  // the call's eps (the rows phase may run at tau)
-  bool want_meta = false;
   int fallback = 0;
   cudaEvent_t ev[4];
 };
@@ -2052,17 +2014,14 @@ kdb_status rows_phase(Mst& m, float eps_run) {
   for (auto& R : L.ranks) {
     KDB_CUDA(cudaMemsetAsync(R.ctr, 0, sizeof(RoundCounters), st));
     R.compact = false;
-    R.meta_ok = false;
     if (R.n_rows > 0 && use_compact) {
       R.compact = true;
-      R.meta_ok = m.want_meta;
       // 32-byte sector loads need 32-B aligned arrays, k % 8 in {0, 4} and rows
       // long enough for the third sector (k >= 20)
       const bool a32 = vec && k >= 20 && !(((uintptr_t)R.nbr | (uintptr_t)R.dist) & 31u);
 #define KDB_ELL_LAUNCH(V, A)                                                                                    \
   LAUNCH((k_light_ell<V, A>), grid_for(R.n_rows), kThreads, st, R.nbr, R.dist, R.n_rows, k, eps_run, R.row_begin, \
-         comp, general ? nullptr : L.kmin, R.LE, R.act[0], &R.ctr->n_act[0], &R.ctr->grab,                     \
-         m.want_meta ? R.meta : nullptr, m.eps_full)
+         comp, general ? nullptr : L.kmin, R.LE, R.act[0], &R.ctr->n_act[0], &R.ctr->grab)
       if (a32) KDB_ELL_LAUNCH(true, true);
       else if (vec) KDB_ELL_LAUNCH(true, false);
       else KDB_ELL_LAUNCH(false, false);
@@ -2322,9 +2281,6 @@ kdb_status filter_phase(Mst& m, float eps, bool* overflow) {
     KDB_CUDA(cudaMemsetAsync(R.n_hs_dev, 0, 2 * sizeof(uint32_t), st));
     if (cap_env >= 0) R.hs_cap = (uint32_t)std::min<int64_t>(R.hs_cap, cap_env);
     if (R.n_rows == 0) continue;
-    if (!R.meta_ok)
-      LAUNCH(k_row_meta, grid_for(R.n_rows), kThreads, st, R.dist, R.n_rows, m.k, m.tau, eps, R.row_begin, m.comp,
-             R.meta);
     const int vec = (m.k % 4) == 0 ? 4 : 1;
     FastDiv fd;  // entry index within a tile -> row within the tile
     fd.d = (uint64_t)m.k;
@@ -2335,7 +2291,7 @@ kdb_status filter_phase(Mst& m, float eps, bool* overflow) {
     const int grid = (int)std::min<int64_t>(ntiles, 1 << 30);
 #define KDB_FILTER_LAUNCH(V, F)                                                                                  \
   LAUNCH_DYN((k_filter<V, F>), grid, kFilterThreads, kFilterSmem, st, R.nbr, R.dist, R.n_rows, m.k, m.tau, eps,  \
-             R.row_begin, m.N, m.comp, R.meta, rng, L.bloom, fd, R.hs[0], R.hs_cap, R.n_hs_dev, L.fcount + 1)
+             R.row_begin, m.N, m.comp, rng, L.bloom, fd, R.hs[0], R.hs_cap, R.n_hs_dev, L.fcount + 1)
     if (vec == 4 && fast) KDB_FILTER_LAUNCH(4, true);
     else if (vec == 4) KDB_FILTER_LAUNCH(4, false);
     else if (fast) KDB_FILTER_LAUNCH(1, true);
@@ -2641,11 +2597,8 @@ kdb_status kdb_mst(const kdb_graph* g, float eps, const uint32_t* core_bits, int
     KDB_TRY(pick_tau(m, light_m, &m.tau));
     filtered = m.tau < eps;
   }
-  m.eps_full = eps;
   if (filtered) {
-    m.want_meta = true;
     KDB_TRY(rows_phase(m, m.tau));
-    m.want_meta = false;
     bool overflow = false;
     KDB_TRY(filter_phase(m, eps, &overflow));
     if (overflow) {  // too many crossing heavy entries for the survivor buffers
