@@ -690,7 +690,9 @@ __global__ void __launch_bounds__(256) k_light_ell(const int32_t* __restrict__ n
                                                    int64_t n_rows, int32_t k, float eps, int64_t row_begin,
                                                    const int32_t* __restrict__ comp, uint32_t* __restrict__ kmin,
                                                    int4* __restrict__ LE, Rec* __restrict__ act,
-                                                   uint32_t* __restrict__ n_act, uint32_t* __restrict__ grab) {
+                                                   uint32_t* __restrict__ n_act, uint32_t* __restrict__ grab,
+                                                   int direct, int all_core, int64_t N, uint64_t* __restrict__ Kc,
+                                                   uint32_t* __restrict__ Bc, int32_t* __restrict__ tgt) {
   __shared__ __align__(16) Rec s_rec[kChunk];
   __shared__ uint32_t s_n, s_chunk, s_base;
   for (;;) {
@@ -763,7 +765,51 @@ __global__ void __launch_bounds__(256) k_light_ell(const int32_t* __restrict__ n
 #pragma unroll
       for (int q = 0; q < kW / 2; ++q)
         __stcs(o + q, make_int4(J[2 * q], __float_as_int(w[2 * q]), J[2 * q + 1], __float_as_int(w[2 * q + 1])));
-      if (w[0] <= eps) s_rec[atomicAdd(&s_n, 1u)] = Rec{(int32_t)v, 0};
+      if (!direct) {
+        if (w[0] <= eps) s_rec[atomicAdd(&s_n, 1u)] = Rec{(int32_t)v, 0};
+        continue;
+      }
+      // Round 1 fused (exact mode, singleton components): the row's first
+      // candidate group, from the registers, is its component's minimum (see
+      // k_light_first); the list written is round 1's OUTPUT (rows that offered).
+      RowScan r{false, (int)k, kSent, kSentB, -1};
+      float wstar = 0.f;
+      bool done = false;
+#pragma unroll
+      for (int c = 0; c < kW; ++c) {
+        if (done || c >= k) continue;
+        const int32_t Jc = J[c];
+        if (!r.found) {
+          if (!(w[c] <= eps)) { done = true; continue; }  // sorted: no candidate at all
+          if (Jc < 0 || Jc >= N || Jc == v) continue;
+          const int32_t cc = all_core ? Jc : gat(comp + Jc);
+          if (cc < 0) continue;
+          r.found = true;
+          r.h = c;
+          wstar = w[c];
+          r.best = pack_key(mono_bits(w[c]), (uint32_t)min(v, (int64_t)Jc));
+          r.bestb = (uint32_t)max(v, (int64_t)Jc);
+          r.bestc = cc;
+        } else {
+          if (w[c] != wstar) { done = true; continue; }
+          if (Jc < 0 || Jc >= N || Jc == v) continue;
+          const int32_t cc = all_core ? Jc : gat(comp + Jc);
+          if (cc < 0) continue;
+          const uint64_t kk = pack_key(mono_bits(w[c]), (uint32_t)min(v, (int64_t)Jc));
+          const uint32_t bb = (uint32_t)max(v, (int64_t)Jc);
+          if (kk < r.best || (kk == r.best && bb < r.bestb)) { r.best = kk; r.bestb = bb; r.bestc = cc; }
+        }
+      }
+      if (!done && k > kW) {  // the search or the tie group runs past the ELL: scan the row in place
+        unsigned long long rd = 0;
+        r = scan_row<false, true>(nr, dr, k, eps, (int32_t)v, -1, 0, N, comp, all_core, rd);
+      }
+      if (r.found) {
+        Kc[cv] = r.best;
+        Bc[cv] = r.bestb;
+        tgt[cv] = r.bestc;
+        s_rec[atomicAdd(&s_n, 1u)] = Rec{(int32_t)v, r.h};
+      }
     }
     __syncthreads();
     if (threadIdx.x == 0) s_base = s_n ? atomicAdd(n_act, s_n) : 0u;
@@ -2011,6 +2057,10 @@ kdb_status rows_phase(Mst& m, float eps_run) {
     LAUNCH(k_fill_comp_arrays, grid_for(C), kThreads, st, C, L.ranks[r].Kc, L.ranks[r].Bc, nullptr);
   KDB_CUDA(cudaGetLastError());
   const bool use_compact = env_int("KDB_COMPACT", 1) != 0;
+  // exact mode: round 1 (singleton components) is fused into the ELL pass
+  const bool fuse1 = !general && use_compact && env_int("KDB_FUSE1", 1) != 0;
+  if (!general)  // hook targets of round 1 (written by the round-1 offers)
+    for (auto& R : L.ranks) LAUNCH(k_fill_i32, grid_for(C), kThreads, st, R.tgt, C, INT32_MAX);
   for (auto& R : L.ranks) {
     KDB_CUDA(cudaMemsetAsync(R.ctr, 0, sizeof(RoundCounters), st));
     R.compact = false;
@@ -2021,7 +2071,8 @@ kdb_status rows_phase(Mst& m, float eps_run) {
       const bool a32 = vec && k >= 20 && !(((uintptr_t)R.nbr | (uintptr_t)R.dist) & 31u);
 #define KDB_ELL_LAUNCH(V, A)                                                                                    \
   LAUNCH((k_light_ell<V, A>), grid_for(R.n_rows), kThreads, st, R.nbr, R.dist, R.n_rows, k, eps_run, R.row_begin, \
-         comp, general ? nullptr : L.kmin, R.LE, R.act[0], &R.ctr->n_act[0], &R.ctr->grab)
+         comp, general ? nullptr : L.kmin, R.LE, R.act[0], &R.ctr->n_act[0], &R.ctr->grab, fuse1 ? 1 : 0,      \
+         L.all_core, N, R.Kc, R.Bc, R.tgt)
       if (a32) KDB_ELL_LAUNCH(true, true);
       else if (vec) KDB_ELL_LAUNCH(true, false);
       else KDB_ELL_LAUNCH(false, false);
@@ -2032,10 +2083,7 @@ kdb_status rows_phase(Mst& m, float eps_run) {
              general ? nullptr : L.kmin, R.act[0], &R.ctr->n_act[0]);
     KDB_CUDA(cudaGetLastError());
   }
-  if (!general) {
-    KDB_TRY(allreduce_min_u32(comm, L.kmin, C, st));
-    for (auto& R : L.ranks) LAUNCH(k_fill_i32, grid_for(C), kThreads, st, R.tgt, C, INT32_MAX);
-  }
+  if (!general) KDB_TRY(allreduce_min_u32(comm, L.kmin, C, st));
   KDB_CUDA(cudaEventRecord(ev[1], st));
   // ---- general mode: in-edge lists --------------------------------------------
   if (general) {
@@ -2070,7 +2118,12 @@ kdb_status rows_phase(Mst& m, float eps_run) {
   m.t_inlist += elapsed(ev[1], ev[2]);
 
   // ---- Boruvka rounds -------------------------------------------------------------
-  int cur = 0;
+  // fused round 1: the ELL pass already wrote round 1's offers and its OUTPUT
+  // list into act[0], so round 1 "reads" act[1] and "writes" act[0]
+  bool any_compact = false;
+  for (auto& R : L.ranks) any_compact |= R.compact;
+  const bool fused = fuse1 && any_compact;
+  int cur = fused ? 1 : 0;
   int rounds = 0, stalls = 0;
   const uint32_t* kmin_cert = general ? nullptr : L.kmin;
   while (C > 0) {
@@ -2080,6 +2133,7 @@ kdb_status rows_phase(Mst& m, float eps_run) {
     KDB_CUDA(cudaEventRecord(ev[0], st));
     // a3: offers (rows, then in-lists), per rank, into that rank's Kc partial
     for (auto& R : L.ranks) {
+      if (direct && fused && R.compact) continue;  // done by the ELL pass
       KDB_CUDA(cudaMemsetAsync(&R.ctr->n_act[0], 0, 3 * sizeof(uint32_t), st));  // n_act[0..1], n_off
       KDB_CUDA(cudaMemsetAsync(&R.ctr->grab, 0, sizeof(uint32_t), st));
       if (R.n_act && R.compact) {

@@ -355,3 +355,17 @@ def test_wide_rows_exact(k):
         exp = oracle_run(nbr, dist, M, eps)
         assert_parity(run_gpu(nbr, dist, M, eps, exact=True), exp)
         assert_parity(run_gpu(nbr, dist, M, eps, exact=False), exp)
+
+
+@pytest.mark.parametrize("fuse", ["0", "1"])
+@pytest.mark.parametrize("P", [0, 3])
+def test_round1_fused_into_ell(c1_graph, fuse, P, monkeypatch):
+    """Exact mode: round 1 (singleton components) computed inside the light-ELL
+    pass (KDB_FUSE1=1, default) or by its own kernel (0) -- same forest."""
+    import paper_2009_04552_b200 as kdb
+    monkeypatch.setenv("KDB_FUSE1", fuse)
+    X, nbr, dist = c1_graph
+    for M, f in ((8, 1.5), (3, 0.7), (12, 3.0)):
+        eps = eps_from_graph(dist, M, f)
+        got = run_gpu(nbr, dist, M, eps, exact=True, comm=kdb.Comm.sim(P) if P else None)
+        assert_parity(got, oracle_run(nbr, dist, M, eps))
