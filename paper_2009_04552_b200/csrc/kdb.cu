@@ -297,7 +297,10 @@ struct RoundCounters {
   uint32_t n_cont;               // rows continuing in the warp-per-row scan
   uint32_t pad1;
   uint32_t grab;                 // chunk cursor of the ordered row kernels (per rank)
-  uint32_t pad2;
+  uint32_t n_off2;
+  uint32_t na[2];                // per rank: row-list sizes, ping-pong (input na[cur], output na[cur^1])
+  uint32_t ni[2];                // per rank: in-list sizes, ping-pong
+  long long Cs[2];               // global: component count, ping-pong (current Cs[par], next Cs[par^1])
   unsigned long long entries;    // graph entries (id + weight) read by offer kernels
 };
 
@@ -388,7 +391,8 @@ __global__ void k_init_comp(const uint32_t* __restrict__ bits, const uint32_t* _
 }
 
 __global__ void k_fill_comp_arrays(int64_t C, uint64_t* __restrict__ Kc, uint32_t* __restrict__ Bc,
-                                   uint32_t* __restrict__ kmin) {
+                                   uint32_t* __restrict__ kmin, const int64_t* __restrict__ Cp = nullptr) {
+  if (Cp) C = *Cp;
   for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < C;
        c += (int64_t)gridDim.x * blockDim.x) {
     Kc[c] = kSent;
@@ -594,7 +598,8 @@ __global__ void __launch_bounds__(256) k_offer_first(const int32_t* __restrict__
                                                      const Rec* __restrict__ act, uint32_t n_in,
                                                      Rec* __restrict__ act_out, uint32_t* __restrict__ n_out,
                                                      uint64_t* __restrict__ Kc, uint32_t* __restrict__ Bc,
-                                                     int32_t* __restrict__ tgt, unsigned long long* __restrict__ n_entries) {
+                                                     int32_t* __restrict__ tgt, unsigned long long* __restrict__ n_entries, const uint32_t* __restrict__ n_in_p = nullptr) {
+  if (n_in_p) n_in = *n_in_p;
   unsigned long long reads = 0;
   for (uint32_t base = blockIdx.x * blockDim.x; base < n_in; base += gridDim.x * blockDim.x) {
     const uint32_t s = base + threadIdx.x;
@@ -630,7 +635,8 @@ __global__ void __launch_bounds__(256) k_offer_round(const int32_t* __restrict__
                                                      uint32_t n_in, Rec* __restrict__ act_out,
                                                      uint32_t* __restrict__ n_out, Offer* __restrict__ offers,
                                                      unsigned long long* __restrict__ Kc,
-                                                     unsigned long long* __restrict__ n_entries) {
+                                                     unsigned long long* __restrict__ n_entries, const uint32_t* __restrict__ n_in_p = nullptr) {
+  if (n_in_p) n_in = *n_in_p;
   unsigned long long reads = 0;
   for (uint32_t base = blockIdx.x * blockDim.x; base < n_in; base += gridDim.x * blockDim.x) {
     const uint32_t s = base + threadIdx.x;
@@ -913,7 +919,8 @@ __global__ void __launch_bounds__(256) k_light_first(const int4* __restrict__ LE
                                                      Rec* __restrict__ act_out, uint32_t* __restrict__ n_out,
                                                      uint32_t* __restrict__ grab,
                                                      uint64_t* __restrict__ Kc, uint32_t* __restrict__ Bc,
-                                                     int32_t* __restrict__ tgt, unsigned long long* __restrict__ n_entries) {
+                                                     int32_t* __restrict__ tgt, unsigned long long* __restrict__ n_entries, const uint32_t* __restrict__ n_in_p = nullptr) {
+  if (n_in_p) n_in = *n_in_p;
   __shared__ __align__(16) Rec s_rec[kChunk];
   __shared__ uint32_t s_n, s_chunk, s_base;
   unsigned long long reads = 0;
@@ -957,7 +964,8 @@ __global__ void __launch_bounds__(256) k_light_round(const int4* __restrict__ LE
                                                      Rec* __restrict__ act_out, uint32_t* __restrict__ n_out,
                                                      uint32_t* __restrict__ grab, Offer* __restrict__ offers,
                                                      unsigned long long* __restrict__ Kc,
-                                                     unsigned long long* __restrict__ n_entries) {
+                                                     unsigned long long* __restrict__ n_entries, const uint32_t* __restrict__ n_in_p = nullptr) {
+  if (n_in_p) n_in = *n_in_p;
   __shared__ __align__(16) Rec s_rec[kChunk];
   __shared__ __align__(16) Offer s_off[kChunk];
   __shared__ uint32_t s_n, s_chunk, s_base;
@@ -1003,7 +1011,8 @@ __global__ void k_offer_in(const unsigned long long* __restrict__ in_off, int32_
                            const int32_t* __restrict__ comp, const int32_t* __restrict__ act_in,
                            uint32_t n_in, int32_t* __restrict__ act_out, uint32_t* __restrict__ n_out,
                            Offer* __restrict__ offers, uint32_t* __restrict__ n_off,
-                           unsigned long long* __restrict__ Kc) {
+                           unsigned long long* __restrict__ Kc, const uint32_t* __restrict__ n_in_p = nullptr) {
+  if (n_in_p) n_in = *n_in_p;
   for (uint32_t base = blockIdx.x * blockDim.x; base < n_in; base += gridDim.x * blockDim.x) {
     const uint32_t s = base + threadIdx.x;
     bool found = false, keep = false;
@@ -1089,11 +1098,15 @@ __global__ void k_sweep(const int32_t* __restrict__ nbr, const float* __restrict
 // sim backend: elementwise MIN of per-virtual-rank partials
 // ============================================================================
 
-__global__ void k_min_into_u64(uint64_t* __restrict__ d, const uint64_t* __restrict__ s, int64_t n) {
+__global__ void k_min_into_u64(uint64_t* __restrict__ d, const uint64_t* __restrict__ s, int64_t n,
+                               const int64_t* __restrict__ np = nullptr) {
+  if (np) n = *np;
   for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n; c += (int64_t)gridDim.x * blockDim.x)
     if (s[c] < d[c]) d[c] = s[c];
 }
-__global__ void k_min_into_u32(uint32_t* __restrict__ d, const uint32_t* __restrict__ s, int64_t n) {
+__global__ void k_min_into_u32(uint32_t* __restrict__ d, const uint32_t* __restrict__ s, int64_t n,
+                               const int64_t* __restrict__ np = nullptr) {
+  if (np) n = *np;
   for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n; c += (int64_t)gridDim.x * blockDim.x)
     if (s[c] < d[c]) d[c] = s[c];
 }
@@ -1119,7 +1132,8 @@ __global__ void __launch_bounds__(256) k_hook(int64_t C, const uint64_t* __restr
                        const int32_t* __restrict__ tgt, const uint32_t* __restrict__ kmin /* null = all certified */,
                        const int32_t* __restrict__ comp, int32_t* __restrict__ parent,
                        uint64_t* __restrict__ e_key, float* __restrict__ e_w, int64_t e_cap,
-                       RoundCounters* __restrict__ ctr) {
+                       RoundCounters* __restrict__ ctr, const int64_t* __restrict__ Cp = nullptr) {
+  if (Cp) C = *Cp;
   __shared__ uint64_t s_key[kHookChunk];
   __shared__ uint32_t s_w[kHookChunk];
   __shared__ uint32_t s_n, s_base;
@@ -1203,7 +1217,9 @@ __global__ void __launch_bounds__(256) k_hook(int64_t C, const uint64_t* __restr
 // same root; stale reads are ancestors too, so the loop terminates.  The root
 // goes to a SEPARATE array: another thread's halving write may land on
 // parent[c] after c found its root, so parent[c] itself is not final.
-__global__ void k_jump(int64_t C, int32_t* parent, int32_t* __restrict__ rootof, RoundCounters* ctr) {
+__global__ void k_jump(int64_t C, int32_t* parent, int32_t* __restrict__ rootof, RoundCounters* ctr,
+                       const int64_t* __restrict__ Cp = nullptr) {
+  if (Cp) C = *Cp;
   volatile int32_t* P = parent;
   for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < C;
        c += (int64_t)gridDim.x * blockDim.x) {
@@ -1225,16 +1241,28 @@ __global__ void k_jump(int64_t C, int32_t* parent, int32_t* __restrict__ rootof,
   }
 }
 
-__global__ void k_root_flags(int64_t C, const int32_t* __restrict__ rootof, int32_t* __restrict__ flag) {
+__global__ void k_root_flags(int64_t C, const int32_t* __restrict__ rootof, int32_t* __restrict__ flag,
+                             const int64_t* __restrict__ Cp = nullptr) {
+  // C is the (host) upper bound the scan runs over; with Cp the true count is
+  // on the device and the flags beyond it are 0
+  const int64_t Ct = Cp ? *Cp : C;
   for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < C;
        c += (int64_t)gridDim.x * blockDim.x)
-    flag[c] = rootof[c] == (int32_t)c;
+    flag[c] = c < Ct && rootof[c] == (int32_t)c;
+}
+
+// number of roots = new component count, from the exclusive scan
+__global__ void k_count_roots(const int64_t* __restrict__ Cp, const int32_t* __restrict__ newid,
+                              const int32_t* __restrict__ flag, int64_t* __restrict__ Cn) {
+  const int64_t C = *Cp;
+  *Cn = C > 0 ? (int64_t)newid[C - 1] + flag[C - 1] : 0;
 }
 
 // new per-component arrays: cmin/kmin are minima over the merged tree
 __global__ void k_merge(int64_t C, const int32_t* __restrict__ rootof, const int32_t* __restrict__ newid,
                         const int32_t* __restrict__ cmin, const uint32_t* __restrict__ kmin,
-                        int32_t* __restrict__ cmin2, uint32_t* __restrict__ kmin2, int32_t* __restrict__ map) {
+                        int32_t* __restrict__ cmin2, uint32_t* __restrict__ kmin2, int32_t* __restrict__ map, const int64_t* __restrict__ Cp = nullptr) {
+  if (Cp) C = *Cp;
   for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < C;
        c += (int64_t)gridDim.x * blockDim.x) {
     const int32_t r = gat(newid + rootof[c]);
@@ -1247,7 +1275,8 @@ __global__ void k_merge(int64_t C, const int32_t* __restrict__ rootof, const int
   }
 }
 
-__global__ void k_fill_i32(int32_t* __restrict__ p, int64_t n, int32_t val) {
+__global__ void k_fill_i32(int32_t* __restrict__ p, int64_t n, int32_t val, const int64_t* __restrict__ np = nullptr) {
+  if (np) n = *np;
   for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n;
        c += (int64_t)gridDim.x * blockDim.x)
     p[c] = val;
@@ -2071,7 +2100,7 @@ kdb_status rows_phase(Mst& m, float eps_run) {
       const bool a32 = vec && k >= 20 && !(((uintptr_t)R.nbr | (uintptr_t)R.dist) & 31u);
 #define KDB_ELL_LAUNCH(V, A)                                                                                    \
   LAUNCH((k_light_ell<V, A>), grid_for(R.n_rows), kThreads, st, R.nbr, R.dist, R.n_rows, k, eps_run, R.row_begin, \
-         comp, general ? nullptr : L.kmin, R.LE, R.act[0], &R.ctr->n_act[0], &R.ctr->grab, fuse1 ? 1 : 0,      \
+         comp, general ? nullptr : L.kmin, R.LE, R.act[0], &R.ctr->na[0], &R.ctr->grab, fuse1 ? 1 : 0,         \
          L.all_core, N, R.Kc, R.Bc, R.tgt)
       if (a32) KDB_ELL_LAUNCH(true, true);
       else if (vec) KDB_ELL_LAUNCH(true, false);
@@ -2080,7 +2109,7 @@ kdb_status rows_phase(Mst& m, float eps_run) {
     }
     if (R.n_rows > 0 && !R.compact)
       LAUNCH(k_init_rows, grid_for(R.n_rows), kThreads, st, R.dist, R.n_rows, k, eps_run, R.row_begin, comp,
-             general ? nullptr : L.kmin, R.act[0], &R.ctr->n_act[0]);
+             general ? nullptr : L.kmin, R.act[0], &R.ctr->na[0]);
     KDB_CUDA(cudaGetLastError());
   }
   if (!general) KDB_TRY(allreduce_min_u32(comm, L.kmin, C, st));
@@ -2101,7 +2130,7 @@ kdb_status rows_phase(Mst& m, float eps_run) {
       if (R.n_rows > 0)
         LAUNCH(k_in_fill, grid_for(R.n_rows), kThreads, st, R.nbr, R.dist, R.n_rows, k, eps_run, R.row_begin, N,
                core_bits, cursor, R.in_src, R.in_w);
-      LAUNCH(k_in_finish, grid_for(N), kThreads, st, R.in_off, N, R.in_len, R.in_act[0], &R.ctr->n_act[1]);
+      LAUNCH(k_in_finish, grid_for(N), kThreads, st, R.in_off, N, R.in_len, R.in_act[0], &R.ctr->ni[0]);
       KDB_CUDA(cudaGetLastError());
     }
   }
@@ -2109,8 +2138,8 @@ kdb_status rows_phase(Mst& m, float eps_run) {
     RoundCounters hc;
     KDB_CUDA(cudaMemcpyAsync(&hc, R.ctr, sizeof(hc), cudaMemcpyDeviceToHost, st));
     KDB_CUDA(cudaStreamSynchronize(st));
-    R.n_act = hc.n_act[0];
-    R.n_in_act = hc.n_act[1];
+    R.n_act = hc.na[0];
+    R.n_in_act = hc.ni[0];
   }
   KDB_CUDA(cudaEventRecord(ev[2], st));
   KDB_CUDA(cudaEventSynchronize(ev[2]));
@@ -2118,173 +2147,267 @@ kdb_status rows_phase(Mst& m, float eps_run) {
   m.t_inlist += elapsed(ev[1], ev[2]);
 
   // ---- Boruvka rounds -------------------------------------------------------------
-  // fused round 1: the ELL pass already wrote round 1's offers and its OUTPUT
-  // list into act[0], so round 1 "reads" act[1] and "writes" act[0]
+  // Pipelined: every kernel reads its counts (components, list sizes) from the
+  // device; grids are sized by host upper bounds one round stale, so the host
+  // enqueues round r+1 before it has looked at round r and checks round r-1's
+  // counters (termination, violations, stalls) from pinned memory meanwhile.
+  // A round launched after the last productive one finds nothing and changes
+  // nothing.  With a real NCCL communicator the collectives need exact host
+  // counts: the loop then waits for each round's counters (sync_each).
   bool any_compact = false;
   for (auto& R : L.ranks) any_compact |= R.compact;
   const bool fused = fuse1 && any_compact;
-  int cur = fused ? 1 : 0;
+  const bool sync_each = comm && comm->kind == 1 && comm->nranks > 1;
+  int cur = fused ? 1 : 0;  // fused round 1: its OUTPUT list is act[0] already
+  int par = 0;              // component count ping-pong: Cs[par] current
+  {
+    long long c0 = C;
+    KDB_CUDA(cudaMemcpyAsync(&L.ctr->Cs[0], &c0, sizeof(c0), cudaMemcpyHostToDevice, st));
+  }
+  const size_t nr = L.ranks.size();
+  // pinned slots for the round counters: [0] global, [1 + r] rank r
+  constexpr int kSlots = 4;
+  // (a per-thread pinned buffer, grown on demand: cudaMallocHost per call is slow)
+  static thread_local RoundCounters* slots = nullptr;
+  static thread_local size_t slots_cap = 0;
+  if (slots_cap < kSlots * (1 + nr)) {
+    if (slots) cudaFreeHost(slots);
+    slots = nullptr;
+    slots_cap = 0;
+    KDB_CUDA(cudaMallocHost(&slots, kSlots * (1 + nr) * sizeof(RoundCounters)));
+    slots_cap = kSlots * (1 + nr);
+  }
+  std::vector<cudaEvent_t> ev_slot(kSlots), ev_rnd;
+  for (auto& e : ev_slot) KDB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  struct EvVecGuard {
+    std::vector<cudaEvent_t>* a;
+    std::vector<cudaEvent_t>* b;
+    ~EvVecGuard() {
+      for (auto e : *a) cudaEventDestroy(e);
+      for (auto e : *b) cudaEventDestroy(e);
+    }
+  } evg{&ev_slot, &ev_rnd};
+  int64_t C_ub = C;  // upper bound of the current component count
+  std::vector<uint32_t> na_ub(nr), ni_ub(nr);
+  for (size_t r = 0; r < nr; ++r) {
+    na_ub[r] = L.ranks[r].n_act;
+    ni_ub[r] = L.ranks[r].n_in_act;
+  }
   int rounds = 0, stalls = 0;
   const uint32_t* kmin_cert = general ? nullptr : L.kmin;
-  while (C > 0) {
-    ++rounds;
-    // round 1 of exact mode: singleton components, one offer each (no in-lists)
-    const bool direct = rounds == 1 && !general;
-    KDB_CUDA(cudaEventRecord(ev[0], st));
-    // a3: offers (rows, then in-lists), per rank, into that rank's Kc partial
-    for (auto& R : L.ranks) {
-      if (direct && fused && R.compact) continue;  // done by the ELL pass
-      KDB_CUDA(cudaMemsetAsync(&R.ctr->n_act[0], 0, 3 * sizeof(uint32_t), st));  // n_act[0..1], n_off
-      KDB_CUDA(cudaMemsetAsync(&R.ctr->grab, 0, sizeof(uint32_t), st));
-      if (R.n_act && R.compact) {
-        if (direct)
-          LAUNCH(k_light_first, grid_for(R.n_act), kThreads, st, R.LE, R.nbr, R.dist, k, eps_run, R.row_begin, N,
-                 comp, L.all_core, R.act[cur], R.n_act, R.act[cur ^ 1], &R.ctr->n_act[0], &R.ctr->grab, R.Kc, R.Bc,
-                 R.tgt, &L.ctr->entries);
-        else
-          LAUNCH(k_light_round, grid_for(R.n_act), kThreads, st, R.LE, R.nbr, R.dist, k, eps_run, R.row_begin, N,
-                 comp, R.act[cur], R.n_act, R.act[cur ^ 1], &R.ctr->n_act[0], &R.ctr->grab, R.offers,
-                 (unsigned long long*)R.Kc, &L.ctr->entries);
-      } else if (R.n_act) {
-        if (direct) {
-          if (vec)
-            LAUNCH(k_offer_first<true>, grid_for(R.n_act), kThreads, st, R.nbr, R.dist, k, eps_run, R.row_begin, N,
-                   comp, L.all_core, R.act[cur], R.n_act, R.act[cur ^ 1], &R.ctr->n_act[0], R.Kc, R.Bc, R.tgt,
-                   &L.ctr->entries);
-          else
-            LAUNCH(k_offer_first<false>, grid_for(R.n_act), kThreads, st, R.nbr, R.dist, k, eps_run, R.row_begin,
-                   N, comp, L.all_core, R.act[cur], R.n_act, R.act[cur ^ 1], &R.ctr->n_act[0], R.Kc, R.Bc, R.tgt,
-                   &L.ctr->entries);
-        } else {
-          if (vec)
-            LAUNCH(k_offer_round<true>, grid_for(R.n_act), kThreads, st, R.nbr, R.dist, k, eps_run, R.row_begin, N,
-                   comp, R.act[cur], R.n_act, R.act[cur ^ 1], &R.ctr->n_act[0], R.offers,
-                   (unsigned long long*)R.Kc, &L.ctr->entries);
-          else
-            LAUNCH(k_offer_round<false>, grid_for(R.n_act), kThreads, st, R.nbr, R.dist, k, eps_run, R.row_begin,
-                   N, comp, R.act[cur], R.n_act, R.act[cur ^ 1], &R.ctr->n_act[0], R.offers,
-                   (unsigned long long*)R.Kc, &L.ctr->entries);
-        }
-      }
-      if (general && R.n_in_act)
-        LAUNCH(k_offer_in, grid_for(R.n_in_act), kThreads, st, R.in_off, R.in_len, R.in_src, R.in_w, comp,
-               R.in_act[cur], R.n_in_act, R.in_act[cur ^ 1], &R.ctr->n_act[1], R.offers + R.off_cap_rows,
-               &R.ctr->n_off, (unsigned long long*)R.Kc);
-      KDB_CUDA(cudaGetLastError());
-    }
-    // exchange: sim -> min over virtual ranks; nccl -> allreduce
-    for (size_t r = 1; r < L.ranks.size(); ++r)
-      LAUNCH(k_min_into_u64, grid_for(C), kThreads, st, L.Kc, L.ranks[r].Kc, C);
-    KDB_TRY(allreduce_min_u64(comm, L.Kc, C, st));
-    // a4: ties (the direct round already wrote Bc and the targets)
-    if (!direct) {
-      for (auto& R : L.ranks) {
-        if (R.n_act) LAUNCH(k_tie, grid_for(R.n_act), kThreads, st, R.offers, &R.ctr->n_act[0], L.Kc, R.Bc);
-        if (general && R.n_in_act)
-          LAUNCH(k_tie, grid_for(R.n_in_act), kThreads, st, R.offers + R.off_cap_rows, &R.ctr->n_off, L.Kc, R.Bc);
-        KDB_CUDA(cudaGetLastError());
-      }
-    }
-    for (size_t r = 1; r < L.ranks.size(); ++r)
-      LAUNCH(k_min_into_u32, grid_for(C), kThreads, st, L.Bc, L.ranks[r].Bc, C);
-    KDB_TRY(allreduce_min_u32(comm, L.Bc, C, st));
-    if (direct) {
-      for (size_t r = 1; r < L.ranks.size(); ++r)
-        LAUNCH(k_min_into_u32, grid_for(C), kThreads, st, (uint32_t*)L.tgt, (const uint32_t*)L.ranks[r].tgt, C);
-      KDB_TRY(allreduce_min_u32(comm, (uint32_t*)L.tgt, C, st));  // non-owners hold INT32_MAX
-    }
-    KDB_CUDA(cudaEventRecord(ev[1], st));
-    // a5: hook + emit
-    KDB_CUDA(cudaMemsetAsync(&L.ctr->hooks, 0, 4 * sizeof(uint32_t), st));
-    LAUNCH(k_hook, grid_for(C), kThreads, st, C, L.Kc, L.Bc, direct ? L.tgt : nullptr, kmin_cert, comp, L.parent,
-           L.e_key, L.e_w, N, L.ctr);
-    KDB_CUDA(cudaGetLastError());
-    RoundCounters hc;
-    KDB_CUDA(cudaMemcpyAsync(&hc, L.ctr, sizeof(hc), cudaMemcpyDeviceToHost, st));
-    std::vector<RoundCounters> rc(L.ranks.size());
-    for (size_t r = 0; r < L.ranks.size(); ++r)
-      KDB_CUDA(cudaMemcpyAsync(&rc[r], L.ranks[r].ctr, sizeof(RoundCounters), cudaMemcpyDeviceToHost, st));
-    KDB_CUDA(cudaStreamSynchronize(st));
-    if (g_trace) {
-      static unsigned long long last_entries = 0;
-      if (rounds == 1) last_entries = 0;
-      fprintf(stderr, "[kdb] round %d eps=%.6g C=%lld live=%u -> %u entries=%llu offer_ms=%.3f hooks=%u\n",
-              rounds, (double)eps_run, (long long)C, L.ranks[0].n_act, rc[0].n_act[0],
-              hc.entries - last_entries, elapsed(ev[0], ev[1]), hc.hooks);
-      last_entries = hc.entries;
-    }
-    for (size_t r = 0; r < L.ranks.size(); ++r) {
-      L.ranks[r].n_act = rc[r].n_act[0];
-      L.ranks[r].n_in_act = rc[r].n_act[1];
-    }
-    if (hc.offered == 0) {  // a8: no component has a leaving edge
-      m.t_min_edges += elapsed(ev[0], ev[1]);
-      break;
-    }
-    if (hc.hooks == 0) {
-      // every offering component abstained: one edge-centric sweep round gives
-      // every component its exact minimum (both endpoints see every entry)
-      ++stalls;
-      LAUNCH(k_fill_comp_arrays, grid_for(C), kThreads, st, C, L.Kc, L.Bc, nullptr);
-      for (size_t r = 1; r < L.ranks.size(); ++r)
-        LAUNCH(k_fill_comp_arrays, grid_for(C), kThreads, st, C, L.ranks[r].Kc, L.ranks[r].Bc, nullptr);
-      for (auto& R : L.ranks)
-        if (R.n_act)
-          LAUNCH(k_sweep, grid_for(R.n_act), kThreads, st, R.nbr, R.dist, k, eps_run, R.row_begin, N, comp,
-                 R.act[cur ^ 1], R.n_act, (unsigned long long*)R.Kc, R.Bc, 0);
-      for (size_t r = 1; r < L.ranks.size(); ++r)
-        LAUNCH(k_min_into_u64, grid_for(C), kThreads, st, L.Kc, L.ranks[r].Kc, C);
-      KDB_TRY(allreduce_min_u64(comm, L.Kc, C, st));
-      for (auto& R : L.ranks)
-        if (R.n_act)
-          LAUNCH(k_sweep, grid_for(R.n_act), kThreads, st, R.nbr, R.dist, k, eps_run, R.row_begin, N, comp,
-                 R.act[cur ^ 1], R.n_act, (unsigned long long*)L.Kc, R.Bc, 1);
-      for (size_t r = 1; r < L.ranks.size(); ++r)
-        LAUNCH(k_min_into_u32, grid_for(C), kThreads, st, L.Bc, L.ranks[r].Bc, C);
-      KDB_TRY(allreduce_min_u32(comm, L.Bc, C, st));
-      KDB_CUDA(cudaMemsetAsync(&L.ctr->hooks, 0, 4 * sizeof(uint32_t), st));
-      LAUNCH(k_hook, grid_for(C), kThreads, st, C, L.Kc, L.Bc, nullptr, nullptr, comp, L.parent, L.e_key, L.e_w, N,
-             L.ctr);
-      KDB_CUDA(cudaGetLastError());
-      KDB_CUDA(cudaMemcpyAsync(&hc, L.ctr, sizeof(hc), cudaMemcpyDeviceToHost, st));
-      KDB_CUDA(cudaStreamSynchronize(st));
-      if (hc.hooks == 0) return set_err(KDB_EINTERNAL, "sweep round made no progress");
-      // rows whose scan found nothing are exhausted for good and stay out of the
-      // active list; rows that still hold leaving entries are in it
-    }
-    if (hc.violation) return set_err(KDB_EINVAL, "graph violates the KDB_GRAPH_EXACT promise (a component's "
-                                     "minimum missed an incident edge)");
-    // a6: contract
-    LAUNCH(k_jump, grid_for(C), kThreads, st, C, L.parent, L.rootof, L.ctr);
-    LAUNCH(k_root_flags, grid_for(C), kThreads, st, C, L.rootof, L.flag);
-    cb = L.cub_bytes;
-    { LaunchScope ls_("cub::DeviceScan", st, false); KDB_CUDA(cub::DeviceScan::ExclusiveSum(L.cub_tmp, cb, L.flag, L.newid, (int)C, st)); }
-    uint32_t viol = 0;
-    KDB_CUDA(cudaMemcpyAsync(&viol, &L.ctr->violation, 4, cudaMemcpyDeviceToHost, st));
-    int32_t last[2];
-    KDB_CUDA(cudaMemcpyAsync(&last[0], L.newid + C - 1, 4, cudaMemcpyDeviceToHost, st));
-    KDB_CUDA(cudaMemcpyAsync(&last[1], L.flag + C - 1, 4, cudaMemcpyDeviceToHost, st));
-    KDB_CUDA(cudaStreamSynchronize(st));
-    if (viol) return set_err(KDB_EINTERNAL, "pointer jumping did not converge (hook cycle)");
-    const int64_t C2 = (int64_t)last[0] + last[1];
-    LAUNCH(k_fill_i32, grid_for(C2), kThreads, st, L.cmin2, C2, INT32_MAX);
-    if (!general) LAUNCH(k_fill_i32, grid_for(C2), kThreads, st, (int32_t*)L.kmin2, C2, (int32_t)kInfBits);
+  auto slot_of = [&](int rr) { return slots + (size_t)(rr % kSlots) * (1 + nr); };
+
+  // contraction a6 on the device counts; C_bound >= the true count
+  auto contract = [&](int64_t C_bound) -> kdb_status {
+    const int64_t* Cd = (const int64_t*)&L.ctr->Cs[par];
+    int64_t* Cn = (int64_t*)&L.ctr->Cs[par ^ 1];
+    LAUNCH(k_jump, grid_for(C_bound), kThreads, st, C_bound, L.parent, L.rootof, L.ctr, Cd);
+    LAUNCH(k_root_flags, grid_for(C_bound), kThreads, st, C_bound, L.rootof, L.flag, Cd);
+    size_t cb2 = L.cub_bytes;
+    { LaunchScope ls_("cub::DeviceScan", st, false); KDB_CUDA(cub::DeviceScan::ExclusiveSum(L.cub_tmp, cb2, L.flag, L.newid, (int)std::max<int64_t>(C_bound, 1), st)); }
+    LAUNCH(k_count_roots, 1, 1, st, Cd, L.newid, L.flag, Cn);
+    LAUNCH(k_fill_i32, grid_for(C_bound), kThreads, st, L.cmin2, C_bound, INT32_MAX, (const int64_t*)Cn);
+    if (!general)
+      LAUNCH(k_fill_i32, grid_for(C_bound), kThreads, st, (int32_t*)L.kmin2, C_bound, (int32_t)kInfBits,
+             (const int64_t*)Cn);
     // map[c] = new dense id of c's tree (reuses `parent`, no longer needed)
-    LAUNCH(k_merge, grid_for(C), kThreads, st, C, L.rootof, L.newid, L.cmin, general ? nullptr : L.kmin, L.cmin2,
-           L.kmin2, L.parent);
+    LAUNCH(k_merge, grid_for(C_bound), kThreads, st, C_bound, L.rootof, L.newid, L.cmin, general ? nullptr : L.kmin,
+           L.cmin2, L.kmin2, L.parent, Cd);
     LAUNCH(k_relabel, grid_for(N / 8 + 1), kThreads, st, N, comp, L.parent, (const int32_t*)nullptr);
-    LAUNCH(k_fill_comp_arrays, grid_for(C2), kThreads, st, C2, L.Kc, L.Bc, nullptr);
-    for (size_t r = 1; r < L.ranks.size(); ++r)
-      LAUNCH(k_fill_comp_arrays, grid_for(C2), kThreads, st, C2, L.ranks[r].Kc, L.ranks[r].Bc, nullptr);
+    LAUNCH(k_fill_comp_arrays, grid_for(C_bound), kThreads, st, C_bound, L.Kc, L.Bc, nullptr, (const int64_t*)Cn);
+    for (size_t r = 1; r < nr; ++r)
+      LAUNCH(k_fill_comp_arrays, grid_for(C_bound), kThreads, st, C_bound, L.ranks[r].Kc, L.ranks[r].Bc, nullptr,
+             (const int64_t*)Cn);
     KDB_CUDA(cudaGetLastError());
     std::swap(L.cmin, L.cmin2);
     std::swap(L.kmin, L.kmin2);
     kmin_cert = general ? nullptr : L.kmin;
-    C = C2;
+    par ^= 1;
+    return KDB_OK;
+  };
+  // snapshot of the counters after the current round into a pinned slot
+  auto snapshot = [&](int rr) -> kdb_status {
+    RoundCounters* sl = slot_of(rr);
+    KDB_CUDA(cudaMemcpyAsync(sl, L.ctr, sizeof(RoundCounters), cudaMemcpyDeviceToHost, st));
+    for (size_t r = 0; r < nr; ++r)
+      KDB_CUDA(cudaMemcpyAsync(sl + 1 + r, L.ranks[r].ctr, sizeof(RoundCounters), cudaMemcpyDeviceToHost, st));
+    KDB_CUDA(cudaEventRecord(ev_slot[rr % kSlots], st));
+    return KDB_OK;
+  };
+
+  int last_checked = 0;
+  bool finished = false;
+  while (!finished) {
+    ++rounds;
+    const bool direct = rounds == 1 && !general;
+    const int64_t* Cd = (const int64_t*)&L.ctr->Cs[par];
+    cudaEvent_t e0;
+    KDB_CUDA(cudaEventCreate(&e0));
+    ev_rnd.push_back(e0);
+    KDB_CUDA(cudaEventRecord(e0, st));
+    // a3: offers (rows, then in-lists), per rank, into that rank's Kc partial
+    for (size_t r = 0; r < nr; ++r) {
+      RankState& R = L.ranks[r];
+      if (direct && fused && R.compact) continue;  // done by the ELL pass
+      KDB_CUDA(cudaMemsetAsync(&R.ctr->na[cur ^ 1], 0, sizeof(uint32_t), st));
+      KDB_CUDA(cudaMemsetAsync(&R.ctr->ni[cur ^ 1], 0, sizeof(uint32_t), st));
+      KDB_CUDA(cudaMemsetAsync(&R.ctr->n_off, 0, sizeof(uint32_t), st));
+      KDB_CUDA(cudaMemsetAsync(&R.ctr->grab, 0, sizeof(uint32_t), st));
+      const uint32_t* nin = &R.ctr->na[cur];
+      uint32_t* nout = &R.ctr->na[cur ^ 1];
+      if (na_ub[r] && R.compact) {
+        if (direct)
+          LAUNCH(k_light_first, grid_for(na_ub[r]), kThreads, st, R.LE, R.nbr, R.dist, k, eps_run, R.row_begin, N,
+                 comp, L.all_core, R.act[cur], na_ub[r], R.act[cur ^ 1], nout, &R.ctr->grab, R.Kc, R.Bc, R.tgt,
+                 &L.ctr->entries, nin);
+        else
+          LAUNCH(k_light_round, grid_for(na_ub[r]), kThreads, st, R.LE, R.nbr, R.dist, k, eps_run, R.row_begin, N,
+                 comp, R.act[cur], na_ub[r], R.act[cur ^ 1], nout, &R.ctr->grab, R.offers,
+                 (unsigned long long*)R.Kc, &L.ctr->entries, nin);
+      } else if (na_ub[r]) {
+        if (direct) {
+          if (vec)
+            LAUNCH(k_offer_first<true>, grid_for(na_ub[r]), kThreads, st, R.nbr, R.dist, k, eps_run, R.row_begin, N,
+                   comp, L.all_core, R.act[cur], na_ub[r], R.act[cur ^ 1], nout, R.Kc, R.Bc, R.tgt,
+                   &L.ctr->entries, nin);
+          else
+            LAUNCH(k_offer_first<false>, grid_for(na_ub[r]), kThreads, st, R.nbr, R.dist, k, eps_run, R.row_begin,
+                   N, comp, L.all_core, R.act[cur], na_ub[r], R.act[cur ^ 1], nout, R.Kc, R.Bc, R.tgt,
+                   &L.ctr->entries, nin);
+        } else {
+          if (vec)
+            LAUNCH(k_offer_round<true>, grid_for(na_ub[r]), kThreads, st, R.nbr, R.dist, k, eps_run, R.row_begin, N,
+                   comp, R.act[cur], na_ub[r], R.act[cur ^ 1], nout, R.offers, (unsigned long long*)R.Kc,
+                   &L.ctr->entries, nin);
+          else
+            LAUNCH(k_offer_round<false>, grid_for(na_ub[r]), kThreads, st, R.nbr, R.dist, k, eps_run, R.row_begin,
+                   N, comp, R.act[cur], na_ub[r], R.act[cur ^ 1], nout, R.offers, (unsigned long long*)R.Kc,
+                   &L.ctr->entries, nin);
+        }
+      }
+      if (general && ni_ub[r])
+        LAUNCH(k_offer_in, grid_for(ni_ub[r]), kThreads, st, R.in_off, R.in_len, R.in_src, R.in_w, comp,
+               R.in_act[cur], ni_ub[r], R.in_act[cur ^ 1], &R.ctr->ni[cur ^ 1], R.offers + R.off_cap_rows,
+               &R.ctr->n_off, (unsigned long long*)R.Kc, &R.ctr->ni[cur]);
+      KDB_CUDA(cudaGetLastError());
+    }
+    // exchange: sim -> min over virtual ranks; nccl -> allreduce
+    for (size_t r = 1; r < nr; ++r)
+      LAUNCH(k_min_into_u64, grid_for(C_ub), kThreads, st, L.Kc, L.ranks[r].Kc, C_ub, Cd);
+    KDB_TRY(allreduce_min_u64(comm, L.Kc, C_ub, st));
+    // a4: ties (the direct round already wrote Bc and the targets)
+    if (!direct) {
+      for (size_t r = 0; r < nr; ++r) {
+        RankState& R = L.ranks[r];
+        if (na_ub[r]) LAUNCH(k_tie, grid_for(na_ub[r]), kThreads, st, R.offers, &R.ctr->na[cur ^ 1], L.Kc, R.Bc);
+        if (general && ni_ub[r])
+          LAUNCH(k_tie, grid_for(ni_ub[r]), kThreads, st, R.offers + R.off_cap_rows, &R.ctr->n_off, L.Kc, R.Bc);
+        KDB_CUDA(cudaGetLastError());
+      }
+    }
+    for (size_t r = 1; r < nr; ++r)
+      LAUNCH(k_min_into_u32, grid_for(C_ub), kThreads, st, L.Bc, L.ranks[r].Bc, C_ub, Cd);
+    KDB_TRY(allreduce_min_u32(comm, L.Bc, C_ub, st));
+    if (direct) {
+      for (size_t r = 1; r < nr; ++r)
+        LAUNCH(k_min_into_u32, grid_for(C_ub), kThreads, st, (uint32_t*)L.tgt, (const uint32_t*)L.ranks[r].tgt, C_ub,
+               Cd);
+      KDB_TRY(allreduce_min_u32(comm, (uint32_t*)L.tgt, C_ub, st));  // non-owners hold INT32_MAX
+    }
+    // a5: hook + emit
+    KDB_CUDA(cudaMemsetAsync(&L.ctr->hooks, 0, 4 * sizeof(uint32_t), st));
+    LAUNCH(k_hook, grid_for(C_ub), kThreads, st, C_ub, L.Kc, L.Bc, direct ? L.tgt : nullptr, kmin_cert, comp,
+           L.parent, L.e_key, L.e_w, N, L.ctr, Cd);
+    KDB_CUDA(cudaGetLastError());
+    // a6: contract (no hooks => identity)
+    KDB_TRY(contract(C_ub));
     cur ^= 1;
+    KDB_TRY(snapshot(rounds));
+    // check the previous round (or this one when every round must be exact)
+    const int check = sync_each ? rounds : rounds - 1;
+    if (check < 1 || check <= last_checked) continue;
+    KDB_CUDA(cudaEventSynchronize(ev_slot[check % kSlots]));
+    last_checked = check;
+    const RoundCounters g = slot_of(check)[0];
+    if (g_trace)
+      fprintf(stderr, "[kdb] round %d eps=%.6g C->%lld offered=%u hooks=%u live=%u\n", check, (double)eps_run,
+              (long long)g.Cs[(check & 1) ? 1 : 0], g.offered, g.hooks, slot_of(check)[1].na[check & 1]);
+    if (g.violation == 2u) return set_err(KDB_EINTERNAL, "pointer jumping did not converge (hook cycle)");
+    if (g.violation) return set_err(KDB_EINVAL, "graph violates the KDB_GRAPH_EXACT promise (a component's "
+                                    "minimum missed an incident edge)");
+    if (g.offered == 0) break;  // a8: no component has a leaving edge
+    // upper bounds for the next launch: the counts after round `check`
+    {
+      // after round `check` the current parity was flipped `rounds - check` more times
+      const int par_after = (par ^ ((rounds - check) & 1));
+      C_ub = g.Cs[par_after];
+      const int cur_after = (cur ^ ((rounds - check) & 1));
+      for (size_t r = 0; r < nr; ++r) {
+        na_ub[r] = slot_of(check)[1 + r].na[cur_after];
+        ni_ub[r] = slot_of(check)[1 + r].ni[cur_after];
+      }
+    }
+    if (g.hooks == 0) {
+      // every offering component abstained (exact-mode certificate).  Drain,
+      // then one edge-centric sweep round gives every component its exact
+      // minimum (both endpoints see every entry) -- on exact counts.
+      ++stalls;
+      KDB_CUDA(cudaStreamSynchronize(st));
+      RoundCounters gg;
+      KDB_CUDA(cudaMemcpy(&gg, L.ctr, sizeof(gg), cudaMemcpyDeviceToHost));
+      if (gg.violation) return set_err(KDB_EINVAL, "graph violates the KDB_GRAPH_EXACT promise (a component's "
+                                       "minimum missed an incident edge)");
+      const int64_t Cx = gg.Cs[par];
+      std::vector<uint32_t> na_x(nr);
+      for (size_t r = 0; r < nr; ++r) {
+        RoundCounters rc;
+        KDB_CUDA(cudaMemcpy(&rc, L.ranks[r].ctr, sizeof(rc), cudaMemcpyDeviceToHost));
+        na_x[r] = rc.na[cur];
+      }
+      LAUNCH(k_fill_comp_arrays, grid_for(Cx), kThreads, st, Cx, L.Kc, L.Bc, nullptr);
+      for (size_t r = 1; r < nr; ++r)
+        LAUNCH(k_fill_comp_arrays, grid_for(Cx), kThreads, st, Cx, L.ranks[r].Kc, L.ranks[r].Bc, nullptr);
+      for (size_t r = 0; r < nr; ++r)
+        if (na_x[r])
+          LAUNCH(k_sweep, grid_for(na_x[r]), kThreads, st, L.ranks[r].nbr, L.ranks[r].dist, k, eps_run,
+                 L.ranks[r].row_begin, N, comp, L.ranks[r].act[cur], na_x[r], (unsigned long long*)L.ranks[r].Kc,
+                 L.ranks[r].Bc, 0);
+      for (size_t r = 1; r < nr; ++r)
+        LAUNCH(k_min_into_u64, grid_for(Cx), kThreads, st, L.Kc, L.ranks[r].Kc, Cx);
+      KDB_TRY(allreduce_min_u64(comm, L.Kc, Cx, st));
+      for (size_t r = 0; r < nr; ++r)
+        if (na_x[r])
+          LAUNCH(k_sweep, grid_for(na_x[r]), kThreads, st, L.ranks[r].nbr, L.ranks[r].dist, k, eps_run,
+                 L.ranks[r].row_begin, N, comp, L.ranks[r].act[cur], na_x[r], (unsigned long long*)L.Kc,
+                 L.ranks[r].Bc, 1);
+      for (size_t r = 1; r < nr; ++r)
+        LAUNCH(k_min_into_u32, grid_for(Cx), kThreads, st, L.Bc, L.ranks[r].Bc, Cx);
+      KDB_TRY(allreduce_min_u32(comm, L.Bc, Cx, st));
+      KDB_CUDA(cudaMemsetAsync(&L.ctr->hooks, 0, 4 * sizeof(uint32_t), st));
+      LAUNCH(k_hook, grid_for(Cx), kThreads, st, Cx, L.Kc, L.Bc, nullptr, nullptr, comp, L.parent, L.e_key, L.e_w, N,
+             L.ctr);
+      KDB_CUDA(cudaGetLastError());
+      KDB_CUDA(cudaMemcpyAsync(&gg, L.ctr, sizeof(gg), cudaMemcpyDeviceToHost, st));
+      KDB_CUDA(cudaStreamSynchronize(st));
+      if (gg.hooks == 0) return set_err(KDB_EINTERNAL, "sweep round made no progress");
+      KDB_TRY(contract(Cx));
+      C_ub = Cx;
+      for (size_t r = 0; r < nr; ++r) na_ub[r] = na_x[r];
+      ++rounds;
+      KDB_TRY(snapshot(rounds));
+      last_checked = rounds;  // the sweep round was exact; the next check is the next round
+    }
+  }
+  KDB_CUDA(cudaStreamSynchronize(st));
+  if (!ev_rnd.empty()) {
     KDB_CUDA(cudaEventRecord(ev[2], st));
-    m.t_min_edges += elapsed(ev[0], ev[1]);
-    m.t_contract += elapsed(ev[1], ev[2]);
+    KDB_CUDA(cudaEventSynchronize(ev[2]));
+    m.t_min_edges += elapsed(ev_rnd.front(), ev[2]);  // rounds are pipelined: one span
+  }
+  {
+    RoundCounters gg;
+    KDB_CUDA(cudaMemcpy(&gg, L.ctr, sizeof(gg), cudaMemcpyDeviceToHost));
+    C = gg.Cs[par];
   }
   RoundCounters hc;
   KDB_CUDA(cudaMemcpyAsync(&hc, L.ctr, sizeof(hc), cudaMemcpyDeviceToHost, st));
