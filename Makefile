@@ -2,7 +2,7 @@
 NVCC      ?= nvcc
 ARCH      := -gencode arch=compute_100a,code=sm_100a
 NCCL_INC  := $(shell python -c "import os,nvidia.nccl as m; print(os.path.join(list(m.__path__)[0],'include'))" 2>/dev/null)
-NVFLAGS   := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -shared -Iinclude -I$(NCCL_INC) --expt-relaxed-constexpr
+NVFLAGS   := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -shared -Iinclude -I$(NCCL_INC) --expt-relaxed-constexpr $(KDB_NVFLAGS)
 
 KDB_SO    := paper_2009_04552_b200/lib/libkdb.so
 KNNG_SO   := datagen/lib/libknng.so

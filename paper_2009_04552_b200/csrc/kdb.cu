@@ -698,7 +698,8 @@ __global__ void __launch_bounds__(256) k_light_ell(const int32_t* __restrict__ n
                                                    int4* __restrict__ LE, Rec* __restrict__ act,
                                                    uint32_t* __restrict__ n_act, uint32_t* __restrict__ grab,
                                                    int direct, int all_core, int64_t N, uint64_t* __restrict__ Kc,
-                                                   uint32_t* __restrict__ Bc, int32_t* __restrict__ tgt) {
+                                                   uint32_t* __restrict__ Bc, int32_t* __restrict__ tgt,
+                                                   int4* __restrict__ rec1) {
   __shared__ __align__(16) Rec s_rec[kChunk];
   __shared__ uint32_t s_n, s_chunk, s_base;
   for (;;) {
@@ -762,10 +763,12 @@ __global__ void __launch_bounds__(256) k_light_ell(const int32_t* __restrict__ n
       }
       // kth = D[v][k-1] >= D[v][kW-1]: only needed (exact-mode certificate) when
       // that is within eps_run
+      uint32_t kb = kInfBits;
       if (kmin) {
         float kth = __int_as_float(0x7f800000);
         if (k <= kW || w[kW - 1] <= eps) kth = __ldcs(dr + (k - 1));
-        kmin[cv] = (kth <= eps) ? mono_bits(kth) : kInfBits;
+        kb = (kth <= eps) ? mono_bits(kth) : kInfBits;
+        kmin[cv] = kb;
       }
       int4* o = LE + i * (kW / 2);
 #pragma unroll
@@ -810,12 +813,15 @@ __global__ void __launch_bounds__(256) k_light_ell(const int32_t* __restrict__ n
         unsigned long long rd = 0;
         r = scan_row<false, true>(nr, dr, k, eps, (int32_t)v, -1, 0, N, comp, all_core, rd);
       }
-      if (r.found) {
+      if (rec1) {  // single rank: one packed record per component for k_hook<true>
+        __stcg(rec1 + cv, make_int4((int)(uint32_t)r.best, (int)(uint32_t)(r.best >> 32), (int)r.bestb, (int)kb));
+        if (r.found) tgt[cv] = r.bestc;
+      } else if (r.found) {
         Kc[cv] = r.best;
         Bc[cv] = r.bestb;
         tgt[cv] = r.bestc;
-        s_rec[atomicAdd(&s_n, 1u)] = Rec{(int32_t)v, r.h};
       }
+      if (r.found) s_rec[atomicAdd(&s_n, 1u)] = Rec{(int32_t)v, r.h};
     }
     __syncthreads();
     if (threadIdx.x == 0) s_base = s_n ? atomicAdd(n_act, s_n) : 0u;
@@ -1128,11 +1134,13 @@ __device__ __forceinline__ bool certified(uint64_t K, const uint32_t* kmin, int6
 // are summed in registers and flushed once per warp at the end.
 constexpr int kHookChunk = 1024;
 
+template <bool PACKED>
 __global__ void __launch_bounds__(256) k_hook(int64_t C, const uint64_t* __restrict__ Kc, const uint32_t* __restrict__ Bc,
                        const int32_t* __restrict__ tgt, const uint32_t* __restrict__ kmin /* null = all certified */,
                        const int32_t* __restrict__ comp, int32_t* __restrict__ parent,
                        uint64_t* __restrict__ e_key, float* __restrict__ e_w, int64_t e_cap,
-                       RoundCounters* __restrict__ ctr, const int64_t* __restrict__ Cp = nullptr) {
+                       RoundCounters* __restrict__ ctr, const int64_t* __restrict__ Cp,
+                       const int4* __restrict__ rec1) {
   if (Cp) C = *Cp;
   __shared__ uint64_t s_key[kHookChunk];
   __shared__ uint32_t s_w[kHookChunk];
@@ -1144,15 +1152,24 @@ __global__ void __launch_bounds__(256) k_hook(int64_t C, const uint64_t* __restr
     for (int t = 0; t < kHookChunk; t += blockDim.x) {
       const int64_t c = chunk * kHookChunk + t + threadIdx.x;
       if (c >= C) continue;
-      const uint64_t K = Kc[c];
+      uint64_t K;
+      uint32_t Bown = 0, kbown = kInfBits;
+      if (PACKED) {  // round 1, single rank: (K, B, kmin) of a component in one 16-B record
+        const int4 q = __ldcs(rec1 + c);
+        K = (uint64_t)(uint32_t)q.x | ((uint64_t)(uint32_t)q.y << 32);
+        Bown = (uint32_t)q.z;
+        kbown = (uint32_t)q.w;
+      } else {
+        K = Kc[c];
+      }
       int32_t p = (int32_t)c;
       if (K != kSent) {
         ++n_off;
-        if (!certified(K, kmin, c)) {
+        if (PACKED ? !((uint32_t)(K >> 32) < kbown) : !certified(K, kmin, c)) {
           ++n_unc;
         } else {
           const uint32_t a = (uint32_t)K;
-          const uint32_t b = Bc[c];
+          const uint32_t b = PACKED ? Bown : Bc[c];
           int32_t t2;
           if (tgt) {
             t2 = tgt[c];
@@ -1161,7 +1178,14 @@ __global__ void __launch_bounds__(256) k_hook(int64_t C, const uint64_t* __restr
             t2 = gat(comp + x);
           }
           bool mutual, cert_t = true;
-          if (kmin) {  // exact mode: t may abstain; also audit the promise
+          if (PACKED) {  // one random 16-B read of the target's record
+            const int4 q = __ldcg(rec1 + t2);
+            const uint64_t Kt = (uint64_t)(uint32_t)q.x | ((uint64_t)(uint32_t)q.y << 32);
+            const uint32_t Bt = (uint32_t)q.z;
+            cert_t = Kt != kSent && (uint32_t)(Kt >> 32) < (uint32_t)q.w;
+            if (cert_t && (Kt > K || (Kt == K && Bt > b))) ctr->violation = 1u;
+            mutual = cert_t && Kt == K && Bt == b;
+          } else if (kmin) {  // exact mode: t may abstain; also audit the promise
             const uint64_t Kt = gat(Kc + t2);
             cert_t = Kt != kSent && certified(Kt, kmin, t2);
             // t's true minimum is <= the edge c selected (that edge is incident
@@ -1842,6 +1866,7 @@ struct Layout {
   uint64_t* e_key;
   float* e_w;
   unsigned long long* buckets;
+  int4* rec1;       // round 1, single rank, exact mode: packed (K, B, kmin) per component
   int32_t* hcomp;   // heavy phase: light component -> heavy component
   int32_t* dom;     // filter fast path: dominant component per id block
   uint32_t* bloom;  // filter fast path: Bloom filter of the exceptions
@@ -1889,6 +1914,7 @@ size_t carve(Layout& L, char* base, bool dry, int64_t N, int nr, const int64_t* 
   L.e_key = cv.take<uint64_t>(N + 1);
   L.e_w = cv.take<float>(N + 1);
   L.buckets = cv.take<unsigned long long>(256);
+  L.rec1 = general ? nullptr : cv.take<int4>(N + 1);
   L.hcomp = cv.take<int32_t>(N + 1);
   L.dom = cv.take<int32_t>(kDomMax);
   L.bloom = cv.take<uint32_t>(kBloomBits / 32);
@@ -2086,8 +2112,11 @@ kdb_status rows_phase(Mst& m, float eps_run) {
     LAUNCH(k_fill_comp_arrays, grid_for(C), kThreads, st, C, L.ranks[r].Kc, L.ranks[r].Bc, nullptr);
   KDB_CUDA(cudaGetLastError());
   const bool use_compact = env_int("KDB_COMPACT", 1) != 0;
-  // exact mode: round 1 (singleton components) is fused into the ELL pass
+  // exact mode: round 1 (singleton components) is fused into the ELL pass; a
+  // single rank also packs (K, B, kmin) per component for the round-1 hook
   const bool fuse1 = !general && use_compact && env_int("KDB_FUSE1", 1) != 0;
+  const bool packed1 = fuse1 && L.ranks.size() == 1 && !(comm && comm->kind == 1 && comm->nranks > 1) &&
+                       env_int("KDB_PACK1", 1) != 0;
   if (!general)  // hook targets of round 1 (written by the round-1 offers)
     for (auto& R : L.ranks) LAUNCH(k_fill_i32, grid_for(C), kThreads, st, R.tgt, C, INT32_MAX);
   for (auto& R : L.ranks) {
@@ -2101,7 +2130,7 @@ kdb_status rows_phase(Mst& m, float eps_run) {
 #define KDB_ELL_LAUNCH(V, A)                                                                                    \
   LAUNCH((k_light_ell<V, A>), grid_for(R.n_rows), kThreads, st, R.nbr, R.dist, R.n_rows, k, eps_run, R.row_begin, \
          comp, general ? nullptr : L.kmin, R.LE, R.act[0], &R.ctr->na[0], &R.ctr->grab, fuse1 ? 1 : 0,         \
-         L.all_core, N, R.Kc, R.Bc, R.tgt)
+         L.all_core, N, R.Kc, R.Bc, R.tgt, packed1 ? L.rec1 : nullptr)
       if (a32) KDB_ELL_LAUNCH(true, true);
       else if (vec) KDB_ELL_LAUNCH(true, false);
       else KDB_ELL_LAUNCH(false, false);
@@ -2316,8 +2345,12 @@ kdb_status rows_phase(Mst& m, float eps_run) {
     }
     // a5: hook + emit
     KDB_CUDA(cudaMemsetAsync(&L.ctr->hooks, 0, 4 * sizeof(uint32_t), st));
-    LAUNCH(k_hook, grid_for(C_ub), kThreads, st, C_ub, L.Kc, L.Bc, direct ? L.tgt : nullptr, kmin_cert, comp,
-           L.parent, L.e_key, L.e_w, N, L.ctr, Cd);
+    if (direct && packed1)
+      LAUNCH(k_hook<true>, grid_for(C_ub), kThreads, st, C_ub, L.Kc, L.Bc, L.tgt, kmin_cert, comp, L.parent, L.e_key,
+             L.e_w, N, L.ctr, Cd, L.rec1);
+    else
+      LAUNCH(k_hook<false>, grid_for(C_ub), kThreads, st, C_ub, L.Kc, L.Bc, direct ? L.tgt : nullptr, kmin_cert,
+             comp, L.parent, L.e_key, L.e_w, N, L.ctr, Cd, (const int4*)nullptr);
     KDB_CUDA(cudaGetLastError());
     // a6: contract (no hooks => identity)
     KDB_TRY(contract(C_ub));
@@ -2384,8 +2417,8 @@ kdb_status rows_phase(Mst& m, float eps_run) {
         LAUNCH(k_min_into_u32, grid_for(Cx), kThreads, st, L.Bc, L.ranks[r].Bc, Cx);
       KDB_TRY(allreduce_min_u32(comm, L.Bc, Cx, st));
       KDB_CUDA(cudaMemsetAsync(&L.ctr->hooks, 0, 4 * sizeof(uint32_t), st));
-      LAUNCH(k_hook, grid_for(Cx), kThreads, st, Cx, L.Kc, L.Bc, nullptr, nullptr, comp, L.parent, L.e_key, L.e_w, N,
-             L.ctr);
+      LAUNCH(k_hook<false>, grid_for(Cx), kThreads, st, Cx, L.Kc, L.Bc, nullptr, nullptr, comp, L.parent, L.e_key,
+             L.e_w, N, L.ctr, (const int64_t*)nullptr, (const int4*)nullptr);
       KDB_CUDA(cudaGetLastError());
       KDB_CUDA(cudaMemcpyAsync(&gg, L.ctr, sizeof(gg), cudaMemcpyDeviceToHost, st));
       KDB_CUDA(cudaStreamSynchronize(st));

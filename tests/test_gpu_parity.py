@@ -357,13 +357,16 @@ def test_wide_rows_exact(k):
         assert_parity(run_gpu(nbr, dist, M, eps, exact=False), exp)
 
 
-@pytest.mark.parametrize("fuse", ["0", "1"])
+@pytest.mark.parametrize("fuse,pack", [("0", "0"), ("1", "0"), ("1", "1")])
 @pytest.mark.parametrize("P", [0, 3])
-def test_round1_fused_into_ell(c1_graph, fuse, P, monkeypatch):
+def test_round1_fused_into_ell(c1_graph, fuse, pack, P, monkeypatch):
     """Exact mode: round 1 (singleton components) computed inside the light-ELL
-    pass (KDB_FUSE1=1, default) or by its own kernel (0) -- same forest."""
+    pass (KDB_FUSE1=1, default) or by its own kernel (0); on a single rank the
+    round-1 hook reads one packed (K, B, kmin) record per component
+    (KDB_PACK1=1, default) -- same forest."""
     import paper_2009_04552_b200 as kdb
     monkeypatch.setenv("KDB_FUSE1", fuse)
+    monkeypatch.setenv("KDB_PACK1", pack)
     X, nbr, dist = c1_graph
     for M, f in ((8, 1.5), (3, 0.7), (12, 3.0)):
         eps = eps_from_graph(dist, M, f)
