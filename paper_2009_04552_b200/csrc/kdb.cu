@@ -1204,8 +1204,8 @@ __global__ void __launch_bounds__(256) k_hook(int64_t C, const uint64_t* __restr
             p = t2;
             ++n_hook;
             const uint32_t j = atomicAdd(&s_n, 1u);
-            s_key[j] = ((uint64_t)a << 32) | b;
-            s_w[j] = (uint32_t)(K >> 32);
+            s_key[j] = ((uint64_t)b << 32) | (uint32_t)(K >> 32);  // (b, w bits): the sort payload
+            s_w[j] = a;                                               // a: the sort key
           }
         }
       }
@@ -1217,7 +1217,7 @@ __global__ void __launch_bounds__(256) k_hook(int64_t C, const uint64_t* __restr
     for (uint32_t j = threadIdx.x; j < s_n; j += blockDim.x) {
       if ((int64_t)(s_base + j) < e_cap) {
         e_key[s_base + j] = s_key[j];
-        e_w[s_base + j] = __uint_as_float(s_w[j]);
+        reinterpret_cast<uint32_t*>(e_w)[s_base + j] = s_w[j];
       }
     }
   }
@@ -1345,19 +1345,12 @@ __global__ void k_relabel(int64_t N, int32_t* __restrict__ comp, const int32_t* 
 // MSF output in (a, b) order: radix sort on the 32-bit a (only ceil(log2 N)
 // bits) carrying (b, w) as a 64-bit payload, then each run of equal a (tiny:
 // a vertex is the smaller endpoint of few MSF edges) is sorted by b in place.
-__global__ void k_msf_pack(int64_t m, const uint64_t* __restrict__ keys, const float* __restrict__ w,
-                           uint32_t* __restrict__ ka, unsigned long long* __restrict__ vb) {
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x) {
-    const uint64_t x = keys[e];
-    ka[e] = (uint32_t)(x >> 32);
-    vb[e] = (x << 32) | __float_as_uint(w[e]);
-  }
-}
+// ka = the sorted a (the caller's mst_a); splits the (b, w) payload into mst_b /
+// mst_w and sorts every run of equal a by b
 __global__ void k_msf_unpack(int64_t m, const uint32_t* __restrict__ ka, const unsigned long long* __restrict__ vb,
-                             uint32_t* __restrict__ a, uint32_t* __restrict__ b, float* __restrict__ w) {
+                             uint32_t* __restrict__ b, float* __restrict__ w) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t ai = ka[i];
-    a[i] = ai;
     if (i > 0 && ka[i - 1] == ai) continue;  // not the start of a run
     int64_t j = i + 1;
     while (j < m && ka[j] == ai) ++j;
@@ -1752,8 +1745,8 @@ __global__ void k_hook_h(int64_t C, const uint64_t* __restrict__ Kc, const uint3
     block_count(&ctr->hooks, emit);
     const uint32_t slot = block_reserve(&ctr->msf_count, emit);
     if (emit && (int64_t)slot < e_cap) {
-      e_key[slot] = ((uint64_t)a << 32) | b;
-      e_w[slot] = __uint_as_float(wb);
+      e_key[slot] = ((uint64_t)b << 32) | wb;
+      reinterpret_cast<uint32_t*>(e_w)[slot] = a;
     }
   }
 }
@@ -2839,18 +2832,17 @@ kdb_status kdb_mst(const kdb_graph* g, float eps, const uint32_t* core_bits, int
   unsigned long long bk[256];
   if (ne > 0) {
     size_t cb = L.cub_bytes;
-    uint32_t* ka = reinterpret_cast<uint32_t*>(L.parent);  // N + 1 each, free now
-    uint32_t* ka2 = reinterpret_cast<uint32_t*>(L.rootof);
-    unsigned long long* vb = reinterpret_cast<unsigned long long*>(L.Kc);
-    unsigned long long* vb2 = reinterpret_cast<unsigned long long*>(L.e_key);
-    LAUNCH(k_msf_pack, grid_for(ne), kThreads, st, ne, L.e_key, L.e_w, ka, vb);
+    unsigned long long* vb2 = reinterpret_cast<unsigned long long*>(L.Kc);  // N + 1, free now
     int abits = 1;
     while (abits < 32 && ((int64_t)1 << abits) < N) ++abits;
     {
+      // the emitted (a, (b, w)) pairs sort straight into the caller's mst_a
       LaunchScope ls_("cub::DeviceRadixSort", st, false);
-      KDB_CUDA(cub::DeviceRadixSort::SortPairs(L.cub_tmp, cb, ka, ka2, vb, vb2, (int)ne, 0, abits, st));
+      KDB_CUDA(cub::DeviceRadixSort::SortPairs(L.cub_tmp, cb, reinterpret_cast<const uint32_t*>(L.e_w), mst_a,
+                                               reinterpret_cast<const unsigned long long*>(L.e_key), vb2, (int)ne, 0,
+                                               abits, st));
     }
-    LAUNCH(k_msf_unpack, grid_for(ne), kThreads, st, ne, ka2, vb2, mst_a, mst_b, mst_w);
+    LAUNCH(k_msf_unpack, grid_for(ne), kThreads, st, ne, mst_a, vb2, mst_b, mst_w);
     KDB_CUDA(cudaMemsetAsync(L.buckets, 0, 256 * sizeof(unsigned long long), st));
     LAUNCH(k_wbuckets, grid_for(ne), kThreads, st, ne, mst_w, L.buckets);
     KDB_CUDA(cudaGetLastError());
