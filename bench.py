@@ -227,7 +227,8 @@ def run_ours(args):
 
     W = make_workload(args.config, args.scale, args.seed, dev)
     N, k, M, eps = W["N"], W["k"], W["M"], W["eps"]
-    rb, re_ = N * rank // world, N * (rank + 1) // world
+    from paper_2009_04552_b200.dist import max_over_ranks, rank_rows
+    rb, re_ = rank_rows(N, rank, world)
     if world > 1:  # keep this rank's rows only
         W["nbr"] = W["nbr"][rb:re_].clone()
         W["dist"] = W["dist"][rb:re_].clone()
@@ -273,10 +274,7 @@ def run_ours(args):
         barrier()
         kdb.profile(False)
         ms_ = e0.elapsed_time(e1) / args.steps
-        t_ = torch.tensor([ms_], dtype=torch.float64, device=dev)
-        if world > 1:
-            tdist.all_reduce(t_, op=tdist.ReduceOp.MAX)
-        return float(t_.item()), st_, out
+        return max_over_ranks(ms_, dev), st_, out
 
     clocks = ClockSampler(local)
     kdb.profile_reset()

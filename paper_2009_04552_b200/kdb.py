@@ -103,13 +103,16 @@ class Comm:
 
     @classmethod
     def nccl(cls, rank: int, nranks: int, group=None) -> "Comm":
-        import torch.distributed as dist
+        from .dist import share_nccl_id
+
+        def make_id():
+            b = (C.c_ubyte * 128)()
+            _check(lib().kdb_nccl_unique_id(C.cast(b, C.c_void_p)), "kdb_nccl_unique_id")
+            return bytes(b)
+
+        uid = share_nccl_id(rank, make_id, group)
         buf = (C.c_ubyte * 128)()
-        if rank == 0:
-            _check(lib().kdb_nccl_unique_id(C.cast(buf, C.c_void_p)), "kdb_nccl_unique_id")
-        obj = [bytes(buf)]
-        dist.broadcast_object_list(obj, src=0, group=group)
-        C.memmove(buf, obj[0], 128)
+        C.memmove(buf, uid, 128)
         h = C.c_void_p()
         _check(lib().kdb_comm_create_nccl(C.byref(h), C.cast(buf, C.c_void_p), int(rank), int(nranks)),
                "kdb_comm_create_nccl")
