@@ -38,13 +38,13 @@ def _load():
         P = C.c_void_p
         i64, i32, f32 = C.c_int64, C.c_int32, C.c_float
         lib.oracle_core_mark.argtypes = [i64, i32, P, i32, f32, P]
-        lib.oracle_candidate_count.argtypes = [i64, i32, P, P, P, f32]
+        lib.oracle_candidate_count.argtypes = [i64, i32, P, P, P, f32, i32]
         lib.oracle_candidate_count.restype = i64
-        lib.oracle_candidates.argtypes = [i64, i32, P, P, P, f32, P, P, P, i64]
+        lib.oracle_candidates.argtypes = [i64, i32, P, P, P, f32, i32, P, P, P, i64]
         lib.oracle_candidates.restype = i64
         lib.oracle_kruskal.argtypes = [i64, i64, P, P, P, P, P, P, P, P, i64, P, P]
         lib.oracle_border.argtypes = [i64, i32, P, P, P, f32, P, P]
-        lib.oracle_kdbscan.argtypes = [i64, i32, P, P, i32, f32, P, P, P, P, P, i64, P, P, P]
+        lib.oracle_kdbscan.argtypes = [i64, i32, P, P, i32, f32, i32, P, P, P, P, P, i64, P, P, P]
         _lib = lib
     return _lib
 
@@ -70,15 +70,24 @@ def core_mark(dist, M: int, eps) -> np.ndarray:
     return core
 
 
-def candidates(nbr, dist, core, eps):
-    """Candidate multiset (a, b, w) in row order."""
+def _cols(edge_cols, k):
+    c = k if edge_cols is None else int(edge_cols)
+    if not 1 <= c <= k:
+        raise ValueError(f"edge_cols must be in [1, k={k}]")
+    return c
+
+
+def candidates(nbr, dist, core, eps, edge_cols=None):
+    """Candidate multiset (a, b, w) in row order, from
+    the first `edge_cols` columns (default all k; edge_cols = M is Def. 6)."""
     nbr, dist = _graph(nbr, dist)
     core = np.ascontiguousarray(core, np.uint8)
     n, k = nbr.shape
+    kc = _cols(edge_cols, k)
     lib = _load()
-    m = lib.oracle_candidate_count(n, k, _p(nbr), _p(dist), _p(core), np.float32(eps))
+    m = lib.oracle_candidate_count(n, k, _p(nbr), _p(dist), _p(core), np.float32(eps), kc)
     a = np.empty(m, np.uint32); b = np.empty(m, np.uint32); w = np.empty(m, np.float32)
-    lib.oracle_candidates(n, k, _p(nbr), _p(dist), _p(core), np.float32(eps), _p(a), _p(b), _p(w), m)
+    lib.oracle_candidates(n, k, _p(nbr), _p(dist), _p(core), np.float32(eps), kc, _p(a), _p(b), _p(w), m)
     return a, b, w
 
 
@@ -109,8 +118,12 @@ def border(nbr, dist, core, eps, comp):
     return labels
 
 
-def kdbscan(nbr, dist, M: int, eps):
+def kdbscan(nbr, dist, M: int, eps, edge_cols=None):
     """The whole clustering stage (Alg. 1 as its plain definition).
+
+    edge_cols: candidate edges come from the first edge_cols columns of each
+    row (default k = reading #3; edge_cols = M is the paper's direct
+    M-reachability, Def. 6 PAPER.md:958-962 / Thm. 2(ii)).
 
     Returns dict(core uint8[n], labels int32[n], msf_a/msf_b uint32[c] sorted by
     (a, b), msf_w float32[c], msf_weight float (fp64 sum in key order),
@@ -118,13 +131,14 @@ def kdbscan(nbr, dist, M: int, eps):
     """
     nbr, dist = _graph(nbr, dist)
     n, k = nbr.shape
+    kc = _cols(edge_cols, k)
     core = np.empty(n, np.uint8)
     labels = np.empty(n, np.int32)
     cap = max(n - 1, 0)
     ma = np.empty(cap, np.uint32); mb = np.empty(cap, np.uint32); mw = np.empty(cap, np.float32)
     cnt = C.c_int64(0); tot = C.c_double(0.0)
     times = np.zeros(3, np.float64)
-    rc = _load().oracle_kdbscan(n, k, _p(nbr), _p(dist), int(M), np.float32(eps), _p(core),
+    rc = _load().oracle_kdbscan(n, k, _p(nbr), _p(dist), int(M), np.float32(eps), kc, _p(core),
                                 _p(labels), _p(ma), _p(mb), _p(mw), cap, C.byref(cnt),
                                 C.byref(tot), _p(times))
     if rc == -1:

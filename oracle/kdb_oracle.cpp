@@ -27,6 +27,13 @@
 //                                               -- Lemma 1(ii),
 //                                                  SPEC.md:344, reading #13
 //
+// edge_cols: candidate entries are taken from the first
+// edge_cols columns of each row only.  edge_cols = k is the all-k reading #3
+// (north_star); edge_cols = M is the paper's own kNN-DBSCAN edge set -- direct
+// M-reachability, Def. 6: q in N_M(p) or p in N_M(q), and
+// Alg. 2's scan bound L[i] <= M; Thm. 2(ii):
+// the MST clusters of G_M,core are the kNN-DBSCAN clusters.
+//
 // Pins (tests/test_oracle_pins.py): worked examples W1-W3 from the paper's
 // Fig. cycle / Fig. cut_mst (tests/golden/), brute-force classic DBSCAN at
 // k = N-1 (Thm. 2(i)), Prim's MSF weight multiset, brute-force MSF enumeration,
@@ -105,13 +112,14 @@ int oracle_core_mark(int64_t n, int32_t k, const float* dist, int32_t M, float e
   return 0;
 }
 
-// Step 2. Number of candidate entries (directed copies counted separately).
+// Step 2. Number of candidate entries (directed copies counted separately) in
+// the first edge_cols columns.
 int64_t oracle_candidate_count(int64_t n, int32_t k, const int32_t* nbr, const float* dist,
-                               const uint8_t* core, float eps) {
+                               const uint8_t* core, float eps, int32_t edge_cols) {
   int64_t m = 0;
   for (int64_t i = 0; i < n; ++i) {
     if (!core[i]) continue;
-    for (int32_t c = 0; c < k; ++c) {
+    for (int32_t c = 0; c < edge_cols; ++c) {
       int64_t J = nbr[i * (int64_t)k + c];
       float w = dist[i * (int64_t)k + c];
       if (J >= 0 && J < n && J != i && core[J] && w <= eps) ++m;
@@ -122,12 +130,12 @@ int64_t oracle_candidate_count(int64_t n, int32_t k, const int32_t* nbr, const f
 
 // Step 2 (materialised): the candidate multiset in row order as (a, b, w).
 int64_t oracle_candidates(int64_t n, int32_t k, const int32_t* nbr, const float* dist,
-                          const uint8_t* core, float eps, uint32_t* ea, uint32_t* eb,
+                          const uint8_t* core, float eps, int32_t edge_cols, uint32_t* ea, uint32_t* eb,
                           float* ew, int64_t cap) {
   int64_t m = 0;
   for (int64_t i = 0; i < n; ++i) {
     if (!core[i]) continue;
-    for (int32_t c = 0; c < k; ++c) {
+    for (int32_t c = 0; c < edge_cols; ++c) {
       int64_t J = nbr[i * (int64_t)k + c];
       float w = dist[i * (int64_t)k + c];
       if (J >= 0 && J < n && J != i && core[J] && w <= eps) {
@@ -206,17 +214,17 @@ int oracle_border(int64_t n, int32_t k, const int32_t* nbr, const float* dist,
 // times[0..2] = seconds spent in core / candidates+Kruskal / border.
 // Returns 0; -1 bad args; -2 msf_cap too small.
 int oracle_kdbscan(int64_t n, int32_t k, const int32_t* nbr, const float* dist, int32_t M,
-                   float eps, uint8_t* core, int32_t* labels, uint32_t* msf_a, uint32_t* msf_b,
-                   float* msf_w, int64_t msf_cap, int64_t* msf_count, double* msf_weight,
-                   double* times) {
-  if (n < 0 || k < 1 || M < 1 || M > k || !(eps > 0.0f)) return -1;
+                   float eps, int32_t edge_cols, uint8_t* core, int32_t* labels, uint32_t* msf_a,
+                   uint32_t* msf_b, float* msf_w, int64_t msf_cap, int64_t* msf_count,
+                   double* msf_weight, double* times) {
+  if (n < 0 || k < 1 || M < 1 || M > k || !(eps > 0.0f) || edge_cols < 1 || edge_cols > k) return -1;
   double t0 = now_s();
   oracle_core_mark(n, k, dist, M, eps, core);
   double t1 = now_s();
-  int64_t m = oracle_candidate_count(n, k, nbr, dist, core, eps);
+  int64_t m = oracle_candidate_count(n, k, nbr, dist, core, eps, edge_cols);
   std::vector<uint32_t> ea((size_t)m), eb((size_t)m);
   std::vector<float> ew((size_t)m);
-  oracle_candidates(n, k, nbr, dist, core, eps, ea.data(), eb.data(), ew.data(), m);
+  oracle_candidates(n, k, nbr, dist, core, eps, edge_cols, ea.data(), eb.data(), ew.data(), m);
   std::vector<int32_t> comp((size_t)n);
   int rc = oracle_kruskal(n, m, ea.data(), eb.data(), ew.data(), core, comp.data(), msf_a, msf_b,
                           msf_w, msf_cap, msf_count, msf_weight);

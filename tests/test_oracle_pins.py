@@ -382,3 +382,82 @@ def test_oracle_rejects_bad_arguments():
         oracle.kdbscan(nbr, dist, 3, 1.0)      # M > k
     with pytest.raises(ValueError):
         oracle.kdbscan(nbr, dist, 1, 0.0)      # eps not > 0
+
+
+# ---------------- edge_cols = M: direct M-reachability (Def. 6-9, Thm. 2(ii)) --
+def _m_reach_bruteforce(X, M, eps):
+    """kNN-DBSCAN clusters of core points straight from Def. 6-9 (PAPER.md:958-
+    975) and Lemma 1(i): N_M(p) = the M nearest OTHER points by fp64 distance
+    (reading #1), p -M-> q iff p core and (q in N_M(p) or p in N_M(q)); clusters
+    = classes of M-reachability over core points (Lemma 3), labelled by their
+    minimum id.  Returns (core, N_M sets, label dict)."""
+    D = points_dist64(X)
+    n = len(X)
+    order = np.argsort(D + np.diag(np.full(n, np.inf)), axis=1, kind="stable")
+    NM = [set(order[p, :M].tolist()) for p in range(n)]
+    F = D.astype(np.float32)
+    core = np.array([max(F[p, q] for q in NM[p]) <= np.float32(eps) for p in range(n)])
+    edges = []
+    for p in range(n):
+        for q in range(n):
+            if p < q and core[p] and core[q] and (q in NM[p] or p in NM[q]):
+                edges.append(((0, p, q), None))
+    lab = bfs_components(n, edges, [v for v in range(n) if core[v]])
+    return core, NM, lab
+
+
+@pytest.mark.parametrize("seed,k,M,q", [(0, 12, 3, 0.5), (1, 12, 5, 0.6), (2, 16, 4, 0.7),
+                                         (3, 10, 2, 0.8), (4, 20, 6, 0.5), (5, 8, 8, 0.9)])
+def test_edge_cols_M_equals_def6_reachability(seed, k, M, q):
+    X = clumpy_points(300 + seed, 160, dup_frac=0.0)
+    nbr, dist = knn_bruteforce(X, k)
+    eps = np.float32(np.quantile(dist[:, M - 1].astype(np.float64), q))
+    core_bf, NM, lab = _m_reach_bruteforce(X, M, eps)
+    # the graph's first M columns are N_M (continuous points: no distance ties)
+    assert all(set(nbr[p, :M].tolist()) == NM[p] for p in range(len(X)))
+    r = oracle.kdbscan(nbr, dist, M, eps, edge_cols=M)
+    assert np.array_equal(r["core"].astype(bool), core_bf)
+    for v, c in lab.items():
+        assert r["labels"][v] == c
+    # the MSF is Prim's forest of the candidate edges of columns < M
+    core = core_bf
+    E = candidate_edges(nbr[:, :M].copy(), dist[:, :M].copy(), core, eps)
+    got = sorted((mono(w), a, b) for a, b, w in zip(r["msf_a"], r["msf_b"], r["msf_w"]))
+    assert got == sorted(prim_msf([v for v in range(len(X)) if core[v]], E))
+    # border rule unchanged (Lemma 1(ii) only looks inside N_M(p)): a non-core
+    # point takes the label of the first core entry of its row within eps
+    for i in np.nonzero(~core)[0]:
+        js = [int(nbr[i, c]) for c in range(k) if dist[i, c] <= eps and core[nbr[i, c]]]
+        assert r["labels"][i] == (lab[js[0]] if js else -1)
+
+
+def test_edge_cols_refines_all_k_and_default_is_k():
+    """Fewer candidate edges => every edge_cols=M cluster lies inside one
+    all-k cluster (the argument of Thm. 1 applied to edge subsets); edge_cols=k
+    is the default exactly; and the restriction is not vacuous on this input."""
+    finer_somewhere = False
+    for seed in range(6):
+        X = clumpy_points(400 + seed, 200, dup_frac=0.05)
+        k, M = 16, 3
+        nbr, dist = knn_bruteforce(X, k)
+        eps = np.float32(np.quantile(dist[:, k - 1].astype(np.float64), 0.7))
+        rk = oracle.kdbscan(nbr, dist, M, eps)
+        rk2 = oracle.kdbscan(nbr, dist, M, eps, edge_cols=k)
+        for f in ("core", "labels", "msf_a", "msf_b", "msf_w"):
+            assert np.array_equal(rk[f], rk2[f])
+        assert rk["msf_weight"] == rk2["msf_weight"]
+        rm = oracle.kdbscan(nbr, dist, M, eps, edge_cols=M)
+        cores = np.nonzero(rk["core"])[0]
+        for c in set(rm["labels"][cores].tolist()):
+            assert len(set(rk["labels"][cores[rm["labels"][cores] == c]].tolist())) == 1
+        nm, nk = len(set(rm["labels"][cores].tolist())), len(set(rk["labels"][cores].tolist()))
+        assert nm >= nk
+        finer_somewhere |= nm > nk
+    assert finer_somewhere
+
+
+def test_edge_cols_bad_arguments():
+    nbr = np.zeros((3, 2), np.int32); dist = np.zeros((3, 2), np.float32)
+    for bad in (0, 3):
+        with pytest.raises(ValueError):
+            oracle.kdbscan(nbr, dist, 1, 1.0, edge_cols=bad)
