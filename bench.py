@@ -48,6 +48,12 @@ def parse():
     ap.add_argument("--general", action="store_true", help="do not promise an exact graph")
     ap.add_argument("--cpu-sample-rows", type=int, default=1_500_000)
     ap.add_argument("--out", default=None, help="also append the JSON line to this file")
+    ap.add_argument("--edge-cols", default=None,
+                    help="candidate edges from the first EDGE_COLS columns ('M' = Def. 6's edge set, "
+                         "SURVEY.md 8(f) NEXT 1); default all k (north_star)")
+    ap.add_argument("--eps-factors", default=None,
+                    help="comma list: one step = the whole stage at every eps = f x median D[:, M-1] on "
+                         "the same resident graph (Fig. eps_mnist protocol, PAPER.md:459-488)")
     return ap.parse_args()
 
 
@@ -142,7 +148,34 @@ def make_workload(cfg_name: str, scale: float, seed: int, device):
     med = median_like_numpy(dist[:, cfg["M"] - 1])
     eps = float(np.float32(cfg["eps_factor"] * med))
     return dict(X=X, truth=truth, nbr=nbr, dist=dist, eps=eps, M=cfg["M"], k=cfg["k"], N=len(X),
-                d=X.shape[1], gen_s=t1 - t0, graph_build_s=t2 - t1, knng=info)
+                d=X.shape[1], gen_s=t1 - t0, graph_build_s=t2 - t1, knng=info, med=med)
+
+
+def stage_params(args, W):
+    """(edge_cols, [eps ...]) of one step: edge_cols 0 = all k; the eps list is
+    the config's eps unless --eps-factors asks for a sweep."""
+    ec = 0
+    if args.edge_cols:
+        ec = W["M"] if args.edge_cols == "M" else int(args.edge_cols)
+        if not 1 <= ec <= W["k"]:
+            raise SystemExit(f"--edge-cols must be in [1, k={W['k']}] or 'M'")
+        ec = 0 if ec == W["k"] else ec
+    if args.eps_factors:
+        eps_list = [float(np.float32(float(f) * W["med"])) for f in args.eps_factors.split(",")]
+    else:
+        eps_list = [W["eps"]]
+    return ec, eps_list
+
+
+def stage_desc(ec, eps_list, W):
+    d = {}
+    if ec:
+        d["edge_cols"] = ec
+        d["edge_set"] = "first edge_cols columns (Def. 6 direct M-reachability when = M)"
+    if len(eps_list) > 1:
+        d["eps_sweep"] = eps_list
+        d["unit_note"] = "value = N*k*len(eps_sweep) / step time: one step clusters the graph at every eps"
+    return d
 
 
 def workload_desc(cfg_name, W, scale):
@@ -159,12 +192,14 @@ def workload_desc(cfg_name, W, scale):
             "graph_build_s": round(W["graph_build_s"], 2)}
 
 
-def oracle_sample(nbr_rows: np.ndarray, dist_rows: np.ndarray, M: int, eps: float):
-    """Time the CPU oracle (as it stands) on rows [0, n_s) of the workload; entries
-    pointing at ids >= n_s fall outside the sample and are skipped by the oracle."""
+def oracle_sample(nbr_rows: np.ndarray, dist_rows: np.ndarray, M: int, eps_list, edge_cols=0):
+    """Time the CPU oracle (as it stands) on rows [0, n_s) of the workload at every
+    eps of the step; entries pointing at ids >= n_s fall outside the sample and
+    are skipped by the oracle."""
     import oracle
     t = time.perf_counter()
-    r = oracle.kdbscan(nbr_rows, dist_rows, M, np.float32(eps))
+    for eps in eps_list:
+        r = oracle.kdbscan(nbr_rows, dist_rows, M, np.float32(eps), edge_cols=edge_cols or None)
     dt = time.perf_counter() - t
     return dt, r
 
@@ -177,23 +212,24 @@ def run_reference(args):
         return  # rank 0 alone runs the oracle arm
     torch.cuda.set_device(local)
     W = make_workload(args.config, args.scale, args.seed, f"cuda:{local}")
+    ec, eps_list = stage_params(args, W)
     ns = min(args.cpu_sample_rows, W["N"])
     nbr = W["nbr"][:ns].cpu().numpy()
     dist = W["dist"][:ns].cpu().numpy()
     del W["nbr"], W["dist"]
     times = []
     for it in range(args.warmup + args.steps):
-        dt, _ = oracle_sample(nbr, dist, W["M"], W["eps"])
+        dt, _ = oracle_sample(nbr, dist, W["M"], eps_list, ec)
         if it >= args.warmup:
             times.append(dt)
     t = float(np.mean(times))
-    value = ns * W["k"] / t
+    value = ns * W["k"] * len(eps_list) / t
     sample = (f"rows [0, {ns}) of {args.config} (cluster-major ids; entries to ids >= {ns} skipped), "
               f"{ns * W['k']} entries per step")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": workload_desc(args.config, W, args.scale),
+            "config": dict(workload_desc(args.config, W, args.scale), **stage_desc(ec, eps_list, W)),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     emit(line, args)
@@ -234,7 +270,9 @@ def run_ours(args):
         W["dist"] = W["dist"][rb:re_].clone()
         torch.cuda.empty_cache()
     comm = kdb.Comm.nccl(rank, world) if world > 1 else None
-    g = kdb.Graph(W["nbr"], W["dist"], n_total=N, row_begin=rb, exact=not args.general)
+    ec, eps_list = stage_params(args, W)
+    kc = ec or k
+    g = kdb.Graph(W["nbr"], W["dist"], n_total=N, row_begin=rb, exact=not args.general, edge_cols=ec)
     ws = torch.empty(kdb.workspace_bytes(g, comm), dtype=torch.uint8, device=dev)
     outs = {"comp": torch.empty(N, dtype=torch.int32, device=dev),
             "a": torch.empty(max(N - 1, 1), dtype=torch.int32, device=dev),
@@ -244,9 +282,10 @@ def run_ours(args):
     stream = torch.cuda.current_stream()
 
     def step(graph):
-        bits = kdb.core_mark(graph, M, eps, comm)
-        r = kdb.mst(graph, eps, bits, comm, workspace=ws, out=outs)
-        lb = kdb.label(graph, eps, bits, r.comp, out=lab)
+        for e in eps_list:
+            bits = kdb.core_mark(graph, M, e, comm)
+            r = kdb.mst(graph, e, bits, comm, workspace=ws, out=outs)
+            lb = kdb.label(graph, e, bits, r.comp, out=lab)
         return bits, r, lb
 
     for _ in range(args.warmup):
@@ -268,7 +307,7 @@ def run_ours(args):
         out = None
         for _ in range(args.steps):
             out = step(g)
-            st_.append(out[1].stats)
+            st_.append(out[1].stats)  # stats of the step's last eps
         e1.record(stream)
         torch.cuda.synchronize()
         barrier()
@@ -283,14 +322,15 @@ def run_ours(args):
     ms_prof, stats_prof, _ = timed(True)
     prof = kdb.profile_read()
     clk = clocks.stop()
-    value = N * k / (ms * 1e-3)
+    F = len(eps_list)
+    value = N * k * F / (ms * 1e-3)
     n_clusters = int(torch.unique(r.comp[r.comp >= 0]).numel()) if rank == 0 else None
     msf_count, msf_weight = r.count, r.weight
 
     # ---- e2e: host buffers through the public API ---------------------------------
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(args, kdb, W, N, k, M, eps, rb, re_, comm, ws, outs, dev, world)
+        e2e = run_e2e(args, kdb, W, N, k, M, eps_list, ec, rb, re_, comm, ws, outs, dev, world)
 
     # ---- roofline of the dominant kernel ------------------------------------------------
     peaks = measured_peaks()
@@ -303,7 +343,7 @@ def run_ours(args):
     if dom:
         name, (tot_ms, nl) = dom
         per_launch_ms = tot_ms / nl
-        algo_bytes = algo_bytes_per_launch(name, N, k, world, nl / args.steps, stats)
+        algo_bytes = algo_bytes_per_launch(name, N, kc, world, nl / args.steps, stats)
         achieved = algo_bytes / (per_launch_ms * 1e-3) / 1e9 if algo_bytes else None
         traffic = measured_traffic().get(base_name(name), {}).get("dram_bytes_per_launch")
         roof = {"kernel": name, "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -312,11 +352,11 @@ def run_ours(args):
                 "ms_per_launch": per_launch_ms, "share_of_step": tot_ms / args.steps / ms_prof,
                 "instrumented_ms_per_step": ms_prof,
                 "algo_bytes_per_launch": algo_bytes}
-    t_min_ms = (8.0 * N * k + 4.0 * N + N / 8.0) / (peak * 1e9) * 1e3 / world
+    t_min_ms = F * (8.0 * N * kc + 4.0 * N + N / 8.0) / (peak * 1e9) * 1e3 / world
     kernels = {}
     for n, v in sorted(prof.items(), key=lambda kv: -kv[1][0]):
         e = {"ms_per_step": v[0] / args.steps, "launches_per_step": v[1] / args.steps}
-        ab = algo_bytes_per_launch(n, N, k, world, v[1] / args.steps, stats) if v[1] else None
+        ab = algo_bytes_per_launch(n, N, kc, world, v[1] / args.steps, stats) if v[1] else None
         if ab:
             gbs = ab / (v[0] / v[1] * 1e-3) / 1e9
             e.update(algo_gbs=gbs, frac_of_peak=gbs / peak)
@@ -326,8 +366,8 @@ def run_ours(args):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         ns = min(args.cpu_sample_rows, N)
-        dt, _ = oracle_sample(W["nbr"][:ns].cpu().numpy(), W["dist"][:ns].cpu().numpy(), M, eps)
-        cpu = {"value": ns * k / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+        dt, _ = oracle_sample(W["nbr"][:ns].cpu().numpy(), W["dist"][:ns].cpu().numpy(), M, eps_list, ec)
+        cpu = {"value": ns * k * F / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
                "sample": f"rows [0, {ns}) of the workload ({ns * k} entries; entries to ids >= {ns} skipped), "
                          f"one single-threaded run, {dt:.1f} s"}
 
@@ -336,7 +376,8 @@ def run_ours(args):
                 "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "f32", "data": "synthetic",
                 "config": dict(workload_desc(args.config, W, args.scale),
-                               parallelism=f"row-partitioned x{world}", exact_graph=not args.general),
+                               parallelism=f"row-partitioned x{world}", exact_graph=not args.general,
+                               **stage_desc(ec, eps_list, W)),
                 "roofline": roof,
                 "stage_roofline": {"t_min_ms": t_min_ms, "frac": t_min_ms / ms,
                                    "bytes": "8 N k + 4 N + N/8 (SURVEY.md 8(d))", "peak": peak},
@@ -399,7 +440,7 @@ def measured_traffic():
         return {}
 
 
-def run_e2e(args, kdb, W, N, k, M, eps, rb, re_, comm, ws, outs, dev, world):
+def run_e2e(args, kdb, W, N, k, M, eps_list, ec, rb, re_, comm, ws, outs, dev, world):
     """Same metric through the public API from PINNED HOST buffers: each step copies
     this rank's graph rows host->device and reads the labels back."""
     import torch
@@ -422,11 +463,12 @@ def run_e2e(args, kdb, W, N, k, M, eps, rb, re_, comm, ws, outs, dev, world):
     for _ in range(steps):
         d_nbr.copy_(h_nbr, non_blocking=True)
         d_dist.copy_(h_dist, non_blocking=True)
-        g = kdb.Graph(d_nbr, d_dist, n_total=N, row_begin=rb, exact=not args.general)
-        bits = kdb.core_mark(g, M, eps, comm)
-        r = kdb.mst(g, eps, bits, comm, workspace=ws, out=outs)
-        lb = kdb.label(g, eps, bits, r.comp)
-        h_lab.copy_(lb, non_blocking=True)
+        g = kdb.Graph(d_nbr, d_dist, n_total=N, row_begin=rb, exact=not args.general, edge_cols=ec)
+        for eps in eps_list:
+            bits = kdb.core_mark(g, M, eps, comm)
+            r = kdb.mst(g, eps, bits, comm, workspace=ws, out=outs)
+            lb = kdb.label(g, eps, bits, r.comp)
+            h_lab.copy_(lb, non_blocking=True)
     e1.record(stream)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / steps
@@ -436,8 +478,8 @@ def run_e2e(args, kdb, W, N, k, M, eps, rb, re_, comm, ws, outs, dev, world):
         tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
     ms = float(t.item())
     del h_nbr, h_dist
-    return {"value": N * k / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms, "steps": steps,
-            "h2d_bytes_per_step": int(n_rows) * k * 8, "d2h_bytes_per_step": int(n_rows) * 4}
+    return {"value": N * k * len(eps_list) / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms, "steps": steps,
+            "h2d_bytes_per_step": int(n_rows) * k * 8, "d2h_bytes_per_step": int(n_rows) * 4 * len(eps_list)}
 
 
 def main():

@@ -14,9 +14,13 @@
  *   row i lists i's neighbours EXCLUDING i itself, weights non-decreasing fp32,
  *   padding entries are (id -1, weight +inf) at the row tail.  core(i) is
  *   D[i][M-1] <= eps, i.e. at least M other points within eps.
- * Candidate edges: every stored entry (i, c) with J = nbr[i][c] >= 0, J != i,
- *   core(i), core(J) and D[i][c] <= eps is the UNDIRECTED edge {i, J} with
- *   weight w = D[i][c] (reading #3: all k columns; reading #4: undirected).
+ * Candidate edges: every stored entry (i, c) with c < edge_cols, J = nbr[i][c] >= 0,
+ *   J != i, core(i), core(J) and D[i][c] <= eps is the UNDIRECTED edge {i, J}
+ *   with weight w = D[i][c] (reading #4: undirected).  edge_cols = k (the
+ *   default) is reading #3, all k columns; edge_cols = M is the paper's direct
+ *   M-reachability, Def. 6: p core and q in N_M(p) or
+ *   p in N_M(q), with Alg. 2's scan bound L[i] <= M; by
+ *   Thm. 2(ii) its MSF clusters are the kNN-DBSCAN clusters.
  * Edge order O1 (reading #6): (mono(w), a = min(i,J), b = max(i,J)) where
  *   mono(w) is the fp32 bit pattern with -0 canonicalised to +0.  The MSF under
  *   this strict order is unique; kdb_mst returns exactly it.
@@ -74,6 +78,13 @@ typedef struct {
   const float* dist;   /* device [n_rows][k_max] fp32 >= 0, non-decreasing per row,
                           +inf = padding; 16-B aligned                              */
   uint32_t flags;      /* KDB_GRAPH_EXACT or 0                                       */
+  int32_t edge_cols;   /* candidate edges come from columns [0, edge_cols) of each row;
+                          0 = all k_max.  Only kdb_mst reads it; 0 <= edge_cols <= k_max
+                          (EINVAL otherwise).  edge_cols = M gives Def. 6's edge set.
+                          The kernels keep the row stride k_max and never read columns
+                          >= edge_cols (the first edge_cols columns of an exact k-NN
+                          graph are an exact edge_cols-NN graph, so KDB_GRAPH_EXACT
+                          stays valid with the certificate taken at column edge_cols-1). */
 } kdb_graph;
 
 /* ---- communicators ------------------------------------------------------ */

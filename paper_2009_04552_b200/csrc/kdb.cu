@@ -420,7 +420,7 @@ struct Offer {
 // local rows: certificate bound kth'(v) into kmin[comp v] (exact mode); the
 // active list holds the core rows whose first entry is within eps (a row
 // starting beyond it offers nothing, ever).  comp[v] >= 0 <=> v is core.
-__global__ void k_init_rows(const float* __restrict__ dist, int64_t n_rows, int32_t k, float eps,
+__global__ void k_init_rows(const float* __restrict__ dist, int64_t n_rows, int32_t ld, int32_t k, float eps,
                             int64_t row_begin, const int32_t* __restrict__ comp, uint32_t* __restrict__ kmin,
                             Rec* __restrict__ act, uint32_t* __restrict__ n_act) {
   for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n_rows; base += (int64_t)gridDim.x * blockDim.x) {
@@ -430,9 +430,9 @@ __global__ void k_init_rows(const float* __restrict__ dist, int64_t n_rows, int3
     if (i < n_rows) {
       const int32_t cv = comp[v];
       if (cv >= 0) {
-        want = __ldcs(dist + i * k) <= eps;
+        want = __ldcs(dist + i * ld) <= eps;
         if (kmin) {
-          const float kth = __ldcs(dist + i * k + (k - 1));
+          const float kth = __ldcs(dist + i * ld + (k - 1));
           kmin[cv] = (kth <= eps) ? mono_bits(kth) : kInfBits;
         }
       }
@@ -446,16 +446,16 @@ __global__ void k_init_rows(const float* __restrict__ dist, int64_t n_rows, int3
 // general mode: in-edge lists (transpose of local candidate entries)
 // ============================================================================
 __global__ void k_in_count(const int32_t* __restrict__ nbr, const float* __restrict__ dist,
-                           int64_t n_rows, int32_t k, float eps, int64_t row_begin, int64_t N,
+                           int64_t n_rows, int32_t ld, int32_t k, float eps, int64_t row_begin, int64_t N,
                            const uint32_t* __restrict__ bits, unsigned long long* __restrict__ cnt) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_rows;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t v = row_begin + i;
     if (!is_core(bits, v)) continue;
     for (int32_t c = 0; c < k; ++c) {
-      const float w = __ldg(dist + i * k + c);
+      const float w = __ldg(dist + i * ld + c);
       if (!(w <= eps)) break;
-      const int64_t J = __ldg(nbr + i * k + c);
+      const int64_t J = __ldg(nbr + i * ld + c);
       if (J < 0 || J >= N || J == v || !is_core(bits, J)) continue;
       atomicAdd(cnt + J, 1ull);
     }
@@ -463,7 +463,7 @@ __global__ void k_in_count(const int32_t* __restrict__ nbr, const float* __restr
 }
 
 __global__ void k_in_fill(const int32_t* __restrict__ nbr, const float* __restrict__ dist,
-                          int64_t n_rows, int32_t k, float eps, int64_t row_begin, int64_t N,
+                          int64_t n_rows, int32_t ld, int32_t k, float eps, int64_t row_begin, int64_t N,
                           const uint32_t* __restrict__ bits, unsigned long long* __restrict__ cursor,
                           int32_t* __restrict__ in_src, float* __restrict__ in_w) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_rows;
@@ -471,9 +471,9 @@ __global__ void k_in_fill(const int32_t* __restrict__ nbr, const float* __restri
     const int64_t v = row_begin + i;
     if (!is_core(bits, v)) continue;
     for (int32_t c = 0; c < k; ++c) {
-      const float w = __ldg(dist + i * k + c);
+      const float w = __ldg(dist + i * ld + c);
       if (!(w <= eps)) break;
-      const int64_t J = __ldg(nbr + i * k + c);
+      const int64_t J = __ldg(nbr + i * ld + c);
       if (J < 0 || J >= N || J == v || !is_core(bits, J)) continue;
       const unsigned long long s = atomicAdd(cursor + J, 1ull);
       in_src[s] = (int32_t)v;
@@ -513,7 +513,8 @@ __global__ void k_in_finish(const unsigned long long* __restrict__ off, int64_t 
 template <bool VEC>
 __device__ __forceinline__ void load_chunk(const int32_t* nr, const float* dr, int c0, int k, int32_t (&J)[4],
                                            float (&w)[4]) {
-  if (VEC) {  // k % 4 == 0: an aligned 4-chunk never straddles the row end
+  if (VEC) {  // row stride % 4 == 0: an aligned 4-chunk never straddles the row end (entries
+              // at or beyond the candidate bound k are ignored by the callers)
     const int4 j4 = __ldcs(reinterpret_cast<const int4*>(nr + c0));
     const float4 w4 = __ldcs(reinterpret_cast<const float4*>(dr + c0));
     J[0] = j4.x; J[1] = j4.y; J[2] = j4.z; J[3] = j4.w;
@@ -593,7 +594,7 @@ __device__ __forceinline__ RowScan scan_row(const int32_t* __restrict__ nr, cons
 // writes Kc, Bc and the hook target directly.  Rows that offered stay active.
 template <bool VEC>
 __global__ void __launch_bounds__(256) k_offer_first(const int32_t* __restrict__ nbr, const float* __restrict__ dist,
-                                                     int32_t k, float eps, int64_t row_begin, int64_t N,
+                                                     int32_t ld, int32_t k, float eps, int64_t row_begin, int64_t N,
                                                      const int32_t* __restrict__ comp, int all_core,
                                                      const Rec* __restrict__ act, uint32_t n_in,
                                                      Rec* __restrict__ act_out, uint32_t* __restrict__ n_out,
@@ -610,7 +611,7 @@ __global__ void __launch_bounds__(256) k_offer_first(const int32_t* __restrict__
       const Rec a{a2.x, a2.y};
       v = a.v;
       const int64_t i = (int64_t)v - row_begin;
-      r = scan_row<VEC, true>(nbr + i * k, dist + i * k, k, eps, v, -1, a.h, N, comp, all_core, reads);
+      r = scan_row<VEC, true>(nbr + i * ld, dist + i * ld, k, eps, v, -1, a.h, N, comp, all_core, reads);
       if (r.found) {
         const int32_t cv = all_core ? v : gat(comp + v);
         Kc[cv] = r.best;
@@ -630,7 +631,7 @@ __global__ void __launch_bounds__(256) k_offer_first(const int32_t* __restrict__
 // row's next record, to the same slot of the offer list (for the tie pass).
 template <bool VEC>
 __global__ void __launch_bounds__(256) k_offer_round(const int32_t* __restrict__ nbr, const float* __restrict__ dist,
-                                                     int32_t k, float eps, int64_t row_begin, int64_t N,
+                                                     int32_t ld, int32_t k, float eps, int64_t row_begin, int64_t N,
                                                      const int32_t* __restrict__ comp, const Rec* __restrict__ act,
                                                      uint32_t n_in, Rec* __restrict__ act_out,
                                                      uint32_t* __restrict__ n_out, Offer* __restrict__ offers,
@@ -648,7 +649,7 @@ __global__ void __launch_bounds__(256) k_offer_round(const int32_t* __restrict__
       v = a.v;
       cv = gat(comp + v);
       const int64_t i = (int64_t)v - row_begin;
-      r = scan_row<VEC, false>(nbr + i * k, dist + i * k, k, eps, v, cv, a.h, N, comp, 0, reads);
+      r = scan_row<VEC, false>(nbr + i * ld, dist + i * ld, k, eps, v, cv, a.h, N, comp, 0, reads);
       if (r.found) atomicMin(Kc + cv, (unsigned long long)r.best);
     }
     const uint32_t slot = block_reserve(n_out, r.found);
@@ -693,7 +694,7 @@ constexpr int kChunk = 1024;
 // Rows are taken in ordered chunks; the initial list keeps row order.
 template <bool VEC, bool A32>
 __global__ void __launch_bounds__(256) k_light_ell(const int32_t* __restrict__ nbr, const float* __restrict__ dist,
-                                                   int64_t n_rows, int32_t k, float eps, int64_t row_begin,
+                                                   int64_t n_rows, int32_t ld, int32_t k, float eps, int64_t row_begin,
                                                    const int32_t* __restrict__ comp, uint32_t* __restrict__ kmin,
                                                    int4* __restrict__ LE, Rec* __restrict__ act,
                                                    uint32_t* __restrict__ n_act, uint32_t* __restrict__ grab,
@@ -713,15 +714,15 @@ __global__ void __launch_bounds__(256) k_light_ell(const int32_t* __restrict__ n
       const int64_t v = row_begin + i;
       const int32_t cv = comp[v];
       if (cv < 0) continue;
-      const int32_t* nr = nbr + i * k;
-      const float* dr = dist + i * k;
+      const int32_t* nr = nbr + i * ld;
+      const float* dr = dist + i * ld;
       int32_t J[kW];
       float w[kW];
       if (VEC && A32) {
         // whole 32-byte sectors (LDG.256): a row starts at a 32-B boundary or
-        // 16 B past one (k % 8 == 4), so 2 or 3 sectors cover its first kW
+        // 16 B past one (ld % 8 == 4), so 2 or 3 sectors cover its first kW
         // entries -- one request per sector instead of one per 16-B half
-        const int sh = (int)((i * k) & 7);  // 0 or 4
+        const int sh = (int)((i * ld) & 7);  // 0 or 4
         int4 a0, a1, a2, a3, a4, a5, b0, b1, b2, b3, b4, b5;
         const int4* pj = reinterpret_cast<const int4*>(nr - sh);
         const int4* pd = reinterpret_cast<const int4*>(dr - sh);
@@ -744,7 +745,7 @@ __global__ void __launch_bounds__(256) k_light_ell(const int32_t* __restrict__ n
           J[c] = sh ? SJ[c + 4] : SJ[c];
           w[c] = __int_as_float(sh ? SW[c + 4] : SW[c]);
         }
-      } else if (VEC && k >= kW) {
+      } else if (VEC && ld >= kW) {
 #pragma unroll
         for (int q = 0; q < kW / 4; ++q) {
           // L1-allocating loads: the two 16-B halves of a sector are separate
@@ -760,6 +761,11 @@ __global__ void __launch_bounds__(256) k_light_ell(const int32_t* __restrict__ n
           J[c] = c < k ? __ldg(nr + c) : -1;
           w[c] = c < k ? __ldg(dr + c) : __int_as_float(0x7f800000);
         }
+      }
+      if (VEC && k < kW) {  // edge_cols < kW: columns >= k are not candidates (padding)
+#pragma unroll
+        for (int c = 0; c < kW; ++c)
+          if (c >= k) { J[c] = -1; w[c] = __int_as_float(0x7f800000); }
       }
       // kth = D[v][k-1] >= D[v][kW-1]: only needed (exact-mode certificate) when
       // that is within eps_run
@@ -837,7 +843,10 @@ __global__ void __launch_bounds__(256) k_light_ell(const int32_t* __restrict__ n
 // rest (rare: a candidate prefix longer than kW) from the graph row.  DIRECT:
 // singleton components (round 1, exact mode), every candidate leaves; with
 // all_core a vertex's dense component id is the vertex itself (no gathers).
-template <bool DIRECT>
+// GW: component gathers are issued GW entries at a time; once the minimum is
+// found only entries of its weight (decided from the loaded w) are gathered,
+// so a smaller GW trades memory-level parallelism for L2 sector traffic.
+template <bool DIRECT, int GW = 4>
 __device__ __forceinline__ RowScan scan_ell(const int4* __restrict__ le, const int32_t* __restrict__ nr,
                                             const float* __restrict__ dr, int k, float eps, int32_t v, int32_t cv,
                                             int h, int64_t N, const int32_t* __restrict__ comp, int all_core,
@@ -852,16 +861,20 @@ __device__ __forceinline__ RowScan scan_ell(const int4* __restrict__ le, const i
     ld256cs(le + (c0 >> 1), p0, p1);
     const int32_t J[4] = {p0.x, p0.z, p1.x, p1.z};
     const float w[4] = {__int_as_float(p0.y), __int_as_float(p0.w), __int_as_float(p1.y), __int_as_float(p1.w)};
-    int32_t cj[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int idx = c0 + j;
-      const bool cand = idx >= h && idx < kend && w[j] <= eps && J[j] >= 0 && J[j] < N && J[j] != v;
-      cj[j] = cand ? ((DIRECT && all_core) ? J[j] : gat(comp + J[j])) : -1;
-    }
     reads += (unsigned long long)(min(c0 + 4, kend) - max(c0, h));
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int g0 = 0; g0 < 4; g0 += GW) {
+    if (done) break;
+    int32_t cj[4];
+#pragma unroll
+    for (int j = g0; j < g0 + GW; ++j) {
+      const int idx = c0 + j;
+      bool cand = idx >= h && idx < kend && w[j] <= eps && J[j] >= 0 && J[j] < N && J[j] != v;
+      if (GW < 4 && r.found && mono_bits(w[j]) != wstar) cand = false;  // past the tie group: no gather
+      cj[j] = cand ? ((DIRECT && all_core) ? J[j] : gat(comp + J[j])) : -1;
+    }
+#pragma unroll
+    for (int j = g0; j < g0 + GW; ++j) {
       const int idx = c0 + j;
       if (done || idx < h || idx >= kend) continue;
       const bool leaving = cj[j] >= 0 && (DIRECT || cj[j] != cv);
@@ -882,6 +895,7 @@ __device__ __forceinline__ RowScan scan_ell(const int4* __restrict__ le, const i
         const uint32_t bb = (uint32_t)max(v, J[j]);
         if (kk < r.best || (kk == r.best && bb < r.bestb)) { r.best = kk; r.bestb = bb; r.bestc = cj[j]; }
       }
+    }
     }
     c0 += 4;
   }
@@ -919,7 +933,7 @@ __device__ __forceinline__ RowScan scan_ell(const int4* __restrict__ le, const i
 
 // round 1 (exact mode, singletons) over the ELL; see k_offer_first
 __global__ void __launch_bounds__(256) k_light_first(const int4* __restrict__ LE, const int32_t* __restrict__ nbr,
-                                                     const float* __restrict__ dist, int32_t k, float eps,
+                                                     const float* __restrict__ dist, int32_t ld, int32_t k, float eps,
                                                      int64_t row_begin, int64_t N, const int32_t* __restrict__ comp,
                                                      int all_core, const Rec* __restrict__ act, uint32_t n_in,
                                                      Rec* __restrict__ act_out, uint32_t* __restrict__ n_out,
@@ -941,7 +955,7 @@ __global__ void __launch_bounds__(256) k_light_first(const int4* __restrict__ LE
       const int2 a = __ldcs(reinterpret_cast<const int2*>(act + s));
       const int32_t v = a.x;
       const int64_t i = (int64_t)v - row_begin;
-      const RowScan r = scan_ell<true>(LE + i * (kW / 2), nbr + i * k, dist + i * k, k, eps, v, -1, a.y, N, comp,
+      const RowScan r = scan_ell<true>(LE + i * (kW / 2), nbr + i * ld, dist + i * ld, k, eps, v, -1, a.y, N, comp,
                                        all_core, reads);
       if (r.found) {
         const int32_t cv = all_core ? v : gat(comp + v);
@@ -963,8 +977,9 @@ __global__ void __launch_bounds__(256) k_light_first(const int4* __restrict__ LE
 }
 
 // later rounds over the ELL; see k_offer_round
+template <int GW>
 __global__ void __launch_bounds__(256) k_light_round(const int4* __restrict__ LE, const int32_t* __restrict__ nbr,
-                                                     const float* __restrict__ dist, int32_t k, float eps,
+                                                     const float* __restrict__ dist, int32_t ld, int32_t k, float eps,
                                                      int64_t row_begin, int64_t N, const int32_t* __restrict__ comp,
                                                      const Rec* __restrict__ act, uint32_t n_in,
                                                      Rec* __restrict__ act_out, uint32_t* __restrict__ n_out,
@@ -988,8 +1003,8 @@ __global__ void __launch_bounds__(256) k_light_round(const int4* __restrict__ LE
       const int32_t v = a.x;
       const int32_t cv = gat(comp + v);
       const int64_t i = (int64_t)v - row_begin;
-      const RowScan r = scan_ell<false>(LE + i * (kW / 2), nbr + i * k, dist + i * k, k, eps, v, cv, a.y, N, comp,
-                                        0, reads);
+      const RowScan r = scan_ell<false, GW>(LE + i * (kW / 2), nbr + i * ld, dist + i * ld, k, eps, v, cv, a.y, N,
+                                            comp, 0, reads);
       if (r.found) {
         atomicMin(Kc + cv, (unsigned long long)r.best);
         const uint32_t j = atomicAdd(&s_n, 1u);
@@ -1072,7 +1087,7 @@ __global__ void k_tie(const Offer* __restrict__ offers, const uint32_t* __restri
 
 // stall fallback (exact mode): offer EVERY live leaving entry of the active
 // rows to both endpoint components (rows outside the active list have none)
-__global__ void k_sweep(const int32_t* __restrict__ nbr, const float* __restrict__ dist, int32_t k, float eps,
+__global__ void k_sweep(const int32_t* __restrict__ nbr, const float* __restrict__ dist, int32_t ld, int32_t k, float eps,
                         int64_t row_begin, int64_t N, const int32_t* __restrict__ comp,
                         const Rec* __restrict__ act, uint32_t n_act, unsigned long long* __restrict__ Kc,
                         uint32_t* __restrict__ Bc, int tie_phase) {
@@ -1081,9 +1096,9 @@ __global__ void k_sweep(const int32_t* __restrict__ nbr, const float* __restrict
     const int64_t i = v - row_begin;
     const int32_t cv = comp[v];
     for (int32_t c = act[s].h; c < k; ++c) {
-      const float w = __ldg(dist + i * k + c);
+      const float w = __ldg(dist + i * ld + c);
       if (!(w <= eps)) break;
-      const int64_t J = __ldg(nbr + i * k + c);
+      const int64_t J = __ldg(nbr + i * ld + c);
       if (J < 0 || J >= N || J == v) continue;
       const int32_t cj = comp[J];
       if (cj < 0 || cj == cv) continue;
@@ -1390,27 +1405,68 @@ __global__ void k_wbuckets(int64_t m, const float* __restrict__ w, unsigned long
 }
 
 // a10: labels of this rank's rows
+// kLabelG lanes per row, 4 entries per lane and step: a non-core row's scan
+// (at most M-1 entries within eps, then the first one beyond) is read as
+// 64-byte coalesced pieces instead of a serial per-thread walk.  The first
+// event in column order decides: an entry beyond eps ends the scan (noise so
+// far), a core neighbour within eps gives the label.
+constexpr int kLabelG = 4;
+template <bool VEC>
 __global__ void k_label(const int32_t* __restrict__ nbr, const float* __restrict__ dist, int64_t n_rows,
                         int32_t k, float eps, int64_t row_begin, int64_t N,
                         const uint32_t* __restrict__ bits, const int32_t* __restrict__ comp,
                         int32_t* __restrict__ labels) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_rows;
-       i += (int64_t)gridDim.x * blockDim.x) {
+  constexpr int G = kLabelG, RPW = 32 / G;
+  const int lane = threadIdx.x & 31, sub = lane & (G - 1);
+  const unsigned gmask = ((1u << G) - 1u) << (lane & ~(G - 1));
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = warp * RPW + lane / G; i - lane / G < n_rows; i += nwarps * RPW) {
+    if (i >= n_rows) continue;  // the whole group skips together
     const int64_t v = row_begin + i;
-    int32_t lab = -1;
     if (is_core(bits, v)) {
-      lab = comp[v];
-    } else {
-      for (int32_t c = 0; c < k; ++c) {
-        const float w = __ldg(dist + i * k + c);
-        if (!(w <= eps)) break;
-        const int64_t J = __ldg(nbr + i * k + c);
-        if (J < 0 || J >= N || !is_core(bits, J)) continue;
-        lab = comp[J];
-        break;
+      if (sub == 0) labels[i] = comp[v];
+      continue;
+    }
+    const int32_t* nr = nbr + i * k;
+    const float* dr = dist + i * k;
+    int32_t lab = -1;
+    bool decided = false;
+    for (int c0 = 0; c0 < k && !decided; c0 += 4 * G) {
+      const int c = c0 + 4 * sub;
+      int32_t J[4];
+      float w[4];
+      if (VEC && c + 4 <= k) {
+        const int4 j4 = __ldcs(reinterpret_cast<const int4*>(nr + c));
+        const float4 w4 = __ldcs(reinterpret_cast<const float4*>(dr + c));
+        J[0] = j4.x; J[1] = j4.y; J[2] = j4.z; J[3] = j4.w;
+        w[0] = w4.x; w[1] = w4.y; w[2] = w4.z; w[3] = w4.w;
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const bool in = c + j < k;
+          J[j] = in ? __ldcs(nr + c + j) : -1;
+          w[j] = in ? __ldcs(dr + c + j) : __int_as_float(0x7f800000);
+        }
+      }
+      // this lane's first event: 0..3 = index, hit = core neighbour within eps
+      int ev = 4;
+      bool hit = false;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (ev < 4) continue;
+        if (c + j >= k) { ev = j; break; }  // row end: treated as "beyond eps"
+        if (!(w[j] <= eps)) { ev = j; continue; }
+        const int64_t Jj = J[j];
+        if (Jj >= 0 && Jj < N && is_core(bits, Jj)) { ev = j; hit = true; lab = (int32_t)Jj; }
+      }
+      const unsigned any = __ballot_sync(gmask, ev < 4) & gmask;
+      if (any) {
+        decided = true;
+        if (lane == __ffs(any) - 1) labels[i] = hit ? comp[lab] : -1;
       }
     }
-    labels[i] = lab;
+    if (!decided && sub == 0) labels[i] = -1;
   }
 }
 
@@ -1430,10 +1486,10 @@ __global__ void k_label(const int32_t* __restrict__ nbr, const float* __restrict
 // exact for ANY valid graph (no certificate, no in-edge lists).
 
 // tau sampling: column `col` of every stride-th local row
-__global__ void k_sample_col(const float* __restrict__ dist, int64_t n_rows, int32_t k, int32_t col, int64_t stride,
+__global__ void k_sample_col(const float* __restrict__ dist, int64_t n_rows, int32_t ld, int32_t col, int64_t stride,
                              int64_t n_out, float* __restrict__ out) {
   for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n_out; s += (int64_t)gridDim.x * blockDim.x)
-    out[s] = __ldg(dist + (s * stride) * k + col);
+    out[s] = __ldg(dist + (s * stride) * ld + col);
 }
 
 struct HEdge {     // a survivor: a heavy candidate entry that crosses light components
@@ -1551,9 +1607,12 @@ struct FRow {
   uint32_t pad;
 };
 
-template <int VEC, bool FAST>
+// COLS (edge_cols < row stride ld): only columns < k are candidates; the sweep
+// enumerates just the ceil(k / VEC) chunks at the head of each row (fd then
+// divides by that count), so columns >= k cost neither loads nor issue slots.
+template <int VEC, bool FAST, bool COLS>
 __global__ void __launch_bounds__(kFilterThreads) k_filter(
-    const int32_t* __restrict__ nbr, const float* __restrict__ dist, int64_t n_rows, int32_t k, float tau, float eps,
+    const int32_t* __restrict__ nbr, const float* __restrict__ dist, int64_t n_rows, int32_t ld, int32_t k, float tau, float eps,
     int64_t row_begin, int64_t N, const int32_t* __restrict__ comp, const int2* __restrict__ rng, const uint32_t* __restrict__ bloom, FastDiv fd,
     HEdge* __restrict__ out, uint32_t cap, uint32_t* __restrict__ n_out, unsigned long long* __restrict__ n_slow) {
   extern __shared__ uint32_t s_bloom[];
@@ -1583,9 +1642,10 @@ __global__ void __launch_bounds__(kFilterThreads) k_filter(
       s_row[threadIdx.x] = fr;
     }
     __syncthreads();
-    const int32_t* __restrict__ nt = nbr + r0 * k;  // this tile's ids (contiguous)
-    const float* __restrict__ dt = dist + r0 * k;
-    const uint32_t n_chunks = (uint32_t)(((int64_t)nr * k) / VEC);
+    const int32_t* __restrict__ nt = nbr + r0 * ld;  // this tile's ids (contiguous)
+    const float* __restrict__ dt = dist + r0 * ld;
+    const uint32_t cpr = (uint32_t)((k + VEC - 1) / VEC);  // COLS: chunks per row
+    const uint32_t n_chunks = COLS ? (uint32_t)nr * cpr : (uint32_t)(((int64_t)nr * ld) / VEC);
     // kFilterUnroll chunks per thread and step: their id loads are issued
     // together (the sweep is bound by load latency x loads in flight)
     for (uint32_t base = 0; base < n_chunks; base += blockDim.x * kFilterUnroll) {
@@ -1593,23 +1653,34 @@ __global__ void __launch_bounds__(kFilterThreads) k_filter(
 #pragma unroll
       for (int t = 0; t < kFilterUnroll; ++t) {
         const uint32_t u = base + t * blockDim.x + threadIdx.x;
+        uint32_t off = u;  // chunk offset from the tile start
+        if (COLS && u < n_chunks) {
+          const uint32_t lr = (fd.d > 1 && fd.d < 2048) ? __umulhi(u, fd.m32) : (uint32_t)fdiv(u, fd);
+          off = lr * (uint32_t)(ld / VEC) + (u - lr * cpr);
+        }
         if (VEC == 4) {
-          const int4 j4 = u < n_chunks ? __ldcs(reinterpret_cast<const int4*>(nt) + u) : make_int4(-1, -1, -1, -1);
+          const int4 j4 = u < n_chunks ? __ldcs(reinterpret_cast<const int4*>(nt) + off) : make_int4(-1, -1, -1, -1);
           J[t][0] = j4.x; J[t][1] = j4.y; J[t][2] = j4.z; J[t][3] = j4.w;
         } else {
-          J[t][0] = u < n_chunks ? __ldcs(nt + u) : -1;
+          J[t][0] = u < n_chunks ? __ldcs(nt + off) : -1;
         }
       }
 #pragma unroll
       for (int t = 0; t < kFilterUnroll; ++t) {
         const uint32_t u = base + t * blockDim.x + threadIdx.x;
-        uint32_t survm = 0, lr = 0, col = 0;
+        uint32_t survm = 0, lr = 0, col = 0, off = u;
         int32_t cj[VEC], cr = -1;
         float w[VEC];
         if (u < n_chunks) {
-          const uint32_t n = u * VEC;
-          lr = (k > 1 && k < 2048) ? __umulhi(n, fd.m32) : (uint32_t)fdiv(n, fd);  // row within the tile
-          col = n - lr * (uint32_t)k;
+          if (COLS) {
+            lr = (fd.d > 1 && fd.d < 2048) ? __umulhi(u, fd.m32) : (uint32_t)fdiv(u, fd);  // row within the tile
+            col = (u - lr * cpr) * VEC;
+            off = lr * (uint32_t)(ld / VEC) + (u - lr * cpr);
+          } else {
+            const uint32_t n = u * VEC;
+            lr = (fd.d > 1 && fd.d < 2048) ? __umulhi(n, fd.m32) : (uint32_t)fdiv(n, fd);  // row within the tile
+            col = n - lr * (uint32_t)ld;
+          }
           const FRow fr = s_row[lr];
           cr = fr.cr;
           // Fast test first: J in the id range of comp[v] and not a possible
@@ -1629,14 +1700,15 @@ __global__ void __launch_bounds__(kFilterThreads) k_filter(
             }
             slowm |= ((fast & 1u) ^ 1u) << j;
           }
+          if (COLS) slowm &= (1u << min((uint32_t)VEC, (uint32_t)k - col)) - 1u;
           if (fr.cr < 0) slowm = 0;  // non-core row: no candidate entries
           if (slowm) {
             const uint32_t v = (uint32_t)(row_begin + r0 + lr);
             if (VEC == 4) {
-              const float4 w4 = __ldg(reinterpret_cast<const float4*>(dt) + u);
+              const float4 w4 = __ldg(reinterpret_cast<const float4*>(dt) + off);
               w[0] = w4.x; w[1] = w4.y; w[2] = w4.z; w[3] = w4.w;
             } else {
-              w[0] = __ldg(dt + u);
+              w[0] = __ldg(dt + off);
             }
 #pragma unroll
             for (int j = 0; j < VEC; ++j) {
@@ -1965,6 +2037,7 @@ kdb_status validate_graph(const kdb_graph* g) {
   if (((uintptr_t)g->nbr & 15u) || ((uintptr_t)g->dist & 15u))
     return set_err(KDB_EINVAL, "nbr/dist must be 16-byte aligned");
   if (g->flags & ~KDB_GRAPH_EXACT) return set_err(KDB_EINVAL, "unknown graph flags");
+  if (g->edge_cols < 0 || g->edge_cols > g->k_max) return set_err(KDB_EINVAL, "edge_cols must be in [0, k_max]");
   return KDB_OK;
 }
 
@@ -2016,7 +2089,8 @@ struct Mst {
   kdb_comm* comm = nullptr;
   cudaStream_t st = nullptr;
   int64_t N = 0;
-  int32_t k = 0;
+  int32_t k = 0;   // candidate columns: edge_cols (kdb.h), else k_max
+  int32_t ld = 0;  // row stride k_max
   const uint32_t* bits = nullptr;
   int32_t* comp = nullptr;
   bool general = false;
@@ -2047,7 +2121,7 @@ kdb_status pick_tau(Mst& m, int m0, float* tau_out) {
   if (n > 0) {
     const int64_t S = std::min<int64_t>(n, kTauSamples);
     const int64_t stride = n / S;
-    LAUNCH(k_sample_col, grid_for(S), kThreads, m.st, g->dist, n, m.k, m0 - 1, stride, S, L.tau_sample);
+    LAUNCH(k_sample_col, grid_for(S), kThreads, m.st, g->dist, n, m.ld, m0 - 1, stride, S, L.tau_sample);
     KDB_CUDA(cudaGetLastError());
     std::vector<float> h(S);
     KDB_CUDA(cudaMemcpyAsync(h.data(), L.tau_sample, S * sizeof(float), cudaMemcpyDeviceToHost, m.st));
@@ -2077,11 +2151,12 @@ kdb_status rows_phase(Mst& m, float eps_run) {
   kdb_comm* comm = m.comm;
   cudaStream_t st = m.st;
   const int64_t N = m.N;
-  const int32_t k = m.k;
+  const int32_t k = m.k;    // candidate columns (edge_cols)
+  const int32_t ld = m.ld;  // row stride
   const uint32_t* core_bits = m.bits;
   int32_t* comp = m.comp;
   const bool general = m.general;
-  const bool vec = (k % 4) == 0;
+  const bool vec = (ld % 4) == 0;
   cudaEvent_t* ev = m.ev;
   KDB_CUDA(cudaEventRecord(ev[0], st));
 
@@ -2105,6 +2180,7 @@ kdb_status rows_phase(Mst& m, float eps_run) {
     LAUNCH(k_fill_comp_arrays, grid_for(C), kThreads, st, C, L.ranks[r].Kc, L.ranks[r].Bc, nullptr);
   KDB_CUDA(cudaGetLastError());
   const bool use_compact = env_int("KDB_COMPACT", 1) != 0;
+  const int gw = env_int("KDB_GW", 4);  // component-gather width of the later light rounds (scan_ell)
   // exact mode: round 1 (singleton components) is fused into the ELL pass; a
   // single rank also packs (K, B, kmin) per component for the round-1 hook
   const bool fuse1 = !general && use_compact && env_int("KDB_FUSE1", 1) != 0;
@@ -2117,11 +2193,11 @@ kdb_status rows_phase(Mst& m, float eps_run) {
     R.compact = false;
     if (R.n_rows > 0 && use_compact) {
       R.compact = true;
-      // 32-byte sector loads need 32-B aligned arrays, k % 8 in {0, 4} and rows
-      // long enough for the third sector (k >= 20)
-      const bool a32 = vec && k >= 20 && !(((uintptr_t)R.nbr | (uintptr_t)R.dist) & 31u);
+      // 32-byte sector loads need 32-B aligned arrays, ld % 8 in {0, 4} and rows
+      // long enough for the third sector (ld >= 20)
+      const bool a32 = vec && ld >= 20 && !(((uintptr_t)R.nbr | (uintptr_t)R.dist) & 31u);
 #define KDB_ELL_LAUNCH(V, A)                                                                                    \
-  LAUNCH((k_light_ell<V, A>), grid_for(R.n_rows), kThreads, st, R.nbr, R.dist, R.n_rows, k, eps_run, R.row_begin, \
+  LAUNCH((k_light_ell<V, A>), grid_for(R.n_rows), kThreads, st, R.nbr, R.dist, R.n_rows, ld, k, eps_run, R.row_begin, \
          comp, general ? nullptr : L.kmin, R.LE, R.act[0], &R.ctr->na[0], &R.ctr->grab, fuse1 ? 1 : 0,         \
          L.all_core, N, R.Kc, R.Bc, R.tgt, packed1 ? L.rec1 : nullptr)
       if (a32) KDB_ELL_LAUNCH(true, true);
@@ -2130,7 +2206,7 @@ kdb_status rows_phase(Mst& m, float eps_run) {
 #undef KDB_ELL_LAUNCH
     }
     if (R.n_rows > 0 && !R.compact)
-      LAUNCH(k_init_rows, grid_for(R.n_rows), kThreads, st, R.dist, R.n_rows, k, eps_run, R.row_begin, comp,
+      LAUNCH(k_init_rows, grid_for(R.n_rows), kThreads, st, R.dist, R.n_rows, ld, k, eps_run, R.row_begin, comp,
              general ? nullptr : L.kmin, R.act[0], &R.ctr->na[0]);
     KDB_CUDA(cudaGetLastError());
   }
@@ -2143,14 +2219,14 @@ kdb_status rows_phase(Mst& m, float eps_run) {
       unsigned long long* cursor = reinterpret_cast<unsigned long long*>(L.e_key);
       KDB_CUDA(cudaMemsetAsync(cursor, 0, (N + 1) * sizeof(unsigned long long), st));
       if (R.n_rows > 0)
-        LAUNCH(k_in_count, grid_for(R.n_rows), kThreads, st, R.nbr, R.dist, R.n_rows, k, eps_run, R.row_begin, N,
+        LAUNCH(k_in_count, grid_for(R.n_rows), kThreads, st, R.nbr, R.dist, R.n_rows, ld, k, eps_run, R.row_begin, N,
                core_bits, cursor);
       cb = L.cub_bytes;
       { LaunchScope ls_("cub::DeviceScan", st, false); KDB_CUDA(cub::DeviceScan::ExclusiveSum(L.cub_tmp, cb, cursor, R.in_off, (int)(N + 1), st)); }
       KDB_CUDA(cudaMemcpyAsync(cursor, R.in_off, (N + 1) * sizeof(unsigned long long),
                                cudaMemcpyDeviceToDevice, st));
       if (R.n_rows > 0)
-        LAUNCH(k_in_fill, grid_for(R.n_rows), kThreads, st, R.nbr, R.dist, R.n_rows, k, eps_run, R.row_begin, N,
+        LAUNCH(k_in_fill, grid_for(R.n_rows), kThreads, st, R.nbr, R.dist, R.n_rows, ld, k, eps_run, R.row_begin, N,
                core_bits, cursor, R.in_src, R.in_w);
       LAUNCH(k_in_finish, grid_for(N), kThreads, st, R.in_off, N, R.in_len, R.in_act[0], &R.ctr->ni[0]);
       KDB_CUDA(cudaGetLastError());
@@ -2279,30 +2355,37 @@ kdb_status rows_phase(Mst& m, float eps_run) {
       uint32_t* nout = &R.ctr->na[cur ^ 1];
       if (na_ub[r] && R.compact) {
         if (direct)
-          LAUNCH(k_light_first, grid_for(na_ub[r]), kThreads, st, R.LE, R.nbr, R.dist, k, eps_run, R.row_begin, N,
+          LAUNCH(k_light_first, grid_for(na_ub[r]), kThreads, st, R.LE, R.nbr, R.dist, ld, k, eps_run, R.row_begin, N,
                  comp, L.all_core, R.act[cur], na_ub[r], R.act[cur ^ 1], nout, &R.ctr->grab, R.Kc, R.Bc, R.tgt,
                  &L.ctr->entries, nin);
         else
-          LAUNCH(k_light_round, grid_for(na_ub[r]), kThreads, st, R.LE, R.nbr, R.dist, k, eps_run, R.row_begin, N,
-                 comp, R.act[cur], na_ub[r], R.act[cur ^ 1], nout, &R.ctr->grab, R.offers,
-                 (unsigned long long*)R.Kc, &L.ctr->entries, nin);
+        {
+#define KDB_LR_LAUNCH(GW)                                                                                       \
+  LAUNCH(k_light_round<GW>, grid_for(na_ub[r]), kThreads, st, R.LE, R.nbr, R.dist, ld, k, eps_run, R.row_begin, N, \
+         comp, R.act[cur], na_ub[r], R.act[cur ^ 1], nout, &R.ctr->grab, R.offers, (unsigned long long*)R.Kc,      \
+         &L.ctr->entries, nin)
+          if (gw == 1) KDB_LR_LAUNCH(1);
+          else if (gw == 2) KDB_LR_LAUNCH(2);
+          else KDB_LR_LAUNCH(4);
+#undef KDB_LR_LAUNCH
+        }
       } else if (na_ub[r]) {
         if (direct) {
           if (vec)
-            LAUNCH(k_offer_first<true>, grid_for(na_ub[r]), kThreads, st, R.nbr, R.dist, k, eps_run, R.row_begin, N,
+            LAUNCH(k_offer_first<true>, grid_for(na_ub[r]), kThreads, st, R.nbr, R.dist, ld, k, eps_run, R.row_begin, N,
                    comp, L.all_core, R.act[cur], na_ub[r], R.act[cur ^ 1], nout, R.Kc, R.Bc, R.tgt,
                    &L.ctr->entries, nin);
           else
-            LAUNCH(k_offer_first<false>, grid_for(na_ub[r]), kThreads, st, R.nbr, R.dist, k, eps_run, R.row_begin,
+            LAUNCH(k_offer_first<false>, grid_for(na_ub[r]), kThreads, st, R.nbr, R.dist, ld, k, eps_run, R.row_begin,
                    N, comp, L.all_core, R.act[cur], na_ub[r], R.act[cur ^ 1], nout, R.Kc, R.Bc, R.tgt,
                    &L.ctr->entries, nin);
         } else {
           if (vec)
-            LAUNCH(k_offer_round<true>, grid_for(na_ub[r]), kThreads, st, R.nbr, R.dist, k, eps_run, R.row_begin, N,
+            LAUNCH(k_offer_round<true>, grid_for(na_ub[r]), kThreads, st, R.nbr, R.dist, ld, k, eps_run, R.row_begin, N,
                    comp, R.act[cur], na_ub[r], R.act[cur ^ 1], nout, R.offers, (unsigned long long*)R.Kc,
                    &L.ctr->entries, nin);
           else
-            LAUNCH(k_offer_round<false>, grid_for(na_ub[r]), kThreads, st, R.nbr, R.dist, k, eps_run, R.row_begin,
+            LAUNCH(k_offer_round<false>, grid_for(na_ub[r]), kThreads, st, R.nbr, R.dist, ld, k, eps_run, R.row_begin,
                    N, comp, R.act[cur], na_ub[r], R.act[cur ^ 1], nout, R.offers, (unsigned long long*)R.Kc,
                    &L.ctr->entries, nin);
         }
@@ -2395,7 +2478,7 @@ kdb_status rows_phase(Mst& m, float eps_run) {
         LAUNCH(k_fill_comp_arrays, grid_for(Cx), kThreads, st, Cx, L.ranks[r].Kc, L.ranks[r].Bc, nullptr);
       for (size_t r = 0; r < nr; ++r)
         if (na_x[r])
-          LAUNCH(k_sweep, grid_for(na_x[r]), kThreads, st, L.ranks[r].nbr, L.ranks[r].dist, k, eps_run,
+          LAUNCH(k_sweep, grid_for(na_x[r]), kThreads, st, L.ranks[r].nbr, L.ranks[r].dist, ld, k, eps_run,
                  L.ranks[r].row_begin, N, comp, L.ranks[r].act[cur], na_x[r], (unsigned long long*)L.ranks[r].Kc,
                  L.ranks[r].Bc, 0);
       for (size_t r = 1; r < nr; ++r)
@@ -2403,7 +2486,7 @@ kdb_status rows_phase(Mst& m, float eps_run) {
       KDB_TRY(allreduce_min_u64(comm, L.Kc, Cx, st));
       for (size_t r = 0; r < nr; ++r)
         if (na_x[r])
-          LAUNCH(k_sweep, grid_for(na_x[r]), kThreads, st, L.ranks[r].nbr, L.ranks[r].dist, k, eps_run,
+          LAUNCH(k_sweep, grid_for(na_x[r]), kThreads, st, L.ranks[r].nbr, L.ranks[r].dist, ld, k, eps_run,
                  L.ranks[r].row_begin, N, comp, L.ranks[r].act[cur], na_x[r], (unsigned long long*)L.Kc,
                  L.ranks[r].Bc, 1);
       for (size_t r = 1; r < nr; ++r)
@@ -2484,21 +2567,29 @@ kdb_status filter_phase(Mst& m, float eps, bool* overflow) {
     KDB_CUDA(cudaMemsetAsync(R.n_hs_dev, 0, 2 * sizeof(uint32_t), st));
     if (cap_env >= 0) R.hs_cap = (uint32_t)std::min<int64_t>(R.hs_cap, cap_env);
     if (R.n_rows == 0) continue;
-    const int vec = (m.k % 4) == 0 ? 4 : 1;
-    FastDiv fd;  // entry index within a tile -> row within the tile
-    fd.d = (uint64_t)m.k;
+    const int vec = (m.ld % 4) == 0 ? 4 : 1;
+    const bool cols = m.k < m.ld;  // edge_cols < row stride
+    FastDiv fd;  // entry (COLS: chunk) index within a tile -> row within the tile
+    fd.d = cols ? (uint64_t)((m.k + vec - 1) / vec) : (uint64_t)m.ld;
     fd.M = fd.d > 1 ? (~0ull / fd.d) + 1 : 0;
     fd.m32 = fd.d > 1 ? (uint32_t)((0xffffffffull / fd.d) + 1) : 0;
     fd.pad = 0;
     const int64_t ntiles = (R.n_rows + kFilterThreads - 1) / kFilterThreads;
     const int grid = (int)std::min<int64_t>(ntiles, 1 << 30);
-#define KDB_FILTER_LAUNCH(V, F)                                                                                  \
-  LAUNCH_DYN((k_filter<V, F>), grid, kFilterThreads, kFilterSmem, st, R.nbr, R.dist, R.n_rows, m.k, m.tau, eps,  \
-             R.row_begin, m.N, m.comp, rng, L.bloom, fd, R.hs[0], R.hs_cap, R.n_hs_dev, L.fcount + 1)
-    if (vec == 4 && fast) KDB_FILTER_LAUNCH(4, true);
-    else if (vec == 4) KDB_FILTER_LAUNCH(4, false);
-    else if (fast) KDB_FILTER_LAUNCH(1, true);
-    else KDB_FILTER_LAUNCH(1, false);
+#define KDB_FILTER_LAUNCH(V, F, CO)                                                                              \
+  LAUNCH_DYN((k_filter<V, F, CO>), grid, kFilterThreads, kFilterSmem, st, R.nbr, R.dist, R.n_rows, m.ld, m.k,      \
+             m.tau, eps, R.row_begin, m.N, m.comp, rng, L.bloom, fd, R.hs[0], R.hs_cap, R.n_hs_dev, L.fcount + 1)
+    if (cols) {
+      if (vec == 4 && fast) KDB_FILTER_LAUNCH(4, true, true);
+      else if (vec == 4) KDB_FILTER_LAUNCH(4, false, true);
+      else if (fast) KDB_FILTER_LAUNCH(1, true, true);
+      else KDB_FILTER_LAUNCH(1, false, true);
+    } else {
+      if (vec == 4 && fast) KDB_FILTER_LAUNCH(4, true, false);
+      else if (vec == 4) KDB_FILTER_LAUNCH(4, false, false);
+      else if (fast) KDB_FILTER_LAUNCH(1, true, false);
+      else KDB_FILTER_LAUNCH(1, false, false);
+    }
 #undef KDB_FILTER_LAUNCH
     KDB_CUDA(cudaGetLastError());
   }
@@ -2740,13 +2831,17 @@ kdb_status kdb_core_mark(const kdb_graph* g, int32_t M, float eps, uint32_t* cor
   return KDB_OK;
 }
 
+int32_t edge_cols_of(const kdb_graph* g) {
+  return (g->edge_cols > 0 && g->edge_cols < g->k_max) ? g->edge_cols : g->k_max;
+}
+
 size_t kdb_mst_workspace_bytes(const kdb_graph* g, kdb_comm* comm) {
   if (validate_graph(g) != KDB_OK) return 0;
   std::vector<int64_t> rb, rn;
   rank_ranges(g, comm, rb, rn);
   Layout L;
-  return carve(L, nullptr, true, g->n_total, (int)rb.size(), rb.data(), rn.data(),
-               !(g->flags & KDB_GRAPH_EXACT), g->k_max);
+  return carve(L, nullptr, true, g->n_total, (int)rb.size(), rb.data(), rn.data(), !(g->flags & KDB_GRAPH_EXACT),
+               edge_cols_of(g));
 }
 
 kdb_status kdb_mst(const kdb_graph* g, float eps, const uint32_t* core_bits, int32_t* comp,
@@ -2768,7 +2863,8 @@ kdb_status kdb_mst(const kdb_graph* g, float eps, const uint32_t* core_bits, int
   m.comm = comm;
   m.st = (cudaStream_t)stream;
   m.N = N;
-  m.k = g->k_max;
+  m.k = edge_cols_of(g);  // kernels stride rows by ld and take candidates from columns < k
+  m.ld = g->k_max;
   m.bits = core_bits;
   m.comp = comp;
   m.general = !(g->flags & KDB_GRAPH_EXACT);
@@ -2783,8 +2879,8 @@ kdb_status kdb_mst(const kdb_graph* g, float eps, const uint32_t* core_bits, int
   if (N == 0) return KDB_OK;
   cudaStream_t st = m.st;
   for (auto& R : L.ranks) {
-    R.nbr = g->nbr + (R.row_begin - g->row_begin) * m.k;
-    R.dist = g->dist + (R.row_begin - g->row_begin) * m.k;
+    R.nbr = g->nbr + (R.row_begin - g->row_begin) * m.ld;
+    R.dist = g->dist + (R.row_begin - g->row_begin) * m.ld;
   }
   for (auto& e : m.ev) KDB_CUDA(cudaEventCreate(&e));
   struct EvGuard {
@@ -2881,8 +2977,12 @@ kdb_status kdb_label(const kdb_graph* g, float eps, const uint32_t* core_bits, c
   if (g->n_rows > 0 && (!core_bits || !comp || !labels)) return set_err(KDB_EINVAL, "NULL device pointer");
   if (g->n_rows == 0) return KDB_OK;
   cudaStream_t st = (cudaStream_t)stream;
-  LAUNCH(k_label, grid_for(g->n_rows), kThreads, st, g->nbr, g->dist, g->n_rows, g->k_max, eps, g->row_begin,
-                                                    g->n_total, core_bits, comp, labels);
+  if (g->k_max % 4 == 0)
+    LAUNCH(k_label<true>, grid_for(g->n_rows * kLabelG), kThreads, st, g->nbr, g->dist, g->n_rows, g->k_max, eps,
+           g->row_begin, g->n_total, core_bits, comp, labels);
+  else
+    LAUNCH(k_label<false>, grid_for(g->n_rows * kLabelG), kThreads, st, g->nbr, g->dist, g->n_rows, g->k_max, eps,
+           g->row_begin, g->n_total, core_bits, comp, labels);
   KDB_CUDA(cudaGetLastError());
   if (g_prof.on) {
     KDB_CUDA(cudaStreamSynchronize(st));

@@ -13,6 +13,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import dataclasses
 from dataclasses import dataclass
 
 import torch
@@ -32,7 +33,7 @@ _lib = None
 class _Graph(C.Structure):
     _fields_ = [("n_total", C.c_int64), ("row_begin", C.c_int64), ("n_rows", C.c_int64),
                 ("k_max", C.c_int32), ("nbr", C.c_void_p), ("dist", C.c_void_p),
-                ("flags", C.c_uint32)]
+                ("flags", C.c_uint32), ("edge_cols", C.c_int32)]
 
 
 def lib():
@@ -132,12 +133,16 @@ class Comm:
 
 @dataclass
 class Graph:
-    """This rank's rows of the kNN graph (device tensors, [n_rows, k])."""
+    """This rank's rows of the kNN graph (device tensors, [n_rows, k]).
+
+    edge_cols: candidate edges come from the first edge_cols columns of each
+    row (0 = all k, reading #3; M = Def. 6's direct M-reachability)."""
     nbr: torch.Tensor
     dist: torch.Tensor
     n_total: int
     row_begin: int = 0
     exact: bool = False
+    edge_cols: int = 0
 
     def __post_init__(self):
         if self.nbr.dtype != torch.int32 or self.dist.dtype != torch.float32:
@@ -160,7 +165,7 @@ class Graph:
     def c(self) -> _Graph:
         return _Graph(int(self.n_total), int(self.row_begin), self.n_rows, self.k,
                       self.nbr.data_ptr(), self.dist.data_ptr(),
-                      KDB_GRAPH_EXACT if self.exact else 0)
+                      KDB_GRAPH_EXACT if self.exact else 0, int(self.edge_cols))
 
 
 def _h(comm):
@@ -259,12 +264,33 @@ def profile_read() -> dict:
     return {nm[i]: (ms[i], int(cnt[i])) for i in range(n)}
 
 
-def kdbscan(g: Graph, M: int, eps: float, comm: Comm | None = None, stream=None):
-    """The whole clustering stage (Alg. 1): returns (core_bits, MstResult, labels)."""
+def kdbscan(g: Graph, M: int, eps: float, comm: Comm | None = None, stream=None, edge_cols: int | None = None,
+            workspace: torch.Tensor | None = None):
+    """The whole clustering stage (Alg. 1): returns (core_bits, MstResult, labels).
+    edge_cols overrides g.edge_cols (M = the paper's Def. 6 edge set)."""
+    if edge_cols is not None:
+        g = dataclasses.replace(g, edge_cols=int(edge_cols))
     bits = core_mark(g, M, eps, comm, stream)
-    r = mst(g, eps, bits, comm, stream)
+    r = mst(g, eps, bits, comm, stream, workspace=workspace)
     lab = label(g, eps, bits, r.comp, stream)
     return bits, r, lab
+
+
+def kdbscan_sweep(g: Graph, M: int, eps_values, comm: Comm | None = None, stream=None,
+                  edge_cols: int | None = None):
+    """Multi-eps sweep on ONE resident graph (Fig. eps_mnist protocol, PAPER.md:
+    459-488: the kNN graph is built once and reused for every eps): one
+    workspace, the three calls per eps.  Returns [(eps, core_bits, MstResult,
+    labels)] in the order given."""
+    if edge_cols is not None:
+        g = dataclasses.replace(g, edge_cols=int(edge_cols))
+    nws = workspace_bytes(g, comm)
+    ws = torch.empty(max(nws, 256), dtype=torch.uint8, device=g.dist.device)
+    out = []
+    for eps in eps_values:
+        bits, r, lab = kdbscan(g, M, eps, comm, stream, workspace=ws)
+        out.append((float(eps), bits, r, lab))
+    return out
 
 
 def unpack_core(bits: torch.Tensor, n: int) -> torch.Tensor:

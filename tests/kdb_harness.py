@@ -11,13 +11,16 @@ import paper_2009_04552_b200 as kdb
 
 
 def run_gpu(nbr: np.ndarray, dist: np.ndarray, M: int, eps, *, exact: bool = False,
-            comm: "kdb.Comm | None" = None, device: str = "cuda:0"):
+            comm: "kdb.Comm | None" = None, device: str = "cuda:0", edge_cols: int = 0):
     g = kdb.Graph(torch.from_numpy(np.ascontiguousarray(nbr, np.int32)).to(device),
                   torch.from_numpy(np.ascontiguousarray(dist, np.float32)).to(device),
-                  n_total=nbr.shape[0], exact=exact)
+                  n_total=nbr.shape[0], exact=exact, edge_cols=edge_cols)
     bits, r, lab = kdb.kdbscan(g, M, float(np.float32(eps)), comm=comm)
     torch.cuda.synchronize()
-    n = nbr.shape[0]
+    return result_dict(bits, r, lab, nbr.shape[0])
+
+
+def result_dict(bits, r, lab, n):
     return dict(core=kdb.unpack_core(bits, n).numpy(), comp=r.comp.cpu().numpy(),
                 msf_a=r.a.cpu().numpy().astype(np.uint32), msf_b=r.b.cpu().numpy().astype(np.uint32),
                 msf_w=r.w.cpu().numpy(), msf_weight=r.weight, labels=lab.cpu().numpy(), stats=r.stats)
@@ -41,5 +44,5 @@ def assert_parity(got: dict, exp: dict, rel_tol: float = 1e-6):
         f"MSF weight {got['msf_weight']!r} vs {ew!r}"
 
 
-def oracle_run(nbr, dist, M, eps):
-    return oracle.kdbscan(nbr, dist, M, np.float32(eps))
+def oracle_run(nbr, dist, M, eps, edge_cols=None):
+    return oracle.kdbscan(nbr, dist, M, np.float32(eps), edge_cols=edge_cols or None)

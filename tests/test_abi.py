@@ -47,9 +47,9 @@ def test_library_exports_every_declared_symbol(lib):
         assert re.search(rf"\bT {f}$", out, flags=re.M), f
 
 
-def _graph(n_total=10, row_begin=0, n_rows=10, k=4, nbr=0x1000, dist=0x2000, flags=0):
+def _graph(n_total=10, row_begin=0, n_rows=10, k=4, nbr=0x1000, dist=0x2000, flags=0, edge_cols=0):
     import paper_2009_04552_b200.kdb as K
-    return K._Graph(n_total, row_begin, n_rows, k, nbr, dist, flags)
+    return K._Graph(n_total, row_begin, n_rows, k, nbr, dist, flags, edge_cols)
 
 
 @pytest.mark.parametrize("kw,M,eps", [
@@ -64,6 +64,8 @@ def _graph(n_total=10, row_begin=0, n_rows=10, k=4, nbr=0x1000, dist=0x2000, fla
     (dict(nbr=0), 2, 0.5),                 # NULL
     (dict(dist=0x2004), 2, 0.5),           # misaligned
     (dict(flags=8), 2, 0.5),               # unknown flag
+    (dict(edge_cols=-1), 2, 0.5),          # edge_cols < 0
+    (dict(edge_cols=5), 2, 0.5),           # edge_cols > k
 ])
 def test_core_mark_validation(lib, kw, M, eps):
     g = _graph(**kw)
@@ -89,6 +91,18 @@ def test_mst_validation_and_workspace(lib):
                      None, None, P(0x1000), 1 << 40, None, None)
     assert rc == 1
     assert lib.kdb_status_string(2) == b"KDB_ENOMEM"
+
+
+def test_edge_cols_workspace(lib):
+    """edge_cols = k is the default; edge_cols < k needs no extra workspace (the
+    kernels read the first edge_cols columns in place, kdb.h); the general-mode
+    in-edge lists shrink with it."""
+    ws = lambda **kw: lib.kdb_mst_workspace_bytes(C.byref(_graph(n_total=1000, n_rows=1000, k=32, **kw)), None)
+    assert ws(edge_cols=32) == ws(edge_cols=0)
+    assert ws(edge_cols=8) < ws(edge_cols=0)
+    wx = lambda **kw: lib.kdb_mst_workspace_bytes(C.byref(_graph(n_total=1000, n_rows=1000, k=32, flags=1, **kw)), None)
+    assert wx(edge_cols=8) <= wx(edge_cols=0)
+    assert lib.kdb_mst_workspace_bytes(C.byref(_graph(edge_cols=9)), None) == 0  # invalid -> 0
 
 
 def test_sim_comm_lifecycle(lib):

@@ -40,8 +40,8 @@ def _workload(name, scale=1.0):
     return nbr, dist, cfg["M"], eps
 
 
-def _gpu(nbr, dist, M, eps, exact=True, comm=None):
-    g = kdb.Graph(nbr, dist, n_total=nbr.shape[0], exact=exact)
+def _gpu(nbr, dist, M, eps, exact=True, comm=None, edge_cols=0):
+    g = kdb.Graph(nbr, dist, n_total=nbr.shape[0], exact=exact, edge_cols=edge_cols)
     bits, r, lab = kdb.kdbscan(g, M, eps, comm=comm)
     torch.cuda.synchronize()
     n = nbr.shape[0]
@@ -57,6 +57,33 @@ def test_config_full_oracle_parity(name):
     got = _gpu(nbr, dist, M, eps)
     exp = oracle_run(nbr.cpu().numpy(), dist.cpu().numpy(), M, eps)
     assert_parity(got, exp)
+
+
+def test_config_c2_edge_cols_M():
+    """C2 at full size with the paper's Def. 6 edge set (edge_cols = M)."""
+    nbr, dist, M, eps = _workload("C2")
+    got = _gpu(nbr, dist, M, eps, edge_cols=M)
+    exp = oracle_run(nbr.cpu().numpy(), dist.cpu().numpy(), M, eps, edge_cols=M)
+    assert_parity(got, exp)
+
+
+def test_config_c4_edge_cols_M():
+    """C4 at full size, edge_cols = M: properties on every vertex/edge, MSF edges
+    drawn from the first M columns, and bit-identical to the unfiltered path."""
+    nbr, dist, M, eps = _workload("C4")
+    got = _gpu(nbr, dist, M, eps, edge_cols=M)
+    _check_properties(nbr, dist, M, eps, got)
+    a = torch.from_numpy(got["msf_a"].astype(np.int64)).cuda()
+    b = torch.from_numpy(got["msf_b"].astype(np.int64)).cuda()
+    inrow = (nbr[a, :M].long() == b[:, None]).any(1) | (nbr[b, :M].long() == a[:, None]).any(1)
+    assert bool(inrow.all())
+    os.environ["KDB_FILTER"] = "0"
+    try:
+        alt = _gpu(nbr, dist, M, eps, edge_cols=M)
+    finally:
+        del os.environ["KDB_FILTER"]
+    for key in ("core", "comp", "labels", "msf_a", "msf_b", "msf_w"):
+        assert np.array_equal(got[key], alt[key]), key
 
 
 def _masked_prefix(nbr, dist, ns):
