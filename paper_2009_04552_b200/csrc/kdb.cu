@@ -162,11 +162,6 @@ struct Prof {
 };
 Prof g_prof;
 const int g_trace = getenv("KDB_TRACE") ? atoi(getenv("KDB_TRACE")) : 0;  // per-round log to stderr
-const int g_fa = getenv("KDB_FA") ? atoi(getenv("KDB_FA")) : 1;  // first block lines, awake rows
-const int g_fs = getenv("KDB_FS") ? atoi(getenv("KDB_FS")) : 4;  // first block lines, woken rows
-const int g_lazy = getenv("KDB_LAZY") ? atoi(getenv("KDB_LAZY")) : 1;
-const int g_qmax = getenv("KDB_QMAX") ? atoi(getenv("KDB_QMAX")) : 1;
-const uint32_t g_chunk = getenv("KDB_CHUNK") ? (uint32_t)atoi(getenv("KDB_CHUNK")) : (1u << 30);
 
 struct LaunchScope {
   const char* name;
