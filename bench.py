@@ -326,6 +326,15 @@ def run_ours(args):
     value = N * k * F / (ms * 1e-3)
     n_clusters = int(torch.unique(r.comp[r.comp >= 0]).numel()) if rank == 0 else None
     msf_count, msf_weight = r.count, r.weight
+    # clustering quality against the generator's ground truth (outside the timed
+    # region): kdb_nmi on the device
+    quality = None
+    if world == 1 and W.get("truth") is not None:
+        truth = torch.from_numpy(np.ascontiguousarray(W["truth"], np.int32)).to(dev)
+        v_nmi, n_cl, n_truth = kdb.nmi(lb[:N].contiguous(), truth)
+        quality = {"nmi": v_nmi, "clusters": n_cl, "truth_clusters": n_truth,
+                   "convention": "SPEC.md:421-431 (2I/(H(A)+H(B)), noise = one pseudo-cluster)"}
+        del truth
 
     # ---- e2e: host buffers through the public API ---------------------------------
     e2e = None
@@ -381,7 +390,7 @@ def run_ours(args):
                 "roofline": roof,
                 "stage_roofline": {"t_min_ms": t_min_ms, "frac": t_min_ms / ms,
                                    "bytes": "8 N k + 4 N + N/8 (SURVEY.md 8(d))", "peak": peak},
-                "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+                "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "quality": quality,
                 "clocks": clk, "kernels": kernels,
                 "mst": {"edges": msf_count, "weight": msf_weight, "clusters": n_clusters,
                         "rounds": stats[-1]["rounds"], "stall_rounds": stats[-1]["stall_rounds"],

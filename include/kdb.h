@@ -149,6 +149,23 @@ kdb_status kdb_mst(const kdb_graph* g, float eps, const uint32_t* core_bits, int
 kdb_status kdb_label(const kdb_graph* g, float eps, const uint32_t* core_bits, const int32_t* comp,
                      int32_t* labels, kdb_stream_t stream);
 
+/* Clustering quality.  The paper reports NMI
+ * ("normalized mutual information ... almost one", PAPER.md:340,
+ * 389) without a formula; the convention is SPEC.md:421-431:
+ *   NMI(A, B) = 2 I(A;B) / (H(A) + H(B)), natural log, over the joint label
+ *   histogram, every NOISE (-1) point in ONE shared pseudo-cluster per
+ *   labelling; both entropies 0 -> 1; exactly one entropy 0 -> 0.
+ *   clusters_a/_b: the number of distinct non-NOISE labels.
+ * a, b: device int32[n] labels (>= -1; any values, e.g. kdb_label output and a
+ * generator's ground truth).  nmi, clusters_a, clusters_b: host outputs.
+ * workspace: device, >= kdb_nmi_workspace_bytes(n) bytes, 256-B aligned.
+ * EINVAL: NULL pointers, n outside [0, 2^31-1), a label < -1.  ENOMEM: small
+ * workspace.  Synchronises `stream`; n = 0 gives nmi = 1, no clusters. */
+size_t kdb_nmi_workspace_bytes(int64_t n);
+kdb_status kdb_nmi(const int32_t* a, const int32_t* b, int64_t n, double* nmi /* host */,
+                   int64_t* clusters_a /* host */, int64_t* clusters_b /* host */, void* workspace,
+                   size_t ws_bytes, kdb_stream_t stream);
+
 /* Per-phase device times (ms) and counters of the most recent kdb_mst call on
  * this thread: out[0] = rounds, out[1] = init/sweep ms, out[2] = min-edge ms
  * (offer + tie + exchange), out[3] = hook/jump/relabel ms, out[4] = finalize ms,

@@ -40,6 +40,8 @@
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 #include <cub/device/device_select.cuh>
+#include <cub/device/device_reduce.cuh>
+#include <cub/device/device_run_length_encode.cuh>
 #include <thrust/iterator/transform_iterator.h>
 
 #include <algorithm>
@@ -1513,12 +1515,17 @@ constexpr size_t kFilterSmem = kBloomBits / 8;
 // Blocked Bloom filter: key x selects ONE 32-bit word (top 15 bits of x*C1)
 // and sets 3 bits in it (three 5-bit fields of x*C2): a single shared-memory
 // probe per test, false-positive rate ~1e-4 at ~2e4 keys.
-__device__ __forceinline__ uint32_t bloom_word(uint32_t x) { return (x * 0x9E3779B1u) >> 17; }
-__device__ __forceinline__ uint32_t bloom_mask(uint32_t x) {
-  const uint32_t h = x * 0x85EBCA77u;
-  // 1 << (s & 31) as one funnel shift (SHF.L.W wraps the amount)
-  return __funnelshift_l(0u, 1u, h >> 27) | __funnelshift_l(0u, 1u, h >> 22) | __funnelshift_l(0u, 1u, h >> 17);
+// One multiplicative hash h = x * phi serves both: the word from its top 15
+// bits, the three bit positions from bits [0,5), [5,10), [10,15) (the low bits
+// of h are a bijection of the low bits of x, independent of the word choice).
+// 1 << (s & 31) is one funnel shift (SHF.L.W wraps the amount).
+__device__ __forceinline__ uint32_t bloom_hash(uint32_t x) { return x * 0x9E3779B1u; }
+__device__ __forceinline__ uint32_t bloom_word_h(uint32_t h) { return h >> 17; }
+__device__ __forceinline__ uint32_t bloom_mask_h(uint32_t h) {
+  return __funnelshift_l(0u, 1u, h) | __funnelshift_l(0u, 1u, h >> 5) | __funnelshift_l(0u, 1u, h >> 10);
 }
+__device__ __forceinline__ uint32_t bloom_word(uint32_t x) { return bloom_word_h(bloom_hash(x)); }
+__device__ __forceinline__ uint32_t bloom_mask(uint32_t x) { return bloom_mask_h(bloom_hash(x)); }
 
 // dom[blk]: majority component among 32 sampled vertices of the id block (-1 if none is core)
 __global__ void k_dom(const int32_t* __restrict__ comp, int64_t N, int shift, int64_t nblk,
@@ -1583,7 +1590,7 @@ struct FastDiv {
   uint64_t M;
   uint64_t d;
   uint32_t m32;  // ceil(2^32 / d): n / d == umulhi(n, m32) for n < 2^32 / d
-  uint32_t pad;
+  uint32_t small;  // 1 < d < 2048: the 32-bit path is exact for the tile's indices
 };
 __device__ __forceinline__ uint64_t fdiv(uint64_t q, const FastDiv& f) { return f.d == 1 ? q : __umul64hi(q, f.M); }
 
@@ -1650,7 +1657,7 @@ __global__ void __launch_bounds__(kFilterThreads) k_filter(
         const uint32_t u = base + t * blockDim.x + threadIdx.x;
         uint32_t off = u;  // chunk offset from the tile start
         if (COLS && u < n_chunks) {
-          const uint32_t lr = (fd.d > 1 && fd.d < 2048) ? __umulhi(u, fd.m32) : (uint32_t)fdiv(u, fd);
+          const uint32_t lr = fd.small ? __umulhi(u, fd.m32) : (uint32_t)fdiv(u, fd);
           off = lr * (uint32_t)(ld / VEC) + (u - lr * cpr);
         }
         if (VEC == 4) {
@@ -1668,12 +1675,12 @@ __global__ void __launch_bounds__(kFilterThreads) k_filter(
         float w[VEC];
         if (u < n_chunks) {
           if (COLS) {
-            lr = (fd.d > 1 && fd.d < 2048) ? __umulhi(u, fd.m32) : (uint32_t)fdiv(u, fd);  // row within the tile
+            lr = fd.small ? __umulhi(u, fd.m32) : (uint32_t)fdiv(u, fd);  // row within the tile
             col = (u - lr * cpr) * VEC;
             off = lr * (uint32_t)(ld / VEC) + (u - lr * cpr);
           } else {
             const uint32_t n = u * VEC;
-            lr = (fd.d > 1 && fd.d < 2048) ? __umulhi(n, fd.m32) : (uint32_t)fdiv(n, fd);  // row within the tile
+            lr = fd.small ? __umulhi(n, fd.m32) : (uint32_t)fdiv(n, fd);  // row within the tile
             col = n - lr * (uint32_t)ld;
           }
           const FRow fr = s_row[lr];
@@ -1688,9 +1695,10 @@ __global__ void __launch_bounds__(kFilterThreads) k_filter(
             uint32_t fast = 0;
             if (FAST) {
               const uint32_t Jj = (uint32_t)J[t][j];
+              const uint32_t hh = bloom_hash(Jj);
               uint32_t word;
-              asm("ld.shared.u32 %0, [%1];" : "=r"(word) : "r"(s_base + bloom_word(Jj) * 4u));
-              const uint32_t bm = bloom_mask(Jj);
+              asm("ld.shared.u32 %0, [%1];" : "=r"(word) : "r"(s_base + bloom_word_h(hh) * 4u));
+              const uint32_t bm = bloom_mask_h(hh);
               fast = (uint32_t)((Jj - fr.lo) < fr.span) & (uint32_t)((word & bm) != bm);
             }
             slowm |= ((fast & 1u) ^ 1u) << j;
@@ -2568,7 +2576,7 @@ kdb_status filter_phase(Mst& m, float eps, bool* overflow) {
     fd.d = cols ? (uint64_t)((m.k + vec - 1) / vec) : (uint64_t)m.ld;
     fd.M = fd.d > 1 ? (~0ull / fd.d) + 1 : 0;
     fd.m32 = fd.d > 1 ? (uint32_t)((0xffffffffull / fd.d) + 1) : 0;
-    fd.pad = 0;
+    fd.small = (fd.d > 1 && fd.d < 2048) ? 1u : 0u;
     const int64_t ntiles = (R.n_rows + kFilterThreads - 1) / kFilterThreads;
     const int grid = (int)std::min<int64_t>(ntiles, 1 << 30);
 #define KDB_FILTER_LAUNCH(V, F, CO)                                                                              \
@@ -2983,6 +2991,182 @@ kdb_status kdb_label(const kdb_graph* g, float eps, const uint32_t* core_bits, c
     KDB_CUDA(cudaStreamSynchronize(st));
     g_prof.drain();
   }
+  return KDB_OK;
+}
+
+
+// ============================================================================
+// Clustering quality: NMI and cluster counts
+// ============================================================================
+// NMI = 2 I / (H(A) + H(B)) with NOISE as one pseudo-cluster per labelling
+// (the paper reports NMI without a formula).
+// With S_x = sum over the cells of a histogram of n ln n:
+//   H(A) = ln N - S_a / N,  I = (S_ab + N ln N - S_a - S_b) / N.
+// The histograms are run lengths of sorted keys (label + 1: NOISE -> 0).
+}  // extern "C"
+namespace {
+__global__ void k_nmi_keys(const int32_t* __restrict__ a, const int32_t* __restrict__ b, int64_t n, int bb,
+                           uint64_t* __restrict__ pk, uint32_t* __restrict__ ka, uint32_t* __restrict__ kb) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t x = (uint32_t)(a[i] + 1), y = (uint32_t)(b[i] + 1);
+    pk[i] = ((uint64_t)x << bb) | y;
+    ka[i] = x;
+    kb[i] = y;
+  }
+}
+// f[i] = c ln c for the run lengths c of one histogram
+__global__ void k_nlogn(const int32_t* __restrict__ cnt, const int32_t* __restrict__ n_runs, double* __restrict__ out) {
+  const int m = *n_runs;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
+    const double c = (double)cnt[i];
+    out[i] = c * log(c);
+  }
+}
+struct NmiWs {
+  uint64_t *k0, *k1, *uniq;
+  int32_t* cnt;
+  double* f;
+  int32_t* runs;
+  double* sum;
+  int32_t* mm;  // min a, max a, min b, max b
+  void* tmp;
+  size_t tmp_bytes;
+};
+size_t nmi_carve(NmiWs& w, char* base, bool dry, int64_t n) {
+  Carver cv{base, 0, 0, dry};
+  const int64_t m = std::max<int64_t>(n, 1);
+  w.k0 = cv.take<uint64_t>(m);
+  w.k1 = cv.take<uint64_t>(m);
+  w.uniq = cv.take<uint64_t>(m);
+  w.cnt = cv.take<int32_t>(m);
+  w.f = cv.take<double>(m);
+  w.runs = cv.take<int32_t>(4);
+  w.sum = cv.take<double>(4);
+  w.mm = cv.take<int32_t>(4);
+  size_t t = 0, x = 0;
+  const int ni = (int)m;
+  cub::DeviceRadixSort::SortKeys(nullptr, x, (const uint64_t*)nullptr, (uint64_t*)nullptr, ni);
+  t = std::max(t, x);
+  cub::DeviceRadixSort::SortKeys(nullptr, x, (const uint32_t*)nullptr, (uint32_t*)nullptr, ni);
+  t = std::max(t, x);
+  cub::DeviceRunLengthEncode::Encode(nullptr, x, (const uint64_t*)nullptr, (uint64_t*)nullptr, (int32_t*)nullptr,
+                                     (int32_t*)nullptr, ni);
+  t = std::max(t, x);
+  cub::DeviceRunLengthEncode::Encode(nullptr, x, (const uint32_t*)nullptr, (uint32_t*)nullptr, (int32_t*)nullptr,
+                                     (int32_t*)nullptr, ni);
+  t = std::max(t, x);
+  cub::DeviceReduce::Sum(nullptr, x, (const double*)nullptr, (double*)nullptr, ni);
+  t = std::max(t, x);
+  cub::DeviceReduce::Min(nullptr, x, (const int32_t*)nullptr, (int32_t*)nullptr, ni);
+  t = std::max(t, x);
+  cub::DeviceReduce::Max(nullptr, x, (const int32_t*)nullptr, (int32_t*)nullptr, ni);
+  t = std::max(t, x);
+  w.tmp_bytes = t;
+  w.tmp = cv.take<char>(t);
+  return cv.off + 256;
+}
+int bits_for(uint64_t v) {
+  int b = 1;
+  while (b < 64 && (v >> b)) ++b;
+  return b;
+}
+// run lengths of the sorted keys (T = u32 / u64) -> w.cnt, their count -> w.runs[slot], c ln c -> w.f
+template <typename T>
+kdb_status nmi_hist(NmiWs& w, const T* sorted, int64_t n, int slot, cudaStream_t st) {
+  size_t tb = w.tmp_bytes;
+  {
+    LaunchScope ls_("cub::DeviceRunLengthEncode", st, false);
+    KDB_CUDA(cub::DeviceRunLengthEncode::Encode(w.tmp, tb, sorted, reinterpret_cast<T*>(w.uniq), w.cnt,
+                                                w.runs + slot, (int)n, st));
+  }
+  LAUNCH(k_nlogn, grid_for(n), kThreads, st, w.cnt, w.runs + slot, w.f);
+  KDB_CUDA(cudaGetLastError());
+  return KDB_OK;
+}
+}  // namespace
+extern "C" {
+
+size_t kdb_nmi_workspace_bytes(int64_t n) {
+  if (n < 0 || n >= (int64_t)INT32_MAX) return 0;
+  NmiWs w;
+  return nmi_carve(w, nullptr, true, n);
+}
+
+kdb_status kdb_nmi(const int32_t* a, const int32_t* b, int64_t n, double* nmi, int64_t* clusters_a,
+                   int64_t* clusters_b, void* workspace, size_t ws_bytes, kdb_stream_t stream) {
+  if (!nmi || !clusters_a || !clusters_b) return set_err(KDB_EINVAL, "NULL host output");
+  if (n < 0 || n >= (int64_t)INT32_MAX) return set_err(KDB_EINVAL, "n out of range [0, 2^31-1)");
+  if (n > 0 && (!a || !b || !workspace)) return set_err(KDB_EINVAL, "NULL device pointer");
+  if ((uintptr_t)workspace & 255u) return set_err(KDB_EINVAL, "workspace must be 256-byte aligned");
+  NmiWs w;
+  const size_t need = nmi_carve(w, (char*)workspace, false, n);
+  if (n > 0 && ws_bytes < need) return set_err(KDB_ENOMEM, "workspace %zu < required %zu bytes", ws_bytes, need);
+  *nmi = 1.0;
+  *clusters_a = *clusters_b = 0;
+  if (n == 0) return KDB_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int ni = (int)n;
+  size_t tb = w.tmp_bytes;
+  {
+    LaunchScope ls_("cub::DeviceReduce", st, false);
+    KDB_CUDA(cub::DeviceReduce::Min(w.tmp, tb, a, w.mm + 0, ni, st));
+    KDB_CUDA(cub::DeviceReduce::Max(w.tmp, tb, a, w.mm + 1, ni, st));
+    KDB_CUDA(cub::DeviceReduce::Min(w.tmp, tb, b, w.mm + 2, ni, st));
+    KDB_CUDA(cub::DeviceReduce::Max(w.tmp, tb, b, w.mm + 3, ni, st));
+  }
+  int32_t mm[4];
+  KDB_CUDA(cudaMemcpyAsync(mm, w.mm, sizeof(mm), cudaMemcpyDeviceToHost, st));
+  KDB_CUDA(cudaStreamSynchronize(st));
+  if (mm[0] < -1 || mm[2] < -1) return set_err(KDB_EINVAL, "labels must be >= -1 (NOISE)");
+  const int ba = bits_for((uint64_t)mm[1] + 1), bb = bits_for((uint64_t)mm[3] + 1);
+  // pair keys -> k0; a + 1 -> f (first n u32); b + 1 -> f (next n u32)
+  uint32_t* sa = reinterpret_cast<uint32_t*>(w.f);
+  uint32_t* sb = sa + n;
+  LAUNCH(k_nmi_keys, grid_for(n), kThreads, st, a, b, n, bb, w.k0, sa, sb);
+  KDB_CUDA(cudaGetLastError());
+  double S[3];
+  int32_t runs[3];
+  uint32_t first[3];
+  for (int pass = 0; pass < 3; ++pass) {
+    tb = w.tmp_bytes;
+    if (pass == 0) {
+      {
+        LaunchScope ls_("cub::DeviceRadixSort", st, false);
+        KDB_CUDA(cub::DeviceRadixSort::SortKeys(w.tmp, tb, w.k0, w.k1, ni, 0, std::min(64, ba + bb), st));
+      }
+      // the single-label keys move to k0 (free now) before f is overwritten
+      KDB_CUDA(cudaMemcpyAsync(w.k0, sa, 2 * n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st));
+      KDB_TRY(nmi_hist<uint64_t>(w, w.k1, n, 0, st));
+    } else {
+      uint32_t* src = reinterpret_cast<uint32_t*>(w.k0) + (pass == 1 ? 0 : n);
+      uint32_t* dst = reinterpret_cast<uint32_t*>(w.k1);
+      {
+        LaunchScope ls_("cub::DeviceRadixSort", st, false);
+        KDB_CUDA(cub::DeviceRadixSort::SortKeys(w.tmp, tb, src, dst, ni, 0, pass == 1 ? ba : bb, st));
+      }
+      KDB_TRY(nmi_hist<uint32_t>(w, dst, n, pass, st));
+    }
+    KDB_CUDA(cudaMemcpyAsync(&runs[pass], w.runs + pass, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    KDB_CUDA(cudaMemcpyAsync(&first[pass], w.uniq, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    KDB_CUDA(cudaStreamSynchronize(st));
+    tb = w.tmp_bytes;
+    {
+      LaunchScope ls_("cub::DeviceReduce", st, false);
+      KDB_CUDA(cub::DeviceReduce::Sum(w.tmp, tb, w.f, w.sum + pass, runs[pass], st));
+    }
+    KDB_CUDA(cudaMemcpyAsync(&S[pass], w.sum + pass, sizeof(double), cudaMemcpyDeviceToHost, st));
+    KDB_CUDA(cudaStreamSynchronize(st));
+  }
+  const double N = (double)n, lnN = log(N);
+  const double Ha = lnN - S[1] / N, Hb = lnN - S[2] / N;
+  const double I = (S[0] + N * lnN - S[1] - S[2]) / N;
+  const bool za = runs[1] == 1, zb = runs[2] == 1;  // a single cell: zero entropy (exactly)
+  if (za && zb) *nmi = 1.0;
+  else if (za || zb) *nmi = 0.0;
+  else *nmi = std::min(1.0, std::max(0.0, 2.0 * I / (Ha + Hb)));
+  // the smallest key is NOISE + 1 = 0 iff the labelling has noise
+  *clusters_a = runs[1] - (first[1] == 0u ? 1 : 0);
+  *clusters_b = runs[2] - (first[2] == 0u ? 1 : 0);
   return KDB_OK;
 }
 

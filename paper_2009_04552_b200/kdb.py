@@ -55,6 +55,9 @@ def lib():
     L.kdb_comm_destroy.argtypes = [P]
     L.kdb_comm_destroy.restype = None
     L.kdb_core_mark.argtypes = [G, i32, f32, P, P, P]
+    L.kdb_nmi_workspace_bytes.argtypes = [i64]
+    L.kdb_nmi_workspace_bytes.restype = C.c_size_t
+    L.kdb_nmi.argtypes = [P, P, i64, C.POINTER(C.c_double), C.POINTER(i64), C.POINTER(i64), P, C.c_size_t, P]
     L.kdb_mst_workspace_bytes.argtypes = [G, P]
     L.kdb_mst_workspace_bytes.restype = C.c_size_t
     L.kdb_mst.argtypes = [G, f32, P, P, P, P, P, i64, C.POINTER(i64), C.POINTER(C.c_double), P,
@@ -74,7 +77,7 @@ def lib():
 EXPORTS = sorted(["kdb_nccl_unique_id", "kdb_comm_create_nccl", "kdb_comm_create_sim", "kdb_comm_destroy",
                   "kdb_core_mark", "kdb_mst_workspace_bytes", "kdb_mst", "kdb_label", "kdb_last_mst_stats",
                   "kdb_profile_enable", "kdb_profile_reset", "kdb_launch_count", "kdb_profile_read",
-                  "kdb_status_string", "kdb_last_error"])
+                  "kdb_status_string", "kdb_last_error", "kdb_nmi_workspace_bytes", "kdb_nmi"])
 
 
 def _check(rc: int, what: str):
@@ -238,6 +241,22 @@ def label(g: Graph, eps: float, core_bits: torch.Tensor, comp: torch.Tensor, str
                            C.c_void_p(comp.data_ptr()), C.c_void_p(labels.data_ptr()), _stream(stream)),
            "kdb_label")
     return labels[:g.n_rows]
+
+
+def nmi(a: torch.Tensor, b: torch.Tensor, stream=None) -> tuple[float, int, int]:
+    """kdb_nmi: (NMI, clusters in a, clusters in b) of two device int32 labellings
+    (SPEC.md convention: NOISE = one pseudo-cluster; arithmetic-mean normalisation)."""
+    if a.dtype != torch.int32 or b.dtype != torch.int32 or a.shape != b.shape or a.dim() != 1:
+        raise KdbError("a, b must be 1-D int32 tensors of equal length")
+    if not (a.is_cuda and b.is_cuda):
+        raise KdbError("a, b must be CUDA tensors (there is no CPU path)")
+    a = a.contiguous(); b = b.contiguous()
+    n = int(a.numel())
+    ws = torch.empty(max(int(lib().kdb_nmi_workspace_bytes(n)), 256), dtype=torch.uint8, device=a.device)
+    v = C.c_double(0.0); ca = C.c_int64(0); cb = C.c_int64(0)
+    _check(lib().kdb_nmi(C.c_void_p(a.data_ptr()), C.c_void_p(b.data_ptr()), n, C.byref(v), C.byref(ca),
+                         C.byref(cb), C.c_void_p(ws.data_ptr()), ws.numel(), _stream(stream)), "kdb_nmi")
+    return v.value, ca.value, cb.value
 
 
 def profile(on: bool = True):

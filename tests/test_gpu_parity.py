@@ -373,3 +373,4 @@ def test_round1_fused_into_ell(c1_graph, fuse, pack, P, monkeypatch):
         got = run_gpu(nbr, dist, M, eps, exact=True, comm=kdb.Comm.sim(P) if P else None)
         assert_parity(got, oracle_run(nbr, dist, M, eps))
 
+

@@ -8,6 +8,6 @@ python bench.py $ARGS > gpurun_out/plain_${TAG}.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_${TAG}.csv \
     python bench.py $ARGS > gpurun_out/ncu_launches_${TAG}.log 2>&1
 echo "ncu launches rc=$?"
-ncu --set full --clock-control none --import-source on -k regex:"k_filter|k_light_ell|k_light_round|k_hook" -s 0 -c 5 \
+ncu --set full --clock-control none --import-source on -k regex:"k_filter|k_light_ell|k_light_round|k_hook|k_label|k_core_mark" -s 0 -c 8 \
     -o gpurun_out/prof_${TAG} python bench.py $ARGS > gpurun_out/ncu_full_${TAG}.log 2>&1
 echo "ncu full rc=$?"
