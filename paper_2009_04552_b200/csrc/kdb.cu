@@ -1508,8 +1508,14 @@ static_assert(sizeof(HEdge) == 24, "HEdge layout");
 // without touching comp[].  Everything else takes the exact gather.
 constexpr int kDomMax = 16384;         // dom table entries (64 KB of shared memory)
 constexpr int kBloomBits = 1 << 20;    // 128 KB of shared memory
-constexpr int kFilterThreads = 1024;
-constexpr int kFilterUnroll = 4;
+#ifndef KDB_FILTER_THREADS
+#define KDB_FILTER_THREADS 1024
+#endif
+#ifndef KDB_FILTER_UNROLL
+#define KDB_FILTER_UNROLL 4
+#endif
+constexpr int kFilterThreads = KDB_FILTER_THREADS;  // rows per tile = threads per block
+constexpr int kFilterUnroll = KDB_FILTER_UNROLL;    // 16-B id chunks in flight per thread
 constexpr size_t kFilterSmem = kBloomBits / 8;
 
 // Blocked Bloom filter: key x selects ONE 32-bit word (top 15 bits of x*C1)

@@ -19,7 +19,8 @@ from dataclasses import dataclass
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libkdb.so")
+# KDB_LIBRARY: an alternative build of the same library (tuning experiments)
+LIB_PATH = os.environ.get("KDB_LIBRARY") or os.path.join(_HERE, "lib", "libkdb.so")
 KDB_GRAPH_EXACT = 1
 
 

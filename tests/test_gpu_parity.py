@@ -374,3 +374,4 @@ def test_round1_fused_into_ell(c1_graph, fuse, pack, P, monkeypatch):
         assert_parity(got, oracle_run(nbr, dist, M, eps))
 
 
+
