@@ -138,6 +138,24 @@ kdb_status kdb_mst(const kdb_graph* g, float eps, const uint32_t* core_bits, int
                    int64_t* mst_count, double* mst_weight, void* workspace, size_t ws_bytes,
                    kdb_comm* comm, kdb_stream_t stream);
 
+/* The paper's INEXACT MST (PAPER.md:1053-1060,
+ * Alg. 2 ParallelLocalMST + Alg. 4 DistributedCutMST):
+ * vertex-partition the N points into `nparts` contiguous groups
+ * [floor(pN/nparts), floor((p+1)N/nparts)) (the distributed row layout,
+ * PAPER.md:517); MST_p,local = the MSF of group p's internal candidate edges;
+ * every local subtree is a super vertex; MST_cut = the MSF of the candidate
+ * edges between groups over the super vertices.  Output = U_p MST_p,local U
+ * MST_cut, every MSF taken under O1 of the original edges.  By Thm. 3(ii)
+ * comp/labels equal kdb_mst's; the forest and its weight in
+ * general do not (weight >= kdb_mst's).  Arguments and outputs as kdb_mst;
+ * single process (the whole graph: row_begin 0, n_rows = n_total), workspace
+ * >= kdb_mst_inexact_workspace_bytes(g, nparts).  EINVAL: nparts < 1, a partial
+ * graph.  Synchronises `stream`. */
+size_t kdb_mst_inexact_workspace_bytes(const kdb_graph* g, int32_t nparts);
+kdb_status kdb_mst_inexact(const kdb_graph* g, float eps, const uint32_t* core_bits, int32_t nparts, int32_t* comp,
+                           uint32_t* mst_a, uint32_t* mst_b, float* mst_w, int64_t mst_cap, int64_t* mst_count,
+                           double* mst_weight, void* workspace, size_t ws_bytes, kdb_stream_t stream);
+
 /* Alg. 1 line 13 ClusterBorder (body omitted in the paper,
  * SURVEY.md §8(c) reading #13, Lemma 1(ii)):
  *   labels[i] (device int32[n_rows]) for local row v = row_begin + i:

@@ -1769,6 +1769,69 @@ __global__ void __launch_bounds__(kFilterThreads) k_filter(
   if ((threadIdx.x & 31) == 0 && slow) atomicAdd(n_slow, (unsigned long long)slow);
 }
 
+// ---- inexact MST (Alg. 2 + 4) -------
+// Group of id x under the contiguous split lo_p = floor(p N / P).
+__device__ __forceinline__ int part_of(int64_t x, int64_t N, int P) {
+  int64_t p = (x * P) / N;
+  if (((p + 1) * N) / P <= x) ++p;
+  else if ((p * N) / P > x) --p;
+  return (int)p;
+}
+// Local view: row v keeps, in stored order, its entries (columns < kc) whose
+// target lies in v's own group; the rest of the row is padding.  The exact
+// pipeline on this view computes U_i MST_i,local (no edge joins two groups).
+__global__ void k_local_view(const int32_t* __restrict__ nbr, const float* __restrict__ dist, int64_t n, int32_t ld,
+                             int32_t kc, int P, int32_t* __restrict__ lnbr, float* __restrict__ ldist) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+    const int pv = part_of(v, n, P);
+    const int32_t* nr = nbr + v * ld;
+    const float* dr = dist + v * ld;
+    int32_t* on = lnbr + v * ld;
+    float* od = ldist + v * ld;
+    int o = 0;
+    for (int c = 0; c < kc; ++c) {
+      const int32_t J = nr[c];
+      if (J >= 0 && J < n && part_of(J, n, P) == pv) {
+        on[o] = J;
+        od[o] = dr[c];
+        ++o;
+      }
+    }
+    for (; o < ld; ++o) {
+      on[o] = -1;
+      od[o] = __int_as_float(0x7f800000);
+    }
+  }
+}
+// E_cut: candidate entries of core rows whose target is a core point of another
+// group, as survivors between local components (comp = dense local ids).
+__global__ void k_cut_edges(const int32_t* __restrict__ nbr, const float* __restrict__ dist, int64_t n, int32_t ld,
+                            int32_t kc, float eps, int P, const uint32_t* __restrict__ bits,
+                            const int32_t* __restrict__ comp, HEdge* __restrict__ out, uint32_t cap,
+                            uint32_t* __restrict__ n_out) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+    if (!is_core(bits, v)) continue;
+    const int pv = part_of(v, n, P);
+    const int32_t cv = comp[v];
+    for (int c = 0; c < kc; ++c) {
+      const float w = dist[v * ld + c];
+      if (!(w <= eps)) break;
+      const int64_t J = nbr[v * ld + c];
+      if (J < 0 || J >= n || J == v || !is_core(bits, J) || part_of(J, n, P) == pv) continue;
+      const uint32_t s = atomicAdd(n_out, 1u);
+      if (s < cap) {
+        HEdge h;
+        h.key = pack_key(mono_bits(w), (uint32_t)min(v, J));
+        h.b = (uint32_t)max(v, J);
+        h.x = cv;
+        h.y = comp[J];
+        h.pad = 0;
+        out[s] = h;
+      }
+    }
+  }
+}
+
 // heavy phase, per round: x = hcomp[e.x], y = hcomp[e.y]; intra -> dropped for
 // good; else offer the key to both components (undirected)
 __global__ void k_hedge_offer(const HEdge* __restrict__ E, uint32_t n, const int32_t* __restrict__ hcomp,
@@ -1970,7 +2033,7 @@ size_t cub_tmp_bytes(int64_t N, int64_t cap_edges) {
 
 // carve the workspace; returns bytes needed
 size_t carve(Layout& L, char* base, bool dry, int64_t N, int nr, const int64_t* rb, const int64_t* rn,
-             bool general, int32_t k) {
+             bool general, int32_t k, int64_t hs_cap_override = -1) {
   Carver cv{base, 0, 0, dry};
   const int64_t nwords = (N + 31) / 32;
   L.woff = cv.take<uint32_t>(nwords + 1);
@@ -2018,7 +2081,9 @@ size_t carve(Layout& L, char* base, bool dry, int64_t N, int nr, const int64_t* 
       R.Bc = L.Bc;
       R.tgt = L.tgt;
     }
-    R.hs_cap = (uint32_t)std::min<int64_t>(survivor_cap(n, k), (int64_t)UINT32_MAX - 1);
+    R.hs_cap = (uint32_t)std::min<int64_t>(hs_cap_override >= 0 ? std::max<int64_t>(hs_cap_override, 1)
+                                                                   : survivor_cap(n, k),
+                                           (int64_t)UINT32_MAX - 1);
     R.hs[0] = cv.take<HEdge>(R.hs_cap);
     R.hs[1] = cv.take<HEdge>(R.hs_cap);
     R.hkeep = cv.take<uint8_t>(R.hs_cap);
@@ -2853,10 +2918,16 @@ size_t kdb_mst_workspace_bytes(const kdb_graph* g, kdb_comm* comm) {
                edge_cols_of(g));
 }
 
-kdb_status kdb_mst(const kdb_graph* g, float eps, const uint32_t* core_bits, int32_t* comp,
-                   uint32_t* mst_a, uint32_t* mst_b, float* mst_w, int64_t mst_cap, int64_t* mst_count,
-                   double* mst_weight, void* workspace, size_t ws_bytes, kdb_comm* comm,
-                   kdb_stream_t stream) {
+}  // extern "C"
+namespace {
+// bytes of the inexact mode's local view (nbr + dist copies of the rows)
+size_t local_view_bytes(const kdb_graph* g) {
+  return 2 * (((size_t)g->n_rows * g->k_max * 4 + 255) & ~size_t(255));
+}
+// kdb_mst (nparts = 0) and kdb_mst_inexact (nparts >= 1 contiguous groups)
+kdb_status mst_impl(const kdb_graph* g, float eps, const uint32_t* core_bits, int32_t* comp, uint32_t* mst_a,
+                    uint32_t* mst_b, float* mst_w, int64_t mst_cap, int64_t* mst_count, double* mst_weight,
+                    void* workspace, size_t ws_bytes, kdb_comm* comm, kdb_stream_t stream, int32_t nparts) {
   KDB_TRY(validate_graph(g));
   KDB_TRY(validate_eps(eps));
   const int64_t N = g->n_total;
@@ -2867,6 +2938,19 @@ kdb_status kdb_mst(const kdb_graph* g, float eps, const uint32_t* core_bits, int
   if (comm && comm->kind == 2 && (g->row_begin != 0 || g->n_rows != g->n_total))
     return set_err(KDB_EINVAL, "sim communicator needs the full graph");
   if ((uintptr_t)workspace & 255u) return set_err(KDB_EINVAL, "workspace must be 256-byte aligned");
+  const bool inexact = nparts > 0;
+  if (inexact && (comm || g->row_begin != 0 || g->n_rows != g->n_total))
+    return set_err(KDB_EINVAL, "kdb_mst_inexact: single process, full graph");
+  int32_t* lnbr = nullptr;
+  float* ldist = nullptr;
+  if (inexact) {  // the local view leads the workspace
+    const size_t lv = local_view_bytes(g);
+    if (ws_bytes < lv) return set_err(KDB_ENOMEM, "workspace %zu < required %zu bytes", ws_bytes, lv);
+    lnbr = reinterpret_cast<int32_t*>(workspace);
+    ldist = reinterpret_cast<float*>((char*)workspace + lv / 2);
+    workspace = (char*)workspace + lv;
+    ws_bytes -= lv;
+  }
   Mst m;
   m.g = g;
   m.comm = comm;
@@ -2876,11 +2960,13 @@ kdb_status kdb_mst(const kdb_graph* g, float eps, const uint32_t* core_bits, int
   m.ld = g->k_max;
   m.bits = core_bits;
   m.comp = comp;
-  m.general = !(g->flags & KDB_GRAPH_EXACT);
+  // the local view is no kNN graph (no certificate): in-edge lists
+  m.general = inexact || !(g->flags & KDB_GRAPH_EXACT);
   Layout& L = m.L;
   std::vector<int64_t> rb, rn;
   rank_ranges(g, comm, rb, rn);
-  const size_t need = carve(L, (char*)workspace, false, N, (int)rb.size(), rb.data(), rn.data(), m.general, m.k);
+  const size_t need = carve(L, (char*)workspace, false, N, (int)rb.size(), rb.data(), rn.data(), m.general, m.k,
+                            inexact ? g->n_rows * (int64_t)m.k : -1);
   if (ws_bytes < need) return set_err(KDB_ENOMEM, "workspace %zu < required %zu bytes", ws_bytes, need);
   *mst_count = 0;
   *mst_weight = 0.0;
@@ -2901,11 +2987,35 @@ kdb_status kdb_mst(const kdb_graph* g, float eps, const uint32_t* core_bits, int
   // plain rows-Boruvka over the whole candidate graph otherwise.
   const int light_m = env_int("KDB_LIGHT", 10);
   bool filtered = false;
-  if (env_int("KDB_FILTER", 1) && light_m >= 1 && light_m < m.k) {
+  if (inexact) {
+    // U_i MST_i,local: the rows phase on the local view; then MST_cut: the cut
+    // entries of the real rows as survivors between local components
+    RankState& R = L.ranks[0];
+    LAUNCH(k_local_view, grid_for(N), kThreads, st, g->nbr, g->dist, N, m.ld, m.k, (int)nparts, lnbr, ldist);
+    R.nbr = lnbr;
+    R.dist = ldist;
+    KDB_TRY(rows_phase(m, eps));
+    KDB_CUDA(cudaEventRecord(m.ev[0], st));
+    KDB_CUDA(cudaMemsetAsync(R.n_hs_dev, 0, 2 * sizeof(uint32_t), st));
+    LAUNCH(k_cut_edges, grid_for(N), kThreads, st, g->nbr, g->dist, N, m.ld, m.k, eps, (int)nparts, core_bits,
+           comp, R.hs[0], R.hs_cap, R.n_hs_dev);
+    KDB_CUDA(cudaGetLastError());
+    uint32_t ncut = 0;
+    KDB_CUDA(cudaMemcpyAsync(&ncut, R.n_hs_dev, 4, cudaMemcpyDeviceToHost, st));
+    KDB_CUDA(cudaStreamSynchronize(st));
+    if (ncut > R.hs_cap) return set_err(KDB_EINTERNAL, "cut entries exceed their buffer");
+    R.n_hs = ncut;
+    m.survivors = ncut;
+    KDB_CUDA(cudaEventRecord(m.ev[1], st));
+    m.t_filter += elapsed(m.ev[0], m.ev[1]);
+    KDB_TRY(heavy_phase(m));
+  } else if (env_int("KDB_FILTER", 1) && light_m >= 1 && light_m < m.k) {
     KDB_TRY(pick_tau(m, light_m, &m.tau));
     filtered = m.tau < eps;
   }
-  if (filtered) {
+  if (inexact) {
+    // done above
+  } else if (filtered) {
     KDB_TRY(rows_phase(m, m.tau));
     bool overflow = false;
     KDB_TRY(filter_phase(m, eps, &overflow));
@@ -2977,6 +3087,33 @@ kdb_status kdb_mst(const kdb_graph* g, float eps, const uint32_t* core_bits, int
   g_stats[15] = (double)m.exceptions;
   g_stats[16] = (double)m.slow_entries;
   return KDB_OK;
+}
+
+}  // namespace
+extern "C" {
+
+kdb_status kdb_mst(const kdb_graph* g, float eps, const uint32_t* core_bits, int32_t* comp,
+                   uint32_t* mst_a, uint32_t* mst_b, float* mst_w, int64_t mst_cap, int64_t* mst_count,
+                   double* mst_weight, void* workspace, size_t ws_bytes, kdb_comm* comm,
+                   kdb_stream_t stream) {
+  return mst_impl(g, eps, core_bits, comp, mst_a, mst_b, mst_w, mst_cap, mst_count, mst_weight, workspace, ws_bytes,
+                  comm, stream, 0);
+}
+
+size_t kdb_mst_inexact_workspace_bytes(const kdb_graph* g, int32_t nparts) {
+  if (validate_graph(g) != KDB_OK || nparts < 1) return 0;
+  std::vector<int64_t> rb{g->row_begin}, rn{g->n_rows};
+  Layout L;
+  return local_view_bytes(g) + carve(L, nullptr, true, g->n_total, 1, rb.data(), rn.data(), true, edge_cols_of(g),
+                                     g->n_rows * (int64_t)edge_cols_of(g));
+}
+
+kdb_status kdb_mst_inexact(const kdb_graph* g, float eps, const uint32_t* core_bits, int32_t nparts, int32_t* comp,
+                           uint32_t* mst_a, uint32_t* mst_b, float* mst_w, int64_t mst_cap, int64_t* mst_count,
+                           double* mst_weight, void* workspace, size_t ws_bytes, kdb_stream_t stream) {
+  if (nparts < 1) return set_err(KDB_EINVAL, "nparts must be >= 1");
+  return mst_impl(g, eps, core_bits, comp, mst_a, mst_b, mst_w, mst_cap, mst_count, mst_weight, workspace, ws_bytes,
+                  nullptr, stream, nparts);
 }
 
 kdb_status kdb_label(const kdb_graph* g, float eps, const uint32_t* core_bits, const int32_t* comp,

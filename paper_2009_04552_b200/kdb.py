@@ -59,6 +59,10 @@ def lib():
     L.kdb_nmi_workspace_bytes.argtypes = [i64]
     L.kdb_nmi_workspace_bytes.restype = C.c_size_t
     L.kdb_nmi.argtypes = [P, P, i64, C.POINTER(C.c_double), C.POINTER(i64), C.POINTER(i64), P, C.c_size_t, P]
+    L.kdb_mst_inexact_workspace_bytes.argtypes = [G, i32]
+    L.kdb_mst_inexact_workspace_bytes.restype = C.c_size_t
+    L.kdb_mst_inexact.argtypes = [G, f32, P, i32, P, P, P, P, i64, C.POINTER(i64), C.POINTER(C.c_double), P,
+                                  C.c_size_t, P]
     L.kdb_mst_workspace_bytes.argtypes = [G, P]
     L.kdb_mst_workspace_bytes.restype = C.c_size_t
     L.kdb_mst.argtypes = [G, f32, P, P, P, P, P, i64, C.POINTER(i64), C.POINTER(C.c_double), P,
@@ -78,7 +82,8 @@ def lib():
 EXPORTS = sorted(["kdb_nccl_unique_id", "kdb_comm_create_nccl", "kdb_comm_create_sim", "kdb_comm_destroy",
                   "kdb_core_mark", "kdb_mst_workspace_bytes", "kdb_mst", "kdb_label", "kdb_last_mst_stats",
                   "kdb_profile_enable", "kdb_profile_reset", "kdb_launch_count", "kdb_profile_read",
-                  "kdb_status_string", "kdb_last_error", "kdb_nmi_workspace_bytes", "kdb_nmi"])
+                  "kdb_status_string", "kdb_last_error", "kdb_nmi_workspace_bytes", "kdb_nmi",
+                  "kdb_mst_inexact_workspace_bytes", "kdb_mst_inexact"])
 
 
 def _check(rc: int, what: str):
@@ -229,6 +234,34 @@ def mst(g: Graph, eps: float, core_bits: torch.Tensor, comm: Comm | None = None,
                  filter_ms=st[8], heavy_ms=st[9], survivors=int(st[10]), heavy_rounds=int(st[11]),
                  tau=st[12], light_components=int(st[13]), fallback=int(st[14]),
                  filter_exceptions=int(st[15]), filter_slow_entries=int(st[16]))
+    m = cnt.value
+    return MstResult(comp[:N], a[:m], b[:m], w[:m], m, tot.value, stats)
+
+
+def mst_inexact(g: Graph, eps: float, core_bits: torch.Tensor, nparts: int, stream=None) -> MstResult:
+    """kdb_mst_inexact: the paper's inexact MST over `nparts` contiguous groups
+    (local MSFs + cut MSF over super vertices).  Same
+    components as mst(); the forest is not the minimum one in general."""
+    dev = g.dist.device
+    N = g.n_total
+    comp = torch.empty(max(N, 1), dtype=torch.int32, device=dev)
+    cap = max(N - 1, 0)
+    a = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
+    b = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
+    w = torch.empty(max(cap, 1), dtype=torch.float32, device=dev)
+    gc = g.c()
+    nws = int(lib().kdb_mst_inexact_workspace_bytes(C.byref(gc), int(nparts)))
+    ws = torch.empty(max(nws, 256), dtype=torch.uint8, device=dev)
+    cnt = C.c_int64(0)
+    tot = C.c_double(0.0)
+    _check(lib().kdb_mst_inexact(C.byref(gc), float(eps), C.c_void_p(core_bits.data_ptr()), int(nparts),
+                                 C.c_void_p(comp.data_ptr()), C.c_void_p(a.data_ptr()), C.c_void_p(b.data_ptr()),
+                                 C.c_void_p(w.data_ptr()), cap, C.byref(cnt), C.byref(tot),
+                                 C.c_void_p(ws.data_ptr()), ws.numel(), _stream(stream)), "kdb_mst_inexact")
+    st = (C.c_double * 20)()
+    lib().kdb_last_mst_stats(st, 20)
+    stats = dict(rounds=int(st[0]), cut_entries=int(st[10]), heavy_rounds=int(st[11]), local_components=int(st[13]),
+                 local_ms=st[1] + st[2] + st[3] + st[5], cut_ms=st[8] + st[9])
     m = cnt.value
     return MstResult(comp[:N], a[:m], b[:m], w[:m], m, tot.value, stats)
 

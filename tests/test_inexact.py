@@ -127,3 +127,46 @@ def test_part_of_matches_ranges():
         lo = [(p * N) // P for p in range(P + 1)]
         exp = np.concatenate([np.full(lo[p + 1] - lo[p], p) for p in range(P)])
         assert np.array_equal(oinx.part_of(np.arange(N), N, P), exp)
+
+
+# ------------------------------------------------------------- GPU parity ----
+def _gpu_inexact(nbr, dist, M, eps, P, edge_cols=0):
+    import torch
+    import paper_2009_04552_b200 as kdb
+    g = kdb.Graph(torch.from_numpy(nbr).cuda(), torch.from_numpy(dist).cuda(), n_total=nbr.shape[0],
+                  edge_cols=edge_cols)
+    bits = kdb.core_mark(g, M, float(eps))
+    r = kdb.mst_inexact(g, float(eps), bits, P)
+    lab = kdb.label(g, float(eps), bits, r.comp)
+    torch.cuda.synchronize()
+    return dict(core=kdb.unpack_core(bits, nbr.shape[0]).numpy(), comp=r.comp.cpu().numpy(),
+                labels=lab.cpu().numpy(), msf_a=r.a.cpu().numpy().astype(np.uint32),
+                msf_b=r.b.cpu().numpy().astype(np.uint32), msf_w=r.w.cpu().numpy(), msf_weight=r.weight,
+                stats=r.stats)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("ci", range(len(CASES)))
+@pytest.mark.parametrize("P", [1, 2, 3, 5, 8])
+def test_kdb_mst_inexact_parity(ci, P):
+    from tests.kdb_harness import assert_parity
+    nbr, dist, M, eps = CASES[ci]
+    exp = oinx.kdbscan_inexact(nbr, dist, M, eps, P)
+    assert_parity(_gpu_inexact(nbr, dist, M, eps, P), exp)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("P", [2, 4, 7])
+def test_kdb_mst_inexact_c1(P):
+    from datagen import gen_c1
+    from tests.kdb_harness import assert_parity
+    X, _ = gen_c1(0)
+    nbr, dist = knn_bruteforce(X, 16)
+    for f, ec in ((1.5, 0), (1.0, 0), (1.5, 8)):
+        eps = eps_from_graph(dist, 8, f)
+        exp = oinx.kdbscan_inexact(nbr, dist, 8, eps, P, edge_cols=ec or None)
+        got = _gpu_inexact(nbr, dist, 8, eps, P, edge_cols=ec)
+        assert_parity(got, exp)
+        ex = oracle.kdbscan(nbr, dist, 8, eps, edge_cols=ec or None)
+        assert np.array_equal(got["labels"], ex["labels"])   # Thm. 3(ii)
+        assert got["msf_weight"] >= ex["msf_weight"] * (1 - 1e-12)
