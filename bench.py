@@ -51,6 +51,9 @@ def parse():
     ap.add_argument("--edge-cols", default=None,
                     help="candidate edges from the first EDGE_COLS columns ('M' = Def. 6's edge set, "
                          "SURVEY.md 8(f) NEXT 1); default all k (north_star)")
+    ap.add_argument("--inexact", type=int, default=0,
+                    help="also time the paper's inexact MST over P contiguous groups (kdb_mst_inexact, "
+                         "SURVEY.md 8(f) NEXT 2) and compare it with the exact step; N=1 only")
     ap.add_argument("--eps-factors", default=None,
                     help="comma list: one step = the whole stage at every eps = f x median D[:, M-1] on "
                          "the same resident graph (Fig. eps_mnist protocol, PAPER.md:459-488)")
@@ -341,6 +344,11 @@ def run_ours(args):
     if not args.no_e2e:
         e2e = run_e2e(args, kdb, W, N, k, M, eps_list, ec, rb, re_, comm, ws, outs, dev, world)
 
+    # ---- NEXT 2: the paper's inexact MST against the exact step ---------------------------
+    inexact = None
+    if args.inexact and world == 1:
+        inexact = run_inexact(args, kdb, g, M, eps_list[-1], r, lb, ms, stats[-1], stream, dev)
+
     # ---- roofline of the dominant kernel ------------------------------------------------
     peaks = measured_peaks()
     peak = peaks["hbm_gbs"] if peaks else 6650.0
@@ -391,6 +399,7 @@ def run_ours(args):
                 "stage_roofline": {"t_min_ms": t_min_ms, "frac": t_min_ms / ms,
                                    "bytes": "8 N k + 4 N + N/8 (SURVEY.md 8(d))", "peak": peak},
                 "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "quality": quality,
+                **({"inexact": inexact} if inexact else {}),
                 "clocks": clk, "kernels": kernels,
                 "mst": {"edges": msf_count, "weight": msf_weight, "clusters": n_clusters,
                         "rounds": stats[-1]["rounds"], "stall_rounds": stats[-1]["stall_rounds"],
@@ -447,6 +456,39 @@ def measured_traffic():
         return json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
     except Exception:
         return {}
+
+
+def run_inexact(args, kdb, g, M, eps, r_exact, lab_exact, ms_exact, st_exact, stream, dev):
+    """Time core_mark -> kdb_mst_inexact(P groups) -> label like the exact step and
+    compare: Thm. 3(ii) says the labels agree; the forest weight does not."""
+    import torch
+    P = int(args.inexact)
+    for _ in range(max(args.warmup, 1)):
+        bits = kdb.core_mark(g, M, eps)
+        ri = kdb.mst_inexact(g, eps, bits, P)
+        li = kdb.label(g, eps, bits, ri.comp)
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        bits = kdb.core_mark(g, M, eps)
+        ri = kdb.mst_inexact(g, eps, bits, P)
+        li = kdb.label(g, eps, bits, ri.comp)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms_i = e0.elapsed_time(e1) / args.steps
+    # the exact step's labels are those of its last eps
+    same = bool(torch.equal(li[:g.n_rows], lab_exact[:g.n_rows]))
+    return {"groups": P, "ms_per_step": ms_i, "exact_ms_per_step": ms_exact,
+            "labels_equal_exact": same, "msf_edges": ri.count, "msf_edges_exact": r_exact.count,
+            "msf_weight": ri.weight, "msf_weight_exact": r_exact.weight,
+            "weight_ratio": ri.weight / r_exact.weight if r_exact.weight else None,
+            "local_components": ri.stats["local_components"], "cut_entries": ri.stats["cut_entries"],
+            "allreduce_payload_bytes_per_rank": {
+                "exact": st_exact.get("payload_rows_bytes", 0) + st_exact.get("payload_heavy_bytes", 0),
+                "inexact": ri.stats["payload_heavy_bytes"],
+                "note": "MIN all-reduces over the component arrays (Kc 8 B + Bc 4 B per component and "
+                        "round) that P ranks would issue; the inexact local phase needs none"}}
 
 
 def run_e2e(args, kdb, W, N, k, M, eps_list, ec, rb, re_, comm, ws, outs, dev, world):

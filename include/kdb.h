@@ -188,7 +188,15 @@ kdb_status kdb_nmi(const int32_t* a, const int32_t* b, int64_t n, double* nmi /*
  * this thread: out[0] = rounds, out[1] = init/sweep ms, out[2] = min-edge ms
  * (offer + tie + exchange), out[3] = hook/jump/relabel ms, out[4] = finalize ms,
  * out[5] = in-edge build ms, out[6] = stall (sweep) rounds, out[7] = graph entries
- * read by the per-vertex offer kernel (all rounds).  Returns entries written. */
+ * read by the per-vertex offer kernel (all rounds), out[8] = filter (inexact: cut)
+ * ms, out[9] = heavy-phase ms, out[10] = survivors (inexact: cut entries),
+ * out[11] = heavy rounds, out[12] = light threshold (-1: none), out[13] =
+ * components after the rows phase, out[14] = overflow fallback, out[15] = filter
+ * exceptions, out[16] = filter slow entries, out[17] / out[18] = bytes per rank
+ * carried by the MIN all-reduces over component arrays in the rows / heavy
+ * phase (counted with or without a communicator; with kdb_mst_inexact the
+ * local phase needs none: groups never share a component).  Returns entries
+ * written. */
 int kdb_last_mst_stats(double* out, int cap);
 
 /* Measurement hooks (bench.py).  kdb_launch_count(): kernels this library has

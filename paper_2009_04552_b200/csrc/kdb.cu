@@ -2170,6 +2170,9 @@ struct Mst {
   bool general = false;
   int64_t C = 0;         // components after the rows phase (light components under the filter)
   int64_t C_heavy = -1;  // components after the heavy phase (-1: no heavy phase ran)
+  // bytes per rank carried by the MIN all-reduces over component arrays (issued
+  // with a communicator; counted either way): rows phase, heavy / cut phase
+  double payload_rows = 0, payload_heavy = 0;
   int rounds = 0, stalls = 0, heavy_rounds = 0;
   double t_init = 0, t_inlist = 0, t_min_edges = 0, t_contract = 0, t_filter = 0, t_heavy = 0;
   unsigned long long entries = 0, survivors = 0, exceptions = 0, slow_entries = 0;
@@ -2285,6 +2288,7 @@ kdb_status rows_phase(Mst& m, float eps_run) {
     KDB_CUDA(cudaGetLastError());
   }
   if (!general) KDB_TRY(allreduce_min_u32(comm, L.kmin, C, st));
+  if (!general) m.payload_rows += 4.0 * C;
   KDB_CUDA(cudaEventRecord(ev[1], st));
   // ---- general mode: in-edge lists --------------------------------------------
   if (general) {
@@ -2474,6 +2478,7 @@ kdb_status rows_phase(Mst& m, float eps_run) {
     for (size_t r = 1; r < nr; ++r)
       LAUNCH(k_min_into_u64, grid_for(C_ub), kThreads, st, L.Kc, L.ranks[r].Kc, C_ub, Cd);
     KDB_TRY(allreduce_min_u64(comm, L.Kc, C_ub, st));
+    m.payload_rows += 8.0 * C_ub;
     // a4: ties (the direct round already wrote Bc and the targets)
     if (!direct) {
       for (size_t r = 0; r < nr; ++r) {
@@ -2487,11 +2492,13 @@ kdb_status rows_phase(Mst& m, float eps_run) {
     for (size_t r = 1; r < nr; ++r)
       LAUNCH(k_min_into_u32, grid_for(C_ub), kThreads, st, L.Bc, L.ranks[r].Bc, C_ub, Cd);
     KDB_TRY(allreduce_min_u32(comm, L.Bc, C_ub, st));
+    m.payload_rows += 4.0 * C_ub;
     if (direct) {
       for (size_t r = 1; r < nr; ++r)
         LAUNCH(k_min_into_u32, grid_for(C_ub), kThreads, st, (uint32_t*)L.tgt, (const uint32_t*)L.ranks[r].tgt, C_ub,
                Cd);
       KDB_TRY(allreduce_min_u32(comm, (uint32_t*)L.tgt, C_ub, st));  // non-owners hold INT32_MAX
+      m.payload_rows += 4.0 * C_ub;
     }
     // a5: hook + emit
     KDB_CUDA(cudaMemsetAsync(&L.ctr->hooks, 0, 4 * sizeof(uint32_t), st));
@@ -2558,6 +2565,7 @@ kdb_status rows_phase(Mst& m, float eps_run) {
       for (size_t r = 1; r < nr; ++r)
         LAUNCH(k_min_into_u64, grid_for(Cx), kThreads, st, L.Kc, L.ranks[r].Kc, Cx);
       KDB_TRY(allreduce_min_u64(comm, L.Kc, Cx, st));
+      m.payload_rows += 8.0 * Cx;
       for (size_t r = 0; r < nr; ++r)
         if (na_x[r])
           LAUNCH(k_sweep, grid_for(na_x[r]), kThreads, st, L.ranks[r].nbr, L.ranks[r].dist, ld, k, eps_run,
@@ -2566,6 +2574,7 @@ kdb_status rows_phase(Mst& m, float eps_run) {
       for (size_t r = 1; r < nr; ++r)
         LAUNCH(k_min_into_u32, grid_for(Cx), kThreads, st, L.Bc, L.ranks[r].Bc, Cx);
       KDB_TRY(allreduce_min_u32(comm, L.Bc, Cx, st));
+      m.payload_rows += 4.0 * Cx;
       KDB_CUDA(cudaMemsetAsync(&L.ctr->hooks, 0, 4 * sizeof(uint32_t), st));
       LAUNCH(k_hook<false>, grid_for(Cx), kThreads, st, Cx, L.Kc, L.Bc, nullptr, nullptr, comp, L.parent, L.e_key,
              L.e_w, N, L.ctr, (const int64_t*)nullptr, (const int4*)nullptr);
@@ -2731,6 +2740,7 @@ kdb_status heavy_phase(Mst& m) {
     for (size_t r = 1; r < L.ranks.size(); ++r)
       LAUNCH(k_min_into_u64, grid_for(C), kThreads, st, L.Kc, L.ranks[r].Kc, C);
     KDB_TRY(allreduce_min_u64(comm, L.Kc, C, st));
+    m.payload_heavy += 8.0 * C;
     for (size_t r = 0; r < L.ranks.size(); ++r) {
       RankState& R = L.ranks[r];
       if (R.n_hs)
@@ -2739,6 +2749,7 @@ kdb_status heavy_phase(Mst& m) {
     for (size_t r = 1; r < L.ranks.size(); ++r)
       LAUNCH(k_min_into_u32, grid_for(C), kThreads, st, L.Bc, L.ranks[r].Bc, C);
     KDB_TRY(allreduce_min_u32(comm, L.Bc, C, st));
+    m.payload_heavy += 4.0 * C;
     KDB_CUDA(cudaMemsetAsync(&L.ctr->hooks, 0, 4 * sizeof(uint32_t), st));
     LAUNCH(k_hook_h, grid_for(C), kThreads, st, C, L.Kc, L.Bc, m.comp, L.hcomp, L.parent, L.e_key, L.e_w, m.N, L.ctr);
     KDB_CUDA(cudaGetLastError());
@@ -3086,6 +3097,8 @@ kdb_status mst_impl(const kdb_graph* g, float eps, const uint32_t* core_bits, in
   g_stats[14] = m.fallback;
   g_stats[15] = (double)m.exceptions;
   g_stats[16] = (double)m.slow_entries;
+  g_stats[17] = inexact ? 0.0 : m.payload_rows;  // inexact: the groups' local phases share nothing
+  g_stats[18] = m.payload_heavy;
   return KDB_OK;
 }
 

@@ -233,7 +233,8 @@ def mst(g: Graph, eps: float, core_bits: torch.Tensor, comm: Comm | None = None,
                  finalize_ms=st[4], inlist_ms=st[5], stall_rounds=int(st[6]), entries_read=int(st[7]),
                  filter_ms=st[8], heavy_ms=st[9], survivors=int(st[10]), heavy_rounds=int(st[11]),
                  tau=st[12], light_components=int(st[13]), fallback=int(st[14]),
-                 filter_exceptions=int(st[15]), filter_slow_entries=int(st[16]))
+                 filter_exceptions=int(st[15]), filter_slow_entries=int(st[16]),
+                 payload_rows_bytes=st[17], payload_heavy_bytes=st[18])
     m = cnt.value
     return MstResult(comp[:N], a[:m], b[:m], w[:m], m, tot.value, stats)
 
@@ -261,7 +262,8 @@ def mst_inexact(g: Graph, eps: float, core_bits: torch.Tensor, nparts: int, stre
     st = (C.c_double * 20)()
     lib().kdb_last_mst_stats(st, 20)
     stats = dict(rounds=int(st[0]), cut_entries=int(st[10]), heavy_rounds=int(st[11]), local_components=int(st[13]),
-                 local_ms=st[1] + st[2] + st[3] + st[5], cut_ms=st[8] + st[9])
+                 local_ms=st[1] + st[2] + st[3] + st[5], cut_ms=st[8] + st[9],
+                 payload_rows_bytes=st[17], payload_heavy_bytes=st[18])
     m = cnt.value
     return MstResult(comp[:N], a[:m], b[:m], w[:m], m, tot.value, stats)
 
