@@ -5,18 +5,18 @@ NCCL_INC  := $(shell python -c "import os,nvidia.nccl as m; print(os.path.join(l
 NVFLAGS   := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -shared -Iinclude -I$(NCCL_INC) --expt-relaxed-constexpr $(KDB_NVFLAGS)
 
 KDB_SO    := paper_2009_04552_b200/lib/libkdb.so
-KNNG_SO   := datagen/lib/libknng.so
+KNNG_SO   := paper_2009_04552_b200/lib/libknng.so
 ORACLE_SO := oracle/liboracle.so
 
-all: $(KDB_SO) $(ORACLE_SO) $(if $(wildcard datagen/csrc/knng.cu),$(KNNG_SO))
+all: $(KDB_SO) $(ORACLE_SO) $(KNNG_SO)
 
 $(KDB_SO): paper_2009_04552_b200/csrc/kdb.cu include/kdb.h
 	@mkdir -p $(dir $@)
 	$(NVCC) $(NVFLAGS) -o $@ $< -ldl
 
-$(KNNG_SO): datagen/csrc/knng.cu
+$(KNNG_SO): paper_2009_04552_b200/csrc/knng.cu include/knng.h
 	@mkdir -p $(dir $@)
-	$(NVCC) $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -shared -o $@ $<
+	$(NVCC) $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -shared -Iinclude -o $@ $<
 
 $(ORACLE_SO): oracle/kdb_oracle.cpp
 	g++ -O2 -std=c++17 -shared -fPIC -o $@ $<

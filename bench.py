@@ -51,6 +51,9 @@ def parse():
     ap.add_argument("--edge-cols", default=None,
                     help="candidate edges from the first EDGE_COLS columns ('M' = Def. 6's edge set, "
                          "SURVEY.md 8(f) NEXT 1); default all k (north_star)")
+    ap.add_argument("--stage", default="cluster", choices=["cluster", "knng"],
+                    help="knng: time the exact kNN-graph builder (SURVEY.md 8(f) NEXT 3) on the points of "
+                         "--config instead of the clustering stage; compare with Table 2 (PAPER.md:21-36)")
     ap.add_argument("--inexact", type=int, default=0,
                     help="also time the paper's inexact MST over P contiguous groups (kdb_mst_inexact, "
                          "SURVEY.md 8(f) NEXT 2) and compare it with the exact step; N=1 only")
@@ -533,8 +536,65 @@ def run_e2e(args, kdb, W, N, k, M, eps_list, ec, rb, re_, comm, ws, outs, dev, w
             "h2d_bytes_per_step": int(n_rows) * k * 8, "d2h_bytes_per_step": int(n_rows) * 4 * len(eps_list)}
 
 
+# Table 2: GOFMM kNN-graph time, approximate (99% accuracy), on Frontera cores
+TABLE2 = {(64_000_000, 3, 100): (1792, 363.0), (64_000_000, 5, 100): (1792, 379.0),
+          (64_000_000, 32, 100): (1792, 926.0), (256_000_000, 3, 100): (7168, 583.0),
+          (256_000_000, 5, 100): (7168, 628.0)}
+
+
+def run_knng(args):
+    """One step = build the exact kNN graph of the config's points on the GPU
+    (grid cell search for d <= 5, certified brute force otherwise); CUDA events
+    on the launching stream around the whole call (it synchronises inside)."""
+    import torch
+    from datagen import CONFIGS, gen_config_points
+    from paper_2009_04552_b200.knng import build_knng_brute, build_knng_grid
+    rank, world, local = dist_env()
+    if rank != 0:
+        return
+    torch.cuda.set_device(local)
+    dev = torch.device(f"cuda:{local}")
+    cfg = CONFIGS[args.config]
+    X, _ = gen_config_points(args.config, args.seed, args.scale)
+    n, d = X.shape
+    k = cfg["k"]
+    Xd = torch.from_numpy(X).to(dev)
+    build = (lambda: build_knng_grid(Xd, k, device=dev)) if d <= 5 else (lambda: build_knng_brute(Xd, k, device=dev))
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        out = build()
+        del out
+    torch.cuda.synchronize()
+    times, info = [], None
+    for _ in range(args.steps):
+        e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        nbr, dist, info = build()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        times.append(e0.elapsed_time(e1) / 1e3)
+        del nbr, dist
+    t = float(np.median(times))
+    ref = TABLE2.get((n, d, k))
+    line = {"metric": "k-NNG build time", "value": t, "unit": "s", "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": False, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32 (fp64 re-rank / cell test)", "data": "synthetic",
+            "stage": "knng",
+            "config": {"workload": f"{args.config} points" + (f" scaled x{args.scale}" if args.scale != 1.0 else ""),
+                       "N": n, "d": d, "k": k, "builder": "grid cell search" if d <= 5 else "certified brute force",
+                       "exact": True},
+            "points_per_s": n / t, "info": info,
+            "table2": ({"cores": ref[0], "seconds": ref[1], "accuracy": "99% (GOFMM, approximate)",
+                        "note": "another machine and an approximate method: context, not the target"}
+                       if ref else None)}
+    emit(line, args)
+
+
 def main():
     args = parse()
+    if args.stage == "knng":
+        run_knng(args)
+        return
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -1,19 +1,23 @@
-// knng.cu -- exact k-NN graph builder for low-dimensional point sets (d <= 5),
-// uniform-grid cell search.  INPUT GENERATOR ONLY: not part of the clustering
-// hot path, shares no code with paper_2009_04552_b200/ or oracle/.
+// knng.cu -- exact k-NN graph builders (C-ABI in
+// include/knng.h).  The stage that precedes clustering (Table 2,
+// PAPER.md:21-36 times GOFMM's approximate builder); shares no code with the
+// clustering kernels (kdb.cu) or the oracle.
 //
 // Output convention: rows exclude self; fp64 distance
 // sqrt(sum_t (x_t - y_t)^2) from fp32 coordinates, summed in dimension order
 // without fused multiply-add (bit-identical to datagen/knn_cpu.py); each row is
 // ordered by (fp64 distance, index) and stored as fp32 dist / int32 nbr.
 //
-// Exactness: a query q in cell c collects every point of the 3^D block around c
-// whose distance is <= h' = h (1 - 1e-6); the block contains the whole ball of
-// radius h' (cell coordinates are computed in fp64).  If at least k such points
-// exist, the k nearest are among them (any point left out is farther than h').
-// Otherwise the query is redone with rings of radius R = 2, 3, ... cells.
+// Grid builder exactness: a query q in cell c collects every point of the 3^D
+// block around c whose distance is <= h' = h (1 - 1e-6); the block contains the
+// whole ball of radius h' (cell coordinates are computed in fp64).  If at least
+// k such points exist, the k nearest are among them (any point left out is
+// farther than h').  Otherwise the query is redone with rings of radius
+// R = 2, 3, ... cells.
 
 #include <cuda_runtime.h>
+
+#include "knng.h"
 
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>

@@ -113,3 +113,23 @@ def test_sim_comm_lifecycle(lib):
     assert lib.kdb_core_mark(C.byref(g), 2, 0.5, C.c_void_p(0x3000), h, None) == 1
     lib.kdb_comm_destroy(h)
     assert lib.kdb_comm_create_sim(C.byref(h), 0) == 1
+
+
+def test_knng_library_exports_every_declared_symbol():
+    """libknng.so (the kNN-graph builder stage, include/knng.h) loads without a
+    GPU and exports every declared entry point."""
+    from paper_2009_04552_b200 import knng
+    if not os.path.exists(knng.LIB_PATH):
+        subprocess.check_call(["make", "-C", ROOT, os.path.relpath(knng.LIB_PATH, ROOT)])
+    src = re.sub(r"/\*.*?\*/", "", open(os.path.join(ROOT, "include", "knng.h")).read(), flags=re.S)
+    fns = sorted(set(re.findall(r"\b(knng_[a-z_0-9]+)\s*\(", src)))
+    assert fns == ["knng_brute", "knng_exact_row", "knng_grid", "knng_grid_ws", "knng_ladder"]
+    L = C.CDLL(knng.LIB_PATH)
+    assert all(hasattr(L, f) for f in fns)
+    out = subprocess.run(["nm", "-D", "--defined-only", knng.LIB_PATH], capture_output=True, text=True).stdout
+    for f in fns:
+        assert re.search(rf"\bT {f}$", out, flags=re.M), f
+    # host-side argument checks, nothing launched (D out of range / k >= n)
+    L.knng_brute.argtypes = [C.c_void_p, C.c_int64, C.c_int, C.c_int, C.c_int] + [C.c_void_p] * 8
+    assert L.knng_brute(None, 10, 65, 3, 8, *([None] * 8)) == 4
+    assert L.knng_brute(None, 10, 3, 10, 16, *([None] * 8)) == 4
