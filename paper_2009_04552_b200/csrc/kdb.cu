@@ -1301,7 +1301,7 @@ __global__ void k_merge(int64_t C, const int32_t* __restrict__ rootof, const int
   if (Cp) C = *Cp;
   for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < C;
        c += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t r = gat(newid + rootof[c]);
+    const int32_t r = newid ? gat(newid + rootof[c]) : rootof[c];  // sparse ids: the root itself
     map[c] = r;
     atomicMin(cmin2 + r, cmin[c]);
     if (kmin) {
@@ -1330,14 +1330,19 @@ __global__ void k_relabel(int64_t N, int32_t* __restrict__ comp, const int32_t* 
     int32_t c[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
     // read-only maps through L1 (__ldg): when few components remain, 64M
     // gathers hit a handful of lines, which would serialise on their L2 slices
+    const int32_t c0[8] = {c[0], c[1], c[2], c[3], c[4], c[5], c[6], c[7]};
 #pragma unroll
     for (int j = 0; j < 8; ++j) c[j] = c[j] >= 0 ? __ldg(m1 + c[j]) : c[j];
     if (m2) {
 #pragma unroll
       for (int j = 0; j < 8; ++j) c[j] = c[j] >= 0 ? __ldg(m2 + c[j]) : c[j];
     }
-    p[0] = make_int4(c[0], c[1], c[2], c[3]);
-    p[1] = make_int4(c[4], c[5], c[6], c[7]);
+    // sparse ids (late rounds): most vertices keep theirs -- store only changes
+    bool ch0 = false, ch1 = false;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) { ch0 |= c[j] != c0[j]; ch1 |= c[j + 4] != c0[j + 4]; }
+    if (ch0) p[0] = make_int4(c[0], c[1], c[2], c[3]);
+    if (ch1) p[1] = make_int4(c[4], c[5], c[6], c[7]);
   }
   for (int64_t v = n8 * 8 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < N;
        v += (int64_t)gridDim.x * blockDim.x) {
@@ -2258,6 +2263,7 @@ kdb_status rows_phase(Mst& m, float eps_run) {
   KDB_CUDA(cudaGetLastError());
   const bool use_compact = env_int("KDB_COMPACT", 1) != 0;
   const int gw = env_int("KDB_GW", 4);  // component-gather width of the later light rounds (scan_ell)
+  const bool sparse_ids = env_int("KDB_SPARSE", 1) != 0;  // keep root ids once few components remain
   // exact mode: round 1 (singleton components) is fused into the ELL pass; a
   // single rank also packs (K, B, kmin) per component for the round-1 hook
   const bool fuse1 = !general && use_compact && env_int("KDB_FUSE1", 1) != 0;
@@ -2378,17 +2384,25 @@ kdb_status rows_phase(Mst& m, float eps_run) {
     const int64_t* Cd = (const int64_t*)&L.ctr->Cs[par];
     int64_t* Cn = (int64_t*)&L.ctr->Cs[par ^ 1];
     LAUNCH(k_jump, grid_for(C_bound), kThreads, st, C_bound, L.parent, L.rootof, L.ctr, Cd);
-    LAUNCH(k_root_flags, grid_for(C_bound), kThreads, st, C_bound, L.rootof, L.flag, Cd);
-    size_t cb2 = L.cub_bytes;
-    { LaunchScope ls_("cub::DeviceScan", st, false); KDB_CUDA(cub::DeviceScan::ExclusiveSum(L.cub_tmp, cb2, L.flag, L.newid, (int)std::max<int64_t>(C_bound, 1), st)); }
-    LAUNCH(k_count_roots, 1, 1, st, Cd, L.newid, L.flag, Cn);
+    // sparse ids once few components remain: a component keeps its root's id
+    // (no dense renumbering; the id range stays C_bound), so the relabel only
+    // rewrites the vertices of merged components
+    const bool sparse = sparse_ids && C_bound <= N / 64;
+    if (!sparse) {
+      LAUNCH(k_root_flags, grid_for(C_bound), kThreads, st, C_bound, L.rootof, L.flag, Cd);
+      size_t cb2 = L.cub_bytes;
+      { LaunchScope ls_("cub::DeviceScan", st, false); KDB_CUDA(cub::DeviceScan::ExclusiveSum(L.cub_tmp, cb2, L.flag, L.newid, (int)std::max<int64_t>(C_bound, 1), st)); }
+      LAUNCH(k_count_roots, 1, 1, st, Cd, L.newid, L.flag, Cn);
+    } else {
+      KDB_CUDA(cudaMemcpyAsync(Cn, Cd, sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
+    }
     LAUNCH(k_fill_i32, grid_for(C_bound), kThreads, st, L.cmin2, C_bound, INT32_MAX, (const int64_t*)Cn);
     if (!general)
       LAUNCH(k_fill_i32, grid_for(C_bound), kThreads, st, (int32_t*)L.kmin2, C_bound, (int32_t)kInfBits,
              (const int64_t*)Cn);
     // map[c] = new dense id of c's tree (reuses `parent`, no longer needed)
-    LAUNCH(k_merge, grid_for(C_bound), kThreads, st, C_bound, L.rootof, L.newid, L.cmin, general ? nullptr : L.kmin,
-           L.cmin2, L.kmin2, L.parent, Cd);
+    LAUNCH(k_merge, grid_for(C_bound), kThreads, st, C_bound, L.rootof, sparse ? (const int32_t*)nullptr : L.newid,
+           L.cmin, general ? nullptr : L.kmin, L.cmin2, L.kmin2, L.parent, Cd);
     LAUNCH(k_relabel, grid_for(N / 8 + 1), kThreads, st, N, comp, L.parent, (const int32_t*)nullptr);
     LAUNCH(k_fill_comp_arrays, grid_for(C_bound), kThreads, st, C_bound, L.Kc, L.Bc, nullptr, (const int64_t*)Cn);
     for (size_t r = 1; r < nr; ++r)

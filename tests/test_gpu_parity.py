@@ -375,3 +375,31 @@ def test_round1_fused_into_ell(c1_graph, fuse, pack, P, monkeypatch):
 
 
 
+
+
+@pytest.mark.parametrize("sparse", ["0", "1"])
+@pytest.mark.parametrize("case", RANDOM_CASES)
+def test_sparse_ids_toggle(case, sparse, monkeypatch):
+    """Late rounds keep root ids (no dense renumbering) -- same bits either way,
+    general and exact mode, filtered and unfiltered."""
+    monkeypatch.setenv("KDB_SPARSE", sparse)
+    n, k, M, seed, levels, sym, pad, zero, local, q = case
+    nbr, dist = random_graph(n, k, seed, levels=levels, symmetric=sym, pad_frac=pad, zero_frac=zero, local=local)
+    eps = np.float32(np.quantile(dist[np.isfinite(dist)].astype(np.float64), q))
+    exp = oracle_run(nbr, dist, M, eps)
+    for filt in ("0", "1"):
+        monkeypatch.setenv("KDB_FILTER", filt)
+        assert_parity(run_gpu(nbr, dist, M, eps, exact=False), exp)
+
+
+@pytest.mark.parametrize("sparse", ["0", "1"])
+@pytest.mark.parametrize("P", [0, 3])
+def test_c1_sparse_ids(c1_graph, sparse, P, monkeypatch):
+    import paper_2009_04552_b200 as kdb
+    monkeypatch.setenv("KDB_SPARSE", sparse)
+    X, nbr, dist = c1_graph
+    for exact in (False, True):
+        for f in (1.0, 1.5, 3.0):
+            eps = eps_from_graph(dist, 8, f)
+            got = run_gpu(nbr, dist, 8, eps, exact=exact, comm=kdb.Comm.sim(P) if P else None)
+            assert_parity(got, oracle_run(nbr, dist, 8, eps))
