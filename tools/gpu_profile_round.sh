@@ -8,6 +8,9 @@ python bench.py $ARGS > gpurun_out/plain_${TAG}.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_${TAG}.csv \
     python bench.py $ARGS > gpurun_out/ncu_launches_${TAG}.log 2>&1
 echo "ncu launches rc=$?"
-ncu --set full --clock-control none --import-source on -k regex:"k_filter|k_light_ell|k_light_round|k_hook|k_label|k_core_mark" -s 0 -c 8 \
+ncu --set full --clock-control none --import-source on -k regex:"k_core_mark|k_light_ell|k_light_round|k_hook" -s 0 -c 5 \
     -o gpurun_out/prof_${TAG} python bench.py $ARGS > gpurun_out/ncu_full_${TAG}.log 2>&1
 echo "ncu full rc=$?"
+ncu --set full --clock-control none --import-source on -k regex:"k_filter|k_label|k_relabel|k_tie" -s 0 -c 4 \
+    -o gpurun_out/prof2_${TAG} python bench.py $ARGS > gpurun_out/ncu_full2_${TAG}.log 2>&1
+echo "ncu full2 rc=$?"
