@@ -1,6 +1,6 @@
 """Write profiles/ncu_traffic.json (per-launch DRAM bytes per kernel, averaged
 over the captured launches) and a readable summary from an ncu --set full report.
-usage: python tools/ncu_traffic.py <report.ncu-rep> <summary.txt>"""
+usage: python tools/ncu_traffic.py <summary.txt> <report.ncu-rep> [<report2.ncu-rep> ...]"""
 import csv
 import json
 import os
@@ -16,11 +16,12 @@ KEYS = ['gpu__time_duration.sum', 'dram__bytes_read.sum', 'dram__bytes_write.sum
         'lts__t_sectors_srcunit_tex_op_read.sum', 'lts__t_sectors_srcunit_tex_op_read_lookup_miss.sum']
 
 
-def main(rep, out):
+def main(out, reps):
+  agg, lines, srcs = {}, [], {}
+  for rep in reps:
     raw = subprocess.run(['ncu', '-i', rep, '--page', 'raw', '--csv'], capture_output=True, text=True).stdout
     rows = list(csv.reader(raw.splitlines()))
     hdr, units = rows[0], rows[1]
-    agg, lines = {}, []
     for r in rows[2:]:
         name = r[hdr.index('Kernel Name')]
         base = name.split('(')[0].replace('void ', '').replace('<unnamed>::', '').split('<')[0].strip()
@@ -42,19 +43,20 @@ def main(rep, out):
         a = agg.setdefault(base, {'launches': 0, 'dram_bytes': 0.0})
         a['launches'] += 1
         a['dram_bytes'] += tb
+        srcs[base] = os.path.basename(rep)
         lines.append(f'--- {name[:110]}')
         for k in KEYS:
             if k in hdr:
                 lines.append(f'    {k} [{units[hdr.index(k)]}] = {r[hdr.index(k)]}')
-    traffic = {k: {'dram_bytes_per_launch': v['dram_bytes'] / v['launches'], 'launches_captured': v['launches'],
-                   'source': os.path.basename(rep)} for k, v in agg.items()}
-    with open(os.path.join(ROOT, 'profiles', 'ncu_traffic.json'), 'w') as f:
-        json.dump(traffic, f, indent=1)
-    with open(out, 'w') as f:
-        f.write(f'# ncu --set full --clock-control none, {os.path.basename(rep)} (B200, gpurun box)\n')
-        f.write('\n'.join(lines) + '\n')
-    print(json.dumps(traffic, indent=1))
+  traffic = {k: {'dram_bytes_per_launch': v['dram_bytes'] / v['launches'], 'launches_captured': v['launches'],
+                 'source': srcs[k]} for k, v in agg.items()}
+  with open(os.path.join(ROOT, 'profiles', 'ncu_traffic.json'), 'w') as f:
+    json.dump(traffic, f, indent=1)
+  with open(out, 'w') as f:
+    f.write(f'# ncu --set full --clock-control none, {", ".join(os.path.basename(r) for r in reps)} (B200, gpurun box)\n')
+    f.write('\n'.join(lines) + '\n')
+  print(json.dumps(traffic, indent=1))
 
 
 if __name__ == '__main__':
-    main(sys.argv[1], sys.argv[2])
+  main(sys.argv[1], sys.argv[2:])
