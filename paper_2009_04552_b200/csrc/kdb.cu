@@ -1407,68 +1407,79 @@ __global__ void k_wbuckets(int64_t m, const float* __restrict__ w, unsigned long
 }
 
 // a10: labels of this rank's rows
-// kLabelG lanes per row, 4 entries per lane and step: a non-core row's scan
-// (at most M-1 entries within eps, then the first one beyond) is read as
-// 64-byte coalesced pieces instead of a serial per-thread walk.  The first
-// event in column order decides: an entry beyond eps ends the scan (noise so
-// far), a core neighbour within eps gives the label.
+// One row per lane: a core row's label is comp[v] (the common case); the
+// warp's non-core rows (ballot) are then scanned cooperatively, kLabelG lanes
+// per row and 4 entries per lane and step, so a scan (at most M-1 entries within
+// eps, then the first one beyond) is read as 64-byte coalesced pieces instead of
+// a serial per-thread walk.  The first event in column order decides: an entry
+// beyond eps ends the scan (noise), a core neighbour within eps gives the label.
 constexpr int kLabelG = 4;
 template <bool VEC>
 __global__ void k_label(const int32_t* __restrict__ nbr, const float* __restrict__ dist, int64_t n_rows,
                         int32_t k, float eps, int64_t row_begin, int64_t N,
                         const uint32_t* __restrict__ bits, const int32_t* __restrict__ comp,
                         int32_t* __restrict__ labels) {
-  constexpr int G = kLabelG, RPW = 32 / G;
+  constexpr int G = kLabelG, RPS = 32 / G;  // rows per cooperative step
   const int lane = threadIdx.x & 31, sub = lane & (G - 1);
   const unsigned gmask = ((1u << G) - 1u) << (lane & ~(G - 1));
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t i = warp * RPW + lane / G; i - lane / G < n_rows; i += nwarps * RPW) {
-    if (i >= n_rows) continue;  // the whole group skips together
-    const int64_t v = row_begin + i;
-    if (is_core(bits, v)) {
-      if (sub == 0) labels[i] = comp[v];
-      continue;
+  for (int64_t base = warp * 32; base < n_rows; base += nwarps * 32) {  // warp-uniform
+    const int64_t i = base + lane;
+    bool pending = false;
+    if (i < n_rows) {
+      const int64_t v = row_begin + i;
+      if (is_core(bits, v)) labels[i] = comp[v];
+      else pending = true;
     }
-    const int32_t* nr = nbr + i * k;
-    const float* dr = dist + i * k;
-    int32_t lab = -1;
-    bool decided = false;
-    for (int c0 = 0; c0 < k && !decided; c0 += 4 * G) {
-      const int c = c0 + 4 * sub;
-      int32_t J[4];
-      float w[4];
-      if (VEC && c + 4 <= k) {
-        const int4 j4 = __ldcs(reinterpret_cast<const int4*>(nr + c));
-        const float4 w4 = __ldcs(reinterpret_cast<const float4*>(dr + c));
-        J[0] = j4.x; J[1] = j4.y; J[2] = j4.z; J[3] = j4.w;
-        w[0] = w4.x; w[1] = w4.y; w[2] = w4.z; w[3] = w4.w;
-      } else {
+    unsigned todo = __ballot_sync(0xffffffffu, pending);
+    while (todo) {  // RPS non-core rows of this warp at a time, G lanes each
+      const int slot = lane / G;
+      unsigned t = todo;
+      for (int s2 = 0; s2 < slot && t; ++s2) t &= t - 1;  // the slot-th pending row
+      const int r = t ? __ffs(t) - 1 : -1;
+      for (int s2 = 0; s2 < RPS && todo; ++s2) todo &= todo - 1;
+      if (r < 0) continue;  // the whole group idles this step
+      const int64_t ii = base + r;
+      const int32_t* nr = nbr + ii * k;
+      const float* dr = dist + ii * k;
+      int32_t lab = -1;
+      bool decided = false;
+      for (int c0 = 0; c0 < k && !decided; c0 += 4 * G) {
+        const int c = c0 + 4 * sub;
+        int32_t J[4];
+        float w[4];
+        if (VEC && c + 4 <= k) {
+          const int4 j4 = __ldcs(reinterpret_cast<const int4*>(nr + c));
+          const float4 w4 = __ldcs(reinterpret_cast<const float4*>(dr + c));
+          J[0] = j4.x; J[1] = j4.y; J[2] = j4.z; J[3] = j4.w;
+          w[0] = w4.x; w[1] = w4.y; w[2] = w4.z; w[3] = w4.w;
+        } else {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const bool in = c + j < k;
+            J[j] = in ? __ldcs(nr + c + j) : -1;
+            w[j] = in ? __ldcs(dr + c + j) : __int_as_float(0x7f800000);
+          }
+        }
+        int ev = 4;
+        bool hit = false;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          const bool in = c + j < k;
-          J[j] = in ? __ldcs(nr + c + j) : -1;
-          w[j] = in ? __ldcs(dr + c + j) : __int_as_float(0x7f800000);
+          if (ev < 4) continue;
+          if (c + j >= k) { ev = j; break; }  // row end: as beyond eps
+          if (!(w[j] <= eps)) { ev = j; continue; }
+          const int64_t Jj = J[j];
+          if (Jj >= 0 && Jj < N && is_core(bits, Jj)) { ev = j; hit = true; lab = (int32_t)Jj; }
+        }
+        const unsigned any = __ballot_sync(gmask, ev < 4) & gmask;
+        if (any) {
+          decided = true;
+          if (lane == __ffs(any) - 1) labels[ii] = hit ? comp[lab] : -1;
         }
       }
-      // this lane's first event: 0..3 = index, hit = core neighbour within eps
-      int ev = 4;
-      bool hit = false;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        if (ev < 4) continue;
-        if (c + j >= k) { ev = j; break; }  // row end: treated as "beyond eps"
-        if (!(w[j] <= eps)) { ev = j; continue; }
-        const int64_t Jj = J[j];
-        if (Jj >= 0 && Jj < N && is_core(bits, Jj)) { ev = j; hit = true; lab = (int32_t)Jj; }
-      }
-      const unsigned any = __ballot_sync(gmask, ev < 4) & gmask;
-      if (any) {
-        decided = true;
-        if (lane == __ffs(any) - 1) labels[i] = hit ? comp[lab] : -1;
-      }
+      if (!decided && sub == 0) labels[ii] = -1;
     }
-    if (!decided && sub == 0) labels[i] = -1;
   }
 }
 
@@ -3151,10 +3162,10 @@ kdb_status kdb_label(const kdb_graph* g, float eps, const uint32_t* core_bits, c
   if (g->n_rows == 0) return KDB_OK;
   cudaStream_t st = (cudaStream_t)stream;
   if (g->k_max % 4 == 0)
-    LAUNCH(k_label<true>, grid_for(g->n_rows * kLabelG), kThreads, st, g->nbr, g->dist, g->n_rows, g->k_max, eps,
+    LAUNCH(k_label<true>, grid_for(g->n_rows), kThreads, st, g->nbr, g->dist, g->n_rows, g->k_max, eps,
            g->row_begin, g->n_total, core_bits, comp, labels);
   else
-    LAUNCH(k_label<false>, grid_for(g->n_rows * kLabelG), kThreads, st, g->nbr, g->dist, g->n_rows, g->k_max, eps,
+    LAUNCH(k_label<false>, grid_for(g->n_rows), kThreads, st, g->nbr, g->dist, g->n_rows, g->k_max, eps,
            g->row_begin, g->n_total, core_bits, comp, labels);
   KDB_CUDA(cudaGetLastError());
   if (g_prof.on) {

@@ -341,7 +341,7 @@ def test_filter_fast_path_toggle(c1_graph, fast, light, monkeypatch):
     assert_parity(got2, oracle_run(nbr2, dist2, 8, eps2))
 
 
-@pytest.mark.parametrize("k", [20, 24, 28, 100])
+@pytest.mark.parametrize("k", [20, 24, 28, 37, 100, 130])
 def test_wide_rows_exact(k):
     """k % 4 == 0 and k >= 20: the light ELL is read with 32-byte sector loads
     (rows start at a 32-B boundary or 16 B past one)."""
