@@ -54,6 +54,9 @@ def parse():
     ap.add_argument("--stage", default="cluster", choices=["cluster", "knng"],
                     help="knng: time the exact kNN-graph builder (SURVEY.md 8(f) NEXT 3) on the points of "
                          "--config instead of the clustering stage; compare with Table 2 (PAPER.md:21-36)")
+    ap.add_argument("--nccl1", action="store_true",
+                    help="N=1 through a 1-rank NCCL communicator with every collective issued "
+                         "(KDB_NCCL_FORCE=1): the multi-rank host path and its per-round syncs")
     ap.add_argument("--inexact", type=int, default=0,
                     help="also time the paper's inexact MST over P contiguous groups (kdb_mst_inexact, "
                          "SURVEY.md 8(f) NEXT 2) and compare it with the exact step; N=1 only")
@@ -276,6 +279,9 @@ def run_ours(args):
         W["dist"] = W["dist"][rb:re_].clone()
         torch.cuda.empty_cache()
     comm = kdb.Comm.nccl(rank, world) if world > 1 else None
+    if args.nccl1 and world == 1:
+        os.environ["KDB_NCCL_FORCE"] = "1"
+        comm = kdb.Comm.nccl_single()
     ec, eps_list = stage_params(args, W)
     kc = ec or k
     g = kdb.Graph(W["nbr"], W["dist"], n_total=N, row_begin=rb, exact=not args.general, edge_cols=ec)
@@ -396,7 +402,9 @@ def run_ours(args):
                 "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "f32", "data": "synthetic",
                 "config": dict(workload_desc(args.config, W, args.scale),
-                               parallelism=f"row-partitioned x{world}", exact_graph=not args.general,
+                               parallelism=f"row-partitioned x{world}" + (" (1-rank NCCL, collectives forced)"
+                                                                           if args.nccl1 and world == 1 else ""),
+                               exact_graph=not args.general,
                                **stage_desc(ec, eps_list, W)),
                 "roofline": roof,
                 "stage_roofline": {"t_min_ms": t_min_ms, "frac": t_min_ms / ms,

@@ -2153,17 +2153,28 @@ void rank_ranges(const kdb_graph* g, kdb_comm* comm, std::vector<int64_t>& rb, s
   }
 }
 
+// Collectives run with a real NCCL communicator of > 1 rank -- or, with
+// KDB_NCCL_FORCE=1 (tests), on a 1-rank NCCL communicator too, so one GPU runs
+// the multi-rank host logic (exact per-round counts, agreed branches) through
+// real NCCL calls.
+bool multi_rank(const kdb_comm* comm) {
+  if (!comm || comm->kind != 1) return false;
+  if (comm->nranks > 1) return true;
+  const char* f = getenv("KDB_NCCL_FORCE");
+  return f && atoi(f) != 0;
+}
+
 kdb_status allreduce_min_u64(kdb_comm* comm, uint64_t* p, int64_t n, cudaStream_t st) {
-  if (!comm || comm->kind != 1 || comm->nranks == 1 || n <= 0) return KDB_OK;
+  if (!multi_rank(comm) || n <= 0) return KDB_OK;
   return nccl_check(g_nccl.AllReduce(p, p, (size_t)n, ncclUint64, ncclMin, comm->nccl, st), "ncclAllReduce(u64,min)");
 }
 kdb_status allreduce_min_u32(kdb_comm* comm, uint32_t* p, int64_t n, cudaStream_t st) {
-  if (!comm || comm->kind != 1 || comm->nranks == 1 || n <= 0) return KDB_OK;
+  if (!multi_rank(comm) || n <= 0) return KDB_OK;
   return nccl_check(g_nccl.AllReduce(p, p, (size_t)n, ncclUint32, ncclMin, comm->nccl, st), "ncclAllReduce(u32,min)");
 }
 
 kdb_status allreduce_max_u32(kdb_comm* comm, uint32_t* p, int64_t n, cudaStream_t st) {
-  if (!comm || comm->kind != 1 || comm->nranks == 1 || n <= 0) return KDB_OK;
+  if (!multi_rank(comm) || n <= 0) return KDB_OK;
   return nccl_check(g_nccl.AllReduce(p, p, (size_t)n, ncclUint32, ncclMax, comm->nccl, st), "ncclAllReduce(u32,max)");
 }
 
@@ -2225,7 +2236,7 @@ kdb_status pick_tau(Mst& m, int m0, float* tau_out) {
     memcpy(&tb, &t, 4);
     if (tb == 0x80000000u) tb = 0u;
   }
-  if (m.comm && m.comm->kind == 1 && m.comm->nranks > 1) {
+  if (multi_rank(m.comm)) {
     uint32_t* d = reinterpret_cast<uint32_t*>(L.tau_sample);
     KDB_CUDA(cudaMemcpyAsync(d, &tb, 4, cudaMemcpyHostToDevice, m.st));
     KDB_TRY(allreduce_min_u32(m.comm, d, 1, m.st));
@@ -2278,7 +2289,7 @@ kdb_status rows_phase(Mst& m, float eps_run) {
   // exact mode: round 1 (singleton components) is fused into the ELL pass; a
   // single rank also packs (K, B, kmin) per component for the round-1 hook
   const bool fuse1 = !general && use_compact && env_int("KDB_FUSE1", 1) != 0;
-  const bool packed1 = fuse1 && L.ranks.size() == 1 && !(comm && comm->kind == 1 && comm->nranks > 1) &&
+  const bool packed1 = fuse1 && L.ranks.size() == 1 && !(multi_rank(comm)) &&
                        env_int("KDB_PACK1", 1) != 0;
   if (!general)  // hook targets of round 1 (written by the round-1 offers)
     for (auto& R : L.ranks) LAUNCH(k_fill_i32, grid_for(C), kThreads, st, R.tgt, C, INT32_MAX);
@@ -2350,7 +2361,7 @@ kdb_status rows_phase(Mst& m, float eps_run) {
   bool any_compact = false;
   for (auto& R : L.ranks) any_compact |= R.compact;
   const bool fused = fuse1 && any_compact;
-  const bool sync_each = comm && comm->kind == 1 && comm->nranks > 1;
+  const bool sync_each = multi_rank(comm);
   int cur = fused ? 1 : 0;  // fused round 1: its OUTPUT list is act[0] already
   int par = 0;              // component count ping-pong: Cs[par] current
   {
@@ -2711,7 +2722,7 @@ kdb_status filter_phase(Mst& m, float eps, bool* overflow) {
     tot += n;
     if (n > R.hs_cap) over = 1;
   }
-  if (m.comm && m.comm->kind == 1 && m.comm->nranks > 1) {  // every rank must take the same branch
+  if (multi_rank(m.comm)) {  // every rank must take the same branch
     uint32_t* d = L.ranks[0].n_hs_dev + 1;
     KDB_CUDA(cudaMemcpyAsync(d, &over, 4, cudaMemcpyHostToDevice, st));
     KDB_TRY(allreduce_max_u32(m.comm, d, 1, st));
@@ -2931,7 +2942,7 @@ kdb_status kdb_core_mark(const kdb_graph* g, int32_t M, float eps, uint32_t* cor
     KDB_CUDA(cudaGetLastError());
   }
   // ranks own disjoint bits: SUM == OR
-  if (comm && comm->kind == 1 && comm->nranks > 1)
+  if (multi_rank(comm))
     KDB_TRY(nccl_check(g_nccl.AllReduce(core_bits, core_bits, (size_t)nwords, ncclUint32, ncclSum,
                                         comm->nccl, st), "ncclAllReduce(core bits)"));
   if (g_prof.on) {  // profiling mode only: resolve timings now (synchronises)

@@ -128,6 +128,16 @@ class Comm:
                "kdb_comm_create_nccl")
         return cls(h, nranks, rank, "nccl")
 
+    @classmethod
+    def nccl_single(cls) -> "Comm":
+        """A 1-rank NCCL communicator without torch.distributed (tests, bench
+        --nccl1; with KDB_NCCL_FORCE=1 the library issues every collective)."""
+        b = (C.c_ubyte * 128)()
+        _check(lib().kdb_nccl_unique_id(C.cast(b, C.c_void_p)), "kdb_nccl_unique_id")
+        h = C.c_void_p()
+        _check(lib().kdb_comm_create_nccl(C.byref(h), C.cast(b, C.c_void_p), 0, 1), "kdb_comm_create_nccl")
+        return cls(h, 1, 0, "nccl")
+
     def close(self):
         if self.handle is not None:
             lib().kdb_comm_destroy(self.handle)

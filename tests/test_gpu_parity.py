@@ -403,3 +403,29 @@ def test_c1_sparse_ids(c1_graph, sparse, P, monkeypatch):
             eps = eps_from_graph(dist, 8, f)
             got = run_gpu(nbr, dist, 8, eps, exact=exact, comm=kdb.Comm.sim(P) if P else None)
             assert_parity(got, oracle_run(nbr, dist, 8, eps))
+
+
+@pytest.mark.parametrize("exact", [False, True])
+def test_nccl_communicator_one_rank(c1_graph, exact, monkeypatch):
+    """A real NCCL communicator (1 rank; KDB_NCCL_FORCE=1 issues every collective
+    anyway): the multi-rank host logic -- exact per-round counts (sync_each),
+    all-reduced core bits / keys / ties / targets / tau / overflow branch, the
+    heavy-phase exchanges -- runs through NCCL on one GPU and gives the oracle's
+    result."""
+    import ctypes as C
+    import paper_2009_04552_b200 as kdb
+    monkeypatch.setenv("KDB_NCCL_FORCE", "1")
+    b = (C.c_ubyte * 128)()
+    assert kdb.lib().kdb_nccl_unique_id(C.cast(b, C.c_void_p)) == 0
+    h = C.c_void_p()
+    assert kdb.lib().kdb_comm_create_nccl(C.byref(h), C.cast(b, C.c_void_p), 0, 1) == 0
+    comm = kdb.Comm(h, 1, 0, "nccl")  # == kdb.Comm.nccl_single()
+    X, nbr, dist = c1_graph
+    try:
+        for light in ("2", "10"):
+            monkeypatch.setenv("KDB_LIGHT", light)
+            for f in (1.0, 1.5):
+                eps = eps_from_graph(dist, 8, f)
+                assert_parity(run_gpu(nbr, dist, 8, eps, exact=exact, comm=comm), oracle_run(nbr, dist, 8, eps))
+    finally:
+        comm.close()
