@@ -429,3 +429,20 @@ def test_nccl_communicator_one_rank(c1_graph, exact, monkeypatch):
                 assert_parity(run_gpu(nbr, dist, 8, eps, exact=exact, comm=comm), oracle_run(nbr, dist, 8, eps))
     finally:
         comm.close()
+
+
+@pytest.mark.parametrize("k", [1, 2, 3, 5])
+def test_narrow_rows(k):
+    """Rows narrower than the light ELL (kW = 16) and than one 4-entry chunk;
+    M = k and M = 1; general and exact mode; sim ranks."""
+    import paper_2009_04552_b200 as kdb
+    rng = np.random.default_rng(100 + k)
+    X = rng.standard_normal((1500, 2)).astype(np.float32)
+    nbr, dist = knn_bruteforce(X, k)
+    for M in sorted({1, k}):
+        for f in (1.0, 3.0):
+            eps = eps_from_graph(dist, M, f)
+            exp = oracle_run(nbr, dist, M, eps)
+            for exact in (False, True):
+                assert_parity(run_gpu(nbr, dist, M, eps, exact=exact), exp)
+            assert_parity(run_gpu(nbr, dist, M, eps, comm=kdb.Comm.sim(3)), exp)
