@@ -276,6 +276,13 @@ __device__ __forceinline__ bool is_core(const uint32_t* __restrict__ bits, int64
 template <typename T>
 __device__ __forceinline__ T gat(const T* p) { return __ldcg(p); }
 
+// atomicMin preceded by a plain read: an offer that cannot lower the current
+// key issues no atomic (same-address atomics serialise at the L2 slice when
+// many rows offer to one component).  A stale read only lets an atomic through.
+__device__ __forceinline__ void min_offer(unsigned long long* p, unsigned long long x) {
+  if (x < __ldcg(p)) atomicMin(p, x);
+}
+
 __device__ __forceinline__ uint64_t pack_key(uint32_t wbits, uint32_t a) {
   return ((uint64_t)wbits << 32) | a;
 }
@@ -633,7 +640,8 @@ __global__ void __launch_bounds__(256) k_offer_round(const int32_t* __restrict__
                                                      uint32_t n_in, Rec* __restrict__ act_out,
                                                      uint32_t* __restrict__ n_out, Offer* __restrict__ offers,
                                                      unsigned long long* __restrict__ Kc,
-                                                     unsigned long long* __restrict__ n_entries, const uint32_t* __restrict__ n_in_p = nullptr) {
+                                                     unsigned long long* __restrict__ n_entries, const uint32_t* __restrict__ n_in_p = nullptr,
+                                                     int precheck = 0) {
   if (n_in_p) n_in = *n_in_p;
   unsigned long long reads = 0;
   for (uint32_t base = blockIdx.x * blockDim.x; base < n_in; base += gridDim.x * blockDim.x) {
@@ -647,7 +655,10 @@ __global__ void __launch_bounds__(256) k_offer_round(const int32_t* __restrict__
       cv = gat(comp + v);
       const int64_t i = (int64_t)v - row_begin;
       r = scan_row<VEC, false>(nbr + i * ld, dist + i * ld, k, eps, v, cv, a.h, N, comp, 0, reads);
-      if (r.found) atomicMin(Kc + cv, (unsigned long long)r.best);
+      if (r.found) {
+        if (precheck) min_offer(Kc + cv, (unsigned long long)r.best);
+        else atomicMin(Kc + cv, (unsigned long long)r.best);
+      }
     }
     const uint32_t slot = block_reserve(n_out, r.found);
     if (r.found) {
@@ -982,7 +993,8 @@ __global__ void __launch_bounds__(256) k_light_round(const int4* __restrict__ LE
                                                      Rec* __restrict__ act_out, uint32_t* __restrict__ n_out,
                                                      uint32_t* __restrict__ grab, Offer* __restrict__ offers,
                                                      unsigned long long* __restrict__ Kc,
-                                                     unsigned long long* __restrict__ n_entries, const uint32_t* __restrict__ n_in_p = nullptr) {
+                                                     unsigned long long* __restrict__ n_entries, const uint32_t* __restrict__ n_in_p = nullptr,
+                                                     int precheck = 0) {
   if (n_in_p) n_in = *n_in_p;
   __shared__ __align__(16) Rec s_rec[kChunk];
   __shared__ __align__(16) Offer s_off[kChunk];
@@ -1003,7 +1015,8 @@ __global__ void __launch_bounds__(256) k_light_round(const int4* __restrict__ LE
       const RowScan r = scan_ell<false, GW>(LE + i * (kW / 2), nbr + i * ld, dist + i * ld, k, eps, v, cv, a.y, N,
                                             comp, 0, reads);
       if (r.found) {
-        atomicMin(Kc + cv, (unsigned long long)r.best);
+        if (precheck) min_offer(Kc + cv, (unsigned long long)r.best);
+        else atomicMin(Kc + cv, (unsigned long long)r.best);
         const uint32_t j = atomicAdd(&s_n, 1u);
         s_rec[j] = Rec{v, r.h};
         s_off[j] = Offer{cv, r.bestb, r.best};
@@ -1858,8 +1871,8 @@ __global__ void k_hedge_offer(const HEdge* __restrict__ E, uint32_t n, const int
     const bool live = x != y;
     keep[s] = live;
     if (live) {
-      atomicMin(Kc + x, (unsigned long long)e.key);
-      atomicMin(Kc + y, (unsigned long long)e.key);
+      min_offer(Kc + x, (unsigned long long)e.key);
+      min_offer(Kc + y, (unsigned long long)e.key);
     }
   }
 }
@@ -2457,6 +2470,16 @@ kdb_status rows_phase(Mst& m, float eps_run) {
     KDB_CUDA(cudaEventCreate(&e0));
     ev_rnd.push_back(e0);
     KDB_CUDA(cudaEventRecord(e0, st));
+    // offers read the current key before their atomicMin once many rows offer
+    // to each component (same-address atomics serialise; early rounds have
+    // about one row per component and only pay the extra read)
+    int precheck = 0;
+    {
+      uint64_t live = 0;
+      for (size_t r = 0; r < nr; ++r) live += na_ub[r];
+      const int pc = env_int("KDB_PRECHECK", -1);
+      precheck = pc >= 0 ? pc : (live > 8 * (uint64_t)std::max<int64_t>(C_ub, 1) ? 1 : 0);
+    }
     // a3: offers (rows, then in-lists), per rank, into that rank's Kc partial
     for (size_t r = 0; r < nr; ++r) {
       RankState& R = L.ranks[r];
@@ -2477,7 +2500,7 @@ kdb_status rows_phase(Mst& m, float eps_run) {
 #define KDB_LR_LAUNCH(GW)                                                                                       \
   LAUNCH(k_light_round<GW>, grid_for(na_ub[r]), kThreads, st, R.LE, R.nbr, R.dist, ld, k, eps_run, R.row_begin, N, \
          comp, R.act[cur], na_ub[r], R.act[cur ^ 1], nout, &R.ctr->grab, R.offers, (unsigned long long*)R.Kc,      \
-         &L.ctr->entries, nin)
+         &L.ctr->entries, nin, precheck)
           if (gw == 1) KDB_LR_LAUNCH(1);
           else if (gw == 2) KDB_LR_LAUNCH(2);
           else KDB_LR_LAUNCH(4);
@@ -2497,11 +2520,11 @@ kdb_status rows_phase(Mst& m, float eps_run) {
           if (vec)
             LAUNCH(k_offer_round<true>, grid_for(na_ub[r]), kThreads, st, R.nbr, R.dist, ld, k, eps_run, R.row_begin, N,
                    comp, R.act[cur], na_ub[r], R.act[cur ^ 1], nout, R.offers, (unsigned long long*)R.Kc,
-                   &L.ctr->entries, nin);
+                   &L.ctr->entries, nin, precheck);
           else
             LAUNCH(k_offer_round<false>, grid_for(na_ub[r]), kThreads, st, R.nbr, R.dist, ld, k, eps_run, R.row_begin,
                    N, comp, R.act[cur], na_ub[r], R.act[cur ^ 1], nout, R.offers, (unsigned long long*)R.Kc,
-                   &L.ctr->entries, nin);
+                   &L.ctr->entries, nin, precheck);
         }
       }
       if (general && ni_ub[r])

@@ -446,3 +446,19 @@ def test_narrow_rows(k):
             for exact in (False, True):
                 assert_parity(run_gpu(nbr, dist, M, eps, exact=exact), exp)
             assert_parity(run_gpu(nbr, dist, M, eps, comm=kdb.Comm.sim(3)), exp)
+
+
+@pytest.mark.parametrize("pre", ["0", "1"])
+@pytest.mark.parametrize("case", RANDOM_CASES)
+def test_offer_precheck_toggle(case, pre, monkeypatch):
+    """Offers read the current key before their atomicMin (KDB_PRECHECK forces
+    it on / off; by default it switches on once live rows outnumber the
+    components 8 to 1) -- the same forest either way, in every round kernel."""
+    monkeypatch.setenv("KDB_PRECHECK", pre)
+    n, k, M, seed, levels, sym, pad, zero, local, q = case
+    nbr, dist = random_graph(n, k, seed, levels=levels, symmetric=sym, pad_frac=pad, zero_frac=zero, local=local)
+    eps = np.float32(np.quantile(dist[np.isfinite(dist)].astype(np.float64), q))
+    exp = oracle_run(nbr, dist, M, eps)
+    for compact in ("0", "1"):
+        monkeypatch.setenv("KDB_COMPACT", compact)
+        assert_parity(run_gpu(nbr, dist, M, eps, exact=False), exp)
