@@ -14,3 +14,4 @@ echo "ncu full rc=$?"
 ncu --set full --clock-control none --import-source on -k regex:"k_filter|k_label|k_relabel|k_tie" -s 0 -c 4 \
     -o gpurun_out/prof2_${TAG} python bench.py $ARGS > gpurun_out/ncu_full2_${TAG}.log 2>&1
 echo "ncu full2 rc=$?"
+# part B (the light rounds, filter, label): tools/gpu_profile_round_b.sh -- separate call (64 MiB copy-back cap)
