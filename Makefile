@@ -10,7 +10,7 @@ ORACLE_SO := oracle/liboracle.so
 
 all: $(KDB_SO) $(ORACLE_SO) $(KNNG_SO)
 
-$(KDB_SO): paper_2009_04552_b200/csrc/kdb.cu include/kdb.h
+$(KDB_SO): paper_2009_04552_b200/csrc/kdb.cu $(wildcard paper_2009_04552_b200/csrc/kdb_*.cuh) include/kdb.h
 	@mkdir -p $(dir $@)
 	$(NVCC) $(NVFLAGS) -o $@ $< -ldl
 

@@ -1,0 +1,913 @@
+// kdb_host.cuh -- host side: workspace layout, the rows / filter / heavy phases and the round loop
+// Part of kdb.cu's single translation unit: included inside its anonymous
+// namespace, after kdb.cu's helpers; not a standalone header.
+#pragma once
+
+// ============================================================================
+// host side
+// ============================================================================
+// exact value of sum_e bk[e] * 2^(max(e,1) - 150), rounded once to double
+double exact_bucket_sum(const unsigned long long* bk) {
+  uint64_t L[7] = {0, 0, 0, 0, 0, 0, 0};  // little-endian limbs, value * 2^149
+  for (int e = 0; e < 256; ++e) {
+    if (!bk[e]) continue;
+    const int sh = (e ? e : 1) - 1;  // 2^(max(e,1)-150) = 2^(sh) * 2^-149
+    const int q = sh / 64, r = sh % 64;
+    unsigned __int128 add0 = (unsigned __int128)bk[e] << r;  // up to 128 bits
+    uint64_t parts[3] = {(uint64_t)add0, (uint64_t)(add0 >> 64), 0};
+    unsigned __int128 carry = 0;
+    for (int j = q; j < 7; ++j) {
+      unsigned __int128 s = (unsigned __int128)L[j] + carry + (j - q < 3 ? parts[j - q] : 0);
+      L[j] = (uint64_t)s;
+      carry = s >> 64;
+    }
+  }
+  int top = -1;
+  for (int j = 6; j >= 0; --j)
+    if (L[j]) { top = j * 64 + 63 - __builtin_clzll(L[j]); break; }
+  if (top < 0) return 0.0;
+  auto bit = [&](int p) -> int { return p < 0 ? 0 : (int)((L[p / 64] >> (p % 64)) & 1u); };
+  // 53-bit mantissa [top-52, top], round bit top-53, sticky below
+  uint64_t man = 0;
+  for (int p = top; p > top - 53; --p) man = (man << 1) | (uint64_t)bit(p);
+  const int rb = bit(top - 53);
+  bool sticky = false;
+  for (int p = top - 54; p >= 0 && !sticky; --p) sticky = bit(p);
+  if (rb && (sticky || (man & 1u))) ++man;  // round to nearest even
+  return ldexp((double)man, top - 52 - 149);
+}
+
+// heavy-phase survivor capacity per rank (edges); beyond it kdb_mst falls back
+// to plain rows-Boruvka over the whole candidate graph (still exact)
+constexpr int kTauSamples = 8192;
+inline int64_t survivor_cap(int64_t n_rows, int64_t k) {
+  return std::max<int64_t>(n_rows / 4, std::min<int64_t>(n_rows * k / 4, (int64_t)1 << 24)) + 65536;
+}
+
+struct Carver {
+  char* base;
+  size_t off = 0, cap;
+  bool dry;
+  template <typename T>
+  T* take(size_t n) {
+    off = (off + 255) & ~size_t(255);
+    T* p = dry ? nullptr : reinterpret_cast<T*>(base + off);
+    off += n * sizeof(T);
+    return p;
+  }
+};
+
+struct RankState {
+  int64_t row_begin = 0, n_rows = 0;
+  const int32_t* nbr = nullptr;
+  const float* dist = nullptr;
+  Rec* act[2] = {nullptr, nullptr};  // active rows (v, head), ping-pong
+  uint32_t n_act = 0;                 // live rows in act[cur]
+  bool compact = false;               // rows phase reads the light ELL (else the graph rows)
+  int4* LE = nullptr;                 // light ELL [n_rows][kW] (J, w bits) pairs
+  // offers: [0, n_rows) from rows (same slot as the row's next record),
+  // [n_rows, n_rows + N) from in-lists (general mode)
+  Offer* offers = nullptr;
+  int64_t off_cap_rows = 0;
+  // per-rank partial Kc/Bc (sim ranks > 0) -- else alias the shared ones
+  uint64_t* Kc = nullptr;
+  uint32_t* Bc = nullptr;
+  int32_t* tgt = nullptr;
+  // in-edge lists (general mode)
+  unsigned long long* in_off = nullptr;
+  int32_t* in_len = nullptr;
+  int32_t* in_src = nullptr;
+  float* in_w = nullptr;
+  int32_t* in_act[2] = {nullptr, nullptr};
+  uint32_t n_in_act = 0;
+  RoundCounters* ctr = nullptr;  // per-rank counters (act/off)
+  // heavy phase: survivors (ping-pong) and their keep flags
+  HEdge* hs[2] = {nullptr, nullptr};
+  uint8_t* hkeep = nullptr;
+  uint32_t hs_cap = 0, n_hs = 0;
+  uint32_t* n_hs_dev = nullptr;  // [2]: filter count, compaction count
+};
+
+struct Layout {
+  // shared
+  uint32_t* woff;
+  int32_t *cmin, *cmin2, *parent, *rootof, *newid, *flag;
+  uint32_t *kmin, *kmin2;
+  uint64_t* Kc;
+  uint32_t* Bc;
+  int32_t* tgt;
+  int all_core = 0;
+  uint64_t* e_key;
+  float* e_w;
+  unsigned long long* buckets;
+  int4* rec1;       // round 1, single rank, exact mode: packed (K, B, kmin) per component
+  int32_t* hcomp;   // heavy phase: light component -> heavy component
+  int32_t* dom;     // filter fast path: dominant component per id block
+  uint32_t* bloom;  // filter fast path: Bloom filter of the exceptions
+  unsigned long long* fcount;  // [0] exceptions, [1] slow-path entries
+  float* tau_sample;
+  RoundCounters* ctr;
+  void* cub_tmp;
+  size_t cub_bytes;
+  std::vector<RankState> ranks;
+};
+
+size_t cub_tmp_bytes(int64_t N, int64_t cap_edges) {
+  size_t a = 0, b = 0, c = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, a, (const int32_t*)nullptr, (int32_t*)nullptr, (int)std::max<int64_t>(N + 1, 1));
+  cub::DeviceScan::ExclusiveSum(nullptr, b, (const unsigned long long*)nullptr,
+                                (unsigned long long*)nullptr, (int)std::max<int64_t>(N + 1, 1));
+  cub::DeviceRadixSort::SortPairs(nullptr, c, (const uint32_t*)nullptr, (uint32_t*)nullptr,
+                                  (const unsigned long long*)nullptr, (unsigned long long*)nullptr,
+                                  (int)std::max<int64_t>(cap_edges, 1));
+  size_t f = 0;
+  size_t h3 = 0;
+  cub::DeviceSelect::Flagged(nullptr, h3, (const HEdge*)nullptr, (const uint8_t*)nullptr, (HEdge*)nullptr,
+                             (uint32_t*)nullptr, (int)std::min<int64_t>(survivor_cap(N, 65535) + 1, INT32_MAX));
+  f = std::max(f, h3);
+  return std::max(std::max(a, f), std::max(b, c)) + 256;
+}
+
+// carve the workspace; returns bytes needed
+size_t carve(Layout& L, char* base, bool dry, int64_t N, int nr, const int64_t* rb, const int64_t* rn,
+             bool general, int32_t k, int64_t hs_cap_override = -1) {
+  Carver cv{base, 0, 0, dry};
+  const int64_t nwords = (N + 31) / 32;
+  L.woff = cv.take<uint32_t>(nwords + 1);
+  L.cmin = cv.take<int32_t>(N + 1);
+  L.cmin2 = cv.take<int32_t>(N + 1);
+  L.parent = cv.take<int32_t>(N + 1);
+  L.rootof = cv.take<int32_t>(N + 1);
+  L.newid = cv.take<int32_t>(N + 1);
+  L.flag = cv.take<int32_t>(N + 1);
+  L.kmin = cv.take<uint32_t>(N + 1);
+  L.kmin2 = cv.take<uint32_t>(N + 1);
+  L.Kc = cv.take<uint64_t>(N + 1);
+  L.Bc = cv.take<uint32_t>(N + 1);
+  L.tgt = cv.take<int32_t>(N + 1);
+  L.e_key = cv.take<uint64_t>(N + 1);
+  L.e_w = cv.take<float>(N + 1);
+  L.buckets = cv.take<unsigned long long>(256);
+  L.rec1 = general ? nullptr : cv.take<int4>(N + 1);
+  L.hcomp = cv.take<int32_t>(N + 1);
+  L.dom = cv.take<int32_t>(kDomMax);
+  L.bloom = cv.take<uint32_t>(kBloomBits / 32);
+  L.fcount = cv.take<unsigned long long>(2);
+  L.tau_sample = cv.take<float>(kTauSamples);
+  L.ctr = cv.take<RoundCounters>(1);
+  L.cub_bytes = cub_tmp_bytes(N, N + 1);
+  L.cub_tmp = cv.take<char>(L.cub_bytes);
+  L.ranks.assign(nr, RankState());
+  for (int r = 0; r < nr; ++r) {
+    RankState& R = L.ranks[r];
+    R.row_begin = rb[r];
+    R.n_rows = rn[r];
+    const int64_t n = std::max<int64_t>(rn[r], 1);
+    R.act[0] = cv.take<Rec>(n);
+    R.act[1] = cv.take<Rec>(n);
+    R.LE = cv.take<int4>(n * (kW / 2));
+    R.off_cap_rows = n;
+    R.offers = cv.take<Offer>(general ? n + N : n);
+    R.ctr = cv.take<RoundCounters>(1);
+    if (r > 0) {
+      R.Kc = cv.take<uint64_t>(N + 1);
+      R.Bc = cv.take<uint32_t>(N + 1);
+      R.tgt = cv.take<int32_t>(N + 1);
+    } else {
+      R.Kc = L.Kc;
+      R.Bc = L.Bc;
+      R.tgt = L.tgt;
+    }
+    R.hs_cap = (uint32_t)std::min<int64_t>(hs_cap_override >= 0 ? std::max<int64_t>(hs_cap_override, 1)
+                                                                   : survivor_cap(n, k),
+                                           (int64_t)UINT32_MAX - 1);
+    R.hs[0] = cv.take<HEdge>(R.hs_cap);
+    R.hs[1] = cv.take<HEdge>(R.hs_cap);
+    R.hkeep = cv.take<uint8_t>(R.hs_cap);
+    R.n_hs_dev = cv.take<uint32_t>(2);
+    if (general) {
+      R.in_off = cv.take<unsigned long long>(N + 1);
+      R.in_len = cv.take<int32_t>(N);
+      R.in_src = cv.take<int32_t>(n * (int64_t)k);
+      R.in_w = cv.take<float>(n * (int64_t)k);
+      R.in_act[0] = cv.take<int32_t>(N);
+      R.in_act[1] = cv.take<int32_t>(N);
+    }
+  }
+  return cv.off + 256;
+}
+
+kdb_status validate_graph(const kdb_graph* g) {
+  if (!g) return set_err(KDB_EINVAL, "graph is NULL");
+  if (g->n_total < 0 || g->n_total >= (int64_t)INT32_MAX)
+    return set_err(KDB_EINVAL, "n_total out of range [0, 2^31-1)");
+  if (g->k_max < 1 || g->k_max > 65535) return set_err(KDB_EINVAL, "k_max must be in [1, 65535]");
+  if (g->n_rows < 0 || g->row_begin < 0 || g->row_begin + g->n_rows > g->n_total)
+    return set_err(KDB_EINVAL, "rank row range outside [0, n_total)");
+  if (g->n_rows > 0 && (!g->nbr || !g->dist)) return set_err(KDB_EINVAL, "nbr/dist is NULL");
+  if (((uintptr_t)g->nbr & 15u) || ((uintptr_t)g->dist & 15u))
+    return set_err(KDB_EINVAL, "nbr/dist must be 16-byte aligned");
+  if (g->flags & ~KDB_GRAPH_EXACT) return set_err(KDB_EINVAL, "unknown graph flags");
+  if (g->edge_cols < 0 || g->edge_cols > g->k_max) return set_err(KDB_EINVAL, "edge_cols must be in [0, k_max]");
+  return KDB_OK;
+}
+
+kdb_status validate_eps(float eps) {
+  if (!(eps > 0.0f) || !(eps < __builtin_inff())) return set_err(KDB_EINVAL, "eps must be in (0, +inf)");
+  return KDB_OK;
+}
+
+// rank ranges of the computation this process performs
+void rank_ranges(const kdb_graph* g, kdb_comm* comm, std::vector<int64_t>& rb, std::vector<int64_t>& rn) {
+  rb.clear();
+  rn.clear();
+  if (comm && comm->kind == 2) {
+    const int P = comm->nranks;
+    for (int r = 0; r < P; ++r) {
+      const int64_t b = g->n_rows * r / P, e = g->n_rows * (r + 1) / P;
+      rb.push_back(g->row_begin + b);
+      rn.push_back(e - b);
+    }
+  } else {
+    rb.push_back(g->row_begin);
+    rn.push_back(g->n_rows);
+  }
+}
+
+// Collectives run with a real NCCL communicator of > 1 rank -- or, with
+// KDB_NCCL_FORCE=1 (tests), on a 1-rank NCCL communicator too, so one GPU runs
+// the multi-rank host logic (exact per-round counts, agreed branches) through
+// real NCCL calls.
+bool multi_rank(const kdb_comm* comm) {
+  if (!comm || comm->kind != 1) return false;
+  if (comm->nranks > 1) return true;
+  const char* f = getenv("KDB_NCCL_FORCE");
+  return f && atoi(f) != 0;
+}
+
+kdb_status allreduce_min_u64(kdb_comm* comm, uint64_t* p, int64_t n, cudaStream_t st) {
+  if (!multi_rank(comm) || n <= 0) return KDB_OK;
+  return nccl_check(g_nccl.AllReduce(p, p, (size_t)n, ncclUint64, ncclMin, comm->nccl, st), "ncclAllReduce(u64,min)");
+}
+kdb_status allreduce_min_u32(kdb_comm* comm, uint32_t* p, int64_t n, cudaStream_t st) {
+  if (!multi_rank(comm) || n <= 0) return KDB_OK;
+  return nccl_check(g_nccl.AllReduce(p, p, (size_t)n, ncclUint32, ncclMin, comm->nccl, st), "ncclAllReduce(u32,min)");
+}
+
+kdb_status allreduce_max_u32(kdb_comm* comm, uint32_t* p, int64_t n, cudaStream_t st) {
+  if (!multi_rank(comm) || n <= 0) return KDB_OK;
+  return nccl_check(g_nccl.AllReduce(p, p, (size_t)n, ncclUint32, ncclMax, comm->nccl, st), "ncclAllReduce(u32,max)");
+}
+
+int env_int(const char* name, int dflt) {
+  const char* s = getenv(name);
+  return (s && *s) ? atoi(s) : dflt;
+}
+
+// One kdb_mst call: the workspace layout plus the phase bookkeeping.
+struct Mst {
+  Layout L;
+  const kdb_graph* g = nullptr;
+  kdb_comm* comm = nullptr;
+  cudaStream_t st = nullptr;
+  int64_t N = 0;
+  int32_t k = 0;   // candidate columns: edge_cols (kdb.h), else k_max
+  int32_t ld = 0;  // row stride k_max
+  const uint32_t* bits = nullptr;
+  int32_t* comp = nullptr;
+  bool general = false;
+  int64_t C = 0;         // components after the rows phase (light components under the filter)
+  int64_t C_heavy = -1;  // components after the heavy phase (-1: no heavy phase ran)
+  // bytes per rank carried by the MIN all-reduces over component arrays (issued
+  // with a communicator; counted either way): rows phase, heavy / cut phase
+  double payload_rows = 0, payload_heavy = 0;
+  int rounds = 0, stalls = 0, heavy_rounds = 0;
+  double t_init = 0, t_inlist = 0, t_min_edges = 0, t_contract = 0, t_filter = 0, t_heavy = 0;
+  unsigned long long entries = 0, survivors = 0, exceptions = 0, slow_entries = 0;
+  float tau = 0.f;
+  int fallback = 0;
+  cudaEvent_t ev[4];
+};
+
+float elapsed(cudaEvent_t a, cudaEvent_t b) {
+  float ms = 0;
+  cudaEventSynchronize(b);
+  cudaEventElapsedTime(&ms, a, b);
+  return ms;
+}
+
+// Light threshold: the median of column m0-1 over sampled local rows, made
+// global with an all-reduce MIN (all ranks must filter with the same tau).
+kdb_status pick_tau(Mst& m, int m0, float* tau_out) {
+  const kdb_graph* g = m.g;
+  Layout& L = m.L;
+  const int64_t n = g->n_rows;
+  uint32_t tb = kInfBits;
+  if (n > 0) {
+    const int64_t S = std::min<int64_t>(n, kTauSamples);
+    const int64_t stride = n / S;
+    LAUNCH(k_sample_col, grid_for(S), kThreads, m.st, g->dist, n, m.ld, m0 - 1, stride, S, L.tau_sample);
+    KDB_CUDA(cudaGetLastError());
+    std::vector<float> h(S);
+    KDB_CUDA(cudaMemcpyAsync(h.data(), L.tau_sample, S * sizeof(float), cudaMemcpyDeviceToHost, m.st));
+    KDB_CUDA(cudaStreamSynchronize(m.st));
+    std::nth_element(h.begin(), h.begin() + S / 2, h.end());
+    float t = h[S / 2];
+    if (!(t >= 0.f)) t = __builtin_inff();  // NaN guard
+    memcpy(&tb, &t, 4);
+    if (tb == 0x80000000u) tb = 0u;
+  }
+  if (multi_rank(m.comm)) {
+    uint32_t* d = reinterpret_cast<uint32_t*>(L.tau_sample);
+    KDB_CUDA(cudaMemcpyAsync(d, &tb, 4, cudaMemcpyHostToDevice, m.st));
+    KDB_TRY(allreduce_min_u32(m.comm, d, 1, m.st));
+    KDB_CUDA(cudaMemcpyAsync(&tb, d, 4, cudaMemcpyDeviceToHost, m.st));
+    KDB_CUDA(cudaStreamSynchronize(m.st));
+  }
+  memcpy(tau_out, &tb, 4);
+  return KDB_OK;
+}
+
+// a2-a8: rows-Boruvka over the candidate entries with w <= eps_run (from
+// singletons).  Leaves comp[] = dense component ids (0..C-1), L.cmin = minimum
+// core id per component, m.C.  Resets the MSF counter.
+kdb_status rows_phase(Mst& m, float eps_run) {
+  Layout& L = m.L;
+  kdb_comm* comm = m.comm;
+  cudaStream_t st = m.st;
+  const int64_t N = m.N;
+  const int32_t k = m.k;    // candidate columns (edge_cols)
+  const int32_t ld = m.ld;  // row stride
+  const uint32_t* core_bits = m.bits;
+  int32_t* comp = m.comp;
+  const bool general = m.general;
+  const bool vec = (ld % 4) == 0;
+  cudaEvent_t* ev = m.ev;
+  KDB_CUDA(cudaEventRecord(ev[0], st));
+
+  // ---- a2: dense component ids -------------------------------------------------
+  const int64_t nwords = (N + 31) / 32;
+  uint32_t* popc = reinterpret_cast<uint32_t*>(L.flag);  // scratch, nwords + 1 <= N + 1
+  KDB_CUDA(cudaMemsetAsync(popc + nwords, 0, sizeof(uint32_t), st));
+  KDB_CUDA(cudaMemsetAsync(L.ctr, 0, sizeof(RoundCounters), st));
+  LAUNCH(k_popc_words, grid_for(nwords), kThreads, st, core_bits, nwords, popc);
+  KDB_CUDA(cudaGetLastError());
+  size_t cb = L.cub_bytes;
+  { LaunchScope ls_("cub::DeviceScan", st, false); KDB_CUDA(cub::DeviceScan::ExclusiveSum(L.cub_tmp, cb, popc, L.woff, (int)(nwords + 1), st)); }
+  uint32_t C32 = 0;  // woff[nwords] = number of core points
+  KDB_CUDA(cudaMemcpyAsync(&C32, L.woff + nwords, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+  KDB_CUDA(cudaStreamSynchronize(st));
+  int64_t C = C32;
+  L.all_core = (C == N) ? 1 : 0;  // then the dense id of a vertex is the vertex itself
+  LAUNCH(k_init_comp, grid_for(N), kThreads, st, core_bits, L.woff, N, comp, L.cmin);
+  LAUNCH(k_fill_comp_arrays, grid_for(C), kThreads, st, C, L.Kc, L.Bc, general ? nullptr : L.kmin);
+  for (size_t r = 1; r < L.ranks.size(); ++r)
+    LAUNCH(k_fill_comp_arrays, grid_for(C), kThreads, st, C, L.ranks[r].Kc, L.ranks[r].Bc, nullptr);
+  KDB_CUDA(cudaGetLastError());
+  const bool use_compact = env_int("KDB_COMPACT", 1) != 0;
+  const int gw = env_int("KDB_GW", 4);  // component-gather width of the later light rounds (scan_ell)
+  const bool sparse_ids = env_int("KDB_SPARSE", 1) != 0;  // keep root ids once few components remain
+  // exact mode: round 1 (singleton components) is fused into the ELL pass; a
+  // single rank also packs (K, B, kmin) per component for the round-1 hook
+  const bool fuse1 = !general && use_compact && env_int("KDB_FUSE1", 1) != 0;
+  const bool packed1 = fuse1 && L.ranks.size() == 1 && !(multi_rank(comm)) &&
+                       env_int("KDB_PACK1", 1) != 0;
+  if (!general)  // hook targets of round 1 (written by the round-1 offers)
+    for (auto& R : L.ranks) LAUNCH(k_fill_i32, grid_for(C), kThreads, st, R.tgt, C, INT32_MAX);
+  for (auto& R : L.ranks) {
+    KDB_CUDA(cudaMemsetAsync(R.ctr, 0, sizeof(RoundCounters), st));
+    R.compact = false;
+    if (R.n_rows > 0 && use_compact) {
+      R.compact = true;
+      // 32-byte sector loads need 32-B aligned arrays, ld % 8 in {0, 4} and rows
+      // long enough for the third sector (ld >= 20)
+      const bool a32 = vec && ld >= 20 && !(((uintptr_t)R.nbr | (uintptr_t)R.dist) & 31u);
+#define KDB_ELL_LAUNCH(V, A)                                                                                    \
+  LAUNCH((k_light_ell<V, A>), grid_for(R.n_rows), kThreads, st, R.nbr, R.dist, R.n_rows, ld, k, eps_run, R.row_begin, \
+         comp, general ? nullptr : L.kmin, R.LE, R.act[0], &R.ctr->na[0], &R.ctr->grab, fuse1 ? 1 : 0,         \
+         L.all_core, N, R.Kc, R.Bc, R.tgt, packed1 ? L.rec1 : nullptr)
+      if (a32) KDB_ELL_LAUNCH(true, true);
+      else if (vec) KDB_ELL_LAUNCH(true, false);
+      else KDB_ELL_LAUNCH(false, false);
+#undef KDB_ELL_LAUNCH
+    }
+    if (R.n_rows > 0 && !R.compact)
+      LAUNCH(k_init_rows, grid_for(R.n_rows), kThreads, st, R.dist, R.n_rows, ld, k, eps_run, R.row_begin, comp,
+             general ? nullptr : L.kmin, R.act[0], &R.ctr->na[0]);
+    KDB_CUDA(cudaGetLastError());
+  }
+  if (!general) KDB_TRY(allreduce_min_u32(comm, L.kmin, C, st));
+  if (!general) m.payload_rows += 4.0 * C;
+  KDB_CUDA(cudaEventRecord(ev[1], st));
+  // ---- general mode: in-edge lists --------------------------------------------
+  if (general) {
+    for (auto& R : L.ranks) {
+      // counts -> scan -> offsets; e_key (N+1 u64) is scratch for counts and cursors
+      unsigned long long* cursor = reinterpret_cast<unsigned long long*>(L.e_key);
+      KDB_CUDA(cudaMemsetAsync(cursor, 0, (N + 1) * sizeof(unsigned long long), st));
+      if (R.n_rows > 0)
+        LAUNCH(k_in_count, grid_for(R.n_rows), kThreads, st, R.nbr, R.dist, R.n_rows, ld, k, eps_run, R.row_begin, N,
+               core_bits, cursor);
+      cb = L.cub_bytes;
+      { LaunchScope ls_("cub::DeviceScan", st, false); KDB_CUDA(cub::DeviceScan::ExclusiveSum(L.cub_tmp, cb, cursor, R.in_off, (int)(N + 1), st)); }
+      KDB_CUDA(cudaMemcpyAsync(cursor, R.in_off, (N + 1) * sizeof(unsigned long long),
+                               cudaMemcpyDeviceToDevice, st));
+      if (R.n_rows > 0)
+        LAUNCH(k_in_fill, grid_for(R.n_rows), kThreads, st, R.nbr, R.dist, R.n_rows, ld, k, eps_run, R.row_begin, N,
+               core_bits, cursor, R.in_src, R.in_w);
+      LAUNCH(k_in_finish, grid_for(N), kThreads, st, R.in_off, N, R.in_len, R.in_act[0], &R.ctr->ni[0]);
+      KDB_CUDA(cudaGetLastError());
+    }
+  }
+  for (auto& R : L.ranks) {
+    RoundCounters hc;
+    KDB_CUDA(cudaMemcpyAsync(&hc, R.ctr, sizeof(hc), cudaMemcpyDeviceToHost, st));
+    KDB_CUDA(cudaStreamSynchronize(st));
+    R.n_act = hc.na[0];
+    R.n_in_act = hc.ni[0];
+  }
+  KDB_CUDA(cudaEventRecord(ev[2], st));
+  KDB_CUDA(cudaEventSynchronize(ev[2]));
+  m.t_init += elapsed(ev[0], ev[1]);
+  m.t_inlist += elapsed(ev[1], ev[2]);
+
+  // ---- Boruvka rounds -------------------------------------------------------------
+  // Pipelined: every kernel reads its counts (components, list sizes) from the
+  // device; grids are sized by host upper bounds one round stale, so the host
+  // enqueues round r+1 before it has looked at round r and checks round r-1's
+  // counters (termination, violations, stalls) from pinned memory meanwhile.
+  // A round launched after the last productive one finds nothing and changes
+  // nothing.  With a real NCCL communicator the collectives need exact host
+  // counts: the loop then waits for each round's counters (sync_each).
+  bool any_compact = false;
+  for (auto& R : L.ranks) any_compact |= R.compact;
+  const bool fused = fuse1 && any_compact;
+  const bool sync_each = multi_rank(comm);
+  int cur = fused ? 1 : 0;  // fused round 1: its OUTPUT list is act[0] already
+  int par = 0;              // component count ping-pong: Cs[par] current
+  {
+    long long c0 = C;
+    KDB_CUDA(cudaMemcpyAsync(&L.ctr->Cs[0], &c0, sizeof(c0), cudaMemcpyHostToDevice, st));
+  }
+  const size_t nr = L.ranks.size();
+  // pinned slots for the round counters: [0] global, [1 + r] rank r
+  constexpr int kSlots = 4;
+  // (a per-thread pinned buffer, grown on demand: cudaMallocHost per call is slow)
+  static thread_local RoundCounters* slots = nullptr;
+  static thread_local size_t slots_cap = 0;
+  if (slots_cap < kSlots * (1 + nr)) {
+    if (slots) cudaFreeHost(slots);
+    slots = nullptr;
+    slots_cap = 0;
+    KDB_CUDA(cudaMallocHost(&slots, kSlots * (1 + nr) * sizeof(RoundCounters)));
+    slots_cap = kSlots * (1 + nr);
+  }
+  std::vector<cudaEvent_t> ev_slot(kSlots), ev_rnd;
+  for (auto& e : ev_slot) KDB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  struct EvVecGuard {
+    std::vector<cudaEvent_t>* a;
+    std::vector<cudaEvent_t>* b;
+    ~EvVecGuard() {
+      for (auto e : *a) cudaEventDestroy(e);
+      for (auto e : *b) cudaEventDestroy(e);
+    }
+  } evg{&ev_slot, &ev_rnd};
+  int64_t C_ub = C;  // upper bound of the current component count
+  std::vector<uint32_t> na_ub(nr), ni_ub(nr);
+  for (size_t r = 0; r < nr; ++r) {
+    na_ub[r] = L.ranks[r].n_act;
+    ni_ub[r] = L.ranks[r].n_in_act;
+  }
+  int rounds = 0, stalls = 0;
+  const uint32_t* kmin_cert = general ? nullptr : L.kmin;
+  auto slot_of = [&](int rr) { return slots + (size_t)(rr % kSlots) * (1 + nr); };
+
+  // contraction a6 on the device counts; C_bound >= the true count
+  auto contract = [&](int64_t C_bound) -> kdb_status {
+    const int64_t* Cd = (const int64_t*)&L.ctr->Cs[par];
+    int64_t* Cn = (int64_t*)&L.ctr->Cs[par ^ 1];
+    LAUNCH(k_jump, grid_for(C_bound), kThreads, st, C_bound, L.parent, L.rootof, L.ctr, Cd);
+    // sparse ids once few components remain: a component keeps its root's id
+    // (no dense renumbering; the id range stays C_bound), so the relabel only
+    // rewrites the vertices of merged components
+    const bool sparse = sparse_ids && C_bound <= N / 64;
+    if (!sparse) {
+      LAUNCH(k_root_flags, grid_for(C_bound), kThreads, st, C_bound, L.rootof, L.flag, Cd);
+      size_t cb2 = L.cub_bytes;
+      { LaunchScope ls_("cub::DeviceScan", st, false); KDB_CUDA(cub::DeviceScan::ExclusiveSum(L.cub_tmp, cb2, L.flag, L.newid, (int)std::max<int64_t>(C_bound, 1), st)); }
+      LAUNCH(k_count_roots, 1, 1, st, Cd, L.newid, L.flag, Cn);
+    } else {
+      KDB_CUDA(cudaMemcpyAsync(Cn, Cd, sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
+    }
+    LAUNCH(k_fill_i32, grid_for(C_bound), kThreads, st, L.cmin2, C_bound, INT32_MAX, (const int64_t*)Cn);
+    if (!general)
+      LAUNCH(k_fill_i32, grid_for(C_bound), kThreads, st, (int32_t*)L.kmin2, C_bound, (int32_t)kInfBits,
+             (const int64_t*)Cn);
+    // map[c] = new dense id of c's tree (reuses `parent`, no longer needed)
+    LAUNCH(k_merge, grid_for(C_bound), kThreads, st, C_bound, L.rootof, sparse ? (const int32_t*)nullptr : L.newid,
+           L.cmin, general ? nullptr : L.kmin, L.cmin2, L.kmin2, L.parent, Cd);
+    LAUNCH(k_relabel, grid_for(N / 8 + 1), kThreads, st, N, comp, L.parent, (const int32_t*)nullptr);
+    LAUNCH(k_fill_comp_arrays, grid_for(C_bound), kThreads, st, C_bound, L.Kc, L.Bc, nullptr, (const int64_t*)Cn);
+    for (size_t r = 1; r < nr; ++r)
+      LAUNCH(k_fill_comp_arrays, grid_for(C_bound), kThreads, st, C_bound, L.ranks[r].Kc, L.ranks[r].Bc, nullptr,
+             (const int64_t*)Cn);
+    KDB_CUDA(cudaGetLastError());
+    std::swap(L.cmin, L.cmin2);
+    std::swap(L.kmin, L.kmin2);
+    kmin_cert = general ? nullptr : L.kmin;
+    par ^= 1;
+    return KDB_OK;
+  };
+  // snapshot of the counters after the current round into a pinned slot
+  auto snapshot = [&](int rr) -> kdb_status {
+    RoundCounters* sl = slot_of(rr);
+    KDB_CUDA(cudaMemcpyAsync(sl, L.ctr, sizeof(RoundCounters), cudaMemcpyDeviceToHost, st));
+    for (size_t r = 0; r < nr; ++r)
+      KDB_CUDA(cudaMemcpyAsync(sl + 1 + r, L.ranks[r].ctr, sizeof(RoundCounters), cudaMemcpyDeviceToHost, st));
+    KDB_CUDA(cudaEventRecord(ev_slot[rr % kSlots], st));
+    return KDB_OK;
+  };
+
+  int last_checked = 0;
+  bool finished = false;
+  while (!finished) {
+    ++rounds;
+    const bool direct = rounds == 1 && !general;
+    const int64_t* Cd = (const int64_t*)&L.ctr->Cs[par];
+    cudaEvent_t e0;
+    KDB_CUDA(cudaEventCreate(&e0));
+    ev_rnd.push_back(e0);
+    KDB_CUDA(cudaEventRecord(e0, st));
+    // offers read the current key before their atomicMin once many rows offer
+    // to each component (same-address atomics serialise; early rounds have
+    // about one row per component and only pay the extra read)
+    int precheck = 0;
+    {
+      uint64_t live = 0;
+      for (size_t r = 0; r < nr; ++r) live += na_ub[r];
+      const int pc = env_int("KDB_PRECHECK", -1);
+      precheck = pc >= 0 ? pc : (live > 8 * (uint64_t)std::max<int64_t>(C_ub, 1) ? 1 : 0);
+    }
+    // a3: offers (rows, then in-lists), per rank, into that rank's Kc partial
+    for (size_t r = 0; r < nr; ++r) {
+      RankState& R = L.ranks[r];
+      if (direct && fused && R.compact) continue;  // done by the ELL pass
+      KDB_CUDA(cudaMemsetAsync(&R.ctr->na[cur ^ 1], 0, sizeof(uint32_t), st));
+      KDB_CUDA(cudaMemsetAsync(&R.ctr->ni[cur ^ 1], 0, sizeof(uint32_t), st));
+      KDB_CUDA(cudaMemsetAsync(&R.ctr->n_off, 0, sizeof(uint32_t), st));
+      KDB_CUDA(cudaMemsetAsync(&R.ctr->grab, 0, sizeof(uint32_t), st));
+      const uint32_t* nin = &R.ctr->na[cur];
+      uint32_t* nout = &R.ctr->na[cur ^ 1];
+      if (na_ub[r] && R.compact) {
+        if (direct)
+          LAUNCH(k_light_first, grid_for(na_ub[r]), kThreads, st, R.LE, R.nbr, R.dist, ld, k, eps_run, R.row_begin, N,
+                 comp, L.all_core, R.act[cur], na_ub[r], R.act[cur ^ 1], nout, &R.ctr->grab, R.Kc, R.Bc, R.tgt,
+                 &L.ctr->entries, nin);
+        else
+        {
+#define KDB_LR_LAUNCH(GW)                                                                                       \
+  LAUNCH(k_light_round<GW>, grid_for(na_ub[r]), kThreads, st, R.LE, R.nbr, R.dist, ld, k, eps_run, R.row_begin, N, \
+         comp, R.act[cur], na_ub[r], R.act[cur ^ 1], nout, &R.ctr->grab, R.offers, (unsigned long long*)R.Kc,      \
+         &L.ctr->entries, nin, precheck)
+          if (gw == 1) KDB_LR_LAUNCH(1);
+          else if (gw == 2) KDB_LR_LAUNCH(2);
+          else KDB_LR_LAUNCH(4);
+#undef KDB_LR_LAUNCH
+        }
+      } else if (na_ub[r]) {
+        if (direct) {
+          if (vec)
+            LAUNCH(k_offer_first<true>, grid_for(na_ub[r]), kThreads, st, R.nbr, R.dist, ld, k, eps_run, R.row_begin, N,
+                   comp, L.all_core, R.act[cur], na_ub[r], R.act[cur ^ 1], nout, R.Kc, R.Bc, R.tgt,
+                   &L.ctr->entries, nin);
+          else
+            LAUNCH(k_offer_first<false>, grid_for(na_ub[r]), kThreads, st, R.nbr, R.dist, ld, k, eps_run, R.row_begin,
+                   N, comp, L.all_core, R.act[cur], na_ub[r], R.act[cur ^ 1], nout, R.Kc, R.Bc, R.tgt,
+                   &L.ctr->entries, nin);
+        } else {
+          if (vec)
+            LAUNCH(k_offer_round<true>, grid_for(na_ub[r]), kThreads, st, R.nbr, R.dist, ld, k, eps_run, R.row_begin, N,
+                   comp, R.act[cur], na_ub[r], R.act[cur ^ 1], nout, R.offers, (unsigned long long*)R.Kc,
+                   &L.ctr->entries, nin, precheck);
+          else
+            LAUNCH(k_offer_round<false>, grid_for(na_ub[r]), kThreads, st, R.nbr, R.dist, ld, k, eps_run, R.row_begin,
+                   N, comp, R.act[cur], na_ub[r], R.act[cur ^ 1], nout, R.offers, (unsigned long long*)R.Kc,
+                   &L.ctr->entries, nin, precheck);
+        }
+      }
+      if (general && ni_ub[r])
+        LAUNCH(k_offer_in, grid_for(ni_ub[r]), kThreads, st, R.in_off, R.in_len, R.in_src, R.in_w, comp,
+               R.in_act[cur], ni_ub[r], R.in_act[cur ^ 1], &R.ctr->ni[cur ^ 1], R.offers + R.off_cap_rows,
+               &R.ctr->n_off, (unsigned long long*)R.Kc, &R.ctr->ni[cur]);
+      KDB_CUDA(cudaGetLastError());
+    }
+    // exchange: sim -> min over virtual ranks; nccl -> allreduce
+    for (size_t r = 1; r < nr; ++r)
+      LAUNCH(k_min_into_u64, grid_for(C_ub), kThreads, st, L.Kc, L.ranks[r].Kc, C_ub, Cd);
+    KDB_TRY(allreduce_min_u64(comm, L.Kc, C_ub, st));
+    m.payload_rows += 8.0 * C_ub;
+    // a4: ties (the direct round already wrote Bc and the targets)
+    if (!direct) {
+      for (size_t r = 0; r < nr; ++r) {
+        RankState& R = L.ranks[r];
+        if (na_ub[r]) LAUNCH(k_tie, grid_for(na_ub[r]), kThreads, st, R.offers, &R.ctr->na[cur ^ 1], L.Kc, R.Bc);
+        if (general && ni_ub[r])
+          LAUNCH(k_tie, grid_for(ni_ub[r]), kThreads, st, R.offers + R.off_cap_rows, &R.ctr->n_off, L.Kc, R.Bc);
+        KDB_CUDA(cudaGetLastError());
+      }
+    }
+    for (size_t r = 1; r < nr; ++r)
+      LAUNCH(k_min_into_u32, grid_for(C_ub), kThreads, st, L.Bc, L.ranks[r].Bc, C_ub, Cd);
+    KDB_TRY(allreduce_min_u32(comm, L.Bc, C_ub, st));
+    m.payload_rows += 4.0 * C_ub;
+    if (direct) {
+      for (size_t r = 1; r < nr; ++r)
+        LAUNCH(k_min_into_u32, grid_for(C_ub), kThreads, st, (uint32_t*)L.tgt, (const uint32_t*)L.ranks[r].tgt, C_ub,
+               Cd);
+      KDB_TRY(allreduce_min_u32(comm, (uint32_t*)L.tgt, C_ub, st));  // non-owners hold INT32_MAX
+      m.payload_rows += 4.0 * C_ub;
+    }
+    // a5: hook + emit
+    KDB_CUDA(cudaMemsetAsync(&L.ctr->hooks, 0, 4 * sizeof(uint32_t), st));
+    if (direct && packed1)
+      LAUNCH(k_hook<true>, grid_for(C_ub), kThreads, st, C_ub, L.Kc, L.Bc, L.tgt, kmin_cert, comp, L.parent, L.e_key,
+             L.e_w, N, L.ctr, Cd, L.rec1);
+    else
+      LAUNCH(k_hook<false>, grid_for(C_ub), kThreads, st, C_ub, L.Kc, L.Bc, direct ? L.tgt : nullptr, kmin_cert,
+             comp, L.parent, L.e_key, L.e_w, N, L.ctr, Cd, (const int4*)nullptr);
+    KDB_CUDA(cudaGetLastError());
+    // a6: contract (no hooks => identity)
+    KDB_TRY(contract(C_ub));
+    cur ^= 1;
+    KDB_TRY(snapshot(rounds));
+    // check the previous round (or this one when every round must be exact)
+    const int check = sync_each ? rounds : rounds - 1;
+    if (check < 1 || check <= last_checked) continue;
+    KDB_CUDA(cudaEventSynchronize(ev_slot[check % kSlots]));
+    last_checked = check;
+    const RoundCounters g = slot_of(check)[0];
+    if (g_trace)
+      fprintf(stderr, "[kdb] round %d eps=%.6g C->%lld offered=%u hooks=%u live=%u\n", check, (double)eps_run,
+              (long long)g.Cs[(check & 1) ? 1 : 0], g.offered, g.hooks, slot_of(check)[1].na[check & 1]);
+    if (g.violation == 2u) return set_err(KDB_EINTERNAL, "pointer jumping did not converge (hook cycle)");
+    if (g.violation) return set_err(KDB_EINVAL, "graph violates the KDB_GRAPH_EXACT promise (a component's "
+                                    "minimum missed an incident edge)");
+    if (g.offered == 0) break;  // a8: no component has a leaving edge
+    // upper bounds for the next launch: the counts after round `check`
+    {
+      // after round `check` the current parity was flipped `rounds - check` more times
+      const int par_after = (par ^ ((rounds - check) & 1));
+      C_ub = g.Cs[par_after];
+      const int cur_after = (cur ^ ((rounds - check) & 1));
+      for (size_t r = 0; r < nr; ++r) {
+        na_ub[r] = slot_of(check)[1 + r].na[cur_after];
+        ni_ub[r] = slot_of(check)[1 + r].ni[cur_after];
+      }
+    }
+    if (g.hooks == 0) {
+      // every offering component abstained (exact-mode certificate).  Drain,
+      // then one edge-centric sweep round gives every component its exact
+      // minimum (both endpoints see every entry) -- on exact counts.
+      ++stalls;
+      KDB_CUDA(cudaStreamSynchronize(st));
+      RoundCounters gg;
+      KDB_CUDA(cudaMemcpy(&gg, L.ctr, sizeof(gg), cudaMemcpyDeviceToHost));
+      if (gg.violation) return set_err(KDB_EINVAL, "graph violates the KDB_GRAPH_EXACT promise (a component's "
+                                       "minimum missed an incident edge)");
+      const int64_t Cx = gg.Cs[par];
+      std::vector<uint32_t> na_x(nr);
+      for (size_t r = 0; r < nr; ++r) {
+        RoundCounters rc;
+        KDB_CUDA(cudaMemcpy(&rc, L.ranks[r].ctr, sizeof(rc), cudaMemcpyDeviceToHost));
+        na_x[r] = rc.na[cur];
+      }
+      LAUNCH(k_fill_comp_arrays, grid_for(Cx), kThreads, st, Cx, L.Kc, L.Bc, nullptr);
+      for (size_t r = 1; r < nr; ++r)
+        LAUNCH(k_fill_comp_arrays, grid_for(Cx), kThreads, st, Cx, L.ranks[r].Kc, L.ranks[r].Bc, nullptr);
+      for (size_t r = 0; r < nr; ++r)
+        if (na_x[r])
+          LAUNCH(k_sweep, grid_for(na_x[r]), kThreads, st, L.ranks[r].nbr, L.ranks[r].dist, ld, k, eps_run,
+                 L.ranks[r].row_begin, N, comp, L.ranks[r].act[cur], na_x[r], (unsigned long long*)L.ranks[r].Kc,
+                 L.ranks[r].Bc, 0);
+      for (size_t r = 1; r < nr; ++r)
+        LAUNCH(k_min_into_u64, grid_for(Cx), kThreads, st, L.Kc, L.ranks[r].Kc, Cx);
+      KDB_TRY(allreduce_min_u64(comm, L.Kc, Cx, st));
+      m.payload_rows += 8.0 * Cx;
+      for (size_t r = 0; r < nr; ++r)
+        if (na_x[r])
+          LAUNCH(k_sweep, grid_for(na_x[r]), kThreads, st, L.ranks[r].nbr, L.ranks[r].dist, ld, k, eps_run,
+                 L.ranks[r].row_begin, N, comp, L.ranks[r].act[cur], na_x[r], (unsigned long long*)L.Kc,
+                 L.ranks[r].Bc, 1);
+      for (size_t r = 1; r < nr; ++r)
+        LAUNCH(k_min_into_u32, grid_for(Cx), kThreads, st, L.Bc, L.ranks[r].Bc, Cx);
+      KDB_TRY(allreduce_min_u32(comm, L.Bc, Cx, st));
+      m.payload_rows += 4.0 * Cx;
+      KDB_CUDA(cudaMemsetAsync(&L.ctr->hooks, 0, 4 * sizeof(uint32_t), st));
+      LAUNCH(k_hook<false>, grid_for(Cx), kThreads, st, Cx, L.Kc, L.Bc, nullptr, nullptr, comp, L.parent, L.e_key,
+             L.e_w, N, L.ctr, (const int64_t*)nullptr, (const int4*)nullptr);
+      KDB_CUDA(cudaGetLastError());
+      KDB_CUDA(cudaMemcpyAsync(&gg, L.ctr, sizeof(gg), cudaMemcpyDeviceToHost, st));
+      KDB_CUDA(cudaStreamSynchronize(st));
+      if (gg.hooks == 0) return set_err(KDB_EINTERNAL, "sweep round made no progress");
+      KDB_TRY(contract(Cx));
+      C_ub = Cx;
+      for (size_t r = 0; r < nr; ++r) na_ub[r] = na_x[r];
+      ++rounds;
+      KDB_TRY(snapshot(rounds));
+      last_checked = rounds;  // the sweep round was exact; the next check is the next round
+    }
+  }
+  KDB_CUDA(cudaStreamSynchronize(st));
+  if (!ev_rnd.empty()) {
+    KDB_CUDA(cudaEventRecord(ev[2], st));
+    KDB_CUDA(cudaEventSynchronize(ev[2]));
+    m.t_min_edges += elapsed(ev_rnd.front(), ev[2]);  // rounds are pipelined: one span
+  }
+  {
+    RoundCounters gg;
+    KDB_CUDA(cudaMemcpy(&gg, L.ctr, sizeof(gg), cudaMemcpyDeviceToHost));
+    C = gg.Cs[par];
+  }
+  RoundCounters hc;
+  KDB_CUDA(cudaMemcpyAsync(&hc, L.ctr, sizeof(hc), cudaMemcpyDeviceToHost, st));
+  KDB_CUDA(cudaStreamSynchronize(st));
+  m.entries += hc.entries;
+  m.rounds += rounds;
+  m.stalls += stalls;
+  m.C = C;
+  return KDB_OK;
+}
+
+// Filter: every rank streams its rows once and keeps the heavy candidate
+// entries (tau < w <= eps) whose endpoints lie in different light components.
+kdb_status filter_phase(Mst& m, float eps, bool* overflow) {
+  Layout& L = m.L;
+  cudaStream_t st = m.st;
+  KDB_CUDA(cudaEventRecord(m.ev[0], st));
+  // KDB_SURVCAP (tests): a smaller survivor capacity, to exercise the fallback
+  const int64_t cap_env = env_int("KDB_SURVCAP", -1);
+  // fast-path tables (identical on every rank: comp is replicated)
+  int shift = 0;
+  while (((m.N + ((int64_t)1 << shift) - 1) >> shift) > kDomMax) ++shift;
+  const int64_t nblk = (m.N + ((int64_t)1 << shift) - 1) >> shift;
+  bool fast = env_int("KDB_FASTFILTER", 1) != 0;
+  unsigned long long fc[2] = {0, 0};
+  int2* rng = reinterpret_cast<int2*>(L.Kc);  // C_L entries; Kc is refilled by the heavy phase
+  KDB_CUDA(cudaMemsetAsync(L.fcount, 0, 2 * sizeof(unsigned long long), st));
+  if (fast) {
+    const int64_t C = m.C;
+    KDB_CUDA(cudaMemsetAsync(L.bloom, 0, kBloomBits / 8, st));
+    LAUNCH(k_dom, grid_for(nblk * 32), kThreads, st, m.comp, m.N, shift, nblk, L.dom);
+    LAUNCH(k_bloom_build, grid_for(m.N), kThreads, st, m.comp, m.N, shift, L.dom, L.bloom,
+           reinterpret_cast<uint32_t*>(L.fcount));
+    LAUNCH(k_fill_i32, grid_for(C), kThreads, st, L.parent, C, INT32_MAX);
+    LAUNCH(k_fill_i32, grid_for(C), kThreads, st, L.rootof, C, -1);
+    LAUNCH(k_fill_i32, grid_for(C), kThreads, st, L.newid, C, 0);
+    LAUNCH(k_rng_acc, grid_for(nblk), kThreads, st, L.dom, nblk, L.parent, L.rootof, L.newid);
+    LAUNCH(k_rng_fin, grid_for(C), kThreads, st, C, m.N, shift, L.parent, L.rootof, L.newid, rng);
+    KDB_CUDA(cudaGetLastError());
+    KDB_CUDA(cudaMemcpyAsync(fc, L.fcount, sizeof(fc), cudaMemcpyDeviceToHost, st));
+    KDB_CUDA(cudaStreamSynchronize(st));
+    fc[0] &= 0xffffffffull;  // block_count wrote the low 32-bit word
+    m.exceptions = fc[0];
+    // a saturated filter would send almost every entry down the slow path
+    if (fc[0] > (unsigned long long)kBloomBits / 4) fast = false;
+  }
+  for (auto& R : L.ranks) {
+    KDB_CUDA(cudaMemsetAsync(R.n_hs_dev, 0, 2 * sizeof(uint32_t), st));
+    if (cap_env >= 0) R.hs_cap = (uint32_t)std::min<int64_t>(R.hs_cap, cap_env);
+    if (R.n_rows == 0) continue;
+    const int vec = (m.ld % 4) == 0 ? 4 : 1;
+    const bool cols = m.k < m.ld;  // edge_cols < row stride
+    FastDiv fd;  // entry (COLS: chunk) index within a tile -> row within the tile
+    fd.d = cols ? (uint64_t)((m.k + vec - 1) / vec) : (uint64_t)m.ld;
+    fd.M = fd.d > 1 ? (~0ull / fd.d) + 1 : 0;
+    fd.m32 = fd.d > 1 ? (uint32_t)((0xffffffffull / fd.d) + 1) : 0;
+    fd.small = (fd.d > 1 && fd.d < 2048) ? 1u : 0u;
+    const int64_t ntiles = (R.n_rows + kFilterThreads - 1) / kFilterThreads;
+    const int grid = (int)std::min<int64_t>(ntiles, 1 << 30);
+#define KDB_FILTER_LAUNCH(V, F, CO)                                                                              \
+  LAUNCH_DYN((k_filter<V, F, CO>), grid, kFilterThreads, kFilterSmem, st, R.nbr, R.dist, R.n_rows, m.ld, m.k,      \
+             m.tau, eps, R.row_begin, m.N, m.comp, rng, L.bloom, fd, R.hs[0], R.hs_cap, R.n_hs_dev, L.fcount + 1)
+    if (cols) {
+      if (vec == 4 && fast) KDB_FILTER_LAUNCH(4, true, true);
+      else if (vec == 4) KDB_FILTER_LAUNCH(4, false, true);
+      else if (fast) KDB_FILTER_LAUNCH(1, true, true);
+      else KDB_FILTER_LAUNCH(1, false, true);
+    } else {
+      if (vec == 4 && fast) KDB_FILTER_LAUNCH(4, true, false);
+      else if (vec == 4) KDB_FILTER_LAUNCH(4, false, false);
+      else if (fast) KDB_FILTER_LAUNCH(1, true, false);
+      else KDB_FILTER_LAUNCH(1, false, false);
+    }
+#undef KDB_FILTER_LAUNCH
+    KDB_CUDA(cudaGetLastError());
+  }
+  uint32_t over = 0;
+  unsigned long long tot = 0;
+  for (auto& R : L.ranks) {
+    uint32_t n = 0;
+    KDB_CUDA(cudaMemcpyAsync(&n, R.n_hs_dev, 4, cudaMemcpyDeviceToHost, st));
+    KDB_CUDA(cudaStreamSynchronize(st));
+    R.n_hs = n;
+    tot += n;
+    if (n > R.hs_cap) over = 1;
+  }
+  if (multi_rank(m.comm)) {  // every rank must take the same branch
+    uint32_t* d = L.ranks[0].n_hs_dev + 1;
+    KDB_CUDA(cudaMemcpyAsync(d, &over, 4, cudaMemcpyHostToDevice, st));
+    KDB_TRY(allreduce_max_u32(m.comm, d, 1, st));
+    KDB_CUDA(cudaMemcpyAsync(&over, d, 4, cudaMemcpyDeviceToHost, st));
+    KDB_CUDA(cudaStreamSynchronize(st));
+  }
+  KDB_CUDA(cudaMemcpyAsync(&fc[1], L.fcount + 1, 8, cudaMemcpyDeviceToHost, st));
+  KDB_CUDA(cudaStreamSynchronize(st));
+  m.slow_entries = fc[1];
+  KDB_CUDA(cudaEventRecord(m.ev[1], st));
+  m.t_filter += elapsed(m.ev[0], m.ev[1]);
+  m.survivors = tot;
+  *overflow = over != 0;
+  return KDB_OK;
+}
+
+// Heavy phase: edge-centric Boruvka over the survivors in light-component
+// space.  hcomp maps light component -> current heavy component (replicated).
+kdb_status heavy_phase(Mst& m) {
+  Layout& L = m.L;
+  cudaStream_t st = m.st;
+  kdb_comm* comm = m.comm;
+  const int64_t CL = m.C;
+  int64_t C = CL;
+  KDB_CUDA(cudaEventRecord(m.ev[0], st));
+  LAUNCH(k_iota, grid_for(CL), kThreads, st, L.hcomp, CL);
+  std::vector<int> cur(L.ranks.size(), 0);
+  int rounds = 0;
+  while (C > 1) {
+    ++rounds;
+    LAUNCH(k_fill_comp_arrays, grid_for(C), kThreads, st, C, L.Kc, L.Bc, nullptr);
+    for (size_t r = 1; r < L.ranks.size(); ++r)
+      LAUNCH(k_fill_comp_arrays, grid_for(C), kThreads, st, C, L.ranks[r].Kc, L.ranks[r].Bc, nullptr);
+    for (size_t r = 0; r < L.ranks.size(); ++r) {
+      RankState& R = L.ranks[r];
+      if (R.n_hs == 0) continue;
+      LAUNCH(k_hedge_offer, grid_for(R.n_hs), kThreads, st, R.hs[cur[r]], R.n_hs, L.hcomp,
+             (unsigned long long*)R.Kc, R.hkeep);
+      size_t cb = L.cub_bytes;
+      { LaunchScope ls_("cub::DeviceSelect", st, false);
+        KDB_CUDA(cub::DeviceSelect::Flagged(L.cub_tmp, cb, R.hs[cur[r]], R.hkeep, R.hs[cur[r] ^ 1],
+                                            R.n_hs_dev + 1, (int)R.n_hs, st)); }
+      cur[r] ^= 1;
+      KDB_CUDA(cudaGetLastError());
+    }
+    for (auto& R : L.ranks) {
+      if (R.n_hs == 0) continue;
+      KDB_CUDA(cudaMemcpyAsync(&R.n_hs, R.n_hs_dev + 1, 4, cudaMemcpyDeviceToHost, st));
+    }
+    KDB_CUDA(cudaStreamSynchronize(st));
+    for (size_t r = 1; r < L.ranks.size(); ++r)
+      LAUNCH(k_min_into_u64, grid_for(C), kThreads, st, L.Kc, L.ranks[r].Kc, C);
+    KDB_TRY(allreduce_min_u64(comm, L.Kc, C, st));
+    m.payload_heavy += 8.0 * C;
+    for (size_t r = 0; r < L.ranks.size(); ++r) {
+      RankState& R = L.ranks[r];
+      if (R.n_hs)
+        LAUNCH(k_hedge_tie, grid_for(R.n_hs), kThreads, st, R.hs[cur[r]], R.n_hs, L.hcomp, L.Kc, R.Bc);
+    }
+    for (size_t r = 1; r < L.ranks.size(); ++r)
+      LAUNCH(k_min_into_u32, grid_for(C), kThreads, st, L.Bc, L.ranks[r].Bc, C);
+    KDB_TRY(allreduce_min_u32(comm, L.Bc, C, st));
+    m.payload_heavy += 4.0 * C;
+    KDB_CUDA(cudaMemsetAsync(&L.ctr->hooks, 0, 4 * sizeof(uint32_t), st));
+    LAUNCH(k_hook_h, grid_for(C), kThreads, st, C, L.Kc, L.Bc, m.comp, L.hcomp, L.parent, L.e_key, L.e_w, m.N, L.ctr);
+    KDB_CUDA(cudaGetLastError());
+    RoundCounters hc;
+    KDB_CUDA(cudaMemcpyAsync(&hc, L.ctr, sizeof(hc), cudaMemcpyDeviceToHost, st));
+    KDB_CUDA(cudaStreamSynchronize(st));
+    if (hc.offered == 0) break;
+    if (hc.hooks == 0) return set_err(KDB_EINTERNAL, "heavy phase made no progress");
+    LAUNCH(k_jump, grid_for(C), kThreads, st, C, L.parent, L.rootof, L.ctr);
+    LAUNCH(k_root_flags, grid_for(C), kThreads, st, C, L.rootof, L.flag);
+    size_t cb = L.cub_bytes;
+    { LaunchScope ls_("cub::DeviceScan", st, false); KDB_CUDA(cub::DeviceScan::ExclusiveSum(L.cub_tmp, cb, L.flag, L.newid, (int)C, st)); }
+    uint32_t viol = 0;
+    int32_t last[2];
+    KDB_CUDA(cudaMemcpyAsync(&viol, &L.ctr->violation, 4, cudaMemcpyDeviceToHost, st));
+    KDB_CUDA(cudaMemcpyAsync(&last[0], L.newid + C - 1, 4, cudaMemcpyDeviceToHost, st));
+    KDB_CUDA(cudaMemcpyAsync(&last[1], L.flag + C - 1, 4, cudaMemcpyDeviceToHost, st));
+    KDB_CUDA(cudaStreamSynchronize(st));
+    if (viol) return set_err(KDB_EINTERNAL, "heavy-phase pointer jumping did not converge");
+    const int64_t C2 = (int64_t)last[0] + last[1];
+    LAUNCH(k_fill_i32, grid_for(C2), kThreads, st, L.cmin2, C2, INT32_MAX);
+    LAUNCH(k_merge, grid_for(C), kThreads, st, C, L.rootof, L.newid, L.cmin, nullptr, L.cmin2, nullptr, L.parent);
+    LAUNCH(k_relabel_h, grid_for(CL), kThreads, st, CL, L.hcomp, L.parent);
+    KDB_CUDA(cudaGetLastError());
+    std::swap(L.cmin, L.cmin2);
+    C = C2;
+  }
+  KDB_CUDA(cudaEventRecord(m.ev[1], st));
+  m.t_heavy += elapsed(m.ev[0], m.ev[1]);
+  m.heavy_rounds = rounds;
+  m.C_heavy = C;
+  return KDB_OK;
+}
+

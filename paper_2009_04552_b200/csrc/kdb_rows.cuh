@@ -1,0 +1,1162 @@
+// kdb_rows.cuh -- core mark, initial state, in-edge lists and the Boruvka round kernels
+// Part of kdb.cu's single translation unit: included inside its anonymous
+// namespace, after kdb.cu's helpers; not a standalone header.
+#pragma once
+
+// ============================================================================
+// a1: core marking
+// ============================================================================
+// One thread per 32-bit word of core flags: 32 independent loads of
+// D[v][M-1] in flight, the word is stored whole (atomicOr only for the
+// partial words at this rank's range ends; the caller zeroed the bits).
+__global__ void k_core_mark(const float* __restrict__ dist, int64_t n_rows, int32_t k, int32_t M,
+                            float eps, int64_t row_begin, uint32_t* __restrict__ bits) {
+  const int64_t r_end = row_begin + n_rows;
+  const int64_t w0 = row_begin >> 5, w1 = (r_end + 31) >> 5;
+  for (int64_t wd = w0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; wd < w1;
+       wd += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v0 = wd << 5;
+    float d[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const int64_t v = v0 + j;
+      d[j] = (v >= row_begin && v < r_end) ? __ldcs(dist + (v - row_begin) * k + (M - 1))
+                                            : __int_as_float(0x7f800000);
+    }
+    uint32_t word = 0;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) word |= (d[j] <= eps ? 1u : 0u) << j;
+    if (v0 >= row_begin && v0 + 32 <= r_end)
+      bits[wd] = word;
+    else if (word)
+      atomicOr(bits + wd, word);
+  }
+}
+
+// ============================================================================
+// a2: initial state
+// ============================================================================
+__global__ void k_popc_words(const uint32_t* __restrict__ bits, int64_t nwords, uint32_t* out) {
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < nwords;
+       w += (int64_t)gridDim.x * blockDim.x)
+    out[w] = __popc(bits[w]);
+}
+
+// comp[v] = rank of v among core points (dense id) or -1; cmin[comp] = v
+__global__ void k_init_comp(const uint32_t* __restrict__ bits, const uint32_t* __restrict__ woff,
+                            int64_t N, int32_t* __restrict__ comp, int32_t* __restrict__ cmin) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < N;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t word = bits[v >> 5];
+    if ((word >> (v & 31)) & 1u) {
+      const int32_t c = (int32_t)(woff[v >> 5] + __popc(word & ((1u << (v & 31)) - 1u)));
+      comp[v] = c;
+      cmin[c] = (int32_t)v;
+    } else {
+      comp[v] = -1;
+    }
+  }
+}
+
+__global__ void k_fill_comp_arrays(int64_t C, uint64_t* __restrict__ Kc, uint32_t* __restrict__ Bc,
+                                   uint32_t* __restrict__ kmin, const int64_t* __restrict__ Cp = nullptr) {
+  if (Cp) C = *Cp;
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < C;
+       c += (int64_t)gridDim.x * blockDim.x) {
+    Kc[c] = kSent;
+    Bc[c] = kSentB;
+    if (kmin) kmin[c] = kInfBits;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// ---------------------------------------------------------------------------
+// Active rows and offers.  The scan position L[i] travels with
+// the row id: one coalesced 8-byte record per live row.  Every entry before h is
+// dead for good -- not a candidate, or intra-component (components only merge).
+struct Rec {
+  int32_t v;  // global row id
+  int32_t h;  // head
+};
+// one row's (or in-list's) minimum leaving edge: its component, the key's b, the key
+struct Offer {
+  int32_t c;
+  uint32_t b;
+  uint64_t key;
+};
+
+// local rows: certificate bound kth'(v) into kmin[comp v] (exact mode); the
+// active list holds the core rows whose first entry is within eps (a row
+// starting beyond it offers nothing, ever).  comp[v] >= 0 <=> v is core.
+__global__ void k_init_rows(const float* __restrict__ dist, int64_t n_rows, int32_t ld, int32_t k, float eps,
+                            int64_t row_begin, const int32_t* __restrict__ comp, uint32_t* __restrict__ kmin,
+                            Rec* __restrict__ act, uint32_t* __restrict__ n_act) {
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n_rows; base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = base + threadIdx.x;
+    const int64_t v = row_begin + i;
+    bool want = false;
+    if (i < n_rows) {
+      const int32_t cv = comp[v];
+      if (cv >= 0) {
+        want = __ldcs(dist + i * ld) <= eps;
+        if (kmin) {
+          const float kth = __ldcs(dist + i * ld + (k - 1));
+          kmin[cv] = (kth <= eps) ? mono_bits(kth) : kInfBits;
+        }
+      }
+    }
+    const uint32_t slot = block_reserve(n_act, want);
+    if (want) act[slot] = Rec{(int32_t)v, 0};
+  }
+}
+
+// ============================================================================
+// general mode: in-edge lists (transpose of local candidate entries)
+// ============================================================================
+__global__ void k_in_count(const int32_t* __restrict__ nbr, const float* __restrict__ dist,
+                           int64_t n_rows, int32_t ld, int32_t k, float eps, int64_t row_begin, int64_t N,
+                           const uint32_t* __restrict__ bits, unsigned long long* __restrict__ cnt) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_rows;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = row_begin + i;
+    if (!is_core(bits, v)) continue;
+    for (int32_t c = 0; c < k; ++c) {
+      const float w = __ldg(dist + i * ld + c);
+      if (!(w <= eps)) break;
+      const int64_t J = __ldg(nbr + i * ld + c);
+      if (J < 0 || J >= N || J == v || !is_core(bits, J)) continue;
+      atomicAdd(cnt + J, 1ull);
+    }
+  }
+}
+
+__global__ void k_in_fill(const int32_t* __restrict__ nbr, const float* __restrict__ dist,
+                          int64_t n_rows, int32_t ld, int32_t k, float eps, int64_t row_begin, int64_t N,
+                          const uint32_t* __restrict__ bits, unsigned long long* __restrict__ cursor,
+                          int32_t* __restrict__ in_src, float* __restrict__ in_w) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_rows;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = row_begin + i;
+    if (!is_core(bits, v)) continue;
+    for (int32_t c = 0; c < k; ++c) {
+      const float w = __ldg(dist + i * ld + c);
+      if (!(w <= eps)) break;
+      const int64_t J = __ldg(nbr + i * ld + c);
+      if (J < 0 || J >= N || J == v || !is_core(bits, J)) continue;
+      const unsigned long long s = atomicAdd(cursor + J, 1ull);
+      in_src[s] = (int32_t)v;
+      in_w[s] = w;
+    }
+  }
+}
+
+// in_len[t] = count, in-active list = targets with in-edges
+__global__ void k_in_finish(const unsigned long long* __restrict__ off, int64_t N,
+                            int32_t* __restrict__ in_len, int32_t* __restrict__ in_active,
+                            uint32_t* __restrict__ n_in_active) {
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < N;
+       base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = base + threadIdx.x;
+    bool want = false;
+    if (t < N) {
+      const int32_t len = (int32_t)(off[t + 1] - off[t]);
+      in_len[t] = len;
+      want = len > 0;
+    }
+    const uint32_t slot = block_reserve(n_in_active, want);
+    if (want) in_active[slot] = (int32_t)t;
+  }
+}
+
+
+// ============================================================================
+// a3: per-vertex minimum leaving entry (rows)
+// ============================================================================
+// For vertex v the incident edges of its row are ordered, under O1 with v fixed,
+// by (mono(w), far id) (reading #6).  Rows are sorted by w, so the first entry
+// at/after the head whose far endpoint lies in another component opens the
+// minimum group; equal-weight entries after it may carry a smaller far id and
+// are examined too.  The head only passes entries that can never leave again.
+// comp[J] < 0 marks non-core J (not a candidate); J == v gives comp[J] == comp[v].
+template <bool VEC>
+__device__ __forceinline__ void load_chunk(const int32_t* nr, const float* dr, int c0, int k, int32_t (&J)[4],
+                                           float (&w)[4]) {
+  if (VEC) {  // row stride % 4 == 0: an aligned 4-chunk never straddles the row end (entries
+              // at or beyond the candidate bound k are ignored by the callers)
+    const int4 j4 = __ldcs(reinterpret_cast<const int4*>(nr + c0));
+    const float4 w4 = __ldcs(reinterpret_cast<const float4*>(dr + c0));
+    J[0] = j4.x; J[1] = j4.y; J[2] = j4.z; J[3] = j4.w;
+    w[0] = w4.x; w[1] = w4.y; w[2] = w4.z; w[3] = w4.w;
+  } else {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const bool in = c0 + j < k;
+      J[j] = in ? __ldcs(nr + c0 + j) : -1;
+      w[j] = in ? __ldcs(dr + c0 + j) : __int_as_float(0x7f800000);
+    }
+  }
+}
+
+struct RowScan {
+  bool found;
+  int h;          // new head: the first leaving entry, or k when exhausted
+  uint64_t best;  // minimum key of the group
+  uint32_t bestb;
+  int32_t bestc;  // component of the best entry's far endpoint
+};
+
+// Scan row (nr, dr) of vertex v (component cv) from head h.  direct: singleton
+// components (round 1, exact mode) -- every candidate leaves; with all_core the
+// dense component id of a vertex is the vertex itself (no gathers at all).
+template <bool VEC, bool DIRECT>
+__device__ __forceinline__ RowScan scan_row(const int32_t* __restrict__ nr, const float* __restrict__ dr, int k,
+                                            float eps, int32_t v, int32_t cv, int h, int64_t N,
+                                            const int32_t* __restrict__ comp, int all_core,
+                                            unsigned long long& reads) {
+  RowScan r{false, k, kSent, kSentB, -1};
+  float wstar = 0.f;
+  int c0 = h & ~3;
+  bool done = false;
+  while (!done && c0 < k) {
+    int32_t J[4];
+    float w[4];
+    load_chunk<VEC>(nr, dr, c0, k, J, w);
+    int32_t cj[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int idx = c0 + j;
+      const bool cand = idx >= h && idx < k && w[j] <= eps && J[j] >= 0 && J[j] < N && J[j] != v;
+      cj[j] = cand ? ((DIRECT && all_core) ? J[j] : gat(comp + J[j])) : -1;
+    }
+    reads += (unsigned long long)(min(c0 + 4, k) - max(c0, h));
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int idx = c0 + j;
+      if (done || idx < h || idx >= k) continue;
+      const bool leaving = cj[j] >= 0 && (DIRECT || cj[j] != cv);
+      if (!r.found) {
+        if (!(w[j] <= eps)) { r.h = k; done = true; continue; }  // sorted: nothing left
+        if (!leaving) { h = idx + 1; continue; }                   // dead entry
+        r.found = true;
+        r.h = idx;
+        wstar = w[j];
+        r.best = pack_key(mono_bits(w[j]), (uint32_t)min(v, J[j]));
+        r.bestb = (uint32_t)max(v, J[j]);
+        r.bestc = cj[j];
+      } else {
+        if (w[j] != wstar) { done = true; continue; }
+        if (!leaving) continue;
+        const uint64_t kk = pack_key(mono_bits(w[j]), (uint32_t)min(v, J[j]));
+        const uint32_t bb = (uint32_t)max(v, J[j]);
+        if (kk < r.best || (kk == r.best && bb < r.bestb)) { r.best = kk; r.bestb = bb; r.bestc = cj[j]; }
+      }
+    }
+    c0 += 4;
+  }
+  if (!r.found) r.h = k;
+  return r;
+}
+
+// Round 1 with singleton components (exact mode): the row's first candidate
+// group IS its component's minimum -- no atomics and no tie pass; the owner
+// writes Kc, Bc and the hook target directly.  Rows that offered stay active.
+template <bool VEC>
+__global__ void __launch_bounds__(256) k_offer_first(const int32_t* __restrict__ nbr, const float* __restrict__ dist,
+                                                     int32_t ld, int32_t k, float eps, int64_t row_begin, int64_t N,
+                                                     const int32_t* __restrict__ comp, int all_core,
+                                                     const Rec* __restrict__ act, uint32_t n_in,
+                                                     Rec* __restrict__ act_out, uint32_t* __restrict__ n_out,
+                                                     uint64_t* __restrict__ Kc, uint32_t* __restrict__ Bc,
+                                                     int32_t* __restrict__ tgt, unsigned long long* __restrict__ n_entries, const uint32_t* __restrict__ n_in_p = nullptr) {
+  if (n_in_p) n_in = *n_in_p;
+  unsigned long long reads = 0;
+  for (uint32_t base = blockIdx.x * blockDim.x; base < n_in; base += gridDim.x * blockDim.x) {
+    const uint32_t s = base + threadIdx.x;
+    RowScan r{false, 0, kSent, kSentB, -1};
+    int32_t v = -1;
+    if (s < n_in) {
+      const int2 a2 = __ldcs(reinterpret_cast<const int2*>(act + s));
+      const Rec a{a2.x, a2.y};
+      v = a.v;
+      const int64_t i = (int64_t)v - row_begin;
+      r = scan_row<VEC, true>(nbr + i * ld, dist + i * ld, k, eps, v, -1, a.h, N, comp, all_core, reads);
+      if (r.found) {
+        const int32_t cv = all_core ? v : gat(comp + v);
+        Kc[cv] = r.best;
+        Bc[cv] = r.bestb;
+        tgt[cv] = r.bestc;
+      }
+    }
+    const uint32_t slot = block_reserve(n_out, r.found);
+    if (r.found) act_out[slot] = Rec{v, r.h};
+  }
+  for (int o = 16; o > 0; o >>= 1) reads += __shfl_xor_sync(0xffffffffu, reads, o);
+  if ((threadIdx.x & 31) == 0 && reads) atomicAdd(n_entries, reads);
+}
+
+// Later rounds: one thread per live row; the offer goes to Kc[comp v] by a
+// 64-bit atomicMin (Alg. 3 pwrite, reading #7) and, with the
+// row's next record, to the same slot of the offer list (for the tie pass).
+template <bool VEC>
+__global__ void __launch_bounds__(256) k_offer_round(const int32_t* __restrict__ nbr, const float* __restrict__ dist,
+                                                     int32_t ld, int32_t k, float eps, int64_t row_begin, int64_t N,
+                                                     const int32_t* __restrict__ comp, const Rec* __restrict__ act,
+                                                     uint32_t n_in, Rec* __restrict__ act_out,
+                                                     uint32_t* __restrict__ n_out, Offer* __restrict__ offers,
+                                                     unsigned long long* __restrict__ Kc,
+                                                     unsigned long long* __restrict__ n_entries, const uint32_t* __restrict__ n_in_p = nullptr,
+                                                     int precheck = 0) {
+  if (n_in_p) n_in = *n_in_p;
+  unsigned long long reads = 0;
+  for (uint32_t base = blockIdx.x * blockDim.x; base < n_in; base += gridDim.x * blockDim.x) {
+    const uint32_t s = base + threadIdx.x;
+    RowScan r{false, 0, kSent, kSentB, -1};
+    int32_t v = -1, cv = -1;
+    if (s < n_in) {
+      const int2 a2 = __ldcs(reinterpret_cast<const int2*>(act + s));
+      const Rec a{a2.x, a2.y};
+      v = a.v;
+      cv = gat(comp + v);
+      const int64_t i = (int64_t)v - row_begin;
+      r = scan_row<VEC, false>(nbr + i * ld, dist + i * ld, k, eps, v, cv, a.h, N, comp, 0, reads);
+      if (r.found) {
+        if (precheck) min_offer(Kc + cv, (unsigned long long)r.best);
+        else atomicMin(Kc + cv, (unsigned long long)r.best);
+      }
+    }
+    const uint32_t slot = block_reserve(n_out, r.found);
+    if (r.found) {
+      act_out[slot] = Rec{v, r.h};
+      offers[slot] = Offer{cv, r.bestb, r.best};
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) reads += __shfl_xor_sync(0xffffffffu, reads, o);
+  if ((threadIdx.x & 31) == 0 && reads) atomicAdd(n_entries, reads);
+}
+
+// ---------------------------------------------------------------------------
+// Light ELL.  A random visit of a 400-byte-strided graph row is expensive
+// (scattered sectors, HBM row activations), so the first kW columns of every
+// core row are copied ONCE into a dense, 128-byte-aligned ELL of (J, w bits)
+// pairs and every Boruvka round reads that instead.  Rows whose candidate
+// prefix (w <= eps_run) runs past column kW continue in the graph row itself.
+constexpr int kW = 16;
+
+// one 32-byte streaming load (evict-first: LDG.E.EF.ENL2.256) -- a light-ELL
+// chunk is read once per round; keep L2 for the component gathers
+__device__ __forceinline__ void ld256cs(const int4* p, int4& a, int4& b) {
+  asm volatile("ld.global.cs.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
+               : "l"(p));
+}
+
+// one 32-byte load (sm_100: LDG.E.ENL2.256); p must be 32-byte aligned
+__device__ __forceinline__ void ld256(const int4* p, int4& a, int4& b) {
+  asm volatile("ld.global.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
+               : "l"(p));
+}
+
+// records per chunk of the ordered row kernels (see k_light_first)
+constexpr int kChunk = 1024;
+
+// one thread per row: 4 x (int4 + float4) loads in flight, 8 x int4 stores.
+// Exact mode also writes the certificate bound kth'(v) into kmin[comp v]; kth
+// is only loaded when the ELL row is entirely within eps (else kth > eps).
+// Rows are taken in ordered chunks; the initial list keeps row order.
+template <bool VEC, bool A32>
+__global__ void __launch_bounds__(256) k_light_ell(const int32_t* __restrict__ nbr, const float* __restrict__ dist,
+                                                   int64_t n_rows, int32_t ld, int32_t k, float eps, int64_t row_begin,
+                                                   const int32_t* __restrict__ comp, uint32_t* __restrict__ kmin,
+                                                   int4* __restrict__ LE, Rec* __restrict__ act,
+                                                   uint32_t* __restrict__ n_act, uint32_t* __restrict__ grab,
+                                                   int direct, int all_core, int64_t N, uint64_t* __restrict__ Kc,
+                                                   uint32_t* __restrict__ Bc, int32_t* __restrict__ tgt,
+                                                   int4* __restrict__ rec1) {
+  __shared__ __align__(16) Rec s_rec[kChunk];
+  __shared__ uint32_t s_n, s_chunk, s_base;
+  for (;;) {
+    if (threadIdx.x == 0) { s_chunk = atomicAdd(grab, 1u); s_n = 0; }
+    __syncthreads();
+    const int64_t base = (int64_t)s_chunk * kChunk;
+    if (base >= n_rows) break;
+    for (int t = 0; t < kChunk; t += 256) {
+      const int64_t i = base + t + threadIdx.x;
+      if (i >= n_rows) continue;
+      const int64_t v = row_begin + i;
+      const int32_t cv = comp[v];
+      if (cv < 0) continue;
+      const int32_t* nr = nbr + i * ld;
+      const float* dr = dist + i * ld;
+      int32_t J[kW];
+      float w[kW];
+      if (VEC && A32) {
+        // whole 32-byte sectors (LDG.256): a row starts at a 32-B boundary or
+        // 16 B past one (ld % 8 == 4), so 2 or 3 sectors cover its first kW
+        // entries -- one request per sector instead of one per 16-B half
+        const int sh = (int)((i * ld) & 7);  // 0 or 4
+        int4 a0, a1, a2, a3, a4, a5, b0, b1, b2, b3, b4, b5;
+        const int4* pj = reinterpret_cast<const int4*>(nr - sh);
+        const int4* pd = reinterpret_cast<const int4*>(dr - sh);
+        ld256(pj, a0, a1);
+        ld256(pj + 2, a2, a3);
+        ld256(pd, b0, b1);
+        ld256(pd + 2, b2, b3);
+        if (sh) {
+          ld256(pj + 4, a4, a5);
+          ld256(pd + 4, b4, b5);
+        } else {
+          a4 = a5 = b4 = b5 = make_int4(0, 0, 0, 0);
+        }
+        const int32_t SJ[24] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w, a2.x, a2.y, a2.z, a2.w,
+                                a3.x, a3.y, a3.z, a3.w, a4.x, a4.y, a4.z, a4.w, a5.x, a5.y, a5.z, a5.w};
+        const int32_t SW[24] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w, b2.x, b2.y, b2.z, b2.w,
+                                b3.x, b3.y, b3.z, b3.w, b4.x, b4.y, b4.z, b4.w, b5.x, b5.y, b5.z, b5.w};
+#pragma unroll
+        for (int c = 0; c < kW; ++c) {
+          J[c] = sh ? SJ[c + 4] : SJ[c];
+          w[c] = __int_as_float(sh ? SW[c + 4] : SW[c]);
+        }
+      } else if (VEC && ld >= kW) {
+#pragma unroll
+        for (int q = 0; q < kW / 4; ++q) {
+          // L1-allocating loads: the two 16-B halves of a sector are separate
+          // instructions; the second must hit L1, not re-request the sector
+          const int4 j4 = __ldg(reinterpret_cast<const int4*>(nr + 4 * q));
+          const float4 w4 = __ldg(reinterpret_cast<const float4*>(dr + 4 * q));
+          J[4 * q] = j4.x; J[4 * q + 1] = j4.y; J[4 * q + 2] = j4.z; J[4 * q + 3] = j4.w;
+          w[4 * q] = w4.x; w[4 * q + 1] = w4.y; w[4 * q + 2] = w4.z; w[4 * q + 3] = w4.w;
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < kW; ++c) {
+          J[c] = c < k ? __ldg(nr + c) : -1;
+          w[c] = c < k ? __ldg(dr + c) : __int_as_float(0x7f800000);
+        }
+      }
+      if (VEC && k < kW) {  // edge_cols < kW: columns >= k are not candidates (padding)
+#pragma unroll
+        for (int c = 0; c < kW; ++c)
+          if (c >= k) { J[c] = -1; w[c] = __int_as_float(0x7f800000); }
+      }
+      // kth = D[v][k-1] >= D[v][kW-1]: only needed (exact-mode certificate) when
+      // that is within eps_run
+      uint32_t kb = kInfBits;
+      if (kmin) {
+        float kth = __int_as_float(0x7f800000);
+        if (k <= kW || w[kW - 1] <= eps) kth = __ldcs(dr + (k - 1));
+        kb = (kth <= eps) ? mono_bits(kth) : kInfBits;
+        kmin[cv] = kb;
+      }
+      int4* o = LE + i * (kW / 2);
+#pragma unroll
+      for (int q = 0; q < kW / 2; ++q)
+        __stcs(o + q, make_int4(J[2 * q], __float_as_int(w[2 * q]), J[2 * q + 1], __float_as_int(w[2 * q + 1])));
+      if (!direct) {
+        if (w[0] <= eps) s_rec[atomicAdd(&s_n, 1u)] = Rec{(int32_t)v, 0};
+        continue;
+      }
+      // Round 1 fused (exact mode, singleton components): the row's first
+      // candidate group, from the registers, is its component's minimum (see
+      // k_light_first); the list written is round 1's OUTPUT (rows that offered).
+      RowScan r{false, (int)k, kSent, kSentB, -1};
+      float wstar = 0.f;
+      bool done = false;
+#pragma unroll
+      for (int c = 0; c < kW; ++c) {
+        if (done || c >= k) continue;
+        const int32_t Jc = J[c];
+        if (!r.found) {
+          if (!(w[c] <= eps)) { done = true; continue; }  // sorted: no candidate at all
+          if (Jc < 0 || Jc >= N || Jc == v) continue;
+          const int32_t cc = all_core ? Jc : gat(comp + Jc);
+          if (cc < 0) continue;
+          r.found = true;
+          r.h = c;
+          wstar = w[c];
+          r.best = pack_key(mono_bits(w[c]), (uint32_t)min(v, (int64_t)Jc));
+          r.bestb = (uint32_t)max(v, (int64_t)Jc);
+          r.bestc = cc;
+        } else {
+          if (w[c] != wstar) { done = true; continue; }
+          if (Jc < 0 || Jc >= N || Jc == v) continue;
+          const int32_t cc = all_core ? Jc : gat(comp + Jc);
+          if (cc < 0) continue;
+          const uint64_t kk = pack_key(mono_bits(w[c]), (uint32_t)min(v, (int64_t)Jc));
+          const uint32_t bb = (uint32_t)max(v, (int64_t)Jc);
+          if (kk < r.best || (kk == r.best && bb < r.bestb)) { r.best = kk; r.bestb = bb; r.bestc = cc; }
+        }
+      }
+      if (!done && k > kW) {  // the search or the tie group runs past the ELL: scan the row in place
+        unsigned long long rd = 0;
+        r = scan_row<false, true>(nr, dr, k, eps, (int32_t)v, -1, 0, N, comp, all_core, rd);
+      }
+      if (rec1) {  // single rank: one packed record per component for k_hook<true>
+        __stcg(rec1 + cv, make_int4((int)(uint32_t)r.best, (int)(uint32_t)(r.best >> 32), (int)r.bestb, (int)kb));
+        if (r.found) tgt[cv] = r.bestc;
+      } else if (r.found) {
+        Kc[cv] = r.best;
+        Bc[cv] = r.bestb;
+        tgt[cv] = r.bestc;
+      }
+      if (r.found) s_rec[atomicAdd(&s_n, 1u)] = Rec{(int32_t)v, r.h};
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) s_base = s_n ? atomicAdd(n_act, s_n) : 0u;
+    __syncthreads();
+    for (uint32_t j = threadIdx.x; j < s_n; j += blockDim.x) act[s_base + j] = s_rec[j];
+    __syncthreads();
+  }
+}
+
+
+
+// Scan row v (component cv) from head h: columns < kW from the ELL row, the
+// rest (rare: a candidate prefix longer than kW) from the graph row.  DIRECT:
+// singleton components (round 1, exact mode), every candidate leaves; with
+// all_core a vertex's dense component id is the vertex itself (no gathers).
+// GW: component gathers are issued GW entries at a time; once the minimum is
+// found only entries of its weight (decided from the loaded w) are gathered,
+// so a smaller GW trades memory-level parallelism for L2 sector traffic.
+template <bool DIRECT, int GW = 4>
+__device__ __forceinline__ RowScan scan_ell(const int4* __restrict__ le, const int32_t* __restrict__ nr,
+                                            const float* __restrict__ dr, int k, float eps, int32_t v, int32_t cv,
+                                            int h, int64_t N, const int32_t* __restrict__ comp, int all_core,
+                                            unsigned long long& reads) {
+  RowScan r{false, k, kSent, kSentB, -1};
+  uint32_t wstar = 0;
+  const int kend = min(k, kW);
+  int c0 = h & ~3;
+  bool done = false;
+  while (!done && c0 < kend) {
+    int4 p0, p1;
+    ld256cs(le + (c0 >> 1), p0, p1);
+    const int32_t J[4] = {p0.x, p0.z, p1.x, p1.z};
+    const float w[4] = {__int_as_float(p0.y), __int_as_float(p0.w), __int_as_float(p1.y), __int_as_float(p1.w)};
+    reads += (unsigned long long)(min(c0 + 4, kend) - max(c0, h));
+#pragma unroll
+    for (int g0 = 0; g0 < 4; g0 += GW) {
+    if (done) break;
+    int32_t cj[4];
+#pragma unroll
+    for (int j = g0; j < g0 + GW; ++j) {
+      const int idx = c0 + j;
+      bool cand = idx >= h && idx < kend && w[j] <= eps && J[j] >= 0 && J[j] < N && J[j] != v;
+      if (GW < 4 && r.found && mono_bits(w[j]) != wstar) cand = false;  // past the tie group: no gather
+      cj[j] = cand ? ((DIRECT && all_core) ? J[j] : gat(comp + J[j])) : -1;
+    }
+#pragma unroll
+    for (int j = g0; j < g0 + GW; ++j) {
+      const int idx = c0 + j;
+      if (done || idx < h || idx >= kend) continue;
+      const bool leaving = cj[j] >= 0 && (DIRECT || cj[j] != cv);
+      const uint32_t wb = mono_bits(w[j]);
+      if (!r.found) {
+        if (!(w[j] <= eps)) { r.h = k; done = true; continue; }  // sorted: nothing left
+        if (!leaving) { h = idx + 1; continue; }                   // dead entry
+        r.found = true;
+        r.h = idx;
+        wstar = wb;
+        r.best = pack_key(wb, (uint32_t)min(v, J[j]));
+        r.bestb = (uint32_t)max(v, J[j]);
+        r.bestc = cj[j];
+      } else {
+        if (wb != wstar) { done = true; continue; }
+        if (!leaving) continue;
+        const uint64_t kk = pack_key(wb, (uint32_t)min(v, J[j]));
+        const uint32_t bb = (uint32_t)max(v, J[j]);
+        if (kk < r.best || (kk == r.best && bb < r.bestb)) { r.best = kk; r.bestb = bb; r.bestc = cj[j]; }
+      }
+    }
+    }
+    c0 += 4;
+  }
+  if (!done && k > kW) {
+    // the candidate prefix (or the minimum's tie group) runs past the ELL
+    if (!r.found) {
+      RowScan t = scan_row<false, DIRECT>(nr, dr, k, eps, v, cv, max(h, kW), N, comp, all_core, reads);
+      return t;
+    }
+    // continue the tie group of weight wstar in the graph row
+    for (int c = kW; c < k; ++c) {
+      const float wc = __ldcg(dr + c);
+      if (mono_bits(wc) != wstar || !(wc <= eps)) break;
+      const int32_t Jc = __ldcg(nr + c);
+      ++reads;
+      if (Jc < 0 || Jc >= N || Jc == v) continue;
+      const int32_t cc = (DIRECT && all_core) ? Jc : gat(comp + Jc);
+      if (cc < 0 || (!DIRECT && cc == cv)) continue;
+      const uint64_t kk = pack_key(wstar, (uint32_t)min(v, Jc));
+      const uint32_t bb = (uint32_t)max(v, Jc);
+      if (kk < r.best || (kk == r.best && bb < r.bestb)) { r.best = kk; r.bestb = bb; r.bestc = cc; }
+    }
+  }
+  if (!r.found) r.h = k;
+  return r;
+}
+
+// The row kernels below take their input in ORDER: a block grabs the next
+// chunk of kChunk records from a cursor, so all SMs work on neighbouring rows
+// at any time and the component gathers of a cluster stay L2-resident (random
+// gathers run at ~2.9e11/s while their working set is below ~64 MB, at DRAM
+// rates beyond).  Outputs are staged in shared memory and written with ONE
+// global reservation per chunk, so the next list keeps the order too.
+
+
+// round 1 (exact mode, singletons) over the ELL; see k_offer_first
+__global__ void __launch_bounds__(256) k_light_first(const int4* __restrict__ LE, const int32_t* __restrict__ nbr,
+                                                     const float* __restrict__ dist, int32_t ld, int32_t k, float eps,
+                                                     int64_t row_begin, int64_t N, const int32_t* __restrict__ comp,
+                                                     int all_core, const Rec* __restrict__ act, uint32_t n_in,
+                                                     Rec* __restrict__ act_out, uint32_t* __restrict__ n_out,
+                                                     uint32_t* __restrict__ grab,
+                                                     uint64_t* __restrict__ Kc, uint32_t* __restrict__ Bc,
+                                                     int32_t* __restrict__ tgt, unsigned long long* __restrict__ n_entries, const uint32_t* __restrict__ n_in_p = nullptr) {
+  if (n_in_p) n_in = *n_in_p;
+  __shared__ __align__(16) Rec s_rec[kChunk];
+  __shared__ uint32_t s_n, s_chunk, s_base;
+  unsigned long long reads = 0;
+  for (;;) {
+    if (threadIdx.x == 0) { s_chunk = atomicAdd(grab, 1u); s_n = 0; }
+    __syncthreads();
+    const uint64_t base = (uint64_t)s_chunk * kChunk;
+    if (base >= n_in) break;
+    for (int t = 0; t < kChunk; t += 256) {
+      const uint64_t s = base + t + threadIdx.x;
+      if (s >= n_in) continue;
+      const int2 a = __ldcs(reinterpret_cast<const int2*>(act + s));
+      const int32_t v = a.x;
+      const int64_t i = (int64_t)v - row_begin;
+      const RowScan r = scan_ell<true>(LE + i * (kW / 2), nbr + i * ld, dist + i * ld, k, eps, v, -1, a.y, N, comp,
+                                       all_core, reads);
+      if (r.found) {
+        const int32_t cv = all_core ? v : gat(comp + v);
+        Kc[cv] = r.best;
+        Bc[cv] = r.bestb;
+        tgt[cv] = r.bestc;
+        s_rec[atomicAdd(&s_n, 1u)] = Rec{v, r.h};
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) s_base = s_n ? atomicAdd(n_out, s_n) : 0u;
+    __syncthreads();
+    for (uint32_t j = threadIdx.x; j < s_n; j += blockDim.x)
+      __stcs(reinterpret_cast<int2*>(act_out + s_base + j), *reinterpret_cast<const int2*>(s_rec + j));
+    __syncthreads();
+  }
+  for (int o = 16; o > 0; o >>= 1) reads += __shfl_xor_sync(0xffffffffu, reads, o);
+  if ((threadIdx.x & 31) == 0 && reads) atomicAdd(n_entries, reads);
+}
+
+// later rounds over the ELL; see k_offer_round
+template <int GW>
+__global__ void __launch_bounds__(256) k_light_round(const int4* __restrict__ LE, const int32_t* __restrict__ nbr,
+                                                     const float* __restrict__ dist, int32_t ld, int32_t k, float eps,
+                                                     int64_t row_begin, int64_t N, const int32_t* __restrict__ comp,
+                                                     const Rec* __restrict__ act, uint32_t n_in,
+                                                     Rec* __restrict__ act_out, uint32_t* __restrict__ n_out,
+                                                     uint32_t* __restrict__ grab, Offer* __restrict__ offers,
+                                                     unsigned long long* __restrict__ Kc,
+                                                     unsigned long long* __restrict__ n_entries, const uint32_t* __restrict__ n_in_p = nullptr,
+                                                     int precheck = 0) {
+  if (n_in_p) n_in = *n_in_p;
+  __shared__ __align__(16) Rec s_rec[kChunk];
+  __shared__ __align__(16) Offer s_off[kChunk];
+  __shared__ uint32_t s_n, s_chunk, s_base;
+  unsigned long long reads = 0;
+  for (;;) {
+    if (threadIdx.x == 0) { s_chunk = atomicAdd(grab, 1u); s_n = 0; }
+    __syncthreads();
+    const uint64_t base = (uint64_t)s_chunk * kChunk;
+    if (base >= n_in) break;
+    for (int t = 0; t < kChunk; t += 256) {
+      const uint64_t s = base + t + threadIdx.x;
+      if (s >= n_in) continue;
+      const int2 a = __ldcs(reinterpret_cast<const int2*>(act + s));
+      const int32_t v = a.x;
+      const int32_t cv = gat(comp + v);
+      const int64_t i = (int64_t)v - row_begin;
+      const RowScan r = scan_ell<false, GW>(LE + i * (kW / 2), nbr + i * ld, dist + i * ld, k, eps, v, cv, a.y, N,
+                                            comp, 0, reads);
+      if (r.found) {
+        if (precheck) min_offer(Kc + cv, (unsigned long long)r.best);
+        else atomicMin(Kc + cv, (unsigned long long)r.best);
+        const uint32_t j = atomicAdd(&s_n, 1u);
+        s_rec[j] = Rec{v, r.h};
+        s_off[j] = Offer{cv, r.bestb, r.best};
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) s_base = s_n ? atomicAdd(n_out, s_n) : 0u;
+    __syncthreads();
+    for (uint32_t j = threadIdx.x; j < s_n; j += blockDim.x) {
+      __stcs(reinterpret_cast<int2*>(act_out + s_base + j), *reinterpret_cast<const int2*>(s_rec + j));
+      __stcs(reinterpret_cast<int4*>(offers + s_base + j), *reinterpret_cast<const int4*>(s_off + j));
+    }
+    __syncthreads();
+  }
+  for (int o = 16; o > 0; o >>= 1) reads += __shfl_xor_sync(0xffffffffu, reads, o);
+  if ((threadIdx.x & 31) == 0 && reads) atomicAdd(n_entries, reads);
+}
+
+// in-edge lists: scan the live in-entries of target t, drop intra entries
+// (swap-remove; they never revive), offer the minimum leaving one.
+__global__ void k_offer_in(const unsigned long long* __restrict__ in_off, int32_t* __restrict__ in_len,
+                           int32_t* __restrict__ in_src, float* __restrict__ in_w,
+                           const int32_t* __restrict__ comp, const int32_t* __restrict__ act_in,
+                           uint32_t n_in, int32_t* __restrict__ act_out, uint32_t* __restrict__ n_out,
+                           Offer* __restrict__ offers, uint32_t* __restrict__ n_off,
+                           unsigned long long* __restrict__ Kc, const uint32_t* __restrict__ n_in_p = nullptr) {
+  if (n_in_p) n_in = *n_in_p;
+  for (uint32_t base = blockIdx.x * blockDim.x; base < n_in; base += gridDim.x * blockDim.x) {
+    const uint32_t s = base + threadIdx.x;
+    bool found = false, keep = false;
+    uint64_t best = kSent;
+    uint32_t bestb = kSentB;
+    int32_t t = -1, ct = -1;
+    if (s < n_in) {
+      t = act_in[s];
+      ct = comp[t];
+      const unsigned long long o = in_off[t];
+      int32_t len = in_len[t];
+      int32_t e = 0;
+      while (e < len) {
+        const int32_t u = in_src[o + e];
+        if (comp[u] == ct) {  // intra for good: swap-remove
+          --len;
+          in_src[o + e] = in_src[o + len];
+          in_w[o + e] = in_w[o + len];
+          continue;
+        }
+        const uint64_t kk = pack_key(mono_bits(in_w[o + e]), (uint32_t)min(u, t));
+        const uint32_t bb = (uint32_t)max(u, t);
+        if (kk < best || (kk == best && bb < bestb)) { best = kk; bestb = bb; }
+        found = true;
+        ++e;
+      }
+      in_len[t] = len;
+      keep = len > 0;
+    }
+    const uint32_t a = block_reserve(n_out, keep);
+    if (keep) act_out[a] = t;
+    const uint32_t o2 = block_reserve(n_off, found);
+    if (found) {
+      offers[o2] = Offer{ct, bestb, best};
+      atomicMin(Kc + ct, (unsigned long long)best);
+    }
+  }
+}
+
+// ============================================================================
+// a4: tie pass (b of the minimum key); the offer count is read on the device
+// ============================================================================
+__global__ void k_tie(const Offer* __restrict__ offers, const uint32_t* __restrict__ n_p,
+                      const uint64_t* __restrict__ Kc, uint32_t* __restrict__ Bc) {
+  const uint32_t n = *n_p;
+  for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < n; s += gridDim.x * blockDim.x) {
+    const Offer o = offers[s];
+    if (o.key == gat(Kc + o.c)) atomicMin(Bc + o.c, o.b);
+  }
+}
+
+// stall fallback (exact mode): offer EVERY live leaving entry of the active
+// rows to both endpoint components (rows outside the active list have none)
+__global__ void k_sweep(const int32_t* __restrict__ nbr, const float* __restrict__ dist, int32_t ld, int32_t k, float eps,
+                        int64_t row_begin, int64_t N, const int32_t* __restrict__ comp,
+                        const Rec* __restrict__ act, uint32_t n_act, unsigned long long* __restrict__ Kc,
+                        uint32_t* __restrict__ Bc, int tie_phase) {
+  for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < n_act; s += gridDim.x * blockDim.x) {
+    const int64_t v = act[s].v;
+    const int64_t i = v - row_begin;
+    const int32_t cv = comp[v];
+    for (int32_t c = act[s].h; c < k; ++c) {
+      const float w = __ldg(dist + i * ld + c);
+      if (!(w <= eps)) break;
+      const int64_t J = __ldg(nbr + i * ld + c);
+      if (J < 0 || J >= N || J == v) continue;
+      const int32_t cj = comp[J];
+      if (cj < 0 || cj == cv) continue;
+      const uint64_t kk = pack_key(mono_bits(w), (uint32_t)min(v, J));
+      const uint32_t bb = (uint32_t)max(v, J);
+      if (!tie_phase) {
+        atomicMin(Kc + cv, (unsigned long long)kk);
+        atomicMin(Kc + cj, (unsigned long long)kk);
+      } else {
+        if (kk == Kc[cv]) atomicMin(Bc + cv, bb);
+        if (kk == Kc[cj]) atomicMin(Bc + cj, bb);
+      }
+    }
+  }
+}
+
+// ============================================================================
+// sim backend: elementwise MIN of per-virtual-rank partials
+// ============================================================================
+
+__global__ void k_min_into_u64(uint64_t* __restrict__ d, const uint64_t* __restrict__ s, int64_t n,
+                               const int64_t* __restrict__ np = nullptr) {
+  if (np) n = *np;
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n; c += (int64_t)gridDim.x * blockDim.x)
+    if (s[c] < d[c]) d[c] = s[c];
+}
+__global__ void k_min_into_u32(uint32_t* __restrict__ d, const uint32_t* __restrict__ s, int64_t n,
+                               const int64_t* __restrict__ np = nullptr) {
+  if (np) n = *np;
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n; c += (int64_t)gridDim.x * blockDim.x)
+    if (s[c] < d[c]) d[c] = s[c];
+}
+
+// ============================================================================
+// a5: hook (break symmetry) + MSF emission
+// ============================================================================
+
+
+__device__ __forceinline__ bool certified(uint64_t K, const uint32_t* kmin, int64_t c) {
+  return kmin == nullptr || (uint32_t)(K >> 32) < gat(kmin + c);
+}
+
+// tgt != null: the hook target of every offering component is known (round 1,
+// written by its single offer), so t = tgt[c] and "mutual" is tgt[t] == c.
+// Otherwise t is found from the selected edge's endpoints.
+// Components are taken in chunks of kHookChunk; a chunk's emitted MSF edges are
+// staged in shared memory and written with one reservation; the round counters
+// are summed in registers and flushed once per warp at the end.
+constexpr int kHookChunk = 1024;
+
+template <bool PACKED>
+__global__ void __launch_bounds__(256) k_hook(int64_t C, const uint64_t* __restrict__ Kc, const uint32_t* __restrict__ Bc,
+                       const int32_t* __restrict__ tgt, const uint32_t* __restrict__ kmin /* null = all certified */,
+                       const int32_t* __restrict__ comp, int32_t* __restrict__ parent,
+                       uint64_t* __restrict__ e_key, float* __restrict__ e_w, int64_t e_cap,
+                       RoundCounters* __restrict__ ctr, const int64_t* __restrict__ Cp,
+                       const int4* __restrict__ rec1) {
+  if (Cp) C = *Cp;
+  __shared__ uint64_t s_key[kHookChunk];
+  __shared__ uint32_t s_w[kHookChunk];
+  __shared__ uint32_t s_n, s_base;
+  uint32_t n_off = 0, n_unc = 0, n_hook = 0;
+  for (int64_t chunk = blockIdx.x; chunk * kHookChunk < C; chunk += gridDim.x) {
+    if (threadIdx.x == 0) s_n = 0;
+    __syncthreads();
+    for (int t = 0; t < kHookChunk; t += blockDim.x) {
+      const int64_t c = chunk * kHookChunk + t + threadIdx.x;
+      if (c >= C) continue;
+      uint64_t K;
+      uint32_t Bown = 0, kbown = kInfBits;
+      if (PACKED) {  // round 1, single rank: (K, B, kmin) of a component in one 16-B record
+        const int4 q = __ldcs(rec1 + c);
+        K = (uint64_t)(uint32_t)q.x | ((uint64_t)(uint32_t)q.y << 32);
+        Bown = (uint32_t)q.z;
+        kbown = (uint32_t)q.w;
+      } else {
+        K = Kc[c];
+      }
+      int32_t p = (int32_t)c;
+      if (K != kSent) {
+        ++n_off;
+        if (PACKED ? !((uint32_t)(K >> 32) < kbown) : !certified(K, kmin, c)) {
+          ++n_unc;
+        } else {
+          const uint32_t a = (uint32_t)K;
+          const uint32_t b = PACKED ? Bown : Bc[c];
+          int32_t t2;
+          if (tgt) {
+            t2 = tgt[c];
+          } else {
+            const int32_t x = (gat(comp + a) == (int32_t)c) ? (int32_t)b : (int32_t)a;
+            t2 = gat(comp + x);
+          }
+          bool mutual, cert_t = true;
+          if (PACKED) {  // one random 16-B read of the target's record
+            const int4 q = __ldcg(rec1 + t2);
+            const uint64_t Kt = (uint64_t)(uint32_t)q.x | ((uint64_t)(uint32_t)q.y << 32);
+            const uint32_t Bt = (uint32_t)q.z;
+            cert_t = Kt != kSent && (uint32_t)(Kt >> 32) < (uint32_t)q.w;
+            if (cert_t && (Kt > K || (Kt == K && Bt > b))) ctr->violation = 1u;
+            mutual = cert_t && Kt == K && Bt == b;
+          } else if (kmin) {  // exact mode: t may abstain; also audit the promise
+            const uint64_t Kt = gat(Kc + t2);
+            cert_t = Kt != kSent && certified(Kt, kmin, t2);
+            // t's true minimum is <= the edge c selected (that edge is incident
+            // to t); a larger key means t's offer missed an incident edge --
+            // impossible under a true EXACT promise, and the only way a hook
+            // cycle longer than a mutual pair could form (Fig. cycle).
+            const uint32_t Bt = cert_t ? gat(Bc + t2) : 0u;
+            if (cert_t && (Kt > K || (Kt == K && Bt > b))) ctr->violation = 1u;
+            mutual = cert_t && Kt == K && Bt == b;
+          } else if (tgt) {
+            mutual = gat(tgt + t2) == (int32_t)c;
+          } else {
+            mutual = gat(Kc + t2) == K && gat(Bc + t2) == b;
+          }
+          if (!(mutual && c < t2)) {
+            p = t2;
+            ++n_hook;
+            const uint32_t j = atomicAdd(&s_n, 1u);
+            s_key[j] = ((uint64_t)b << 32) | (uint32_t)(K >> 32);  // (b, w bits): the sort payload
+            s_w[j] = a;                                               // a: the sort key
+          }
+        }
+      }
+      parent[c] = p;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) s_base = s_n ? atomicAdd(&ctr->msf_count, s_n) : 0u;
+    __syncthreads();
+    for (uint32_t j = threadIdx.x; j < s_n; j += blockDim.x) {
+      if ((int64_t)(s_base + j) < e_cap) {
+        e_key[s_base + j] = s_key[j];
+        reinterpret_cast<uint32_t*>(e_w)[s_base + j] = s_w[j];
+      }
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    n_off += __shfl_xor_sync(0xffffffffu, n_off, o);
+    n_unc += __shfl_xor_sync(0xffffffffu, n_unc, o);
+    n_hook += __shfl_xor_sync(0xffffffffu, n_hook, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (n_off) atomicAdd(&ctr->offered, n_off);
+    if (n_unc) atomicAdd(&ctr->uncertified, n_unc);
+    if (n_hook) atomicAdd(&ctr->hooks, n_hook);
+  }
+}
+
+// ============================================================================
+// a6: pointer jumping, dense renumbering, relabel
+// ============================================================================
+// Path halving on the hook forest.  Concurrent writes only ever replace a
+// parent pointer by one of its ancestors, so every thread still reaches the
+// same root; stale reads are ancestors too, so the loop terminates.  The root
+// goes to a SEPARATE array: another thread's halving write may land on
+// parent[c] after c found its root, so parent[c] itself is not final.
+__global__ void k_jump(int64_t C, int32_t* parent, int32_t* __restrict__ rootof, RoundCounters* ctr,
+                       const int64_t* __restrict__ Cp = nullptr) {
+  if (Cp) C = *Cp;
+  volatile int32_t* P = parent;
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < C;
+       c += (int64_t)gridDim.x * blockDim.x) {
+    int32_t x = (int32_t)c;
+    int64_t steps = 0;
+    while (true) {
+      const int32_t p = P[x];
+      if (p == x) break;
+      const int32_t gp = P[p];
+      if (gp == p) { x = p; break; }
+      P[x] = gp;
+      x = gp;
+      if (++steps > C) {  // defence in depth: never spin on a cycle
+        ctr->violation = 2u;
+        break;
+      }
+    }
+    rootof[c] = x;
+  }
+}
+
+__global__ void k_root_flags(int64_t C, const int32_t* __restrict__ rootof, int32_t* __restrict__ flag,
+                             const int64_t* __restrict__ Cp = nullptr) {
+  // C is the (host) upper bound the scan runs over; with Cp the true count is
+  // on the device and the flags beyond it are 0
+  const int64_t Ct = Cp ? *Cp : C;
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < C;
+       c += (int64_t)gridDim.x * blockDim.x)
+    flag[c] = c < Ct && rootof[c] == (int32_t)c;
+}
+
+// number of roots = new component count, from the exclusive scan
+__global__ void k_count_roots(const int64_t* __restrict__ Cp, const int32_t* __restrict__ newid,
+                              const int32_t* __restrict__ flag, int64_t* __restrict__ Cn) {
+  const int64_t C = *Cp;
+  *Cn = C > 0 ? (int64_t)newid[C - 1] + flag[C - 1] : 0;
+}
+
+// new per-component arrays: cmin/kmin are minima over the merged tree
+__global__ void k_merge(int64_t C, const int32_t* __restrict__ rootof, const int32_t* __restrict__ newid,
+                        const int32_t* __restrict__ cmin, const uint32_t* __restrict__ kmin,
+                        int32_t* __restrict__ cmin2, uint32_t* __restrict__ kmin2, int32_t* __restrict__ map, const int64_t* __restrict__ Cp = nullptr) {
+  if (Cp) C = *Cp;
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < C;
+       c += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t r = newid ? gat(newid + rootof[c]) : rootof[c];  // sparse ids: the root itself
+    map[c] = r;
+    atomicMin(cmin2 + r, cmin[c]);
+    if (kmin) {
+      const uint32_t km = kmin[c];
+      if (km != kInfBits) atomicMin(kmin2 + r, km);  // kmin2 starts at +inf
+    }
+  }
+}
+
+__global__ void k_fill_i32(int32_t* __restrict__ p, int64_t n, int32_t val, const int64_t* __restrict__ np = nullptr) {
+  if (np) n = *np;
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n;
+       c += (int64_t)gridDim.x * blockDim.x)
+    p[c] = val;
+}
+
+// comp[v] = m2[m1[comp[v]]] (m2 optional) for every comp[v] >= 0.  Each thread
+// takes 8 consecutive vertices per step (two int4 loads, 8 independent
+// gathers in flight): the loop is bound by gather latency otherwise.
+__global__ void k_relabel(int64_t N, int32_t* __restrict__ comp, const int32_t* __restrict__ m1,
+                          const int32_t* __restrict__ m2) {
+  const int64_t n8 = ((uintptr_t)comp & 15u) ? 0 : N / 8;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n8; q += (int64_t)gridDim.x * blockDim.x) {
+    int4* p = reinterpret_cast<int4*>(comp) + 2 * q;
+    int4 a = p[0], b = p[1];
+    int32_t c[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    // read-only maps through L1 (__ldg): when few components remain, 64M
+    // gathers hit a handful of lines, which would serialise on their L2 slices
+    const int32_t c0[8] = {c[0], c[1], c[2], c[3], c[4], c[5], c[6], c[7]};
+#pragma unroll
+    for (int j = 0; j < 8; ++j) c[j] = c[j] >= 0 ? __ldg(m1 + c[j]) : c[j];
+    if (m2) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) c[j] = c[j] >= 0 ? __ldg(m2 + c[j]) : c[j];
+    }
+    // sparse ids (late rounds): most vertices keep theirs -- store only changes
+    bool ch0 = false, ch1 = false;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) { ch0 |= c[j] != c0[j]; ch1 |= c[j + 4] != c0[j + 4]; }
+    if (ch0) p[0] = make_int4(c[0], c[1], c[2], c[3]);
+    if (ch1) p[1] = make_int4(c[4], c[5], c[6], c[7]);
+  }
+  for (int64_t v = n8 * 8 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < N;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    int32_t c = comp[v];
+    if (c >= 0) {
+      c = __ldg(m1 + c);
+      if (m2) c = __ldg(m2 + c);
+      comp[v] = c;
+    }
+  }
+}
+
+// ============================================================================
+// a9 / a11: canonical labels, MSF output, exact weight
+// ============================================================================
+
+// MSF output in (a, b) order: radix sort on the 32-bit a (only ceil(log2 N)
+// bits) carrying (b, w) as a 64-bit payload, then each run of equal a (tiny:
+// a vertex is the smaller endpoint of few MSF edges) is sorted by b in place.
+// ka = the sorted a (the caller's mst_a); splits the (b, w) payload into mst_b /
+// mst_w and sorts every run of equal a by b
+__global__ void k_msf_unpack(int64_t m, const uint32_t* __restrict__ ka, const unsigned long long* __restrict__ vb,
+                             uint32_t* __restrict__ b, float* __restrict__ w) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t ai = ka[i];
+    if (i > 0 && ka[i - 1] == ai) continue;  // not the start of a run
+    int64_t j = i + 1;
+    while (j < m && ka[j] == ai) ++j;
+    for (int64_t p = i; p < j; ++p) {  // insertion sort of the run [i, j) by b
+      const unsigned long long x = vb[p];
+      int64_t q = p;
+      while (q > i && (uint32_t)(b[q - 1]) > (uint32_t)(x >> 32)) {
+        b[q] = b[q - 1];
+        w[q] = w[q - 1];
+        --q;
+      }
+      b[q] = (uint32_t)(x >> 32);
+      w[q] = __uint_as_float((uint32_t)x);
+    }
+  }
+}
+
+// exact sum: integer mantissas bucketed by biased exponent (order independent)
+__global__ void k_wbuckets(int64_t m, const float* __restrict__ w, unsigned long long* __restrict__ bk) {
+  __shared__ unsigned long long sb[256];
+  for (int t = threadIdx.x; t < 256; t += blockDim.x) sb[t] = 0;
+  __syncthreads();
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t u = __float_as_uint(w[e]) & 0x7fffffffu;
+    const uint32_t ex = u >> 23;
+    uint32_t man = u & 0x7fffffu;
+    if (ex) man |= 0x800000u;
+    // lanes sharing an exponent pre-sum (32 x 2^24 < 2^32) -> one smem atomic each
+    const unsigned grp = __match_any_sync(__activemask(), ex);
+    const uint32_t sum = __reduce_add_sync(grp, man);
+    if ((threadIdx.x & 31) == __ffs(grp) - 1 && sum) atomicAdd(sb + ex, (unsigned long long)sum);
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < 256; t += blockDim.x)
+    if (sb[t]) atomicAdd(bk + t, sb[t]);
+}
+
+// a10: labels of this rank's rows
+// One row per lane: a core row's label is comp[v] (the common case); the
+// warp's non-core rows (ballot) are then scanned cooperatively, kLabelG lanes
+// per row and 4 entries per lane and step, so a scan (at most M-1 entries within
+// eps, then the first one beyond) is read as 64-byte coalesced pieces instead of
+// a serial per-thread walk.  The first event in column order decides: an entry
+// beyond eps ends the scan (noise), a core neighbour within eps gives the label.
+constexpr int kLabelG = 4;
+template <bool VEC>
+__global__ void k_label(const int32_t* __restrict__ nbr, const float* __restrict__ dist, int64_t n_rows,
+                        int32_t k, float eps, int64_t row_begin, int64_t N,
+                        const uint32_t* __restrict__ bits, const int32_t* __restrict__ comp,
+                        int32_t* __restrict__ labels) {
+  constexpr int G = kLabelG, RPS = 32 / G;  // rows per cooperative step
+  const int lane = threadIdx.x & 31, sub = lane & (G - 1);
+  const unsigned gmask = ((1u << G) - 1u) << (lane & ~(G - 1));
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t base = warp * 32; base < n_rows; base += nwarps * 32) {  // warp-uniform
+    const int64_t i = base + lane;
+    bool pending = false;
+    if (i < n_rows) {
+      const int64_t v = row_begin + i;
+      if (is_core(bits, v)) labels[i] = comp[v];
+      else pending = true;
+    }
+    unsigned todo = __ballot_sync(0xffffffffu, pending);
+    while (todo) {  // RPS non-core rows of this warp at a time, G lanes each
+      const int slot = lane / G;
+      unsigned t = todo;
+      for (int s2 = 0; s2 < slot && t; ++s2) t &= t - 1;  // the slot-th pending row
+      const int r = t ? __ffs(t) - 1 : -1;
+      for (int s2 = 0; s2 < RPS && todo; ++s2) todo &= todo - 1;
+      if (r < 0) continue;  // the whole group idles this step
+      const int64_t ii = base + r;
+      const int32_t* nr = nbr + ii * k;
+      const float* dr = dist + ii * k;
+      int32_t lab = -1;
+      bool decided = false;
+      for (int c0 = 0; c0 < k && !decided; c0 += 4 * G) {
+        const int c = c0 + 4 * sub;
+        int32_t J[4];
+        float w[4];
+        if (VEC && c + 4 <= k) {
+          const int4 j4 = __ldcs(reinterpret_cast<const int4*>(nr + c));
+          const float4 w4 = __ldcs(reinterpret_cast<const float4*>(dr + c));
+          J[0] = j4.x; J[1] = j4.y; J[2] = j4.z; J[3] = j4.w;
+          w[0] = w4.x; w[1] = w4.y; w[2] = w4.z; w[3] = w4.w;
+        } else {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const bool in = c + j < k;
+            J[j] = in ? __ldcs(nr + c + j) : -1;
+            w[j] = in ? __ldcs(dr + c + j) : __int_as_float(0x7f800000);
+          }
+        }
+        int ev = 4;
+        bool hit = false;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          if (ev < 4) continue;
+          if (c + j >= k) { ev = j; break; }  // row end: as beyond eps
+          if (!(w[j] <= eps)) { ev = j; continue; }
+          const int64_t Jj = J[j];
+          if (Jj >= 0 && Jj < N && is_core(bits, Jj)) { ev = j; hit = true; lab = (int32_t)Jj; }
+        }
+        const unsigned any = __ballot_sync(gmask, ev < 4) & gmask;
+        if (any) {
+          decided = true;
+          if (lane == __ffs(any) - 1) labels[ii] = hit ? comp[lab] : -1;
+        }
+      }
+      if (!decided && sub == 0) labels[ii] = -1;
+    }
+  }
+}
+
