@@ -462,3 +462,24 @@ def test_offer_precheck_toggle(case, pre, monkeypatch):
     for compact in ("0", "1"):
         monkeypatch.setenv("KDB_COMPACT", compact)
         assert_parity(run_gpu(nbr, dist, M, eps, exact=False), exp)
+
+
+@pytest.mark.parametrize("L", [7, 30])
+@pytest.mark.parametrize("P", [0, 3])
+def test_torus_ties_force_the_sweep_round(L, P):
+    """L x L torus, k = 4: every row holds its 4 lattice neighbours at w = 1, so
+    kth'(v) = 1 equals every offer and no component can certify (reading #20):
+    the exact mode must stall and finish with edge-centric sweep rounds.  The
+    graph is an exact kNN graph of the torus metric (symmetric, mirrored)."""
+    import paper_2009_04552_b200 as kdb
+    n = L * L
+    ids = np.arange(n).reshape(L, L)
+    nb = np.stack([np.roll(ids, 1, 0), np.roll(ids, -1, 0), np.roll(ids, 1, 1), np.roll(ids, -1, 1)], -1)
+    nbr = nb.reshape(n, 4).astype(np.int32)
+    dist = np.ones((n, 4), np.float32)
+    exp = oracle_run(nbr, dist, 4, 1.0)
+    got = run_gpu(nbr, dist, 4, 1.0, exact=True, comm=kdb.Comm.sim(P) if P else None)
+    assert_parity(got, exp)
+    assert got["stats"]["stall_rounds"] > 0
+    assert len(exp["msf_a"]) == n - 1
+    assert_parity(run_gpu(nbr, dist, 4, 1.0, exact=False), exp)
