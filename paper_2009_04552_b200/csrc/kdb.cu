@@ -574,10 +574,11 @@ kdb_status mst_impl(const kdb_graph* g, float eps, const uint32_t* core_bits, in
     LAUNCH(k_cut_edges, grid_for(N), kThreads, st, g->nbr, g->dist, N, m.ld, m.k, eps, (int)nparts, core_bits,
            comp, R.hs[0], R.hs_cap, R.n_hs_dev);
     KDB_CUDA(cudaGetLastError());
-    uint32_t ncut = 0;
-    KDB_CUDA(cudaMemcpyAsync(&ncut, R.n_hs_dev, 4, cudaMemcpyDeviceToHost, st));
+    uint32_t nc[2] = {0, 0};  // count, sticky overflow flag
+    KDB_CUDA(cudaMemcpyAsync(nc, R.n_hs_dev, 8, cudaMemcpyDeviceToHost, st));
     KDB_CUDA(cudaStreamSynchronize(st));
-    if (ncut > R.hs_cap) return set_err(KDB_EINTERNAL, "cut entries exceed their buffer");
+    const uint32_t ncut = nc[0];
+    if (ncut > R.hs_cap || nc[1]) return set_err(KDB_EINTERNAL, "cut entries exceed their buffer");
     R.n_hs = ncut;
     m.survivors = ncut;
     KDB_CUDA(cudaEventRecord(m.ev[1], st));
@@ -688,6 +689,9 @@ kdb_status kdb_mst_inexact(const kdb_graph* g, float eps, const uint32_t* core_b
                            uint32_t* mst_a, uint32_t* mst_b, float* mst_w, int64_t mst_cap, int64_t* mst_count,
                            double* mst_weight, void* workspace, size_t ws_bytes, kdb_stream_t stream) {
   if (nparts < 1) return set_err(KDB_EINVAL, "nparts must be >= 1");
+  // the cut entries are counted in 32 bits (survivor buffers)
+  if (g && g->n_rows * (int64_t)edge_cols_of(g) >= (int64_t)UINT32_MAX - 1)
+    return set_err(KDB_EINVAL, "kdb_mst_inexact: n_rows * edge_cols must stay below 2^32");
   return mst_impl(g, eps, core_bits, comp, mst_a, mst_b, mst_w, mst_cap, mst_count, mst_weight, workspace, ws_bytes,
                   nullptr, stream, nparts);
 }

@@ -279,7 +279,11 @@ __global__ void __launch_bounds__(kFilterThreads) k_filter(
           }
           const int tot = __shfl_sync(0xffffffffu, incl, 31);
           uint32_t base_slot = 0;
-          if (lane == 31) base_slot = atomicAdd(n_out, (uint32_t)tot);
+          if (lane == 31) {
+            base_slot = atomicAdd(n_out, (uint32_t)tot);
+            // sticky overflow flag in n_out[1]: the 32-bit count itself could wrap
+            if ((uint64_t)base_slot + (uint64_t)tot > (uint64_t)cap) atomicOr(n_out + 1, 1u);
+          }
           base_slot = __shfl_sync(0xffffffffu, base_slot, 31);
           uint32_t slot = base_slot + (uint32_t)(incl - cnt);
 #pragma unroll
@@ -355,6 +359,7 @@ __global__ void k_cut_edges(const int32_t* __restrict__ nbr, const float* __rest
       const int64_t J = nbr[v * ld + c];
       if (J < 0 || J >= n || J == v || !is_core(bits, J) || part_of(J, n, P) == pv) continue;
       const uint32_t s = atomicAdd(n_out, 1u);
+      if (s >= cap) atomicOr(n_out + 1, 1u);  // sticky overflow flag (the count could wrap)
       if (s < cap) {
         HEdge h;
         h.key = pack_key(mono_bits(w), (uint32_t)min(v, J));

@@ -806,12 +806,12 @@ kdb_status filter_phase(Mst& m, float eps, bool* overflow) {
   uint32_t over = 0;
   unsigned long long tot = 0;
   for (auto& R : L.ranks) {
-    uint32_t n = 0;
-    KDB_CUDA(cudaMemcpyAsync(&n, R.n_hs_dev, 4, cudaMemcpyDeviceToHost, st));
+    uint32_t nf[2] = {0, 0};  // count, sticky overflow flag
+    KDB_CUDA(cudaMemcpyAsync(nf, R.n_hs_dev, 8, cudaMemcpyDeviceToHost, st));
     KDB_CUDA(cudaStreamSynchronize(st));
-    R.n_hs = n;
-    tot += n;
-    if (n > R.hs_cap) over = 1;
+    R.n_hs = nf[0];
+    tot += nf[0];
+    if (nf[0] > R.hs_cap || nf[1]) over = 1;
   }
   if (multi_rank(m.comm)) {  // every rank must take the same branch
     uint32_t* d = L.ranks[0].n_hs_dev + 1;
