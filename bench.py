@@ -239,9 +239,23 @@ def run_reference(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": dict(workload_desc(args.config, W, args.scale), **stage_desc(ec, eps_list, W)),
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample,
+                             "cpu_model": host_cpu()[0], "box_cores": host_cpu()[1]},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     emit(line, args)
+
+
+def host_cpu():
+    """(model name, logical cores) of the host the oracle baseline runs on."""
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return model, os.cpu_count()
 
 
 def emit(line, args):
@@ -394,6 +408,7 @@ def run_ours(args):
         ns = min(args.cpu_sample_rows, N)
         dt, _ = oracle_sample(W["nbr"][:ns].cpu().numpy(), W["dist"][:ns].cpu().numpy(), M, eps_list, ec)
         cpu = {"value": ns * k * F / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+               "cpu_model": host_cpu()[0], "box_cores": host_cpu()[1],
                "sample": f"rows [0, {ns}) of the workload ({ns * k} entries; entries to ids >= {ns} skipped), "
                          f"one single-threaded run, {dt:.1f} s"}
 
