@@ -302,7 +302,7 @@ struct RoundCounters {
   uint32_t violation;            // a hook target's key exceeds the hooker's: the
                                  // KDB_GRAPH_EXACT promise was false (or a bug)
   uint32_t n_cont;               // rows continuing in the warp-per-row scan
-  uint32_t pad1;
+  uint32_t n_deep;               // per rank: rows whose kW ELL entries are all within eps_run
   uint32_t grab;                 // chunk cursor of the ordered row kernels (per rank)
   uint32_t n_off2;
   uint32_t na[2];                // per rank: row-list sizes, ping-pong (input na[cur], output na[cur^1])

@@ -63,6 +63,7 @@ struct RankState {
   const float* dist = nullptr;
   Rec* act[2] = {nullptr, nullptr};  // active rows (v, head), ping-pong
   uint32_t n_act = 0;                 // live rows in act[cur]
+  uint32_t n_deep = 0;                // rows whose ELL entries are all light (k_light_ell)
   bool compact = false;               // rows phase reads the light ELL (else the graph rows)
   int4* LE = nullptr;                 // light ELL [n_rows][kW] (J, w bits) pairs
   // offers: [0, n_rows) from rows (same slot as the row's next record),
@@ -385,7 +386,7 @@ kdb_status rows_phase(Mst& m, float eps_run) {
 #define KDB_ELL_LAUNCH(V, A)                                                                                    \
   LAUNCH((k_light_ell<V, A>), grid_for(R.n_rows), kThreads, st, R.nbr, R.dist, R.n_rows, ld, k, eps_run, R.row_begin, \
          comp, general ? nullptr : L.kmin, R.LE, R.act[0], &R.ctr->na[0], &R.ctr->grab, fuse1 ? 1 : 0,         \
-         L.all_core, N, R.Kc, R.Bc, R.tgt, packed1 ? L.rec1 : nullptr)
+         L.all_core, N, R.Kc, R.Bc, R.tgt, packed1 ? L.rec1 : nullptr, &R.ctr->n_deep)
       if (a32) KDB_ELL_LAUNCH(true, true);
       else if (vec) KDB_ELL_LAUNCH(true, false);
       else KDB_ELL_LAUNCH(false, false);
@@ -424,6 +425,7 @@ kdb_status rows_phase(Mst& m, float eps_run) {
     KDB_CUDA(cudaMemcpyAsync(&hc, R.ctr, sizeof(hc), cudaMemcpyDeviceToHost, st));
     KDB_CUDA(cudaStreamSynchronize(st));
     R.n_act = hc.na[0];
+    R.n_deep = hc.n_deep;
     R.n_in_act = hc.ni[0];
   }
   KDB_CUDA(cudaEventRecord(ev[2], st));
@@ -569,8 +571,16 @@ kdb_status rows_phase(Mst& m, float eps_run) {
   LAUNCH(k_light_round<GW>, grid_for(na_ub[r]), kThreads, st, R.LE, R.nbr, R.dist, ld, k, eps_run, R.row_begin, N, \
          comp, R.act[cur], na_ub[r], R.act[cur ^ 1], nout, &R.ctr->grab, R.offers, (unsigned long long*)R.Kc,      \
          &L.ctr->entries, nin, precheck)
+          // pipelined chunk loads pay when many rows scan past their first chunk
+          // (C3: its inner shell is all light); they cost occupancy otherwise
+          const int pk = env_int("KDB_PIPE", -1);
+          const bool pipe = pk >= 0 ? pk != 0 : (uint64_t)R.n_deep * 100 > (uint64_t)R.n_rows * 15;
           if (gw == 1) KDB_LR_LAUNCH(1);
           else if (gw == 2) KDB_LR_LAUNCH(2);
+          else if (pipe)
+            LAUNCH((k_light_round<4, true>), grid_for(na_ub[r]), kThreads, st, R.LE, R.nbr, R.dist, ld, k, eps_run,
+                   R.row_begin, N, comp, R.act[cur], na_ub[r], R.act[cur ^ 1], nout, &R.ctr->grab, R.offers,
+                   (unsigned long long*)R.Kc, &L.ctr->entries, nin, precheck);
           else KDB_LR_LAUNCH(4);
 #undef KDB_LR_LAUNCH
         }

@@ -372,9 +372,10 @@ __global__ void __launch_bounds__(256) k_light_ell(const int32_t* __restrict__ n
                                                    uint32_t* __restrict__ n_act, uint32_t* __restrict__ grab,
                                                    int direct, int all_core, int64_t N, uint64_t* __restrict__ Kc,
                                                    uint32_t* __restrict__ Bc, int32_t* __restrict__ tgt,
-                                                   int4* __restrict__ rec1) {
+                                                   int4* __restrict__ rec1, uint32_t* __restrict__ n_deep) {
   __shared__ __align__(16) Rec s_rec[kChunk];
   __shared__ uint32_t s_n, s_chunk, s_base;
+  uint32_t deep = 0;  // rows whose kW ELL entries are all within eps (their scans go past the first chunk)
   for (;;) {
     if (threadIdx.x == 0) { s_chunk = atomicAdd(grab, 1u); s_n = 0; }
     __syncthreads();
@@ -448,6 +449,7 @@ __global__ void __launch_bounds__(256) k_light_ell(const int32_t* __restrict__ n
         kb = (kth <= eps) ? mono_bits(kth) : kInfBits;
         kmin[cv] = kb;
       }
+      deep += w[kW - 1] <= eps;
       int4* o = LE + i * (kW / 2);
 #pragma unroll
       for (int q = 0; q < kW / 2; ++q)
@@ -507,6 +509,8 @@ __global__ void __launch_bounds__(256) k_light_ell(const int32_t* __restrict__ n
     for (uint32_t j = threadIdx.x; j < s_n; j += blockDim.x) act[s_base + j] = s_rec[j];
     __syncthreads();
   }
+  for (int o = 16; o > 0; o >>= 1) deep += __shfl_xor_sync(0xffffffffu, deep, o);
+  if ((threadIdx.x & 31) == 0 && deep) atomicAdd(n_deep, deep);
 }
 
 
@@ -518,7 +522,7 @@ __global__ void __launch_bounds__(256) k_light_ell(const int32_t* __restrict__ n
 // GW: component gathers are issued GW entries at a time; once the minimum is
 // found only entries of its weight (decided from the loaded w) are gathered,
 // so a smaller GW trades memory-level parallelism for L2 sector traffic.
-template <bool DIRECT, int GW = 4>
+template <bool DIRECT, int GW = 4, bool PIPE = false>
 __device__ __forceinline__ RowScan scan_ell(const int4* __restrict__ le, const int32_t* __restrict__ nr,
                                             const float* __restrict__ dr, int k, float eps, int32_t v, int32_t cv,
                                             int h, int64_t N, const int32_t* __restrict__ comp, int all_core,
@@ -528,9 +532,20 @@ __device__ __forceinline__ RowScan scan_ell(const int4* __restrict__ le, const i
   const int kend = min(k, kW);
   int c0 = h & ~3;
   bool done = false;
+  // PIPE: the next chunk's load is issued with the current one, so a row whose
+  // chunk holds no leaving entry does not wait a second load latency (chosen per
+  // input: pays when many rows scan past their first chunk, see rows_phase)
+  int4 q0, q1;
+  if (PIPE && c0 < kend) ld256cs(le + (c0 >> 1), q0, q1);
   while (!done && c0 < kend) {
     int4 p0, p1;
-    ld256cs(le + (c0 >> 1), p0, p1);
+    if (PIPE) {
+      p0 = q0;
+      p1 = q1;
+      if (c0 + 4 < kend) ld256cs(le + ((c0 + 4) >> 1), q0, q1);
+    } else {
+      ld256cs(le + (c0 >> 1), p0, p1);
+    }
     const int32_t J[4] = {p0.x, p0.z, p1.x, p1.z};
     const float w[4] = {__int_as_float(p0.y), __int_as_float(p0.w), __int_as_float(p1.y), __int_as_float(p1.w)};
     reads += (unsigned long long)(min(c0 + 4, kend) - max(c0, h));
@@ -649,7 +664,7 @@ __global__ void __launch_bounds__(256) k_light_first(const int4* __restrict__ LE
 }
 
 // later rounds over the ELL; see k_offer_round
-template <int GW>
+template <int GW, bool PIPE = false>
 __global__ void __launch_bounds__(256) k_light_round(const int4* __restrict__ LE, const int32_t* __restrict__ nbr,
                                                      const float* __restrict__ dist, int32_t ld, int32_t k, float eps,
                                                      int64_t row_begin, int64_t N, const int32_t* __restrict__ comp,
@@ -676,8 +691,8 @@ __global__ void __launch_bounds__(256) k_light_round(const int4* __restrict__ LE
       const int32_t v = a.x;
       const int32_t cv = gat(comp + v);
       const int64_t i = (int64_t)v - row_begin;
-      const RowScan r = scan_ell<false, GW>(LE + i * (kW / 2), nbr + i * ld, dist + i * ld, k, eps, v, cv, a.y, N,
-                                            comp, 0, reads);
+      const RowScan r = scan_ell<false, GW, PIPE>(LE + i * (kW / 2), nbr + i * ld, dist + i * ld, k, eps, v, cv, a.y,
+                                                  N, comp, 0, reads);
       if (r.found) {
         if (precheck) min_offer(Kc + cv, (unsigned long long)r.best);
         else atomicMin(Kc + cv, (unsigned long long)r.best);

@@ -483,3 +483,18 @@ def test_torus_ties_force_the_sweep_round(L, P):
     assert got["stats"]["stall_rounds"] > 0
     assert len(exp["msf_a"]) == n - 1
     assert_parity(run_gpu(nbr, dist, 4, 1.0, exact=False), exp)
+
+
+@pytest.mark.parametrize("pipe", ["0", "1"])
+@pytest.mark.parametrize("case", RANDOM_CASES)
+def test_pipelined_chunk_loads_toggle(case, pipe, monkeypatch):
+    """scan_ell with the next ELL chunk's load issued ahead (KDB_PIPE forces it
+    on / off; by default it follows the share of all-light ELL rows)."""
+    monkeypatch.setenv("KDB_PIPE", pipe)
+    n, k, M, seed, levels, sym, pad, zero, local, q = case
+    nbr, dist = random_graph(n, k, seed, levels=levels, symmetric=sym, pad_frac=pad, zero_frac=zero, local=local)
+    eps = np.float32(np.quantile(dist[np.isfinite(dist)].astype(np.float64), q))
+    exp = oracle_run(nbr, dist, M, eps)
+    for light in ("2", "10"):
+        monkeypatch.setenv("KDB_LIGHT", light)
+        assert_parity(run_gpu(nbr, dist, M, eps, exact=False), exp)
