@@ -41,6 +41,7 @@
 #include <nccl.h>
 
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_segmented_sort.cuh>
 #include <cub/device/device_scan.cuh>
 #include <cub/device/device_select.cuh>
 #include <cub/device/device_reduce.cuh>
@@ -632,7 +633,27 @@ kdb_status mst_impl(const kdb_graph* g, float eps, const uint32_t* core_bits, in
                                                reinterpret_cast<const unsigned long long*>(L.e_key), vb2, (int)ne, 0,
                                                abits, st));
     }
-    LAUNCH(k_msf_unpack, grid_for(ne), kThreads, st, ne, mst_a, vb2, mst_b, mst_w);
+    // runs of equal a longer than kRunMax (a hub vertex: duplicates, stars) are
+    // left to a segmented sort instead of one thread's insertion sort
+    int32_t* seg_b = L.cmin2;  // free after the phases
+    int32_t* seg_e = L.newid;
+    KDB_CUDA(cudaMemsetAsync(&L.ctr->n_off, 0, sizeof(uint32_t), st));
+    LAUNCH(k_msf_unpack, grid_for(ne), kThreads, st, ne, mst_a, vb2, mst_b, mst_w, seg_b, seg_e, &L.ctr->n_off);
+    uint32_t nseg = 0;
+    KDB_CUDA(cudaMemcpyAsync(&nseg, &L.ctr->n_off, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    KDB_CUDA(cudaStreamSynchronize(st));
+    if (nseg > 0) {
+      uint32_t* kout = reinterpret_cast<uint32_t*>(vb2);  // vb2 (8 (N + 1) bytes) is free after the unpack
+      float* vout = reinterpret_cast<float*>(kout + ne);
+      size_t cbs = L.cub_bytes;
+      {
+        LaunchScope ls_("cub::DeviceSegmentedSort", st, false);
+        KDB_CUDA(cub::DeviceSegmentedSort::SortPairs(L.cub_tmp, cbs, mst_b, kout, mst_w, vout, (int)ne, (int)nseg,
+                                                     seg_b, seg_e, st));
+      }
+      LAUNCH(k_copy_segments, (int)std::min<uint32_t>(nseg, 1u << 20), kThreads, st, seg_b, seg_e, nseg, kout, vout,
+             mst_b, mst_w);
+    }
     KDB_CUDA(cudaMemsetAsync(L.buckets, 0, 256 * sizeof(unsigned long long), st));
     LAUNCH(k_wbuckets, grid_for(ne), kThreads, st, ne, mst_w, L.buckets);
     KDB_CUDA(cudaGetLastError());

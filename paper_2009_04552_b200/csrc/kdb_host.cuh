@@ -122,7 +122,12 @@ size_t cub_tmp_bytes(int64_t N, int64_t cap_edges) {
                                   (const unsigned long long*)nullptr, (unsigned long long*)nullptr,
                                   (int)std::max<int64_t>(cap_edges, 1));
   size_t f = 0;
-  size_t h3 = 0;
+  size_t h3 = 0, g3 = 0;
+  cub::DeviceSegmentedSort::SortPairs(nullptr, g3, (const uint32_t*)nullptr, (uint32_t*)nullptr,
+                                      (const float*)nullptr, (float*)nullptr, (int)std::max<int64_t>(N + 1, 1),
+                                      (int)std::max<int64_t>(N / (kRunMax + 1) + 1, 1), (const int32_t*)nullptr,
+                                      (const int32_t*)nullptr);
+  f = std::max(f, g3);
   cub::DeviceSelect::Flagged(nullptr, h3, (const HEdge*)nullptr, (const uint8_t*)nullptr, (HEdge*)nullptr,
                              (uint32_t*)nullptr, (int)std::min<int64_t>(survivor_cap(N, 65535) + 1, INT32_MAX));
   f = std::max(f, h3);

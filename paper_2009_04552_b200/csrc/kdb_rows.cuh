@@ -1056,13 +1056,26 @@ __global__ void k_relabel(int64_t N, int32_t* __restrict__ comp, const int32_t* 
 // a vertex is the smaller endpoint of few MSF edges) is sorted by b in place.
 // ka = the sorted a (the caller's mst_a); splits the (b, w) payload into mst_b /
 // mst_w and sorts every run of equal a by b
+constexpr int kRunMax = 32;  // longer runs of equal a go to the segmented sort
 __global__ void k_msf_unpack(int64_t m, const uint32_t* __restrict__ ka, const unsigned long long* __restrict__ vb,
-                             uint32_t* __restrict__ b, float* __restrict__ w) {
+                             uint32_t* __restrict__ b, float* __restrict__ w, int32_t* __restrict__ seg_b,
+                             int32_t* __restrict__ seg_e, uint32_t* __restrict__ nseg) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t ai = ka[i];
     if (i > 0 && ka[i - 1] == ai) continue;  // not the start of a run
     int64_t j = i + 1;
     while (j < m && ka[j] == ai) ++j;
+    if (j - i > kRunMax) {  // a hub: unpacked as is, sorted by b afterwards (k_copy_segments)
+      for (int64_t p = i; p < j; ++p) {
+        const unsigned long long x = vb[p];
+        b[p] = (uint32_t)(x >> 32);
+        w[p] = __uint_as_float((uint32_t)x);
+      }
+      const uint32_t s = atomicAdd(nseg, 1u);
+      seg_b[s] = (int32_t)i;
+      seg_e[s] = (int32_t)j;
+      continue;
+    }
     for (int64_t p = i; p < j; ++p) {  // insertion sort of the run [i, j) by b
       const unsigned long long x = vb[p];
       int64_t q = p;
@@ -1075,6 +1088,17 @@ __global__ void k_msf_unpack(int64_t m, const uint32_t* __restrict__ ka, const u
       w[q] = __uint_as_float((uint32_t)x);
     }
   }
+}
+
+// the sorted long runs back into the output (one block per run)
+__global__ void k_copy_segments(const int32_t* __restrict__ seg_b, const int32_t* __restrict__ seg_e, uint32_t nseg,
+                                const uint32_t* __restrict__ kout, const float* __restrict__ vout,
+                                uint32_t* __restrict__ b, float* __restrict__ w) {
+  for (uint32_t s = blockIdx.x; s < nseg; s += gridDim.x)
+    for (int32_t p = seg_b[s] + threadIdx.x; p < seg_e[s]; p += blockDim.x) {
+      b[p] = kout[p];
+      w[p] = vout[p];
+    }
 }
 
 // exact sum: integer mantissas bucketed by biased exponent (order independent)

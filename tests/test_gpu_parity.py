@@ -498,3 +498,29 @@ def test_pipelined_chunk_loads_toggle(case, pipe, monkeypatch):
     for light in ("2", "10"):
         monkeypatch.setenv("KDB_LIGHT", light)
         assert_parity(run_gpu(nbr, dist, M, eps, exact=False), exp)
+
+
+@pytest.mark.parametrize("n", [40, 5000, 50000])
+def test_star_forest_hub_runs(n):
+    """Every vertex's nearest neighbour is vertex 0: the MSF is a star, one run
+    of n-1 edges with a = 0.  Runs longer than kRunMax are sorted by the
+    segmented sort (an insertion sort per run was quadratic: 220 s at 1e5)."""
+    import time
+    k = 4
+    rng = np.random.default_rng(n)
+    nbr = np.empty((n, k), np.int32)
+    dist = np.empty((n, k), np.float32)
+    nbr[0] = np.arange(1, k + 1)
+    dist[0] = 0.1
+    others = rng.integers(1, n, size=(n, k - 1)).astype(np.int32)
+    v = np.arange(n, dtype=np.int32)[:, None]
+    others = np.where(others == v, (v % (n - 1)) + 1, others).astype(np.int32)  # no self entries
+    nbr[1:, 0] = 0
+    nbr[1:, 1:] = others[1:]
+    dist[1:] = [0.1, 0.5, 0.6, 0.7]
+    exp = oracle_run(nbr, dist, 1, 1.0)
+    t = time.time()
+    got = run_gpu(nbr, dist, 1, 1.0, exact=False)
+    assert time.time() - t < 5.0
+    assert_parity(got, exp)
+    assert np.all(got["msf_a"] == 0) and len(got["msf_a"]) == n - 1
