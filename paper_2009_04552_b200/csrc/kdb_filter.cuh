@@ -50,6 +50,9 @@ constexpr int kBloomBits = 1 << 20;    // 128 KB of shared memory
 #ifndef KDB_FILTER_UNROLL
 #define KDB_FILTER_UNROLL 4
 #endif
+#ifndef KDB_FILTER_PREFETCH
+#define KDB_FILTER_PREFETCH 1
+#endif
 constexpr int kFilterThreads = KDB_FILTER_THREADS;  // threads per block
 constexpr int kFilterUnroll = KDB_FILTER_UNROLL;    // 16-B id chunks in flight per thread
 // rows per tile: threads x unroll, so a tile of ld-entry rows is exactly ld / VEC
@@ -202,17 +205,25 @@ __global__ void __launch_bounds__(kFilterThreads) k_filter(
       int32_t J[kFilterUnroll][VEC];
 #pragma unroll
       for (int t = 0; t < kFilterUnroll; ++t) {
-        const uint32_t u = base + t * blockDim.x + threadIdx.x;
+        // past the end (ragged last step only): reload the last chunk instead
+        // of predicating the load -- the consumer skips u >= n_chunks anyway
+        const uint32_t u = min(base + t * blockDim.x + threadIdx.x, n_chunks - 1);
         uint32_t off = u;  // chunk offset from the tile start
-        if (COLS && u < n_chunks) {
+        if (COLS) {
           const uint32_t lr = fd.small ? __umulhi(u, fd.m32) : (uint32_t)fdiv(u, fd);
           off = lr * (uint32_t)(ld / VEC) + (u - lr * cpr);
         }
+#if KDB_FILTER_PREFETCH
+        {  // the next step's chunk into L2 (its load then waits on L2, not HBM)
+          const uint32_t un = base + (t + KDB_FILTER_PREFETCH * kFilterUnroll) * blockDim.x + threadIdx.x;
+          if (!COLS && un < n_chunks) asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const int4*>(nt) + un));
+        }
+#endif
         if (VEC == 4) {
-          const int4 j4 = u < n_chunks ? __ldcs(reinterpret_cast<const int4*>(nt) + off) : make_int4(-1, -1, -1, -1);
+          const int4 j4 = __ldcs(reinterpret_cast<const int4*>(nt) + off);
           J[t][0] = j4.x; J[t][1] = j4.y; J[t][2] = j4.z; J[t][3] = j4.w;
         } else {
-          J[t][0] = u < n_chunks ? __ldcs(nt + off) : -1;
+          J[t][0] = __ldcs(nt + off);
         }
       }
 #pragma unroll
