@@ -357,6 +357,23 @@ def test_wide_rows_exact(k):
         assert_parity(run_gpu(nbr, dist, M, eps, exact=False), exp)
 
 
+@pytest.mark.parametrize("k", [1028, 1030])
+def test_very_wide_rows_filter_division(k):
+    """Rows of >= 1,024 entries: the filter's entry -> row division inside a
+    4,096-row tile leaves the 32-bit multiply-high path (exact only for
+    n * d < 2^32) for the 64-bit one; VEC 4 (k % 4 == 0) and VEC 1."""
+    rng = np.random.default_rng(k)
+    n = 2500
+    X = np.concatenate([rng.standard_normal((n // 2, 3)) * 0.05, rng.standard_normal((n - n // 2, 3)) * 0.05 + 1.0])
+    X = X.astype(np.float32)
+    nbr, dist = knn_bruteforce(X, k)
+    for M, f in ((k // 2, 1.5), (5, 1.0)):
+        eps = eps_from_graph(dist, M, f)
+        exp = oracle_run(nbr, dist, M, eps)
+        assert_parity(run_gpu(nbr, dist, M, eps, exact=True), exp)
+        assert_parity(run_gpu(nbr, dist, M, eps, exact=False), exp)
+
+
 @pytest.mark.parametrize("fuse,pack", [("0", "0"), ("1", "0"), ("1", "1")])
 @pytest.mark.parametrize("P", [0, 3])
 def test_round1_fused_into_ell(c1_graph, fuse, pack, P, monkeypatch):
