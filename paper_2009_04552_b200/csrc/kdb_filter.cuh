@@ -55,10 +55,12 @@ constexpr int kBloomBits = 1 << 20;    // 128 KB of shared memory
 #endif
 constexpr int kFilterThreads = KDB_FILTER_THREADS;  // threads per block
 constexpr int kFilterUnroll = KDB_FILTER_UNROLL;    // 16-B id chunks in flight per thread
-// rows per tile: threads x unroll, so a tile of ld-entry rows is exactly ld / VEC
-// sweep steps (no ragged last step with most warps idle at the tile barrier)
-constexpr int kFilterRows = kFilterThreads * kFilterUnroll;
-constexpr size_t kFilterSmem = kBloomBits / 8 + (size_t)kFilterRows * 16;  // Bloom words, then the tile's FRow
+// Each WARP sweeps its own tiles of 32 x unroll rows (a tile of ld-entry rows
+// is exactly ld / VEC sweep steps), staged in its own slice of shared memory:
+// no block barrier after the Bloom copy, warps never wait for each other.
+constexpr int kFilterRows = 32 * kFilterUnroll;  // rows per warp tile
+constexpr int kFilterWarps = kFilterThreads / 32;
+constexpr size_t kFilterSmem = kBloomBits / 8 + (size_t)kFilterWarps * kFilterRows * 16;  // Bloom words, then each warp's FRow tile
 
 // Blocked Bloom filter: key x selects ONE 32-bit word and sets 2-4 bits in it:
 // a single shared-memory probe per test.  One multiplicative hash h = x * phi
@@ -169,7 +171,8 @@ __global__ void __launch_bounds__(kFilterThreads) k_filter(
     int64_t row_begin, int64_t N, const int32_t* __restrict__ comp, const int2* __restrict__ rng, const uint32_t* __restrict__ bloom, FastDiv fd,
     HEdge* __restrict__ out, uint32_t cap, uint32_t* __restrict__ n_out, unsigned long long* __restrict__ n_slow) {
   extern __shared__ uint32_t s_bloom[];
-  FRow* s_row = reinterpret_cast<FRow*>(s_bloom + kBloomBits / 32);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  FRow* s_row = reinterpret_cast<FRow*>(s_bloom + kBloomBits / 32) + wid * kFilterRows;
   constexpr int R = kFilterRows;
   const uint32_t s_base = (uint32_t)__cvta_generic_to_shared(s_bloom);
   if (FAST) {
@@ -178,11 +181,12 @@ __global__ void __launch_bounds__(kFilterThreads) k_filter(
   const uint32_t Nu = (uint32_t)N;
   const int64_t n_tiles = (n_rows + R - 1) / R;
   uint32_t slow = 0;
-  for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+  __syncthreads();  // the Bloom copy is complete
+  for (int64_t tile = (int64_t)blockIdx.x * kFilterWarps + wid; tile < n_tiles; tile += (int64_t)gridDim.x * kFilterWarps) {
     const int64_t r0 = tile * R;
     const int nr = (int)((n_rows - r0) < R ? (n_rows - r0) : R);
-    __syncthreads();  // previous tile's readers are done with s_row (and the Bloom copy is complete)
-    for (int ti = threadIdx.x; ti < nr; ti += blockDim.x) {
+    __syncwarp();  // the warp's previous tile readers are done with its s_row slice
+    for (int ti = lane; ti < nr; ti += 32) {
       const int64_t i = r0 + ti;
       FRow fr;
       fr.cr = __ldg(comp + row_begin + i);
@@ -194,20 +198,20 @@ __global__ void __launch_bounds__(kFilterThreads) k_filter(
       }
       s_row[ti] = fr;
     }
-    __syncthreads();
+    __syncwarp();
     const int32_t* __restrict__ nt = nbr + r0 * ld;  // this tile's ids (contiguous)
     const float* __restrict__ dt = dist + r0 * ld;
     const uint32_t cpr = (uint32_t)((k + VEC - 1) / VEC);  // COLS: chunks per row
     const uint32_t n_chunks = COLS ? (uint32_t)nr * cpr : (uint32_t)(((int64_t)nr * ld) / VEC);
     // kFilterUnroll chunks per thread and step: their id loads are issued
     // together (the sweep is bound by load latency x loads in flight)
-    for (uint32_t base = 0; base < n_chunks; base += blockDim.x * kFilterUnroll) {
+    for (uint32_t base = 0; base < n_chunks; base += 32 * kFilterUnroll) {
       int32_t J[kFilterUnroll][VEC];
 #pragma unroll
       for (int t = 0; t < kFilterUnroll; ++t) {
         // past the end (ragged last step only): reload the last chunk instead
         // of predicating the load -- the consumer skips u >= n_chunks anyway
-        const uint32_t u = min(base + t * blockDim.x + threadIdx.x, n_chunks - 1);
+        const uint32_t u = min(base + t * 32 + lane, n_chunks - 1);
         uint32_t off = u;  // chunk offset from the tile start
         if (COLS) {
           const uint32_t lr = fd.small ? __umulhi(u, fd.m32) : (uint32_t)fdiv(u, fd);
@@ -215,7 +219,7 @@ __global__ void __launch_bounds__(kFilterThreads) k_filter(
         }
 #if KDB_FILTER_PREFETCH
         {  // the next step's chunk into L2 (its load then waits on L2, not HBM)
-          const uint32_t un = base + (t + KDB_FILTER_PREFETCH * kFilterUnroll) * blockDim.x + threadIdx.x;
+          const uint32_t un = base + (t + KDB_FILTER_PREFETCH * kFilterUnroll) * 32 + lane;
           if (!COLS && un < n_chunks) asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const int4*>(nt) + un));
         }
 #endif
@@ -228,7 +232,7 @@ __global__ void __launch_bounds__(kFilterThreads) k_filter(
       }
 #pragma unroll
       for (int t = 0; t < kFilterUnroll; ++t) {
-        const uint32_t u = base + t * blockDim.x + threadIdx.x;
+        const uint32_t u = base + t * 32 + lane;
         uint32_t survm = 0, lr = 0, col = 0, off = u;
         int32_t cj[VEC], cr = -1;
         float w[VEC];
@@ -288,7 +292,6 @@ __global__ void __launch_bounds__(kFilterThreads) k_filter(
         if (__any_sync(0xffffffffu, survm != 0)) {  // rare: warp-aggregated append
           const int cnt = __popc(survm);
           int incl = cnt;
-          const int lane = threadIdx.x & 31;
 #pragma unroll
           for (int o = 1; o < 32; o <<= 1) {
             const int x = __shfl_up_sync(0xffffffffu, incl, o);

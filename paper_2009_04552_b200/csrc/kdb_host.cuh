@@ -800,8 +800,8 @@ kdb_status filter_phase(Mst& m, float eps, bool* overflow) {
     fd.m32 = fd.d > 1 ? (uint32_t)((0xffffffffull / fd.d) + 1) : 0;
     // umulhi(n, m32) == n / d for n * d < 2^32; tile indices n < kFilterRows * d
     fd.small = (fd.d > 1 && fd.d * fd.d * (uint64_t)kFilterRows < (1ull << 32)) ? 1u : 0u;
-    const int64_t ntiles = (R.n_rows + kFilterRows - 1) / kFilterRows;
-    const int grid = (int)std::min<int64_t>(ntiles, 1 << 30);
+    const int64_t ntiles = (R.n_rows + kFilterRows - 1) / kFilterRows;  // warp tiles
+    const int grid = (int)std::min<int64_t>((ntiles + kFilterWarps - 1) / kFilterWarps, 1 << 30);
 #define KDB_FILTER_LAUNCH(V, F, CO)                                                                              \
   LAUNCH_DYN((k_filter<V, F, CO>), grid, kFilterThreads, kFilterSmem, st, R.nbr, R.dist, R.n_rows, m.ld, m.k,      \
              m.tau, eps, R.row_begin, m.N, m.comp, rng, L.bloom, fd, R.hs[0], R.hs_cap, R.n_hs_dev, L.fcount + 1)
