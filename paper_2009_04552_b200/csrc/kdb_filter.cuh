@@ -147,10 +147,10 @@ struct FastDiv {
 };
 __device__ __forceinline__ uint64_t fdiv(uint64_t q, const FastDiv& f) { return f.d == 1 ? q : __umul64hi(q, f.M); }
 
-// The filter: every rank streams its rows once, in tiles of kFilterRows
-// rows.  Per tile, thread i stages row i's data in shared memory (comp[v] and
-// the id range of comp[v]); then the tile's R*k ids are swept in flat order,
-// VEC per thread and step.  Fast path: J inside the id range of comp[v] and
+// The filter: every rank streams its rows once, each warp in its own tiles of
+// kFilterRows rows.  Per tile, the warp's lanes stage the rows' data in the
+// warp's slice of shared memory (comp[v] and the id range of comp[v]); then
+// the tile's R*k ids are swept in flat order, VEC per lane and chunk.  Fast path: J inside the id range of comp[v] and
 // not in the Bloom filter of the exceptions => comp[J] == comp[v]: the entry
 // is intra (or light, or beyond eps, or J == v -- none a candidate leaving
 // edge), decided from the id alone.  Otherwise the chunk's weights are loaded
