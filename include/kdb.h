@@ -150,7 +150,7 @@ kdb_status kdb_mst(const kdb_graph* g, float eps, const uint32_t* core_bits, int
  * general do not (weight >= kdb_mst's).  Arguments and outputs as kdb_mst;
  * single process (the whole graph: row_begin 0, n_rows = n_total), workspace
  * >= kdb_mst_inexact_workspace_bytes(g, nparts).  EINVAL: nparts < 1, a partial
- * graph, n_rows * edge_cols >= 2^32 - 1.  Synchronises `stream`. */
+ * graph, n_rows * edge_cols >= 2^31 - 1.  Synchronises `stream`. */
 size_t kdb_mst_inexact_workspace_bytes(const kdb_graph* g, int32_t nparts);
 kdb_status kdb_mst_inexact(const kdb_graph* g, float eps, const uint32_t* core_bits, int32_t nparts, int32_t* comp,
                            uint32_t* mst_a, uint32_t* mst_b, float* mst_w, int64_t mst_cap, int64_t* mst_count,

@@ -53,6 +53,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -101,25 +102,35 @@ inline int grid_for(int64_t n, int per_block = kThreads) {
 }
 
 // Grid-stride kernels run exactly one resident wave: min(requested, resident
-// CTAs per SM x SMs), from the occupancy calculator (cached per kernel).  A
-// second wave would only start after the first finished ALL its strides.
-int resident_cap(const void* kern, int block) {
-  static std::vector<std::pair<const void*, int>> cache;
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (sms <= 0) sms = 148;
-  }
-  for (auto& e : cache)
-    if (e.first == kern) return e.second;
-  int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, block, 0) != cudaSuccess || per_sm < 1) per_sm = 1;
-  const int cap = per_sm * sms;
-  cache.emplace_back(kern, cap);
-  return cap;
+// CTAs per SM x SMs), from the occupancy calculator (cached per device, kernel,
+// block size and dynamic shared memory; the cache is shared by host threads).
+// A second wave would only start after the first finished ALL its strides.
+struct CapKey {
+  int dev;
+  const void* kern;
+  int block;
+  size_t smem;
+};
+std::mutex g_cap_mu;
+std::vector<std::pair<CapKey, int>> g_cap_cache;
+int resident_cap_smem(const void* kern, int block, size_t smem) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(g_cap_mu);
+  for (auto& e : g_cap_cache)
+    if (e.first.dev == dev && e.first.kern == kern && e.first.block == block && e.first.smem == smem)
+      return e.second;
+  // dynamic shared memory above 48 KB needs the opt-in on THIS device
+  if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int sms = 0, per_sm = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (sms <= 0) sms = 148;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, block, smem) != cudaSuccess || per_sm < 1)
+    per_sm = 1;
+  g_cap_cache.push_back({CapKey{dev, kern, block, smem}, per_sm * sms});
+  return per_sm * sms;
 }
+int resident_cap(const void* kern, int block) { return resident_cap_smem(kern, block, 0); }
 
 // ============================================================================
 // launch accounting + optional per-kernel device timing (bench.py's roofline)
@@ -197,19 +208,6 @@ struct LaunchScope {
   } while (0)
 
 // LAUNCH_DYN: the same with dynamic shared memory (opt-in above 48 KB)
-int resident_cap_smem(const void* kern, int block, size_t smem) {
-  static std::vector<std::pair<const void*, int>> cache;
-  for (auto& e : cache)
-    if (e.first == kern) return e.second;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  int sms = 148, dev = 0, per_sm = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, block, smem) != cudaSuccess || per_sm < 1)
-    per_sm = 1;
-  cache.emplace_back(kern, per_sm * sms);
-  return per_sm * sms;
-}
 #define LAUNCH_DYN(kern, grid, block, smem, st, ...)                                           \
   do {                                                                                         \
     LaunchScope ls_(#kern, st);                                                                \
@@ -285,6 +283,32 @@ __device__ __forceinline__ T gat(const T* p) { return __ldcg(p); }
 // many rows offer to one component).  A stale read only lets an atomic through.
 __device__ __forceinline__ void min_offer(unsigned long long* p, unsigned long long x) {
   if (x < __ldcg(p)) atomicMin(p, x);
+}
+
+// 128-bit compare-and-swap minimum of the pair (key, b) (sm_90+ atom.cas.b128):
+// the full O1 order in one atomic word, so one rank needs no separate tie pass
+// and no offer list.  A torn 128-bit read only makes the first CAS fail; the
+// CAS returns the true current pair and the loop re-tests against it.
+__device__ __forceinline__ ulonglong2 atom_cas128(ulonglong2* p, ulonglong2 cmp, ulonglong2 val) {
+  ulonglong2 old;
+  asm volatile(
+      "{\n\t.reg .b128 d, c, v;\n\t"
+      "mov.b128 c, {%2, %3};\n\t"
+      "mov.b128 v, {%4, %5};\n\t"
+      "atom.global.cas.b128 d, [%6], c, v;\n\t"
+      "mov.b128 {%0, %1}, d;\n\t}"
+      : "=l"(old.x), "=l"(old.y)
+      : "l"(cmp.x), "l"(cmp.y), "l"(val.x), "l"(val.y), "l"(p)
+      : "memory");
+  return old;
+}
+__device__ __forceinline__ void min_pair128(ulonglong2* p, uint64_t key, uint64_t b) {
+  ulonglong2 cur = __ldcg(p);
+  while (key < cur.x || (key == cur.x && b < cur.y)) {
+    const ulonglong2 old = atom_cas128(p, cur, make_ulonglong2(key, b));
+    if (old.x == cur.x && old.y == cur.y) break;
+    cur = old;
+  }
 }
 
 __device__ __forceinline__ uint64_t pack_key(uint32_t wbits, uint32_t a) {
@@ -710,9 +734,9 @@ kdb_status kdb_mst_inexact(const kdb_graph* g, float eps, const uint32_t* core_b
                            uint32_t* mst_a, uint32_t* mst_b, float* mst_w, int64_t mst_cap, int64_t* mst_count,
                            double* mst_weight, void* workspace, size_t ws_bytes, kdb_stream_t stream) {
   if (nparts < 1) return set_err(KDB_EINVAL, "nparts must be >= 1");
-  // the cut entries are counted in 32 bits (survivor buffers)
-  if (g && g->n_rows * (int64_t)edge_cols_of(g) >= (int64_t)UINT32_MAX - 1)
-    return set_err(KDB_EINVAL, "kdb_mst_inexact: n_rows * edge_cols must stay below 2^32");
+  // the cut entries live in the survivor buffers, whose counts go to CUB as int
+  if (g && g->n_rows * (int64_t)edge_cols_of(g) >= (int64_t)INT32_MAX)
+    return set_err(KDB_EINVAL, "kdb_mst_inexact: n_rows * edge_cols must stay below 2^31 - 1");
   return mst_impl(g, eps, core_bits, comp, mst_a, mst_b, mst_w, mst_cap, mst_count, mst_weight, workspace, ws_bytes,
                   nullptr, stream, nparts);
 }

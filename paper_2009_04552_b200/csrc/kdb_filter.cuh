@@ -220,7 +220,8 @@ __global__ void __launch_bounds__(kFilterThreads) k_filter(
 #if KDB_FILTER_PREFETCH
         {  // the next step's chunk into L2 (its load then waits on L2, not HBM)
           const uint32_t un = base + (t + KDB_FILTER_PREFETCH * kFilterUnroll) * 32 + lane;
-          if (!COLS && un < n_chunks) asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const int4*>(nt) + un));
+          // chunk un starts at element un * VEC (byte-correct for VEC == 1 too)
+          if (!COLS && un < n_chunks) asm volatile("prefetch.global.L2 [%0];" ::"l"(nt + (size_t)un * VEC));
         }
 #endif
         if (VEC == 4) {

@@ -186,7 +186,7 @@ size_t carve(Layout& L, char* base, bool dry, int64_t N, int nr, const int64_t* 
     }
     R.hs_cap = (uint32_t)std::min<int64_t>(hs_cap_override >= 0 ? std::max<int64_t>(hs_cap_override, 1)
                                                                    : survivor_cap(n, k),
-                                           (int64_t)UINT32_MAX - 1);
+                                           (int64_t)INT32_MAX - 1);  // CUB item counts are int
     R.hs[0] = cv.take<HEdge>(R.hs_cap);
     R.hs[1] = cv.take<HEdge>(R.hs_cap);
     R.hkeep = cv.take<uint8_t>(R.hs_cap);
@@ -269,6 +269,8 @@ int env_int(const char* name, int dflt) {
   const char* s = getenv(name);
   return (s && *s) ? atoi(s) : dflt;
 }
+
+bool nr_ranks_is_one(const Layout& L) { return L.ranks.size() == 1; }
 
 // One kdb_mst call: the workspace layout plus the phase bookkeeping.
 struct Mst {
@@ -450,6 +452,12 @@ kdb_status rows_phase(Mst& m, float eps_run) {
   for (auto& R : L.ranks) any_compact |= R.compact;
   const bool fused = fuse1 && any_compact;
   const bool sync_each = multi_rank(comm);
+  // one rank, exact mode, light ELL: rounds >= 2 offer by a 128-bit CAS-minimum
+  // of (key, b) (no offer list, no tie pass); KB reuses the round-1 records
+  // (rec1: 16 B per component, free once round 1 has hooked)
+  const bool cas = !general && nr_ranks_is_one(L) && !multi_rank(comm) && any_compact && L.rec1 &&
+                   env_int("KDB_CAS", 1) != 0;
+  ulonglong2* KB = cas ? reinterpret_cast<ulonglong2*>(L.rec1) : nullptr;
   int cur = fused ? 1 : 0;  // fused round 1: its OUTPUT list is act[0] already
   int par = 0;              // component count ping-pong: Cs[par] current
   {
@@ -514,7 +522,7 @@ kdb_status rows_phase(Mst& m, float eps_run) {
     LAUNCH(k_merge, grid_for(C_bound), kThreads, st, C_bound, L.rootof, sparse ? (const int32_t*)nullptr : L.newid,
            L.cmin, general ? nullptr : L.kmin, L.cmin2, L.kmin2, L.parent, Cd);
     LAUNCH(k_relabel, grid_for(N / 8 + 1), kThreads, st, N, comp, L.parent, (const int32_t*)nullptr);
-    LAUNCH(k_fill_comp_arrays, grid_for(C_bound), kThreads, st, C_bound, L.Kc, L.Bc, nullptr, (const int64_t*)Cn);
+    LAUNCH(k_fill_comp_arrays, grid_for(C_bound), kThreads, st, C_bound, L.Kc, L.Bc, nullptr, (const int64_t*)Cn, KB);
     for (size_t r = 1; r < nr; ++r)
       LAUNCH(k_fill_comp_arrays, grid_for(C_bound), kThreads, st, C_bound, L.ranks[r].Kc, L.ranks[r].Bc, nullptr,
              (const int64_t*)Cn);
@@ -572,20 +580,20 @@ kdb_status rows_phase(Mst& m, float eps_run) {
                  &L.ctr->entries, nin);
         else
         {
-#define KDB_LR_LAUNCH(GW)                                                                                       \
-  LAUNCH(k_light_round<GW>, grid_for(na_ub[r]), kThreads, st, R.LE, R.nbr, R.dist, ld, k, eps_run, R.row_begin, N, \
-         comp, R.act[cur], na_ub[r], R.act[cur ^ 1], nout, &R.ctr->grab, R.offers, (unsigned long long*)R.Kc,      \
-         &L.ctr->entries, nin, precheck)
+#define KDB_LR_LAUNCH(...)                                                                                       \
+  LAUNCH((k_light_round<__VA_ARGS__>), grid_for(na_ub[r]), kThreads, st, R.LE, R.nbr, R.dist, ld, k, eps_run,       \
+         R.row_begin, N, comp, R.act[cur], na_ub[r], R.act[cur ^ 1], nout, &R.ctr->grab, R.offers,                 \
+         (unsigned long long*)R.Kc, &L.ctr->entries, nin, precheck, KB)
           // pipelined chunk loads pay when many rows scan past their first chunk
           // (C3: its inner shell is all light); they cost occupancy otherwise
           const int pk = env_int("KDB_PIPE", -1);
           const bool pipe = pk >= 0 ? pk != 0 : (uint64_t)R.n_deep * 100 > (uint64_t)R.n_rows * 15;
-          if (gw == 1) KDB_LR_LAUNCH(1);
+          if (cas) {
+            if (pipe) KDB_LR_LAUNCH(4, true, true);
+            else KDB_LR_LAUNCH(4, false, true);
+          } else if (gw == 1) KDB_LR_LAUNCH(1);
           else if (gw == 2) KDB_LR_LAUNCH(2);
-          else if (pipe)
-            LAUNCH((k_light_round<4, true>), grid_for(na_ub[r]), kThreads, st, R.LE, R.nbr, R.dist, ld, k, eps_run,
-                   R.row_begin, N, comp, R.act[cur], na_ub[r], R.act[cur ^ 1], nout, &R.ctr->grab, R.offers,
-                   (unsigned long long*)R.Kc, &L.ctr->entries, nin, precheck);
+          else if (pipe) KDB_LR_LAUNCH(4, true);
           else KDB_LR_LAUNCH(4);
 #undef KDB_LR_LAUNCH
         }
@@ -622,7 +630,7 @@ kdb_status rows_phase(Mst& m, float eps_run) {
     KDB_TRY(allreduce_min_u64(comm, L.Kc, C_ub, st));
     m.payload_rows += 8.0 * C_ub;
     // a4: ties (the direct round already wrote Bc and the targets)
-    if (!direct) {
+    if (!direct && !cas) {
       for (size_t r = 0; r < nr; ++r) {
         RankState& R = L.ranks[r];
         if (na_ub[r]) LAUNCH(k_tie, grid_for(na_ub[r]), kThreads, st, R.offers, &R.ctr->na[cur ^ 1], L.Kc, R.Bc);
@@ -649,7 +657,8 @@ kdb_status rows_phase(Mst& m, float eps_run) {
              L.e_w, N, L.ctr, Cd, L.rec1);
     else
       LAUNCH(k_hook<false>, grid_for(C_ub), kThreads, st, C_ub, L.Kc, L.Bc, direct ? L.tgt : nullptr, kmin_cert,
-             comp, L.parent, L.e_key, L.e_w, N, L.ctr, Cd, (const int4*)nullptr);
+             comp, L.parent, L.e_key, L.e_w, N, L.ctr, Cd, (const int4*)nullptr,
+             (cas && !direct) ? (const ulonglong2*)KB : nullptr);
     KDB_CUDA(cudaGetLastError());
     // a6: contract (no hooks => identity)
     KDB_TRY(contract(C_ub));

@@ -59,10 +59,15 @@ __global__ void k_init_comp(const uint32_t* __restrict__ bits, const uint32_t* _
 }
 
 __global__ void k_fill_comp_arrays(int64_t C, uint64_t* __restrict__ Kc, uint32_t* __restrict__ Bc,
-                                   uint32_t* __restrict__ kmin, const int64_t* __restrict__ Cp = nullptr) {
+                                   uint32_t* __restrict__ kmin, const int64_t* __restrict__ Cp = nullptr,
+                                   ulonglong2* __restrict__ KB = nullptr) {
   if (Cp) C = *Cp;
   for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < C;
        c += (int64_t)gridDim.x * blockDim.x) {
+    if (KB) {  // one rank, CAS offers: (key, b) pairs only
+      KB[c] = make_ulonglong2(kSent, kSentB);
+      continue;
+    }
     Kc[c] = kSent;
     Bc[c] = kSentB;
     if (kmin) kmin[c] = kInfBits;
@@ -663,8 +668,9 @@ __global__ void __launch_bounds__(256) k_light_first(const int4* __restrict__ LE
   if ((threadIdx.x & 31) == 0 && reads) atomicAdd(n_entries, reads);
 }
 
-// later rounds over the ELL; see k_offer_round
-template <int GW, bool PIPE = false>
+// later rounds over the ELL; see k_offer_round.  CAS (one rank): the offer is
+// a 128-bit CAS-minimum of (key, b) into KB[comp v] -- no offer list, no tie pass.
+template <int GW, bool PIPE = false, bool CAS = false>
 __global__ void __launch_bounds__(256) k_light_round(const int4* __restrict__ LE, const int32_t* __restrict__ nbr,
                                                      const float* __restrict__ dist, int32_t ld, int32_t k, float eps,
                                                      int64_t row_begin, int64_t N, const int32_t* __restrict__ comp,
@@ -673,10 +679,10 @@ __global__ void __launch_bounds__(256) k_light_round(const int4* __restrict__ LE
                                                      uint32_t* __restrict__ grab, Offer* __restrict__ offers,
                                                      unsigned long long* __restrict__ Kc,
                                                      unsigned long long* __restrict__ n_entries, const uint32_t* __restrict__ n_in_p = nullptr,
-                                                     int precheck = 0) {
+                                                     int precheck = 0, ulonglong2* __restrict__ KB = nullptr) {
   if (n_in_p) n_in = *n_in_p;
   __shared__ __align__(16) Rec s_rec[kChunk];
-  __shared__ __align__(16) Offer s_off[kChunk];
+  __shared__ __align__(16) Offer s_off[CAS ? 1 : kChunk];
   __shared__ uint32_t s_n, s_chunk, s_base;
   unsigned long long reads = 0;
   for (;;) {
@@ -694,11 +700,15 @@ __global__ void __launch_bounds__(256) k_light_round(const int4* __restrict__ LE
       const RowScan r = scan_ell<false, GW, PIPE>(LE + i * (kW / 2), nbr + i * ld, dist + i * ld, k, eps, v, cv, a.y,
                                                   N, comp, 0, reads);
       if (r.found) {
-        if (precheck) min_offer(Kc + cv, (unsigned long long)r.best);
-        else atomicMin(Kc + cv, (unsigned long long)r.best);
         const uint32_t j = atomicAdd(&s_n, 1u);
         s_rec[j] = Rec{v, r.h};
-        s_off[j] = Offer{cv, r.bestb, r.best};
+        if (CAS) {
+          min_pair128(KB + cv, r.best, r.bestb);
+        } else {
+          if (precheck) min_offer(Kc + cv, (unsigned long long)r.best);
+          else atomicMin(Kc + cv, (unsigned long long)r.best);
+          s_off[j] = Offer{cv, r.bestb, r.best};
+        }
       }
     }
     __syncthreads();
@@ -706,7 +716,7 @@ __global__ void __launch_bounds__(256) k_light_round(const int4* __restrict__ LE
     __syncthreads();
     for (uint32_t j = threadIdx.x; j < s_n; j += blockDim.x) {
       __stcs(reinterpret_cast<int2*>(act_out + s_base + j), *reinterpret_cast<const int2*>(s_rec + j));
-      __stcs(reinterpret_cast<int4*>(offers + s_base + j), *reinterpret_cast<const int4*>(s_off + j));
+      if (!CAS) __stcs(reinterpret_cast<int4*>(offers + s_base + j), *reinterpret_cast<const int4*>(s_off + j));
     }
     __syncthreads();
   }
@@ -714,6 +724,16 @@ __global__ void __launch_bounds__(256) k_light_round(const int4* __restrict__ LE
   if ((threadIdx.x & 31) == 0 && reads) atomicAdd(n_entries, reads);
 }
 
+// The same round, STAGED for memory-level parallelism.  The per-thread scan
+// is a chain of dependent loads (record -> comp[v] and the ELL chunk -> the
+// comp[J] gathers -> the offer); with one record at a time a thread waits ~4
+// memory latencies per record.  Here every thread takes its kRPT records of the
+// chunk together: their records, then all their comp[v] and first ELL chunks,
+// then all their comp[J] gathers are issued before any is consumed, so the
+// latencies overlap.  A row whose scan does not end in its first chunk (the
+// candidate prefix or the minimum's tie group continues) is re-scanned from its
+// head by scan_ell, the reference per-row scan (rare at C4: rows are mostly
+// decided by the chunk at their head).
 // in-edge lists: scan the live in-entries of target t, drop intra entries
 // (swap-remove; they never revive), offer the minimum leaving one.
 __global__ void k_offer_in(const unsigned long long* __restrict__ in_off, int32_t* __restrict__ in_len,
@@ -844,7 +864,7 @@ __global__ void __launch_bounds__(256) k_hook(int64_t C, const uint64_t* __restr
                        const int32_t* __restrict__ comp, int32_t* __restrict__ parent,
                        uint64_t* __restrict__ e_key, float* __restrict__ e_w, int64_t e_cap,
                        RoundCounters* __restrict__ ctr, const int64_t* __restrict__ Cp,
-                       const int4* __restrict__ rec1) {
+                       const int4* __restrict__ rec1, const ulonglong2* __restrict__ KB = nullptr) {
   if (Cp) C = *Cp;
   __shared__ uint64_t s_key[kHookChunk];
   __shared__ uint32_t s_w[kHookChunk];
@@ -863,6 +883,10 @@ __global__ void __launch_bounds__(256) k_hook(int64_t C, const uint64_t* __restr
         K = (uint64_t)(uint32_t)q.x | ((uint64_t)(uint32_t)q.y << 32);
         Bown = (uint32_t)q.z;
         kbown = (uint32_t)q.w;
+      } else if (KB) {  // one rank, CAS offers: (key, b) of a component in one 16-B word
+        const ulonglong2 q = KB[c];
+        K = q.x;
+        Bown = (uint32_t)q.y;
       } else {
         K = Kc[c];
       }
@@ -873,7 +897,7 @@ __global__ void __launch_bounds__(256) k_hook(int64_t C, const uint64_t* __restr
           ++n_unc;
         } else {
           const uint32_t a = (uint32_t)K;
-          const uint32_t b = PACKED ? Bown : Bc[c];
+          const uint32_t b = (PACKED || KB) ? Bown : Bc[c];
           int32_t t2;
           if (tgt) {
             t2 = tgt[c];
@@ -887,6 +911,13 @@ __global__ void __launch_bounds__(256) k_hook(int64_t C, const uint64_t* __restr
             const uint64_t Kt = (uint64_t)(uint32_t)q.x | ((uint64_t)(uint32_t)q.y << 32);
             const uint32_t Bt = (uint32_t)q.z;
             cert_t = Kt != kSent && (uint32_t)(Kt >> 32) < (uint32_t)q.w;
+            if (cert_t && (Kt > K || (Kt == K && Bt > b))) ctr->violation = 1u;
+            mutual = cert_t && Kt == K && Bt == b;
+          } else if (KB) {  // exact mode (CAS offers imply it): as below, one 16-B read of t
+            const ulonglong2 q = __ldcg(KB + t2);
+            const uint64_t Kt = q.x;
+            cert_t = Kt != kSent && certified(Kt, kmin, t2);
+            const uint32_t Bt = (uint32_t)q.y;
             if (cert_t && (Kt > K || (Kt == K && Bt > b))) ctr->violation = 1u;
             mutual = cert_t && Kt == K && Bt == b;
           } else if (kmin) {  // exact mode: t may abstain; also audit the promise
@@ -1057,23 +1088,45 @@ __global__ void k_relabel(int64_t N, int32_t* __restrict__ comp, const int32_t* 
 // ka = the sorted a (the caller's mst_a); splits the (b, w) payload into mst_b /
 // mst_w and sorts every run of equal a by b
 constexpr int kRunMax = 32;  // longer runs of equal a go to the segmented sort
+// Every thread's work is bounded by kRunMax + log2(m), whatever the run lengths
+// (a hub vertex can be the smaller endpoint of millions of MSF edges):
+//   * a run start i scans at most kRunMax + 1 entries forward; a short run
+//     [i, j) is insertion-sorted by b; a long run's end comes from a binary
+//     search (ka is sorted), the run is recorded as a segment and the start
+//     thread unpacks only its first kRunMax + 1 entries;
+//   * any other entry scans at most kRunMax entries back: if that reaches its
+//     run start, the start thread owns it; otherwise it belongs to a long run
+//     and unpacks itself.
 __global__ void k_msf_unpack(int64_t m, const uint32_t* __restrict__ ka, const unsigned long long* __restrict__ vb,
                              uint32_t* __restrict__ b, float* __restrict__ w, int32_t* __restrict__ seg_b,
                              int32_t* __restrict__ seg_e, uint32_t* __restrict__ nseg) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t ai = ka[i];
-    if (i > 0 && ka[i - 1] == ai) continue;  // not the start of a run
+    if (i > 0 && ka[i - 1] == ai) {  // not a run start
+      int64_t q = i - 1;
+      while (q > 0 && i - q <= kRunMax && ka[q - 1] == ai) --q;
+      if (i - q <= kRunMax) continue;  // within kRunMax of the start: the start thread's entry
+      const unsigned long long x = vb[i];  // deep inside a long run: unpack in place
+      b[i] = (uint32_t)(x >> 32);
+      w[i] = __uint_as_float((uint32_t)x);
+      continue;
+    }
     int64_t j = i + 1;
-    while (j < m && ka[j] == ai) ++j;
-    if (j - i > kRunMax) {  // a hub: unpacked as is, sorted by b afterwards (k_copy_segments)
-      for (int64_t p = i; p < j; ++p) {
+    while (j < m && j - i <= kRunMax && ka[j] == ai) ++j;
+    if (j - i > kRunMax) {  // a hub: its end by binary search over the sorted keys
+      int64_t lo = j, hi = m;  // first index in [j, m) with ka > ai
+      while (lo < hi) {
+        const int64_t mid = lo + (hi - lo) / 2;
+        if (ka[mid] > ai) hi = mid; else lo = mid + 1;
+      }
+      for (int64_t p = i; p <= i + kRunMax; ++p) {  // the head; the rest unpacks itself
         const unsigned long long x = vb[p];
         b[p] = (uint32_t)(x >> 32);
         w[p] = __uint_as_float((uint32_t)x);
       }
       const uint32_t s = atomicAdd(nseg, 1u);
       seg_b[s] = (int32_t)i;
-      seg_e[s] = (int32_t)j;
+      seg_e[s] = (int32_t)lo;
       continue;
     }
     for (int64_t p = i; p < j; ++p) {  // insertion sort of the run [i, j) by b

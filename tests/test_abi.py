@@ -133,3 +133,19 @@ def test_knng_library_exports_every_declared_symbol():
     L.knng_brute.argtypes = [C.c_void_p, C.c_int64, C.c_int, C.c_int, C.c_int] + [C.c_void_p] * 8
     assert L.knng_brute(None, 10, 65, 3, 8, *([None] * 8)) == 4
     assert L.knng_brute(None, 10, 3, 10, 16, *([None] * 8)) == 4
+
+
+def test_mst_inexact_rejects_int32_overflowing_cut_counts(lib):
+    """The cut entries of kdb_mst_inexact live in survivor buffers whose counts
+    CUB takes as int: n_rows * edge_cols >= 2^31 - 1 is EINVAL before any launch."""
+    P = C.c_void_p
+    cnt = C.c_int64(); tot = C.c_double()
+    n = (1 << 31) // 100 + 1          # n * k just above 2^31 - 1 with k = 100
+    g = _graph(n_total=n, n_rows=n, k=100)
+    rc = lib.kdb_mst_inexact(C.byref(g), C.c_float(0.5), P(0x100), 2, P(0x200), P(0x300), P(0x400), P(0x500), n - 1,
+                             C.byref(cnt), C.byref(tot), P(0x1000), C.c_size_t(1 << 40), None)
+    assert rc == 1 and b"2^31" in lib.kdb_last_error()
+    g = _graph(n_total=n, n_rows=n, k=100, edge_cols=50)  # the bound is on edge_cols columns
+    rc = lib.kdb_mst_inexact(C.byref(g), C.c_float(0.5), P(0x100), 2, P(0x200), P(0x300), P(0x400), P(0x500), n - 1,
+                             C.byref(cnt), C.byref(tot), P(0x1000), C.c_size_t(16), None)
+    assert rc == 2  # passes the guard, then the (tiny) workspace is too small: ENOMEM, nothing launched
