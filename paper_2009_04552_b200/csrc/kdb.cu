@@ -89,6 +89,24 @@ kdb_status set_err(kdb_status s, const char* fmt, ...) {
     if (s_ != KDB_OK) return s_;      \
   } while (0)
 
+#ifndef KDB_GUARDS
+#define KDB_GUARDS 0
+#endif
+constexpr size_t kGuardBytes = KDB_GUARDS ? 256 : 0;
+constexpr unsigned char kGuardByte = 0xA5;
+// debug build: device-side bounds checks record a bit here instead of trapping
+__device__ unsigned int g_dbg_viol = 0;
+#if KDB_GUARDS
+#define KDB_DCHECK(cond, bit) \
+  do {                        \
+    if (!(cond)) atomicOr(&g_dbg_viol, (bit)); \
+  } while (0)
+#else
+#define KDB_DCHECK(cond, bit) \
+  do {                        \
+  } while (0)
+#endif
+
 constexpr uint64_t kSent = ~0ull;      // sentinel key (reading #11)
 constexpr uint32_t kSentB = ~0u;
 constexpr uint32_t kInfBits = 0x7f800000u;
@@ -567,6 +585,7 @@ kdb_status mst_impl(const kdb_graph* g, float eps, const uint32_t* core_bits, in
   const size_t need = carve(L, (char*)workspace, false, N, (int)rb.size(), rb.data(), rn.data(), m.general, m.k,
                             inexact ? g->n_rows * (int64_t)m.k : -1);
   if (ws_bytes < need) return set_err(KDB_ENOMEM, "workspace %zu < required %zu bytes", ws_bytes, need);
+  KDB_TRY(guards_fill((char*)workspace, L.guards, (cudaStream_t)stream));
   *mst_count = 0;
   *mst_weight = 0.0;
   for (auto& s : g_stats) s = 0;
@@ -687,6 +706,7 @@ kdb_status mst_impl(const kdb_graph* g, float eps, const uint32_t* core_bits, in
   KDB_CUDA(cudaStreamSynchronize(st));
   const double t_fin = elapsed(m.ev[0], m.ev[1]);
   if (g_prof.on) g_prof.drain();
+  KDB_TRY(guards_check((const char*)workspace, L.guards, st, "kdb_mst"));
   *mst_count = ne;
   *mst_weight = ne > 0 ? exact_bucket_sum(bk) : 0.0;
   g_stats[0] = m.rounds;
@@ -800,8 +820,9 @@ struct NmiWs {
   void* tmp;
   size_t tmp_bytes;
 };
-size_t nmi_carve(NmiWs& w, char* base, bool dry, int64_t n) {
+size_t nmi_carve(NmiWs& w, char* base, bool dry, int64_t n, std::vector<size_t>* guards = nullptr) {
   Carver cv{base, 0, 0, dry};
+  cv.guards = guards;
   const int64_t m = std::max<int64_t>(n, 1);
   w.k0 = cv.take<uint64_t>(m);
   w.k1 = cv.take<uint64_t>(m);
@@ -867,12 +888,14 @@ kdb_status kdb_nmi(const int32_t* a, const int32_t* b, int64_t n, double* nmi, i
   if (n > 0 && (!a || !b || !workspace)) return set_err(KDB_EINVAL, "NULL device pointer");
   if ((uintptr_t)workspace & 255u) return set_err(KDB_EINVAL, "workspace must be 256-byte aligned");
   NmiWs w;
-  const size_t need = nmi_carve(w, (char*)workspace, false, n);
+  std::vector<size_t> guards;
+  const size_t need = nmi_carve(w, (char*)workspace, false, n, &guards);
   if (n > 0 && ws_bytes < need) return set_err(KDB_ENOMEM, "workspace %zu < required %zu bytes", ws_bytes, need);
   *nmi = 1.0;
   *clusters_a = *clusters_b = 0;
   if (n == 0) return KDB_OK;
   cudaStream_t st = (cudaStream_t)stream;
+  KDB_TRY(guards_fill((char*)workspace, guards, st));
   const int ni = (int)n;
   size_t tb = w.tmp_bytes;
   {
@@ -925,6 +948,7 @@ kdb_status kdb_nmi(const int32_t* a, const int32_t* b, int64_t n, double* nmi, i
     KDB_CUDA(cudaMemcpyAsync(&S[pass], w.sum + pass, sizeof(double), cudaMemcpyDeviceToHost, st));
     KDB_CUDA(cudaStreamSynchronize(st));
   }
+  KDB_TRY(guards_check((const char*)workspace, guards, st, "kdb_nmi"));
   const double N = (double)n, lnN = log(N);
   const double Ha = lnN - S[1] / N, Hb = lnN - S[2] / N;
   const double I = (S[0] + N * lnN - S[1] - S[2]) / N;

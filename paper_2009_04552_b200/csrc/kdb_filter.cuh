@@ -439,6 +439,7 @@ __global__ void k_hook_h(int64_t C, const uint64_t* __restrict__ Kc, const uint3
         wb = (uint32_t)(K >> 32);
         const int32_t ca = gat(hcomp + gat(compL + a));
         const int32_t t = ca == (int32_t)c ? gat(hcomp + gat(compL + b)) : ca;
+        KDB_DCHECK(t >= 0 && t < C, 16u);
         const bool mutual = gat(Kc + t) == K && gat(Bc + t) == b;
         if (!(mutual && c < t)) {
           p = t;

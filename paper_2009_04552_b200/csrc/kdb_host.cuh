@@ -44,18 +44,53 @@ inline int64_t survivor_cap(int64_t n_rows, int64_t k) {
   return std::max<int64_t>(n_rows / 4, std::min<int64_t>(n_rows * k / 4, (int64_t)1 << 24)) + 65536;
 }
 
+// Workspace carving.  The debug build (-DKDB_GUARDS=1, lib/libkdb_dbg.so)
+// puts a 256-B guard band after every array; kdb_mst / kdb_nmi fill the bands
+// with a pattern before their first launch and verify them after the last
+// (KDB_EINTERNAL on an overrun) -- the memcheck this pool's GPUs cannot run.
 struct Carver {
   char* base;
   size_t off = 0, cap;
   bool dry;
+  std::vector<size_t>* guards = nullptr;
   template <typename T>
   T* take(size_t n) {
     off = (off + 255) & ~size_t(255);
     T* p = dry ? nullptr : reinterpret_cast<T*>(base + off);
     off += n * sizeof(T);
+    if (kGuardBytes) {
+      off = (off + 255) & ~size_t(255);
+      if (guards) guards->push_back(off);
+      off += kGuardBytes;
+    }
     return p;
   }
 };
+
+kdb_status guards_fill(char* base, const std::vector<size_t>& g, cudaStream_t st) {
+  for (size_t o : g) KDB_CUDA(cudaMemsetAsync(base + o, kGuardByte, kGuardBytes, st));
+  if (!g.empty()) {
+    const unsigned int z = 0;
+    KDB_CUDA(cudaMemcpyToSymbolAsync(g_dbg_viol, &z, sizeof(z), 0, cudaMemcpyHostToDevice, st));
+  }
+  return KDB_OK;
+}
+
+kdb_status guards_check(const char* base, const std::vector<size_t>& g, cudaStream_t st, const char* what) {
+  if (g.empty()) return KDB_OK;
+  std::vector<unsigned char> h(kGuardBytes);
+  for (size_t i = 0; i < g.size(); ++i) {
+    KDB_CUDA(cudaMemcpyAsync(h.data(), base + g[i], kGuardBytes, cudaMemcpyDeviceToHost, st));
+    KDB_CUDA(cudaStreamSynchronize(st));
+    for (unsigned char c : h)
+      if (c != kGuardByte) return set_err(KDB_EINTERNAL, "%s: workspace guard band %zu overwritten", what, i);
+  }
+  unsigned int viol = 0;
+  KDB_CUDA(cudaMemcpyFromSymbolAsync(&viol, g_dbg_viol, sizeof(viol), 0, cudaMemcpyDeviceToHost, st));
+  KDB_CUDA(cudaStreamSynchronize(st));
+  if (viol) return set_err(KDB_EINTERNAL, "%s: device bounds check failed (mask 0x%x)", what, viol);
+  return KDB_OK;
+}
 
 struct RankState {
   int64_t row_begin = 0, n_rows = 0;
@@ -111,6 +146,7 @@ struct Layout {
   void* cub_tmp;
   size_t cub_bytes;
   std::vector<RankState> ranks;
+  std::vector<size_t> guards;  // debug build: guard band offsets
 };
 
 size_t cub_tmp_bytes(int64_t N, int64_t cap_edges) {
@@ -138,6 +174,8 @@ size_t cub_tmp_bytes(int64_t N, int64_t cap_edges) {
 size_t carve(Layout& L, char* base, bool dry, int64_t N, int nr, const int64_t* rb, const int64_t* rn,
              bool general, int32_t k, int64_t hs_cap_override = -1) {
   Carver cv{base, 0, 0, dry};
+  L.guards.clear();
+  cv.guards = &L.guards;
   const int64_t nwords = (N + 31) / 32;
   L.woff = cv.take<uint32_t>(nwords + 1);
   L.cmin = cv.take<int32_t>(N + 1);

@@ -696,6 +696,7 @@ __global__ void __launch_bounds__(256) k_light_round(const int4* __restrict__ LE
       const int2 a = __ldcs(reinterpret_cast<const int2*>(act + s));
       const int32_t v = a.x;
       const int32_t cv = gat(comp + v);
+      KDB_DCHECK(cv >= 0 && v >= row_begin && v < N, 8u);  // a live row is a local core vertex
       const int64_t i = (int64_t)v - row_begin;
       const RowScan r = scan_ell<false, GW, PIPE>(LE + i * (kW / 2), nbr + i * ld, dist + i * ld, k, eps, v, cv, a.y,
                                                   N, comp, 0, reads);
@@ -870,6 +871,10 @@ __global__ void __launch_bounds__(256) k_hook(int64_t C, const uint64_t* __restr
   __shared__ uint32_t s_w[kHookChunk];
   __shared__ uint32_t s_n, s_base;
   uint32_t n_off = 0, n_unc = 0, n_hook = 0;
+#ifdef KDB_INJECT_OVERRUN
+  // guard self-test build only (tools/guard_selftest.sh): one write past e_key
+  if (blockIdx.x == 0 && threadIdx.x == 0) e_key[e_cap + 32] = 0ull;  // e_key holds e_cap + 1: this is in the guard
+#endif
   for (int64_t chunk = blockIdx.x; chunk * kHookChunk < C; chunk += gridDim.x) {
     if (threadIdx.x == 0) s_n = 0;
     __syncthreads();
@@ -905,6 +910,7 @@ __global__ void __launch_bounds__(256) k_hook(int64_t C, const uint64_t* __restr
             const int32_t x = (gat(comp + a) == (int32_t)c) ? (int32_t)b : (int32_t)a;
             t2 = gat(comp + x);
           }
+          KDB_DCHECK(t2 >= 0 && t2 < C, 1u);
           bool mutual, cert_t = true;
           if (PACKED) {  // one random 16-B read of the target's record
             const int4 q = __ldcg(rec1 + t2);
@@ -996,6 +1002,7 @@ __global__ void k_jump(int64_t C, int32_t* parent, int32_t* __restrict__ rootof,
         break;
       }
     }
+    KDB_DCHECK(x >= 0 && x < C, 4u);
     rootof[c] = x;
   }
 }
@@ -1024,7 +1031,9 @@ __global__ void k_merge(int64_t C, const int32_t* __restrict__ rootof, const int
   if (Cp) C = *Cp;
   for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < C;
        c += (int64_t)gridDim.x * blockDim.x) {
+    KDB_DCHECK(rootof[c] >= 0 && rootof[c] < C, 2u);
     const int32_t r = newid ? gat(newid + rootof[c]) : rootof[c];  // sparse ids: the root itself
+    KDB_DCHECK(r >= 0 && r < C, 2u);
     map[c] = r;
     atomicMin(cmin2 + r, cmin[c]);
     if (kmin) {

@@ -149,3 +149,17 @@ def test_mst_inexact_rejects_int32_overflowing_cut_counts(lib):
     rc = lib.kdb_mst_inexact(C.byref(g), C.c_float(0.5), P(0x100), 2, P(0x200), P(0x300), P(0x400), P(0x500), n - 1,
                              C.byref(cnt), C.byref(tot), P(0x1000), C.c_size_t(16), None)
     assert rc == 2  # passes the guard, then the (tiny) workspace is too small: ENOMEM, nothing launched
+
+
+def test_debug_build_exports_and_guards(lib):
+    """lib/libkdb_dbg.so (guard bands + device bounds checks, tests/test_gpu_debug.py)
+    exports the same C-ABI and asks for more workspace (its guard bands)."""
+    import paper_2009_04552_b200 as kdb
+    dbg = os.path.join(os.path.dirname(kdb.LIB_PATH), "libkdb_dbg.so")
+    if not os.path.exists(dbg):
+        subprocess.check_call(["make", "-C", ROOT, os.path.relpath(dbg, ROOT)])
+    D = C.CDLL(dbg)
+    assert all(hasattr(D, f) for f in declared_functions())
+    D.kdb_mst_workspace_bytes.restype = C.c_size_t
+    g = _graph(n_total=1000, n_rows=1000, k=32, flags=1)
+    assert D.kdb_mst_workspace_bytes(C.byref(g), None) > lib.kdb_mst_workspace_bytes(C.byref(g), None)
