@@ -143,7 +143,7 @@ def make_workload(cfg_name: str, scale: float, seed: int, device):
     """Points (numpy, seeded), exact kNN graph on the GPU, eps from the config rule."""
     import torch
     from datagen import CONFIGS, gen_config_points
-    from datagen.knng_gpu import build_knng_brute, build_knng_grid
+    from paper_2009_04552_b200.knng import build_knng_brute, build_knng_grid
     cfg = CONFIGS[cfg_name]
     t0 = time.time()
     X, truth = gen_config_points(cfg_name, seed, scale)

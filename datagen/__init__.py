@@ -3,9 +3,13 @@
 This package is shared by BOTH sides of the parity check (the CPU oracle in
 ``oracle/`` and the CUDA product path in ``paper_2009_04552_b200/``).  It holds
 none of the method's arithmetic: it only produces inputs -- point sets, the
-k-NN graph those points induce (the paper's input, "the directed
-k-nearest neighbor graph G_k"), random graphs with adversarial structure, and
-the epsilon rule of the configs.  It never imports either side.
+CPU brute-force k-NN graph of small point sets (the paper's input, PAPER.md:517
+"the directed k-nearest neighbor graph G_k"), random graphs with adversarial
+structure, and the epsilon rule of the configs.  It never imports either side.
+Large graphs come from the package's kNN-graph builder (a separate, separately
+timed input stage, paper_2009_04552_b200/knng.py; it
+shares no code with the clustering kernels), which the callers (bench.py,
+tests/) import directly.
 
 Recipes follow BASELINE.json ``configs`` and SURVEY.md §8(d).
 """

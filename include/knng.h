@@ -51,6 +51,15 @@ int knng_ladder(const float* X, int64_t n, int D, const int32_t* samples, int S,
 int knng_grid(const float* X, int64_t n, int D, int k, double h, const double* lo, double span_cells, double diag,
               int32_t* nbr, float* dist, void* ws, size_t ws_bytes, cudaStream_t st, int64_t* n_fallback);
 
+/* The same for the query rows [q_begin, q_begin + q_count) only (one rank's
+ * contiguous rows of a distributed graph): the grid is built over
+ * all n points (every point is a candidate), nbr/dist are [q_count][k] with
+ * row r holding query q_begin + r.  Cells holding no such query are skipped.
+ * 4 also for a range outside [0, n).  knng_grid == knng_grid_rows(0, n). */
+int knng_grid_rows(const float* X, int64_t n, int D, int k, double h, const double* lo, double span_cells,
+                   double diag, int64_t q_begin, int64_t q_count, int32_t* nbr, float* dist, void* ws,
+                   size_t ws_bytes, cudaStream_t st, int64_t* n_fallback);
+
 /* Certified brute force: per query an fp32 heap of the Kp nearest candidates
  * (k <= Kp <= 256; hs float[n*Kp], hi int32[n*Kp], hcount int32[n] scratch),
  * then an fp64 re-rank into nbr/dist [n][k].  A row whose k-th fp64 distance is

@@ -160,7 +160,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_cells(const float* __restrict__
                                                        const int64_t* __restrict__ ustart, int64_t ncell, int64_t n,
                                                        int bits, double hq, int k, int32_t* __restrict__ nbr,
                                                        float* __restrict__ dist, int32_t* __restrict__ fb,
-                                                       unsigned int* __restrict__ nfb) {
+                                                       unsigned int* __restrict__ nfb, int64_t qb, int64_t qe) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double (*wd)[kWarpBuf] = reinterpret_cast<double (*)[kWarpBuf]>(smem_raw);
   int (*wi)[kWarpBuf] = reinterpret_cast<int (*)[kWarpBuf]>(smem_raw + sizeof(double) * kWarps * kWarpBuf);
@@ -174,6 +174,12 @@ __global__ void __launch_bounds__(kWarps * 32) k_cells(const float* __restrict__
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int64_t c = blockIdx.x; c < ncell; c += gridDim.x) {
     const unsigned long long key = ukey[c];
+    {
+      // query rows [qb, qe) only: ids inside a cell are ascending (stable key
+      // sort of 0..n-1), so a cell without such a query is skipped whole
+      const int64_t b0 = ustart[c], e0 = (c + 1 < ncell ? ustart[c + 1] : n);
+      if (sid[b0] >= qe || sid[e0 - 1] < qb) continue;  // block-uniform
+    }
     if (threadIdx.x == 0) nnb = 0;
     __syncthreads();
     for (int o = threadIdx.x; o < NB; o += blockDim.x) {
@@ -212,8 +218,9 @@ __global__ void __launch_bounds__(kWarps * 32) k_cells(const float* __restrict__
     __syncthreads();
     for (int64_t q0 = qbeg; q0 < qend; q0 += kWarps) {
       const int64_t q = q0 + warp;
-      const bool active = q < qend;
-      const int32_t qi = active ? sid[q] : -1;
+      const int32_t q_id = q < qend ? sid[q] : -1;
+      const bool active = q < qend && q_id >= qb && q_id < qe;
+      const int32_t qi = active ? q_id : -1;
       float qx[D];
       for (int u = 0; u < D; ++u) qx[u] = active ? X[(int64_t)qi * D + u] : 0.f;
       int cnt = 0;
@@ -255,8 +262,8 @@ __global__ void __launch_bounds__(kWarps * 32) k_cells(const float* __restrict__
       __syncwarp();
       warp_bitonic(wd[warp], wi[warp], n2);
       for (int t = lane; t < k; t += 32) {
-        nbr[(int64_t)qi * k + t] = wi[warp][t];
-        dist[(int64_t)qi * k + t] = (float)wd[warp][t];
+        nbr[((int64_t)qi - qb) * k + t] = wi[warp][t];
+        dist[((int64_t)qi - qb) * k + t] = (float)wd[warp][t];
       }
       __syncwarp();
     }
@@ -277,7 +284,7 @@ __global__ void __launch_bounds__(256) k_fallback(const float* __restrict__ X, c
                                                   double hq, double lo0, double lo1, double lo2, double lo3, double lo4,
                                                   double inv_h, int k, const int32_t* __restrict__ fb, unsigned nfb,
                                                   int32_t* __restrict__ nbr, float* __restrict__ dist,
-                                                  int* __restrict__ fail, int max_ring, double diag) {
+                                                  int* __restrict__ fail, int max_ring, double diag, int64_t qb) {
   extern __shared__ __align__(16) unsigned char smem[];
   double* sd = reinterpret_cast<double*>(smem);
   int* si = reinterpret_cast<int*>(sd + kFbCap);
@@ -355,8 +362,8 @@ __global__ void __launch_bounds__(256) k_fallback(const float* __restrict__ X, c
       __syncthreads();
       block_bitonic(sd, si, n2);
       for (int t = threadIdx.x; t < k; t += blockDim.x) {
-        nbr[(int64_t)qi * k + t] = t < c ? si[t] : -1;
-        dist[(int64_t)qi * k + t] = t < c ? (float)sd[t] : __int_as_float(0x7f800000);
+        nbr[((int64_t)qi - qb) * k + t] = t < c ? si[t] : -1;
+        dist[((int64_t)qi - qb) * k + t] = t < c ? (float)sd[t] : __int_as_float(0x7f800000);
       }
       if (c < k && threadIdx.x == 0) atomicExch(fail, 2);
       __syncthreads();
@@ -598,9 +605,13 @@ int knng_ladder(const float* X, int64_t n, int D, const int32_t* samples, int S,
 
 // build the exact kNN graph. returns 0 ok, 1 cuda error, 2 grid overflow (h too
 // small for the bounding box), 3 fallback capacity exceeded, 4 bad args.
-int knng_grid(const float* X, int64_t n, int D, int k, double h, const double* lo, double span_cells, double diag,
-              int32_t* nbr, float* dist, void* ws, size_t ws_bytes, cudaStream_t st, int64_t* n_fallback) {
+int knng_grid_rows(const float* X, int64_t n, int D, int k, double h, const double* lo, double span_cells,
+                   double diag, int64_t q_begin, int64_t q_count, int32_t* nbr, float* dist, void* ws,
+                   size_t ws_bytes, cudaStream_t st, int64_t* n_fallback) {
   if (D < 1 || D > 5 || k < 1 || k > n - 1 || !(h > 0)) return 4;
+  if (q_begin < 0 || q_count < 0 || q_begin + q_count > n) return 4;
+  if (q_count == 0) { *n_fallback = 0; return 0; }
+  const int64_t qb = q_begin, qe = q_begin + q_count;
   if (ws_bytes < knng_grid_ws(n)) return 4;
   char* p = (char*)ws;
   auto take = [&](size_t b) { char* r = p; p += (b + 255) & ~size_t(255); return (void*)r; };
@@ -647,7 +658,8 @@ int knng_grid(const float* X, int64_t n, int D, int k, double h, const double* l
   {                                                                                                        \
     const int sm = (int)((sizeof(double) + sizeof(int)) * kWarps * kWarpBuf + (sizeof(float) * DD + 4) * kCandCap); \
     cudaFuncSetAttribute(k_cells<DD>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);                    \
-    k_cells<DD><<<gcells, kWarps * 32, sm, st>>>(X, sid, ukey, ustart, ncell, n, gp.bits, hq, k, nbr, dist, fb, nfb); \
+    k_cells<DD><<<gcells, kWarps * 32, sm, st>>>(X, sid, ukey, ustart, ncell, n, gp.bits, hq, k, nbr, dist, fb, nfb, \
+                                                 qb, qe);                                                  \
   }
   switch (D) {
     case 1: CELLS(1) break;
@@ -674,7 +686,7 @@ int knng_grid(const float* X, int64_t n, int D, int k, double h, const double* l
 #define FB(DD)                                                                                                   \
   cudaFuncSetAttribute(k_fallback<DD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);                    \
   k_fallback<DD><<<gf, 256, sm, st>>>(X, sid, ukey, ustart, ncell, n, gp.bits, hq, l[0], l[1], l[2], l[3], l[4], \
-                                      gp.inv_h, k, fb, hfb, nbr, dist, fail, max_ring, dg * 1.000001 + 1e-30);
+                                      gp.inv_h, k, fb, hfb, nbr, dist, fail, max_ring, dg * 1.000001 + 1e-30, qb);
     switch (D) {
       case 1: FB(1) break;
       case 2: FB(2) break;
@@ -689,6 +701,11 @@ int knng_grid(const float* X, int64_t n, int D, int k, double h, const double* l
     if (hfail) return 3;
   }
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
+}
+
+int knng_grid(const float* X, int64_t n, int D, int k, double h, const double* lo, double span_cells, double diag,
+              int32_t* nbr, float* dist, void* ws, size_t ws_bytes, cudaStream_t st, int64_t* n_fallback) {
+  return knng_grid_rows(X, n, D, k, h, lo, span_cells, diag, 0, n, nbr, dist, ws, ws_bytes, st, n_fallback);
 }
 
 // brute-force candidates + exact re-rank; rows failing the certificate are

@@ -34,6 +34,9 @@ def _load():
         L.knng_grid.argtypes = [C.c_void_p, C.c_int64, C.c_int, C.c_int, C.c_double, C.c_void_p, C.c_double,
                                 C.c_double, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p,
                                 C.POINTER(C.c_int64)]
+        L.knng_grid_rows.argtypes = [C.c_void_p, C.c_int64, C.c_int, C.c_int, C.c_double, C.c_void_p, C.c_double,
+                                     C.c_double, C.c_int64, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p,
+                                     C.c_size_t, C.c_void_p, C.POINTER(C.c_int64)]
         L.knng_brute.argtypes = [C.c_void_p, C.c_int64, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p,
                                  C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         L.knng_exact_row.argtypes = [C.c_void_p, C.c_int64, C.c_int, C.c_int64, C.c_void_p, C.c_void_p]
@@ -60,9 +63,11 @@ def estimate_radius(Xd: torch.Tensor, k: int, n_samples: int = 256, quantile: fl
     return float(np.quantile(r_up, quantile))
 
 
-def build_knng_grid(X, k: int, h: float | None = None, device: str = "cuda"):
+def build_knng_grid(X, k: int, h: float | None = None, device: str = "cuda", rows=None):
     """Exact self-excluded kNN graph of X (np/torch float32 [n, d], d <= 5).
-    Returns (nbr int32 [n,k], dist float32 [n,k], info dict) as CUDA tensors."""
+    Returns (nbr int32 [n,k], dist float32 [n,k], info dict) as CUDA tensors.
+    rows=(begin, end): only query rows [begin, end) (one rank's rows; every
+    point stays a candidate) -> [end - begin, k] tensors (knng_grid_rows)."""
     Xd = torch.as_tensor(np.ascontiguousarray(X, np.float32) if isinstance(X, np.ndarray) else X)
     Xd = Xd.to(device=device, dtype=torch.float32).contiguous()
     n, d = Xd.shape
@@ -77,8 +82,11 @@ def build_knng_grid(X, k: int, h: float | None = None, device: str = "cuda"):
     if span >= (1 << bits) - 2:
         h = (np.max(hi - lo) + 4 * h) / ((1 << bits) - 4)  # coarsen: exact either way
         lo = (Xd.min(0).values.double() - 2.0 * h).cpu().numpy().astype(np.float64)
-    nbr = torch.empty((n, k), dtype=torch.int32, device=device)
-    dist = torch.empty((n, k), dtype=torch.float32, device=device)
+    qb, qe = (0, n) if rows is None else (int(rows[0]), int(rows[1]))
+    if not 0 <= qb <= qe <= n:
+        raise ValueError("rows must satisfy 0 <= begin <= end <= n")
+    nbr = torch.empty((qe - qb, k), dtype=torch.int32, device=device)
+    dist = torch.empty((qe - qb, k), dtype=torch.float32, device=device)
     L = _load()
     ws_bytes = L.knng_grid_ws(n)
     ws = torch.empty(ws_bytes, dtype=torch.uint8, device=device)
@@ -87,8 +95,8 @@ def build_knng_grid(X, k: int, h: float | None = None, device: str = "cuda"):
     st = torch.cuda.current_stream().cuda_stream
     span = float(np.max((hi - lo) / h)) + 2
     diag = float(np.sqrt(np.sum((hi - lo) ** 2)))
-    rc = L.knng_grid(Xd.data_ptr(), n, d, k, float(h), lo_c, span, diag, nbr.data_ptr(), dist.data_ptr(),
-                     ws.data_ptr(), ws_bytes, st, C.byref(nfb))
+    rc = L.knng_grid_rows(Xd.data_ptr(), n, d, k, float(h), lo_c, span, diag, qb, qe - qb, nbr.data_ptr(),
+                          dist.data_ptr(), ws.data_ptr(), ws_bytes, st, C.byref(nfb))
     if rc:
         raise RuntimeError(f"knng_grid failed rc={rc}")
     del ws

@@ -123,7 +123,7 @@ def test_knng_library_exports_every_declared_symbol():
         subprocess.check_call(["make", "-C", ROOT, os.path.relpath(knng.LIB_PATH, ROOT)])
     src = re.sub(r"/\*.*?\*/", "", open(os.path.join(ROOT, "include", "knng.h")).read(), flags=re.S)
     fns = sorted(set(re.findall(r"\b(knng_[a-z_0-9]+)\s*\(", src)))
-    assert fns == ["knng_brute", "knng_exact_row", "knng_grid", "knng_grid_ws", "knng_ladder"]
+    assert fns == ["knng_brute", "knng_exact_row", "knng_grid", "knng_grid_rows", "knng_grid_ws", "knng_ladder"]
     L = C.CDLL(knng.LIB_PATH)
     assert all(hasattr(L, f) for f in fns)
     out = subprocess.run(["nm", "-D", "--defined-only", knng.LIB_PATH], capture_output=True, text=True).stdout

@@ -21,7 +21,7 @@ import torch
 
 import paper_2009_04552_b200 as kdb
 from datagen import CONFIGS, gen_config_points
-from datagen.knng_gpu import build_knng_brute, build_knng_grid
+from paper_2009_04552_b200.knng import build_knng_brute, build_knng_grid
 from tests.kdb_harness import assert_parity, oracle_run
 
 pytestmark = pytest.mark.gpu
