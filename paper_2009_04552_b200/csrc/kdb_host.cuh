@@ -406,10 +406,6 @@ kdb_status rows_phase(Mst& m, float eps_run) {
   int64_t C = C32;
   L.all_core = (C == N) ? 1 : 0;  // then the dense id of a vertex is the vertex itself
   LAUNCH(k_init_comp, grid_for(N), kThreads, st, core_bits, L.woff, N, comp, L.cmin);
-  LAUNCH(k_fill_comp_arrays, grid_for(C), kThreads, st, C, L.Kc, L.Bc, general ? nullptr : L.kmin);
-  for (size_t r = 1; r < L.ranks.size(); ++r)
-    LAUNCH(k_fill_comp_arrays, grid_for(C), kThreads, st, C, L.ranks[r].Kc, L.ranks[r].Bc, nullptr);
-  KDB_CUDA(cudaGetLastError());
   const bool use_compact = env_int("KDB_COMPACT", 1) != 0;
   const int gw = env_int("KDB_GW", 4);  // component-gather width of the later light rounds (scan_ell)
   const bool sparse_ids = env_int("KDB_SPARSE", 1) != 0;  // keep root ids once few components remain
@@ -418,8 +414,18 @@ kdb_status rows_phase(Mst& m, float eps_run) {
   const bool fuse1 = !general && use_compact && env_int("KDB_FUSE1", 1) != 0;
   const bool packed1 = fuse1 && L.ranks.size() == 1 && !(multi_rank(comm)) &&
                        env_int("KDB_PACK1", 1) != 0;
-  if (!general)  // hook targets of round 1 (written by the round-1 offers)
-    for (auto& R : L.ranks) LAUNCH(k_fill_i32, grid_for(C), kThreads, st, R.tgt, C, INT32_MAX);
+  // Per-component slots of round 1.  Packed round 1 (one rank, fused ELL pass)
+  // writes a whole record and the certificate bound for EVERY component (each
+  // is one core row of this rank) and the hook reads tgt only under a finite
+  // key: nothing to initialise.
+  if (!packed1) {
+    LAUNCH(k_fill_comp_arrays, grid_for(C), kThreads, st, C, L.Kc, L.Bc, general ? nullptr : L.kmin);
+    for (size_t r = 1; r < L.ranks.size(); ++r)
+      LAUNCH(k_fill_comp_arrays, grid_for(C), kThreads, st, C, L.ranks[r].Kc, L.ranks[r].Bc, nullptr);
+    if (!general)  // hook targets of round 1 (written by the round-1 offers)
+      for (auto& R : L.ranks) LAUNCH(k_fill_i32, grid_for(C), kThreads, st, R.tgt, C, INT32_MAX);
+  }
+  KDB_CUDA(cudaGetLastError());
   for (auto& R : L.ranks) {
     KDB_CUDA(cudaMemsetAsync(R.ctr, 0, sizeof(RoundCounters), st));
     R.compact = false;
@@ -709,8 +715,9 @@ kdb_status rows_phase(Mst& m, float eps_run) {
     last_checked = check;
     const RoundCounters g = slot_of(check)[0];
     if (g_trace)
-      fprintf(stderr, "[kdb] round %d eps=%.6g C->%lld offered=%u hooks=%u live=%u\n", check, (double)eps_run,
-              (long long)g.Cs[(check & 1) ? 1 : 0], g.offered, g.hooks, slot_of(check)[1].na[check & 1]);
+      fprintf(stderr, "[kdb] round %d eps=%.6g C->%lld offered=%u hooks=%u live=%u entries=%llu\n", check,
+              (double)eps_run, (long long)g.Cs[(check & 1) ? 1 : 0], g.offered, g.hooks,
+              slot_of(check)[1].na[check & 1], (unsigned long long)g.entries);
     if (g.violation == 2u) return set_err(KDB_EINTERNAL, "pointer jumping did not converge (hook cycle)");
     if (g.violation) return set_err(KDB_EINVAL, "graph violates the KDB_GRAPH_EXACT promise (a component's "
                                     "minimum missed an incident edge)");

@@ -64,8 +64,8 @@ __global__ void k_fill_comp_arrays(int64_t C, uint64_t* __restrict__ Kc, uint32_
   if (Cp) C = *Cp;
   for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < C;
        c += (int64_t)gridDim.x * blockDim.x) {
-    if (KB) {  // one rank, CAS offers: (key, b) pairs only
-      KB[c] = make_ulonglong2(kSent, kSentB);
+    if (KB) {  // one rank, CAS offers: (key, b << 32 | target) words only
+      KB[c] = make_ulonglong2(kSent, ~0ull);
       continue;
     }
     Kc[c] = kSent;
@@ -704,7 +704,10 @@ __global__ void __launch_bounds__(256) k_light_round(const int4* __restrict__ LE
         const uint32_t j = atomicAdd(&s_n, 1u);
         s_rec[j] = Rec{v, r.h};
         if (CAS) {
-          min_pair128(KB + cv, r.best, r.bestb);
+          // (b, target component) in the second word: the CAS-minimum orders by
+          // (key, b) -- equal (key, b) is the same edge, hence the same target --
+          // and the hook reads the target without gathering comp[]
+          min_pair128(KB + cv, r.best, ((uint64_t)r.bestb << 32) | (uint32_t)r.bestc);
         } else {
           if (precheck) min_offer(Kc + cv, (unsigned long long)r.best);
           else atomicMin(Kc + cv, (unsigned long long)r.best);
@@ -883,15 +886,17 @@ __global__ void __launch_bounds__(256) k_hook(int64_t C, const uint64_t* __restr
       if (c >= C) continue;
       uint64_t K;
       uint32_t Bown = 0, kbown = kInfBits;
+      int32_t tKB = -1;
       if (PACKED) {  // round 1, single rank: (K, B, kmin) of a component in one 16-B record
         const int4 q = __ldcs(rec1 + c);
         K = (uint64_t)(uint32_t)q.x | ((uint64_t)(uint32_t)q.y << 32);
         Bown = (uint32_t)q.z;
         kbown = (uint32_t)q.w;
-      } else if (KB) {  // one rank, CAS offers: (key, b) of a component in one 16-B word
+      } else if (KB) {  // one rank, CAS offers: (key, b << 32 | target) of a component in one 16-B word
         const ulonglong2 q = KB[c];
         K = q.x;
-        Bown = (uint32_t)q.y;
+        Bown = (uint32_t)(q.y >> 32);
+        tKB = (int32_t)(uint32_t)q.y;
       } else {
         K = Kc[c];
       }
@@ -906,6 +911,8 @@ __global__ void __launch_bounds__(256) k_hook(int64_t C, const uint64_t* __restr
           int32_t t2;
           if (tgt) {
             t2 = tgt[c];
+          } else if (KB) {
+            t2 = tKB;
           } else {
             const int32_t x = (gat(comp + a) == (int32_t)c) ? (int32_t)b : (int32_t)a;
             t2 = gat(comp + x);
@@ -923,7 +930,7 @@ __global__ void __launch_bounds__(256) k_hook(int64_t C, const uint64_t* __restr
             const ulonglong2 q = __ldcg(KB + t2);
             const uint64_t Kt = q.x;
             cert_t = Kt != kSent && certified(Kt, kmin, t2);
-            const uint32_t Bt = (uint32_t)q.y;
+            const uint32_t Bt = (uint32_t)(q.y >> 32);
             if (cert_t && (Kt > K || (Kt == K && Bt > b))) ctr->violation = 1u;
             mutual = cert_t && Kt == K && Bt == b;
           } else if (kmin) {  // exact mode: t may abstain; also audit the promise
