@@ -54,6 +54,10 @@ def parse():
     ap.add_argument("--stage", default="cluster", choices=["cluster", "knng"],
                     help="knng: time the exact kNN-graph builder (SURVEY.md 8(f) NEXT 3) on the points of "
                          "--config instead of the clustering stage; compare with Table 2 (PAPER.md:21-36)")
+    ap.add_argument("--sim", type=int, default=0,
+                    help="N=1: run the library's sim communicator with this many virtual ranks (every rank's "
+                         "work in sequence on one GPU; per-rank local-phase times feed the scaling model, "
+                         "DESIGN.md §7)")
     ap.add_argument("--nccl1", action="store_true",
                     help="N=1 through a 1-rank NCCL communicator with every collective issued "
                          "(KDB_NCCL_FORCE=1): the multi-rank host path and its per-round syncs")
@@ -139,8 +143,12 @@ def median_like_numpy(col):
     return float((a + b) / 2)
 
 
-def make_workload(cfg_name: str, scale: float, seed: int, device):
-    """Points (numpy, seeded), exact kNN graph on the GPU, eps from the config rule."""
+def make_workload(cfg_name: str, scale: float, seed: int, device, rank=0, world=1):
+    """Points (numpy, seeded), exact kNN graph on the GPU, eps from the config rule.
+    world > 1: this rank's rows [b, e) only (the grid builder searches all points
+    for its query rows: knng_grid_rows), so no rank ever holds the whole graph
+    (C5: 204.8 GB); eps still comes from the median over ALL rows (the column
+    D[:, M-1] is all-gathered)."""
     import torch
     from datagen import CONFIGS, gen_config_points
     from paper_2009_04552_b200.knng import build_knng_brute, build_knng_grid
@@ -148,16 +156,36 @@ def make_workload(cfg_name: str, scale: float, seed: int, device):
     t0 = time.time()
     X, truth = gen_config_points(cfg_name, seed, scale)
     t1 = time.time()
+    sliced = False
     if X.shape[1] <= 5:   # uniform-grid cell search (C1, C4, C5)
-        nbr, dist, info = build_knng_grid(X, cfg["k"], device=device)
+        if world > 1:
+            from paper_2009_04552_b200.dist import rank_rows
+            rows = rank_rows(len(X), rank, world)
+            nbr, dist, info = build_knng_grid(X, cfg["k"], device=device, rows=rows)
+            sliced = True
+        else:
+            nbr, dist, info = build_knng_grid(X, cfg["k"], device=device)
     else:                 # brute force with exact re-rank (C2 d=50, C3 d=10)
         nbr, dist, info = build_knng_brute(X, cfg["k"], device=device)
     torch.cuda.synchronize()
     t2 = time.time()
-    med = median_like_numpy(dist[:, cfg["M"] - 1])
+    col = dist[:, cfg["M"] - 1].contiguous()
+    if sliced:  # the eps rule's median is over every row: gather the column
+        import torch.distributed as tdist
+        sizes = [torch.zeros(1, dtype=torch.int64, device=device) for _ in range(world)]
+        tdist.all_gather(sizes, torch.tensor([col.numel()], dtype=torch.int64, device=device))
+        mx = int(max(int(x.item()) for x in sizes))
+        pad = torch.full((mx,), float("inf"), dtype=col.dtype, device=device)
+        pad[:col.numel()] = col
+        parts = [torch.empty(mx, dtype=col.dtype, device=device) for _ in range(world)]
+        tdist.all_gather(parts, pad)
+        col = torch.cat([p_[:int(n_.item())] for p_, n_ in zip(parts, sizes)])
+        del parts, pad
+    med = median_like_numpy(col)
+    del col
     eps = float(np.float32(cfg["eps_factor"] * med))
     return dict(X=X, truth=truth, nbr=nbr, dist=dist, eps=eps, M=cfg["M"], k=cfg["k"], N=len(X),
-                d=X.shape[1], gen_s=t1 - t0, graph_build_s=t2 - t1, knng=info, med=med)
+                d=X.shape[1], gen_s=t1 - t0, graph_build_s=t2 - t1, knng=info, med=med, sliced=sliced)
 
 
 def stage_params(args, W):
@@ -284,11 +312,11 @@ def run_ours(args):
         if world > 1:
             tdist.barrier()
 
-    W = make_workload(args.config, args.scale, args.seed, dev)
-    N, k, M, eps = W["N"], W["k"], W["M"], W["eps"]
     from paper_2009_04552_b200.dist import max_over_ranks, rank_rows
+    W = make_workload(args.config, args.scale, args.seed, dev, rank=rank, world=world)
+    N, k, M, eps = W["N"], W["k"], W["M"], W["eps"]
     rb, re_ = rank_rows(N, rank, world)
-    if world > 1:  # keep this rank's rows only
+    if world > 1 and not W["sliced"]:  # keep this rank's rows only
         W["nbr"] = W["nbr"][rb:re_].clone()
         W["dist"] = W["dist"][rb:re_].clone()
         torch.cuda.empty_cache()
@@ -296,6 +324,8 @@ def run_ours(args):
     if args.nccl1 and world == 1:
         os.environ["KDB_NCCL_FORCE"] = "1"
         comm = kdb.Comm.nccl_single()
+    if args.sim and world == 1:  # P virtual ranks on this GPU (DESIGN.md §7 scaling model)
+        comm = kdb.Comm.sim(args.sim)
     ec, eps_list = stage_params(args, W)
     kc = ec or k
     g = kdb.Graph(W["nbr"], W["dist"], n_total=N, row_begin=rb, exact=not args.general, edge_cols=ec)
@@ -352,6 +382,10 @@ def run_ours(args):
     value = N * k * F / (ms * 1e-3)
     n_clusters = int(torch.unique(r.comp[r.comp >= 0]).numel()) if rank == 0 else None
     msf_count, msf_weight = r.count, r.weight
+    if world > 1:  # multi-rank output: each rank returns the edges of its a-range (kdb.h)
+        cnt = torch.tensor([msf_count], dtype=torch.int64, device=dev)
+        tdist.all_reduce(cnt)
+        msf_count = int(cnt.item())
     # clustering quality against the generator's ground truth (outside the timed
     # region): kdb_nmi on the device
     quality = None
@@ -418,7 +452,9 @@ def run_ours(args):
                 "vs_baseline": None, "dtype": "f32", "data": "synthetic",
                 "config": dict(workload_desc(args.config, W, args.scale),
                                parallelism=f"row-partitioned x{world}" + (" (1-rank NCCL, collectives forced)"
-                                                                           if args.nccl1 and world == 1 else ""),
+                                                                           if args.nccl1 and world == 1 else "")
+                               + (f" (sim communicator: {args.sim} virtual ranks on one GPU)"
+                                  if args.sim and world == 1 else ""),
                                exact_graph=not args.general,
                                **stage_desc(ec, eps_list, W)),
                 "roofline": roof,
@@ -432,6 +468,9 @@ def run_ours(args):
                         "phase_ms": {k_: stats[-1][k_] for k_ in
                                      ("init_ms", "min_edges_ms", "contract_ms", "filter_ms", "heavy_ms",
                                       "finalize_ms")},
+                        **({"local_first": stats[-1]["local_first"]} if "local_first" in stats[-1] else {}),
+                        "payload_bytes_per_rank": {"rows": stats[-1]["payload_rows_bytes"],
+                                                   "heavy": stats[-1]["payload_heavy_bytes"]},
                         "filter": {k_: stats[-1][k_] for k_ in
                                    ("tau", "light_components", "survivors", "heavy_rounds", "fallback",
                                     "filter_exceptions", "filter_slow_entries")}}}

@@ -121,14 +121,21 @@ kdb_status kdb_core_mark(const kdb_graph* g, int32_t M, float eps, uint32_t* cor
 size_t kdb_mst_workspace_bytes(const kdb_graph* g, kdb_comm* comm);
 
 /* Alg. 1 lines 10-12: ParallelLocalMST + DistributedCutMST,
- * realised as exact global Boruvka.
+ * realised as exact Boruvka.  With more than one
+ * rank and an exact graph (KDB_GRAPH_EXACT) every rank first contracts its own
+ * rows without any exchange (the exact form of the paper's local MST: a
+ * component hooks only along a certified minimum that stays inside the rank),
+ * then the components left are finished by exchanged rounds.
  *   core_bits : device, replicated output of kdb_core_mark.
  *   comp      : device int32[N] out, replicated: for core v the minimum core id of
  *               v's component (the canonical label), -1 for non-core v.
  *   mst_a/b/w : device [mst_cap] out: the MSF edges {a < b} with weight w, sorted
- *               by (a, b); identical on every rank.  mst_cap >= #core - 1 suffices
- *               (EINVAL if the forest does not fit).
- *   mst_count : host out, number of MSF edges.
+ *               by (a, b).  One process: the whole forest.  A real multi-rank NCCL
+ *               communicator: the edges whose smaller endpoint a lies in THIS
+ *               rank's rows [row_begin, row_begin + n_rows) -- the ranks' outputs
+ *               concatenated in rank order are the whole sorted forest.
+ *               mst_cap >= #core - 1 suffices (EINVAL if the output does not fit).
+ *   mst_count : host out, number of MSF edges returned (this rank's share).
  *   mst_weight: host out, the fp64 sum of the MSF weights, computed exactly and
  *               rounded once (independent of summation order and of the rank count).
  *   workspace : device, >= kdb_mst_workspace_bytes(g, comm) bytes, 256-B aligned.
@@ -195,8 +202,14 @@ kdb_status kdb_nmi(const int32_t* a, const int32_t* b, int64_t n, double* nmi /*
  * exceptions, out[16] = filter slow entries, out[17] / out[18] = bytes per rank
  * carried by the MIN all-reduces over component arrays in the rows / heavy
  * phase (counted with or without a communicator; with kdb_mst_inexact the
- * local phase needs none: groups never share a component).  Returns entries
- * written. */
+ * local phase needs none: groups never share a component).  Local-first
+ * contraction (multi-rank exact mode): out[19] = 1 when it ran, out[20] / out[21]
+ * = max / sum over (virtual) ranks of the local-phase ms, out[22] = transition ms,
+ * out[23] = global-phase ms, out[24] = components entering the global phase,
+ * out[25] = rows parked for it (all ranks), out[26] = bytes per rank of the
+ * transition's all-gathers, out[27] = local rounds (max over ranks), out[28] =
+ * global-phase ms of the per-rank offers and ties (all ranks).  Returns
+ * entries written (at most 32). */
 int kdb_last_mst_stats(double* out, int cap);
 
 /* Measurement hooks (bench.py).  kdb_launch_count(): kernels this library has

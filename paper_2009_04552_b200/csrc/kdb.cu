@@ -63,7 +63,7 @@
 namespace {
 
 thread_local std::string g_err;
-thread_local double g_stats[20];
+thread_local double g_stats[32];
 
 kdb_status set_err(kdb_status s, const char* fmt, ...) {
   char buf[512];
@@ -243,6 +243,10 @@ struct NcclApi {
   ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                             cudaStream_t) = nullptr;
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
 };
 NcclApi g_nccl;
@@ -257,7 +261,12 @@ kdb_status nccl_load() {
   g_nccl.AllReduce = (decltype(g_nccl.AllReduce))dlsym(h, "ncclAllReduce");
   g_nccl.CommDestroy = (decltype(g_nccl.CommDestroy))dlsym(h, "ncclCommDestroy");
   g_nccl.GetErrorString = (decltype(g_nccl.GetErrorString))dlsym(h, "ncclGetErrorString");
-  if (!g_nccl.GetUniqueId || !g_nccl.CommInitRank || !g_nccl.AllReduce || !g_nccl.CommDestroy)
+  g_nccl.Broadcast = (decltype(g_nccl.Broadcast))dlsym(h, "ncclBroadcast");
+  g_nccl.AllGather = (decltype(g_nccl.AllGather))dlsym(h, "ncclAllGather");
+  g_nccl.GroupStart = (decltype(g_nccl.GroupStart))dlsym(h, "ncclGroupStart");
+  g_nccl.GroupEnd = (decltype(g_nccl.GroupEnd))dlsym(h, "ncclGroupEnd");
+  if (!g_nccl.GetUniqueId || !g_nccl.CommInitRank || !g_nccl.AllReduce || !g_nccl.CommDestroy ||
+      !g_nccl.Broadcast || !g_nccl.AllGather || !g_nccl.GroupStart || !g_nccl.GroupEnd)
     return set_err(KDB_ENCCL, "NCCL library lacks required symbols");
   g_nccl.h = h;
   return KDB_OK;
@@ -348,6 +357,7 @@ struct RoundCounters {
   uint32_t n_deep;               // per rank: rows whose kW ELL entries are all within eps_run
   uint32_t grab;                 // chunk cursor of the ordered row kernels (per rank)
   uint32_t n_off2;
+  uint32_t n_park;               // per rank, local-first phase: rows parked for the global phase
   uint32_t na[2];                // per rank: row-list sizes, ping-pong (input na[cur], output na[cur^1])
   uint32_t ni[2];                // per rank: in-list sizes, ping-pong
   long long Cs[2];               // global: component count, ping-pong (current Cs[par], next Cs[par^1])
@@ -412,7 +422,7 @@ const char* kdb_status_string(kdb_status s) {
 const char* kdb_last_error(void) { return g_err.c_str(); }
 
 int kdb_last_mst_stats(double* out, int cap) {
-  int n = std::min(cap, 20);
+  int n = std::min(cap, 32);
   for (int i = 0; i < n; ++i) out[i] = g_stats[i];
   return n;
 }
@@ -532,7 +542,7 @@ size_t kdb_mst_workspace_bytes(const kdb_graph* g, kdb_comm* comm) {
   rank_ranges(g, comm, rb, rn);
   Layout L;
   return carve(L, nullptr, true, g->n_total, (int)rb.size(), rb.data(), rn.data(), !(g->flags & KDB_GRAPH_EXACT),
-               edge_cols_of(g));
+               edge_cols_of(g), -1, local_first_on(g, comm));
 }
 
 }  // extern "C"
@@ -579,11 +589,12 @@ kdb_status mst_impl(const kdb_graph* g, float eps, const uint32_t* core_bits, in
   m.comp = comp;
   // the local view is no kNN graph (no certificate): in-edge lists
   m.general = inexact || !(g->flags & KDB_GRAPH_EXACT);
+  m.lf = !inexact && !m.general && local_first_on(g, comm);
   Layout& L = m.L;
   std::vector<int64_t> rb, rn;
   rank_ranges(g, comm, rb, rn);
   const size_t need = carve(L, (char*)workspace, false, N, (int)rb.size(), rb.data(), rn.data(), m.general, m.k,
-                            inexact ? g->n_rows * (int64_t)m.k : -1);
+                            inexact ? g->n_rows * (int64_t)m.k : -1, local_first_on(g, comm) && !inexact);
   if (ws_bytes < need) return set_err(KDB_ENOMEM, "workspace %zu < required %zu bytes", ws_bytes, need);
   KDB_TRY(guards_fill((char*)workspace, L.guards, (cudaStream_t)stream));
   *mst_count = 0;
@@ -654,8 +665,27 @@ kdb_status mst_impl(const kdb_graph* g, float eps, const uint32_t* core_bits, in
   RoundCounters hc;
   KDB_CUDA(cudaMemcpyAsync(&hc, L.ctr, sizeof(hc), cudaMemcpyDeviceToHost, st));
   KDB_CUDA(cudaStreamSynchronize(st));
-  const int64_t ne = (int64_t)hc.msf_count;
+  int64_t ne = (int64_t)hc.msf_count;
   if (ne > N) return set_err(KDB_EINTERNAL, "MSF larger than N-1");
+  const bool dist_out = multi_rank(comm);
+  if (dist_out && ne > 0) {
+    // multi-rank output (kdb.h): this rank returns the MSF edges whose smaller
+    // endpoint lies in its rows -- its local-phase edges and its share of the
+    // replicated global / heavy-phase edges
+    RankState& R0 = L.ranks[0];
+    KDB_CUDA(cudaMemsetAsync(&L.ctr->n_off, 0, sizeof(uint32_t), st));
+    LAUNCH(k_keep_a_range, grid_for(ne), kThreads, st, L.e_key, reinterpret_cast<const uint32_t*>(L.e_w), ne,
+           R0.row_begin, R0.row_begin + R0.n_rows, L.Kc, L.Bc, &L.ctr->n_off);
+    KDB_CUDA(cudaGetLastError());
+    uint32_t kept = 0;
+    KDB_CUDA(cudaMemcpyAsync(&kept, &L.ctr->n_off, sizeof(kept), cudaMemcpyDeviceToHost, st));
+    KDB_CUDA(cudaStreamSynchronize(st));
+    std::swap(L.e_key, L.Kc);
+    float* w = L.e_w;
+    L.e_w = reinterpret_cast<float*>(L.Bc);
+    L.Bc = reinterpret_cast<uint32_t*>(w);
+    ne = kept;
+  }
   if (ne > mst_cap) return set_err(KDB_EINVAL, "mst_cap %lld < MSF size %lld", (long long)mst_cap, (long long)ne);
   // canonical labels: comp[v] = cmin[comp[v]] (through hcomp after a heavy phase)
   if (m.C_heavy >= 0)
@@ -700,15 +730,21 @@ kdb_status mst_impl(const kdb_graph* g, float eps, const uint32_t* core_bits, in
     KDB_CUDA(cudaMemsetAsync(L.buckets, 0, 256 * sizeof(unsigned long long), st));
     LAUNCH(k_wbuckets, grid_for(ne), kThreads, st, ne, mst_w, L.buckets);
     KDB_CUDA(cudaGetLastError());
-    KDB_CUDA(cudaMemcpyAsync(bk, L.buckets, sizeof(bk), cudaMemcpyDeviceToHost, st));
+  } else {
+    KDB_CUDA(cudaMemsetAsync(L.buckets, 0, 256 * sizeof(unsigned long long), st));
   }
+  // the forest's total weight: integer bucket counts, so a SUM over ranks is exact
+  if (dist_out)
+    KDB_TRY(nccl_check(g_nccl.AllReduce(L.buckets, L.buckets, 256, ncclUint64, ncclSum, comm->nccl, st),
+                       "ncclAllReduce(weight buckets)"));
+  KDB_CUDA(cudaMemcpyAsync(bk, L.buckets, sizeof(bk), cudaMemcpyDeviceToHost, st));
   KDB_CUDA(cudaEventRecord(m.ev[1], st));
   KDB_CUDA(cudaStreamSynchronize(st));
   const double t_fin = elapsed(m.ev[0], m.ev[1]);
   if (g_prof.on) g_prof.drain();
   KDB_TRY(guards_check((const char*)workspace, L.guards, st, "kdb_mst"));
   *mst_count = ne;
-  *mst_weight = ne > 0 ? exact_bucket_sum(bk) : 0.0;
+  *mst_weight = exact_bucket_sum(bk);
   g_stats[0] = m.rounds;
   g_stats[1] = m.t_init;
   g_stats[2] = m.t_min_edges;
@@ -728,6 +764,19 @@ kdb_status mst_impl(const kdb_graph* g, float eps, const uint32_t* core_bits, in
   g_stats[16] = (double)m.slow_entries;
   g_stats[17] = inexact ? 0.0 : m.payload_rows;  // inexact: the groups' local phases share nothing
   g_stats[18] = m.payload_heavy;
+  // local-first contraction (multi-rank exact mode): per-virtual-rank local
+  // phase (max / sum over ranks), transition, global phase, and what the
+  // global phase received
+  g_stats[19] = m.lf ? 1.0 : 0.0;
+  g_stats[20] = m.t_local_max;
+  g_stats[21] = m.t_local_sum;
+  g_stats[22] = m.t_transition;
+  g_stats[23] = m.t_global;
+  g_stats[24] = (double)m.C_global;
+  g_stats[25] = (double)m.parked_rows;
+  g_stats[26] = m.payload_transition;
+  g_stats[27] = m.local_rounds;
+  g_stats[28] = m.t_global_scan;
   return KDB_OK;
 }
 

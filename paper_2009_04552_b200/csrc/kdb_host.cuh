@@ -117,6 +117,10 @@ struct RankState {
   int32_t* in_act[2] = {nullptr, nullptr};
   uint32_t n_in_act = 0;
   RoundCounters* ctr = nullptr;  // per-rank counters (act/off)
+  // local-first phase (multi-rank exact mode): the phase's own round counters
+  // and the rows parked for the global phase (heads kept)
+  RoundCounters* lctr = nullptr;
+  Rec* park = nullptr;
   // heavy phase: survivors (ping-pong) and their keep flags
   HEdge* hs[2] = {nullptr, nullptr};
   uint8_t* hkeep = nullptr;
@@ -137,6 +141,7 @@ struct Layout {
   float* e_w;
   unsigned long long* buckets;
   int4* rec1;       // round 1, single rank, exact mode: packed (K, B, kmin) per component
+  uint8_t *frz, *frz2;  // local-first phase: frozen components (ping-pong through the contraction)
   int32_t* hcomp;   // heavy phase: light component -> heavy component
   int32_t* dom;     // filter fast path: dominant component per id block
   uint32_t* bloom;  // filter fast path: Bloom filter of the exceptions
@@ -172,7 +177,7 @@ size_t cub_tmp_bytes(int64_t N, int64_t cap_edges) {
 
 // carve the workspace; returns bytes needed
 size_t carve(Layout& L, char* base, bool dry, int64_t N, int nr, const int64_t* rb, const int64_t* rn,
-             bool general, int32_t k, int64_t hs_cap_override = -1) {
+             bool general, int32_t k, int64_t hs_cap_override = -1, bool local_first = false) {
   Carver cv{base, 0, 0, dry};
   L.guards.clear();
   cv.guards = &L.guards;
@@ -193,6 +198,8 @@ size_t carve(Layout& L, char* base, bool dry, int64_t N, int nr, const int64_t* 
   L.e_w = cv.take<float>(N + 1);
   L.buckets = cv.take<unsigned long long>(256);
   L.rec1 = general ? nullptr : cv.take<int4>(N + 1);
+  L.frz = local_first ? cv.take<uint8_t>(N + 1) : nullptr;
+  L.frz2 = local_first ? cv.take<uint8_t>(N + 1) : nullptr;
   L.hcomp = cv.take<int32_t>(N + 1);
   L.dom = cv.take<int32_t>(kDomMax);
   L.bloom = cv.take<uint32_t>(kBloomBits / 32);
@@ -213,6 +220,10 @@ size_t carve(Layout& L, char* base, bool dry, int64_t N, int nr, const int64_t* 
     R.off_cap_rows = n;
     R.offers = cv.take<Offer>(general ? n + N : n);
     R.ctr = cv.take<RoundCounters>(1);
+    if (local_first) {  // local-first phase (exact mode, > 1 rank)
+      R.lctr = cv.take<RoundCounters>(1);
+      R.park = cv.take<Rec>(n);
+    }
     if (r > 0) {
       R.Kc = cv.take<uint64_t>(N + 1);
       R.Bc = cv.take<uint32_t>(N + 1);
@@ -289,6 +300,21 @@ bool multi_rank(const kdb_comm* comm) {
   return f && atoi(f) != 0;
 }
 
+int env_int(const char* name, int dflt);
+
+// Local-first contraction runs when more than one rank shares
+// the graph (a real NCCL communicator, the sim communicator with P >= 2, or the
+// forced 1-rank NCCL test mode) and the caller promises an exact graph (the
+// certificate is what lets a rank decide from its own rows); KDB_LOCAL=0 turns
+// it off (the replicated-rounds path of round 1).
+bool local_first_on(const kdb_graph* g, const kdb_comm* comm) {
+  if (!(g->flags & KDB_GRAPH_EXACT) || env_int("KDB_LOCAL", 1) == 0) return false;
+  if (env_int("KDB_COMPACT", 1) == 0 || env_int("KDB_FUSE1", 1) == 0 || env_int("KDB_CAS", 1) == 0 ||
+      env_int("KDB_PACK1", 1) == 0)
+    return false;  // the phase runs on the one-rank machinery (ELL, fused round 1, CAS offers)
+  return multi_rank(comm) || (comm && comm->kind == 2 && comm->nranks >= 2);
+}
+
 kdb_status allreduce_min_u64(kdb_comm* comm, uint64_t* p, int64_t n, cudaStream_t st) {
   if (!multi_rank(comm) || n <= 0) return KDB_OK;
   return nccl_check(g_nccl.AllReduce(p, p, (size_t)n, ncclUint64, ncclMin, comm->nccl, st), "ncclAllReduce(u64,min)");
@@ -333,6 +359,20 @@ struct Mst {
   float tau = 0.f;
   int fallback = 0;
   cudaEvent_t ev[4];
+  // local-first contraction: lf = run it (multi-rank exact
+  // mode); local = this Mst is one rank's local phase (view lv, C0 local
+  // components, MSF slots ecap); cont = the global phase continuing from the
+  // parked rows
+  bool lf = false, local = false, cont = false;
+  LocalView lv;
+  int64_t C0 = 0, ecap = -1;
+  uint64_t n_park = 0, msf_local = 0;
+  double t_local_max = 0, t_local_sum = 0, t_transition = 0, t_global = 0;
+  int local_rounds = 0;
+  double t_global_scan = 0;  // global phase: per-rank offers and ties (all ranks, in sequence under sim)
+  int64_t C_global = -1;      // components entering the global phase
+  uint64_t parked_rows = 0;   // rows entering the global phase (all ranks)
+  double payload_transition = 0;  // bytes per rank of the all-gathers between the phases
 };
 
 float elapsed(cudaEvent_t a, cudaEvent_t b) {
@@ -374,6 +414,8 @@ kdb_status pick_tau(Mst& m, int m0, float* tau_out) {
   return KDB_OK;
 }
 
+kdb_status local_first(Mst& m, float eps_run);
+
 // a2-a8: rows-Boruvka over the candidate entries with w <= eps_run (from
 // singletons).  Leaves comp[] = dense component ids (0..C-1), L.cmin = minimum
 // core id per component, m.C.  Resets the MSF counter.
@@ -390,30 +432,47 @@ kdb_status rows_phase(Mst& m, float eps_run) {
   const bool vec = (ld % 4) == 0;
   cudaEvent_t* ev = m.ev;
   KDB_CUDA(cudaEventRecord(ev[0], st));
-
-  // ---- a2: dense component ids -------------------------------------------------
-  const int64_t nwords = (N + 31) / 32;
-  uint32_t* popc = reinterpret_cast<uint32_t*>(L.flag);  // scratch, nwords + 1 <= N + 1
-  KDB_CUDA(cudaMemsetAsync(popc + nwords, 0, sizeof(uint32_t), st));
-  KDB_CUDA(cudaMemsetAsync(L.ctr, 0, sizeof(RoundCounters), st));
-  LAUNCH(k_popc_words, grid_for(nwords), kThreads, st, core_bits, nwords, popc);
-  KDB_CUDA(cudaGetLastError());
-  size_t cb = L.cub_bytes;
-  { LaunchScope ls_("cub::DeviceScan", st, false); KDB_CUDA(cub::DeviceScan::ExclusiveSum(L.cub_tmp, cb, popc, L.woff, (int)(nwords + 1), st)); }
-  uint32_t C32 = 0;  // woff[nwords] = number of core points
-  KDB_CUDA(cudaMemcpyAsync(&C32, L.woff + nwords, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
-  KDB_CUDA(cudaStreamSynchronize(st));
-  int64_t C = C32;
-  L.all_core = (C == N) ? 1 : 0;  // then the dense id of a vertex is the vertex itself
-  LAUNCH(k_init_comp, grid_for(N), kThreads, st, core_bits, L.woff, N, comp, L.cmin);
   const bool use_compact = env_int("KDB_COMPACT", 1) != 0;
   const int gw = env_int("KDB_GW", 4);  // component-gather width of the later light rounds (scan_ell)
   const bool sparse_ids = env_int("KDB_SPARSE", 1) != 0;  // keep root ids once few components remain
+  // local-first phase of one rank (m.local): LOCAL component ids, the rank's
+  // per-component slices, no exchange; the global phase (m.cont) continues the
+  // rounds from the rows the local phases parked
+  const LocalView lv = m.local ? m.lv : LocalView{};
+  uint8_t* frz = m.local ? L.frz : nullptr;
+  const int64_t ecap = m.ecap >= 0 ? m.ecap : N;
+  int64_t C = 0;
+  bool fuse1 = false, packed1 = false;
+  size_t cb = L.cub_bytes;
+  if (m.cont) {
+    C = m.C;  // global components after the local-first phases (state set by local_first)
+  } else {
+  KDB_CUDA(cudaMemsetAsync(L.ctr, 0, sizeof(RoundCounters), st));
+  if (!m.local) {
+    // ---- a2: dense component ids -------------------------------------------------
+    const int64_t nwords = (N + 31) / 32;
+    uint32_t* popc = reinterpret_cast<uint32_t*>(L.flag);  // scratch, nwords + 1 <= N + 1
+    KDB_CUDA(cudaMemsetAsync(popc + nwords, 0, sizeof(uint32_t), st));
+    LAUNCH(k_popc_words, grid_for(nwords), kThreads, st, core_bits, nwords, popc);
+    KDB_CUDA(cudaGetLastError());
+    { LaunchScope ls_("cub::DeviceScan", st, false); KDB_CUDA(cub::DeviceScan::ExclusiveSum(L.cub_tmp, cb, popc, L.woff, (int)(nwords + 1), st)); }
+    uint32_t C32 = 0;  // woff[nwords] = number of core points
+    KDB_CUDA(cudaMemcpyAsync(&C32, L.woff + nwords, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    KDB_CUDA(cudaStreamSynchronize(st));
+    C = C32;
+    L.all_core = (C == N) ? 1 : 0;  // then the dense id of a vertex is the vertex itself
+    LAUNCH(k_init_comp, grid_for(N), kThreads, st, core_bits, L.woff, N, comp, L.cmin);
+    if (m.lf) return local_first(m, eps_run);
+  } else {
+    // local ids: dense over this rank's core rows (the caller shifted comp)
+    C = m.C0;
+    L.all_core = (C == L.ranks[0].n_rows) ? 1 : 0;  // then a row's local id is v - lo
+    KDB_CUDA(cudaMemsetAsync(frz, 0, (size_t)std::max<int64_t>(C, 1), st));
+  }
   // exact mode: round 1 (singleton components) is fused into the ELL pass; a
   // single rank also packs (K, B, kmin) per component for the round-1 hook
-  const bool fuse1 = !general && use_compact && env_int("KDB_FUSE1", 1) != 0;
-  const bool packed1 = fuse1 && L.ranks.size() == 1 && !(multi_rank(comm)) &&
-                       env_int("KDB_PACK1", 1) != 0;
+  fuse1 = !general && use_compact && env_int("KDB_FUSE1", 1) != 0;
+  packed1 = fuse1 && L.ranks.size() == 1 && !(multi_rank(comm)) && env_int("KDB_PACK1", 1) != 0;
   // Per-component slots of round 1.  Packed round 1 (one rank, fused ELL pass)
   // writes a whole record and the certificate bound for EVERY component (each
   // is one core row of this rank) and the hook reads tgt only under a finite
@@ -437,7 +496,7 @@ kdb_status rows_phase(Mst& m, float eps_run) {
 #define KDB_ELL_LAUNCH(V, A)                                                                                    \
   LAUNCH((k_light_ell<V, A>), grid_for(R.n_rows), kThreads, st, R.nbr, R.dist, R.n_rows, ld, k, eps_run, R.row_begin, \
          comp, general ? nullptr : L.kmin, R.LE, R.act[0], &R.ctr->na[0], &R.ctr->grab, fuse1 ? 1 : 0,         \
-         L.all_core, N, R.Kc, R.Bc, R.tgt, packed1 ? L.rec1 : nullptr, &R.ctr->n_deep)
+         L.all_core, N, R.Kc, R.Bc, R.tgt, packed1 ? L.rec1 : nullptr, &R.ctr->n_deep, lv)
       if (a32) KDB_ELL_LAUNCH(true, true);
       else if (vec) KDB_ELL_LAUNCH(true, false);
       else KDB_ELL_LAUNCH(false, false);
@@ -449,7 +508,7 @@ kdb_status rows_phase(Mst& m, float eps_run) {
     KDB_CUDA(cudaGetLastError());
   }
   if (!general) KDB_TRY(allreduce_min_u32(comm, L.kmin, C, st));
-  if (!general) m.payload_rows += 4.0 * C;
+  if (!general && !m.local) m.payload_rows += 4.0 * C;
   KDB_CUDA(cudaEventRecord(ev[1], st));
   // ---- general mode: in-edge lists --------------------------------------------
   if (general) {
@@ -483,6 +542,7 @@ kdb_status rows_phase(Mst& m, float eps_run) {
   KDB_CUDA(cudaEventSynchronize(ev[2]));
   m.t_init += elapsed(ev[0], ev[1]);
   m.t_inlist += elapsed(ev[1], ev[2]);
+  }  // !m.cont
 
   // ---- Boruvka rounds -------------------------------------------------------------
   // Pipelined: every kernel reads its counts (components, list sizes) from the
@@ -538,6 +598,7 @@ kdb_status rows_phase(Mst& m, float eps_run) {
     ni_ub[r] = L.ranks[r].n_in_act;
   }
   int rounds = 0, stalls = 0;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> gscan;  // global phase: per-rank work spans
   const uint32_t* kmin_cert = general ? nullptr : L.kmin;
   auto slot_of = [&](int rr) { return slots + (size_t)(rr % kSlots) * (1 + nr); };
 
@@ -563,9 +624,15 @@ kdb_status rows_phase(Mst& m, float eps_run) {
       LAUNCH(k_fill_i32, grid_for(C_bound), kThreads, st, (int32_t*)L.kmin2, C_bound, (int32_t)kInfBits,
              (const int64_t*)Cn);
     // map[c] = new dense id of c's tree (reuses `parent`, no longer needed)
+    if (frz) KDB_CUDA(cudaMemsetAsync(L.frz2, 0, (size_t)std::max<int64_t>(C_bound, 1), st));
     LAUNCH(k_merge, grid_for(C_bound), kThreads, st, C_bound, L.rootof, sparse ? (const int32_t*)nullptr : L.newid,
-           L.cmin, general ? nullptr : L.kmin, L.cmin2, L.kmin2, L.parent, Cd);
-    LAUNCH(k_relabel, grid_for(N / 8 + 1), kThreads, st, N, comp, L.parent, (const int32_t*)nullptr);
+           L.cmin, general ? nullptr : L.kmin, L.cmin2, L.kmin2, L.parent, Cd, (const uint8_t*)frz,
+           frz ? L.frz2 : nullptr);
+    if (m.local)  // only this rank's rows carry (local) ids
+      LAUNCH(k_relabel, grid_for((lv.hi - lv.lo) / 8 + 1), kThreads, st, lv.hi - lv.lo, comp + lv.lo, L.parent,
+             (const int32_t*)nullptr);
+    else
+      LAUNCH(k_relabel, grid_for(N / 8 + 1), kThreads, st, N, comp, L.parent, (const int32_t*)nullptr);
     LAUNCH(k_fill_comp_arrays, grid_for(C_bound), kThreads, st, C_bound, L.Kc, L.Bc, nullptr, (const int64_t*)Cn, KB);
     for (size_t r = 1; r < nr; ++r)
       LAUNCH(k_fill_comp_arrays, grid_for(C_bound), kThreads, st, C_bound, L.ranks[r].Kc, L.ranks[r].Bc, nullptr,
@@ -573,6 +640,10 @@ kdb_status rows_phase(Mst& m, float eps_run) {
     KDB_CUDA(cudaGetLastError());
     std::swap(L.cmin, L.cmin2);
     std::swap(L.kmin, L.kmin2);
+    if (frz) {
+      std::swap(L.frz, L.frz2);
+      frz = L.frz;
+    }
     kmin_cert = general ? nullptr : L.kmin;
     par ^= 1;
     return KDB_OK;
@@ -591,7 +662,7 @@ kdb_status rows_phase(Mst& m, float eps_run) {
   bool finished = false;
   while (!finished) {
     ++rounds;
-    const bool direct = rounds == 1 && !general;
+    const bool direct = rounds == 1 && !general && !m.cont;
     const int64_t* Cd = (const int64_t*)&L.ctr->Cs[par];
     cudaEvent_t e0;
     KDB_CUDA(cudaEventCreate(&e0));
@@ -606,6 +677,16 @@ kdb_status rows_phase(Mst& m, float eps_run) {
       for (size_t r = 0; r < nr; ++r) live += na_ub[r];
       const int pc = env_int("KDB_PRECHECK", -1);
       precheck = pc >= 0 ? pc : (live > 8 * (uint64_t)std::max<int64_t>(C_ub, 1) ? 1 : 0);
+    }
+    // global phase of the local-first scheme: time the per-rank work (offers,
+    // ties: divides by the rank count on real GPUs) apart from the rest
+    cudaEvent_t gsA = nullptr, gsB = nullptr, gsC = nullptr, gsD = nullptr;
+    if (m.cont) {
+      for (cudaEvent_t* e : {&gsA, &gsB, &gsC, &gsD}) {
+        KDB_CUDA(cudaEventCreate(e));
+        ev_rnd.push_back(*e);
+      }
+      KDB_CUDA(cudaEventRecord(gsA, st));
     }
     // a3: offers (rows, then in-lists), per rank, into that rank's Kc partial
     for (size_t r = 0; r < nr; ++r) {
@@ -627,7 +708,8 @@ kdb_status rows_phase(Mst& m, float eps_run) {
 #define KDB_LR_LAUNCH(...)                                                                                       \
   LAUNCH((k_light_round<__VA_ARGS__>), grid_for(na_ub[r]), kThreads, st, R.LE, R.nbr, R.dist, ld, k, eps_run,       \
          R.row_begin, N, comp, R.act[cur], na_ub[r], R.act[cur ^ 1], nout, &R.ctr->grab, R.offers,                 \
-         (unsigned long long*)R.Kc, &L.ctr->entries, nin, precheck, KB)
+         (unsigned long long*)R.Kc, &L.ctr->entries, nin, precheck, KB, lv, (const uint8_t*)frz, R.park,         \
+         m.local ? &L.ctr->n_park : nullptr)
           // pipelined chunk loads pay when many rows scan past their first chunk
           // (C3: its inner shell is all light); they cost occupancy otherwise
           const int pk = env_int("KDB_PIPE", -1);
@@ -668,11 +750,13 @@ kdb_status rows_phase(Mst& m, float eps_run) {
                &R.ctr->n_off, (unsigned long long*)R.Kc, &R.ctr->ni[cur]);
       KDB_CUDA(cudaGetLastError());
     }
+    if (m.cont) KDB_CUDA(cudaEventRecord(gsB, st));
     // exchange: sim -> min over virtual ranks; nccl -> allreduce
     for (size_t r = 1; r < nr; ++r)
       LAUNCH(k_min_into_u64, grid_for(C_ub), kThreads, st, L.Kc, L.ranks[r].Kc, C_ub, Cd);
     KDB_TRY(allreduce_min_u64(comm, L.Kc, C_ub, st));
     m.payload_rows += 8.0 * C_ub;
+    if (m.cont) KDB_CUDA(cudaEventRecord(gsC, st));
     // a4: ties (the direct round already wrote Bc and the targets)
     if (!direct && !cas) {
       for (size_t r = 0; r < nr; ++r) {
@@ -682,6 +766,11 @@ kdb_status rows_phase(Mst& m, float eps_run) {
           LAUNCH(k_tie, grid_for(ni_ub[r]), kThreads, st, R.offers + R.off_cap_rows, &R.ctr->n_off, L.Kc, R.Bc);
         KDB_CUDA(cudaGetLastError());
       }
+    }
+    if (m.cont) {
+      KDB_CUDA(cudaEventRecord(gsD, st));
+      gscan.push_back({gsA, gsB});
+      gscan.push_back({gsC, gsD});
     }
     for (size_t r = 1; r < nr; ++r)
       LAUNCH(k_min_into_u32, grid_for(C_ub), kThreads, st, L.Bc, L.ranks[r].Bc, C_ub, Cd);
@@ -698,11 +787,11 @@ kdb_status rows_phase(Mst& m, float eps_run) {
     KDB_CUDA(cudaMemsetAsync(&L.ctr->hooks, 0, 4 * sizeof(uint32_t), st));
     if (direct && packed1)
       LAUNCH(k_hook<true>, grid_for(C_ub), kThreads, st, C_ub, L.Kc, L.Bc, L.tgt, kmin_cert, comp, L.parent, L.e_key,
-             L.e_w, N, L.ctr, Cd, L.rec1);
+             L.e_w, ecap, L.ctr, Cd, L.rec1, (const ulonglong2*)nullptr, frz);
     else
       LAUNCH(k_hook<false>, grid_for(C_ub), kThreads, st, C_ub, L.Kc, L.Bc, direct ? L.tgt : nullptr, kmin_cert,
-             comp, L.parent, L.e_key, L.e_w, N, L.ctr, Cd, (const int4*)nullptr,
-             (cas && !direct) ? (const ulonglong2*)KB : nullptr);
+             comp, L.parent, L.e_key, L.e_w, ecap, L.ctr, Cd, (const int4*)nullptr,
+             (cas && !direct) ? (const ulonglong2*)KB : nullptr, frz);
     KDB_CUDA(cudaGetLastError());
     // a6: contract (no hooks => identity)
     KDB_TRY(contract(C_ub));
@@ -722,6 +811,9 @@ kdb_status rows_phase(Mst& m, float eps_run) {
     if (g.violation) return set_err(KDB_EINVAL, "graph violates the KDB_GRAPH_EXACT promise (a component's "
                                     "minimum missed an incident edge)");
     if (g.offered == 0) break;  // a8: no component has a leaving edge
+    // local-first phase: no hook means every component with a leaving edge is
+    // frozen (remote or uncertifiable minimum) -- the rest is the global phase's
+    if (m.local && g.hooks == 0) break;
     // upper bounds for the next launch: the counts after round `check`
     {
       // after round `check` the current parity was flipped `rounds - check` more times
@@ -791,6 +883,7 @@ kdb_status rows_phase(Mst& m, float eps_run) {
     KDB_CUDA(cudaEventRecord(ev[2], st));
     KDB_CUDA(cudaEventSynchronize(ev[2]));
     m.t_min_edges += elapsed(ev_rnd.front(), ev[2]);  // rounds are pipelined: one span
+    for (auto& pr : gscan) m.t_global_scan += elapsed(pr.first, pr.second);
   }
   {
     RoundCounters gg;
@@ -804,6 +897,226 @@ kdb_status rows_phase(Mst& m, float eps_run) {
   m.rounds += rounds;
   m.stalls += stalls;
   m.C = C;
+  if (m.local) {
+    // the rows still live (their components froze in the last rounds) join the
+    // parked ones: together they are this rank's input to the global phase
+    RankState& R = L.ranks[0];
+    RoundCounters rc;
+    KDB_CUDA(cudaMemcpy(&rc, R.ctr, sizeof(rc), cudaMemcpyDeviceToHost));
+    const uint32_t n_live = rc.na[cur];
+    if (n_live)
+      KDB_CUDA(cudaMemcpyAsync(R.park + hc.n_park, R.act[cur], n_live * sizeof(Rec), cudaMemcpyDeviceToDevice, st));
+    m.n_park = hc.n_park + n_live;
+    m.msf_local = hc.msf_count;
+  }
+  return KDB_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Local-first contraction (multi-rank exact mode, SURVEY.md
+// §8(e)(ii)): the paper's local/cut split (Alg. 2 + Alg. 4, PAPER.md:538-541,
+// 698-751) made exact.
+//  1. Local phase, per rank, no exchange: rows-Boruvka on the rank's own rows
+//     with LOCAL component ids.  A component hooks only along its certified
+//     minimum when that minimum is a local edge -- the cut property makes every
+//     such edge an MSF edge whatever the other ranks hold.  A component whose
+//     minimum leaves the rank (or cannot be certified from its rows) freezes:
+//     it never hooks again in this phase, and its rows are parked with their
+//     heads.  Local components may still hook INTO it (its minimum then stays
+//     the same edge).
+//  2. Transition: global dense ids = rank offset + local id; the component ids
+//     of every row, and the per-component minimum core id and certificate
+//     bound, are all-gathered once (NCCL broadcasts, one per rank).
+//  3. Global phase: the replicated-rounds Boruvka continues from the parked
+//     rows over the components the local phases left (C_G).
+// The forest is the Kruskal forest either way (every hook is a true minimum).
+kdb_status local_first(Mst& m, float eps_run) {
+  Layout& L = m.L;
+  cudaStream_t st = m.st;
+  kdb_comm* comm = m.comm;
+  const bool nccl = multi_rank(comm);
+  const int nr = (int)L.ranks.size();
+  const int P = nccl ? comm->nranks : nr;
+  const int me = nccl ? comm->rank : 0;  // first rank index this process runs
+  cudaEvent_t* ev = m.ev;
+  KDB_CUDA(cudaEventRecord(ev[3], st));
+  // ---- every rank's rows --------------------------------------------------------
+  int64_t* scratch = reinterpret_cast<int64_t*>(L.buckets);  // 256 x 8 B, free until the finalize
+  if (P > 64) return set_err(KDB_EINVAL, "local-first phase supports at most 64 ranks");
+  std::vector<int64_t> rb(P), rn(P);
+  if (nccl) {
+    int64_t h[2] = {L.ranks[0].row_begin, L.ranks[0].n_rows};
+    KDB_CUDA(cudaMemcpyAsync(scratch + 2 * me, h, sizeof(h), cudaMemcpyHostToDevice, st));
+    KDB_TRY(nccl_check(g_nccl.AllGather(scratch + 2 * me, scratch, 2, ncclInt64, comm->nccl, st), "ncclAllGather(rows)"));
+    std::vector<int64_t> hh(2 * P);
+    KDB_CUDA(cudaMemcpyAsync(hh.data(), scratch, 2 * P * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    KDB_CUDA(cudaStreamSynchronize(st));
+    for (int r = 0; r < P; ++r) { rb[r] = hh[2 * r]; rn[r] = hh[2 * r + 1]; }
+  } else {
+    for (int r = 0; r < P; ++r) { rb[r] = L.ranks[r].row_begin; rn[r] = L.ranks[r].n_rows; }
+  }
+  // global dense id of each rank's first core row, and its core-row count
+  std::vector<int64_t> lo(P), C0(P);
+  {
+    std::vector<int64_t> pos(2 * P);
+    for (int r = 0; r < P; ++r) { pos[2 * r] = rb[r]; pos[2 * r + 1] = rb[r] + rn[r]; }
+    KDB_CUDA(cudaMemcpyAsync(scratch, pos.data(), 2 * P * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    LAUNCH(k_core_below, 1, 128, st, m.bits, L.woff, scratch, 2 * P, scratch + 2 * P);
+    KDB_CUDA(cudaGetLastError());
+    std::vector<int64_t> cnt(2 * P);
+    KDB_CUDA(cudaMemcpyAsync(cnt.data(), scratch + 2 * P, 2 * P * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    KDB_CUDA(cudaStreamSynchronize(st));
+    for (int r = 0; r < P; ++r) { lo[r] = cnt[2 * r]; C0[r] = cnt[2 * r + 1] - cnt[2 * r]; }
+  }
+  // ---- 1. local phases ------------------------------------------------------------
+  std::vector<int64_t> CL(P, 0), EC(P, 0), NP(P, 0);
+  m.t_local_max = m.t_local_sum = 0;
+  for (int ri = 0; ri < nr; ++ri) {
+    const int r = me + ri;
+    RankState& R = L.ranks[ri];
+    if (C0[r] == 0) {  // no core row: nothing to contract, nothing to park
+      R.compact = true;
+      R.n_deep = 0;
+      continue;
+    }
+    const int64_t o = lo[r];
+    LAUNCH(k_shift_comp, grid_for(rn[r]), kThreads, st, m.comp + rb[r], rn[r], (int32_t)-o);
+    Mst sub;
+    sub.g = m.g;
+    sub.comm = nullptr;
+    sub.st = st;
+    sub.N = m.N;
+    sub.k = m.k;
+    sub.ld = m.ld;
+    sub.bits = m.bits;
+    sub.comp = m.comp;
+    sub.general = false;
+    sub.local = true;
+    sub.lv.lo = rb[r];
+    sub.lv.hi = rb[r] + rn[r];
+    sub.lv.bits = m.bits;
+    sub.C0 = C0[r];
+    sub.ecap = C0[r];
+    for (int i = 0; i < 4; ++i) sub.ev[i] = m.ev[i];
+    Layout& S = sub.L;
+    S = L;
+    S.cmin += o; S.cmin2 += o; S.parent += o; S.rootof += o; S.newid += o; S.flag += o;
+    S.kmin += o; S.kmin2 += o; S.Kc += o; S.Bc += o; S.tgt += o; S.e_key += o; S.e_w += o;
+    S.rec1 += o; S.frz += o; S.frz2 += o;
+    S.ctr = R.lctr;
+    S.ranks.assign(1, R);
+    S.ranks[0].Kc = S.Kc;
+    S.ranks[0].Bc = S.Bc;
+    S.ranks[0].tgt = S.tgt;
+    KDB_TRY(rows_phase(sub, eps_run));
+    R.n_deep = sub.L.ranks[0].n_deep;
+    R.compact = sub.L.ranks[0].compact;
+    CL[r] = sub.C;
+    EC[r] = (int64_t)sub.msf_local;
+    NP[r] = (int64_t)sub.n_park;
+    const double t = sub.t_init + sub.t_min_edges;
+    m.t_local_max = std::max(m.t_local_max, t);
+    m.t_local_sum += t;
+    m.entries += sub.entries;
+    m.rounds = std::max(m.rounds, sub.rounds);
+    m.local_rounds = std::max(m.local_rounds, sub.rounds);
+  }
+  KDB_CUDA(cudaEventRecord(ev[1], st));
+  // ---- 2. transition -----------------------------------------------------------------
+  if (nccl) {  // every rank's (components, local MSF edges, parked rows)
+    int64_t h[3] = {CL[me], EC[me], NP[me]};
+    KDB_CUDA(cudaMemcpyAsync(scratch + 3 * me, h, sizeof(h), cudaMemcpyHostToDevice, st));
+    KDB_TRY(nccl_check(g_nccl.AllGather(scratch + 3 * me, scratch, 3, ncclInt64, comm->nccl, st), "ncclAllGather(counts)"));
+    std::vector<int64_t> hh(3 * P);
+    KDB_CUDA(cudaMemcpyAsync(hh.data(), scratch, 3 * P * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    KDB_CUDA(cudaStreamSynchronize(st));
+    for (int r = 0; r < P; ++r) { CL[r] = hh[3 * r]; EC[r] = hh[3 * r + 1]; NP[r] = hh[3 * r + 2]; }
+  }
+  std::vector<int64_t> off(P + 1, 0), eoff(P + 1, 0);
+  for (int r = 0; r < P; ++r) { off[r + 1] = off[r] + CL[r]; eoff[r + 1] = eoff[r] + EC[r]; }
+  const int64_t CG = off[P];
+  // this process's ranks: per-component data to the global dense positions
+  // (into the *2 arrays, swapped below), row ids local -> global, local MSF
+  // edges compacted (sim: all ranks in rank order; NCCL: this rank's at 0)
+  uint64_t* tK = L.Kc;                              // free: refilled for the global phase
+  uint32_t* tA = reinterpret_cast<uint32_t*>(L.Bc);  // e_w holds the a endpoint as u32
+  int64_t e_here = 0;
+  for (int ri = 0; ri < nr; ++ri) {
+    const int r = me + ri;
+    if (C0[r] == 0) continue;
+    if (CL[r] > 0) {
+      KDB_CUDA(cudaMemcpyAsync(L.cmin2 + off[r], L.cmin + lo[r], CL[r] * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
+      KDB_CUDA(cudaMemcpyAsync(L.kmin2 + off[r], L.kmin + lo[r], CL[r] * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st));
+    }
+    LAUNCH(k_shift_comp, grid_for(rn[r]), kThreads, st, m.comp + rb[r], rn[r], (int32_t)off[r]);
+    const int64_t eo = nccl ? 0 : eoff[r];
+    if (EC[r] > 0) {
+      KDB_CUDA(cudaMemcpyAsync(tK + eo, L.e_key + lo[r], EC[r] * sizeof(uint64_t), cudaMemcpyDeviceToDevice, st));
+      KDB_CUDA(cudaMemcpyAsync(tA + eo, reinterpret_cast<const uint32_t*>(L.e_w) + lo[r], EC[r] * sizeof(uint32_t),
+                               cudaMemcpyDeviceToDevice, st));
+    }
+    e_here += EC[r];
+  }
+  KDB_CUDA(cudaGetLastError());
+  if (nccl) {  // replicate: every rank's row ids and its components' (cmin, kmin)
+    KDB_TRY(nccl_check(g_nccl.GroupStart(), "ncclGroupStart"));
+    for (int r = 0; r < P; ++r) {
+      if (rn[r] > 0)
+        KDB_TRY(nccl_check(g_nccl.Broadcast(m.comp + rb[r], m.comp + rb[r], (size_t)rn[r], ncclInt32, r, comm->nccl, st),
+                           "ncclBroadcast(comp)"));
+      if (CL[r] > 0) {
+        KDB_TRY(nccl_check(g_nccl.Broadcast(L.cmin2 + off[r], L.cmin2 + off[r], (size_t)CL[r], ncclInt32, r,
+                                            comm->nccl, st), "ncclBroadcast(cmin)"));
+        KDB_TRY(nccl_check(g_nccl.Broadcast(L.kmin2 + off[r], L.kmin2 + off[r], (size_t)CL[r], ncclUint32, r,
+                                            comm->nccl, st), "ncclBroadcast(kmin)"));
+      }
+    }
+    KDB_TRY(nccl_check(g_nccl.GroupEnd(), "ncclGroupEnd"));
+  }
+  m.payload_transition = 4.0 * (double)m.N + 8.0 * (double)CG;
+  std::swap(L.cmin, L.cmin2);
+  std::swap(L.kmin, L.kmin2);
+  std::swap(L.e_key, L.Kc);
+  {
+    float* w = L.e_w;
+    L.e_w = reinterpret_cast<float*>(L.Bc);
+    L.Bc = reinterpret_cast<uint32_t*>(w);
+  }
+  L.ranks[0].Kc = L.Kc;
+  L.ranks[0].Bc = L.Bc;
+  // ---- 3. global phase ---------------------------------------------------------------
+  KDB_CUDA(cudaMemsetAsync(L.ctr, 0, sizeof(RoundCounters), st));
+  {
+    const uint32_t ec = (uint32_t)e_here;
+    KDB_CUDA(cudaMemcpyAsync(&L.ctr->msf_count, &ec, sizeof(ec), cudaMemcpyHostToDevice, st));
+  }
+  uint64_t parked = 0;
+  for (int r = 0; r < P; ++r) parked += (uint64_t)NP[r];
+  for (int ri = 0; ri < nr; ++ri) {
+    const int r = me + ri;
+    RankState& R = L.ranks[ri];
+    KDB_CUDA(cudaMemsetAsync(R.ctr, 0, sizeof(RoundCounters), st));
+    const uint32_t np = (uint32_t)NP[r];
+    if (np) KDB_CUDA(cudaMemcpyAsync(R.act[0], R.park, np * sizeof(Rec), cudaMemcpyDeviceToDevice, st));
+    KDB_CUDA(cudaMemcpyAsync(&R.ctr->na[0], &np, sizeof(np), cudaMemcpyHostToDevice, st));
+    R.n_act = np;
+    R.n_in_act = 0;
+    if (!R.compact && R.n_rows > 0) return set_err(KDB_EINTERNAL, "local-first phase without the light ELL");
+  }
+  for (int ri = 0; ri < nr; ++ri)
+    if (CG > 0) LAUNCH(k_fill_comp_arrays, grid_for(CG), kThreads, st, CG, L.ranks[ri].Kc, L.ranks[ri].Bc, nullptr);
+  KDB_CUDA(cudaGetLastError());
+  KDB_CUDA(cudaEventRecord(ev[2], st));
+  m.t_transition = elapsed(ev[1], ev[2]);
+  m.t_init += elapsed(ev[3], ev[2]) - m.t_transition;  // local phases (all virtual ranks, in sequence)
+  m.C_global = CG;
+  m.parked_rows = parked;
+  m.cont = true;
+  m.C = CG;
+  const double tmin0 = m.t_min_edges;
+  KDB_TRY(rows_phase(m, eps_run));
+  m.cont = false;
+  m.t_global = m.t_min_edges - tmin0;
   return KDB_OK;
 }
 

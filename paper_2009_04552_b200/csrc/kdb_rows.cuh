@@ -210,6 +210,25 @@ struct RowScan {
   int32_t bestc;  // component of the best entry's far endpoint
 };
 
+// Local-first phase (multi-rank exact mode): a rank contracts
+// its own rows before any exchange.  Component ids are then LOCAL (dense over
+// the rank's core rows) and an entry whose far endpoint lies outside the
+// rank's rows [lo, hi) is a leaving edge to a component this rank cannot see:
+// its component reads as kRemote (>= 0, so it leaves; never a local id).
+// bits == nullptr: the global view (every id is local, dense ids global).
+constexpr int32_t kRemote = 0x7fffffff;
+struct LocalView {
+  int64_t lo = 0, hi = 0;
+  const uint32_t* bits = nullptr;
+};
+// component of far endpoint J (< 0: not a candidate, i.e. non-core); direct:
+// singleton components whose dense id is the vertex's position in the view
+__device__ __forceinline__ int32_t comp_of(const int32_t* __restrict__ comp, int64_t J, bool direct,
+                                           const LocalView& lv) {
+  if (lv.bits && (J < lv.lo || J >= lv.hi)) return is_core(lv.bits, J) ? kRemote : -1;
+  return direct ? (int32_t)(J - lv.lo) : gat(comp + J);
+}
+
 // Scan row (nr, dr) of vertex v (component cv) from head h.  direct: singleton
 // components (round 1, exact mode) -- every candidate leaves; with all_core the
 // dense component id of a vertex is the vertex itself (no gathers at all).
@@ -217,7 +236,7 @@ template <bool VEC, bool DIRECT>
 __device__ __forceinline__ RowScan scan_row(const int32_t* __restrict__ nr, const float* __restrict__ dr, int k,
                                             float eps, int32_t v, int32_t cv, int h, int64_t N,
                                             const int32_t* __restrict__ comp, int all_core,
-                                            unsigned long long& reads) {
+                                            unsigned long long& reads, const LocalView lv = LocalView{}) {
   RowScan r{false, k, kSent, kSentB, -1};
   float wstar = 0.f;
   int c0 = h & ~3;
@@ -231,7 +250,7 @@ __device__ __forceinline__ RowScan scan_row(const int32_t* __restrict__ nr, cons
     for (int j = 0; j < 4; ++j) {
       const int idx = c0 + j;
       const bool cand = idx >= h && idx < k && w[j] <= eps && J[j] >= 0 && J[j] < N && J[j] != v;
-      cj[j] = cand ? ((DIRECT && all_core) ? J[j] : gat(comp + J[j])) : -1;
+      cj[j] = cand ? comp_of(comp, J[j], DIRECT && all_core, lv) : -1;
     }
     reads += (unsigned long long)(min(c0 + 4, k) - max(c0, h));
 #pragma unroll
@@ -377,7 +396,8 @@ __global__ void __launch_bounds__(256) k_light_ell(const int32_t* __restrict__ n
                                                    uint32_t* __restrict__ n_act, uint32_t* __restrict__ grab,
                                                    int direct, int all_core, int64_t N, uint64_t* __restrict__ Kc,
                                                    uint32_t* __restrict__ Bc, int32_t* __restrict__ tgt,
-                                                   int4* __restrict__ rec1, uint32_t* __restrict__ n_deep) {
+                                                   int4* __restrict__ rec1, uint32_t* __restrict__ n_deep,
+                                                   const LocalView lv = LocalView{}) {
   __shared__ __align__(16) Rec s_rec[kChunk];
   __shared__ uint32_t s_n, s_chunk, s_base;
   uint32_t deep = 0;  // rows whose kW ELL entries are all within eps (their scans go past the first chunk)
@@ -476,7 +496,7 @@ __global__ void __launch_bounds__(256) k_light_ell(const int32_t* __restrict__ n
         if (!r.found) {
           if (!(w[c] <= eps)) { done = true; continue; }  // sorted: no candidate at all
           if (Jc < 0 || Jc >= N || Jc == v) continue;
-          const int32_t cc = all_core ? Jc : gat(comp + Jc);
+          const int32_t cc = comp_of(comp, Jc, all_core, lv);
           if (cc < 0) continue;
           r.found = true;
           r.h = c;
@@ -487,7 +507,7 @@ __global__ void __launch_bounds__(256) k_light_ell(const int32_t* __restrict__ n
         } else {
           if (w[c] != wstar) { done = true; continue; }
           if (Jc < 0 || Jc >= N || Jc == v) continue;
-          const int32_t cc = all_core ? Jc : gat(comp + Jc);
+          const int32_t cc = comp_of(comp, Jc, all_core, lv);
           if (cc < 0) continue;
           const uint64_t kk = pack_key(mono_bits(w[c]), (uint32_t)min(v, (int64_t)Jc));
           const uint32_t bb = (uint32_t)max(v, (int64_t)Jc);
@@ -496,7 +516,7 @@ __global__ void __launch_bounds__(256) k_light_ell(const int32_t* __restrict__ n
       }
       if (!done && k > kW) {  // the search or the tie group runs past the ELL: scan the row in place
         unsigned long long rd = 0;
-        r = scan_row<false, true>(nr, dr, k, eps, (int32_t)v, -1, 0, N, comp, all_core, rd);
+        r = scan_row<false, true>(nr, dr, k, eps, (int32_t)v, -1, 0, N, comp, all_core, rd, lv);
       }
       if (rec1) {  // single rank: one packed record per component for k_hook<true>
         __stcg(rec1 + cv, make_int4((int)(uint32_t)r.best, (int)(uint32_t)(r.best >> 32), (int)r.bestb, (int)kb));
@@ -531,7 +551,7 @@ template <bool DIRECT, int GW = 4, bool PIPE = false>
 __device__ __forceinline__ RowScan scan_ell(const int4* __restrict__ le, const int32_t* __restrict__ nr,
                                             const float* __restrict__ dr, int k, float eps, int32_t v, int32_t cv,
                                             int h, int64_t N, const int32_t* __restrict__ comp, int all_core,
-                                            unsigned long long& reads) {
+                                            unsigned long long& reads, const LocalView lv = LocalView{}) {
   RowScan r{false, k, kSent, kSentB, -1};
   uint32_t wstar = 0;
   const int kend = min(k, kW);
@@ -563,7 +583,7 @@ __device__ __forceinline__ RowScan scan_ell(const int4* __restrict__ le, const i
       const int idx = c0 + j;
       bool cand = idx >= h && idx < kend && w[j] <= eps && J[j] >= 0 && J[j] < N && J[j] != v;
       if (GW < 4 && r.found && mono_bits(w[j]) != wstar) cand = false;  // past the tie group: no gather
-      cj[j] = cand ? ((DIRECT && all_core) ? J[j] : gat(comp + J[j])) : -1;
+      cj[j] = cand ? comp_of(comp, J[j], DIRECT && all_core, lv) : -1;
     }
 #pragma unroll
     for (int j = g0; j < g0 + GW; ++j) {
@@ -594,7 +614,7 @@ __device__ __forceinline__ RowScan scan_ell(const int4* __restrict__ le, const i
   if (!done && k > kW) {
     // the candidate prefix (or the minimum's tie group) runs past the ELL
     if (!r.found) {
-      RowScan t = scan_row<false, DIRECT>(nr, dr, k, eps, v, cv, max(h, kW), N, comp, all_core, reads);
+      RowScan t = scan_row<false, DIRECT>(nr, dr, k, eps, v, cv, max(h, kW), N, comp, all_core, reads, lv);
       return t;
     }
     // continue the tie group of weight wstar in the graph row
@@ -604,7 +624,7 @@ __device__ __forceinline__ RowScan scan_ell(const int4* __restrict__ le, const i
       const int32_t Jc = __ldcg(nr + c);
       ++reads;
       if (Jc < 0 || Jc >= N || Jc == v) continue;
-      const int32_t cc = (DIRECT && all_core) ? Jc : gat(comp + Jc);
+      const int32_t cc = comp_of(comp, Jc, DIRECT && all_core, lv);
       if (cc < 0 || (!DIRECT && cc == cv)) continue;
       const uint64_t kk = pack_key(wstar, (uint32_t)min(v, Jc));
       const uint32_t bb = (uint32_t)max(v, Jc);
@@ -679,7 +699,11 @@ __global__ void __launch_bounds__(256) k_light_round(const int4* __restrict__ LE
                                                      uint32_t* __restrict__ grab, Offer* __restrict__ offers,
                                                      unsigned long long* __restrict__ Kc,
                                                      unsigned long long* __restrict__ n_entries, const uint32_t* __restrict__ n_in_p = nullptr,
-                                                     int precheck = 0, ulonglong2* __restrict__ KB = nullptr) {
+                                                     int precheck = 0, ulonglong2* __restrict__ KB = nullptr,
+                                                     const LocalView lv = LocalView{},
+                                                     const uint8_t* __restrict__ frz = nullptr,
+                                                     Rec* __restrict__ park = nullptr,
+                                                     uint32_t* __restrict__ n_park = nullptr) {
   if (n_in_p) n_in = *n_in_p;
   __shared__ __align__(16) Rec s_rec[kChunk];
   __shared__ __align__(16) Offer s_off[CAS ? 1 : kChunk];
@@ -697,9 +721,21 @@ __global__ void __launch_bounds__(256) k_light_round(const int4* __restrict__ LE
       const int32_t v = a.x;
       const int32_t cv = gat(comp + v);
       KDB_DCHECK(cv >= 0 && v >= row_begin && v < N, 8u);  // a live row is a local core vertex
+      if (frz && frz[cv]) {
+        // local-first phase: the component is frozen (its minimum is a remote or
+        // uncertifiable edge and stays so while it only absorbs local
+        // components): the row waits, head unchanged, for the global phase
+        const unsigned am = __activemask();
+        const int lane = threadIdx.x & 31, leader = __ffs(am) - 1;
+        uint32_t base = 0;
+        if (lane == leader) base = atomicAdd(n_park, (uint32_t)__popc(am));
+        base = __shfl_sync(am, base, leader);
+        park[base + __popc(am & ((1u << lane) - 1u))] = Rec{v, a.y};
+        continue;
+      }
       const int64_t i = (int64_t)v - row_begin;
       const RowScan r = scan_ell<false, GW, PIPE>(LE + i * (kW / 2), nbr + i * ld, dist + i * ld, k, eps, v, cv, a.y,
-                                                  N, comp, 0, reads);
+                                                  N, comp, 0, reads, lv);
       if (r.found) {
         const uint32_t j = atomicAdd(&s_n, 1u);
         s_rec[j] = Rec{v, r.h};
@@ -868,7 +904,8 @@ __global__ void __launch_bounds__(256) k_hook(int64_t C, const uint64_t* __restr
                        const int32_t* __restrict__ comp, int32_t* __restrict__ parent,
                        uint64_t* __restrict__ e_key, float* __restrict__ e_w, int64_t e_cap,
                        RoundCounters* __restrict__ ctr, const int64_t* __restrict__ Cp,
-                       const int4* __restrict__ rec1, const ulonglong2* __restrict__ KB = nullptr) {
+                       const int4* __restrict__ rec1, const ulonglong2* __restrict__ KB = nullptr,
+                       uint8_t* __restrict__ frz = nullptr) {
   if (Cp) C = *Cp;
   __shared__ uint64_t s_key[kHookChunk];
   __shared__ uint32_t s_w[kHookChunk];
@@ -905,6 +942,15 @@ __global__ void __launch_bounds__(256) k_hook(int64_t C, const uint64_t* __restr
         ++n_off;
         if (PACKED ? !((uint32_t)(K >> 32) < kbown) : !certified(K, kmin, c)) {
           ++n_unc;
+          // local-first phase: an uncertified component waits for the global
+          // phase (its true minimum may be an in-edge from another rank's row)
+          if (frz) frz[c] = 1;
+        } else if (frz && (PACKED || KB ? (PACKED ? tgt[c] : tKB) : kRemote) == kRemote) {
+          // local-first phase: the minimum leaves the rank -- frozen (a frozen
+          // component never hooks, so it stays a root and keeps that minimum
+          // while local components hook into it)
+          ++n_unc;
+          frz[c] = 1;
         } else {
           const uint32_t a = (uint32_t)K;
           const uint32_t b = (PACKED || KB) ? Bown : Bc[c];
@@ -1034,7 +1080,8 @@ __global__ void k_count_roots(const int64_t* __restrict__ Cp, const int32_t* __r
 // new per-component arrays: cmin/kmin are minima over the merged tree
 __global__ void k_merge(int64_t C, const int32_t* __restrict__ rootof, const int32_t* __restrict__ newid,
                         const int32_t* __restrict__ cmin, const uint32_t* __restrict__ kmin,
-                        int32_t* __restrict__ cmin2, uint32_t* __restrict__ kmin2, int32_t* __restrict__ map, const int64_t* __restrict__ Cp = nullptr) {
+                        int32_t* __restrict__ cmin2, uint32_t* __restrict__ kmin2, int32_t* __restrict__ map, const int64_t* __restrict__ Cp = nullptr,
+                        const uint8_t* __restrict__ frz = nullptr, uint8_t* __restrict__ frz2 = nullptr) {
   if (Cp) C = *Cp;
   for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < C;
        c += (int64_t)gridDim.x * blockDim.x) {
@@ -1047,6 +1094,47 @@ __global__ void k_merge(int64_t C, const int32_t* __restrict__ rootof, const int
       const uint32_t km = kmin[c];
       if (km != kInfBits) atomicMin(kmin2 + r, km);  // kmin2 starts at +inf
     }
+    if (frz && frz[c]) frz2[r] = 1;  // frozen components are roots; the flag stays with them
+  }
+}
+
+// number of core vertices below each position pos[i] (a rank's first global
+// dense id): woff[p >> 5] + the core bits below p in its word
+__global__ void k_core_below(const uint32_t* __restrict__ bits, const uint32_t* __restrict__ woff,
+                             const int64_t* __restrict__ pos, int n, int64_t* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t p = pos[i];
+  const uint32_t b = (p & 31) ? __popc(bits[p >> 5] & ((1u << (p & 31)) - 1u)) : 0u;
+  out[i] = (int64_t)woff[p >> 5] + b;
+}
+
+// MSF edges (e_w = a, e_key = b << 32 | w bits) whose smaller endpoint a lies
+// in [lo, hi), compacted (multi-rank output: each rank returns its a-range)
+__global__ void k_keep_a_range(const uint64_t* __restrict__ e_key, const uint32_t* __restrict__ e_a, int64_t n,
+                               int64_t lo, int64_t hi, uint64_t* __restrict__ o_key, uint32_t* __restrict__ o_a,
+                               uint32_t* __restrict__ cnt) {
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = base + threadIdx.x;
+    bool keep = false;
+    uint32_t a = 0;
+    if (i < n) {
+      a = e_a[i];
+      keep = (int64_t)a >= lo && (int64_t)a < hi;
+    }
+    const uint32_t slot = block_reserve(cnt, keep);
+    if (keep) {
+      o_key[slot] = e_key[i];
+      o_a[slot] = a;
+    }
+  }
+}
+
+// comp[v] += delta for the core vertices of a row range (local <-> global ids)
+__global__ void k_shift_comp(int32_t* __restrict__ comp, int64_t n, int32_t delta) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t c = comp[v];
+    if (c >= 0) comp[v] = c + delta;
   }
 }
 

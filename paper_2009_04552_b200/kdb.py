@@ -237,14 +237,18 @@ def mst(g: Graph, eps: float, core_bits: torch.Tensor, comm: Comm | None = None,
                          C.c_void_p(w.data_ptr()), cap, C.byref(cnt), C.byref(tot),
                          C.c_void_p(workspace.data_ptr()), workspace.numel(), _h(comm), _stream(stream)),
            "kdb_mst")
-    st = (C.c_double * 20)()
-    lib().kdb_last_mst_stats(st, 20)
+    st = (C.c_double * 32)()
+    lib().kdb_last_mst_stats(st, 32)
     stats = dict(rounds=int(st[0]), init_ms=st[1], min_edges_ms=st[2], contract_ms=st[3],
                  finalize_ms=st[4], inlist_ms=st[5], stall_rounds=int(st[6]), entries_read=int(st[7]),
                  filter_ms=st[8], heavy_ms=st[9], survivors=int(st[10]), heavy_rounds=int(st[11]),
                  tau=st[12], light_components=int(st[13]), fallback=int(st[14]),
                  filter_exceptions=int(st[15]), filter_slow_entries=int(st[16]),
                  payload_rows_bytes=st[17], payload_heavy_bytes=st[18])
+    if st[19]:  # local-first contraction ran (multi-rank exact mode)
+        stats["local_first"] = dict(local_ms_max=st[20], local_ms_sum=st[21], transition_ms=st[22],
+                                    global_ms=st[23], global_components=int(st[24]), parked_rows=int(st[25]),
+                                    transition_bytes=st[26], local_rounds=int(st[27]), global_scan_ms=st[28])
     m = cnt.value
     return MstResult(comp[:N], a[:m], b[:m], w[:m], m, tot.value, stats)
 
