@@ -171,16 +171,8 @@ def make_workload(cfg_name: str, scale: float, seed: int, device, rank=0, world=
     t2 = time.time()
     col = dist[:, cfg["M"] - 1].contiguous()
     if sliced:  # the eps rule's median is over every row: gather the column
-        import torch.distributed as tdist
-        sizes = [torch.zeros(1, dtype=torch.int64, device=device) for _ in range(world)]
-        tdist.all_gather(sizes, torch.tensor([col.numel()], dtype=torch.int64, device=device))
-        mx = int(max(int(x.item()) for x in sizes))
-        pad = torch.full((mx,), float("inf"), dtype=col.dtype, device=device)
-        pad[:col.numel()] = col
-        parts = [torch.empty(mx, dtype=col.dtype, device=device) for _ in range(world)]
-        tdist.all_gather(parts, pad)
-        col = torch.cat([p_[:int(n_.item())] for p_, n_ in zip(parts, sizes)])
-        del parts, pad
+        from paper_2009_04552_b200.dist import gather_rows
+        col = gather_rows(col)
     med = median_like_numpy(col)
     del col
     eps = float(np.float32(cfg["eps_factor"] * med))

@@ -37,3 +37,23 @@ def max_over_ranks(value: float, device=None, group=None) -> float:
     if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
     return float(t.item())
+
+
+def gather_rows(col, group=None):
+    """Concatenate every rank's 1-D tensor ``col`` (this rank's rows of a
+    per-row quantity, any length) in rank order on every rank: the eps rule's
+    median is over ALL rows (bench.py builds only its own rows of the graph)."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size(group) == 1:
+        return col
+    world = dist.get_world_size(group)
+    n = torch.tensor([col.numel()], dtype=torch.int64, device=col.device)
+    sizes = [torch.zeros_like(n) for _ in range(world)]
+    dist.all_gather(sizes, n, group=group)
+    mx = int(max(int(x.item()) for x in sizes))
+    pad = torch.zeros(mx, dtype=col.dtype, device=col.device)
+    pad[:col.numel()] = col
+    parts = [torch.empty_like(pad) for _ in range(world)]
+    dist.all_gather(parts, pad, group=group)
+    return torch.cat([p[:int(k.item())] for p, k in zip(parts, sizes)])

@@ -15,7 +15,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2009_04552_b200.dist import max_over_ranks, rank_rows, share_nccl_id
+from paper_2009_04552_b200.dist import gather_rows, max_over_ranks, rank_rows, share_nccl_id
 
 
 def _free_port():
@@ -75,19 +75,41 @@ def _worker(rank, world, port, out):
         ref = np.full(C, np.iinfo(np.int64).max, np.int64)
         np.minimum.at(ref, comp, key)
         res["min_ok"] = bool(np.array_equal(t.numpy(), ref))
+        # 5. the eps rule's column: every rank's rows (uneven counts) gathered in
+        #    rank order equal the whole column on every rank (bench.py per-rank build)
+        colfull = rng.uniform(size=N + world).astype(np.float32)
+        rb2, re2 = rank_rows(N + world, rank, world)
+        g = gather_rows(torch.from_numpy(colfull[rb2:re2].copy()))
+        res["gather_ok"] = bool(np.array_equal(g.numpy(), colfull))
+        # 6. multi-rank MSF output (kdb.h): rank r keeps the edges whose smaller
+        #    endpoint lies in its rows, sorted by (a, b); concatenated in rank
+        #    order they are the whole sorted forest
+        import oracle
+        from datagen import knn_bruteforce
+        X = np.random.default_rng(5).standard_normal((300, 2)).astype(np.float32)
+        nbr, dstt = knn_bruteforce(X, 8)
+        ex = oracle.kdbscan(nbr, dstt, 4, np.float32(np.median(dstt[:, 3]) * 1.5))
+        a, b = ex["msf_a"].astype(np.int64), ex["msf_b"].astype(np.int64)
+        perm = np.random.default_rng(rank).permutation(len(a))  # emission order is arbitrary
+        ra, rb_ = rank_rows(300, rank, world)
+        keep = perm[(a[perm] >= ra) & (a[perm] < rb_)]
+        mine = sorted(zip(a[keep].tolist(), b[keep].tolist()))
+        allp = [None] * world
+        dist.all_gather_object(allp, mine)
+        res["msf_ok"] = [e for p_ in allp for e in p_] == list(zip(a.tolist(), b.tolist()))
         out[rank] = res
     finally:
         dist.destroy_process_group()
 
 
-def test_gloo_world2_host_logic():
-    world = 2
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_world2_host_logic(world):
     port = _free_port()
     with mp.Manager() as mgr:
         out = mgr.dict()
         mp.spawn(_worker, args=(world, port, out), nprocs=world, join=True)
         res = dict(out)
-    assert set(res) == {0, 1}
+    assert set(res) == set(range(world))
     for r in res.values():
-        assert r["uid_ok"] and r["bits_ok"] and r["min_ok"]
-        assert r["max"] == 2.0
+        assert r["uid_ok"] and r["bits_ok"] and r["min_ok"] and r["gather_ok"] and r["msf_ok"]
+        assert r["max"] == float(world)
