@@ -278,6 +278,38 @@ def host_cpu():
     return model, os.cpu_count()
 
 
+def host_ram_gb():
+    try:
+        for line in open("/proc/meminfo"):
+            if line.startswith("MemTotal"):
+                return round(int(line.split()[1]) / 2**20, 1)
+    except OSError:
+        pass
+    return None
+
+
+def whole_workload_baseline(cfg_name, scale, ec, n_eps):
+    """The oracle on the WHOLE workload, measured once by tools/window_parity.py
+    (the ten closed cluster windows of C4 / C5 are exact independent
+    sub-problems: the sum of their single-threaded oracle times is the
+    whole-workload time) and committed under profiles/r02/ -- quoted, not
+    re-run (about 17 min of CPU per config)."""
+    if ec or n_eps != 1:
+        return None
+    tag = {("C4", 1.0): "C4", ("C5", 0.25): "C5q"}.get((cfg_name, scale))
+    path = os.path.join(ROOT, "profiles", "r02", f"window_parity_{tag}.json") if tag else None
+    if not path or not os.path.exists(path):
+        return None
+    d = json.load(open(path))
+    b = d.get("cpu_baseline_whole_workload")
+    if not b:
+        return None
+    return {"source": os.path.relpath(path, ROOT), "host": d.get("host"),
+            "one_core": b["one_core"], "all_cores": b["all_cores"],
+            "note": "not re-measured in this run: the committed whole-workload oracle timing of the same "
+                    "graph (seed 0), sum over exact cluster windows"}
+
+
 def emit(line, args):
     s = json.dumps(line)
     print(s, flush=True)
@@ -434,9 +466,12 @@ def run_ours(args):
         ns = min(args.cpu_sample_rows, N)
         dt, _ = oracle_sample(W["nbr"][:ns].cpu().numpy(), W["dist"][:ns].cpu().numpy(), M, eps_list, ec)
         cpu = {"value": ns * k * F / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
-               "cpu_model": host_cpu()[0], "box_cores": host_cpu()[1],
+               "cpu_model": host_cpu()[0], "box_cores": host_cpu()[1], "host_ram_gb": host_ram_gb(),
                "sample": f"rows [0, {ns}) of the workload ({ns * k} entries; entries to ids >= {ns} skipped), "
                          f"one single-threaded run, {dt:.1f} s"}
+        whole = whole_workload_baseline(args.config, args.scale, ec, len(eps_list))
+        if whole:
+            cpu["whole_workload_measured"] = whole
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
