@@ -1,6 +1,6 @@
 """Write profiles/ncu_traffic.json (per-launch DRAM bytes per kernel, averaged
 over the captured launches) and a readable summary from an ncu --set full report.
-usage: python tools/ncu_traffic.py <summary.txt> <report.ncu-rep> [<report2.ncu-rep> ...]"""
+usage: python tools/ncu_traffic.py <summary.txt> <report.ncu-rep | raw.csv> [...]"""
 import csv
 import json
 import os
@@ -19,7 +19,10 @@ KEYS = ['gpu__time_duration.sum', 'dram__bytes_read.sum', 'dram__bytes_write.sum
 def main(out, reps):
   agg, lines, srcs = {}, [], {}
   for rep in reps:
-    raw = subprocess.run(['ncu', '-i', rep, '--page', 'raw', '--csv'], capture_output=True, text=True).stdout
+    if rep.endswith('.csv'):  # a raw page already exported on the GPU box (ncu -i rep --page raw --csv)
+        raw = open(rep).read()
+    else:
+        raw = subprocess.run(['ncu', '-i', rep, '--page', 'raw', '--csv'], capture_output=True, text=True).stdout
     rows = list(csv.reader(raw.splitlines()))
     hdr, units = rows[0], rows[1]
     for r in rows[2:]:
