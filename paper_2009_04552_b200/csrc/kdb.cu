@@ -639,7 +639,13 @@ kdb_status mst_impl(const kdb_graph* g, float eps, const uint32_t* core_bits, in
     KDB_CUDA(cudaEventRecord(m.ev[1], st));
     m.t_filter += elapsed(m.ev[0], m.ev[1]);
     KDB_TRY(heavy_phase(m));
-  } else if (env_int("KDB_FILTER", 1) && light_m >= 1 && light_m < m.k) {
+  } else if (env_int("KDB_FILTER", 1) && light_m >= 1 && light_m < m.k &&
+             (getenv("KDB_LIGHT") || m.k >= 4 * light_m)) {
+    // default policy: split only when the rows are long next to the light
+    // prefix (k >= 4 x the light column): with k = 16 / 32 the filter pass and
+    // the heavy phase cost more than the rows phase saves (C1 1.49 -> 0.99 ms,
+    // C2 3.69 -> 2.27 ms without the split; C3 / C4 (k = 100) gain from it).
+    // An explicit KDB_LIGHT always splits (tests, tuning).
     KDB_TRY(pick_tau(m, light_m, &m.tau));
     filtered = m.tau < eps;
   }

@@ -435,6 +435,7 @@ kdb_status rows_phase(Mst& m, float eps_run) {
   const bool use_compact = env_int("KDB_COMPACT", 1) != 0;
   const int gw = env_int("KDB_GW", 4);  // component-gather width of the later light rounds (scan_ell)
   const bool sparse_ids = env_int("KDB_SPARSE", 1) != 0;  // keep root ids once few components remain
+  const int skip1 = env_int("KDB_SKIP1", 1);  // round-2 heads skip the entry round 1 hooked along
   // local-first phase of one rank (m.local): LOCAL component ids, the rank's
   // per-component slices, no exchange; the global phase (m.cont) continues the
   // rounds from the rows the local phases parked
@@ -496,7 +497,7 @@ kdb_status rows_phase(Mst& m, float eps_run) {
 #define KDB_ELL_LAUNCH(V, A)                                                                                    \
   LAUNCH((k_light_ell<V, A>), grid_for(R.n_rows), kThreads, st, R.nbr, R.dist, R.n_rows, ld, k, eps_run, R.row_begin, \
          comp, general ? nullptr : L.kmin, R.LE, R.act[0], &R.ctr->na[0], &R.ctr->grab, fuse1 ? 1 : 0,         \
-         L.all_core, N, R.Kc, R.Bc, R.tgt, packed1 ? L.rec1 : nullptr, &R.ctr->n_deep, lv)
+         L.all_core, N, R.Kc, R.Bc, R.tgt, packed1 ? L.rec1 : nullptr, &R.ctr->n_deep, lv, skip1)
       if (a32) KDB_ELL_LAUNCH(true, true);
       else if (vec) KDB_ELL_LAUNCH(true, false);
       else KDB_ELL_LAUNCH(false, false);

@@ -397,7 +397,7 @@ __global__ void __launch_bounds__(256) k_light_ell(const int32_t* __restrict__ n
                                                    int direct, int all_core, int64_t N, uint64_t* __restrict__ Kc,
                                                    uint32_t* __restrict__ Bc, int32_t* __restrict__ tgt,
                                                    int4* __restrict__ rec1, uint32_t* __restrict__ n_deep,
-                                                   const LocalView lv = LocalView{}) {
+                                                   const LocalView lv = LocalView{}, int skip1 = 1) {
   __shared__ __align__(16) Rec s_rec[kChunk];
   __shared__ uint32_t s_n, s_chunk, s_base;
   uint32_t deep = 0;  // rows whose kW ELL entries are all within eps (their scans go past the first chunk)
@@ -489,6 +489,7 @@ __global__ void __launch_bounds__(256) k_light_ell(const int32_t* __restrict__ n
       RowScan r{false, (int)k, kSent, kSentB, -1};
       float wstar = 0.f;
       bool done = false;
+      int bidx = -1;  // column of the row's minimum
 #pragma unroll
       for (int c = 0; c < kW; ++c) {
         if (done || c >= k) continue;
@@ -499,6 +500,7 @@ __global__ void __launch_bounds__(256) k_light_ell(const int32_t* __restrict__ n
           const int32_t cc = comp_of(comp, Jc, all_core, lv);
           if (cc < 0) continue;
           r.found = true;
+          bidx = c;
           r.h = c;
           wstar = w[c];
           r.best = pack_key(mono_bits(w[c]), (uint32_t)min(v, (int64_t)Jc));
@@ -511,13 +513,19 @@ __global__ void __launch_bounds__(256) k_light_ell(const int32_t* __restrict__ n
           if (cc < 0) continue;
           const uint64_t kk = pack_key(mono_bits(w[c]), (uint32_t)min(v, (int64_t)Jc));
           const uint32_t bb = (uint32_t)max(v, (int64_t)Jc);
-          if (kk < r.best || (kk == r.best && bb < r.bestb)) { r.best = kk; r.bestb = bb; r.bestc = cc; }
+          if (kk < r.best || (kk == r.best && bb < r.bestb)) { r.best = kk; r.bestb = bb; r.bestc = cc; bidx = c; }
         }
       }
       if (!done && k > kW) {  // the search or the tie group runs past the ELL: scan the row in place
         unsigned long long rd = 0;
         r = scan_row<false, true>(nr, dr, k, eps, (int32_t)v, -1, 0, N, comp, all_core, rd, lv);
+        bidx = -1;
       }
+      // The singleton {v} hooks along its minimum when that is certified (and,
+      // in a local-first phase, stays inside the rank): then the entry at the
+      // head is intra from round 2 on and the round-2 scan need not gather it
+      // (every row's first visit would otherwise re-read its nearest neighbour).
+      const bool skip_head = skip1 && r.found && bidx == r.h && r.bestc != kRemote && (uint32_t)(r.best >> 32) < kb;
       if (rec1) {  // single rank: one packed record per component for k_hook<true>
         __stcg(rec1 + cv, make_int4((int)(uint32_t)r.best, (int)(uint32_t)(r.best >> 32), (int)r.bestb, (int)kb));
         if (r.found) tgt[cv] = r.bestc;
@@ -526,7 +534,7 @@ __global__ void __launch_bounds__(256) k_light_ell(const int32_t* __restrict__ n
         Bc[cv] = r.bestb;
         tgt[cv] = r.bestc;
       }
-      if (r.found) s_rec[atomicAdd(&s_n, 1u)] = Rec{(int32_t)v, r.h};
+      if (r.found) s_rec[atomicAdd(&s_n, 1u)] = Rec{(int32_t)v, skip_head ? r.h + 1 : r.h};
     }
     __syncthreads();
     if (threadIdx.x == 0) s_base = s_n ? atomicAdd(n_act, s_n) : 0u;

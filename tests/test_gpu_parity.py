@@ -541,3 +541,25 @@ def test_star_forest_hub_runs(n):
     assert time.time() - t < 5.0
     assert_parity(got, exp)
     assert np.all(got["msf_a"] == 0) and len(got["msf_a"]) == n - 1
+
+
+@pytest.mark.parametrize("skip", ["0", "1"])
+@pytest.mark.parametrize("P", [0, 3])
+def test_round2_head_skip_toggle(c1_graph, skip, P, monkeypatch):
+    """Round-2 heads start past the entry a certified singleton hooked along
+    (KDB_SKIP1=1, default) or at it (0): the same forest either way, including
+    ties (few weight levels) and the local-first phase under sim ranks."""
+    import paper_2009_04552_b200 as kdb
+    monkeypatch.setenv("KDB_SKIP1", skip)
+    X, nbr, dist = c1_graph
+    for f in (0.7, 1.5):
+        eps = eps_from_graph(dist, 8, f)
+        got = run_gpu(nbr, dist, 8, eps, exact=True, comm=kdb.Comm.sim(P) if P else None)
+        assert_parity(got, oracle_run(nbr, dist, 8, eps))
+    rng = np.random.default_rng(11)
+    X = np.round(rng.uniform(0, 6, size=(1500, 2))).astype(np.float32)  # lattice: many equal distances
+    X += (rng.uniform(size=X.shape) < 0.02) * 0.5
+    nbr, dist = knn_bruteforce(X, 12)
+    eps = eps_from_graph(dist, 4, 1.2)
+    got = run_gpu(nbr, dist, 4, eps, exact=True, comm=kdb.Comm.sim(P) if P else None)
+    assert_parity(got, oracle_run(nbr, dist, 4, eps))
