@@ -557,7 +557,7 @@ def test_round2_head_skip_toggle(c1_graph, skip, P, monkeypatch):
         got = run_gpu(nbr, dist, 8, eps, exact=True, comm=kdb.Comm.sim(P) if P else None)
         assert_parity(got, oracle_run(nbr, dist, 8, eps))
     rng = np.random.default_rng(11)
-    X = np.round(rng.uniform(0, 6, size=(1500, 2))).astype(np.float32)  # lattice: many equal distances
+    X = np.round(rng.uniform(0, 30, size=(1500, 2))).astype(np.float32)  # lattice: many equal distances
     X += (rng.uniform(size=X.shape) < 0.02) * 0.5
     nbr, dist = knn_bruteforce(X, 12)
     eps = eps_from_graph(dist, 4, 1.2)
