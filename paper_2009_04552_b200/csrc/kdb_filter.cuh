@@ -71,11 +71,12 @@ constexpr size_t kFilterSmem = kBloomBits / 8 + (size_t)kFilterWarps * kFilterRo
 // two more instructions per entry: filter 7.18 -> 6.92 ms).
 __device__ __forceinline__ uint32_t bloom_hash(uint32_t x) { return x * 0x9E3779B1u; }
 __device__ __forceinline__ uint32_t bloom_word_h(uint32_t h) { return h >> 17; }
-// The word's mask: two fixed 2-bit patterns rotated by bits [0,5) and [5,10)
-// of h (a rotate is one funnel shift): 2-4 bits set, 4 instructions.
+// The word's mask: one fixed 3-bit pattern (bits 0, 10, 21: the 32 rotations
+// are distinct) rotated by bits [0,5) of h -- one funnel shift per key.  The
+// filter is issue-bound; the mask is on its per-entry path.
 __device__ __forceinline__ uint32_t bloom_mask_h(uint32_t h) {
-  constexpr uint32_t P1 = 1u | (1u << 11), P2 = 1u | (1u << 19);
-  return __funnelshift_l(P1, P1, h) | __funnelshift_l(P2, P2, h >> 5);
+  constexpr uint32_t P = 1u | (1u << 10) | (1u << 21);
+  return __funnelshift_l(P, P, h);
 }
 __device__ __forceinline__ uint32_t bloom_word(uint32_t x) { return bloom_word_h(bloom_hash(x)); }
 __device__ __forceinline__ uint32_t bloom_mask(uint32_t x) { return bloom_mask_h(bloom_hash(x)); }
@@ -165,7 +166,7 @@ struct FRow {
 // COLS (edge_cols < row stride ld): only columns < k are candidates; the sweep
 // enumerates just the ceil(k / VEC) chunks at the head of each row (fd then
 // divides by that count), so columns >= k cost neither loads nor issue slots.
-template <int VEC, bool FAST, bool COLS>
+template <int VEC, bool FAST, bool COLS, bool SMALL = false>
 __global__ void __launch_bounds__(kFilterThreads) k_filter(
     const int32_t* __restrict__ nbr, const float* __restrict__ dist, int64_t n_rows, int32_t ld, int32_t k, float tau, float eps,
     int64_t row_begin, int64_t N, const int32_t* __restrict__ comp, const int2* __restrict__ rng, const uint32_t* __restrict__ bloom, FastDiv fd,
@@ -214,7 +215,7 @@ __global__ void __launch_bounds__(kFilterThreads) k_filter(
         const uint32_t u = min(base + t * 32 + lane, n_chunks - 1);
         uint32_t off = u;  // chunk offset from the tile start
         if (COLS) {
-          const uint32_t lr = fd.small ? __umulhi(u, fd.m32) : (uint32_t)fdiv(u, fd);
+          const uint32_t lr = SMALL ? __umulhi(u, fd.m32) : (uint32_t)fdiv(u, fd);
           off = lr * (uint32_t)(ld / VEC) + (u - lr * cpr);
         }
 #if KDB_FILTER_PREFETCH
@@ -239,12 +240,12 @@ __global__ void __launch_bounds__(kFilterThreads) k_filter(
         float w[VEC];
         if (u < n_chunks) {
           if (COLS) {
-            lr = fd.small ? __umulhi(u, fd.m32) : (uint32_t)fdiv(u, fd);  // row within the tile
+            lr = SMALL ? __umulhi(u, fd.m32) : (uint32_t)fdiv(u, fd);  // row within the tile
             col = (u - lr * cpr) * VEC;
             off = lr * (uint32_t)(ld / VEC) + (u - lr * cpr);
           } else {
             const uint32_t n = u * VEC;
-            lr = fd.small ? __umulhi(n, fd.m32) : (uint32_t)fdiv(n, fd);  // row within the tile
+            lr = SMALL ? __umulhi(n, fd.m32) : (uint32_t)fdiv(n, fd);  // row within the tile
             col = n - lr * (uint32_t)ld;
           }
           const FRow fr = s_row[lr];

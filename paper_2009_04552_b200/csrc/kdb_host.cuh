@@ -1170,9 +1170,16 @@ kdb_status filter_phase(Mst& m, float eps, bool* overflow) {
     fd.small = (fd.d > 1 && fd.d * fd.d * (uint64_t)kFilterRows < (1ull << 32)) ? 1u : 0u;
     const int64_t ntiles = (R.n_rows + kFilterRows - 1) / kFilterRows;  // warp tiles
     const int grid = (int)std::min<int64_t>((ntiles + kFilterWarps - 1) / kFilterWarps, 1 << 30);
-#define KDB_FILTER_LAUNCH(V, F, CO)                                                                              \
-  LAUNCH_DYN((k_filter<V, F, CO>), grid, kFilterThreads, kFilterSmem, st, R.nbr, R.dist, R.n_rows, m.ld, m.k,      \
+#define KDB_FILTER_LAUNCH2(V, F, CO, SM)                                                                         \
+  LAUNCH_DYN((k_filter<V, F, CO, SM>), grid, kFilterThreads, kFilterSmem, st, R.nbr, R.dist, R.n_rows, m.ld, m.k,  \
              m.tau, eps, R.row_begin, m.N, m.comp, rng, L.bloom, fd, R.hs[0], R.hs_cap, R.n_hs_dev, L.fcount + 1)
+  // the row-within-tile division: a 32-bit multiply-high when exact (compile-time
+  // branch: it runs once per 16-B chunk of the sweep)
+#define KDB_FILTER_LAUNCH(V, F, CO)                                                                              \
+  do {                                                                                                           \
+    if (fd.small) KDB_FILTER_LAUNCH2(V, F, CO, true);                                                          \
+    else KDB_FILTER_LAUNCH2(V, F, CO, false);                                                                  \
+  } while (0)
     if (cols) {
       if (vec == 4 && fast) KDB_FILTER_LAUNCH(4, true, true);
       else if (vec == 4) KDB_FILTER_LAUNCH(4, false, true);
@@ -1185,6 +1192,7 @@ kdb_status filter_phase(Mst& m, float eps, bool* overflow) {
       else KDB_FILTER_LAUNCH(1, false, false);
     }
 #undef KDB_FILTER_LAUNCH
+#undef KDB_FILTER_LAUNCH2
     KDB_CUDA(cudaGetLastError());
   }
   uint32_t over = 0;
