@@ -436,6 +436,7 @@ kdb_status rows_phase(Mst& m, float eps_run) {
   const int gw = env_int("KDB_GW", 4);  // component-gather width of the later light rounds (scan_ell)
   const bool sparse_ids = env_int("KDB_SPARSE", 1) != 0;  // keep root ids once few components remain
   const int skip1 = env_int("KDB_SKIP1", 1);  // round-2 heads skip the entry round 1 hooked along
+  const int l2hint = env_int("KDB_L2HINT", 0);  // evict-last policy on the light rounds' component gathers
   // local-first phase of one rank (m.local): LOCAL component ids, the rank's
   // per-component slices, no exchange; the global phase (m.cont) continues the
   // rounds from the rows the local phases parked
@@ -710,7 +711,7 @@ kdb_status rows_phase(Mst& m, float eps_run) {
   LAUNCH((k_light_round<__VA_ARGS__>), grid_for(na_ub[r]), kThreads, st, R.LE, R.nbr, R.dist, ld, k, eps_run,       \
          R.row_begin, N, comp, R.act[cur], na_ub[r], R.act[cur ^ 1], nout, &R.ctr->grab, R.offers,                 \
          (unsigned long long*)R.Kc, &L.ctr->entries, nin, precheck, KB, lv, (const uint8_t*)frz, R.park,         \
-         m.local ? &L.ctr->n_park : nullptr)
+         m.local ? &L.ctr->n_park : nullptr, l2hint)
           // pipelined chunk loads pay when many rows scan past their first chunk
           // (C3: its inner shell is all light); they cost occupancy otherwise
           const int pk = env_int("KDB_PIPE", -1);

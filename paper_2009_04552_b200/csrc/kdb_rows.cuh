@@ -220,13 +220,24 @@ constexpr int32_t kRemote = 0x7fffffff;
 struct LocalView {
   int64_t lo = 0, hi = 0;
   const uint32_t* bits = nullptr;
+  uint64_t pol = 0;  // L2 cache policy for the component gathers (0: default)
 };
+__device__ __forceinline__ uint64_t l2_evict_last_policy() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ int32_t gat_hint(const int32_t* p, uint64_t pol) {
+  int32_t r;
+  asm volatile("ld.global.cg.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(pol));
+  return r;
+}
 // component of far endpoint J (< 0: not a candidate, i.e. non-core); direct:
 // singleton components whose dense id is the vertex's position in the view
 __device__ __forceinline__ int32_t comp_of(const int32_t* __restrict__ comp, int64_t J, bool direct,
                                            const LocalView& lv) {
   if (lv.bits && (J < lv.lo || J >= lv.hi)) return is_core(lv.bits, J) ? kRemote : -1;
-  return direct ? (int32_t)(J - lv.lo) : gat(comp + J);
+  return direct ? (int32_t)(J - lv.lo) : (lv.pol ? gat_hint(comp + J, lv.pol) : gat(comp + J));
 }
 
 // Scan row (nr, dr) of vertex v (component cv) from head h.  direct: singleton
@@ -711,8 +722,10 @@ __global__ void __launch_bounds__(256) k_light_round(const int4* __restrict__ LE
                                                      const LocalView lv = LocalView{},
                                                      const uint8_t* __restrict__ frz = nullptr,
                                                      Rec* __restrict__ park = nullptr,
-                                                     uint32_t* __restrict__ n_park = nullptr) {
+                                                     uint32_t* __restrict__ n_park = nullptr, int l2hint = 0) {
   if (n_in_p) n_in = *n_in_p;
+  LocalView lvh = lv;
+  if (l2hint) lvh.pol = l2_evict_last_policy();  // keep the component gathers' lines over the streams
   __shared__ __align__(16) Rec s_rec[kChunk];
   __shared__ __align__(16) Offer s_off[CAS ? 1 : kChunk];
   __shared__ uint32_t s_n, s_chunk, s_base;
@@ -743,7 +756,7 @@ __global__ void __launch_bounds__(256) k_light_round(const int4* __restrict__ LE
       }
       const int64_t i = (int64_t)v - row_begin;
       const RowScan r = scan_ell<false, GW, PIPE>(LE + i * (kW / 2), nbr + i * ld, dist + i * ld, k, eps, v, cv, a.y,
-                                                  N, comp, 0, reads, lv);
+                                                  N, comp, 0, reads, lvh);
       if (r.found) {
         const uint32_t j = atomicAdd(&s_n, 1u);
         s_rec[j] = Rec{v, r.h};
