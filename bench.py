@@ -278,6 +278,24 @@ def host_cpu():
     return model, os.cpu_count()
 
 
+def dram_budget(args, ec, eps_list):
+    """DRAM bytes of one whole step summed over every kernel (ncu, committed:
+    profiles/r02/dram_budget_c4.txt, tools/dram_budget.py) against the
+    algorithmic bytes -- quoted for the default C4 step, not measured here."""
+    if args.config != "C4" or args.scale != 1.0 or ec or len(eps_list) != 1:
+        return None
+    path = os.path.join(ROOT, "profiles", "r02", "dram_budget_c4.txt")
+    if not os.path.exists(path):
+        return None
+    last = [l for l in open(path) if l.startswith("total")]
+    if not last:
+        return None
+    f = last[-1].split()
+    return {"source": os.path.relpath(path, ROOT), "dram_gb_per_step": float(f[2]),
+            "algorithmic_gb": round((8.0 * 64e6 * 100 + 4.0 * 64e6 + 64e6 / 8) / 1e9, 2),
+            "ratio": float(f[-1])}
+
+
 def host_ram_gb():
     try:
         for line in open("/proc/meminfo"):
@@ -488,6 +506,7 @@ def run_ours(args):
                 "stage_roofline": {"t_min_ms": t_min_ms, "frac": t_min_ms / ms,
                                    "bytes": "8 N k + 4 N + N/8 (SURVEY.md 8(d))", "peak": peak},
                 "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "quality": quality,
+                **({"dram_budget": dram_budget(args, ec, eps_list)} if dram_budget(args, ec, eps_list) else {}),
                 **({"inexact": inexact} if inexact else {}),
                 "clocks": clk, "kernels": kernels,
                 "mst": {"edges": msf_count, "weight": msf_weight, "clusters": n_clusters,
