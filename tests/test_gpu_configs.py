@@ -5,7 +5,8 @@ configuration bench.py times (pytest -m gpu).
   with the CPU oracle on the whole workload (north_star: "labels and MST
   bit-identical to the oracle on all five configs").
 * C4 (64M x 3-D, k=100) and C5 (5-D; 1/16 of its 256M points on one GPU): the
-  oracle cannot run at that size in a test, so (i) exact parity on the induced
+  element-by-element oracle parity at full size is tests/test_gpu_windows.py
+  (exact cluster windows); here (i) exact parity on the induced
   subgraph of the first rows (the same data distribution, entries to ids beyond
   the sample masked to padding), (ii) properties that hold at any size, checked
   on every vertex/edge, and (iii) bit-identical outputs from independent code
