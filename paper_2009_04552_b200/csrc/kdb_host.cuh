@@ -416,6 +416,12 @@ kdb_status pick_tau(Mst& m, int m0, float* tau_out) {
 
 kdb_status local_first(Mst& m, float eps_run);
 
+// Records per block chunk of the ordered row kernels (and components per hook
+// chunk): kChunk = 1024 for long lists; short lists use smaller chunks so a
+// thread scans one record instead of four in sequence (small inputs are
+// latency-bound: C1's light rounds took ~40 us each with 1,024-record chunks)
+inline int row_chunk(uint64_t n) { return n >= (1ull << 21) ? kChunk : n >= (1ull << 19) ? 512 : 256; }
+
 // a2-a8: rows-Boruvka over the candidate entries with w <= eps_run (from
 // singletons).  Leaves comp[] = dense component ids (0..C-1), L.cmin = minimum
 // core id per component, m.C.  Resets the MSF counter.
@@ -498,7 +504,8 @@ kdb_status rows_phase(Mst& m, float eps_run) {
 #define KDB_ELL_LAUNCH(V, A)                                                                                    \
   LAUNCH((k_light_ell<V, A>), grid_for(R.n_rows), kThreads, st, R.nbr, R.dist, R.n_rows, ld, k, eps_run, R.row_begin, \
          comp, general ? nullptr : L.kmin, R.LE, R.act[0], &R.ctr->na[0], &R.ctr->grab, fuse1 ? 1 : 0,         \
-         L.all_core, N, R.Kc, R.Bc, R.tgt, packed1 ? L.rec1 : nullptr, &R.ctr->n_deep, lv, skip1)
+         L.all_core, N, R.Kc, R.Bc, R.tgt, packed1 ? L.rec1 : nullptr, &R.ctr->n_deep, lv, skip1,               \
+         row_chunk((uint64_t)R.n_rows))
       if (a32) KDB_ELL_LAUNCH(true, true);
       else if (vec) KDB_ELL_LAUNCH(true, false);
       else KDB_ELL_LAUNCH(false, false);
@@ -608,25 +615,22 @@ kdb_status rows_phase(Mst& m, float eps_run) {
   auto contract = [&](int64_t C_bound) -> kdb_status {
     const int64_t* Cd = (const int64_t*)&L.ctr->Cs[par];
     int64_t* Cn = (int64_t*)&L.ctr->Cs[par ^ 1];
-    LAUNCH(k_jump, grid_for(C_bound), kThreads, st, C_bound, L.parent, L.rootof, L.ctr, Cd);
     // sparse ids once few components remain: a component keeps its root's id
     // (no dense renumbering; the id range stays C_bound), so the relabel only
     // rewrites the vertices of merged components
     const bool sparse = sparse_ids && C_bound <= N / 64;
+    LAUNCH(k_jump, grid_for(C_bound), kThreads, st, C_bound, L.parent, L.rootof, L.ctr, Cd,
+           sparse ? (int32_t*)nullptr : L.flag);
     if (!sparse) {
-      LAUNCH(k_root_flags, grid_for(C_bound), kThreads, st, C_bound, L.rootof, L.flag, Cd);
       size_t cb2 = L.cub_bytes;
       { LaunchScope ls_("cub::DeviceScan", st, false); KDB_CUDA(cub::DeviceScan::ExclusiveSum(L.cub_tmp, cb2, L.flag, L.newid, (int)std::max<int64_t>(C_bound, 1), st)); }
-      LAUNCH(k_count_roots, 1, 1, st, Cd, L.newid, L.flag, Cn);
-    } else {
-      KDB_CUDA(cudaMemcpyAsync(Cn, Cd, sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
     }
-    LAUNCH(k_fill_i32, grid_for(C_bound), kThreads, st, L.cmin2, C_bound, INT32_MAX, (const int64_t*)Cn);
-    if (!general)
-      LAUNCH(k_fill_i32, grid_for(C_bound), kThreads, st, (int32_t*)L.kmin2, C_bound, (int32_t)kInfBits,
-             (const int64_t*)Cn);
+    // new count + next round's slots (cmin2 / kmin2 before k_merge; the offer
+    // slots are free: the hook has read them)
+    LAUNCH(k_round_fill, grid_for(C_bound), kThreads, st, C_bound, Cd, sparse ? (const int32_t*)nullptr : L.newid,
+           (const int32_t*)L.flag, Cn, L.cmin2, general ? (uint32_t*)nullptr : L.kmin2, L.Kc, L.Bc, KB,
+           frz ? L.frz2 : (uint8_t*)nullptr);
     // map[c] = new dense id of c's tree (reuses `parent`, no longer needed)
-    if (frz) KDB_CUDA(cudaMemsetAsync(L.frz2, 0, (size_t)std::max<int64_t>(C_bound, 1), st));
     LAUNCH(k_merge, grid_for(C_bound), kThreads, st, C_bound, L.rootof, sparse ? (const int32_t*)nullptr : L.newid,
            L.cmin, general ? nullptr : L.kmin, L.cmin2, L.kmin2, L.parent, Cd, (const uint8_t*)frz,
            frz ? L.frz2 : nullptr);
@@ -635,7 +639,6 @@ kdb_status rows_phase(Mst& m, float eps_run) {
              (const int32_t*)nullptr);
     else
       LAUNCH(k_relabel, grid_for(N / 8 + 1), kThreads, st, N, comp, L.parent, (const int32_t*)nullptr);
-    LAUNCH(k_fill_comp_arrays, grid_for(C_bound), kThreads, st, C_bound, L.Kc, L.Bc, nullptr, (const int64_t*)Cn, KB);
     for (size_t r = 1; r < nr; ++r)
       LAUNCH(k_fill_comp_arrays, grid_for(C_bound), kThreads, st, C_bound, L.ranks[r].Kc, L.ranks[r].Bc, nullptr,
              (const int64_t*)Cn);
@@ -666,10 +669,12 @@ kdb_status rows_phase(Mst& m, float eps_run) {
     ++rounds;
     const bool direct = rounds == 1 && !general && !m.cont;
     const int64_t* Cd = (const int64_t*)&L.ctr->Cs[par];
-    cudaEvent_t e0;
-    KDB_CUDA(cudaEventCreate(&e0));
-    ev_rnd.push_back(e0);
-    KDB_CUDA(cudaEventRecord(e0, st));
+    if (ev_rnd.empty()) {  // the phase's start (rounds are pipelined: timed as one span)
+      cudaEvent_t e0;
+      KDB_CUDA(cudaEventCreate(&e0));
+      ev_rnd.push_back(e0);
+      KDB_CUDA(cudaEventRecord(e0, st));
+    }
     // offers read the current key before their atomicMin once many rows offer
     // to each component (same-address atomics serialise; early rounds have
     // about one row per component and only pay the extra read)
@@ -704,14 +709,14 @@ kdb_status rows_phase(Mst& m, float eps_run) {
         if (direct)
           LAUNCH(k_light_first, grid_for(na_ub[r]), kThreads, st, R.LE, R.nbr, R.dist, ld, k, eps_run, R.row_begin, N,
                  comp, L.all_core, R.act[cur], na_ub[r], R.act[cur ^ 1], nout, &R.ctr->grab, R.Kc, R.Bc, R.tgt,
-                 &L.ctr->entries, nin);
+                 &L.ctr->entries, nin, row_chunk(na_ub[r]));
         else
         {
 #define KDB_LR_LAUNCH(...)                                                                                       \
   LAUNCH((k_light_round<__VA_ARGS__>), grid_for(na_ub[r]), kThreads, st, R.LE, R.nbr, R.dist, ld, k, eps_run,       \
          R.row_begin, N, comp, R.act[cur], na_ub[r], R.act[cur ^ 1], nout, &R.ctr->grab, R.offers,                 \
          (unsigned long long*)R.Kc, &L.ctr->entries, nin, precheck, KB, lv, (const uint8_t*)frz, R.park,         \
-         m.local ? &L.ctr->n_park : nullptr, l2hint)
+         m.local ? &L.ctr->n_park : nullptr, l2hint, row_chunk(na_ub[r]))
           // pipelined chunk loads pay when many rows scan past their first chunk
           // (C3: its inner shell is all light); they cost occupancy otherwise
           const int pk = env_int("KDB_PIPE", -1);
@@ -789,11 +794,11 @@ kdb_status rows_phase(Mst& m, float eps_run) {
     KDB_CUDA(cudaMemsetAsync(&L.ctr->hooks, 0, 4 * sizeof(uint32_t), st));
     if (direct && packed1)
       LAUNCH(k_hook<true>, grid_for(C_ub), kThreads, st, C_ub, L.Kc, L.Bc, L.tgt, kmin_cert, comp, L.parent, L.e_key,
-             L.e_w, ecap, L.ctr, Cd, L.rec1, (const ulonglong2*)nullptr, frz);
+             L.e_w, ecap, L.ctr, Cd, L.rec1, (const ulonglong2*)nullptr, frz, row_chunk((uint64_t)C_ub));
     else
       LAUNCH(k_hook<false>, grid_for(C_ub), kThreads, st, C_ub, L.Kc, L.Bc, direct ? L.tgt : nullptr, kmin_cert,
              comp, L.parent, L.e_key, L.e_w, ecap, L.ctr, Cd, (const int4*)nullptr,
-             (cas && !direct) ? (const ulonglong2*)KB : nullptr, frz);
+             (cas && !direct) ? (const ulonglong2*)KB : nullptr, frz, row_chunk((uint64_t)C_ub));
     KDB_CUDA(cudaGetLastError());
     // a6: contract (no hooks => identity)
     KDB_TRY(contract(C_ub));
@@ -1278,8 +1283,7 @@ kdb_status heavy_phase(Mst& m) {
     KDB_CUDA(cudaStreamSynchronize(st));
     if (hc.offered == 0) break;
     if (hc.hooks == 0) return set_err(KDB_EINTERNAL, "heavy phase made no progress");
-    LAUNCH(k_jump, grid_for(C), kThreads, st, C, L.parent, L.rootof, L.ctr);
-    LAUNCH(k_root_flags, grid_for(C), kThreads, st, C, L.rootof, L.flag);
+    LAUNCH(k_jump, grid_for(C), kThreads, st, C, L.parent, L.rootof, L.ctr, (const int64_t*)nullptr, L.flag);
     size_t cb = L.cub_bytes;
     { LaunchScope ls_("cub::DeviceScan", st, false); KDB_CUDA(cub::DeviceScan::ExclusiveSum(L.cub_tmp, cb, L.flag, L.newid, (int)C, st)); }
     uint32_t viol = 0;

@@ -408,16 +408,17 @@ __global__ void __launch_bounds__(256) k_light_ell(const int32_t* __restrict__ n
                                                    int direct, int all_core, int64_t N, uint64_t* __restrict__ Kc,
                                                    uint32_t* __restrict__ Bc, int32_t* __restrict__ tgt,
                                                    int4* __restrict__ rec1, uint32_t* __restrict__ n_deep,
-                                                   const LocalView lv = LocalView{}, int skip1 = 1) {
+                                                   const LocalView lv = LocalView{}, int skip1 = 1,
+                                                   int chunk = kChunk) {
   __shared__ __align__(16) Rec s_rec[kChunk];
   __shared__ uint32_t s_n, s_chunk, s_base;
   uint32_t deep = 0;  // rows whose kW ELL entries are all within eps (their scans go past the first chunk)
   for (;;) {
     if (threadIdx.x == 0) { s_chunk = atomicAdd(grab, 1u); s_n = 0; }
     __syncthreads();
-    const int64_t base = (int64_t)s_chunk * kChunk;
+    const int64_t base = (int64_t)s_chunk * chunk;
     if (base >= n_rows) break;
-    for (int t = 0; t < kChunk; t += 256) {
+    for (int t = 0; t < chunk; t += 256) {
       const int64_t i = base + t + threadIdx.x;
       if (i >= n_rows) continue;
       const int64_t v = row_begin + i;
@@ -670,7 +671,8 @@ __global__ void __launch_bounds__(256) k_light_first(const int4* __restrict__ LE
                                                      Rec* __restrict__ act_out, uint32_t* __restrict__ n_out,
                                                      uint32_t* __restrict__ grab,
                                                      uint64_t* __restrict__ Kc, uint32_t* __restrict__ Bc,
-                                                     int32_t* __restrict__ tgt, unsigned long long* __restrict__ n_entries, const uint32_t* __restrict__ n_in_p = nullptr) {
+                                                     int32_t* __restrict__ tgt, unsigned long long* __restrict__ n_entries, const uint32_t* __restrict__ n_in_p = nullptr,
+                                                     int chunk = kChunk) {
   if (n_in_p) n_in = *n_in_p;
   __shared__ __align__(16) Rec s_rec[kChunk];
   __shared__ uint32_t s_n, s_chunk, s_base;
@@ -678,9 +680,9 @@ __global__ void __launch_bounds__(256) k_light_first(const int4* __restrict__ LE
   for (;;) {
     if (threadIdx.x == 0) { s_chunk = atomicAdd(grab, 1u); s_n = 0; }
     __syncthreads();
-    const uint64_t base = (uint64_t)s_chunk * kChunk;
+    const uint64_t base = (uint64_t)s_chunk * chunk;
     if (base >= n_in) break;
-    for (int t = 0; t < kChunk; t += 256) {
+    for (int t = 0; t < chunk; t += 256) {
       const uint64_t s = base + t + threadIdx.x;
       if (s >= n_in) continue;
       const int2 a = __ldcs(reinterpret_cast<const int2*>(act + s));
@@ -722,7 +724,8 @@ __global__ void __launch_bounds__(256) k_light_round(const int4* __restrict__ LE
                                                      const LocalView lv = LocalView{},
                                                      const uint8_t* __restrict__ frz = nullptr,
                                                      Rec* __restrict__ park = nullptr,
-                                                     uint32_t* __restrict__ n_park = nullptr, int l2hint = 0) {
+                                                     uint32_t* __restrict__ n_park = nullptr, int l2hint = 0,
+                                                     int chunk = kChunk) {
   if (n_in_p) n_in = *n_in_p;
   LocalView lvh = lv;
   if (l2hint) lvh.pol = l2_evict_last_policy();  // keep the component gathers' lines over the streams
@@ -733,9 +736,9 @@ __global__ void __launch_bounds__(256) k_light_round(const int4* __restrict__ LE
   for (;;) {
     if (threadIdx.x == 0) { s_chunk = atomicAdd(grab, 1u); s_n = 0; }
     __syncthreads();
-    const uint64_t base = (uint64_t)s_chunk * kChunk;
+    const uint64_t base = (uint64_t)s_chunk * chunk;
     if (base >= n_in) break;
-    for (int t = 0; t < kChunk; t += 256) {
+    for (int t = 0; t < chunk; t += 256) {
       const uint64_t s = base + t + threadIdx.x;
       if (s >= n_in) continue;
       const int2 a = __ldcs(reinterpret_cast<const int2*>(act + s));
@@ -926,7 +929,7 @@ __global__ void __launch_bounds__(256) k_hook(int64_t C, const uint64_t* __restr
                        uint64_t* __restrict__ e_key, float* __restrict__ e_w, int64_t e_cap,
                        RoundCounters* __restrict__ ctr, const int64_t* __restrict__ Cp,
                        const int4* __restrict__ rec1, const ulonglong2* __restrict__ KB = nullptr,
-                       uint8_t* __restrict__ frz = nullptr) {
+                       uint8_t* __restrict__ frz = nullptr, int hchunk = kHookChunk) {
   if (Cp) C = *Cp;
   __shared__ uint64_t s_key[kHookChunk];
   __shared__ uint32_t s_w[kHookChunk];
@@ -936,11 +939,11 @@ __global__ void __launch_bounds__(256) k_hook(int64_t C, const uint64_t* __restr
   // guard self-test build only (tools/guard_selftest.sh): one write past e_key
   if (blockIdx.x == 0 && threadIdx.x == 0) e_key[e_cap + 32] = 0ull;  // e_key holds e_cap + 1: this is in the guard
 #endif
-  for (int64_t chunk = blockIdx.x; chunk * kHookChunk < C; chunk += gridDim.x) {
+  for (int64_t chunk = blockIdx.x; chunk * hchunk < C; chunk += gridDim.x) {
     if (threadIdx.x == 0) s_n = 0;
     __syncthreads();
-    for (int t = 0; t < kHookChunk; t += blockDim.x) {
-      const int64_t c = chunk * kHookChunk + t + threadIdx.x;
+    for (int t = 0; t < hchunk; t += blockDim.x) {
+      const int64_t c = chunk * hchunk + t + threadIdx.x;
       if (c >= C) continue;
       uint64_t K;
       uint32_t Bown = 0, kbown = kInfBits;
@@ -1057,8 +1060,14 @@ __global__ void __launch_bounds__(256) k_hook(int64_t C, const uint64_t* __restr
 // goes to a SEPARATE array: another thread's halving write may land on
 // parent[c] after c found its root, so parent[c] itself is not final.
 __global__ void k_jump(int64_t C, int32_t* parent, int32_t* __restrict__ rootof, RoundCounters* ctr,
-                       const int64_t* __restrict__ Cp = nullptr) {
+                       const int64_t* __restrict__ Cp = nullptr, int32_t* __restrict__ flag = nullptr) {
+  // flag != null (dense renumbering): also the root flags the scan needs, over
+  // the host bound C with zeros beyond the true count (was k_root_flags)
+  const int64_t Cb = C;
   if (Cp) C = *Cp;
+  if (flag)
+    for (int64_t c = C + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < Cb; c += (int64_t)gridDim.x * blockDim.x)
+      flag[c] = 0;
   volatile int32_t* P = parent;
   for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < C;
        c += (int64_t)gridDim.x * blockDim.x) {
@@ -1078,25 +1087,10 @@ __global__ void k_jump(int64_t C, int32_t* parent, int32_t* __restrict__ rootof,
     }
     KDB_DCHECK(x >= 0 && x < C, 4u);
     rootof[c] = x;
+    if (flag) flag[c] = (x == (int32_t)c);
   }
 }
 
-__global__ void k_root_flags(int64_t C, const int32_t* __restrict__ rootof, int32_t* __restrict__ flag,
-                             const int64_t* __restrict__ Cp = nullptr) {
-  // C is the (host) upper bound the scan runs over; with Cp the true count is
-  // on the device and the flags beyond it are 0
-  const int64_t Ct = Cp ? *Cp : C;
-  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < C;
-       c += (int64_t)gridDim.x * blockDim.x)
-    flag[c] = c < Ct && rootof[c] == (int32_t)c;
-}
-
-// number of roots = new component count, from the exclusive scan
-__global__ void k_count_roots(const int64_t* __restrict__ Cp, const int32_t* __restrict__ newid,
-                              const int32_t* __restrict__ flag, int64_t* __restrict__ Cn) {
-  const int64_t C = *Cp;
-  *Cn = C > 0 ? (int64_t)newid[C - 1] + flag[C - 1] : 0;
-}
 
 // new per-component arrays: cmin/kmin are minima over the merged tree
 __global__ void k_merge(int64_t C, const int32_t* __restrict__ rootof, const int32_t* __restrict__ newid,
@@ -1147,6 +1141,32 @@ __global__ void k_keep_a_range(const uint64_t* __restrict__ e_key, const uint32_
     if (keep) {
       o_key[slot] = e_key[i];
       o_a[slot] = a;
+    }
+  }
+}
+
+// The contraction's bookkeeping in one launch (was k_count_roots + two fills +
+// the offer-slot fill + a memset): the new component count -- from the root
+// scan (dense ids) or unchanged (sparse) -- and the next round's
+// per-component slots: cmin2 / kmin2 (minima over the merged trees; before
+// k_merge), the offer slots (Kc/Bc, or the CAS words KB) and the frozen flags.
+__global__ void k_round_fill(int64_t C_bound, const int64_t* __restrict__ Cd, const int32_t* __restrict__ newid,
+                             const int32_t* __restrict__ flag, int64_t* __restrict__ Cn_out, int32_t* __restrict__ cmin2,
+                             uint32_t* __restrict__ kmin2, uint64_t* __restrict__ Kc, uint32_t* __restrict__ Bc,
+                             ulonglong2* __restrict__ KB, uint8_t* __restrict__ frz2) {
+  const int64_t Cc = *Cd;
+  const int64_t Cn = newid ? (Cc > 0 ? (int64_t)newid[Cc - 1] + flag[Cc - 1] : 0) : Cc;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *Cn_out = Cn;
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < C_bound; c += (int64_t)gridDim.x * blockDim.x) {
+    if (frz2) frz2[c] = 0;
+    if (c >= Cn) continue;
+    cmin2[c] = INT32_MAX;
+    if (kmin2) kmin2[c] = kInfBits;
+    if (KB) {
+      KB[c] = make_ulonglong2(kSent, ~0ull);
+    } else {
+      Kc[c] = kSent;
+      Bc[c] = kSentB;
     }
   }
 }

@@ -1,0 +1,7 @@
+# small-input latency after the adaptive row chunks: parity subset + C1..C4 lines
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_local_first.py -x -q > gpurun_out/small2_tests.log 2>&1; echo "tests rc=$?"
+ARGS="--steps 10 --warmup 3 --no-e2e --no-cpu-baseline"
+: > gpurun_out/small2.jsonl
+for c in C1 C2 C3 C4; do timeout 300 python bench.py --config $c $ARGS 2>/dev/null | tail -1 >> gpurun_out/small2.jsonl; done
+echo done
