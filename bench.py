@@ -380,9 +380,11 @@ def run_ours(args):
     stream = torch.cuda.current_stream()
 
     def step(graph):
-        for e in eps_list:
+        # an eps sweep reuses the light ELL inside the step (KDB_GRAPH_REUSE:
+        # same graph and workspace); the step's first eps always rebuilds it
+        for i, e in enumerate(eps_list):
             bits = kdb.core_mark(graph, M, e, comm)
-            r = kdb.mst(graph, e, bits, comm, workspace=ws, out=outs)
+            r = kdb.mst(graph, e, bits, comm, workspace=ws, out=outs, reuse=i > 0)
             lb = kdb.label(graph, e, bits, r.comp, out=lab)
         return bits, r, lb
 
@@ -626,9 +628,9 @@ def run_e2e(args, kdb, W, N, k, M, eps_list, ec, rb, re_, comm, ws, outs, dev, w
         d_nbr.copy_(h_nbr, non_blocking=True)
         d_dist.copy_(h_dist, non_blocking=True)
         g = kdb.Graph(d_nbr, d_dist, n_total=N, row_begin=rb, exact=not args.general, edge_cols=ec)
-        for eps in eps_list:
+        for i, eps in enumerate(eps_list):
             bits = kdb.core_mark(g, M, eps, comm)
-            r = kdb.mst(g, eps, bits, comm, workspace=ws, out=outs)
+            r = kdb.mst(g, eps, bits, comm, workspace=ws, out=outs, reuse=i > 0)
             lb = kdb.label(g, eps, bits, r.comp)
             h_lab.copy_(lb, non_blocking=True)
     e1.record(stream)

@@ -69,6 +69,19 @@ typedef struct CUstream_st* kdb_stream_t; /* == cudaStream_t */
  * e.g. the approximate graph of Fig. cycle). */
 #define KDB_GRAPH_EXACT 1u
 
+/* Caller promise for an eps sweep (Fig. eps_mnist protocol, PAPER.md:459-488:
+ * one kNN graph, many eps): this kdb_mst call gets the same graph (pointers,
+ * contents, row range, k_max, edge_cols) and the same workspace as the
+ * previous kdb_mst call on that workspace, and nothing else wrote the
+ * workspace in between -- only eps and core_bits differ.  The library may then
+ * reuse the light ELL it built from the graph (the first 16 entries of every row
+ * and each row's certificate bound: they depend on the graph and the light
+ * threshold, the median of a fixed column, not on eps).  It checks the pointers,
+ * sizes and threshold it recorded for that workspace and rebuilds on any
+ * mismatch; the contents are the caller's promise.  One process / one rank
+ * only (ignored otherwise).  Results are identical either way. */
+#define KDB_GRAPH_REUSE 2u
+
 typedef struct {
   int64_t n_total;     /* N = |I|, all ranks                                        */
   int64_t row_begin;   /* first global row id held by this rank                     */
@@ -77,7 +90,7 @@ typedef struct {
   const int32_t* nbr;  /* device [n_rows][k_max] global ids, -1 = padding; 16-B aligned */
   const float* dist;   /* device [n_rows][k_max] fp32 >= 0, non-decreasing per row,
                           +inf = padding; 16-B aligned                              */
-  uint32_t flags;      /* KDB_GRAPH_EXACT or 0                                       */
+  uint32_t flags;      /* KDB_GRAPH_EXACT and/or KDB_GRAPH_REUSE, or 0                */
   int32_t edge_cols;   /* candidate edges come from columns [0, edge_cols) of each row;
                           0 = all k_max.  Only kdb_mst reads it; 0 <= edge_cols <= k_max
                           (EINVAL otherwise).  edge_cols = M gives Def. 6's edge set.
@@ -208,7 +221,8 @@ kdb_status kdb_nmi(const int32_t* a, const int32_t* b, int64_t n, double* nmi /*
  * out[23] = global-phase ms, out[24] = components entering the global phase,
  * out[25] = rows parked for it (all ranks), out[26] = bytes per rank of the
  * transition's all-gathers, out[27] = local rounds (max over ranks), out[28] =
- * global-phase ms of the per-rank offers and ties (all ranks).  Returns
+ * global-phase ms of the per-rank offers and ties (all ranks), out[29] = rows
+ * phases that reused a kept light ELL (KDB_GRAPH_REUSE).  Returns
  * entries written (at most 32). */
 int kdb_last_mst_stats(double* out, int cap);
 

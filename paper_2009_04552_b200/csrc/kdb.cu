@@ -555,6 +555,10 @@ size_t local_view_bytes(const kdb_graph* g) {
 kdb_status mst_impl(const kdb_graph* g, float eps, const uint32_t* core_bits, int32_t* comp, uint32_t* mst_a,
                     uint32_t* mst_b, float* mst_w, int64_t mst_cap, int64_t* mst_count, double* mst_weight,
                     void* workspace, size_t ws_bytes, kdb_comm* comm, kdb_stream_t stream, int32_t nparts) {
+  // whatever this call does, a kept light ELL in this workspace is not valid
+  // after it unless this call keeps a new one (see EllKey)
+  const void* ws0 = workspace;
+  EllKey ell_prev = ell_take(ws0);
   KDB_TRY(validate_graph(g));
   KDB_TRY(validate_eps(eps));
   const int64_t N = g->n_total;
@@ -590,6 +594,11 @@ kdb_status mst_impl(const kdb_graph* g, float eps, const uint32_t* core_bits, in
   // the local view is no kNN graph (no certificate): in-edge lists
   m.general = inexact || !(g->flags & KDB_GRAPH_EXACT);
   m.lf = !inexact && !m.general && local_first_on(g, comm);
+  // a kept light ELL is only valid until the workspace's next call: take it out
+  // of the table now, put a new one back on success
+  m.ws = ws0;
+  m.reuse_req = (g->flags & KDB_GRAPH_REUSE) != 0 && env_int("KDB_REUSE", 1) != 0;
+  m.ell_prev = ell_prev;
   Layout& L = m.L;
   std::vector<int64_t> rb, rn;
   rank_ranges(g, comm, rb, rn);
@@ -751,6 +760,7 @@ kdb_status mst_impl(const kdb_graph* g, float eps, const uint32_t* core_bits, in
   KDB_TRY(guards_check((const char*)workspace, L.guards, st, "kdb_mst"));
   *mst_count = ne;
   *mst_weight = exact_bucket_sum(bk);
+  if (m.ell_next.valid) ell_put(m.ell_next);
   g_stats[0] = m.rounds;
   g_stats[1] = m.t_init;
   g_stats[2] = m.t_min_edges;
@@ -783,6 +793,7 @@ kdb_status mst_impl(const kdb_graph* g, float eps, const uint32_t* core_bits, in
   g_stats[26] = m.payload_transition;
   g_stats[27] = m.local_rounds;
   g_stats[28] = m.t_global_scan;
+  g_stats[29] = m.reused;
   return KDB_OK;
 }
 
@@ -942,6 +953,7 @@ kdb_status kdb_nmi(const int32_t* a, const int32_t* b, int64_t n, double* nmi, i
   if (n < 0 || n >= (int64_t)INT32_MAX) return set_err(KDB_EINVAL, "n out of range [0, 2^31-1)");
   if (n > 0 && (!a || !b || !workspace)) return set_err(KDB_EINVAL, "NULL device pointer");
   if ((uintptr_t)workspace & 255u) return set_err(KDB_EINVAL, "workspace must be 256-byte aligned");
+  ell_take(workspace);  // a light ELL kept in this workspace does not survive this call
   NmiWs w;
   std::vector<size_t> guards;
   const size_t need = nmi_carve(w, (char*)workspace, false, n, &guards);

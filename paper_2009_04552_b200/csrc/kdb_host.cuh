@@ -40,8 +40,12 @@ double exact_bucket_sum(const unsigned long long* bk) {
 // heavy-phase survivor capacity per rank (edges); beyond it kdb_mst falls back
 // to plain rows-Boruvka over the whole candidate graph (still exact)
 constexpr int kTauSamples = 8192;
+// (n_rows / 2: an eps near the median of D[:, M-1] leaves half the points
+// non-core, the light graph fragments and C4 keeps 27.6M survivors -- above
+// n_rows / 4 that re-ran the whole rows phase at eps, 40 ms against a few ms of
+// heavy rounds; 48 B per row of workspace)
 inline int64_t survivor_cap(int64_t n_rows, int64_t k) {
-  return std::max<int64_t>(n_rows / 4, std::min<int64_t>(n_rows * k / 4, (int64_t)1 << 24)) + 65536;
+  return std::max<int64_t>(n_rows / 2, std::min<int64_t>(n_rows * k / 4, (int64_t)1 << 24)) + 65536;
 }
 
 // Workspace carving.  The debug build (-DKDB_GUARDS=1, lib/libkdb_dbg.so)
@@ -101,6 +105,7 @@ struct RankState {
   uint32_t n_deep = 0;                // rows whose ELL entries are all light (k_light_ell)
   bool compact = false;               // rows phase reads the light ELL (else the graph rows)
   int4* LE = nullptr;                 // light ELL [n_rows][kW] (J, w bits) pairs
+  uint32_t* kthL = nullptr;           // per row: certificate bound kth' of the ELL's threshold (kept for reuse)
   // offers: [0, n_rows) from rows (same slot as the row's next record),
   // [n_rows, n_rows + N) from in-lists (general mode)
   Offer* offers = nullptr;
@@ -217,6 +222,7 @@ size_t carve(Layout& L, char* base, bool dry, int64_t N, int nr, const int64_t* 
     R.act[0] = cv.take<Rec>(n);
     R.act[1] = cv.take<Rec>(n);
     R.LE = cv.take<int4>(n * (kW / 2));
+    R.kthL = general ? nullptr : cv.take<uint32_t>(n);
     R.off_cap_rows = n;
     R.offers = cv.take<Offer>(general ? n + N : n);
     R.ctr = cv.take<RoundCounters>(1);
@@ -262,7 +268,7 @@ kdb_status validate_graph(const kdb_graph* g) {
   if (g->n_rows > 0 && (!g->nbr || !g->dist)) return set_err(KDB_EINVAL, "nbr/dist is NULL");
   if (((uintptr_t)g->nbr & 15u) || ((uintptr_t)g->dist & 15u))
     return set_err(KDB_EINVAL, "nbr/dist must be 16-byte aligned");
-  if (g->flags & ~KDB_GRAPH_EXACT) return set_err(KDB_EINVAL, "unknown graph flags");
+  if (g->flags & ~(KDB_GRAPH_EXACT | KDB_GRAPH_REUSE)) return set_err(KDB_EINVAL, "unknown graph flags");
   if (g->edge_cols < 0 || g->edge_cols > g->k_max) return set_err(KDB_EINVAL, "edge_cols must be in [0, k_max]");
   return KDB_OK;
 }
@@ -336,6 +342,43 @@ int env_int(const char* name, int dflt) {
 
 bool nr_ranks_is_one(const Layout& L) { return L.ranks.size() == 1; }
 
+// What a kept light ELL was built from.  The ELL (first kW entries of every
+// row) and the per-row certificate bounds depend on the graph and on the
+// rows-phase threshold eps_run only -- for the light phase that is tau, the
+// median of a fixed column, not eps -- so an eps sweep over one graph can skip
+// the ELL pass after its first call.  Host-side table keyed by the workspace.
+struct EllKey {
+  bool valid = false;
+  const void* ws = nullptr;
+  const int32_t* nbr = nullptr;
+  const float* dist = nullptr;
+  int64_t n_total = 0, row_begin = 0, n_rows = 0;
+  int32_t k_max = 0, k = 0;
+  uint32_t eps_run_bits = 0, n_deep = 0;
+  bool same_graph(const EllKey& o) const {
+    return ws == o.ws && nbr == o.nbr && dist == o.dist && n_total == o.n_total && row_begin == o.row_begin &&
+           n_rows == o.n_rows && k_max == o.k_max && k == o.k;
+  }
+};
+std::mutex g_ell_mu;
+std::vector<EllKey> g_ell;  // at most a few workspaces in flight
+EllKey ell_take(const void* ws) {  // remove and return the entry of this workspace
+  std::lock_guard<std::mutex> lk(g_ell_mu);
+  EllKey out;
+  for (size_t i = 0; i < g_ell.size(); ++i)
+    if (g_ell[i].ws == ws) {
+      out = g_ell[i];
+      g_ell.erase(g_ell.begin() + i);
+      break;
+    }
+  return out;
+}
+void ell_put(const EllKey& e) {
+  std::lock_guard<std::mutex> lk(g_ell_mu);
+  if (g_ell.size() >= 64) g_ell.erase(g_ell.begin());
+  g_ell.push_back(e);
+}
+
 // One kdb_mst call: the workspace layout plus the phase bookkeeping.
 struct Mst {
   Layout L;
@@ -369,6 +412,11 @@ struct Mst {
   uint64_t n_park = 0, msf_local = 0;
   double t_local_max = 0, t_local_sum = 0, t_transition = 0, t_global = 0;
   int local_rounds = 0;
+  // light ELL kept across calls on one workspace (KDB_GRAPH_REUSE, eps sweeps)
+  bool reuse_req = false;
+  const void* ws = nullptr;   // the caller's workspace (key of the kept-ELL table)
+  EllKey ell_prev, ell_next;  // what the previous call left / what this call leaves (valid flags inside)
+  int reused = 0;             // rows phases that reused the kept ELL
   double t_global_scan = 0;  // global phase: per-rank offers and ties (all ranks, in sequence under sim)
   int64_t C_global = -1;      // components entering the global phase
   uint64_t parked_rows = 0;   // rows entering the global phase (all ranks)
@@ -477,9 +525,30 @@ kdb_status rows_phase(Mst& m, float eps_run) {
     L.all_core = (C == L.ranks[0].n_rows) ? 1 : 0;  // then a row's local id is v - lo
     KDB_CUDA(cudaMemsetAsync(frz, 0, (size_t)std::max<int64_t>(C, 1), st));
   }
+  // eps sweep on an unchanged graph: reuse the ELL the previous call kept
+  const bool one_rank = L.ranks.size() == 1 && !multi_rank(comm) && !m.local;
+  uint32_t eb = 0;
+  memcpy(&eb, &eps_run, 4);
+  EllKey want;
+  if (one_rank && !general && use_compact) {
+    const RankState& R0 = L.ranks[0];
+    want.valid = true;
+    want.ws = m.ws;
+    want.nbr = R0.nbr;
+    want.dist = R0.dist;
+    want.n_total = N;
+    want.row_begin = R0.row_begin;
+    want.n_rows = R0.n_rows;
+    want.k_max = ld;
+    want.k = k;
+    want.eps_run_bits = eb;
+  }
+  const bool reuse = want.valid && m.reuse_req && m.ell_prev.valid && m.ell_prev.same_graph(want) &&
+                     m.ell_prev.eps_run_bits == eb && L.ranks[0].n_rows > 0;
   // exact mode: round 1 (singleton components) is fused into the ELL pass; a
   // single rank also packs (K, B, kmin) per component for the round-1 hook
-  fuse1 = !general && use_compact && env_int("KDB_FUSE1", 1) != 0;
+  // (with a reused ELL round 1 runs over it: k_light_first)
+  fuse1 = !general && use_compact && env_int("KDB_FUSE1", 1) != 0 && !reuse;
   packed1 = fuse1 && L.ranks.size() == 1 && !(multi_rank(comm)) && env_int("KDB_PACK1", 1) != 0;
   // Per-component slots of round 1.  Packed round 1 (one rank, fused ELL pass)
   // writes a whole record and the certificate bound for EVERY component (each
@@ -496,7 +565,12 @@ kdb_status rows_phase(Mst& m, float eps_run) {
   for (auto& R : L.ranks) {
     KDB_CUDA(cudaMemsetAsync(R.ctr, 0, sizeof(RoundCounters), st));
     R.compact = false;
-    if (R.n_rows > 0 && use_compact) {
+    if (reuse) {
+      R.compact = true;
+      LAUNCH(k_reuse_rows, grid_for(R.n_rows), kThreads, st, R.LE, R.kthL, R.n_rows, R.row_begin, eps_run, comp,
+             L.kmin, R.act[0], &R.ctr->na[0]);
+      ++m.reused;
+    } else if (R.n_rows > 0 && use_compact) {
       R.compact = true;
       // 32-byte sector loads need 32-B aligned arrays, ld % 8 in {0, 4} and rows
       // long enough for the third sector (ld >= 20)
@@ -505,7 +579,7 @@ kdb_status rows_phase(Mst& m, float eps_run) {
   LAUNCH((k_light_ell<V, A>), grid_for(R.n_rows), kThreads, st, R.nbr, R.dist, R.n_rows, ld, k, eps_run, R.row_begin, \
          comp, general ? nullptr : L.kmin, R.LE, R.act[0], &R.ctr->na[0], &R.ctr->grab, fuse1 ? 1 : 0,         \
          L.all_core, N, R.Kc, R.Bc, R.tgt, packed1 ? L.rec1 : nullptr, &R.ctr->n_deep, lv, skip1,               \
-         row_chunk((uint64_t)R.n_rows))
+         row_chunk((uint64_t)R.n_rows), want.valid ? R.kthL : (uint32_t*)nullptr)
       if (a32) KDB_ELL_LAUNCH(true, true);
       else if (vec) KDB_ELL_LAUNCH(true, false);
       else KDB_ELL_LAUNCH(false, false);
@@ -544,8 +618,12 @@ kdb_status rows_phase(Mst& m, float eps_run) {
     KDB_CUDA(cudaMemcpyAsync(&hc, R.ctr, sizeof(hc), cudaMemcpyDeviceToHost, st));
     KDB_CUDA(cudaStreamSynchronize(st));
     R.n_act = hc.na[0];
-    R.n_deep = hc.n_deep;
+    R.n_deep = reuse ? m.ell_prev.n_deep : hc.n_deep;
     R.n_in_act = hc.ni[0];
+  }
+  if (want.valid) {  // what this call's ELL was built from (kept if the call succeeds)
+    m.ell_next = want;
+    m.ell_next.n_deep = L.ranks[0].n_deep;
   }
   KDB_CUDA(cudaEventRecord(ev[2], st));
   KDB_CUDA(cudaEventSynchronize(ev[2]));

@@ -409,7 +409,7 @@ __global__ void __launch_bounds__(256) k_light_ell(const int32_t* __restrict__ n
                                                    uint32_t* __restrict__ Bc, int32_t* __restrict__ tgt,
                                                    int4* __restrict__ rec1, uint32_t* __restrict__ n_deep,
                                                    const LocalView lv = LocalView{}, int skip1 = 1,
-                                                   int chunk = kChunk) {
+                                                   int chunk = kChunk, uint32_t* __restrict__ kthL = nullptr) {
   __shared__ __align__(16) Rec s_rec[kChunk];
   __shared__ uint32_t s_n, s_chunk, s_base;
   uint32_t deep = 0;  // rows whose kW ELL entries are all within eps (their scans go past the first chunk)
@@ -423,7 +423,10 @@ __global__ void __launch_bounds__(256) k_light_ell(const int32_t* __restrict__ n
       if (i >= n_rows) continue;
       const int64_t v = row_begin + i;
       const int32_t cv = comp[v];
-      if (cv < 0) continue;
+      // kthL != null: the ELL (and each row's certificate bound) is kept for the
+      // next call on the same graph (an eps sweep, KDB_GRAPH_REUSE): non-core
+      // rows get theirs too -- another eps may make them core
+      if (cv < 0 && !kthL) continue;
       const int32_t* nr = nbr + i * ld;
       const float* dr = dist + i * ld;
       int32_t J[kW];
@@ -484,13 +487,15 @@ __global__ void __launch_bounds__(256) k_light_ell(const int32_t* __restrict__ n
         float kth = __int_as_float(0x7f800000);
         if (k <= kW || w[kW - 1] <= eps) kth = __ldcs(dr + (k - 1));
         kb = (kth <= eps) ? mono_bits(kth) : kInfBits;
-        kmin[cv] = kb;
+        if (cv >= 0) kmin[cv] = kb;
+        if (kthL) kthL[i] = kb;
       }
       deep += w[kW - 1] <= eps;
       int4* o = LE + i * (kW / 2);
 #pragma unroll
       for (int q = 0; q < kW / 2; ++q)
         __stcs(o + q, make_int4(J[2 * q], __float_as_int(w[2 * q]), J[2 * q + 1], __float_as_int(w[2 * q + 1])));
+      if (cv < 0) continue;
       if (!direct) {
         if (w[0] <= eps) s_rec[atomicAdd(&s_n, 1u)] = Rec{(int32_t)v, 0};
         continue;
@@ -559,6 +564,29 @@ __global__ void __launch_bounds__(256) k_light_ell(const int32_t* __restrict__ n
 }
 
 
+
+// eps sweep on an unchanged graph (KDB_GRAPH_REUSE): the light ELL and each
+// row's certificate bound were kept by the previous call (they depend on the
+// graph and the light threshold, not on eps); only the core-dependent state
+// is rebuilt: kmin per component and the active list (core rows whose first
+// entry is within eps_run) -- round 1 then runs over the ELL (k_light_first).
+__global__ void k_reuse_rows(const int4* __restrict__ LE, const uint32_t* __restrict__ kthL, int64_t n_rows,
+                             int64_t row_begin, float eps, const int32_t* __restrict__ comp, uint32_t* __restrict__ kmin,
+                             Rec* __restrict__ act, uint32_t* __restrict__ n_act) {
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n_rows; base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = base + threadIdx.x;
+    bool want = false;
+    if (i < n_rows) {
+      const int32_t cv = comp[row_begin + i];
+      if (cv >= 0) {
+        kmin[cv] = kthL[i];
+        want = __int_as_float(__ldcs(reinterpret_cast<const int*>(LE + i * (kW / 2)) + 1)) <= eps;
+      }
+    }
+    const uint32_t slot = block_reserve(n_act, want);
+    if (want) act[slot] = Rec{(int32_t)(row_begin + i), 0};
+  }
+}
 
 // Scan row v (component cv) from head h: columns < kW from the ELL row, the
 // rest (rare: a candidate prefix longer than kW) from the graph row.  DIRECT:

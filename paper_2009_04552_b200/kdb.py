@@ -22,6 +22,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 # KDB_LIBRARY: an alternative build of the same library (tuning experiments)
 LIB_PATH = os.environ.get("KDB_LIBRARY") or os.path.join(_HERE, "lib", "libkdb.so")
 KDB_GRAPH_EXACT = 1
+KDB_GRAPH_REUSE = 2
 
 
 class KdbError(RuntimeError):
@@ -212,8 +213,10 @@ class MstResult:
 
 
 def mst(g: Graph, eps: float, core_bits: torch.Tensor, comm: Comm | None = None, stream=None,
-        workspace: torch.Tensor | None = None, out: dict | None = None) -> MstResult:
-    """kdb_mst: exact MSF of the core-core candidate edges + component labels."""
+        workspace: torch.Tensor | None = None, out: dict | None = None, reuse: bool = False) -> MstResult:
+    """kdb_mst: exact MSF of the core-core candidate edges + component labels.
+    reuse=True sets KDB_GRAPH_REUSE: the caller promises the same graph and
+    workspace as the previous mst() call on that workspace (an eps sweep)."""
     dev = g.dist.device
     N = g.n_total
     o = out or {}
@@ -232,6 +235,8 @@ def mst(g: Graph, eps: float, core_bits: torch.Tensor, comm: Comm | None = None,
     cnt = C.c_int64(0)
     tot = C.c_double(0.0)
     gc = g.c()
+    if reuse:
+        gc.flags |= KDB_GRAPH_REUSE
     _check(lib().kdb_mst(C.byref(gc), float(eps), C.c_void_p(core_bits.data_ptr()),
                          C.c_void_p(comp.data_ptr()), C.c_void_p(a.data_ptr()), C.c_void_p(b.data_ptr()),
                          C.c_void_p(w.data_ptr()), cap, C.byref(cnt), C.byref(tot),
@@ -244,7 +249,7 @@ def mst(g: Graph, eps: float, core_bits: torch.Tensor, comm: Comm | None = None,
                  filter_ms=st[8], heavy_ms=st[9], survivors=int(st[10]), heavy_rounds=int(st[11]),
                  tau=st[12], light_components=int(st[13]), fallback=int(st[14]),
                  filter_exceptions=int(st[15]), filter_slow_entries=int(st[16]),
-                 payload_rows_bytes=st[17], payload_heavy_bytes=st[18])
+                 payload_rows_bytes=st[17], payload_heavy_bytes=st[18], ell_reused=int(st[29]))
     if st[19]:  # local-first contraction ran (multi-rank exact mode)
         stats["local_first"] = dict(local_ms_max=st[20], local_ms_sum=st[21], transition_ms=st[22],
                                     global_ms=st[23], global_components=int(st[24]), parked_rows=int(st[25]),
@@ -334,13 +339,13 @@ def profile_read() -> dict:
 
 
 def kdbscan(g: Graph, M: int, eps: float, comm: Comm | None = None, stream=None, edge_cols: int | None = None,
-            workspace: torch.Tensor | None = None):
+            workspace: torch.Tensor | None = None, reuse: bool = False):
     """The whole clustering stage (Alg. 1): returns (core_bits, MstResult, labels).
     edge_cols overrides g.edge_cols (M = the paper's Def. 6 edge set)."""
     if edge_cols is not None:
         g = dataclasses.replace(g, edge_cols=int(edge_cols))
     bits = core_mark(g, M, eps, comm, stream)
-    r = mst(g, eps, bits, comm, stream, workspace=workspace)
+    r = mst(g, eps, bits, comm, stream, workspace=workspace, reuse=reuse)
     lab = label(g, eps, bits, r.comp, stream)
     return bits, r, lab
 
@@ -356,8 +361,10 @@ def kdbscan_sweep(g: Graph, M: int, eps_values, comm: Comm | None = None, stream
     nws = workspace_bytes(g, comm)
     ws = torch.empty(max(nws, 256), dtype=torch.uint8, device=g.dist.device)
     out = []
-    for eps in eps_values:
-        bits, r, lab = kdbscan(g, M, eps, comm, stream, workspace=ws)
+    for i, eps in enumerate(eps_values):
+        # after the first eps the graph and workspace are unchanged: the light
+        # ELL built by the first call is reused (KDB_GRAPH_REUSE)
+        bits, r, lab = kdbscan(g, M, eps, comm, stream, workspace=ws, reuse=i > 0)
         out.append((float(eps), bits, r, lab))
     return out
 
