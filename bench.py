@@ -43,6 +43,10 @@ def parse():
     ap.add_argument("--scale", type=float, default=1.0, help="shrink every cluster (tests only)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--order", default="inertial", choices=["inertial", "generation"],
+                    help="point order (= kNN-graph ids): inertial = the paper's inertial partition of the "
+                         "data set (PAPER.md:45, datagen/partition.py); generation = the generator's "
+                         "cluster-major order")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--general", action="store_true", help="do not promise an exact graph")
@@ -143,7 +147,7 @@ def median_like_numpy(col):
     return float((a + b) / 2)
 
 
-def make_workload(cfg_name: str, scale: float, seed: int, device, rank=0, world=1):
+def make_workload(cfg_name: str, scale: float, seed: int, device, rank=0, world=1, order="inertial"):
     """Points (numpy, seeded), exact kNN graph on the GPU, eps from the config rule.
     world > 1: this rank's rows [b, e) only (the grid builder searches all points
     for its query rows: knng_grid_rows), so no rank ever holds the whole graph
@@ -155,6 +159,14 @@ def make_workload(cfg_name: str, scale: float, seed: int, device, rank=0, world=
     cfg = CONFIGS[cfg_name]
     t0 = time.time()
     X, truth = gen_config_points(cfg_name, seed, scale)
+    t_part = 0.0
+    if order == "inertial":  # the data set is partitioned before clustering
+        from datagen.partition import inertial_order
+        tp = time.time()
+        perm = inertial_order(X, device=device)
+        X, truth = X[perm], truth[perm]
+        del perm
+        t_part = time.time() - tp
     t1 = time.time()
     sliced = False
     if X.shape[1] <= 5:   # uniform-grid cell search (C1, C4, C5)
@@ -177,7 +189,7 @@ def make_workload(cfg_name: str, scale: float, seed: int, device, rank=0, world=
     del col
     eps = float(np.float32(cfg["eps_factor"] * med))
     return dict(X=X, truth=truth, nbr=nbr, dist=dist, eps=eps, M=cfg["M"], k=cfg["k"], N=len(X),
-                d=X.shape[1], gen_s=t1 - t0, graph_build_s=t2 - t1, knng=info, med=med, sliced=sliced)
+                d=X.shape[1], gen_s=t1 - t0, partition_s=t_part, order=order, graph_build_s=t2 - t1, knng=info, med=med, sliced=sliced)
 
 
 def stage_params(args, W):
@@ -217,6 +229,9 @@ def workload_desc(cfg_name, W, scale):
             "graph": "exact kNN, self-excluded, fp32 dist / int32 ids (datagen/csrc/knng.cu " +
                      ("grid builder)" if W["d"] <= 5 else "brute-force builder, fp64 re-rank)"),
             "graph_bytes": int(W["N"]) * int(W["k"]) * 8,
+            "order": W["order"] + (" (recursive inertial bisection to 64-point leaves, PAPER.md:45; "
+                                   f"{W['partition_s']:.1f} s, untimed input preparation)"
+                                   if W["order"] == "inertial" else " (cluster-major, random inside a cluster)"),
             "l2": "no flush: the resident graph (>=1 GB) exceeds the 126 MB L2",
             "graph_build_s": round(W["graph_build_s"], 2)}
 
@@ -240,7 +255,7 @@ def run_reference(args):
     if rank != 0:
         return  # rank 0 alone runs the oracle arm
     torch.cuda.set_device(local)
-    W = make_workload(args.config, args.scale, args.seed, f"cuda:{local}")
+    W = make_workload(args.config, args.scale, args.seed, f"cuda:{local}", order=args.order)
     ec, eps_list = stage_params(args, W)
     ns = min(args.cpu_sample_rows, W["N"])
     nbr = W["nbr"][:ns].cpu().numpy()
@@ -355,7 +370,7 @@ def run_ours(args):
             tdist.barrier()
 
     from paper_2009_04552_b200.dist import max_over_ranks, rank_rows
-    W = make_workload(args.config, args.scale, args.seed, dev, rank=rank, world=world)
+    W = make_workload(args.config, args.scale, args.seed, dev, rank=rank, world=world, order=args.order)
     N, k, M, eps = W["N"], W["k"], W["M"], W["eps"]
     rb, re_ = rank_rows(N, rank, world)
     if world > 1 and not W["sliced"]:  # keep this rank's rows only

@@ -338,6 +338,30 @@ __device__ __forceinline__ void min_pair128(ulonglong2* p, uint64_t key, uint64_
   }
 }
 
+// Warp-collective min_pair128: lanes offering to the SAME component in a run
+// of consecutive lanes (rows of one component next to each other in the row
+// order, e.g. spatially ordered ids) are min-reduced first and only the run's
+// first lane issues the CAS -- same-address CAS loops serialise at the L2
+// slice.  A warp with no such run (random ids) pays one shuffle and a ballot.
+// Lanes with have == false must pass a c that no other lane holds.
+__device__ __forceinline__ void warp_min_pair128(ulonglong2* KB, bool have, int32_t c, uint64_t key, uint64_t b) {
+  const int lane = threadIdx.x & 31;
+  const int32_t cn = __shfl_down_sync(0xffffffffu, c, 1);
+  const unsigned last = __ballot_sync(0xffffffffu, lane == 31 || cn != c);  // lane ends its run
+  if (last != 0xffffffffu) {
+    const int end = lane + __ffs(last >> lane) - 1;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint64_t ok = __shfl_down_sync(0xffffffffu, key, o);
+      const uint64_t obb = __shfl_down_sync(0xffffffffu, b, o);
+      if (lane + o <= end && (ok < key || (ok == key && obb < b))) { key = ok; b = obb; }
+    }
+    const int32_t cp = __shfl_up_sync(0xffffffffu, c, 1);
+    if (lane > 0 && cp == c) have = false;  // not the first lane of its run
+  }
+  if (have) min_pair128(KB + c, key, b);
+}
+
 __device__ __forceinline__ uint64_t pack_key(uint32_t wbits, uint32_t a) {
   return ((uint64_t)wbits << 32) | a;
 }
@@ -397,6 +421,7 @@ __device__ __forceinline__ void block_count(uint32_t* counter, bool pred) {
 
 
 #include "kdb_rows.cuh"
+#include "kdb_tile.cuh"
 #include "kdb_filter.cuh"
 #include "kdb_host.cuh"
 

@@ -172,7 +172,8 @@ template <int VEC, bool FAST, bool COLS, bool SMALL = false>
 __global__ void __launch_bounds__(kFilterThreads) k_filter(
     const int32_t* __restrict__ nbr, const float* __restrict__ dist, int64_t n_rows, int32_t ld, int32_t k, float tau, float eps,
     int64_t row_begin, int64_t N, const int32_t* __restrict__ comp, const int2* __restrict__ rng, const uint32_t* __restrict__ bloom, FastDiv fd,
-    HEdge* __restrict__ out, uint32_t cap, uint32_t* __restrict__ n_out, unsigned long long* __restrict__ n_slow) {
+    HEdge* __restrict__ out, uint32_t cap, uint32_t* __restrict__ n_out, unsigned long long* __restrict__ n_slow,
+    const int32_t* __restrict__ dom, const int2* __restrict__ brun, int shift) {
   extern __shared__ uint32_t s_bloom[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   FRow* s_row = reinterpret_cast<FRow*>(s_bloom + kBloomBits / 32) + wid * kFilterRows;
@@ -196,7 +197,11 @@ __global__ void __launch_bounds__(kFilterThreads) k_filter(
       fr.lo = 0;
       fr.span = 0;
       if (FAST && fr.cr >= 0) {
-        const int2 rg = __ldg(rng + fr.cr);
+        int2 rg = __ldg(rng + fr.cr);
+        if (!(rg.y > rg.x)) {  // no single range: the run of blocks dominated by comp[v] around v
+          const int64_t b = (row_begin + i) >> shift;
+          if (__ldg(dom + b) == fr.cr) rg = __ldg(brun + b);
+        }
         if (rg.y > rg.x) { fr.lo = (uint32_t)rg.x; fr.span = (uint32_t)(rg.y - rg.x); }
       }
       s_row[ti] = fr;

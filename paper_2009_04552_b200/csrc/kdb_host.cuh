@@ -149,6 +149,7 @@ struct Layout {
   uint8_t *frz, *frz2;  // local-first phase: frozen components (ping-pong through the contraction)
   int32_t* hcomp;   // heavy phase: light component -> heavy component
   int32_t* dom;     // filter fast path: dominant component per id block
+  int2* brun;       // filter fast path: id range of the run of equal-dom blocks around each block
   uint32_t* bloom;  // filter fast path: Bloom filter of the exceptions
   unsigned long long* fcount;  // [0] exceptions, [1] slow-path entries
   float* tau_sample;
@@ -207,6 +208,7 @@ size_t carve(Layout& L, char* base, bool dry, int64_t N, int nr, const int64_t* 
   L.frz2 = local_first ? cv.take<uint8_t>(N + 1) : nullptr;
   L.hcomp = cv.take<int32_t>(N + 1);
   L.dom = cv.take<int32_t>(kDomMax);
+  L.brun = cv.take<int2>(kDomMax);
   L.bloom = cv.take<uint32_t>(kBloomBits / 32);
   L.fcount = cv.take<unsigned long long>(2);
   L.tau_sample = cv.take<float>(kTauSamples);
@@ -498,7 +500,7 @@ kdb_status rows_phase(Mst& m, float eps_run) {
   uint8_t* frz = m.local ? L.frz : nullptr;
   const int64_t ecap = m.ecap >= 0 ? m.ecap : N;
   int64_t C = 0;
-  bool fuse1 = false, packed1 = false;
+  bool fuse1 = false, packed1 = false, tile = false;
   size_t cb = L.cub_bytes;
   if (m.cont) {
     C = m.C;  // global components after the local-first phases (state set by local_first)
@@ -548,7 +550,10 @@ kdb_status rows_phase(Mst& m, float eps_run) {
   // exact mode: round 1 (singleton components) is fused into the ELL pass; a
   // single rank also packs (K, B, kmin) per component for the round-1 hook
   // (with a reused ELL round 1 runs over it: k_light_first)
-  fuse1 = !general && use_compact && env_int("KDB_FUSE1", 1) != 0 && !reuse;
+  // tile round (one rank, exact mode, light ELL): round 1 is tile-local
+  // Boruvka in shared memory (k_tile_round) instead of the fused singleton round
+  tile = want.valid && want.row_begin == 0 && env_int("KDB_TILE", 1) != 0 && L.ranks[0].n_rows > 0;
+  fuse1 = !general && use_compact && env_int("KDB_FUSE1", 1) != 0 && !reuse && !tile;
   packed1 = fuse1 && L.ranks.size() == 1 && !(multi_rank(comm)) && env_int("KDB_PACK1", 1) != 0;
   // Per-component slots of round 1.  Packed round 1 (one rank, fused ELL pass)
   // writes a whole record and the certificate bound for EVERY component (each
@@ -753,6 +758,18 @@ kdb_status rows_phase(Mst& m, float eps_run) {
       ev_rnd.push_back(e0);
       KDB_CUDA(cudaEventRecord(e0, st));
     }
+    const bool tile_round = tile && rounds == 1;
+    if (tile_round) {  // round 1: tile-local Boruvka (kdb_tile.cuh); then contract as after any round
+      RankState& R = L.ranks[0];
+      KDB_CUDA(cudaMemsetAsync(&R.ctr->na[cur ^ 1], 0, sizeof(uint32_t), st));
+      KDB_CUDA(cudaMemsetAsync(&R.ctr->grab, 0, sizeof(uint32_t), st));
+      KDB_CUDA(cudaMemsetAsync(&L.ctr->hooks, 0, 4 * sizeof(uint32_t), st));
+      const int64_t ntiles = (R.n_rows + kTileRows - 1) / kTileRows;
+      LAUNCH_DYN(k_tile_round, (int)std::min<int64_t>(ntiles, 1 << 30), kTileRows, sizeof(TileSmem), st, R.LE,
+                 R.n_rows, k, eps_run, N, comp, core_bits, L.kmin, L.parent, L.e_key, L.e_w, ecap, R.act[cur ^ 1],
+                 &R.ctr->na[cur ^ 1], &R.ctr->grab, L.ctr, &L.ctr->entries);
+      KDB_CUDA(cudaGetLastError());
+    } else {
     // offers read the current key before their atomicMin once many rows offer
     // to each component (same-address atomics serialise; early rounds have
     // about one row per component and only pay the extra read)
@@ -878,6 +895,7 @@ kdb_status rows_phase(Mst& m, float eps_run) {
              comp, L.parent, L.e_key, L.e_w, ecap, L.ctr, Cd, (const int4*)nullptr,
              (cas && !direct) ? (const ulonglong2*)KB : nullptr, frz, row_chunk((uint64_t)C_ub));
     KDB_CUDA(cudaGetLastError());
+    }  // !tile_round
     // a6: contract (no hooks => identity)
     KDB_TRY(contract(C_ub));
     cur ^= 1;
@@ -1233,8 +1251,25 @@ kdb_status filter_phase(Mst& m, float eps, bool* overflow) {
     LAUNCH(k_rng_acc, grid_for(nblk), kThreads, st, L.dom, nblk, L.parent, L.rootof, L.newid);
     LAUNCH(k_rng_fin, grid_for(C), kThreads, st, C, m.N, shift, L.parent, L.rootof, L.newid, rng);
     KDB_CUDA(cudaGetLastError());
+    // per-block runs (host: nblk <= kDomMax): a component whose dominated blocks
+    // are not ONE contiguous run has no range in rng (its ids come in several
+    // runs, e.g. a cluster split by the data set's partition); its
+    // rows then use the run of equal-dom blocks around their own block
+    std::vector<int32_t> hdom(nblk);
+    std::vector<int2> hrun(nblk);
+    KDB_CUDA(cudaMemcpyAsync(hdom.data(), L.dom, nblk * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
     KDB_CUDA(cudaMemcpyAsync(fc, L.fcount, sizeof(fc), cudaMemcpyDeviceToHost, st));
     KDB_CUDA(cudaStreamSynchronize(st));
+    for (int64_t b = 0; b < nblk;) {
+      int64_t e = b + 1;
+      while (e < nblk && hdom[e] == hdom[b]) ++e;
+      const int2 r = hdom[b] >= 0 ? make_int2((int32_t)(b << shift), (int32_t)std::min<int64_t>(e << shift, m.N))
+                                  : make_int2(1, 0);
+      for (int64_t x = b; x < e; ++x) hrun[x] = r;
+      b = e;
+    }
+    KDB_CUDA(cudaMemcpyAsync(L.brun, hrun.data(), nblk * sizeof(int2), cudaMemcpyHostToDevice, st));
+    KDB_CUDA(cudaStreamSynchronize(st));  // hrun is a host temporary
     fc[0] &= 0xffffffffull;  // block_count wrote the low 32-bit word
     m.exceptions = fc[0];
     // a saturated filter would send almost every entry down the slow path
@@ -1256,7 +1291,8 @@ kdb_status filter_phase(Mst& m, float eps, bool* overflow) {
     const int grid = (int)std::min<int64_t>((ntiles + kFilterWarps - 1) / kFilterWarps, 1 << 30);
 #define KDB_FILTER_LAUNCH2(V, F, CO, SM)                                                                         \
   LAUNCH_DYN((k_filter<V, F, CO, SM>), grid, kFilterThreads, kFilterSmem, st, R.nbr, R.dist, R.n_rows, m.ld, m.k,  \
-             m.tau, eps, R.row_begin, m.N, m.comp, rng, L.bloom, fd, R.hs[0], R.hs_cap, R.n_hs_dev, L.fcount + 1)
+             m.tau, eps, R.row_begin, m.N, m.comp, rng, L.bloom, fd, R.hs[0], R.hs_cap, R.n_hs_dev, L.fcount + 1, \
+             L.dom, L.brun, shift)
   // the row-within-tile division: a 32-bit multiply-high when exact (compile-time
   // branch: it runs once per 16-B chunk of the sweep)
 #define KDB_FILTER_LAUNCH(V, F, CO)                                                                              \

@@ -768,7 +768,12 @@ __global__ void __launch_bounds__(256) k_light_round(const int4* __restrict__ LE
     if (base >= n_in) break;
     for (int t = 0; t < chunk; t += 256) {
       const uint64_t s = base + t + threadIdx.x;
-      if (s >= n_in) continue;
+      // CAS: the warp's offers are min-reduced over runs of lanes offering to
+      // the same component before the CAS (warp-collective: every lane gets here)
+      bool have = false;
+      int32_t cseg = -1 - (int32_t)(threadIdx.x & 31);
+      uint64_t okey = ~0ull, ob = ~0ull;
+      if (s < n_in) {
       const int2 a = __ldcs(reinterpret_cast<const int2*>(act + s));
       const int32_t v = a.x;
       const int32_t cv = gat(comp + v);
@@ -783,8 +788,7 @@ __global__ void __launch_bounds__(256) k_light_round(const int4* __restrict__ LE
         if (lane == leader) base = atomicAdd(n_park, (uint32_t)__popc(am));
         base = __shfl_sync(am, base, leader);
         park[base + __popc(am & ((1u << lane) - 1u))] = Rec{v, a.y};
-        continue;
-      }
+      } else {
       const int64_t i = (int64_t)v - row_begin;
       const RowScan r = scan_ell<false, GW, PIPE>(LE + i * (kW / 2), nbr + i * ld, dist + i * ld, k, eps, v, cv, a.y,
                                                   N, comp, 0, reads, lvh);
@@ -795,13 +799,19 @@ __global__ void __launch_bounds__(256) k_light_round(const int4* __restrict__ LE
           // (b, target component) in the second word: the CAS-minimum orders by
           // (key, b) -- equal (key, b) is the same edge, hence the same target --
           // and the hook reads the target without gathering comp[]
-          min_pair128(KB + cv, r.best, ((uint64_t)r.bestb << 32) | (uint32_t)r.bestc);
+          have = true;
+          cseg = cv;
+          okey = r.best;
+          ob = ((uint64_t)r.bestb << 32) | (uint32_t)r.bestc;
         } else {
           if (precheck) min_offer(Kc + cv, (unsigned long long)r.best);
           else atomicMin(Kc + cv, (unsigned long long)r.best);
           s_off[j] = Offer{cv, r.bestb, r.best};
         }
       }
+      }
+      }
+      if (CAS) warp_min_pair128(KB, have, cseg, okey, ob);
     }
     __syncthreads();
     if (threadIdx.x == 0) s_base = s_n ? atomicAdd(n_out, s_n) : 0u;

@@ -1,0 +1,251 @@
+// kdb_tile.cuh -- round 1 of the light rows-Boruvka as tile-local Boruvka in shared memory
+// Part of kdb.cu's single translation unit: included inside its anonymous
+// namespace, after kdb_rows.cuh; not a standalone header.
+#pragma once
+
+// ============================================================================
+// Tile round (DESIGN.md §6 "Tile round").  The paper builds a LOCAL MST per
+// process before any exchange (Alg. 2) on points partitioned
+// so that a process's points are spatially compact; here the
+// same idea runs one level down: a CTA takes a tile of kTileRows consecutive
+// rows (a compact piece of the data set when the ids follow the partition),
+// stages the tile's light ELL rows in shared memory and runs Boruvka rounds on
+// the tile's components there, until no component of the tile can hook inside
+// it.  Exactness is the rows-Boruvka's own argument (reading #20): a
+// component's offer is the minimum over its rows' live entries -- entries
+// leaving the TILE included -- and it hooks only along a certified minimum
+// whose other end lies in the tile; a component whose minimum leaves the tile
+// (or cannot be decided from the ELL) waits, and may still absorb components
+// that hook into it (its minimum is then re-taken next round).  So every hook
+// is along an edge of the exact MSF (the cut property under the strict order
+// O1), mutual pairs resolve as in k_hook, and the global rounds continue from
+// the contracted components with the rows still live and their heads.
+//
+// Outputs, as round 1 of rows_phase: parent[c] for every dense core id (the
+// dense id of its in-tile root; depth <= 1), the MSF edges of the tile's hooks
+// (e_key/e_w layout of k_hook), the live rows with their heads, and the
+// counters (hooks, offered).  contract() then renumbers as after any round.
+#ifndef KDB_TILE_ROWS
+#define KDB_TILE_ROWS 1024
+#endif
+constexpr int kTileRows = KDB_TILE_ROWS;    // rows per tile = threads per CTA (one row per thread)
+constexpr int kTileMaxRounds = 48;          // safety bound; tiles converge in ~log2(tile) rounds
+constexpr int32_t kTgtOut = -2;             // the minimum leaves the tile or is undecidable in it
+
+struct TileSmem {
+  int2 E[kTileRows * kW];     // the tile's ELL rows: (J, w bits)
+  uint64_t K[kTileRows];      // per local root: minimum offered key
+  uint64_t ekey[kTileRows];   // staged MSF edges: (b << 32) | w bits
+  uint32_t ea[kTileRows];     //                    a
+  int32_t cvd[kTileRows];     // dense core id of the row (-1: non-core)
+  int32_t lc[kTileRows];      // local root (row index in the tile) of the row's component
+  int32_t par[kTileRows];     // per local root: hook target this round
+  int32_t tg[kTileRows];      // per local root: target of the minimum (kTgtOut: outside); then new root
+  uint32_t B[kTileRows];      // per local root: minimum b among offers of key K
+  uint32_t km[kTileRows];     // per local root: certificate bound (kmin, mono bits)
+  uint32_t wcnt[kTileRows / 32];
+  uint32_t tile, n_edges, edge_base, live_base;
+};
+
+__global__ void __launch_bounds__(kTileRows) k_tile_round(
+    const int4* __restrict__ LE, int64_t n_rows, int32_t k, float eps, int64_t N,
+    const int32_t* __restrict__ comp, const uint32_t* __restrict__ core_bits, const uint32_t* __restrict__ kmin,
+    int32_t* __restrict__ parent,
+    uint64_t* __restrict__ e_key, float* __restrict__ e_w, int64_t e_cap, Rec* __restrict__ act_out,
+    uint32_t* __restrict__ n_out, uint32_t* __restrict__ grab, RoundCounters* __restrict__ ctr,
+    unsigned long long* __restrict__ n_entries) {
+  extern __shared__ __align__(16) unsigned char tile_smem_raw[];
+  TileSmem& S = *reinterpret_cast<TileSmem*>(tile_smem_raw);
+  const int i = threadIdx.x;
+  const int lane = i & 31, wid = i >> 5;
+  uint32_t hooks = 0, offered = 0;
+  unsigned long long reads = 0;
+  for (;;) {
+    if (i == 0) { S.tile = atomicAdd(grab, 1u); S.n_edges = 0; }
+    __syncthreads();
+    const int64_t r0 = (int64_t)S.tile * kTileRows;
+    if (r0 >= n_rows) break;
+    const int nr = (int)min((int64_t)kTileRows, n_rows - r0);
+    {  // the tile's ELL rows: nr * 128 contiguous bytes
+      const int4* src = LE + r0 * (kW / 2);
+      int4* dst = reinterpret_cast<int4*>(S.E);
+      for (int q = i; q < nr * (kW / 2); q += kTileRows) dst[q] = __ldcs(src + q);
+    }
+    const int64_t v = r0 + i;
+    const int32_t cv = i < nr ? __ldg(comp + v) : -1;
+    __syncthreads();  // the tile's ELL is staged
+    if (cv >= 0) {
+      // entries leaving the tile: core test once, from the (L2-resident) core
+      // bits, so the rounds below read shared memory only -- a non-core
+      // target (or padding, or self) becomes J = -1 (never a candidate)
+      int2* er = S.E + i * kW;
+#pragma unroll
+      for (int c = 0; c < kW; ++c) {
+        const int2 e = er[c];
+        const int32_t J = e.x;
+        if (!(__int_as_float(e.y) <= eps)) continue;  // never read by the scans
+        const bool in_tile = J >= r0 && J < r0 + nr;
+        if (J < 0 || J >= N || J == v || (!in_tile && !is_core(core_bits, J))) er[c].x = -1;
+      }
+    }
+    S.cvd[i] = cv;
+    S.lc[i] = cv >= 0 ? i : -1;
+    S.K[i] = kSent;
+    S.B[i] = kSentB;
+    S.tg[i] = -1;
+    S.km[i] = cv >= 0 ? __ldg(kmin + cv) : kInfBits;
+    bool live = cv >= 0;  // the row still has (or may have) a leaving light entry
+    int head = 0;
+    __syncthreads();
+    for (int rr = 0; rr < kTileMaxRounds; ++rr) {
+      // ---- offers: the row's first leaving entry group (ties on w), from its head
+      uint64_t best = kSent;
+      uint32_t bestb = kSentB;
+      int32_t btg = -1;
+      const int32_t myc = live ? S.lc[i] : -1;
+      if (live) {
+        bool found = false, done = false;
+        uint32_t wstar = 0;
+        int c = head;
+        for (; c < kW; ++c) {
+          const int2 e = S.E[i * kW + c];
+          const float w = __int_as_float(e.y);
+          const uint32_t wb = mono_bits(w);
+          if (!found) {
+            if (!(w <= eps)) { done = true; break; }  // sorted: nothing left
+          } else if (wb != wstar) {
+            done = true;
+            break;
+          }
+          ++reads;
+          const int32_t J = e.x;
+          int32_t t = -1;
+          if (J >= 0) {  // (staged: J valid, not v; outside the tile only if core)
+            if (J >= r0 && J < r0 + nr) {
+              const int lj = (int)(J - r0);
+              t = S.cvd[lj] >= 0 ? S.lc[lj] : -1;
+              if (t == myc) t = -1;  // intra: dead for good (components only grow)
+            } else {
+              t = kTgtOut;  // outside the tile: another component
+            }
+          }
+          if (t == -1) {
+            if (!found) head = c + 1;
+            continue;
+          }
+          const uint64_t kk = pack_key(wb, (uint32_t)min(v, (int64_t)J));
+          const uint32_t bb = (uint32_t)max(v, (int64_t)J);
+          if (!found) {
+            found = true;
+            wstar = wb;
+            best = kk;
+            bestb = bb;
+            btg = t;
+          } else if (kk < best || (kk == best && bb < bestb)) {
+            best = kk;
+            bestb = bb;
+            btg = t;
+          }
+        }
+        if (!done && k > kW) {
+          // the candidate prefix (or the minimum's tie group) runs past the ELL:
+          // the row's next entries are unknown here -- a lower bound (w of the
+          // last ELL entry, a = b = 0, below every real key of that weight)
+          // keeps the component from hooking on anything heavier
+          best = pack_key(mono_bits(__int_as_float(S.E[i * kW + kW - 1].y)), 0u);
+          bestb = 0u;
+          btg = kTgtOut;
+          found = true;
+        }
+        if (!found) live = false;
+      }
+      if (best != kSent) atomicMin(reinterpret_cast<unsigned long long*>(&S.K[myc]), (unsigned long long)best);
+      __syncthreads();
+      if (best != kSent && best == S.K[myc]) atomicMin(&S.B[myc], bestb);
+      __syncthreads();
+      if (best != kSent && best == S.K[myc] && bestb == S.B[myc]) S.tg[myc] = btg;  // one edge: one target
+      __syncthreads();
+      // ---- hooks: thread i acts for local root i
+      const bool root = cv >= 0 && S.lc[i] == i;
+      int p = i;
+      bool offers = false;
+      if (root) {
+        const uint64_t K = S.K[i];
+        if (K != kSent) {
+          offers = true;
+          const int32_t t = S.tg[i];
+          if (t >= 0 && (uint32_t)(K >> 32) < S.km[i]) {  // inside the tile and certified
+            const uint32_t b = S.B[i];
+            const uint64_t Kt = S.K[t];
+            const bool cert_t = Kt != kSent && (uint32_t)(Kt >> 32) < S.km[t];
+            const bool mutual = cert_t && Kt == K && S.B[t] == b;
+            if (!(mutual && i < t)) {
+              p = t;
+              const uint32_t j = atomicAdd(&S.n_edges, 1u);
+              S.ekey[j] = ((uint64_t)b << 32) | (uint32_t)(K >> 32);
+              S.ea[j] = (uint32_t)K;
+            }
+          }
+        }
+      }
+      if (root) S.par[i] = p;
+      const int nh = __syncthreads_count(p != i);
+      hooks += (i == 0) ? (uint32_t)nh : 0u;
+      if (nh == 0) {
+        offered += (uint32_t)__syncthreads_count(offers) * (i == 0);
+        break;
+      }
+      // ---- contraction: each root follows the hook forest to its new root
+      int nroot = i;
+      if (root) {
+        int q = p, guard = 0;
+        while (S.par[q] != q && ++guard < kTileRows) q = S.par[q];
+        nroot = q;
+      }
+      __syncthreads();
+      if (root) {
+        S.tg[i] = nroot;
+        if (nroot != i) atomicMin(&S.km[nroot], S.km[i]);
+      }
+      __syncthreads();
+      const int32_t nl = cv >= 0 ? S.tg[S.lc[i]] : -1;
+      __syncthreads();
+      if (cv >= 0) S.lc[i] = nl;
+      S.K[i] = kSent;
+      S.B[i] = kSentB;
+      S.tg[i] = -1;
+      __syncthreads();
+    }
+    // ---- outputs: parent of every core row's dense id, live rows, MSF edges
+    if (cv >= 0) parent[cv] = S.cvd[S.lc[i]];
+    const unsigned lm = __ballot_sync(0xffffffffu, live);
+    if (lane == 0) S.wcnt[wid] = __popc(lm);
+    __syncthreads();
+    if (i == 0) {
+      uint32_t tot = 0;
+      for (int w = 0; w < kTileRows / 32; ++w) {
+        const uint32_t c = S.wcnt[w];
+        S.wcnt[w] = tot;
+        tot += c;
+      }
+      S.live_base = tot ? atomicAdd(n_out, tot) : 0u;
+      S.edge_base = S.n_edges ? atomicAdd(&ctr->msf_count, S.n_edges) : 0u;
+    }
+    __syncthreads();
+    if (live) act_out[S.live_base + S.wcnt[wid] + __popc(lm & ((1u << lane) - 1u))] = Rec{(int32_t)v, head};
+    for (uint32_t j = i; j < S.n_edges; j += kTileRows) {
+      const uint64_t slot = (uint64_t)S.edge_base + j;
+      if ((int64_t)slot < e_cap) {
+        e_key[slot] = S.ekey[j];
+        reinterpret_cast<uint32_t*>(e_w)[slot] = S.ea[j];
+      }
+    }
+    __syncthreads();
+  }
+  if (i == 0) {
+    if (hooks) atomicAdd(&ctr->hooks, hooks);
+    if (hooks + offered) atomicAdd(&ctr->offered, hooks + offered);
+  }
+  for (int o = 16; o > 0; o >>= 1) reads += __shfl_xor_sync(0xffffffffu, reads, o);
+  if (lane == 0 && reads) atomicAdd(n_entries, reads);
+}

@@ -35,10 +35,10 @@ def _golden(name):
     return json.load(open(os.path.join(ROOT, "tests", "golden", f"window_oracle_{name}.json")))
 
 
-def _run(config, scale, live_window=None):
+def _run(config, scale, live_window=None, order="inertial"):
     import bench
-    W = bench.make_workload(config, scale, 0, torch.device("cuda:0"))
-    gold = _golden(config if scale == 1.0 else config + "q")
+    W = bench.make_workload(config, scale, 0, torch.device("cuda:0"), order=order)
+    gold = _golden((config if scale == 1.0 else config + "q") + ("i" if order == "inertial" else ""))
     assert gold["N"] == W["N"] and gold["k"] == W["k"] and gold["M"] == W["M"]
     assert f"{np.float32(W['eps']).view(np.uint32):08x}" == gold["eps_bits"]
     N = W["N"]
@@ -51,12 +51,14 @@ def _run(config, scale, live_window=None):
     wins = wc.cluster_windows(W["truth"])
     assert len(wins) == len(gold["windows"]) == 10
     covered = 0
-    for i, (s, e) in enumerate(wins):
+    for i, win in enumerate(wins):
         gw = gold["windows"][str(i)]
-        assert (gw["s"], gw["e"]) == (s, e)
-        assert wc.window_closed(W["nbr"], s, e), f"window {i} not closed"
-        assert wc.input_checksum(W["nbr"], W["dist"], s, e) == gw["input_checksum"], f"window {i}: input changed"
-        got = wc.gpu_window(full, s, e)
+        if wc.is_range(win):
+            assert (gw["s"], gw["e"]) == win
+        assert gw.get("n", wc.win_size(win)) == wc.win_size(win)
+        assert wc.window_closed(W["nbr"], win), f"window {i} not closed"
+        assert wc.input_checksum(W["nbr"], W["dist"], win) == gw["input_checksum"], f"window {i}: input changed"
+        got = wc.gpu_window(full, win)
         assert got["edges_inside"]
         covered += got["span"][1] - got["span"][0]
         assert len(got["msf_a"]) == gw["msf_edges"]
@@ -67,12 +69,12 @@ def _run(config, scale, live_window=None):
     tot = sum(w["msf_weight"] for w in gold["windows"].values())
     assert abs(r.weight - tot) <= 1e-6 * tot
     if live_window is not None:  # the oracle itself, element by element, on one window
-        s, e = wins[live_window]
-        nw, dw = wc.window_graph_host(W["nbr"], W["dist"], s, e)
+        win = wins[live_window]
+        nw, dw = wc.window_graph_host(W["nbr"], W["dist"], win)
         del W
         exp = wc.run_oracle(nw, dw, gold["M"], float(np.float32(np.uint32(int(gold["eps_bits"], 16)).view(np.float32))))
         assert exp["digest"] == gold["windows"][str(live_window)]["oracle_digest"]
-        assert wc.compare(wc.gpu_window(full, s, e), exp) == []
+        assert wc.compare(wc.gpu_window(full, win), exp) == []
 
 
 def test_c4_full_size_windows_match_oracle():
@@ -81,3 +83,8 @@ def test_c4_full_size_windows_match_oracle():
 
 def test_c5_quarter_scale_windows_match_oracle():
     _run("C5", 0.25)
+
+
+def test_c4_full_size_windows_generation_order():
+    """The same parity with the generator's cluster-major ids (windows are id ranges)."""
+    _run("C4", 1.0, order="generation")

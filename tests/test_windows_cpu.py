@@ -19,9 +19,14 @@ from datagen import CONFIGS, gen_config_points, knn_bruteforce
 from tests import window_check as wc
 
 
-@pytest.mark.parametrize("name,scale", [("C4", 0.00015), ("C5", 0.00004)])
-def test_whole_graph_oracle_is_union_of_windows(name, scale):
+@pytest.mark.parametrize("name,scale,order", [("C4", 0.00015, "generation"), ("C5", 0.00004, "generation"),
+                                              ("C4", 0.00015, "inertial")])
+def test_whole_graph_oracle_is_union_of_windows(name, scale, order):
     X, truth = gen_config_points(name, 0, scale)
+    if order == "inertial":  # clusters become id sets, not ranges
+        from datagen.partition import inertial_order
+        perm = inertial_order(X, device="cpu")
+        X, truth = X[perm], truth[perm]
     k, M = 32, 16  # smaller rows keep the brute force quick; the argument does not depend on k
     nbr, dist = knn_bruteforce(X, k)
     eps = float(np.float32(CONFIGS[name]["eps_factor"] * np.median(dist[:, M - 1].astype(np.float64))))
@@ -32,12 +37,13 @@ def test_whole_graph_oracle_is_union_of_windows(name, scale):
     assert len(wins) == 10
     tn, td = torch.from_numpy(nbr), torch.from_numpy(dist)
     total, edges = 0.0, 0
-    for s, e in wins:
-        assert wc.window_closed(tn, s, e)
-        nw, dw = wc.window_graph_host(tn, td, s, e)
-        assert nw.min() >= 0 and nw.max() < e - s
+    assert all(wc.is_range(w) for w in wins) == (order == "generation")
+    for win in wins:
+        assert wc.window_closed(tn, win)
+        nw, dw = wc.window_graph_host(tn, td, win)
+        assert nw.min() >= 0 and nw.max() < wc.win_size(win)
         r = wc.run_oracle(nw, dw, M, eps)
-        got = wc.gpu_window(res, s, e)
+        got = wc.gpu_window(res, win)
         assert wc.compare(got, r) == []
         assert wc.digest(got["core"], got["labels"], got["msf_a"], got["msf_b"], got["msf_w"]) == r["digest"]
         total += r["msf_weight"]

@@ -61,6 +61,8 @@ def main():
     ap.add_argument("--config", default="C4", choices=["C4", "C5"])
     ap.add_argument("--scale", type=float, default=1.0)
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--order", default="inertial", choices=["inertial", "generation"],
+                    help="point order of the workload (bench.py --order)")
     ap.add_argument("--workers", type=int, default=4)
     ap.add_argument("--windows", default="all", help="'all' or a comma list of window indices")
     ap.add_argument("--out", default=None)
@@ -68,16 +70,16 @@ def main():
     args = ap.parse_args()
     torch.cuda.set_device(0)
     t0 = time.time()
-    W = bench.make_workload(args.config, args.scale, args.seed, torch.device("cuda:0"))
+    W = bench.make_workload(args.config, args.scale, args.seed, torch.device("cuda:0"), order=args.order)
     N, k, M, eps = W["N"], W["k"], W["M"], W["eps"]
     full = gpu_full_run(W)
     wins = wc.cluster_windows(W["truth"])
     sel = range(len(wins)) if args.windows == "all" else [int(x) for x in args.windows.split(",")]
     print(f"[windows] {args.config} x{args.scale}: N={N} k={k} M={M} eps={eps!r} windows={len(wins)} "
           f"gpu step {full['wall_s']:.3f} s", flush=True)
-    need = int(36 * k * max(e - s for s, e in wins) + (1 << 30))
+    need = int(36 * k * max(wc.win_size(w) for w in wins) + (1 << 30))
     workers = max(1, min(args.workers, int(wc.MemGate.available() // need), len(sel)))
-    log = dict(config=args.config, scale=args.scale, seed=args.seed, N=N, k=k, M=M, eps=eps,
+    log = dict(config=args.config, scale=args.scale, seed=args.seed, order=args.order, N=N, k=k, M=M, eps=eps,
                eps_bits=f"{np.float32(eps).view(np.uint32):08x}", gpu=dict(
                    msf_edges=full["count"], msf_weight=full["msf_weight"], stats=full["stats"]),
                path="kdb_core_mark -> kdb_mst -> kdb_label, KDB_GRAPH_EXACT, default knobs (bench.py step)",
@@ -88,36 +90,39 @@ def main():
     golden = {}
     results = {}
     t_pool = time.perf_counter()
-    def finish(i, s, e, chk, r):
-        got = wc.gpu_window(full, s, e)
+    def finish(i, win, chk, r):
+        got = wc.gpu_window(full, win)
+        s, e = win if wc.is_range(win) else (None, None)
         bad = wc.compare(got, r)
         gdig = wc.digest(got["core"], got["labels"], got["msf_a"], got["msf_b"], got["msf_w"])
-        results[i] = dict(index=i, s=s, e=e, closed=True, input_checksum=chk, ok=not bad, failures=bad,
+        results[i] = dict(index=i, s=s, e=e, n=wc.win_size(win), closed=True, input_checksum=chk, ok=not bad,
+                          failures=bad,
                           core=int(r["core"].sum()), msf_edges=int(len(r["msf_a"])),
                           oracle_weight=r["msf_weight"], gpu_weight_window=got["msf_weight"],
                           oracle_digest=r["digest"], gpu_digest=gdig,
                           oracle_s=dict(core=r["times"][0], msf=r["times"][1], border=r["times"][2],
                                         wall=r["wall_s"]))
-        golden[str(i)] = dict(s=s, e=e, input_checksum=chk, oracle_digest=r["digest"],
+        golden[str(i)] = dict(s=s, e=e, n=wc.win_size(win), input_checksum=chk, oracle_digest=r["digest"],
                               msf_edges=int(len(r["msf_a"])), msf_weight=r["msf_weight"])
-        print(f"[window {i}] [{s},{e}) ok={not bad} {bad} oracle {r['wall_s']:.1f} s "
+        print(f"[window {i}] n={wc.win_size(win)} ok={not bad} {bad} oracle {r['wall_s']:.1f} s "
               f"msf={len(r['msf_a'])}", flush=True)
 
     with cf.ThreadPoolExecutor(max_workers=workers) as pool:
         running = {}
         for i in sel:
-            s, e = wins[i]
-            closed = wc.window_closed(W["nbr"], s, e)
-            chk = wc.input_checksum(W["nbr"], W["dist"], s, e)
+            win = wins[i]
+            closed = wc.window_closed(W["nbr"], win)
+            chk = wc.input_checksum(W["nbr"], W["dist"], win)
             if not closed:
-                results[i] = dict(index=i, s=s, e=e, closed=False, ok=False, failures=["window not closed"])
+                results[i] = dict(index=i, n=wc.win_size(win), closed=False, ok=False,
+                                  failures=["window not closed"])
                 continue
             while len(running) >= workers:  # bound the host copies in flight by the workers
                 done, _ = cf.wait(list(running), return_when=cf.FIRST_COMPLETED)
                 for f in done:
                     finish(*running.pop(f), f.result())
-            nbr_w, dist_w = wc.window_graph_host(W["nbr"], W["dist"], s, e)
-            running[pool.submit(wc.run_oracle, nbr_w, dist_w, M, eps)] = (i, s, e, chk)
+            nbr_w, dist_w = wc.window_graph_host(W["nbr"], W["dist"], win)
+            running[pool.submit(wc.run_oracle, nbr_w, dist_w, M, eps)] = (i, win, chk)
             del nbr_w, dist_w
         for f in cf.as_completed(list(running)):
             finish(*running.pop(f), f.result())
@@ -148,7 +153,7 @@ def main():
         os.makedirs(os.path.dirname(os.path.abspath(args.out)), exist_ok=True)
         json.dump(log, open(args.out, "w"), indent=1, default=str)
     if args.golden and golden:
-        g = dict(config=args.config, scale=args.scale, seed=args.seed, N=N, k=k, M=M,
+        g = dict(config=args.config, scale=args.scale, seed=args.seed, order=args.order, N=N, k=k, M=M,
                  eps_bits=log["eps_bits"],
                  source="tools/window_parity.py: oracle/ (kdb_oracle.cpp) run on each exact cluster window; "
                         "digest = tests/window_check.py digest() of the oracle's window-local outputs",
