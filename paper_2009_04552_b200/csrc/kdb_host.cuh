@@ -552,7 +552,7 @@ kdb_status rows_phase(Mst& m, float eps_run) {
   // (with a reused ELL round 1 runs over it: k_light_first)
   // tile round (one rank, exact mode, light ELL): round 1 is tile-local
   // Boruvka in shared memory (k_tile_round) instead of the fused singleton round
-  tile = want.valid && want.row_begin == 0 && env_int("KDB_TILE", 1) != 0 && L.ranks[0].n_rows > 0;
+  tile = want.valid && want.row_begin == 0 && env_int("KDB_TILE", 0) != 0 && L.ranks[0].n_rows > 0;
   fuse1 = !general && use_compact && env_int("KDB_FUSE1", 1) != 0 && !reuse && !tile;
   packed1 = fuse1 && L.ranks.size() == 1 && !(multi_rank(comm)) && env_int("KDB_PACK1", 1) != 0;
   // Per-component slots of round 1.  Packed round 1 (one rank, fused ELL pass)
