@@ -764,10 +764,14 @@ kdb_status rows_phase(Mst& m, float eps_run) {
       KDB_CUDA(cudaMemsetAsync(&R.ctr->na[cur ^ 1], 0, sizeof(uint32_t), st));
       KDB_CUDA(cudaMemsetAsync(&R.ctr->grab, 0, sizeof(uint32_t), st));
       KDB_CUDA(cudaMemsetAsync(&L.ctr->hooks, 0, 4 * sizeof(uint32_t), st));
-      const int64_t ntiles = (R.n_rows + kTileRows - 1) / kTileRows;
-      LAUNCH_DYN(k_tile_round, (int)std::min<int64_t>(ntiles, 1 << 30), kTileRows, sizeof(TileSmem), st, R.LE,
-                 R.n_rows, k, eps_run, N, comp, core_bits, L.kmin, L.parent, L.e_key, L.e_w, ecap, R.act[cur ^ 1],
-                 &R.ctr->na[cur ^ 1], &R.ctr->grab, L.ctr, &L.ctr->entries);
+#define KDB_TILE_LAUNCH(T)                                                                                     \
+  LAUNCH_DYN(k_tile_round<T>, (int)std::min<int64_t>((R.n_rows + (T) - 1) / (T), 1 << 30), (T),                 \
+             sizeof(TileSmem<T>), st, R.LE, R.n_rows, k, eps_run, N, comp, core_bits, L.kmin, L.parent, L.e_key, \
+             L.e_w, ecap, R.act[cur ^ 1], &R.ctr->na[cur ^ 1], &R.ctr->grab, L.ctr, &L.ctr->entries,      \
+             std::max(1, std::min(env_int("KDB_TILE_MAXR", kTileMaxRounds), kTileMaxRounds)))
+      if (env_int("KDB_TILE_ROWS", 1024) == 512) KDB_TILE_LAUNCH(512);
+      else KDB_TILE_LAUNCH(1024);
+#undef KDB_TILE_LAUNCH
       KDB_CUDA(cudaGetLastError());
     } else {
     // offers read the current key before their atomicMin once many rows offer

@@ -25,15 +25,15 @@
 // dense id of its in-tile root; depth <= 1), the MSF edges of the tile's hooks
 // (e_key/e_w layout of k_hook), the live rows with their heads, and the
 // counters (hooks, offered).  contract() then renumbers as after any round.
-#ifndef KDB_TILE_ROWS
-#define KDB_TILE_ROWS 1024
-#endif
-constexpr int kTileRows = KDB_TILE_ROWS;    // rows per tile = threads per CTA (one row per thread)
+// rows per tile = threads per CTA (one row per thread): 1,024 (one CTA per SM)
+// or 512 (two CTAs per SM: one stages its tile while the other runs rounds)
 constexpr int kTileMaxRounds = 48;          // safety bound; tiles converge in ~log2(tile) rounds
 constexpr int32_t kTgtOut = -2;             // the minimum leaves the tile or is undecidable in it
+constexpr int kDead = -1, kOut = -2, kEnd = -3;  // entry codes (else: the target's row in the tile)
 
+template <int kTileRows>
 struct TileSmem {
-  int2 E[kTileRows * kW];     // the tile's ELL rows: (J, w bits)
+  int2 E[kW * kTileRows];     // the tile's ELL, column-major: E[c * T + row] = (J, w bits)
   uint64_t K[kTileRows];      // per local root: minimum offered key
   uint64_t ekey[kTileRows];   // staged MSF edges: (b << 32) | w bits
   uint32_t ea[kTileRows];     //                    a
@@ -41,21 +41,23 @@ struct TileSmem {
   int32_t lc[kTileRows];      // local root (row index in the tile) of the row's component
   int32_t par[kTileRows];     // per local root: hook target this round
   int32_t tg[kTileRows];      // per local root: target of the minimum (kTgtOut: outside); then new root
-  uint32_t B[kTileRows];      // per local root: minimum b among offers of key K
+  uint64_t BT[kTileRows];     // per local root: (b << 32 | target + 2), minimum among offers of key K
   uint32_t km[kTileRows];     // per local root: certificate bound (kmin, mono bits)
+  int16_t code[kW * kTileRows];  // per ELL entry (column-major): target row in the tile, or kOut / kDead / kEnd
   uint32_t wcnt[kTileRows / 32];
   uint32_t tile, n_edges, edge_base, live_base;
 };
 
+template <int kTileRows>
 __global__ void __launch_bounds__(kTileRows) k_tile_round(
     const int4* __restrict__ LE, int64_t n_rows, int32_t k, float eps, int64_t N,
     const int32_t* __restrict__ comp, const uint32_t* __restrict__ core_bits, const uint32_t* __restrict__ kmin,
     int32_t* __restrict__ parent,
     uint64_t* __restrict__ e_key, float* __restrict__ e_w, int64_t e_cap, Rec* __restrict__ act_out,
     uint32_t* __restrict__ n_out, uint32_t* __restrict__ grab, RoundCounters* __restrict__ ctr,
-    unsigned long long* __restrict__ n_entries) {
+    unsigned long long* __restrict__ n_entries, int max_rounds) {
   extern __shared__ __align__(16) unsigned char tile_smem_raw[];
-  TileSmem& S = *reinterpret_cast<TileSmem*>(tile_smem_raw);
+  TileSmem<kTileRows>& S = *reinterpret_cast<TileSmem<kTileRows>*>(tile_smem_raw);
   const int i = threadIdx.x;
   const int lane = i & 31, wid = i >> 5;
   uint32_t hooks = 0, offered = 0;
@@ -66,104 +68,113 @@ __global__ void __launch_bounds__(kTileRows) k_tile_round(
     const int64_t r0 = (int64_t)S.tile * kTileRows;
     if (r0 >= n_rows) break;
     const int nr = (int)min((int64_t)kTileRows, n_rows - r0);
-    {  // the tile's ELL rows: nr * 128 contiguous bytes
+    {  // the tile's ELL rows (nr * 128 contiguous bytes, coalesced) into COLUMN-major
+       // shared memory: E[c * T + row], so a warp's 32 rows read one column
+       // without bank conflicts (row-major 128-B rows put them all in one bank)
       const int4* src = LE + r0 * (kW / 2);
-      int4* dst = reinterpret_cast<int4*>(S.E);
-      for (int q = i; q < nr * (kW / 2); q += kTileRows) dst[q] = __ldcs(src + q);
+      for (int q = i; q < nr * (kW / 2); q += kTileRows) {
+        const int4 x = __ldcs(src + q);
+        const int r = q / (kW / 2), c = 2 * (q % (kW / 2));
+        S.E[c * kTileRows + r] = make_int2(x.x, x.y);
+        S.E[(c + 1) * kTileRows + r] = make_int2(x.z, x.w);
+      }
     }
     const int64_t v = r0 + i;
     const int32_t cv = i < nr ? __ldg(comp + v) : -1;
-    __syncthreads();  // the tile's ELL is staged
+    S.cvd[i] = cv;
+    __syncthreads();  // the tile's ELL and core flags are staged
     if (cv >= 0) {
-      // entries leaving the tile: core test once, from the (L2-resident) core
-      // bits, so the rounds below read shared memory only -- a non-core
-      // target (or padding, or self) becomes J = -1 (never a candidate)
-      int2* er = S.E + i * kW;
+      // one code per entry, so the rounds below read shared memory only:
+      // kEnd (w > eps: the sorted row ends), kDead (padding, self, non-core
+      // target -- the core test of targets outside the tile once, from the
+      // L2-resident core bits), kOut (a core vertex outside the tile: always
+      // another component), else the target's row in the tile
+      const int2* er = S.E + i;       // column c of row i at [c * T]
+      int16_t* cr = S.code + i;
 #pragma unroll
       for (int c = 0; c < kW; ++c) {
-        const int2 e = er[c];
+        const int2 e = er[c * kTileRows];
         const int32_t J = e.x;
-        if (!(__int_as_float(e.y) <= eps)) continue;  // never read by the scans
-        const bool in_tile = J >= r0 && J < r0 + nr;
-        if (J < 0 || J >= N || J == v || (!in_tile && !is_core(core_bits, J))) er[c].x = -1;
+        int cd;
+        if (!(__int_as_float(e.y) <= eps)) cd = kEnd;
+        else if (J < 0 || J >= N || J == v) cd = kDead;
+        else if (J >= r0 && J < r0 + nr) cd = S.cvd[J - r0] >= 0 ? (int)(J - r0) : kDead;
+        else cd = is_core(core_bits, J) ? kOut : kDead;
+        cr[c * kTileRows] = (int16_t)cd;
       }
     }
-    S.cvd[i] = cv;
     S.lc[i] = cv >= 0 ? i : -1;
     S.K[i] = kSent;
-    S.B[i] = kSentB;
+    S.BT[i] = ~0ull;
     S.tg[i] = -1;
     S.km[i] = cv >= 0 ? __ldg(kmin + cv) : kInfBits;
     bool live = cv >= 0;  // the row still has (or may have) a leaving light entry
     int head = 0;
     __syncthreads();
-    for (int rr = 0; rr < kTileMaxRounds; ++rr) {
+    for (int rr = 0; rr < max_rounds; ++rr) {
       // ---- offers: the row's first leaving entry group (ties on w), from its head
       uint64_t best = kSent;
       uint32_t bestb = kSentB;
       int32_t btg = -1;
       const int32_t myc = live ? S.lc[i] : -1;
       if (live) {
-        bool found = false, done = false;
-        uint32_t wstar = 0;
-        int c = head;
-        for (; c < kW; ++c) {
-          const int2 e = S.E[i * kW + c];
-          const float w = __int_as_float(e.y);
-          const uint32_t wb = mono_bits(w);
-          if (!found) {
-            if (!(w <= eps)) { done = true; break; }  // sorted: nothing left
-          } else if (wb != wstar) {
-            done = true;
-            break;
-          }
-          ++reads;
-          const int32_t J = e.x;
-          int32_t t = -1;
-          if (J >= 0) {  // (staged: J valid, not v; outside the tile only if core)
-            if (J >= r0 && J < r0 + nr) {
-              const int lj = (int)(J - r0);
-              t = S.cvd[lj] >= 0 ? S.lc[lj] : -1;
-              if (t == myc) t = -1;  // intra: dead for good (components only grow)
-            } else {
-              t = kTgtOut;  // outside the tile: another component
-            }
-          }
-          if (t == -1) {
-            if (!found) head = c + 1;
-            continue;
-          }
-          const uint64_t kk = pack_key(wb, (uint32_t)min(v, (int64_t)J));
-          const uint32_t bb = (uint32_t)max(v, (int64_t)J);
-          if (!found) {
-            found = true;
-            wstar = wb;
-            best = kk;
-            bestb = bb;
-            btg = t;
-          } else if (kk < best || (kk == best && bb < bestb)) {
-            best = kk;
-            bestb = bb;
-            btg = t;
-          }
+        const int16_t* cr = S.code + i;
+        const int head0 = head;
+        int c = head, fc = -1;
+        int32_t t = -1;
+        for (; c < kW; ++c) {  // dead entries before the first leaving one stay dead
+          const int cd = cr[c * kTileRows];
+          if (cd == kEnd) break;
+          if (cd == kDead) { head = c + 1; continue; }
+          t = cd == kOut ? kTgtOut : S.lc[cd];
+          if (t == myc) { head = c + 1; continue; }  // intra: dead for good (components only grow)
+          fc = c;
+          break;
         }
-        if (!done && k > kW) {
+        reads += (unsigned long long)(min(c + 1, kW) - head0);
+        bool open_end = false;  // the decision may depend on entries past the ELL
+        if (fc >= 0) {
+          const int2 e = S.E[fc * kTileRows + i];
+          const uint32_t wstar = mono_bits(__int_as_float(e.y));
+          const uint32_t vu = (uint32_t)v;
+          best = pack_key(wstar, min(vu, (uint32_t)e.x));
+          bestb = max(vu, (uint32_t)e.x);
+          btg = t;
+          int c2 = fc + 1;
+          for (; c2 < kW; ++c2) {  // the tie group of the minimum's weight
+            const int2 e2 = S.E[c2 * kTileRows + i];
+            if (mono_bits(__int_as_float(e2.y)) != wstar) break;
+            const int cd = cr[c2 * kTileRows];
+            if (cd < 0 && cd != kOut) continue;
+            const int32_t t2 = cd == kOut ? kTgtOut : S.lc[cd];
+            if (t2 == myc) continue;
+            const uint64_t kk = pack_key(wstar, min(vu, (uint32_t)e2.x));
+            const uint32_t bb = max(vu, (uint32_t)e2.x);
+            if (kk < best || (kk == best && bb < bestb)) { best = kk; bestb = bb; btg = t2; }
+          }
+          open_end = c2 == kW;
+        } else {
+          open_end = c == kW;  // every ELL entry is within eps and dead
+        }
+        if (open_end && k > kW) {
           // the candidate prefix (or the minimum's tie group) runs past the ELL:
           // the row's next entries are unknown here -- a lower bound (w of the
           // last ELL entry, a = b = 0, below every real key of that weight)
           // keeps the component from hooking on anything heavier
-          best = pack_key(mono_bits(__int_as_float(S.E[i * kW + kW - 1].y)), 0u);
+          best = pack_key(mono_bits(__int_as_float(S.E[(kW - 1) * kTileRows + i].y)), 0u);
           bestb = 0u;
           btg = kTgtOut;
-          found = true;
+        } else if (fc < 0) {
+          live = false;
         }
-        if (!found) live = false;
       }
       if (best != kSent) atomicMin(reinterpret_cast<unsigned long long*>(&S.K[myc]), (unsigned long long)best);
       __syncthreads();
-      if (best != kSent && best == S.K[myc]) atomicMin(&S.B[myc], bestb);
-      __syncthreads();
-      if (best != kSent && best == S.K[myc] && bestb == S.B[myc]) S.tg[myc] = btg;  // one edge: one target
+      // ties on the key: the smallest b wins and carries its target (equal
+      // (key, b) is one edge, hence one target)
+      if (best != kSent && best == S.K[myc])
+        atomicMin(reinterpret_cast<unsigned long long*>(&S.BT[myc]),
+                  (unsigned long long)(((uint64_t)bestb << 32) | (uint32_t)(btg + 2)));
       __syncthreads();
       // ---- hooks: thread i acts for local root i
       const bool root = cv >= 0 && S.lc[i] == i;
@@ -173,12 +184,13 @@ __global__ void __launch_bounds__(kTileRows) k_tile_round(
         const uint64_t K = S.K[i];
         if (K != kSent) {
           offers = true;
-          const int32_t t = S.tg[i];
+          const uint64_t bt = S.BT[i];
+          const int32_t t = (int32_t)(uint32_t)bt - 2;
           if (t >= 0 && (uint32_t)(K >> 32) < S.km[i]) {  // inside the tile and certified
-            const uint32_t b = S.B[i];
+            const uint32_t b = (uint32_t)(bt >> 32);
             const uint64_t Kt = S.K[t];
             const bool cert_t = Kt != kSent && (uint32_t)(Kt >> 32) < S.km[t];
-            const bool mutual = cert_t && Kt == K && S.B[t] == b;
+            const bool mutual = cert_t && Kt == K && (uint32_t)(S.BT[t] >> 32) == b;
             if (!(mutual && i < t)) {
               p = t;
               const uint32_t j = atomicAdd(&S.n_edges, 1u);
@@ -212,7 +224,7 @@ __global__ void __launch_bounds__(kTileRows) k_tile_round(
       __syncthreads();
       if (cv >= 0) S.lc[i] = nl;
       S.K[i] = kSent;
-      S.B[i] = kSentB;
+      S.BT[i] = ~0ull;
       S.tg[i] = -1;
       __syncthreads();
     }
