@@ -492,7 +492,9 @@ kdb_status rows_phase(Mst& m, float eps_run) {
   const int gw = env_int("KDB_GW", 4);  // component-gather width of the later light rounds (scan_ell)
   const bool sparse_ids = env_int("KDB_SPARSE", 1) != 0;  // keep root ids once few components remain
   const int skip1 = env_int("KDB_SKIP1", 1);  // round-2 heads skip the entry round 1 hooked along
-  const int l2hint = env_int("KDB_L2HINT", 1);  // evict-last L2 policy on the light rounds' component gathers
+  // bit 0: evict-last L2 policy on the light rounds' component gathers; bit 1:
+  // those gathers through L1 (KDB_L1GAT)
+  const int l2hint = (env_int("KDB_L2HINT", 1) ? 1 : 0) | (env_int("KDB_L1GAT", 0) ? 2 : 0);
   // local-first phase of one rank (m.local): LOCAL component ids, the rank's
   // per-component slices, no exchange; the global phase (m.cont) continues the
   // rounds from the rows the local phases parked

@@ -221,6 +221,7 @@ struct LocalView {
   int64_t lo = 0, hi = 0;
   const uint32_t* bits = nullptr;
   uint64_t pol = 0;  // L2 cache policy for the component gathers (0: default)
+  int l1 = 0;        // component gathers through L1 (read-only path): rows of spatially ordered ids
 };
 __device__ __forceinline__ uint64_t l2_evict_last_policy() {
   uint64_t p;
@@ -237,7 +238,9 @@ __device__ __forceinline__ int32_t gat_hint(const int32_t* p, uint64_t pol) {
 __device__ __forceinline__ int32_t comp_of(const int32_t* __restrict__ comp, int64_t J, bool direct,
                                            const LocalView& lv) {
   if (lv.bits && (J < lv.lo || J >= lv.hi)) return is_core(lv.bits, J) ? kRemote : -1;
-  return direct ? (int32_t)(J - lv.lo) : (lv.pol ? gat_hint(comp + J, lv.pol) : gat(comp + J));
+  if (direct) return (int32_t)(J - lv.lo);
+  if (lv.l1) return __ldg(comp + J);  // comp is read-only while a round runs (k_relabel writes it)
+  return lv.pol ? gat_hint(comp + J, lv.pol) : gat(comp + J);
 }
 
 // Scan row (nr, dr) of vertex v (component cv) from head h.  direct: singleton
@@ -756,7 +759,8 @@ __global__ void __launch_bounds__(256) k_light_round(const int4* __restrict__ LE
                                                      int chunk = kChunk) {
   if (n_in_p) n_in = *n_in_p;
   LocalView lvh = lv;
-  if (l2hint) lvh.pol = l2_evict_last_policy();  // keep the component gathers' lines over the streams
+  if (l2hint & 1) lvh.pol = l2_evict_last_policy();  // keep the component gathers' lines over the streams
+  lvh.l1 = (l2hint >> 1) & 1;
   __shared__ __align__(16) Rec s_rec[kChunk];
   __shared__ __align__(16) Offer s_off[CAS ? 1 : kChunk];
   __shared__ uint32_t s_n, s_chunk, s_base;
@@ -776,7 +780,7 @@ __global__ void __launch_bounds__(256) k_light_round(const int4* __restrict__ LE
       if (s < n_in) {
       const int2 a = __ldcs(reinterpret_cast<const int2*>(act + s));
       const int32_t v = a.x;
-      const int32_t cv = gat(comp + v);
+      const int32_t cv = lvh.l1 ? __ldg(comp + v) : gat(comp + v);
       KDB_DCHECK(cv >= 0 && v >= row_begin && v < N, 8u);  // a live row is a local core vertex
       if (frz && frz[cv]) {
         // local-first phase: the component is frozen (its minimum is a remote or
