@@ -20,6 +20,11 @@ $(KDB_DBG): paper_2009_04552_b200/csrc/kdb.cu $(wildcard paper_2009_04552_b200/c
 	@mkdir -p $(dir $@)
 	$(NVCC) $(NVFLAGS) -DKDB_GUARDS=1 -o $@ $< -ldl
 
+# A/B build: light ELL in planes (tools/ scripts load it with KDB_LIBRARY)
+paper_2009_04552_b200/lib/libkdb_ellplanes.so: paper_2009_04552_b200/csrc/kdb.cu $(wildcard paper_2009_04552_b200/csrc/kdb_*.cuh) include/kdb.h
+	@mkdir -p $(dir $@)
+	$(NVCC) $(NVFLAGS) -DKDB_ELL_PLANES=1 -o $@ $< -ldl
+
 $(KNNG_SO): paper_2009_04552_b200/csrc/knng.cu include/knng.h
 	@mkdir -p $(dir $@)
 	$(NVCC) $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -shared -Iinclude -o $@ $<

@@ -350,8 +350,8 @@ __device__ __forceinline__ void warp_min_pair128(ulonglong2* KB, bool have, int3
   const unsigned last = __ballot_sync(0xffffffffu, lane == 31 || cn != c);  // lane ends its run
   if (last != 0xffffffffu) {
     const int end = lane + __ffs(last >> lane) - 1;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
+    const unsigned longest = __reduce_max_sync(0xffffffffu, (unsigned)(end - lane + 1));  // warp-uniform
+    for (int o = 1; o < (int)longest; o <<= 1) {
       const uint64_t ok = __shfl_down_sync(0xffffffffu, key, o);
       const uint64_t obb = __shfl_down_sync(0xffffffffu, b, o);
       if (lane + o <= end && (ok < key || (ok == key && obb < b))) { key = ok; b = obb; }

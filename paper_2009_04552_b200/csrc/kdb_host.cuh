@@ -104,7 +104,7 @@ struct RankState {
   uint32_t n_act = 0;                 // live rows in act[cur]
   uint32_t n_deep = 0;                // rows whose ELL entries are all light (k_light_ell)
   bool compact = false;               // rows phase reads the light ELL (else the graph rows)
-  int4* LE = nullptr;                 // light ELL [n_rows][kW] (J, w bits) pairs
+  int4* LE = nullptr;                 // light ELL: kW/4 planes [kW/4][n_rows] of 32-B chunks ((J, w bits) x 4)
   uint32_t* kthL = nullptr;           // per row: certificate bound kth' of the ELL's threshold (kept for reuse)
   // offers: [0, n_rows) from rows (same slot as the row's next record),
   // [n_rows, n_rows + N) from in-lists (general mode)
@@ -808,13 +808,13 @@ kdb_status rows_phase(Mst& m, float eps_run) {
       uint32_t* nout = &R.ctr->na[cur ^ 1];
       if (na_ub[r] && R.compact) {
         if (direct)
-          LAUNCH(k_light_first, grid_for(na_ub[r]), kThreads, st, R.LE, R.nbr, R.dist, ld, k, eps_run, R.row_begin, N,
+          LAUNCH(k_light_first, grid_for(na_ub[r]), kThreads, st, R.LE, R.n_rows, R.nbr, R.dist, ld, k, eps_run, R.row_begin, N,
                  comp, L.all_core, R.act[cur], na_ub[r], R.act[cur ^ 1], nout, &R.ctr->grab, R.Kc, R.Bc, R.tgt,
                  &L.ctr->entries, nin, row_chunk(na_ub[r]));
         else
         {
 #define KDB_LR_LAUNCH(...)                                                                                       \
-  LAUNCH((k_light_round<__VA_ARGS__>), grid_for(na_ub[r]), kThreads, st, R.LE, R.nbr, R.dist, ld, k, eps_run,       \
+  LAUNCH((k_light_round<__VA_ARGS__>), grid_for(na_ub[r]), kThreads, st, R.LE, R.n_rows, R.nbr, R.dist, ld, k, eps_run,       \
          R.row_begin, N, comp, R.act[cur], na_ub[r], R.act[cur ^ 1], nout, &R.ctr->grab, R.offers,                 \
          (unsigned long long*)R.Kc, &L.ctr->entries, nin, precheck, KB, lv, (const uint8_t*)frz, R.park,         \
          m.local ? &L.ctr->n_park : nullptr, l2hint, row_chunk(na_ub[r]))

@@ -217,6 +217,18 @@ struct RowScan {
 // its component reads as kRemote (>= 0, so it leaves; never a local id).
 // bits == nullptr: the global view (every id is local, dense ids global).
 constexpr int32_t kRemote = 0x7fffffff;
+// Light ELL layout: kW/4 chunks of 32 B ((J, w bits) x 4) per row.
+// 0 (default): row-major 128-B rows.  KDB_ELL_PLANES=1: plane p holds chunk p
+// of every row -- a round reading one chunk per row in row order uses whole
+// 128-B lines (round 2 of C4: 4.3 GB of DRAM instead of 9.3 GB), but the
+// light rounds took 12.58 ms against 11.77 ms in a same-box A/B: a row-major
+// line brings the row's next chunks along for the scans that continue.
+#ifndef KDB_ELL_PLANES
+#define KDB_ELL_PLANES 0
+#endif
+__host__ __device__ __forceinline__ int64_t ell_row(int64_t i) { return KDB_ELL_PLANES ? 2 * i : 8 * i; }  // 8 = kW / 2 int4 per row
+__host__ __device__ __forceinline__ int64_t ell_ps(int64_t n_rows) { return KDB_ELL_PLANES ? 2 * n_rows : 2; }
+
 struct LocalView {
   int64_t lo = 0, hi = 0;
   const uint32_t* bits = nullptr;
@@ -379,6 +391,7 @@ __global__ void __launch_bounds__(256) k_offer_round(const int32_t* __restrict__
 // pairs and every Boruvka round reads that instead.  Rows whose candidate
 // prefix (w <= eps_run) runs past column kW continue in the graph row itself.
 constexpr int kW = 16;
+static_assert(kW == 16, "ell_row() assumes kW / 2 == 8 int4 per row");
 
 // one 32-byte streaming load (evict-first: LDG.E.EF.ENL2.256) -- a light-ELL
 // chunk is read once per round; keep L2 for the component gathers
@@ -494,10 +507,12 @@ __global__ void __launch_bounds__(256) k_light_ell(const int32_t* __restrict__ n
         if (kthL) kthL[i] = kb;
       }
       deep += w[kW - 1] <= eps;
-      int4* o = LE + i * (kW / 2);
+      // chunk p (entries 4p..4p+3, 32 B) of row i: ell_chunk (planes or rows)
+      int4* o = LE + ell_row(i);
 #pragma unroll
       for (int q = 0; q < kW / 2; ++q)
-        __stcs(o + q, make_int4(J[2 * q], __float_as_int(w[2 * q]), J[2 * q + 1], __float_as_int(w[2 * q + 1])));
+        __stcs(o + (int64_t)(q >> 1) * ell_ps(n_rows) + (q & 1),
+               make_int4(J[2 * q], __float_as_int(w[2 * q]), J[2 * q + 1], __float_as_int(w[2 * q + 1])));
       if (cv < 0) continue;
       if (!direct) {
         if (w[0] <= eps) s_rec[atomicAdd(&s_n, 1u)] = Rec{(int32_t)v, 0};
@@ -583,7 +598,7 @@ __global__ void k_reuse_rows(const int4* __restrict__ LE, const uint32_t* __rest
       const int32_t cv = comp[row_begin + i];
       if (cv >= 0) {
         kmin[cv] = kthL[i];
-        want = __int_as_float(__ldcs(reinterpret_cast<const int*>(LE + i * (kW / 2)) + 1)) <= eps;
+        want = __int_as_float(__ldcs(reinterpret_cast<const int*>(LE + ell_row(i)) + 1)) <= eps;
       }
     }
     const uint32_t slot = block_reserve(n_act, want);
@@ -599,7 +614,7 @@ __global__ void k_reuse_rows(const int4* __restrict__ LE, const uint32_t* __rest
 // found only entries of its weight (decided from the loaded w) are gathered,
 // so a smaller GW trades memory-level parallelism for L2 sector traffic.
 template <bool DIRECT, int GW = 4, bool PIPE = false>
-__device__ __forceinline__ RowScan scan_ell(const int4* __restrict__ le, const int32_t* __restrict__ nr,
+__device__ __forceinline__ RowScan scan_ell(const int4* __restrict__ le, int64_t ps, const int32_t* __restrict__ nr,
                                             const float* __restrict__ dr, int k, float eps, int32_t v, int32_t cv,
                                             int h, int64_t N, const int32_t* __restrict__ comp, int all_core,
                                             unsigned long long& reads, const LocalView lv = LocalView{}) {
@@ -612,15 +627,15 @@ __device__ __forceinline__ RowScan scan_ell(const int4* __restrict__ le, const i
   // chunk holds no leaving entry does not wait a second load latency (chosen per
   // input: pays when many rows scan past their first chunk, see rows_phase)
   int4 q0, q1;
-  if (PIPE && c0 < kend) ld256cs(le + (c0 >> 1), q0, q1);
+  if (PIPE && c0 < kend) ld256cs(le + (int64_t)(c0 >> 2) * ps, q0, q1);
   while (!done && c0 < kend) {
     int4 p0, p1;
     if (PIPE) {
       p0 = q0;
       p1 = q1;
-      if (c0 + 4 < kend) ld256cs(le + ((c0 + 4) >> 1), q0, q1);
+      if (c0 + 4 < kend) ld256cs(le + (int64_t)((c0 + 4) >> 2) * ps, q0, q1);
     } else {
-      ld256cs(le + (c0 >> 1), p0, p1);
+      ld256cs(le + (int64_t)(c0 >> 2) * ps, p0, p1);
     }
     const int32_t J[4] = {p0.x, p0.z, p1.x, p1.z};
     const float w[4] = {__int_as_float(p0.y), __int_as_float(p0.w), __int_as_float(p1.y), __int_as_float(p1.w)};
@@ -695,7 +710,8 @@ __device__ __forceinline__ RowScan scan_ell(const int4* __restrict__ le, const i
 
 
 // round 1 (exact mode, singletons) over the ELL; see k_offer_first
-__global__ void __launch_bounds__(256) k_light_first(const int4* __restrict__ LE, const int32_t* __restrict__ nbr,
+__global__ void __launch_bounds__(256) k_light_first(const int4* __restrict__ LE, int64_t ell_rows,
+                                                     const int32_t* __restrict__ nbr,
                                                      const float* __restrict__ dist, int32_t ld, int32_t k, float eps,
                                                      int64_t row_begin, int64_t N, const int32_t* __restrict__ comp,
                                                      int all_core, const Rec* __restrict__ act, uint32_t n_in,
@@ -719,7 +735,7 @@ __global__ void __launch_bounds__(256) k_light_first(const int4* __restrict__ LE
       const int2 a = __ldcs(reinterpret_cast<const int2*>(act + s));
       const int32_t v = a.x;
       const int64_t i = (int64_t)v - row_begin;
-      const RowScan r = scan_ell<true>(LE + i * (kW / 2), nbr + i * ld, dist + i * ld, k, eps, v, -1, a.y, N, comp,
+      const RowScan r = scan_ell<true>(LE + ell_row(i), ell_ps(ell_rows), nbr + i * ld, dist + i * ld, k, eps, v, -1, a.y, N, comp,
                                        all_core, reads);
       if (r.found) {
         const int32_t cv = all_core ? v : gat(comp + v);
@@ -743,7 +759,8 @@ __global__ void __launch_bounds__(256) k_light_first(const int4* __restrict__ LE
 // later rounds over the ELL; see k_offer_round.  CAS (one rank): the offer is
 // a 128-bit CAS-minimum of (key, b) into KB[comp v] -- no offer list, no tie pass.
 template <int GW, bool PIPE = false, bool CAS = false>
-__global__ void __launch_bounds__(256) k_light_round(const int4* __restrict__ LE, const int32_t* __restrict__ nbr,
+__global__ void __launch_bounds__(256) k_light_round(const int4* __restrict__ LE, int64_t ell_rows,
+                                                     const int32_t* __restrict__ nbr,
                                                      const float* __restrict__ dist, int32_t ld, int32_t k, float eps,
                                                      int64_t row_begin, int64_t N, const int32_t* __restrict__ comp,
                                                      const Rec* __restrict__ act, uint32_t n_in,
@@ -794,7 +811,7 @@ __global__ void __launch_bounds__(256) k_light_round(const int4* __restrict__ LE
         park[base + __popc(am & ((1u << lane) - 1u))] = Rec{v, a.y};
       } else {
       const int64_t i = (int64_t)v - row_begin;
-      const RowScan r = scan_ell<false, GW, PIPE>(LE + i * (kW / 2), nbr + i * ld, dist + i * ld, k, eps, v, cv, a.y,
+      const RowScan r = scan_ell<false, GW, PIPE>(LE + ell_row(i), ell_ps(ell_rows), nbr + i * ld, dist + i * ld, k, eps, v, cv, a.y,
                                                   N, comp, 0, reads, lvh);
       if (r.found) {
         const uint32_t j = atomicAdd(&s_n, 1u);

@@ -68,13 +68,15 @@ __global__ void __launch_bounds__(kTileRows) k_tile_round(
     const int64_t r0 = (int64_t)S.tile * kTileRows;
     if (r0 >= n_rows) break;
     const int nr = (int)min((int64_t)kTileRows, n_rows - r0);
-    {  // the tile's ELL rows (nr * 128 contiguous bytes, coalesced) into COLUMN-major
+    {  // the tile's ELL rows (coalesced) into COLUMN-major
        // shared memory: E[c * T + row], so a warp's 32 rows read one column
        // without bank conflicts (row-major 128-B rows put them all in one bank)
-      const int4* src = LE + r0 * (kW / 2);
+      // plane p holds the rows' 32-B chunks p: the tile's part of a plane is
+      // nr * 32 contiguous bytes
       for (int q = i; q < nr * (kW / 2); q += kTileRows) {
-        const int4 x = __ldcs(src + q);
-        const int r = q / (kW / 2), c = 2 * (q % (kW / 2));
+        const int p = q / (2 * nr), j = q - p * 2 * nr;
+        const int4 x = __ldcs(LE + (int64_t)p * ell_ps(n_rows) + ell_row(r0 + (j >> 1)) + (j & 1));
+        const int r = j >> 1, c = 4 * p + 2 * (j & 1);
         S.E[c * kTileRows + r] = make_int2(x.x, x.y);
         S.E[(c + 1) * kTileRows + r] = make_int2(x.z, x.w);
       }
