@@ -43,10 +43,11 @@ def parse():
     ap.add_argument("--scale", type=float, default=1.0, help="shrink every cluster (tests only)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--seed", type=int, default=0)
-    ap.add_argument("--order", default="inertial", choices=["inertial", "generation"],
+    ap.add_argument("--order", default="auto", choices=["auto", "inertial", "generation"],
                     help="point order (= kNN-graph ids): inertial = the paper's inertial partition of the "
                          "data set (PAPER.md:45, datagen/partition.py); generation = the generator's "
-                         "cluster-major order")
+                         "cluster-major order; auto = inertial for d <= 5 (C1, C4, C5), generation above "
+                         "(PAPER.md:45: the partition 'is effective in lower dimension ... less so in higher')")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--general", action="store_true", help="do not promise an exact graph")
@@ -147,7 +148,7 @@ def median_like_numpy(col):
     return float((a + b) / 2)
 
 
-def make_workload(cfg_name: str, scale: float, seed: int, device, rank=0, world=1, order="inertial"):
+def make_workload(cfg_name: str, scale: float, seed: int, device, rank=0, world=1, order="auto"):
     """Points (numpy, seeded), exact kNN graph on the GPU, eps from the config rule.
     world > 1: this rank's rows [b, e) only (the grid builder searches all points
     for its query rows: knng_grid_rows), so no rank ever holds the whole graph
@@ -159,6 +160,8 @@ def make_workload(cfg_name: str, scale: float, seed: int, device, rank=0, world=
     cfg = CONFIGS[cfg_name]
     t0 = time.time()
     X, truth = gen_config_points(cfg_name, seed, scale)
+    if order == "auto":
+        order = "inertial" if X.shape[1] <= 5 else "generation"
     t_part = 0.0
     if order == "inertial":  # the data set is partitioned before clustering
         from datagen.partition import inertial_order
@@ -530,6 +533,7 @@ def run_ours(args):
                         "rounds": stats[-1]["rounds"], "stall_rounds": stats[-1]["stall_rounds"],
                         "phase_ms": {k_: stats[-1][k_] for k_ in
                                      ("init_ms", "min_edges_ms", "contract_ms", "filter_ms", "heavy_ms",
+                                      "heavy_rank_ms", "heavy_simred_ms",
                                       "finalize_ms")},
                         **({"local_first": stats[-1]["local_first"]} if "local_first" in stats[-1] else {}),
                         "payload_bytes_per_rank": {"rows": stats[-1]["payload_rows_bytes"],

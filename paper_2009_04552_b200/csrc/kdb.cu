@@ -819,6 +819,8 @@ kdb_status mst_impl(const kdb_graph* g, float eps, const uint32_t* core_bits, in
   g_stats[27] = m.local_rounds;
   g_stats[28] = m.t_global_scan;
   g_stats[29] = m.reused;
+  g_stats[30] = m.t_heavy_rank;
+  g_stats[31] = m.t_heavy_simred;
   return KDB_OK;
 }
 

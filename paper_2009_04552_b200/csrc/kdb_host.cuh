@@ -420,6 +420,8 @@ struct Mst {
   EllKey ell_prev, ell_next;  // what the previous call left / what this call leaves (valid flags inside)
   int reused = 0;             // rows phases that reused the kept ELL
   double t_global_scan = 0;  // global phase: per-rank offers and ties (all ranks, in sequence under sim)
+  double t_heavy_rank = 0;   // heavy phase: per-rank survivor offers, compaction and ties (all ranks)
+  double t_heavy_simred = 0; // heavy phase: the sim communicator's min-reductions (an all-reduce on GPUs)
   int64_t C_global = -1;      // components entering the global phase
   uint64_t parked_rows = 0;   // rows entering the global phase (all ranks)
   double payload_transition = 0;  // bytes per rank of the all-gathers between the phases
@@ -724,9 +726,23 @@ kdb_status rows_phase(Mst& m, float eps_run) {
              (const int32_t*)nullptr);
     else
       LAUNCH(k_relabel, grid_for(N / 8 + 1), kThreads, st, N, comp, L.parent, (const int32_t*)nullptr);
+    // ranks >= 1 of a sim communicator: their partial offer slots (on GPUs each
+    // rank refills only its own -- k_round_fill above): timed as per-rank work
+    cudaEvent_t fa = nullptr, fb = nullptr;
+    if (m.cont && nr > 1) {
+      KDB_CUDA(cudaEventCreate(&fa));
+      KDB_CUDA(cudaEventCreate(&fb));
+      ev_rnd.push_back(fa);
+      ev_rnd.push_back(fb);
+      KDB_CUDA(cudaEventRecord(fa, st));
+    }
     for (size_t r = 1; r < nr; ++r)
       LAUNCH(k_fill_comp_arrays, grid_for(C_bound), kThreads, st, C_bound, L.ranks[r].Kc, L.ranks[r].Bc, nullptr,
              (const int64_t*)Cn);
+    if (fa) {
+      KDB_CUDA(cudaEventRecord(fb, st));
+      gscan.push_back({fa, fb});
+    }
     KDB_CUDA(cudaGetLastError());
     std::swap(L.cmin, L.cmin2);
     std::swap(L.kmin, L.kmin2);
@@ -1360,9 +1376,15 @@ kdb_status heavy_phase(Mst& m) {
   LAUNCH(k_iota, grid_for(CL), kThreads, st, L.hcomp, CL);
   std::vector<int> cur(L.ranks.size(), 0);
   int rounds = 0;
+  // per-round spans (events, read after the round's host sync): A = per-rank
+  // work (fills of ranks >= 1, offers, compaction), B = sim reductions, C = per-rank ties
+  cudaEvent_t hv[7];
+  for (auto& e : hv) KDB_CUDA(cudaEventCreate(&e));
+  struct HvGuard { cudaEvent_t* e; ~HvGuard() { for (int i = 0; i < 7; ++i) cudaEventDestroy(e[i]); } } hvg{hv};
   while (C > 1) {
     ++rounds;
     LAUNCH(k_fill_comp_arrays, grid_for(C), kThreads, st, C, L.Kc, L.Bc, nullptr);
+    KDB_CUDA(cudaEventRecord(hv[0], st));
     for (size_t r = 1; r < L.ranks.size(); ++r)
       LAUNCH(k_fill_comp_arrays, grid_for(C), kThreads, st, C, L.ranks[r].Kc, L.ranks[r].Bc, nullptr);
     for (size_t r = 0; r < L.ranks.size(); ++r) {
@@ -1381,18 +1403,25 @@ kdb_status heavy_phase(Mst& m) {
       if (R.n_hs == 0) continue;
       KDB_CUDA(cudaMemcpyAsync(&R.n_hs, R.n_hs_dev + 1, 4, cudaMemcpyDeviceToHost, st));
     }
+    KDB_CUDA(cudaEventRecord(hv[1], st));
     KDB_CUDA(cudaStreamSynchronize(st));
+    m.t_heavy_rank += elapsed(hv[0], hv[1]);
+    KDB_CUDA(cudaEventRecord(hv[2], st));
     for (size_t r = 1; r < L.ranks.size(); ++r)
       LAUNCH(k_min_into_u64, grid_for(C), kThreads, st, L.Kc, L.ranks[r].Kc, C);
+    KDB_CUDA(cudaEventRecord(hv[3], st));
     KDB_TRY(allreduce_min_u64(comm, L.Kc, C, st));
     m.payload_heavy += 8.0 * C;
+    KDB_CUDA(cudaEventRecord(hv[4], st));
     for (size_t r = 0; r < L.ranks.size(); ++r) {
       RankState& R = L.ranks[r];
       if (R.n_hs)
         LAUNCH(k_hedge_tie, grid_for(R.n_hs), kThreads, st, R.hs[cur[r]], R.n_hs, L.hcomp, L.Kc, R.Bc);
     }
+    KDB_CUDA(cudaEventRecord(hv[5], st));
     for (size_t r = 1; r < L.ranks.size(); ++r)
       LAUNCH(k_min_into_u32, grid_for(C), kThreads, st, L.Bc, L.ranks[r].Bc, C);
+    KDB_CUDA(cudaEventRecord(hv[6], st));
     KDB_TRY(allreduce_min_u32(comm, L.Bc, C, st));
     m.payload_heavy += 4.0 * C;
     KDB_CUDA(cudaMemsetAsync(&L.ctr->hooks, 0, 4 * sizeof(uint32_t), st));
@@ -1401,6 +1430,8 @@ kdb_status heavy_phase(Mst& m) {
     RoundCounters hc;
     KDB_CUDA(cudaMemcpyAsync(&hc, L.ctr, sizeof(hc), cudaMemcpyDeviceToHost, st));
     KDB_CUDA(cudaStreamSynchronize(st));
+    m.t_heavy_simred += elapsed(hv[2], hv[3]) + elapsed(hv[5], hv[6]);
+    m.t_heavy_rank += elapsed(hv[4], hv[5]);
     if (hc.offered == 0) break;
     if (hc.hooks == 0) return set_err(KDB_EINTERNAL, "heavy phase made no progress");
     LAUNCH(k_jump, grid_for(C), kThreads, st, C, L.parent, L.rootof, L.ctr, (const int64_t*)nullptr, L.flag);

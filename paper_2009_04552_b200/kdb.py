@@ -249,7 +249,8 @@ def mst(g: Graph, eps: float, core_bits: torch.Tensor, comm: Comm | None = None,
                  filter_ms=st[8], heavy_ms=st[9], survivors=int(st[10]), heavy_rounds=int(st[11]),
                  tau=st[12], light_components=int(st[13]), fallback=int(st[14]),
                  filter_exceptions=int(st[15]), filter_slow_entries=int(st[16]),
-                 payload_rows_bytes=st[17], payload_heavy_bytes=st[18], ell_reused=int(st[29]))
+                 payload_rows_bytes=st[17], payload_heavy_bytes=st[18], ell_reused=int(st[29]),
+                 heavy_rank_ms=st[30], heavy_simred_ms=st[31])
     if st[19]:  # local-first contraction ran (multi-rank exact mode)
         stats["local_first"] = dict(local_ms_max=st[20], local_ms_sum=st[21], transition_ms=st[22],
                                     global_ms=st[23], global_components=int(st[24]), parked_rows=int(st[25]),

@@ -28,9 +28,12 @@ from tests.kdb_harness import assert_parity, oracle_run
 pytestmark = pytest.mark.gpu
 
 
-def _workload(name, scale=1.0):
+def _workload(name, scale=1.0, order="generation"):
     cfg = CONFIGS[name]
     X, _ = gen_config_points(name, 0, scale)
+    if order == "inertial":  # bench.py's order for d <= 5 (datagen/partition.py)
+        from datagen.partition import inertial_order
+        X = X[inertial_order(X, device="cuda")]
     build = build_knng_grid if X.shape[1] <= 5 else build_knng_brute
     nbr, dist, _ = build(X, cfg["k"])
     col = dist[:, cfg["M"] - 1].double()
@@ -55,6 +58,15 @@ def _gpu(nbr, dist, M, eps, exact=True, comm=None, edge_cols=0):
 @pytest.mark.parametrize("name", ["C2", "C3"])
 def test_config_full_oracle_parity(name):
     nbr, dist, M, eps = _workload(name)
+    got = _gpu(nbr, dist, M, eps)
+    exp = oracle_run(nbr.cpu().numpy(), dist.cpu().numpy(), M, eps)
+    assert_parity(got, exp)
+
+
+@pytest.mark.parametrize("order", ["generation", "inertial"])
+def test_config_c1_full_oracle_parity(order):
+    """C1 at full size in both point orders (bench.py times it in the inertial order)."""
+    nbr, dist, M, eps = _workload("C1", order=order)
     got = _gpu(nbr, dist, M, eps)
     exp = oracle_run(nbr.cpu().numpy(), dist.cpu().numpy(), M, eps)
     assert_parity(got, exp)

@@ -11,7 +11,8 @@ bench lines measured on one GPU:
     bytes every collective would carry.
 
   T_P = core_mark/P + local_max + transition + [global - global_scan - sim_reductions]
-        + global_scan/P + filter/P + heavy + finalize/P + label/P
+        + global_scan/P + filter/P + heavy_rank/P + [heavy - heavy_rank - heavy_sim_reductions]
+        + finalize/P + label/P
         + collectives (bytes at the stated bus bandwidth + a latency per call)
 
 Assumptions (stated in the output): NCCL all-reduce / all-gather bus bandwidth
@@ -43,14 +44,21 @@ def model(line1, lineP, P):
     lf = mst.get("local_first")
     cm = kern(lineP, "k_core_mark")
     lab = kern(lineP, "k_label")
-    minred = kern(lineP, "k_min_into")
+    # the sim's min-reductions stand in for all-reduces (modelled from the payload);
+    # those of the heavy phase are subtracted there
+    minred = kern(lineP, "k_min_into") - ph.get("heavy_simred_ms", 0.0)
     pay = mst["payload_bytes_per_rank"]
     rounds = mst["rounds"]
     heavy_rounds = mst["filter"]["heavy_rounds"]
     ar = lambda b: 2.0 * (P - 1) / P * b / (BUSBW * 1e9) * 1e3   # ms
     ag = lambda b: (P - 1) / P * b / (BUSBW * 1e9) * 1e3
     parts = {"core_mark": cm / P, "label": lab / P, "filter": ph["filter_ms"] / P,
-             "finalize": ph["finalize_ms"] / P, "heavy (replicated)": ph["heavy_ms"]}
+             "finalize": ph["finalize_ms"] / P}
+    if "heavy_rank_ms" in ph:  # per-rank survivor work divides by P; the sim's reductions are the all-reduce
+        parts["heavy: per-rank offers+ties"] = ph["heavy_rank_ms"] / P
+        parts["heavy: replicated"] = max(ph["heavy_ms"] - ph["heavy_rank_ms"] - ph["heavy_simred_ms"], 0.0)
+    else:
+        parts["heavy (replicated)"] = ph["heavy_ms"]
     if lf:
         glob_rep = max(ph["min_edges_ms"] - lf["global_scan_ms"] - minred, 0.0)
         parts.update({"local phase (max rank)": lf["local_ms_max"],
