@@ -324,7 +324,7 @@ def host_ram_gb():
     return None
 
 
-def whole_workload_baseline(cfg_name, scale, ec, n_eps):
+def whole_workload_baseline(cfg_name, scale, ec, n_eps, order="generation"):
     """The oracle on the WHOLE workload, measured once by tools/window_parity.py
     (the ten closed cluster windows of C4 / C5 are exact independent
     sub-problems: the sum of their single-threaded oracle times is the
@@ -333,6 +333,8 @@ def whole_workload_baseline(cfg_name, scale, ec, n_eps):
     if ec or n_eps != 1:
         return None
     tag = {("C4", 1.0): "C4", ("C5", 0.25): "C5q"}.get((cfg_name, scale))
+    if tag and order == "inertial":
+        tag += "i"
     path = os.path.join(ROOT, "profiles", "r02", f"window_parity_{tag}.json") if tag else None
     if not path or not os.path.exists(path):
         return None
@@ -507,7 +509,7 @@ def run_ours(args):
                "cpu_model": host_cpu()[0], "box_cores": host_cpu()[1], "host_ram_gb": host_ram_gb(),
                "sample": f"rows [0, {ns}) of the workload ({ns * k} entries; entries to ids >= {ns} skipped), "
                          f"one single-threaded run, {dt:.1f} s"}
-        whole = whole_workload_baseline(args.config, args.scale, ec, len(eps_list))
+        whole = whole_workload_baseline(args.config, args.scale, ec, len(eps_list), W["order"])
         if whole:
             cpu["whole_workload_measured"] = whole
 

@@ -739,7 +739,21 @@ kdb_status mst_impl(const kdb_graph* g, float eps, const uint32_t* core_bits, in
     unsigned long long* vb2 = reinterpret_cast<unsigned long long*>(L.Kc);  // N + 1, free now
     int abits = 1;
     while (abits < 32 && ((int64_t)1 << abits) < N) ++abits;
-    {
+    if (4 * ne >= N && env_int("KDB_MSF_COUNT", 1) != 0) {
+      // dense forest (C4: N - 10 edges): a counting sort by a over the N ids --
+      // one atomic and one scatter per edge instead of the radix sort's passes
+      uint32_t* cnt = reinterpret_cast<uint32_t*>(L.flag);     // N + 1, free after the phases
+      uint32_t* off = reinterpret_cast<uint32_t*>(L.rootof);   // N + 1
+      uint32_t* pos = reinterpret_cast<uint32_t*>(L.tgt);      // N + 1 >= ne
+      const uint32_t* ea = reinterpret_cast<const uint32_t*>(L.e_w);
+      KDB_CUDA(cudaMemsetAsync(cnt, 0, (N + 1) * sizeof(uint32_t), st));
+      LAUNCH(k_msf_count, grid_for(ne), kThreads, st, ne, ea, cnt, pos);
+      { LaunchScope ls_("cub::DeviceScan", st, false);
+        KDB_CUDA(cub::DeviceScan::ExclusiveSum(L.cub_tmp, cb, cnt, off, (int)(N + 1), st)); }
+      LAUNCH(k_msf_scatter, grid_for(ne), kThreads, st, ne, ea, reinterpret_cast<const unsigned long long*>(L.e_key),
+             off, pos, reinterpret_cast<uint32_t*>(mst_a), vb2);
+      KDB_CUDA(cudaGetLastError());
+    } else {
       // the emitted (a, (b, w)) pairs sort straight into the caller's mst_a
       LaunchScope ls_("cub::DeviceRadixSort", st, false);
       KDB_CUDA(cub::DeviceRadixSort::SortPairs(L.cub_tmp, cb, reinterpret_cast<const uint32_t*>(L.e_w), mst_a,

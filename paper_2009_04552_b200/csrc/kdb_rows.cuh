@@ -1301,6 +1301,26 @@ constexpr int kRunMax = 32;  // longer runs of equal a go to the segmented sort
 //   * any other entry scans at most kRunMax entries back: if that reaches its
 //     run start, the start thread owns it; otherwise it belongs to a long run
 //     and unpacks itself.
+// a11 (dense forests): counting sort of the emitted edges by their smaller
+// endpoint a -- each edge's rank inside its bucket from the atomic it counts
+// with, then a scatter through the scanned counts; the unpack below sorts each
+// run of equal a by b, so the atomic order never reaches the output
+__global__ void k_msf_count(int64_t m, const uint32_t* __restrict__ a, uint32_t* __restrict__ cnt,
+                            uint32_t* __restrict__ pos) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+    pos[i] = atomicAdd(cnt + a[i], 1u);
+}
+__global__ void k_msf_scatter(int64_t m, const uint32_t* __restrict__ a, const unsigned long long* __restrict__ vb,
+                              const uint32_t* __restrict__ off, const uint32_t* __restrict__ pos,
+                              uint32_t* __restrict__ ka, unsigned long long* __restrict__ vb2) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t ai = a[i];
+    const uint32_t d = off[ai] + pos[i];
+    ka[d] = ai;
+    vb2[d] = vb[i];
+  }
+}
+
 __global__ void k_msf_unpack(int64_t m, const uint32_t* __restrict__ ka, const unsigned long long* __restrict__ vb,
                              uint32_t* __restrict__ b, float* __restrict__ w, int32_t* __restrict__ seg_b,
                              int32_t* __restrict__ seg_e, uint32_t* __restrict__ nseg) {
