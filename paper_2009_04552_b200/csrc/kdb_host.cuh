@@ -500,14 +500,22 @@ kdb_status rows_phase(Mst& m, float eps_run) {
   // local-first phase of one rank (m.local): LOCAL component ids, the rank's
   // per-component slices, no exchange; the global phase (m.cont) continues the
   // rounds from the rows the local phases parked
-  const LocalView lv = m.local ? m.lv : LocalView{};
+  LocalView lv = m.local ? m.lv : LocalView{};
   uint8_t* frz = m.local ? L.frz : nullptr;
   const int64_t ecap = m.ecap >= 0 ? m.ecap : N;
   int64_t C = 0;
   bool fuse1 = false, packed1 = false, tile = false;
   size_t cb = L.cub_bytes;
+  int32_t* gmap = nullptr;   // two-level ids in the global phase (LocalView::gmap)
+  int64_t CG0 = 0;
   if (m.cont) {
     C = m.C;  // global components after the local-first phases (state set by local_first)
+    if (env_int("KDB_GMAP", 1) != 0 && C > 0) {
+      gmap = L.hcomp;  // free until the heavy phase
+      CG0 = C;
+      LAUNCH(k_iota, grid_for(C), kThreads, st, gmap, C);
+      lv.gmap = gmap;
+    }
   } else {
   KDB_CUDA(cudaMemsetAsync(L.ctr, 0, sizeof(RoundCounters), st));
   if (!m.local) {
@@ -724,6 +732,8 @@ kdb_status rows_phase(Mst& m, float eps_run) {
     if (m.local)  // only this rank's rows carry (local) ids
       LAUNCH(k_relabel, grid_for((lv.hi - lv.lo) / 8 + 1), kThreads, st, lv.hi - lv.lo, comp + lv.lo, L.parent,
              (const int32_t*)nullptr);
+    else if (gmap)  // global phase: the map of transition ids, not the N vertices
+      LAUNCH(k_relabel, grid_for(CG0 / 8 + 1), kThreads, st, CG0, gmap, L.parent, (const int32_t*)nullptr);
     else
       LAUNCH(k_relabel, grid_for(N / 8 + 1), kThreads, st, N, comp, L.parent, (const int32_t*)nullptr);
     // ranks >= 1 of a sim communicator: their partial offer slots (on GPUs each
@@ -915,7 +925,7 @@ kdb_status rows_phase(Mst& m, float eps_run) {
     else
       LAUNCH(k_hook<false>, grid_for(C_ub), kThreads, st, C_ub, L.Kc, L.Bc, direct ? L.tgt : nullptr, kmin_cert,
              comp, L.parent, L.e_key, L.e_w, ecap, L.ctr, Cd, (const int4*)nullptr,
-             (cas && !direct) ? (const ulonglong2*)KB : nullptr, frz, row_chunk((uint64_t)C_ub));
+             (cas && !direct) ? (const ulonglong2*)KB : nullptr, frz, row_chunk((uint64_t)C_ub), lv.gmap);
     KDB_CUDA(cudaGetLastError());
     }  // !tile_round
     // a6: contract (no hooks => identity)
@@ -967,6 +977,10 @@ kdb_status rows_phase(Mst& m, float eps_run) {
         KDB_CUDA(cudaMemcpy(&rc, L.ranks[r].ctr, sizeof(rc), cudaMemcpyDeviceToHost));
         na_x[r] = rc.na[cur];
       }
+      if (gmap) {  // the sweep reads comp[] directly: current ids into comp, the map back to identity
+        LAUNCH(k_relabel, grid_for(N / 8 + 1), kThreads, st, N, comp, gmap, (const int32_t*)nullptr);
+        LAUNCH(k_iota, grid_for(CG0), kThreads, st, gmap, CG0);
+      }
       LAUNCH(k_fill_comp_arrays, grid_for(Cx), kThreads, st, Cx, L.Kc, L.Bc, nullptr);
       for (size_t r = 1; r < nr; ++r)
         LAUNCH(k_fill_comp_arrays, grid_for(Cx), kThreads, st, Cx, L.ranks[r].Kc, L.ranks[r].Bc, nullptr);
@@ -1003,6 +1017,8 @@ kdb_status rows_phase(Mst& m, float eps_run) {
       last_checked = rounds;  // the sweep round was exact; the next check is the next round
     }
   }
+  if (gmap)  // the global phase's current ids into comp (the filter and labels read comp)
+    LAUNCH(k_relabel, grid_for(N / 8 + 1), kThreads, st, N, comp, gmap, (const int32_t*)nullptr);
   KDB_CUDA(cudaStreamSynchronize(st));
   if (!ev_rnd.empty()) {
     KDB_CUDA(cudaEventRecord(ev[2], st));

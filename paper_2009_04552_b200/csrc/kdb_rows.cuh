@@ -234,6 +234,10 @@ struct LocalView {
   const uint32_t* bits = nullptr;
   uint64_t pol = 0;  // L2 cache policy for the component gathers (0: default)
   int l1 = 0;        // component gathers through L1 (read-only path): rows of spatially ordered ids
+  // global phase of the local-first scheme: comp[] holds the transition ids
+  // for the whole phase and gmap[transition id] the current component, so a
+  // round relabels the C_G-sized map instead of all N vertices
+  const int32_t* gmap = nullptr;
 };
 __device__ __forceinline__ uint64_t l2_evict_last_policy() {
   uint64_t p;
@@ -251,6 +255,10 @@ __device__ __forceinline__ int32_t comp_of(const int32_t* __restrict__ comp, int
                                            const LocalView& lv) {
   if (lv.bits && (J < lv.lo || J >= lv.hi)) return is_core(lv.bits, J) ? kRemote : -1;
   if (direct) return (int32_t)(J - lv.lo);
+  if (lv.gmap) {
+    const int32_t c = gat(comp + J);
+    return c >= 0 ? gat(lv.gmap + c) : c;
+  }
   if (lv.l1) return __ldg(comp + J);  // comp is read-only while a round runs (k_relabel writes it)
   return lv.pol ? gat_hint(comp + J, lv.pol) : gat(comp + J);
 }
@@ -797,7 +805,8 @@ __global__ void __launch_bounds__(256) k_light_round(const int4* __restrict__ LE
       if (s < n_in) {
       const int2 a = __ldcs(reinterpret_cast<const int2*>(act + s));
       const int32_t v = a.x;
-      const int32_t cv = lvh.l1 ? __ldg(comp + v) : gat(comp + v);
+      int32_t cv = lvh.l1 ? __ldg(comp + v) : gat(comp + v);
+      if (lvh.gmap) cv = gat(lvh.gmap + cv);
       KDB_DCHECK(cv >= 0 && v >= row_begin && v < N, 8u);  // a live row is a local core vertex
       if (frz && frz[cv]) {
         // local-first phase: the component is frozen (its minimum is a remote or
@@ -847,16 +856,6 @@ __global__ void __launch_bounds__(256) k_light_round(const int4* __restrict__ LE
   if ((threadIdx.x & 31) == 0 && reads) atomicAdd(n_entries, reads);
 }
 
-// The same round, STAGED for memory-level parallelism.  The per-thread scan
-// is a chain of dependent loads (record -> comp[v] and the ELL chunk -> the
-// comp[J] gathers -> the offer); with one record at a time a thread waits ~4
-// memory latencies per record.  Here every thread takes its kRPT records of the
-// chunk together: their records, then all their comp[v] and first ELL chunks,
-// then all their comp[J] gathers are issued before any is consumed, so the
-// latencies overlap.  A row whose scan does not end in its first chunk (the
-// candidate prefix or the minimum's tie group continues) is re-scanned from its
-// head by scan_ell, the reference per-row scan (rare at C4: rows are mostly
-// decided by the chunk at their head).
 // in-edge lists: scan the live in-entries of target t, drop intra entries
 // (swap-remove; they never revive), offer the minimum leaving one.
 __global__ void k_offer_in(const unsigned long long* __restrict__ in_off, int32_t* __restrict__ in_len,
@@ -988,7 +987,8 @@ __global__ void __launch_bounds__(256) k_hook(int64_t C, const uint64_t* __restr
                        uint64_t* __restrict__ e_key, float* __restrict__ e_w, int64_t e_cap,
                        RoundCounters* __restrict__ ctr, const int64_t* __restrict__ Cp,
                        const int4* __restrict__ rec1, const ulonglong2* __restrict__ KB = nullptr,
-                       uint8_t* __restrict__ frz = nullptr, int hchunk = kHookChunk) {
+                       uint8_t* __restrict__ frz = nullptr, int hchunk = kHookChunk,
+                       const int32_t* __restrict__ gmap = nullptr) {
   if (Cp) C = *Cp;
   __shared__ uint64_t s_key[kHookChunk];
   __shared__ uint32_t s_w[kHookChunk];
@@ -1043,8 +1043,12 @@ __global__ void __launch_bounds__(256) k_hook(int64_t C, const uint64_t* __restr
           } else if (KB) {
             t2 = tKB;
           } else {
-            const int32_t x = (gat(comp + a) == (int32_t)c) ? (int32_t)b : (int32_t)a;
-            t2 = gat(comp + x);
+            auto cur = [&](uint32_t y) {  // current component of vertex y
+              const int32_t q = gat(comp + y);
+              return gmap ? gat(gmap + q) : q;
+            };
+            const int32_t x = (cur(a) == (int32_t)c) ? (int32_t)b : (int32_t)a;
+            t2 = cur((uint32_t)x);
           }
           KDB_DCHECK(t2 >= 0 && t2 < C, 1u);
           bool mutual, cert_t = true;
