@@ -152,7 +152,9 @@ __device__ __forceinline__ uint64_t fdiv(uint64_t q, const FastDiv& f) { return 
 
 // The filter: every rank streams its rows once, each warp in its own tiles of
 // kFilterRows rows.  Per tile, the warp's lanes stage the rows' data in the
-// warp's slice of shared memory (comp[v] and the id range of comp[v]); then
+// warp's slice of shared memory (comp[v] and an id range of comp[v]: the
+// component's whole range when its dominated blocks form one run, else the run
+// of blocks dominated by comp[v] around v's own block, brun); then
 // the tile's R*k ids are swept in flat order, VEC per lane and chunk.  Fast path: J inside the id range of comp[v] and
 // not in the Bloom filter of the exceptions => comp[J] == comp[v]: the entry
 // is intra (or light, or beyond eps, or J == v -- none a candidate leaving
