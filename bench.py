@@ -523,6 +523,8 @@ def run_ours(args):
                                + (f" (sim communicator: {args.sim} virtual ranks on one GPU)"
                                   if args.sim and world == 1 else ""),
                                exact_graph=not args.general,
+                               knobs={k_: v_ for k_, v_ in sorted(os.environ.items()) if k_.startswith("KDB_")}
+                               or "defaults (no KDB_* overrides)",
                                **stage_desc(ec, eps_list, W)),
                 "roofline": roof,
                 "stage_roofline": {"t_min_ms": t_min_ms, "frac": t_min_ms / ms,

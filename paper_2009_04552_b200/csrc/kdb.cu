@@ -379,6 +379,8 @@ struct RoundCounters {
                                  // KDB_GRAPH_EXACT promise was false (or a bug)
   uint32_t n_cont;               // rows continuing in the warp-per-row scan
   uint32_t n_deep;               // per rank: rows whose kW ELL entries are all within eps_run
+  uint32_t n_local;              // per rank: rows whose nearest neighbour's id is within 2^16 of
+                                 // their own (spatially ordered ids: the component gathers go through L1)
   uint32_t grab;                 // chunk cursor of the ordered row kernels (per rank)
   uint32_t n_off2;
   uint32_t n_park;               // per rank, local-first phase: rows parked for the global phase

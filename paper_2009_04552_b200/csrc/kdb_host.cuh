@@ -103,6 +103,7 @@ struct RankState {
   Rec* act[2] = {nullptr, nullptr};  // active rows (v, head), ping-pong
   uint32_t n_act = 0;                 // live rows in act[cur]
   uint32_t n_deep = 0;                // rows whose ELL entries are all light (k_light_ell)
+  uint32_t n_local = 0;               // rows whose nearest neighbour's id is near their own (k_light_ell)
   bool compact = false;               // rows phase reads the light ELL (else the graph rows)
   int4* LE = nullptr;                 // light ELL: kW/4 planes [kW/4][n_rows] of 32-B chunks ((J, w bits) x 4)
   uint32_t* kthL = nullptr;           // per row: certificate bound kth' of the ELL's threshold (kept for reuse)
@@ -356,7 +357,7 @@ struct EllKey {
   const float* dist = nullptr;
   int64_t n_total = 0, row_begin = 0, n_rows = 0;
   int32_t k_max = 0, k = 0;
-  uint32_t eps_run_bits = 0, n_deep = 0;
+  uint32_t eps_run_bits = 0, n_deep = 0, n_local = 0;
   bool same_graph(const EllKey& o) const {
     return ws == o.ws && nbr == o.nbr && dist == o.dist && n_total == o.n_total && row_begin == o.row_begin &&
            n_rows == o.n_rows && k_max == o.k_max && k == o.k;
@@ -496,7 +497,9 @@ kdb_status rows_phase(Mst& m, float eps_run) {
   const int skip1 = env_int("KDB_SKIP1", 1);  // round-2 heads skip the entry round 1 hooked along
   // bit 0: evict-last L2 policy on the light rounds' component gathers; bit 1:
   // those gathers through L1 (KDB_L1GAT)
-  const int l2hint = (env_int("KDB_L2HINT", 1) ? 1 : 0) | (env_int("KDB_L1GAT", 0) ? 2 : 0);
+  // (KDB_L1GAT; default: when most rows' nearest neighbour has a nearby id, k_light_ell counts them)
+  int l2hint = (env_int("KDB_L2HINT", 1) ? 1 : 0) | (env_int("KDB_L1GAT", 0) > 0 ? 2 : 0);
+  const int l1gat_env = env_int("KDB_L1GAT", -1);
   // local-first phase of one rank (m.local): LOCAL component ids, the rank's
   // per-component slices, no exchange; the global phase (m.cont) continues the
   // rounds from the rows the local phases parked
@@ -636,11 +639,13 @@ kdb_status rows_phase(Mst& m, float eps_run) {
     KDB_CUDA(cudaStreamSynchronize(st));
     R.n_act = hc.na[0];
     R.n_deep = reuse ? m.ell_prev.n_deep : hc.n_deep;
+    R.n_local = reuse ? m.ell_prev.n_local : hc.n_local;
     R.n_in_act = hc.ni[0];
   }
   if (want.valid) {  // what this call's ELL was built from (kept if the call succeeds)
     m.ell_next = want;
     m.ell_next.n_deep = L.ranks[0].n_deep;
+    m.ell_next.n_local = L.ranks[0].n_local;
   }
   KDB_CUDA(cudaEventRecord(ev[2], st));
   KDB_CUDA(cudaEventSynchronize(ev[2]));
@@ -648,6 +653,14 @@ kdb_status rows_phase(Mst& m, float eps_run) {
   m.t_inlist += elapsed(ev[1], ev[2]);
   }  // !m.cont
 
+  if (l1gat_env < 0) {  // auto: spatially ordered ids (e.g. the inertial partition)
+    uint64_t loc = 0, rows = 0;
+    for (auto& R : L.ranks) {
+      loc += R.n_local;
+      rows += (uint64_t)std::max<int64_t>(R.n_rows, 0);
+    }
+    if (rows > 0 && 2 * loc > rows) l2hint |= 2;
+  }
   // ---- Boruvka rounds -------------------------------------------------------------
   // Pipelined: every kernel reads its counts (components, list sizes) from the
   // device; grids are sized by host upper bounds one round stale, so the host
@@ -1151,6 +1164,7 @@ kdb_status local_first(Mst& m, float eps_run) {
     S.ranks[0].tgt = S.tgt;
     KDB_TRY(rows_phase(sub, eps_run));
     R.n_deep = sub.L.ranks[0].n_deep;
+    R.n_local = sub.L.ranks[0].n_local;
     R.compact = sub.L.ranks[0].compact;
     CL[r] = sub.C;
     EC[r] = (int64_t)sub.msf_local;

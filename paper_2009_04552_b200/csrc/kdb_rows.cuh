@@ -437,6 +437,7 @@ __global__ void __launch_bounds__(256) k_light_ell(const int32_t* __restrict__ n
   __shared__ __align__(16) Rec s_rec[kChunk];
   __shared__ uint32_t s_n, s_chunk, s_base;
   uint32_t deep = 0;  // rows whose kW ELL entries are all within eps (their scans go past the first chunk)
+  uint32_t local = 0;  // rows whose nearest neighbour has a nearby id (RoundCounters::n_local)
   for (;;) {
     if (threadIdx.x == 0) { s_chunk = atomicAdd(grab, 1u); s_n = 0; }
     __syncthreads();
@@ -515,6 +516,7 @@ __global__ void __launch_bounds__(256) k_light_ell(const int32_t* __restrict__ n
         if (kthL) kthL[i] = kb;
       }
       deep += w[kW - 1] <= eps;
+      local += (uint32_t)(J[0] >= 0 && (uint32_t)abs((int64_t)J[0] - v) < 65536u);
       // chunk p (entries 4p..4p+3, 32 B) of row i: ell_chunk (planes or rows)
       int4* o = LE + ell_row(i);
 #pragma unroll
@@ -585,8 +587,12 @@ __global__ void __launch_bounds__(256) k_light_ell(const int32_t* __restrict__ n
     for (uint32_t j = threadIdx.x; j < s_n; j += blockDim.x) act[s_base + j] = s_rec[j];
     __syncthreads();
   }
-  for (int o = 16; o > 0; o >>= 1) deep += __shfl_xor_sync(0xffffffffu, deep, o);
+  for (int o = 16; o > 0; o >>= 1) {
+    deep += __shfl_xor_sync(0xffffffffu, deep, o);
+    local += __shfl_xor_sync(0xffffffffu, local, o);
+  }
   if ((threadIdx.x & 31) == 0 && deep) atomicAdd(n_deep, deep);
+  if ((threadIdx.x & 31) == 0 && local) atomicAdd(n_deep + 1, local);  // RoundCounters::n_local
 }
 
 
