@@ -493,6 +493,7 @@ kdb_status rows_phase(Mst& m, float eps_run) {
   KDB_CUDA(cudaEventRecord(ev[0], st));
   const bool use_compact = env_int("KDB_COMPACT", 1) != 0;
   const int gw = env_int("KDB_GW", 4);  // component-gather width of the later light rounds (scan_ell)
+  const bool lean = env_int("KDB_LEAN", 0) != 0;  // chunk scan on bit masks (scan_ell_lean): measured slower, off
   const bool sparse_ids = env_int("KDB_SPARSE", 1) != 0;  // keep root ids once few components remain
   const int skip1 = env_int("KDB_SKIP1", 1);  // round-2 heads skip the entry round 1 hooked along
   // bit 0: evict-last L2 policy on the light rounds' component gathers; bit 1:
@@ -836,13 +837,14 @@ kdb_status rows_phase(Mst& m, float eps_run) {
       KDB_CUDA(cudaEventRecord(gsA, st));
     }
     // a3: offers (rows, then in-lists), per rank, into that rank's Kc partial
+    bool hooks_zeroed = false;
     for (size_t r = 0; r < nr; ++r) {
       RankState& R = L.ranks[r];
       if (direct && fused && R.compact) continue;  // done by the ELL pass
-      KDB_CUDA(cudaMemsetAsync(&R.ctr->na[cur ^ 1], 0, sizeof(uint32_t), st));
-      KDB_CUDA(cudaMemsetAsync(&R.ctr->ni[cur ^ 1], 0, sizeof(uint32_t), st));
-      KDB_CUDA(cudaMemsetAsync(&R.ctr->n_off, 0, sizeof(uint32_t), st));
-      KDB_CUDA(cudaMemsetAsync(&R.ctr->grab, 0, sizeof(uint32_t), st));
+      // this round's counters (and, with rank 0, the hook counters: nothing
+      // writes them before the hook) in one launch instead of five memsets
+      LAUNCH(k_round_reset, 1, 32, st, R.ctr, cur, r == 0 ? L.ctr : (RoundCounters*)nullptr);
+      hooks_zeroed |= r == 0;
       const uint32_t* nin = &R.ctr->na[cur];
       uint32_t* nout = &R.ctr->na[cur ^ 1];
       if (na_ub[r] && R.compact) {
@@ -863,6 +865,7 @@ kdb_status rows_phase(Mst& m, float eps_run) {
           const bool pipe = pk >= 0 ? pk != 0 : (uint64_t)R.n_deep * 100 > (uint64_t)R.n_rows * 15;
           if (cas) {
             if (pipe) KDB_LR_LAUNCH(4, true, true);
+            else if (lean) KDB_LR_LAUNCH(4, false, true, true);
             else KDB_LR_LAUNCH(4, false, true);
           } else if (gw == 1) KDB_LR_LAUNCH(1);
           else if (gw == 2) KDB_LR_LAUNCH(2);
@@ -931,7 +934,7 @@ kdb_status rows_phase(Mst& m, float eps_run) {
       m.payload_rows += 4.0 * C_ub;
     }
     // a5: hook + emit
-    KDB_CUDA(cudaMemsetAsync(&L.ctr->hooks, 0, 4 * sizeof(uint32_t), st));
+    if (!hooks_zeroed) KDB_CUDA(cudaMemsetAsync(&L.ctr->hooks, 0, 4 * sizeof(uint32_t), st));
     if (direct && packed1)
       LAUNCH(k_hook<true>, grid_for(C_ub), kThreads, st, C_ub, L.Kc, L.Bc, L.tgt, kmin_cert, comp, L.parent, L.e_key,
              L.e_w, ecap, L.ctr, Cd, L.rec1, (const ulonglong2*)nullptr, frz, row_chunk((uint64_t)C_ub));

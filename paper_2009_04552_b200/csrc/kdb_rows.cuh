@@ -715,6 +715,111 @@ __device__ __forceinline__ RowScan scan_ell(const int4* __restrict__ le, int64_t
   return r;
 }
 
+// scan_ell for the later light rounds (not DIRECT, all four gathers of a
+// chunk at once, no pipelining) on 4-bit masks instead of a per-entry branch
+// ladder: the dead prefix ends at the first valid entry that is beyond eps or
+// leaving (ffs), the minimum's tie group is the run of equal weights after it
+// (rows are sorted by weight), and keys are packed only for the minimum and its
+// leaving ties.  Same result as scan_ell<false, 4, false> (parity-green), but
+// measured slower (C4: 33.7 against 33.2 ms per step, same box): the mask
+// bookkeeping costs more issue slots than the branches it replaces; off
+// (KDB_LEAN=1 selects it).
+__device__ __forceinline__ RowScan scan_ell_lean(const int4* __restrict__ le, int64_t ps,
+                                                 const int32_t* __restrict__ nr, const float* __restrict__ dr, int k,
+                                                 float eps, int32_t v, int32_t cv, int h, int64_t N,
+                                                 const int32_t* __restrict__ comp, unsigned long long& reads,
+                                                 const LocalView lv) {
+  RowScan r{false, k, kSent, kSentB, -1};
+  uint32_t wstar = 0;
+  const int kend = min(k, kW);
+  int c0 = h & ~3;
+  while (c0 < kend) {
+    int4 p0, p1;
+    ld256cs(le + (int64_t)(c0 >> 2) * ps, p0, p1);
+    const int32_t J[4] = {p0.x, p0.z, p1.x, p1.z};
+    const uint32_t wb[4] = {mono_bits(__int_as_float(p0.y)), mono_bits(__int_as_float(p0.w)),
+                            mono_bits(__int_as_float(p1.y)), mono_bits(__int_as_float(p1.w))};
+    const float w[4] = {__int_as_float(p0.y), __int_as_float(p0.w), __int_as_float(p1.y), __int_as_float(p1.w)};
+    reads += (unsigned long long)(min(c0 + 4, kend) - max(c0, h));
+    uint32_t valid = 0, in = 0;
+    int32_t cj[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int idx = c0 + j;
+      const bool vj = idx >= h && idx < kend;
+      const bool ej = w[j] <= eps;
+      valid |= (uint32_t)vj << j;
+      in |= (uint32_t)(vj && ej) << j;
+      const bool cand = vj && ej && J[j] >= 0 && J[j] < N && J[j] != v;
+      cj[j] = cand ? comp_of(comp, J[j], false, lv) : -1;
+    }
+    uint32_t leave = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) leave |= (uint32_t)(cj[j] >= 0 && cj[j] != cv) << j;
+    int from = 0;  // first position of the chunk still to look at for ties
+    if (!r.found) {
+      const uint32_t stop = valid & (~in | leave);
+      if (stop == 0) {  // every valid entry is dead
+        h = min(c0 + 4, kend);
+        c0 += 4;
+        continue;
+      }
+      const int f = __ffs(stop) - 1;
+      if (!((in >> f) & 1u)) return RowScan{false, k, kSent, kSentB, -1};  // sorted: nothing left
+      int32_t Jf = 0, cf = -1;
+#pragma unroll
+      for (int j = 0; j < 4; ++j)  // select by an unrolled compare (a dynamic index would spill to the stack)
+        if (j == f) { Jf = J[j]; cf = cj[j]; wstar = wb[j]; }
+      r.found = true;
+      r.h = c0 + f;
+      r.best = pack_key(wstar, (uint32_t)min(v, Jf));
+      r.bestb = (uint32_t)max(v, Jf);
+      r.bestc = cf;
+      from = f + 1;
+    }
+    // the tie group: valid positions >= from with the minimum's weight, up to
+    // the first other weight
+    uint32_t differ = 0, tie = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const bool vj = j >= from && ((valid >> j) & 1u);
+      differ |= (uint32_t)(vj && wb[j] != wstar) << j;
+      tie |= (uint32_t)(vj && wb[j] == wstar) << j;
+    }
+    const uint32_t before = differ ? ((1u << (__ffs(differ) - 1)) - 1u) : 0xfu;
+    const uint32_t cmp = tie & leave & before;
+    if (cmp) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (!((cmp >> j) & 1u)) continue;
+        const uint64_t kk = pack_key(wstar, (uint32_t)min(v, J[j]));
+        const uint32_t bb = (uint32_t)max(v, J[j]);
+        if (kk < r.best || (kk == r.best && bb < r.bestb)) { r.best = kk; r.bestb = bb; r.bestc = cj[j]; }
+      }
+    }
+    if (differ) return r;  // the group ended inside the chunk
+    c0 += 4;
+  }
+  if (k > kW) {
+    // the candidate prefix (or the minimum's tie group) runs past the ELL
+    if (!r.found) return scan_row<false, false>(nr, dr, k, eps, v, cv, max(h, kW), N, comp, 0, reads, lv);
+    for (int c = kW; c < k; ++c) {  // continue the tie group of weight wstar in the graph row
+      const float wc = __ldcg(dr + c);
+      if (mono_bits(wc) != wstar || !(wc <= eps)) break;
+      const int32_t Jc = __ldcg(nr + c);
+      ++reads;
+      if (Jc < 0 || Jc >= N || Jc == v) continue;
+      const int32_t cc = comp_of(comp, Jc, false, lv);
+      if (cc < 0 || cc == cv) continue;
+      const uint64_t kk = pack_key(wstar, (uint32_t)min(v, Jc));
+      const uint32_t bb = (uint32_t)max(v, Jc);
+      if (kk < r.best || (kk == r.best && bb < r.bestb)) { r.best = kk; r.bestb = bb; r.bestc = cc; }
+    }
+  }
+  if (!r.found) r.h = k;
+  return r;
+}
+
 // The row kernels below take their input in ORDER: a block grabs the next
 // chunk of kChunk records from a cursor, so all SMs work on neighbouring rows
 // at any time and the component gathers of a cluster stay L2-resident (random
@@ -772,7 +877,7 @@ __global__ void __launch_bounds__(256) k_light_first(const int4* __restrict__ LE
 
 // later rounds over the ELL; see k_offer_round.  CAS (one rank): the offer is
 // a 128-bit CAS-minimum of (key, b) into KB[comp v] -- no offer list, no tie pass.
-template <int GW, bool PIPE = false, bool CAS = false>
+template <int GW, bool PIPE = false, bool CAS = false, bool LEAN = false>
 __global__ void __launch_bounds__(256) k_light_round(const int4* __restrict__ LE, int64_t ell_rows,
                                                      const int32_t* __restrict__ nbr,
                                                      const float* __restrict__ dist, int32_t ld, int32_t k, float eps,
@@ -826,7 +931,10 @@ __global__ void __launch_bounds__(256) k_light_round(const int4* __restrict__ LE
         park[base + __popc(am & ((1u << lane) - 1u))] = Rec{v, a.y};
       } else {
       const int64_t i = (int64_t)v - row_begin;
-      const RowScan r = scan_ell<false, GW, PIPE>(LE + ell_row(i), ell_ps(ell_rows), nbr + i * ld, dist + i * ld, k, eps, v, cv, a.y,
+      const RowScan r = (LEAN && GW == 4 && !PIPE)
+          ? scan_ell_lean(LE + ell_row(i), ell_ps(ell_rows), nbr + i * ld, dist + i * ld, k, eps, v, cv, a.y, N, comp,
+                          reads, lvh)
+          : scan_ell<false, GW, PIPE>(LE + ell_row(i), ell_ps(ell_rows), nbr + i * ld, dist + i * ld, k, eps, v, cv, a.y,
                                                   N, comp, 0, reads, lvh);
       if (r.found) {
         const uint32_t j = atomicAdd(&s_n, 1u);
@@ -1238,6 +1346,16 @@ __global__ void k_round_fill(int64_t C_bound, const int64_t* __restrict__ Cd, co
       Bc[c] = kSentB;
     }
   }
+}
+
+// start of a row round: the rank's output counters; with g, the round's hook counters
+__global__ void k_round_reset(RoundCounters* __restrict__ rc, int cur, RoundCounters* __restrict__ g) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  rc->na[cur ^ 1] = 0;
+  rc->ni[cur ^ 1] = 0;
+  rc->n_off = 0;
+  rc->grab = 0;
+  if (g) g->hooks = g->offered = g->uncertified = g->n_roots = 0;
 }
 
 // comp[v] += delta for the core vertices of a row range (local <-> global ids)
