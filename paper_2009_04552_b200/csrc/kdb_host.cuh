@@ -213,7 +213,7 @@ size_t carve(Layout& L, char* base, bool dry, int64_t N, int nr, const int64_t* 
   L.bloom = cv.take<uint32_t>(kBloomBits / 32);
   L.fcount = cv.take<unsigned long long>(2);
   L.tau_sample = cv.take<float>(kTauSamples);
-  L.ctr = cv.take<RoundCounters>(1);
+  L.ctr = cv.take<RoundCounters>(2);  // [1]: rank 0's counters (one snapshot copy for both)
   L.cub_bytes = cub_tmp_bytes(N, N + 1);
   L.cub_tmp = cv.take<char>(L.cub_bytes);
   L.ranks.assign(nr, RankState());
@@ -228,7 +228,7 @@ size_t carve(Layout& L, char* base, bool dry, int64_t N, int nr, const int64_t* 
     R.kthL = general ? nullptr : cv.take<uint32_t>(n);
     R.off_cap_rows = n;
     R.offers = cv.take<Offer>(general ? n + N : n);
-    R.ctr = cv.take<RoundCounters>(1);
+    R.ctr = r == 0 ? L.ctr + 1 : cv.take<RoundCounters>(1);
     if (local_first) {  // local-first phase (exact mode, > 1 rank)
       R.lctr = cv.take<RoundCounters>(1);
       R.park = cv.take<Rec>(n);
@@ -781,8 +781,11 @@ kdb_status rows_phase(Mst& m, float eps_run) {
   // snapshot of the counters after the current round into a pinned slot
   auto snapshot = [&](int rr) -> kdb_status {
     RoundCounters* sl = slot_of(rr);
-    KDB_CUDA(cudaMemcpyAsync(sl, L.ctr, sizeof(RoundCounters), cudaMemcpyDeviceToHost, st));
-    for (size_t r = 0; r < nr; ++r)
+    // the global counters and rank 0's are adjacent in the workspace (carve):
+    // one copy for both in the one-rank case
+    const size_t r0 = L.ranks[0].ctr == L.ctr + 1 ? 1 : 0;
+    KDB_CUDA(cudaMemcpyAsync(sl, L.ctr, (1 + r0) * sizeof(RoundCounters), cudaMemcpyDeviceToHost, st));
+    for (size_t r = r0; r < nr; ++r)
       KDB_CUDA(cudaMemcpyAsync(sl + 1 + r, L.ranks[r].ctr, sizeof(RoundCounters), cudaMemcpyDeviceToHost, st));
     KDB_CUDA(cudaEventRecord(ev_slot[rr % kSlots], st));
     return KDB_OK;
