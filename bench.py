@@ -167,6 +167,12 @@ def make_workload(cfg_name: str, scale: float, seed: int, device, rank=0, world=
         from datagen.partition import inertial_order
         tp = time.time()
         perm = inertial_order(X, device=device)
+        if world > 1:  # every rank must hold the same order: rank 0's permutation, broadcast
+            import torch.distributed as tdist
+            pt = torch.from_numpy(perm).to(device)
+            tdist.broadcast(pt, 0)
+            perm = pt.cpu().numpy()
+            del pt
         X, truth = X[perm], truth[perm]
         del perm
         t_part = time.time() - tp

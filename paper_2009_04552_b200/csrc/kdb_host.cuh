@@ -508,7 +508,7 @@ kdb_status rows_phase(Mst& m, float eps_run) {
   uint8_t* frz = m.local ? L.frz : nullptr;
   const int64_t ecap = m.ecap >= 0 ? m.ecap : N;
   int64_t C = 0;
-  bool fuse1 = false, packed1 = false, tile = false;
+  bool fuse1 = false, packed1 = false, packed1r = false, tile = false;
   size_t cb = L.cub_bytes;
   int32_t* gmap = nullptr;   // two-level ids in the global phase (LocalView::gmap)
   int64_t CG0 = 0;
@@ -571,11 +571,14 @@ kdb_status rows_phase(Mst& m, float eps_run) {
   tile = want.valid && want.row_begin == 0 && env_int("KDB_TILE", 0) != 0 && L.ranks[0].n_rows > 0;
   fuse1 = !general && use_compact && env_int("KDB_FUSE1", 1) != 0 && !reuse && !tile;
   packed1 = fuse1 && L.ranks.size() == 1 && !(multi_rank(comm)) && env_int("KDB_PACK1", 1) != 0;
+  // a reused ELL (eps sweep): round 1 over it (k_light_first) writes the same
+  // packed records, and k_reuse_rows the sentinel records of the other components
+  packed1r = reuse && L.rec1 && env_int("KDB_PACK1", 1) != 0;
   // Per-component slots of round 1.  Packed round 1 (one rank, fused ELL pass)
   // writes a whole record and the certificate bound for EVERY component (each
   // is one core row of this rank) and the hook reads tgt only under a finite
   // key: nothing to initialise.
-  if (!packed1) {
+  if (!packed1 && !packed1r) {
     LAUNCH(k_fill_comp_arrays, grid_for(C), kThreads, st, C, L.Kc, L.Bc, general ? nullptr : L.kmin);
     for (size_t r = 1; r < L.ranks.size(); ++r)
       LAUNCH(k_fill_comp_arrays, grid_for(C), kThreads, st, C, L.ranks[r].Kc, L.ranks[r].Bc, nullptr);
@@ -589,7 +592,7 @@ kdb_status rows_phase(Mst& m, float eps_run) {
     if (reuse) {
       R.compact = true;
       LAUNCH(k_reuse_rows, grid_for(R.n_rows), kThreads, st, R.LE, R.kthL, R.n_rows, R.row_begin, eps_run, comp,
-             L.kmin, R.act[0], &R.ctr->na[0]);
+             L.kmin, R.act[0], &R.ctr->na[0], packed1r ? L.rec1 : (int4*)nullptr);
       ++m.reused;
     } else if (R.n_rows > 0 && use_compact) {
       R.compact = true;
@@ -854,7 +857,7 @@ kdb_status rows_phase(Mst& m, float eps_run) {
         if (direct)
           LAUNCH(k_light_first, grid_for(na_ub[r]), kThreads, st, R.LE, R.n_rows, R.nbr, R.dist, ld, k, eps_run, R.row_begin, N,
                  comp, L.all_core, R.act[cur], na_ub[r], R.act[cur ^ 1], nout, &R.ctr->grab, R.Kc, R.Bc, R.tgt,
-                 &L.ctr->entries, nin, row_chunk(na_ub[r]));
+                 &L.ctr->entries, nin, row_chunk(na_ub[r]), packed1r ? L.rec1 : (int4*)nullptr, R.kthL, skip1);
         else
         {
 #define KDB_LR_LAUNCH(...)                                                                                       \
@@ -938,7 +941,7 @@ kdb_status rows_phase(Mst& m, float eps_run) {
     }
     // a5: hook + emit
     if (!hooks_zeroed) KDB_CUDA(cudaMemsetAsync(&L.ctr->hooks, 0, 4 * sizeof(uint32_t), st));
-    if (direct && packed1)
+    if (direct && (packed1 || packed1r))
       LAUNCH(k_hook<true>, grid_for(C_ub), kThreads, st, C_ub, L.Kc, L.Bc, L.tgt, kmin_cert, comp, L.parent, L.e_key,
              L.e_w, ecap, L.ctr, Cd, L.rec1, (const ulonglong2*)nullptr, frz, row_chunk((uint64_t)C_ub));
     else

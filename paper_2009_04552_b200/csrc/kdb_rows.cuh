@@ -208,6 +208,7 @@ struct RowScan {
   uint64_t best;  // minimum key of the group
   uint32_t bestb;
   int32_t bestc;  // component of the best entry's far endpoint
+  int bidx;       // scan_ell: ELL column of the best entry (-1: past the ELL); else unset
 };
 
 // Local-first phase (multi-rank exact mode): a rank contracts
@@ -604,7 +605,7 @@ __global__ void __launch_bounds__(256) k_light_ell(const int32_t* __restrict__ n
 // entry is within eps_run) -- round 1 then runs over the ELL (k_light_first).
 __global__ void k_reuse_rows(const int4* __restrict__ LE, const uint32_t* __restrict__ kthL, int64_t n_rows,
                              int64_t row_begin, float eps, const int32_t* __restrict__ comp, uint32_t* __restrict__ kmin,
-                             Rec* __restrict__ act, uint32_t* __restrict__ n_act) {
+                             Rec* __restrict__ act, uint32_t* __restrict__ n_act, int4* __restrict__ rec1 = nullptr) {
   for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n_rows; base += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = base + threadIdx.x;
     bool want = false;
@@ -612,6 +613,9 @@ __global__ void k_reuse_rows(const int4* __restrict__ LE, const uint32_t* __rest
       const int32_t cv = comp[row_begin + i];
       if (cv >= 0) {
         kmin[cv] = kthL[i];
+        // packed round 1 (k_hook<true>) reads every component's record: the
+        // sentinel with the certificate bound; k_light_first overwrites offers
+        if (rec1) __stcg(rec1 + cv, make_int4(-1, -1, -1, (int)kthL[i]));
         want = __int_as_float(__ldcs(reinterpret_cast<const int*>(LE + ell_row(i)) + 1)) <= eps;
       }
     }
@@ -680,12 +684,13 @@ __device__ __forceinline__ RowScan scan_ell(const int4* __restrict__ le, int64_t
         r.best = pack_key(wb, (uint32_t)min(v, J[j]));
         r.bestb = (uint32_t)max(v, J[j]);
         r.bestc = cj[j];
+        r.bidx = idx;
       } else {
         if (wb != wstar) { done = true; continue; }
         if (!leaving) continue;
         const uint64_t kk = pack_key(wb, (uint32_t)min(v, J[j]));
         const uint32_t bb = (uint32_t)max(v, J[j]);
-        if (kk < r.best || (kk == r.best && bb < r.bestb)) { r.best = kk; r.bestb = bb; r.bestc = cj[j]; }
+        if (kk < r.best || (kk == r.best && bb < r.bestb)) { r.best = kk; r.bestb = bb; r.bestc = cj[j]; r.bidx = idx; }
       }
     }
     }
@@ -695,6 +700,7 @@ __device__ __forceinline__ RowScan scan_ell(const int4* __restrict__ le, int64_t
     // the candidate prefix (or the minimum's tie group) runs past the ELL
     if (!r.found) {
       RowScan t = scan_row<false, DIRECT>(nr, dr, k, eps, v, cv, max(h, kW), N, comp, all_core, reads, lv);
+      t.bidx = -1;
       return t;
     }
     // continue the tie group of weight wstar in the graph row
@@ -708,7 +714,7 @@ __device__ __forceinline__ RowScan scan_ell(const int4* __restrict__ le, int64_t
       if (cc < 0 || (!DIRECT && cc == cv)) continue;
       const uint64_t kk = pack_key(wstar, (uint32_t)min(v, Jc));
       const uint32_t bb = (uint32_t)max(v, Jc);
-      if (kk < r.best || (kk == r.best && bb < r.bestb)) { r.best = kk; r.bestb = bb; r.bestc = cc; }
+      if (kk < r.best || (kk == r.best && bb < r.bestb)) { r.best = kk; r.bestb = bb; r.bestc = cc; r.bidx = -1; }
     }
   }
   if (!r.found) r.h = k;
@@ -838,7 +844,8 @@ __global__ void __launch_bounds__(256) k_light_first(const int4* __restrict__ LE
                                                      uint32_t* __restrict__ grab,
                                                      uint64_t* __restrict__ Kc, uint32_t* __restrict__ Bc,
                                                      int32_t* __restrict__ tgt, unsigned long long* __restrict__ n_entries, const uint32_t* __restrict__ n_in_p = nullptr,
-                                                     int chunk = kChunk) {
+                                                     int chunk = kChunk, int4* __restrict__ rec1 = nullptr,
+                                                     const uint32_t* __restrict__ kthL = nullptr, int skip1 = 0) {
   if (n_in_p) n_in = *n_in_p;
   __shared__ __align__(16) Rec s_rec[kChunk];
   __shared__ uint32_t s_n, s_chunk, s_base;
@@ -858,10 +865,18 @@ __global__ void __launch_bounds__(256) k_light_first(const int4* __restrict__ LE
                                        all_core, reads);
       if (r.found) {
         const int32_t cv = all_core ? v : gat(comp + v);
-        Kc[cv] = r.best;
-        Bc[cv] = r.bestb;
+        bool skip_head = false;
+        if (rec1) {  // packed record (K, B, kmin) for k_hook<true>, as the fused ELL pass writes
+          const uint32_t kb = kthL[i];
+          __stcg(rec1 + cv, make_int4((int)(uint32_t)r.best, (int)(uint32_t)(r.best >> 32), (int)r.bestb, (int)kb));
+          // the certified minimum at the head hooks: from round 2 on it is intra
+          skip_head = skip1 && r.bidx == r.h && (uint32_t)(r.best >> 32) < kb;
+        } else {
+          Kc[cv] = r.best;
+          Bc[cv] = r.bestb;
+        }
         tgt[cv] = r.bestc;
-        s_rec[atomicAdd(&s_n, 1u)] = Rec{v, r.h};
+        s_rec[atomicAdd(&s_n, 1u)] = Rec{v, skip_head ? r.h + 1 : r.h};
       }
     }
     __syncthreads();
