@@ -868,7 +868,11 @@ kdb_status rows_phase(Mst& m, float eps_run) {
           // pipelined chunk loads pay when many rows scan past their first chunk
           // (C3: its inner shell is all light); they cost occupancy otherwise
           const int pk = env_int("KDB_PIPE", -1);
-          const bool pipe = pk >= 0 ? pk != 0 : (uint64_t)R.n_deep * 100 > (uint64_t)R.n_rows * 15;
+          // KDB_PIPE_R0..KDB_PIPE_R1 (experiment): pipelined loads in those rounds only
+          const int pr0 = env_int("KDB_PIPE_R0", 0), pr1 = env_int("KDB_PIPE_R1", -1);
+          const bool pipe = pk >= 0 ? pk != 0
+                                    : (rounds >= pr0 && rounds <= pr1) ||
+                                          (uint64_t)R.n_deep * 100 > (uint64_t)R.n_rows * 15;
           if (cas) {
             if (pipe) KDB_LR_LAUNCH(4, true, true);
             else if (lean) KDB_LR_LAUNCH(4, false, true, true);
