@@ -277,14 +277,17 @@ def run_reference(args):
             times.append(dt)
     t = float(np.mean(times))
     value = ns * W["k"] * len(eps_list) / t
-    sample = (f"rows [0, {ns}) of {args.config} (cluster-major ids; entries to ids >= {ns} skipped), "
-              f"{ns * W['k']} entries per step")
+    whole = whole_workload_baseline(args.config, args.scale, ec, len(eps_list), W["order"])
+    sample = (f"rows [0, {ns}) of {args.config} ({W['order']} order: "
+              + ("a compact piece of one cluster" if W["order"] == "inertial" else "cluster-major ids")
+              + f"; entries to ids >= {ns} skipped), {ns * W['k']} entries per step")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": dict(workload_desc(args.config, W, args.scale), **stage_desc(ec, eps_list, W)),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample,
-                             "cpu_model": host_cpu()[0], "box_cores": host_cpu()[1]},
+                             "cpu_model": host_cpu()[0], "box_cores": host_cpu()[1],
+                             **({"whole_workload_measured": whole} if whole else {})},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     emit(line, args)
 
