@@ -374,6 +374,9 @@ def run_ours(args):
     rank, world, local = dist_env()
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    # tuning options (include/kdb.h kdb_set_option): the KDB_* variables of this
+    # process's environment, applied once here -- the library never reads them
+    knobs = kdb.options_from_env()
     torch.cuda.set_device(local)
     dev = torch.device(f"cuda:{local}")
     if world > 1:
@@ -393,7 +396,8 @@ def run_ours(args):
         torch.cuda.empty_cache()
     comm = kdb.Comm.nccl(rank, world) if world > 1 else None
     if args.nccl1 and world == 1:
-        os.environ["KDB_NCCL_FORCE"] = "1"
+        kdb.set_option("KDB_NCCL_FORCE", 1)
+        knobs["KDB_NCCL_FORCE"] = 1
         comm = kdb.Comm.nccl_single()
     if args.sim and world == 1:  # P virtual ranks on this GPU (DESIGN.md §7 scaling model)
         comm = kdb.Comm.sim(args.sim)
@@ -532,8 +536,7 @@ def run_ours(args):
                                + (f" (sim communicator: {args.sim} virtual ranks on one GPU)"
                                   if args.sim and world == 1 else ""),
                                exact_graph=not args.general,
-                               knobs={k_: v_ for k_, v_ in sorted(os.environ.items()) if k_.startswith("KDB_")}
-                               or "defaults (no KDB_* overrides)",
+                               knobs=dict(sorted(knobs.items())) or "defaults (no tuning-option overrides)",
                                **stage_desc(ec, eps_list, W)),
                 "roofline": roof,
                 "stage_roofline": {"t_min_ms": t_min_ms, "frac": t_min_ms / ms,

@@ -240,6 +240,26 @@ int kdb_profile_read(char* names, size_t names_len, double* ms, long long* count
 const char* kdb_status_string(kdb_status s);
 const char* kdb_last_error(void);
 
+/* Tuning options: the experiment switches of DESIGN.md §16 (e.g. "KDB_LIGHT":
+ * light-phase column count, "KDB_FILTER": 0 disables the heavy filter,
+ * "KDB_TRACE": per-round log on stderr).  Every option has a built-in default
+ * (the measured configuration); none changes the result, only the way it is
+ * computed (the parity suite runs the non-default settings).  The library
+ * never reads them from the environment: the caller sets them here (the
+ * Python binding's set_option / options(); bench.py forwards KDB_* variables
+ * of its own environment once at start).  Process-wide, guarded by a mutex;
+ * a call already running may or may not see a change.
+ *   kdb_set_option: KDB_EINVAL for an unknown name (nothing changed).
+ *   kdb_get_option: 1 and *value (host) if set, 0 if the default applies,
+ *                   -1 for an unknown name.
+ *   kdb_reset_options: every option back to its default.
+ *   kdb_option_name: the i-th known name (host out, static storage); 0 past
+ *                    the end. */
+kdb_status kdb_set_option(const char* name, long long value);
+int kdb_get_option(const char* name, long long* value);
+void kdb_reset_options(void);
+int kdb_option_name(int i, const char** name);
+
 #ifdef __cplusplus
 }
 #endif

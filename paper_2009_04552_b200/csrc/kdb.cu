@@ -196,7 +196,39 @@ struct Prof {
   }
 };
 Prof g_prof;
-const int g_trace = getenv("KDB_TRACE") ? atoi(getenv("KDB_TRACE")) : 0;  // per-round log to stderr
+// ============================================================================
+// Tuning options (experiment switches): set only through
+// kdb_set_option (include/kdb.h); the library never reads them from the
+// environment.  Every call site names its own default, which is what runs
+// unless the caller overrode the option.
+// ============================================================================
+const char* const kOptNames[] = {
+    "KDB_CAS",      "KDB_COMPACT", "KDB_FASTFILTER", "KDB_FILTER",  "KDB_FUSE1",   "KDB_GMAP",      "KDB_GW",
+    "KDB_L1GAT",    "KDB_L2HINT",  "KDB_LEAN",       "KDB_LIGHT",   "KDB_LOCAL",   "KDB_MSF_COUNT", "KDB_NCCL_FORCE",
+    "KDB_PACK1",    "KDB_PIPE",    "KDB_PIPE_R0",    "KDB_PIPE_R1", "KDB_PRECHECK", "KDB_REUSE",    "KDB_SKIP1",
+    "KDB_SPARSE",   "KDB_SURVCAP", "KDB_TILE",       "KDB_TILE_MAXR", "KDB_TILE_ROWS", "KDB_TRACE"};
+constexpr int kNumOpts = (int)(sizeof(kOptNames) / sizeof(kOptNames[0]));
+std::mutex g_opt_mu;
+long long g_opt_val[kNumOpts];
+bool g_opt_isset[kNumOpts];
+int opt_index(const char* name) {
+  if (!name) return -1;
+  for (int i = 0; i < kNumOpts; ++i)
+    if (strcmp(kOptNames[i], name) == 0) return i;
+  return -1;
+}
+// the caller's value of option `name`, else the call site's default
+int opt_int(const char* name, int dflt) {
+  const int i = opt_index(name);
+  std::lock_guard<std::mutex> lk(g_opt_mu);
+  return (i >= 0 && g_opt_isset[i]) ? (int)g_opt_val[i] : dflt;
+}
+bool opt_set(const char* name) {
+  const int i = opt_index(name);
+  std::lock_guard<std::mutex> lk(g_opt_mu);
+  return i >= 0 && g_opt_isset[i];
+}
+bool trace_on() { return opt_int("KDB_TRACE", 0) != 0; }  // per-round log to stderr
 
 struct LaunchScope {
   const char* name;
@@ -448,6 +480,34 @@ const char* kdb_status_string(kdb_status s) {
 
 const char* kdb_last_error(void) { return g_err.c_str(); }
 
+kdb_status kdb_set_option(const char* name, long long value) {
+  const int i = opt_index(name);
+  if (i < 0) return set_err(KDB_EINVAL, "unknown option '%s'", name ? name : "(null)");
+  std::lock_guard<std::mutex> lk(g_opt_mu);
+  g_opt_val[i] = value;
+  g_opt_isset[i] = true;
+  return KDB_OK;
+}
+
+int kdb_get_option(const char* name, long long* value) {
+  const int i = opt_index(name);
+  if (i < 0) return -1;
+  std::lock_guard<std::mutex> lk(g_opt_mu);
+  if (value) *value = g_opt_isset[i] ? g_opt_val[i] : 0;
+  return g_opt_isset[i] ? 1 : 0;
+}
+
+void kdb_reset_options(void) {
+  std::lock_guard<std::mutex> lk(g_opt_mu);
+  for (int i = 0; i < kNumOpts; ++i) g_opt_isset[i] = false;
+}
+
+int kdb_option_name(int i, const char** name) {
+  if (i < 0 || i >= kNumOpts) return 0;
+  if (name) *name = kOptNames[i];
+  return 1;
+}
+
 int kdb_last_mst_stats(double* out, int cap) {
   int n = std::min(cap, 32);
   for (int i = 0; i < n; ++i) out[i] = g_stats[i];
@@ -624,7 +684,7 @@ kdb_status mst_impl(const kdb_graph* g, float eps, const uint32_t* core_bits, in
   // a kept light ELL is only valid until the workspace's next call: take it out
   // of the table now, put a new one back on success
   m.ws = ws0;
-  m.reuse_req = (g->flags & KDB_GRAPH_REUSE) != 0 && env_int("KDB_REUSE", 1) != 0;
+  m.reuse_req = (g->flags & KDB_GRAPH_REUSE) != 0 && opt_int("KDB_REUSE", 1) != 0;
   m.ell_prev = ell_prev;
   Layout& L = m.L;
   std::vector<int64_t> rb, rn;
@@ -650,7 +710,7 @@ kdb_status mst_impl(const kdb_graph* g, float eps, const uint32_t* core_bits, in
 
   // Filter-Boruvka when a light threshold below eps exists;
   // plain rows-Boruvka over the whole candidate graph otherwise.
-  const int light_m = env_int("KDB_LIGHT", 10);
+  const int light_m = opt_int("KDB_LIGHT", 10);
   bool filtered = false;
   if (inexact) {
     // U_i MST_i,local: the rows phase on the local view; then MST_cut: the cut
@@ -675,8 +735,8 @@ kdb_status mst_impl(const kdb_graph* g, float eps, const uint32_t* core_bits, in
     KDB_CUDA(cudaEventRecord(m.ev[1], st));
     m.t_filter += elapsed(m.ev[0], m.ev[1]);
     KDB_TRY(heavy_phase(m));
-  } else if (env_int("KDB_FILTER", 1) && light_m >= 1 && light_m < m.k &&
-             (getenv("KDB_LIGHT") || m.k >= 4 * light_m)) {
+  } else if (opt_int("KDB_FILTER", 1) && light_m >= 1 && light_m < m.k &&
+             (opt_set("KDB_LIGHT") || m.k >= 4 * light_m)) {
     // default policy: split only when the rows are long next to the light
     // prefix (k >= 4 x the light column): with k = 16 / 32 the filter pass and
     // the heavy phase cost more than the rows phase saves (C1 1.49 -> 0.99 ms,
@@ -741,7 +801,7 @@ kdb_status mst_impl(const kdb_graph* g, float eps, const uint32_t* core_bits, in
     unsigned long long* vb2 = reinterpret_cast<unsigned long long*>(L.Kc);  // N + 1, free now
     int abits = 1;
     while (abits < 32 && ((int64_t)1 << abits) < N) ++abits;
-    if (4 * ne >= N && env_int("KDB_MSF_COUNT", 0) != 0) {
+    if (4 * ne >= N && opt_int("KDB_MSF_COUNT", 0) != 0) {
       // dense forest (C4: N - 10 edges): a counting sort by a over the N ids --
       // one atomic and one scatter per edge instead of the radix sort's passes.
       // Off by default (KDB_MSF_COUNT=1): C4 2.0 ms (scatter 1.41, count 0.47,

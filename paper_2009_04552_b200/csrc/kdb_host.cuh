@@ -298,18 +298,16 @@ void rank_ranges(const kdb_graph* g, kdb_comm* comm, std::vector<int64_t>& rb, s
   }
 }
 
-// Collectives run with a real NCCL communicator of > 1 rank -- or, with
-// KDB_NCCL_FORCE=1 (tests), on a 1-rank NCCL communicator too, so one GPU runs
+// Collectives run with a real NCCL communicator of > 1 rank -- or, with the
+// option KDB_NCCL_FORCE = 1 (tests, bench --nccl1), on a 1-rank NCCL communicator too, so one GPU runs
 // the multi-rank host logic (exact per-round counts, agreed branches) through
 // real NCCL calls.
 bool multi_rank(const kdb_comm* comm) {
   if (!comm || comm->kind != 1) return false;
   if (comm->nranks > 1) return true;
-  const char* f = getenv("KDB_NCCL_FORCE");
-  return f && atoi(f) != 0;
+  return opt_int("KDB_NCCL_FORCE", 0) != 0;
 }
 
-int env_int(const char* name, int dflt);
 
 // Local-first contraction runs when more than one rank shares
 // the graph (a real NCCL communicator, the sim communicator with P >= 2, or the
@@ -317,9 +315,9 @@ int env_int(const char* name, int dflt);
 // certificate is what lets a rank decide from its own rows); KDB_LOCAL=0 turns
 // it off (the replicated-rounds path of round 1).
 bool local_first_on(const kdb_graph* g, const kdb_comm* comm) {
-  if (!(g->flags & KDB_GRAPH_EXACT) || env_int("KDB_LOCAL", 1) == 0) return false;
-  if (env_int("KDB_COMPACT", 1) == 0 || env_int("KDB_FUSE1", 1) == 0 || env_int("KDB_CAS", 1) == 0 ||
-      env_int("KDB_PACK1", 1) == 0)
+  if (!(g->flags & KDB_GRAPH_EXACT) || opt_int("KDB_LOCAL", 1) == 0) return false;
+  if (opt_int("KDB_COMPACT", 1) == 0 || opt_int("KDB_FUSE1", 1) == 0 || opt_int("KDB_CAS", 1) == 0 ||
+      opt_int("KDB_PACK1", 1) == 0)
     return false;  // the phase runs on the one-rank machinery (ELL, fused round 1, CAS offers)
   return multi_rank(comm) || (comm && comm->kind == 2 && comm->nranks >= 2);
 }
@@ -338,10 +336,6 @@ kdb_status allreduce_max_u32(kdb_comm* comm, uint32_t* p, int64_t n, cudaStream_
   return nccl_check(g_nccl.AllReduce(p, p, (size_t)n, ncclUint32, ncclMax, comm->nccl, st), "ncclAllReduce(u32,max)");
 }
 
-int env_int(const char* name, int dflt) {
-  const char* s = getenv(name);
-  return (s && *s) ? atoi(s) : dflt;
-}
 
 bool nr_ranks_is_one(const Layout& L) { return L.ranks.size() == 1; }
 
@@ -491,16 +485,16 @@ kdb_status rows_phase(Mst& m, float eps_run) {
   const bool vec = (ld % 4) == 0;
   cudaEvent_t* ev = m.ev;
   KDB_CUDA(cudaEventRecord(ev[0], st));
-  const bool use_compact = env_int("KDB_COMPACT", 1) != 0;
-  const int gw = env_int("KDB_GW", 4);  // component-gather width of the later light rounds (scan_ell)
-  const bool lean = env_int("KDB_LEAN", 0) != 0;  // chunk scan on bit masks (scan_ell_lean): measured slower, off
-  const bool sparse_ids = env_int("KDB_SPARSE", 1) != 0;  // keep root ids once few components remain
-  const int skip1 = env_int("KDB_SKIP1", 1);  // round-2 heads skip the entry round 1 hooked along
+  const bool use_compact = opt_int("KDB_COMPACT", 1) != 0;
+  const int gw = opt_int("KDB_GW", 4);  // component-gather width of the later light rounds (scan_ell)
+  const bool lean = opt_int("KDB_LEAN", 0) != 0;  // chunk scan on bit masks (scan_ell_lean): measured slower, off
+  const bool sparse_ids = opt_int("KDB_SPARSE", 1) != 0;  // keep root ids once few components remain
+  const int skip1 = opt_int("KDB_SKIP1", 1);  // round-2 heads skip the entry round 1 hooked along
   // bit 0: evict-last L2 policy on the light rounds' component gathers; bit 1:
   // those gathers through L1 (KDB_L1GAT)
   // (KDB_L1GAT; default: when most rows' nearest neighbour has a nearby id, k_light_ell counts them)
-  int l2hint = (env_int("KDB_L2HINT", 1) ? 1 : 0) | (env_int("KDB_L1GAT", 0) > 0 ? 2 : 0);
-  const int l1gat_env = env_int("KDB_L1GAT", -1);
+  int l2hint = (opt_int("KDB_L2HINT", 1) ? 1 : 0) | (opt_int("KDB_L1GAT", 0) > 0 ? 2 : 0);
+  const int l1gat_env = opt_int("KDB_L1GAT", -1);
   // local-first phase of one rank (m.local): LOCAL component ids, the rank's
   // per-component slices, no exchange; the global phase (m.cont) continues the
   // rounds from the rows the local phases parked
@@ -514,7 +508,7 @@ kdb_status rows_phase(Mst& m, float eps_run) {
   int64_t CG0 = 0;
   if (m.cont) {
     C = m.C;  // global components after the local-first phases (state set by local_first)
-    if (env_int("KDB_GMAP", 1) != 0 && C > 0) {
+    if (opt_int("KDB_GMAP", 1) != 0 && C > 0) {
       gmap = L.hcomp;  // free until the heavy phase
       CG0 = C;
       LAUNCH(k_iota, grid_for(C), kThreads, st, gmap, C);
@@ -568,12 +562,12 @@ kdb_status rows_phase(Mst& m, float eps_run) {
   // (with a reused ELL round 1 runs over it: k_light_first)
   // tile round (one rank, exact mode, light ELL): round 1 is tile-local
   // Boruvka in shared memory (k_tile_round) instead of the fused singleton round
-  tile = want.valid && want.row_begin == 0 && env_int("KDB_TILE", 0) != 0 && L.ranks[0].n_rows > 0;
-  fuse1 = !general && use_compact && env_int("KDB_FUSE1", 1) != 0 && !reuse && !tile;
-  packed1 = fuse1 && L.ranks.size() == 1 && !(multi_rank(comm)) && env_int("KDB_PACK1", 1) != 0;
+  tile = want.valid && want.row_begin == 0 && opt_int("KDB_TILE", 0) != 0 && L.ranks[0].n_rows > 0;
+  fuse1 = !general && use_compact && opt_int("KDB_FUSE1", 1) != 0 && !reuse && !tile;
+  packed1 = fuse1 && L.ranks.size() == 1 && !(multi_rank(comm)) && opt_int("KDB_PACK1", 1) != 0;
   // a reused ELL (eps sweep): round 1 over it (k_light_first) writes the same
   // packed records, and k_reuse_rows the sentinel records of the other components
-  packed1r = reuse && L.rec1 && env_int("KDB_PACK1", 1) != 0;
+  packed1r = reuse && L.rec1 && opt_int("KDB_PACK1", 1) != 0;
   // Per-component slots of round 1.  Packed round 1 (one rank, fused ELL pass)
   // writes a whole record and the certificate bound for EVERY component (each
   // is one core row of this rank) and the hook reads tgt only under a finite
@@ -681,7 +675,7 @@ kdb_status rows_phase(Mst& m, float eps_run) {
   // of (key, b) (no offer list, no tie pass); KB reuses the round-1 records
   // (rec1: 16 B per component, free once round 1 has hooked)
   const bool cas = !general && nr_ranks_is_one(L) && !multi_rank(comm) && any_compact && L.rec1 &&
-                   env_int("KDB_CAS", 1) != 0;
+                   opt_int("KDB_CAS", 1) != 0;
   ulonglong2* KB = cas ? reinterpret_cast<ulonglong2*>(L.rec1) : nullptr;
   int cur = fused ? 1 : 0;  // fused round 1: its OUTPUT list is act[0] already
   int par = 0;              // component count ping-pong: Cs[par] current
@@ -816,8 +810,8 @@ kdb_status rows_phase(Mst& m, float eps_run) {
   LAUNCH_DYN(k_tile_round<T>, (int)std::min<int64_t>((R.n_rows + (T) - 1) / (T), 1 << 30), (T),                 \
              sizeof(TileSmem<T>), st, R.LE, R.n_rows, k, eps_run, N, comp, core_bits, L.kmin, L.parent, L.e_key, \
              L.e_w, ecap, R.act[cur ^ 1], &R.ctr->na[cur ^ 1], &R.ctr->grab, L.ctr, &L.ctr->entries,      \
-             std::max(1, std::min(env_int("KDB_TILE_MAXR", kTileMaxRounds), kTileMaxRounds)))
-      if (env_int("KDB_TILE_ROWS", 1024) == 512) KDB_TILE_LAUNCH(512);
+             std::max(1, std::min(opt_int("KDB_TILE_MAXR", kTileMaxRounds), kTileMaxRounds)))
+      if (opt_int("KDB_TILE_ROWS", 1024) == 512) KDB_TILE_LAUNCH(512);
       else KDB_TILE_LAUNCH(1024);
 #undef KDB_TILE_LAUNCH
       KDB_CUDA(cudaGetLastError());
@@ -829,7 +823,7 @@ kdb_status rows_phase(Mst& m, float eps_run) {
     {
       uint64_t live = 0;
       for (size_t r = 0; r < nr; ++r) live += na_ub[r];
-      const int pc = env_int("KDB_PRECHECK", -1);
+      const int pc = opt_int("KDB_PRECHECK", -1);
       precheck = pc >= 0 ? pc : (live > 8 * (uint64_t)std::max<int64_t>(C_ub, 1) ? 1 : 0);
     }
     // global phase of the local-first scheme: time the per-rank work (offers,
@@ -867,9 +861,9 @@ kdb_status rows_phase(Mst& m, float eps_run) {
          m.local ? &L.ctr->n_park : nullptr, l2hint, row_chunk(na_ub[r]))
           // pipelined chunk loads pay when many rows scan past their first chunk
           // (C3: its inner shell is all light); they cost occupancy otherwise
-          const int pk = env_int("KDB_PIPE", -1);
+          const int pk = opt_int("KDB_PIPE", -1);
           // KDB_PIPE_R0..KDB_PIPE_R1 (experiment): pipelined loads in those rounds only
-          const int pr0 = env_int("KDB_PIPE_R0", 0), pr1 = env_int("KDB_PIPE_R1", -1);
+          const int pr0 = opt_int("KDB_PIPE_R0", 0), pr1 = opt_int("KDB_PIPE_R1", -1);
           const bool pipe = pk >= 0 ? pk != 0
                                     : (rounds >= pr0 && rounds <= pr1) ||
                                           (uint64_t)R.n_deep * 100 > (uint64_t)R.n_rows * 15;
@@ -964,7 +958,7 @@ kdb_status rows_phase(Mst& m, float eps_run) {
     KDB_CUDA(cudaEventSynchronize(ev_slot[check % kSlots]));
     last_checked = check;
     const RoundCounters g = slot_of(check)[0];
-    if (g_trace)
+    if (trace_on())
       fprintf(stderr, "[kdb] round %d eps=%.6g C->%lld offered=%u hooks=%u live=%u entries=%llu\n", check,
               (double)eps_run, (long long)g.Cs[(check & 1) ? 1 : 0], g.offered, g.hooks,
               slot_of(check)[1].na[check & 1], (unsigned long long)g.entries);
@@ -1295,12 +1289,12 @@ kdb_status filter_phase(Mst& m, float eps, bool* overflow) {
   cudaStream_t st = m.st;
   KDB_CUDA(cudaEventRecord(m.ev[0], st));
   // KDB_SURVCAP (tests): a smaller survivor capacity, to exercise the fallback
-  const int64_t cap_env = env_int("KDB_SURVCAP", -1);
+  const int64_t cap_env = opt_int("KDB_SURVCAP", -1);
   // fast-path tables (identical on every rank: comp is replicated)
   int shift = 0;
   while (((m.N + ((int64_t)1 << shift) - 1) >> shift) > kDomMax) ++shift;
   const int64_t nblk = (m.N + ((int64_t)1 << shift) - 1) >> shift;
-  bool fast = env_int("KDB_FASTFILTER", 1) != 0;
+  bool fast = opt_int("KDB_FASTFILTER", 1) != 0;
   unsigned long long fc[2] = {0, 0};
   int2* rng = reinterpret_cast<int2*>(L.Kc);  // C_L entries; Kc is refilled by the heavy phase
   KDB_CUDA(cudaMemsetAsync(L.fcount, 0, 2 * sizeof(unsigned long long), st));

@@ -75,6 +75,10 @@ def lib():
     L.kdb_profile_reset.restype = None
     L.kdb_launch_count.restype = C.c_longlong
     L.kdb_profile_read.argtypes = [C.c_char_p, C.c_size_t, C.POINTER(C.c_double), C.POINTER(C.c_longlong), C.c_int]
+    L.kdb_set_option.argtypes = [C.c_char_p, C.c_longlong]
+    L.kdb_get_option.argtypes = [C.c_char_p, C.POINTER(C.c_longlong)]
+    L.kdb_reset_options.restype = None
+    L.kdb_option_name.argtypes = [C.c_int, C.POINTER(C.c_char_p)]
     _lib = L
     return L
 
@@ -84,7 +88,50 @@ EXPORTS = sorted(["kdb_nccl_unique_id", "kdb_comm_create_nccl", "kdb_comm_create
                   "kdb_core_mark", "kdb_mst_workspace_bytes", "kdb_mst", "kdb_label", "kdb_last_mst_stats",
                   "kdb_profile_enable", "kdb_profile_reset", "kdb_launch_count", "kdb_profile_read",
                   "kdb_status_string", "kdb_last_error", "kdb_nmi_workspace_bytes", "kdb_nmi",
-                  "kdb_mst_inexact_workspace_bytes", "kdb_mst_inexact"])
+                  "kdb_mst_inexact_workspace_bytes", "kdb_mst_inexact", "kdb_set_option", "kdb_get_option",
+                  "kdb_reset_options", "kdb_option_name"])
+
+
+def option_names() -> list[str]:
+    """The tuning options libkdb.so knows (include/kdb.h kdb_set_option)."""
+    L, out, i = lib(), [], 0
+    nm = C.c_char_p()
+    while L.kdb_option_name(i, C.byref(nm)):
+        out.append(nm.value.decode())
+        i += 1
+    return out
+
+
+def set_option(name: str, value) -> None:
+    """Override one tuning option process-wide (DESIGN.md §16 switches)."""
+    _check(lib().kdb_set_option(name.encode(), int(value)), f"set_option({name})")
+
+
+def get_option(name: str):
+    """The caller-set value of an option, None if its default applies."""
+    v = C.c_longlong()
+    rc = lib().kdb_get_option(name.encode(), C.byref(v))
+    if rc < 0:
+        raise KdbError(f"unknown option {name}")
+    return int(v.value) if rc == 1 else None
+
+
+def reset_options() -> None:
+    lib().kdb_reset_options()
+
+
+def options_from_env(environ=None) -> dict:
+    """Apply the KDB_* variables of `environ` that name options (bench.py and
+    the tools scripts call this once at start; the library itself never reads
+    the environment).  Returns what was applied."""
+    environ = os.environ if environ is None else environ
+    applied = {}
+    for name in option_names():
+        v = environ.get(name)
+        if v not in (None, ""):
+            set_option(name, int(v))
+            applied[name] = int(v)
+    return applied
 
 
 def _check(rc: int, what: str):

@@ -13,6 +13,12 @@ import oracle
 import paper_2009_04552_b200 as kdb
 
 
+def kdb_opt(name: str, value) -> None:
+    """Override a libkdb tuning option for the current test (tests/conftest.py
+    resets every option after each test)."""
+    kdb.set_option(name, int(value))
+
+
 def run_gpu(nbr: np.ndarray, dist: np.ndarray, M: int, eps, *, exact: bool = False,
             comm: "kdb.Comm | None" = None, device: str = "cuda:0", edge_cols: int = 0):
     g = kdb.Graph(torch.from_numpy(np.ascontiguousarray(nbr, np.int32)).to(device),

@@ -163,3 +163,30 @@ def test_debug_build_exports_and_guards(lib):
     D.kdb_mst_workspace_bytes.restype = C.c_size_t
     g = _graph(n_total=1000, n_rows=1000, k=32, flags=1)
     assert D.kdb_mst_workspace_bytes(C.byref(g), None) > lib.kdb_mst_workspace_bytes(C.byref(g), None)
+
+
+def test_tuning_options_are_explicit_not_environment(lib, monkeypatch):
+    """Tuning options come only from kdb_set_option (include/kdb.h): an unknown
+    name is rejected, set/get/reset round-trip, and a KDB_* environment
+    variable does not reach the library (the binding forwards it only when
+    asked: options_from_env)."""
+    import paper_2009_04552_b200 as kdb
+    names = kdb.option_names()
+    assert "KDB_LIGHT" in names and "KDB_FILTER" in names and len(names) == len(set(names))
+    assert lib.kdb_set_option(b"KDB_NO_SUCH_OPTION", 1) == 1  # KDB_EINVAL
+    assert lib.kdb_get_option(b"KDB_NO_SUCH_OPTION", None) == -1
+    kdb.reset_options()
+    monkeypatch.setenv("KDB_LIGHT", "3")
+    assert kdb.get_option("KDB_LIGHT") is None  # the environment alone changes nothing
+    assert kdb.options_from_env() == {"KDB_LIGHT": 3}
+    assert kdb.get_option("KDB_LIGHT") == 3
+    kdb.set_option("KDB_FILTER", 0)
+    assert kdb.get_option("KDB_FILTER") == 0
+    kdb.reset_options()
+    assert all(kdb.get_option(n) is None for n in names)
+    # no getenv of a tuning option is left in the library's sources
+    csrc = os.path.join(ROOT, "paper_2009_04552_b200", "csrc")
+    for f in os.listdir(csrc):
+        src = open(os.path.join(csrc, f)).read()
+        for n in names:
+            assert f'getenv("{n}")' not in src, (f, n)

@@ -90,11 +90,11 @@ def test_config_c4_edge_cols_M():
     b = torch.from_numpy(got["msf_b"].astype(np.int64)).cuda()
     inrow = (nbr[a, :M].long() == b[:, None]).any(1) | (nbr[b, :M].long() == a[:, None]).any(1)
     assert bool(inrow.all())
-    os.environ["KDB_FILTER"] = "0"
+    kdb.set_option("KDB_FILTER", 0)
     try:
         alt = _gpu(nbr, dist, M, eps, edge_cols=M)
     finally:
-        del os.environ["KDB_FILTER"]
+        kdb.reset_options()
     for key in ("core", "comp", "labels", "msf_a", "msf_b", "msf_w"):
         assert np.array_equal(got[key], alt[key]), key
 
@@ -168,11 +168,11 @@ def test_config_large_parity(name, scale):
     got = _gpu(nbr, dist, M, eps)
     _check_properties(nbr, dist, M, eps, got)
     # an independent path (no filter: plain rows-Boruvka at eps) gives the same bits
-    os.environ["KDB_FILTER"] = "0"
+    kdb.set_option("KDB_FILTER", 0)
     try:
         alt = _gpu(nbr, dist, M, eps)
     finally:
-        del os.environ["KDB_FILTER"]
+        kdb.reset_options()
     for key in ("core", "comp", "labels", "msf_a", "msf_b", "msf_w"):
         assert np.array_equal(got[key], alt[key]), key
     assert got["msf_weight"] == alt["msf_weight"]

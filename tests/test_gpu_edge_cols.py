@@ -16,6 +16,7 @@ import torch
 
 from datagen import eps_from_graph, gen_c1, knn_bruteforce, random_graph
 from tests.kdb_harness import assert_parity, oracle_run, result_dict, run_gpu
+from tests.kdb_harness import kdb_opt as _kdb_opt
 from tests.test_gpu_parity import RANDOM_CASES
 
 pytestmark = pytest.mark.gpu
@@ -58,7 +59,7 @@ def test_c1_edge_cols_M(c1_graph, light, exact, P, monkeypatch):
     """C1 at full size with the Def. 6 edge set; filtered (light < M) and
     unfiltered (light >= M) paths, exact-graph certificate on and off, sim ranks."""
     import paper_2009_04552_b200 as kdb
-    monkeypatch.setenv("KDB_LIGHT", light)
+    _kdb_opt("KDB_LIGHT", light)
     nbr, dist = c1_graph
     eps = eps_from_graph(dist, 8, 1.5)
     exp = oracle_run(nbr, dist, 8, eps, edge_cols=8)

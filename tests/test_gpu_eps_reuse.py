@@ -14,6 +14,7 @@ import torch
 import paper_2009_04552_b200 as kdb
 from datagen import eps_from_graph, gen_c1, knn_bruteforce
 from tests.kdb_harness import assert_parity, oracle_run, result_dict
+from tests.kdb_harness import kdb_opt as _kdb_opt
 
 pytestmark = pytest.mark.gpu
 
@@ -33,7 +34,7 @@ def test_sweep_reuses_the_ell(case, order, monkeypatch):
         X, _ = gen_c1(0)
         nbr, dist = knn_bruteforce(X, 16)
         M = 8
-        monkeypatch.setenv("KDB_LIGHT", "10")  # k = 16: the light/heavy split only when asked for
+        _kdb_opt("KDB_LIGHT", "10")  # k = 16: the light/heavy split only when asked for
     else:
         nbr, dist = _points(3, 3000, 3, 48)
         M = 12

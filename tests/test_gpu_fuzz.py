@@ -49,14 +49,14 @@ def test_fuzz_random_graphs(c):
     eps = np.float32(np.quantile(fin, c["q"])) if fin.size else np.float32(1.0)
     if not eps > 0:
         eps = np.float32(1e-3)
-    os.environ["KDB_LIGHT"] = c["light"]
+    kdb.set_option("KDB_LIGHT", c["light"])
     try:
         exp = oracle_run(nbr, dist, c["M"], eps, edge_cols=c["edge_cols"] or None)
         got = run_gpu(nbr, dist, c["M"], eps, exact=False, edge_cols=c["edge_cols"],
                       comm=kdb.Comm.sim(c["P"]) if c["P"] else None)
         assert_parity(got, exp)
     finally:
-        os.environ.pop("KDB_LIGHT", None)
+        kdb.reset_options()
 
 
 @settings(max_examples=80, deadline=None, derandomize=True, suppress_health_check=list(HealthCheck))

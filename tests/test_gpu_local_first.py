@@ -17,6 +17,7 @@ import torch
 
 from datagen import eps_from_graph, gen_c1, knn_bruteforce
 from tests.kdb_harness import assert_parity, oracle_run, run_gpu
+from tests.kdb_harness import kdb_opt as _kdb_opt
 
 pytestmark = pytest.mark.gpu
 
@@ -34,9 +35,9 @@ def test_c1_local_first(c1_graph, P, light, monkeypatch):
     import paper_2009_04552_b200 as kdb
     nbr, dist = c1_graph
     if light == "off":
-        monkeypatch.setenv("KDB_FILTER", "0")
+        _kdb_opt("KDB_FILTER", "0")
     else:
-        monkeypatch.setenv("KDB_LIGHT", light)
+        _kdb_opt("KDB_LIGHT", light)
     for f in (0.6, 1.5, 4.0):
         eps = eps_from_graph(dist, 8, f)
         exp = oracle_run(nbr, dist, 8, eps)
@@ -45,9 +46,9 @@ def test_c1_local_first(c1_graph, P, light, monkeypatch):
         lf = got["stats"].get("local_first")
         assert lf is not None and lf["local_ms_sum"] >= lf["local_ms_max"] >= 0
         assert 0 <= lf["parked_rows"] <= len(nbr)
-        monkeypatch.setenv("KDB_LOCAL", "0")
+        _kdb_opt("KDB_LOCAL", "0")
         off = run_gpu(nbr, dist, 8, eps, exact=True, comm=kdb.Comm.sim(P))
-        monkeypatch.delenv("KDB_LOCAL")
+        kdb.reset_options()
         assert "local_first" not in off["stats"]
         assert_parity(off, exp)
 

@@ -15,6 +15,7 @@ import torch
 
 from datagen import eps_from_graph, gen_c1, knn_bruteforce, random_graph
 from tests.kdb_harness import assert_parity, oracle_run, run_gpu
+from tests.kdb_harness import kdb_opt as _kdb_opt
 
 pytestmark = pytest.mark.gpu
 GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
@@ -229,7 +230,7 @@ def test_random_graphs_filter(case, light, monkeypatch):
     """Light thresholds at several columns: the light MSF + filtered heavy MSF
     must equal Kruskal's MSF of the whole candidate graph on adversarial graphs
     (ties in random id order, asymmetric weights, padding, w = 0)."""
-    monkeypatch.setenv("KDB_LIGHT", light)
+    _kdb_opt("KDB_LIGHT", light)
     n, k, M, seed, levels, sym, pad, zero, local, q = case
     if int(light) >= k:
         pytest.skip("light column beyond k")
@@ -244,7 +245,7 @@ def test_random_graphs_filter(case, light, monkeypatch):
 @pytest.mark.parametrize("P", [0, 3])
 def test_c1_filter(c1_graph, light, exact, P, monkeypatch):
     import paper_2009_04552_b200 as kdb
-    monkeypatch.setenv("KDB_LIGHT", light)
+    _kdb_opt("KDB_LIGHT", light)
     X, nbr, dist = c1_graph
     eps = eps_from_graph(dist, 8, 1.5)
     got = run_gpu(nbr, dist, 8, eps, exact=exact, comm=kdb.Comm.sim(P) if P else None)
@@ -257,8 +258,8 @@ def test_c1_filter(c1_graph, light, exact, P, monkeypatch):
 def test_filter_overflow_falls_back(c1_graph, monkeypatch):
     """A survivor buffer too small for the crossing heavy entries: kdb_mst
     reruns plain rows-Boruvka and the result is still exact."""
-    monkeypatch.setenv("KDB_LIGHT", "2")
-    monkeypatch.setenv("KDB_SURVCAP", "0")
+    _kdb_opt("KDB_LIGHT", "2")
+    _kdb_opt("KDB_SURVCAP", "0")
     X, nbr, dist = c1_graph
     eps = eps_from_graph(dist, 8, 1.5)
     got = run_gpu(nbr, dist, 8, eps, exact=True)
@@ -267,7 +268,7 @@ def test_filter_overflow_falls_back(c1_graph, monkeypatch):
 
 
 def test_filter_off_matches(c1_graph, monkeypatch):
-    monkeypatch.setenv("KDB_FILTER", "0")
+    _kdb_opt("KDB_FILTER", "0")
     X, nbr, dist = c1_graph
     eps = eps_from_graph(dist, 8, 1.5)
     got = run_gpu(nbr, dist, 8, eps, exact=True)
@@ -277,7 +278,7 @@ def test_filter_off_matches(c1_graph, monkeypatch):
 
 @pytest.mark.parametrize("light", ["1", "3", "10"])
 def test_points_filter_exact_graphs(light, monkeypatch):
-    monkeypatch.setenv("KDB_LIGHT", light)
+    _kdb_opt("KDB_LIGHT", light)
     rng = np.random.default_rng(int(light))
     for t in range(3):
         n = int(rng.integers(200, 3000))
@@ -299,9 +300,9 @@ def test_points_filter_exact_graphs(light, monkeypatch):
 def test_inplace_rows_mode(case, filt, monkeypatch):
     """KDB_COMPACT=0: the rows phase reads the graph rows in place instead of
     the compact light lists (the path taken when the lists exceed capacity)."""
-    monkeypatch.setenv("KDB_COMPACT", "0")
-    monkeypatch.setenv("KDB_FILTER", filt)
-    monkeypatch.setenv("KDB_LIGHT", "2")
+    _kdb_opt("KDB_COMPACT", "0")
+    _kdb_opt("KDB_FILTER", filt)
+    _kdb_opt("KDB_LIGHT", "2")
     n, k, M, seed, levels, sym, pad, zero, local, q = case
     nbr, dist = random_graph(n, k, seed, levels=levels, symmetric=sym, pad_frac=pad, zero_frac=zero, local=local)
     eps = np.float32(np.quantile(dist[np.isfinite(dist)].astype(np.float64), q))
@@ -310,7 +311,7 @@ def test_inplace_rows_mode(case, filt, monkeypatch):
 
 @pytest.mark.parametrize("exact", [False, True])
 def test_c1_inplace_rows_mode(c1_graph, exact, monkeypatch):
-    monkeypatch.setenv("KDB_COMPACT", "0")
+    _kdb_opt("KDB_COMPACT", "0")
     X, nbr, dist = c1_graph
     eps = eps_from_graph(dist, 8, 1.5)
     for P in (0, 2):
@@ -325,8 +326,8 @@ def test_filter_fast_path_toggle(c1_graph, fast, light, monkeypatch):
     """The filter's shared-memory fast path (dominant component per id block +
     Bloom filter of the exceptions) must give the same survivors as the plain
     per-entry gather; shuffled ids (no block locality) exercise its slow path."""
-    monkeypatch.setenv("KDB_FASTFILTER", fast)
-    monkeypatch.setenv("KDB_LIGHT", light)
+    _kdb_opt("KDB_FASTFILTER", fast)
+    _kdb_opt("KDB_LIGHT", light)
     X, nbr, dist = c1_graph
     eps = eps_from_graph(dist, 8, 1.5)
     got = run_gpu(nbr, dist, 8, eps, exact=True)
@@ -382,8 +383,8 @@ def test_round1_fused_into_ell(c1_graph, fuse, pack, P, monkeypatch):
     round-1 hook reads one packed (K, B, kmin) record per component
     (KDB_PACK1=1, default) -- same forest."""
     import paper_2009_04552_b200 as kdb
-    monkeypatch.setenv("KDB_FUSE1", fuse)
-    monkeypatch.setenv("KDB_PACK1", pack)
+    _kdb_opt("KDB_FUSE1", fuse)
+    _kdb_opt("KDB_PACK1", pack)
     X, nbr, dist = c1_graph
     for M, f in ((8, 1.5), (3, 0.7), (12, 3.0)):
         eps = eps_from_graph(dist, M, f)
@@ -399,13 +400,13 @@ def test_round1_fused_into_ell(c1_graph, fuse, pack, P, monkeypatch):
 def test_sparse_ids_toggle(case, sparse, monkeypatch):
     """Late rounds keep root ids (no dense renumbering) -- same bits either way,
     general and exact mode, filtered and unfiltered."""
-    monkeypatch.setenv("KDB_SPARSE", sparse)
+    _kdb_opt("KDB_SPARSE", sparse)
     n, k, M, seed, levels, sym, pad, zero, local, q = case
     nbr, dist = random_graph(n, k, seed, levels=levels, symmetric=sym, pad_frac=pad, zero_frac=zero, local=local)
     eps = np.float32(np.quantile(dist[np.isfinite(dist)].astype(np.float64), q))
     exp = oracle_run(nbr, dist, M, eps)
     for filt in ("0", "1"):
-        monkeypatch.setenv("KDB_FILTER", filt)
+        _kdb_opt("KDB_FILTER", filt)
         assert_parity(run_gpu(nbr, dist, M, eps, exact=False), exp)
 
 
@@ -413,7 +414,7 @@ def test_sparse_ids_toggle(case, sparse, monkeypatch):
 @pytest.mark.parametrize("P", [0, 3])
 def test_c1_sparse_ids(c1_graph, sparse, P, monkeypatch):
     import paper_2009_04552_b200 as kdb
-    monkeypatch.setenv("KDB_SPARSE", sparse)
+    _kdb_opt("KDB_SPARSE", sparse)
     X, nbr, dist = c1_graph
     for exact in (False, True):
         for f in (1.0, 1.5, 3.0):
@@ -431,7 +432,7 @@ def test_nccl_communicator_one_rank(c1_graph, exact, monkeypatch):
     result."""
     import ctypes as C
     import paper_2009_04552_b200 as kdb
-    monkeypatch.setenv("KDB_NCCL_FORCE", "1")
+    _kdb_opt("KDB_NCCL_FORCE", "1")
     b = (C.c_ubyte * 128)()
     assert kdb.lib().kdb_nccl_unique_id(C.cast(b, C.c_void_p)) == 0
     h = C.c_void_p()
@@ -440,7 +441,7 @@ def test_nccl_communicator_one_rank(c1_graph, exact, monkeypatch):
     X, nbr, dist = c1_graph
     try:
         for light in ("2", "10"):
-            monkeypatch.setenv("KDB_LIGHT", light)
+            _kdb_opt("KDB_LIGHT", light)
             for f in (1.0, 1.5):
                 eps = eps_from_graph(dist, 8, f)
                 assert_parity(run_gpu(nbr, dist, 8, eps, exact=exact, comm=comm), oracle_run(nbr, dist, 8, eps))
@@ -471,13 +472,13 @@ def test_offer_precheck_toggle(case, pre, monkeypatch):
     """Offers read the current key before their atomicMin (KDB_PRECHECK forces
     it on / off; by default it switches on once live rows outnumber the
     components 8 to 1) -- the same forest either way, in every round kernel."""
-    monkeypatch.setenv("KDB_PRECHECK", pre)
+    _kdb_opt("KDB_PRECHECK", pre)
     n, k, M, seed, levels, sym, pad, zero, local, q = case
     nbr, dist = random_graph(n, k, seed, levels=levels, symmetric=sym, pad_frac=pad, zero_frac=zero, local=local)
     eps = np.float32(np.quantile(dist[np.isfinite(dist)].astype(np.float64), q))
     exp = oracle_run(nbr, dist, M, eps)
     for compact in ("0", "1"):
-        monkeypatch.setenv("KDB_COMPACT", compact)
+        _kdb_opt("KDB_COMPACT", compact)
         assert_parity(run_gpu(nbr, dist, M, eps, exact=False), exp)
 
 
@@ -507,13 +508,13 @@ def test_torus_ties_force_the_sweep_round(L, P):
 def test_pipelined_chunk_loads_toggle(case, pipe, monkeypatch):
     """scan_ell with the next ELL chunk's load issued ahead (KDB_PIPE forces it
     on / off; by default it follows the share of all-light ELL rows)."""
-    monkeypatch.setenv("KDB_PIPE", pipe)
+    _kdb_opt("KDB_PIPE", pipe)
     n, k, M, seed, levels, sym, pad, zero, local, q = case
     nbr, dist = random_graph(n, k, seed, levels=levels, symmetric=sym, pad_frac=pad, zero_frac=zero, local=local)
     eps = np.float32(np.quantile(dist[np.isfinite(dist)].astype(np.float64), q))
     exp = oracle_run(nbr, dist, M, eps)
     for light in ("2", "10"):
-        monkeypatch.setenv("KDB_LIGHT", light)
+        _kdb_opt("KDB_LIGHT", light)
         assert_parity(run_gpu(nbr, dist, M, eps, exact=False), exp)
 
 
@@ -550,7 +551,7 @@ def test_round2_head_skip_toggle(c1_graph, skip, P, monkeypatch):
     (KDB_SKIP1=1, default) or at it (0): the same forest either way, including
     ties (few weight levels) and the local-first phase under sim ranks."""
     import paper_2009_04552_b200 as kdb
-    monkeypatch.setenv("KDB_SKIP1", skip)
+    _kdb_opt("KDB_SKIP1", skip)
     X, nbr, dist = c1_graph
     for f in (0.7, 1.5):
         eps = eps_from_graph(dist, 8, f)

@@ -75,8 +75,8 @@ def case_c4slice():
 
 
 def case_fallback():
-    os.environ["KDB_SURVCAP"] = "0"
-    os.environ["KDB_LIGHT"] = "10"  # k = 16: the split runs only when asked for
+    kdb.set_option("KDB_SURVCAP", 0)
+    kdb.set_option("KDB_LIGHT", 10)  # k = 16: the split runs only when asked for
     nbr, dist, M, eps, _ = c1_graph()
     got = run_gpu(nbr, dist, M, eps, exact=True)
     assert got["stats"]["fallback"] == 1
