@@ -867,9 +867,22 @@ kdb_status rows_phase(Mst& m, float eps_run) {
           const bool pipe = pk >= 0 ? pk != 0
                                     : (rounds >= pr0 && rounds <= pr1) ||
                                           (uint64_t)R.n_deep * 100 > (uint64_t)R.n_rows * 15;
+          // the gather's view fixed at compile time when it is the plain one
+          // (no rank window, no global map): KDB_GM = 0 keeps the runtime view
+          const int gm = (!lv.bits && !lv.gmap && opt_int("KDB_GM", 1) != 0)
+                             ? ((l2hint & 2) ? (int)kGmL1 : (l2hint & 1) ? (int)kGmHint : (int)kGmRuntime)
+                             : (int)kGmRuntime;
+          const bool fast_scan = opt_int("KDB_FASTSCAN", 1) != 0;  // scan_ell_fast (straight-line selects)
           if (cas) {
-            if (pipe) KDB_LR_LAUNCH(4, true, true);
-            else if (lean) KDB_LR_LAUNCH(4, false, true, true);
+            if (pipe) {
+              if (gm == kGmL1) KDB_LR_LAUNCH(4, true, true, false, kGmL1);
+              else if (gm == kGmHint) KDB_LR_LAUNCH(4, true, true, false, kGmHint);
+              else KDB_LR_LAUNCH(4, true, true);
+            } else if (lean) KDB_LR_LAUNCH(4, false, true, true);
+            else if (gm == kGmL1 && fast_scan) KDB_LR_LAUNCH(4, false, true, false, kGmL1, true);
+            else if (gm == kGmHint && fast_scan) KDB_LR_LAUNCH(4, false, true, false, kGmHint, true);
+            else if (gm == kGmL1) KDB_LR_LAUNCH(4, false, true, false, kGmL1);
+            else if (gm == kGmHint) KDB_LR_LAUNCH(4, false, true, false, kGmHint);
             else KDB_LR_LAUNCH(4, false, true);
           } else if (gw == 1) KDB_LR_LAUNCH(1);
           else if (gw == 2) KDB_LR_LAUNCH(2);

@@ -263,6 +263,18 @@ __device__ __forceinline__ int32_t comp_of(const int32_t* __restrict__ comp, int
   if (lv.l1) return __ldg(comp + J);  // comp is read-only while a round runs (k_relabel writes it)
   return lv.pol ? gat_hint(comp + J, lv.pol) : gat(comp + J);
 }
+// The gather with its view fixed at compile time (the later light rounds of
+// the one-view case: no rank window, no global map -- ncu showed the runtime
+// dispatch above as ~20 of the ~80 instructions per scanned entry).
+// GM 0: runtime view (comp_of); 1: read-only path (L1); 2: L2 policy hint.
+enum { kGmRuntime = 0, kGmL1 = 1, kGmHint = 2 };
+template <int GM>
+__device__ __forceinline__ int32_t comp_of_m(const int32_t* __restrict__ comp, int64_t J, bool direct,
+                                             const LocalView& lv) {
+  if (GM == kGmL1) return __ldg(comp + J);
+  if (GM == kGmHint) return gat_hint(comp + J, lv.pol);
+  return comp_of(comp, J, direct, lv);
+}
 
 // Scan row (nr, dr) of vertex v (component cv) from head h.  direct: singleton
 // components (round 1, exact mode) -- every candidate leaves; with all_core the
@@ -631,7 +643,7 @@ __global__ void k_reuse_rows(const int4* __restrict__ LE, const uint32_t* __rest
 // GW: component gathers are issued GW entries at a time; once the minimum is
 // found only entries of its weight (decided from the loaded w) are gathered,
 // so a smaller GW trades memory-level parallelism for L2 sector traffic.
-template <bool DIRECT, int GW = 4, bool PIPE = false>
+template <bool DIRECT, int GW = 4, bool PIPE = false, int GM = kGmRuntime>
 __device__ __forceinline__ RowScan scan_ell(const int4* __restrict__ le, int64_t ps, const int32_t* __restrict__ nr,
                                             const float* __restrict__ dr, int k, float eps, int32_t v, int32_t cv,
                                             int h, int64_t N, const int32_t* __restrict__ comp, int all_core,
@@ -665,9 +677,10 @@ __device__ __forceinline__ RowScan scan_ell(const int4* __restrict__ le, int64_t
 #pragma unroll
     for (int j = g0; j < g0 + GW; ++j) {
       const int idx = c0 + j;
-      bool cand = idx >= h && idx < kend && w[j] <= eps && J[j] >= 0 && J[j] < N && J[j] != v;
+      // (uint32_t)J < N: J >= 0 and J < N in one compare (N < 2^31, kdb_mst's check)
+      bool cand = idx >= h && idx < kend && w[j] <= eps && (uint32_t)J[j] < (uint32_t)N && J[j] != v;
       if (GW < 4 && r.found && mono_bits(w[j]) != wstar) cand = false;  // past the tie group: no gather
-      cj[j] = cand ? comp_of(comp, J[j], DIRECT && all_core, lv) : -1;
+      cj[j] = cand ? comp_of_m<GM>(comp, J[j], DIRECT && all_core, lv) : -1;
     }
 #pragma unroll
     for (int j = g0; j < g0 + GW; ++j) {
@@ -710,7 +723,7 @@ __device__ __forceinline__ RowScan scan_ell(const int4* __restrict__ le, int64_t
       const int32_t Jc = __ldcg(nr + c);
       ++reads;
       if (Jc < 0 || Jc >= N || Jc == v) continue;
-      const int32_t cc = comp_of(comp, Jc, DIRECT && all_core, lv);
+      const int32_t cc = comp_of_m<GM>(comp, Jc, DIRECT && all_core, lv);
       if (cc < 0 || (!DIRECT && cc == cv)) continue;
       const uint64_t kk = pack_key(wstar, (uint32_t)min(v, Jc));
       const uint32_t bb = (uint32_t)max(v, Jc);
@@ -719,6 +732,87 @@ __device__ __forceinline__ RowScan scan_ell(const int4* __restrict__ le, int64_t
   }
   if (!r.found) r.h = k;
   return r;
+}
+
+// scan_ell<false, 4, false> for the later light rounds of the one-view case
+// (GM != kGmRuntime), as straight-line selects instead of the per-entry branch
+// ladder: ncu of round 3 (C4) showed ~80 warp instructions per scanned entry,
+// half of them the ladder's divergent paths at 13-18 active lanes.  Same
+// result: the first valid entry beyond eps ends a row with nothing found; dead
+// entries (not leaving) before the first leaving one are passed over; the
+// minimum is the first leaving entry and its tie group (equal weight bits)
+// competes by (key, b); the first other weight ends the scan.  Only a row's
+// final head matters here (r.h = the minimum's column, else k), so the dead
+// prefix is not tracked entry by entry.
+template <int GM>
+__device__ __forceinline__ RowScan scan_ell_fast(const int4* __restrict__ le, int64_t ps,
+                                                 const int32_t* __restrict__ nr, const float* __restrict__ dr, int k,
+                                                 float eps, int32_t v, int32_t cv, int h, int64_t N,
+                                                 const int32_t* __restrict__ comp, unsigned long long& reads,
+                                                 const LocalView lv) {
+  const int kend = min(k, kW);
+  const uint32_t n32 = (uint32_t)N;  // N < 2^31 (kdb_mst's check): J >= 0 && J < N in one compare
+  bool found = false, done = false;
+  uint32_t wstar = 0;
+  uint64_t best = kSent;
+  uint32_t bestb = kSentB;
+  int32_t bestc = -1;
+  int fh = k;
+  for (int c0 = h & ~3; c0 < kend; c0 += 4) {
+    int4 p0, p1;
+    ld256cs(le + (int64_t)(c0 >> 2) * ps, p0, p1);
+    const int32_t J[4] = {p0.x, p0.z, p1.x, p1.z};
+    const float w[4] = {__int_as_float(p0.y), __int_as_float(p0.w), __int_as_float(p1.y), __int_as_float(p1.w)};
+    reads += (unsigned long long)(min(c0 + 4, kend) - max(c0, h));
+    int32_t cj[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int idx = c0 + j;
+      const bool cand = idx >= h && idx < kend && w[j] <= eps && (uint32_t)J[j] < n32 && J[j] != v;
+      cj[j] = cand ? comp_of_m<GM>(comp, J[j], false, lv) : -1;
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int idx = c0 + j;
+      const bool valid = idx >= h && idx < kend && !done;
+      const bool in = w[j] <= eps;
+      const bool leave = cj[j] >= 0 && cj[j] != cv;
+      const uint32_t wb = mono_bits(w[j]);
+      const uint64_t key = pack_key(wb, (uint32_t)min(v, J[j]));
+      const uint32_t bb = (uint32_t)max(v, J[j]);
+      const bool first = valid && !found && in && leave;
+      const bool stop0 = valid && !found && !in;  // sorted: nothing left
+      const bool eq = wb == wstar;
+      const bool end = valid && found && !eq;     // past the minimum's tie group
+      const bool better = valid && found && eq && leave && (key < best || (key == best && bb < bestb));
+      const bool take = first || better;
+      best = take ? key : best;
+      bestb = take ? bb : bestb;
+      bestc = take ? cj[j] : bestc;
+      fh = first ? idx : fh;
+      wstar = first ? wb : wstar;
+      found = found || first;
+      done = done || stop0 || end;
+    }
+    if (done) break;
+  }
+  if (!done && k > kW) {
+    // the candidate prefix (or the minimum's tie group) runs past the ELL (rare)
+    if (!found) return scan_row<false, false>(nr, dr, k, eps, v, cv, max(h, kW), N, comp, 0, reads, lv);
+    for (int c = kW; c < k; ++c) {  // continue the tie group of weight wstar in the graph row
+      const float wc = __ldcg(dr + c);
+      if (mono_bits(wc) != wstar || !(wc <= eps)) break;
+      const int32_t Jc = __ldcg(nr + c);
+      ++reads;
+      if (Jc < 0 || Jc >= N || Jc == v) continue;
+      const int32_t cc = comp_of_m<GM>(comp, Jc, false, lv);
+      if (cc < 0 || cc == cv) continue;
+      const uint64_t kk = pack_key(wstar, (uint32_t)min(v, Jc));
+      const uint32_t bb = (uint32_t)max(v, Jc);
+      if (kk < best || (kk == best && bb < bestb)) { best = kk; bestb = bb; bestc = cc; }
+    }
+  }
+  return RowScan{found, found ? fh : k, best, bestb, bestc, -1};
 }
 
 // scan_ell for the later light rounds (not DIRECT, all four gathers of a
@@ -892,7 +986,7 @@ __global__ void __launch_bounds__(256) k_light_first(const int4* __restrict__ LE
 
 // later rounds over the ELL; see k_offer_round.  CAS (one rank): the offer is
 // a 128-bit CAS-minimum of (key, b) into KB[comp v] -- no offer list, no tie pass.
-template <int GW, bool PIPE = false, bool CAS = false, bool LEAN = false>
+template <int GW, bool PIPE = false, bool CAS = false, bool LEAN = false, int GM = kGmRuntime, bool FAST = false>
 __global__ void __launch_bounds__(256) k_light_round(const int4* __restrict__ LE, int64_t ell_rows,
                                                      const int32_t* __restrict__ nbr,
                                                      const float* __restrict__ dist, int32_t ld, int32_t k, float eps,
@@ -946,10 +1040,13 @@ __global__ void __launch_bounds__(256) k_light_round(const int4* __restrict__ LE
         park[base + __popc(am & ((1u << lane) - 1u))] = Rec{v, a.y};
       } else {
       const int64_t i = (int64_t)v - row_begin;
-      const RowScan r = (LEAN && GW == 4 && !PIPE)
+      const RowScan r = (FAST && GM != kGmRuntime && GW == 4 && !PIPE)
+          ? scan_ell_fast<GM>(LE + ell_row(i), ell_ps(ell_rows), nbr + i * ld, dist + i * ld, k, eps, v, cv, a.y, N,
+                              comp, reads, lvh)
+          : (LEAN && GW == 4 && !PIPE)
           ? scan_ell_lean(LE + ell_row(i), ell_ps(ell_rows), nbr + i * ld, dist + i * ld, k, eps, v, cv, a.y, N, comp,
                           reads, lvh)
-          : scan_ell<false, GW, PIPE>(LE + ell_row(i), ell_ps(ell_rows), nbr + i * ld, dist + i * ld, k, eps, v, cv, a.y,
+          : scan_ell<false, GW, PIPE, GM>(LE + ell_row(i), ell_ps(ell_rows), nbr + i * ld, dist + i * ld, k, eps, v, cv, a.y,
                                                   N, comp, 0, reads, lvh);
       if (r.found) {
         const uint32_t j = atomicAdd(&s_n, 1u);
