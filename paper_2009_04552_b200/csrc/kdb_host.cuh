@@ -872,8 +872,19 @@ kdb_status rows_phase(Mst& m, float eps_run) {
           const int gm = (!lv.bits && !lv.gmap && opt_int("KDB_GM", 1) != 0)
                              ? ((l2hint & 2) ? (int)kGmL1 : (l2hint & 1) ? (int)kGmHint : (int)kGmRuntime)
                              : (int)kGmRuntime;
-          const bool fast_scan = opt_int("KDB_FASTSCAN", 1) != 0;  // scan_ell_fast (straight-line selects)
-          if (cas) {
+          const bool fast_scan = opt_int("KDB_FASTSCAN", 0) != 0;  // scan_ell_fast: measured slower (10.65 vs 10.16 ms), off
+          // lane refill (k_light_refill): the one-view CAS case without pipelined
+          // loads; parity-green but measured 2.7x slower (C4: 27.6 vs 10.2 ms), off
+          const bool refill = cas && !pipe && !lean && gm != kGmRuntime && !frz && opt_int("KDB_REFILL", 0) != 0;
+          if (refill) {
+#define KDB_RF_LAUNCH(G)                                                                                          \
+  LAUNCH(k_light_refill<G>, grid_for(na_ub[r]), kThreads, st, R.LE, R.n_rows, R.nbr, R.dist, ld, k, eps_run,         \
+         R.row_begin, N, comp, R.act[cur], na_ub[r], R.act[cur ^ 1], nout, &R.ctr->grab, KB, &L.ctr->entries, nin, \
+         l2hint)
+            if (gm == kGmL1) KDB_RF_LAUNCH(kGmL1);
+            else KDB_RF_LAUNCH(kGmHint);
+#undef KDB_RF_LAUNCH
+          } else if (cas) {
             if (pipe) {
               if (gm == kGmL1) KDB_LR_LAUNCH(4, true, true, false, kGmL1);
               else if (gm == kGmHint) KDB_LR_LAUNCH(4, true, true, false, kGmHint);

@@ -1082,6 +1082,171 @@ __global__ void __launch_bounds__(256) k_light_round(const int4* __restrict__ LE
   if ((threadIdx.x & 31) == 0 && reads) atomicAdd(n_entries, reads);
 }
 
+// Later light rounds, one view, CAS offers (the single-rank default), with
+// LANE REFILL: a lane whose row is finished takes the warp's next record at
+// once, so every warp step scans one 4-entry chunk of some row on (nearly)
+// every lane.  k_light_round runs a warp until its LONGEST row is done: ncu of
+// round 3 (C4) showed 3.45 chunk steps per warp for 1.6 chunks per row, at
+// 13-18 active lanes, and the chunk loop as 86% of the kernel's instructions.
+// Same scan (scan_ell's entry ladder, GW = 4), same offers (the CAS-minimum of
+// (key, (b, target component)) into KB[cv]) and the same next row list up to
+// order; no shared memory, no block barriers: a warp grabs kRefillChunk
+// records at a time from the round's cursor (records stay roughly in order,
+// so the component gathers keep their L2 locality) and reserves its output
+// slots with one atomic per step that finishes rows.
+constexpr int kRefillChunk = 512;
+#ifndef KDB_REFILL_MINB
+#define KDB_REFILL_MINB 5  // blocks per SM (<= 48 registers: 40 warps, as k_light_round)
+#endif
+template <int GM>
+__global__ void __launch_bounds__(256, KDB_REFILL_MINB) k_light_refill(const int4* __restrict__ LE, int64_t ell_rows,
+                                                      const int32_t* __restrict__ nbr, const float* __restrict__ dist,
+                                                      int32_t ld, int32_t k, float eps, int64_t row_begin, int64_t N,
+                                                      const int32_t* __restrict__ comp, const Rec* __restrict__ act,
+                                                      uint32_t n_in, Rec* __restrict__ act_out,
+                                                      uint32_t* __restrict__ n_out, uint32_t* __restrict__ grab,
+                                                      ulonglong2* __restrict__ KB,
+                                                      unsigned long long* __restrict__ n_entries,
+                                                      const uint32_t* __restrict__ n_in_p, int l2hint) {
+  if (n_in_p) n_in = *n_in_p;
+  LocalView lvh{};
+  if (l2hint & 1) lvh.pol = l2_evict_last_policy();
+  lvh.l1 = (l2hint >> 1) & 1;
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  const int kend = min(k, kW);
+  const int64_t ps = ell_ps(ell_rows);
+  unsigned long long reads = 0;
+  // warp queue [qpos, qend) of records (warp-uniform)
+  uint32_t qpos = 0, qend = 0;
+  bool exhausted = false;
+  // this lane's row
+  bool have = false, found = false, done = false;
+  int32_t v = 0, cv = 0, bestc = -1;
+  int h = 0, c0 = 0, fh = 0;
+  uint32_t wstar = 0, bestb = kSentB;
+  uint64_t best = kSent;
+  for (;;) {
+    // ---- refill: lanes without a row take the next records, in lane order
+    unsigned need = __ballot_sync(0xffffffffu, !have);
+    while (need && !exhausted) {
+      if (qpos >= qend) {
+        uint32_t c = 0;
+        if (lane == 0) c = atomicAdd(grab, 1u);
+        c = __shfl_sync(0xffffffffu, c, 0);
+        const uint64_t b0 = (uint64_t)c * kRefillChunk;
+        if (b0 >= n_in) { exhausted = true; break; }
+        qpos = (uint32_t)b0;
+        qend = (uint32_t)(b0 + kRefillChunk < (uint64_t)n_in ? b0 + kRefillChunk : (uint64_t)n_in);
+      }
+      const uint32_t avail = qend - qpos;
+      const uint32_t rk = __popc(need & lt);
+      if (!have && rk < avail) {
+        const int2 a = __ldcs(reinterpret_cast<const int2*>(act + qpos + rk));
+        v = a.x;
+        h = a.y;
+        cv = lvh.l1 ? __ldg(comp + v) : gat(comp + v);
+        KDB_DCHECK(cv >= 0 && v >= row_begin && v < N, 8u);  // a live row is a local core vertex
+        c0 = h & ~3;
+        found = false;
+        done = false;
+        best = kSent;
+        bestb = kSentB;
+        bestc = -1;
+        fh = k;
+        have = true;
+      }
+      qpos += min((uint32_t)__popc(need), avail);
+      need = __ballot_sync(0xffffffffu, !have);
+    }
+    if (__ballot_sync(0xffffffffu, have) == 0) break;
+    // ---- one chunk step of this lane's row (scan_ell's ladder)
+    bool fin = false;
+    if (have) {
+      const int64_t i = (int64_t)v - row_begin;
+      if (c0 < kend) {
+        int4 p0, p1;
+        ld256cs(LE + ell_row(i) + (int64_t)(c0 >> 2) * ps, p0, p1);
+        const int32_t J[4] = {p0.x, p0.z, p1.x, p1.z};
+        const float w[4] = {__int_as_float(p0.y), __int_as_float(p0.w), __int_as_float(p1.y), __int_as_float(p1.w)};
+        reads += (unsigned long long)(min(c0 + 4, kend) - max(c0, h));
+        int32_t cj[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int idx = c0 + j;
+          const bool cand = idx >= h && idx < kend && w[j] <= eps && (uint32_t)J[j] < (uint32_t)N && J[j] != v;
+          cj[j] = cand ? comp_of_m<GM>(comp, J[j], false, lvh) : -1;
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int idx = c0 + j;
+          if (done || idx < h || idx >= kend) continue;
+          const bool leaving = cj[j] >= 0 && cj[j] != cv;
+          const uint32_t wb = mono_bits(w[j]);
+          if (!found) {
+            if (!(w[j] <= eps)) { done = true; continue; }  // sorted: nothing left
+            if (!leaving) { h = idx + 1; continue; }          // dead entry
+            found = true;
+            fh = idx;
+            wstar = wb;
+            best = pack_key(wb, (uint32_t)min(v, J[j]));
+            bestb = (uint32_t)max(v, J[j]);
+            bestc = cj[j];
+          } else {
+            if (wb != wstar) { done = true; continue; }
+            if (!leaving) continue;
+            const uint64_t kk = pack_key(wb, (uint32_t)min(v, J[j]));
+            const uint32_t bb = (uint32_t)max(v, J[j]);
+            if (kk < best || (kk == best && bb < bestb)) { best = kk; bestb = bb; bestc = cj[j]; }
+          }
+        }
+        c0 += 4;
+      }
+      fin = done || c0 >= kend;
+      if (fin && !done && k > kW) {
+        // the candidate prefix (or the minimum's tie group) runs past the ELL (rare)
+        if (!found) {
+          const RowScan t = scan_row<false, false>(nbr + i * ld, dist + i * ld, k, eps, v, cv, max(h, kW), N, comp,
+                                                   0, reads, lvh);
+          found = t.found;
+          fh = t.h;
+          best = t.best;
+          bestb = t.bestb;
+          bestc = t.bestc;
+        } else {
+          const int32_t* nr = nbr + i * ld;
+          const float* dr = dist + i * ld;
+          for (int c = kW; c < k; ++c) {  // continue the tie group of weight wstar in the graph row
+            const float wc = __ldcg(dr + c);
+            if (mono_bits(wc) != wstar || !(wc <= eps)) break;
+            const int32_t Jc = __ldcg(nr + c);
+            ++reads;
+            if (Jc < 0 || Jc >= N || Jc == v) continue;
+            const int32_t cc = comp_of_m<GM>(comp, Jc, false, lvh);
+            if (cc < 0 || cc == cv) continue;
+            const uint64_t kk = pack_key(wstar, (uint32_t)min(v, Jc));
+            const uint32_t bb = (uint32_t)max(v, Jc);
+            if (kk < best || (kk == best && bb < bestb)) { best = kk; bestb = bb; bestc = cc; }
+          }
+        }
+      }
+      if (fin && found) min_pair128(KB + cv, best, ((uint64_t)bestb << 32) | (uint32_t)bestc);
+    }
+    // ---- finished rows that found an edge stay live (head = the minimum's column)
+    const unsigned out = __ballot_sync(0xffffffffu, fin && found);
+    if (out) {
+      uint32_t base = 0;
+      const int leader = __ffs(out) - 1;
+      if (lane == leader) base = atomicAdd(n_out, (uint32_t)__popc(out));
+      base = __shfl_sync(0xffffffffu, base, leader);
+      if (fin && found) __stcs(reinterpret_cast<int2*>(act_out + base + __popc(out & lt)), make_int2(v, fh));
+    }
+    if (fin) have = false;
+  }
+  for (int o = 16; o > 0; o >>= 1) reads += __shfl_xor_sync(0xffffffffu, reads, o);
+  if (lane == 0 && reads) atomicAdd(n_entries, reads);
+}
+
 // in-edge lists: scan the live in-entries of target t, drop intra entries
 // (swap-remove; they never revive), offer the minimum leaving one.
 __global__ void k_offer_in(const unsigned long long* __restrict__ in_off, int32_t* __restrict__ in_len,
