@@ -1126,6 +1126,8 @@ __global__ void __launch_bounds__(256, KDB_REFILL_MINB) k_light_refill(const int
   int h = 0, c0 = 0, fh = 0;
   uint32_t wstar = 0, bestb = kSentB;
   uint64_t best = kSent;
+  int32_t pc = -1;  // pending offer (component, key, (b, target)) of this lane
+  uint64_t pk = kSent, pb = ~0ull;
   for (;;) {
     // ---- refill: lanes without a row take the next records, in lane order
     unsigned need = __ballot_sync(0xffffffffu, !have);
@@ -1230,7 +1232,20 @@ __global__ void __launch_bounds__(256, KDB_REFILL_MINB) k_light_refill(const int
           }
         }
       }
-      if (fin && found) min_pair128(KB + cv, best, ((uint64_t)bestb << 32) | (uint32_t)bestc);
+      if (fin && found) {
+        // lane-local combine: a lane's successive rows come from nearby records
+        // (in later rounds mostly one component); same-address CAS loops from
+        // many lanes serialise at the L2 slice, so one CAS per run of rows
+        const uint64_t ob = ((uint64_t)bestb << 32) | (uint32_t)bestc;
+        if (pc == cv) {
+          if (best < pk || (best == pk && ob < pb)) { pk = best; pb = ob; }
+        } else {
+          if (pc >= 0) min_pair128(KB + pc, pk, pb);
+          pc = cv;
+          pk = best;
+          pb = ob;
+        }
+      }
     }
     // ---- finished rows that found an edge stay live (head = the minimum's column)
     const unsigned out = __ballot_sync(0xffffffffu, fin && found);
@@ -1243,6 +1258,7 @@ __global__ void __launch_bounds__(256, KDB_REFILL_MINB) k_light_refill(const int
     }
     if (fin) have = false;
   }
+  if (pc >= 0) min_pair128(KB + pc, pk, pb);
   for (int o = 16; o > 0; o >>= 1) reads += __shfl_xor_sync(0xffffffffu, reads, o);
   if (lane == 0 && reads) atomicAdd(n_entries, reads);
 }
