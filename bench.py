@@ -588,7 +588,7 @@ def algo_bytes_per_launch(name, N, k, world, launches_per_step, stats):
         return n_local * (8.0 * KW + 4.0)               # the first kW entries + D[v][k-1] per row
     if bn == "k_filter":
         return n_local * (4.0 * k + 2.0)                # every id (weights only where needed) + row metadata
-    if bn in ("k_light_round", "k_light_refill", "k_light_first", "k_offer_round", "k_offer_first"):
+    if bn in ("k_light_round", "k_light_quad", "k_light_refill", "k_light_first", "k_offer_round", "k_offer_first"):
         er = mean("entries_read")                       # (J, w) entries scanned, all rounds
         rounds = mean("rounds")
         return 8.0 * er / rounds if er and rounds else None

@@ -1263,6 +1263,161 @@ __global__ void __launch_bounds__(256, KDB_REFILL_MINB) k_light_refill(const int
   if (lane == 0 && reads) atomicAdd(n_entries, reads);
 }
 
+// Later light rounds, one view, CAS offers, QUAD PER ROW: the four lanes of a
+// quad take the four entries of a chunk, so the entry ladder of scan_ell
+// becomes four-lane ballots (the first valid entry that is beyond eps or
+// leaving, the minimum's tie group = the valid entries of equal weight bits up
+// to the first other weight) and a two-step quad minimum over (key, b).  The
+// row state is quad-uniform; a warp runs 8 rows at a time, so its chunk loop
+// waits for the longest of 8 rows, not of 32 (ncu of k_light_round, round 3 of
+// C4: 3.45 chunk steps per warp for 1.6 per row, 13-18 active lanes, ~80
+// instructions per scanned entry).  Same offers (the CAS-minimum of (key,
+// (b, target component)) into KB[cv], min-reduced over runs of lanes with one
+// component first) and the same next row list as k_light_round.
+#ifndef KDB_QUAD_MINB
+#define KDB_QUAD_MINB 5  // blocks per SM (<= 48 registers: 40 warps, as k_light_round)
+#endif
+template <int GM>
+__global__ void __launch_bounds__(256, KDB_QUAD_MINB) k_light_quad(const int4* __restrict__ LE, int64_t ell_rows,
+                                                    const int32_t* __restrict__ nbr, const float* __restrict__ dist,
+                                                    int32_t ld, int32_t k, float eps, int64_t row_begin, int64_t N,
+                                                    const int32_t* __restrict__ comp, const Rec* __restrict__ act,
+                                                    uint32_t n_in, Rec* __restrict__ act_out,
+                                                    uint32_t* __restrict__ n_out, uint32_t* __restrict__ grab,
+                                                    ulonglong2* __restrict__ KB,
+                                                    unsigned long long* __restrict__ n_entries,
+                                                    const uint32_t* __restrict__ n_in_p, int l2hint, int chunk) {
+  if (n_in_p) n_in = *n_in_p;
+  LocalView lvh{};
+  if (l2hint & 1) lvh.pol = l2_evict_last_policy();
+  lvh.l1 = (l2hint >> 1) & 1;
+  __shared__ __align__(16) Rec s_rec[kChunk];
+  __shared__ uint32_t s_n, s_chunk, s_base;
+  const int lane = threadIdx.x & 31, ql = lane & 3, qb = lane & ~3;
+  const unsigned qmask = 0xFu << qb;
+  const int kend = min(k, kW);
+  const int64_t ps2 = 2 * ell_ps(ell_rows);  // chunk stride in int2 units
+  const uint32_t n32 = (uint32_t)N;           // N < 2^31 (kdb_mst's check)
+  unsigned long long reads = 0;
+  for (;;) {
+    if (threadIdx.x == 0) { s_chunk = atomicAdd(grab, 1u); s_n = 0; }
+    __syncthreads();
+    const uint64_t base = (uint64_t)s_chunk * chunk;
+    if (base >= n_in) break;
+    for (int t = 0; t < chunk; t += 64) {
+      const uint64_t s = base + t + (threadIdx.x >> 2);
+      bool have = false;
+      int32_t cseg = -1 - lane;
+      uint64_t okey = ~0ull, ob = ~0ull;
+      if (s < n_in) {  // quad-uniform from here on
+        const int2 a = __ldcs(reinterpret_cast<const int2*>(act + s));
+        const int32_t v = a.x;
+        const int h = a.y;
+        const int32_t cv = lvh.l1 ? __ldg(comp + v) : gat(comp + v);
+        KDB_DCHECK(cv >= 0 && v >= row_begin && v < N, 8u);  // a live row is a local core vertex
+        const int64_t i = (int64_t)v - row_begin;
+        const int2* le = reinterpret_cast<const int2*>(LE + ell_row(i)) + ql;
+        bool found = false, done = false;
+        uint32_t wstar = 0, bestb = kSentB;
+        uint64_t best = kSent;
+        int32_t bestc = -1;
+        int fh = k;
+        for (int c0 = h & ~3; c0 < kend; c0 += 4) {
+          const int2 e = __ldcs(le + (int64_t)(c0 >> 2) * ps2);
+          const int idx = c0 + ql;
+          const int32_t J = e.x;
+          const float w = __int_as_float(e.y);
+          const bool valid = idx >= h && idx < kend;
+          const bool in = w <= eps;
+          const bool cand = valid && in && (uint32_t)J < n32 && J != v;
+          const int32_t cj = cand ? comp_of_m<GM>(comp, J, false, lvh) : -1;
+          const bool leave = cj >= 0 && cj != cv;
+          const uint32_t wb = mono_bits(w);
+          if (ql == 0) reads += (unsigned long long)(min(c0 + 4, kend) - max(c0, h));
+          const unsigned bv = (__ballot_sync(qmask, valid) >> qb) & 0xFu;
+          const unsigned bi = (__ballot_sync(qmask, in) >> qb) & 0xFu;
+          const unsigned bl = (__ballot_sync(qmask, leave) >> qb) & 0xFu;
+          int from = 0;
+          if (!found) {
+            const unsigned stop = bv & (~bi | bl);
+            if (stop == 0) continue;  // every valid entry of the chunk is dead
+            const int f = __ffs(stop) - 1;
+            if (!((bi >> f) & 1u)) { done = true; break; }  // sorted: nothing left
+            found = true;
+            fh = c0 + f;
+            wstar = __shfl_sync(qmask, wb, qb + f);
+            from = f;
+          }
+          // the minimum's tie group in this chunk: valid positions >= from of
+          // weight wstar, up to the first other weight
+          const unsigned beq = (__ballot_sync(qmask, wb == wstar) >> qb) & 0xFu;
+          const unsigned at = (0xFu << from) & 0xFu;
+          const unsigned differ = bv & ~beq & at;
+          const unsigned before = differ ? ((1u << (__ffs(differ) - 1)) - 1u) : 0xFu;
+          const bool mine = ((bv & beq & bl & at & before) >> ql) & 1u;
+          uint64_t kk = mine ? pack_key(wb, (uint32_t)min(v, J)) : kSent;
+          uint32_t bb = mine ? (uint32_t)max(v, J) : kSentB;
+          int32_t cc = cj;
+#pragma unroll
+          for (int o = 1; o < 4; o <<= 1) {
+            const uint64_t ok = __shfl_xor_sync(qmask, kk, o);
+            const uint32_t obb = __shfl_xor_sync(qmask, bb, o);
+            const int32_t oc = __shfl_xor_sync(qmask, cc, o);
+            if (ok < kk || (ok == kk && obb < bb)) { kk = ok; bb = obb; cc = oc; }
+          }
+          if (kk < best || (kk == best && bb < bestb)) { best = kk; bestb = bb; bestc = cc; }
+          if (differ) { done = true; break; }
+        }
+        if (!done && k > kW) {
+          // the candidate prefix (or the minimum's tie group) runs past the ELL
+          // (rare): every lane of the quad runs the same scan
+          const int32_t* nr = nbr + i * ld;
+          const float* dr = dist + i * ld;
+          if (!found) {
+            unsigned long long tr = 0;  // entries read, counted once per quad
+            const RowScan r2 = scan_row<false, false>(nr, dr, k, eps, v, cv, max(h, kW), N, comp, 0, tr, lvh);
+            if (ql == 0) reads += tr;
+            found = r2.found;
+            fh = r2.h;
+            best = r2.best;
+            bestb = r2.bestb;
+            bestc = r2.bestc;
+          } else {
+            for (int c = kW; c < k; ++c) {  // continue the tie group of weight wstar in the graph row
+              const float wc = __ldcg(dr + c);
+              if (mono_bits(wc) != wstar || !(wc <= eps)) break;
+              const int32_t Jc = __ldcg(nr + c);
+              if (ql == 0) ++reads;
+              if (Jc < 0 || Jc >= N || Jc == v) continue;
+              const int32_t cc2 = comp_of_m<GM>(comp, Jc, false, lvh);
+              if (cc2 < 0 || cc2 == cv) continue;
+              const uint64_t kk2 = pack_key(wstar, (uint32_t)min(v, Jc));
+              const uint32_t bb2 = (uint32_t)max(v, Jc);
+              if (kk2 < best || (kk2 == best && bb2 < bestb)) { best = kk2; bestb = bb2; bestc = cc2; }
+            }
+          }
+        }
+        if (found) {
+          if (ql == 0) s_rec[atomicAdd(&s_n, 1u)] = Rec{v, fh};
+          have = true;  // all four lanes: runs of lanes with one component reduce before the CAS
+          cseg = cv;
+          okey = best;
+          ob = ((uint64_t)bestb << 32) | (uint32_t)bestc;
+        }
+      }
+      warp_min_pair128(KB, have, cseg, okey, ob);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) s_base = s_n ? atomicAdd(n_out, s_n) : 0u;
+    __syncthreads();
+    for (uint32_t j = threadIdx.x; j < s_n; j += blockDim.x)
+      __stcs(reinterpret_cast<int2*>(act_out + s_base + j), *reinterpret_cast<const int2*>(s_rec + j));
+    __syncthreads();
+  }
+  for (int o = 16; o > 0; o >>= 1) reads += __shfl_xor_sync(0xffffffffu, reads, o);
+  if ((threadIdx.x & 31) == 0 && reads) atomicAdd(n_entries, reads);
+}
+
 // in-edge lists: scan the live in-entries of target t, drop intra entries
 // (swap-remove; they never revive), offer the minimum leaving one.
 __global__ void k_offer_in(const unsigned long long* __restrict__ in_off, int32_t* __restrict__ in_len,
