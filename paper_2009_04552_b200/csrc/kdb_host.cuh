@@ -876,8 +876,9 @@ kdb_status rows_phase(Mst& m, float eps_run) {
           // lane refill (k_light_refill): the one-view CAS case without pipelined
           // loads; parity-green but measured 2.7x slower (C4: 27.6 vs 10.2 ms), off
           const bool refill = cas && !pipe && !lean && gm != kGmRuntime && !frz && opt_int("KDB_REFILL", 0) != 0;
-          // quad per row (k_light_quad): the same one-view CAS case
-          const bool quad = !refill && cas && !pipe && !lean && gm != kGmRuntime && !frz && opt_int("KDB_QUAD", 1) != 0;
+          // quad per row (k_light_quad): the same one-view CAS case; parity-green but
+          // measured 3.5x slower (C4: 35.4 vs 10.2 ms of light rounds, same box), off
+          const bool quad = !refill && cas && !pipe && !lean && gm != kGmRuntime && !frz && opt_int("KDB_QUAD", 0) != 0;
           if (quad) {
             if (gm == kGmL1)
               LAUNCH(k_light_quad<kGmL1>, grid_for(na_ub[r]), kThreads, st, R.LE, R.n_rows, R.nbr, R.dist, ld, k,

@@ -295,6 +295,24 @@ def test_points_filter_exact_graphs(light, monkeypatch):
             assert_parity(run_gpu(nbr, dist, M, eps, exact=False, comm=comm), exp)
 
 
+@pytest.mark.parametrize("knob", ["KDB_QUAD", "KDB_REFILL", "KDB_LEAN", "KDB_FASTSCAN", "KDB_TILE"])
+def test_light_round_variants_kept_off(knob, monkeypatch):
+    """The light-round variants that were measured slower and are off by default
+    (DESIGN.md section 16 and its options table) stay parity-green: exact kNN graphs
+    of clustered point sets with duplicates, one rank, light split forced."""
+    _kdb_opt(knob, "1")
+    _kdb_opt("KDB_LIGHT", "6")
+    rng = np.random.default_rng(len(knob))
+    for t in range(3):
+        n = int(rng.integers(3000, 40000))
+        X = (rng.standard_normal((n, 3)) * rng.uniform(0.1, 1.0)).astype(np.float32)
+        X[rng.integers(0, n, n // 20)] = X[rng.integers(0, n, n // 20)]
+        k = int(rng.integers(12, 24)); M = int(rng.integers(1, k + 1))
+        nbr, dist = knn_bruteforce(X, k)
+        eps = eps_from_graph(dist, M, float(rng.uniform(0.8, 3.0)))
+        assert_parity(run_gpu(nbr, dist, M, eps, exact=True), oracle_run(nbr, dist, M, eps))
+
+
 @pytest.mark.parametrize("filt", ["0", "1"])
 @pytest.mark.parametrize("case", RANDOM_CASES)
 def test_inplace_rows_mode(case, filt, monkeypatch):
