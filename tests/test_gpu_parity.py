@@ -295,22 +295,38 @@ def test_points_filter_exact_graphs(light, monkeypatch):
             assert_parity(run_gpu(nbr, dist, M, eps, exact=False, comm=comm), exp)
 
 
+@pytest.fixture(scope="module")
+def c4_small_graph():
+    """The C4 recipe at 128K points (10 spheres, exact grid kNN graph k = 100) and
+    the oracle's result at the config's eps rule."""
+    from datagen import CONFIGS, gen_config_points
+    from paper_2009_04552_b200.knng import build_knng_grid
+    X, _ = gen_config_points("C4", 0, 0.002)
+    nbr_t, dist_t, _ = build_knng_grid(X, 100, device="cuda")
+    nbr, dist = nbr_t.cpu().numpy(), dist_t.cpu().numpy()
+    eps = float(np.float32(CONFIGS["C4"]["eps_factor"] * float(np.median(dist[:, 49].astype(np.float64)))))
+    return nbr, dist, eps, oracle_run(nbr, dist, 50, eps)
+
+
 @pytest.mark.parametrize("knob", ["KDB_QUAD", "KDB_REFILL", "KDB_LEAN", "KDB_FASTSCAN", "KDB_TILE"])
-def test_light_round_variants_kept_off(knob, monkeypatch):
+def test_light_round_variants_kept_off(knob, c4_small_graph, monkeypatch):
     """The light-round variants that were measured slower and are off by default
-    (DESIGN.md section 16 and its options table) stay parity-green: exact kNN graphs
-    of clustered point sets with duplicates, one rank, light split forced."""
+    (DESIGN.md section 16 and its options table) stay parity-green on the path the
+    bench runs (one rank, exact graph, light split): the C4 recipe at 128K points,
+    and small clustered point sets with duplicate points (ties, w = 0)."""
     _kdb_opt(knob, "1")
+    nbr, dist, eps, exp = c4_small_graph
+    assert_parity(run_gpu(nbr, dist, 50, eps, exact=True), exp)
     _kdb_opt("KDB_LIGHT", "6")
     rng = np.random.default_rng(len(knob))
     for t in range(3):
-        n = int(rng.integers(3000, 40000))
+        n = int(rng.integers(1000, 5000))
         X = (rng.standard_normal((n, 3)) * rng.uniform(0.1, 1.0)).astype(np.float32)
         X[rng.integers(0, n, n // 20)] = X[rng.integers(0, n, n // 20)]
         k = int(rng.integers(12, 24)); M = int(rng.integers(1, k + 1))
-        nbr, dist = knn_bruteforce(X, k)
-        eps = eps_from_graph(dist, M, float(rng.uniform(0.8, 3.0)))
-        assert_parity(run_gpu(nbr, dist, M, eps, exact=True), oracle_run(nbr, dist, M, eps))
+        nbr2, dist2 = knn_bruteforce(X, k)
+        eps2 = eps_from_graph(dist2, M, float(rng.uniform(0.8, 3.0)))
+        assert_parity(run_gpu(nbr2, dist2, M, eps2, exact=True), oracle_run(nbr2, dist2, M, eps2))
 
 
 @pytest.mark.parametrize("filt", ["0", "1"])
