@@ -204,7 +204,7 @@ Prof g_prof;
 // ============================================================================
 const char* const kOptNames[] = {
     "KDB_CAS",      "KDB_COMPACT", "KDB_FASTFILTER", "KDB_FASTSCAN", "KDB_FILTER",  "KDB_FUSE1",   "KDB_GM",  "KDB_GMAP",      "KDB_GW",
-    "KDB_L1GAT",    "KDB_L2HINT",  "KDB_LEAN",       "KDB_LIGHT",   "KDB_LOCAL",   "KDB_MSF_COUNT", "KDB_NCCL_FORCE",
+    "KDB_L1GAT",    "KDB_L2HINT",  "KDB_LEAN",       "KDB_LIGHT",   "KDB_LOCAL",   "KDB_LVL",  "KDB_MSF_COUNT", "KDB_NCCL_FORCE",
     "KDB_PACK1",    "KDB_PIPE",    "KDB_PIPE_R0",    "KDB_PIPE_R1", "KDB_PRECHECK", "KDB_QUAD", "KDB_REFILL", "KDB_REUSE",    "KDB_SKIP1",
     "KDB_SPARSE",   "KDB_SURVCAP", "KDB_TILE",       "KDB_TILE_MAXR", "KDB_TILE_ROWS", "KDB_TRACE"};
 constexpr int kNumOpts = (int)(sizeof(kOptNames) / sizeof(kOptNames[0]));

@@ -879,7 +879,18 @@ kdb_status rows_phase(Mst& m, float eps_run) {
           // quad per row (k_light_quad): the same one-view CAS case; parity-green but
           // measured 3.5x slower (C4: 35.4 vs 10.2 ms of light rounds, same box), off
           const bool quad = !refill && cas && !pipe && !lean && gm != kGmRuntime && !frz && opt_int("KDB_QUAD", 0) != 0;
-          if (quad) {
+          // level-synchronous chunk scan (k_light_lvl): the same one-view CAS case
+          const bool lvl = !refill && cas && !pipe && !lean && gm != kGmRuntime && !frz && opt_int("KDB_LVL", 0) != 0;
+          if (lvl) {
+            if (gm == kGmL1)
+              LAUNCH(k_light_lvl<kGmL1>, grid_for(na_ub[r]), kThreads, st, R.LE, R.n_rows, R.nbr, R.dist, ld, k,
+                     eps_run, R.row_begin, N, comp, R.act[cur], na_ub[r], R.act[cur ^ 1], nout, &R.ctr->grab, KB,
+                     &L.ctr->entries, nin, l2hint, row_chunk(na_ub[r]));
+            else
+              LAUNCH(k_light_lvl<kGmHint>, grid_for(na_ub[r]), kThreads, st, R.LE, R.n_rows, R.nbr, R.dist, ld, k,
+                     eps_run, R.row_begin, N, comp, R.act[cur], na_ub[r], R.act[cur ^ 1], nout, &R.ctr->grab, KB,
+                     &L.ctr->entries, nin, l2hint, row_chunk(na_ub[r]));
+          } else if (quad) {
             if (gm == kGmL1)
               LAUNCH(k_light_quad<kGmL1>, grid_for(na_ub[r]), kThreads, st, R.LE, R.n_rows, R.nbr, R.dist, ld, k,
                      eps_run, R.row_begin, N, comp, R.act[cur], na_ub[r], R.act[cur ^ 1], nout, &R.ctr->grab, KB,

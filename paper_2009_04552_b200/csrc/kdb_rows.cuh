@@ -209,6 +209,7 @@ struct RowScan {
   uint32_t bestb;
   int32_t bestc;  // component of the best entry's far endpoint
   int bidx;       // scan_ell: ELL column of the best entry (-1: past the ELL); else unset
+  bool cont = false;  // scan_ell<ONE>: nothing found in this chunk, the row goes on at column h
 };
 
 // Local-first phase (multi-rank exact mode): a rank contracts
@@ -643,7 +644,7 @@ __global__ void k_reuse_rows(const int4* __restrict__ LE, const uint32_t* __rest
 // GW: component gathers are issued GW entries at a time; once the minimum is
 // found only entries of its weight (decided from the loaded w) are gathered,
 // so a smaller GW trades memory-level parallelism for L2 sector traffic.
-template <bool DIRECT, int GW = 4, bool PIPE = false, int GM = kGmRuntime>
+template <bool DIRECT, int GW = 4, bool PIPE = false, int GM = kGmRuntime, bool ONE = false>
 __device__ __forceinline__ RowScan scan_ell(const int4* __restrict__ le, int64_t ps, const int32_t* __restrict__ nr,
                                             const float* __restrict__ dr, int k, float eps, int32_t v, int32_t cv,
                                             int h, int64_t N, const int32_t* __restrict__ comp, int all_core,
@@ -708,6 +709,8 @@ __device__ __forceinline__ RowScan scan_ell(const int4* __restrict__ le, int64_t
     }
     }
     c0 += 4;
+    // ONE (k_light_lvl): one chunk per visit unless a minimum's tie group runs on
+    if (ONE && !done && !r.found && c0 < kend) { r.h = c0; r.cont = true; return r; }
   }
   if (!done && k > kW) {
     // the candidate prefix (or the minimum's tie group) runs past the ELL
@@ -1406,6 +1409,116 @@ __global__ void __launch_bounds__(256, KDB_QUAD_MINB) k_light_quad(const int4* _
         }
       }
       warp_min_pair128(KB, have, cseg, okey, ob);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) s_base = s_n ? atomicAdd(n_out, s_n) : 0u;
+    __syncthreads();
+    for (uint32_t j = threadIdx.x; j < s_n; j += blockDim.x)
+      __stcs(reinterpret_cast<int2*>(act_out + s_base + j), *reinterpret_cast<const int2*>(s_rec + j));
+    __syncthreads();
+  }
+  for (int o = 16; o > 0; o >>= 1) reads += __shfl_xor_sync(0xffffffffu, reads, o);
+  if ((threadIdx.x & 31) == 0 && reads) atomicAdd(n_entries, reads);
+}
+
+// Later light rounds, one view, CAS offers, LEVEL-SYNCHRONOUS: k_light_round
+// runs a warp until its longest row is done (3.45 chunk steps per warp for 1.6
+// chunks per row in C4's round 3, 13-18 active lanes).  Here a block's records
+// are scanned one ELL chunk per level: level 0 takes the chunk of every record's
+// head; a row that found nothing there (all entries dead) is queued in shared
+// memory with its component and the next chunk's column, and level L + 1 scans
+// the queue of level L with full warps.  At most kW / 4 levels.  Queue pushes
+// keep the warp's lane order (ballot + one shared atomic per warp), so runs of
+// one component stay adjacent for warp_min_pair128.  Same scan, offers and next
+// row list (up to order) as k_light_round<4, false, true>.
+#ifndef KDB_LVL_MINB
+#define KDB_LVL_MINB 5
+#endif
+template <int GM>
+__global__ void __launch_bounds__(256, KDB_LVL_MINB) k_light_lvl(const int4* __restrict__ LE, int64_t ell_rows,
+                                                   const int32_t* __restrict__ nbr, const float* __restrict__ dist,
+                                                   int32_t ld, int32_t k, float eps, int64_t row_begin, int64_t N,
+                                                   const int32_t* __restrict__ comp, const Rec* __restrict__ act,
+                                                   uint32_t n_in, Rec* __restrict__ act_out,
+                                                   uint32_t* __restrict__ n_out, uint32_t* __restrict__ grab,
+                                                   ulonglong2* __restrict__ KB,
+                                                   unsigned long long* __restrict__ n_entries,
+                                                   const uint32_t* __restrict__ n_in_p, int l2hint, int chunk) {
+  if (n_in_p) n_in = *n_in_p;
+  LocalView lvh{};
+  if (l2hint & 1) lvh.pol = l2_evict_last_policy();
+  lvh.l1 = (l2hint >> 1) & 1;
+  constexpr int kLevels = kW / 4 + 1;
+  __shared__ __align__(16) Rec s_rec[kChunk];
+  __shared__ __align__(8) int2 s_qa[2][kChunk];  // (v, next column)
+  __shared__ int32_t s_qc[2][kChunk];            // comp[v]
+  __shared__ uint32_t s_n, s_chunk, s_base, s_nq[kLevels];
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  unsigned long long reads = 0;
+  for (;;) {
+    if (threadIdx.x == 0) { s_chunk = atomicAdd(grab, 1u); s_n = 0; }
+    if (threadIdx.x < kLevels) s_nq[threadIdx.x] = 0;
+    __syncthreads();
+    const uint64_t base = (uint64_t)s_chunk * chunk;
+    if (base >= n_in) break;
+    uint32_t n_items = (uint32_t)min((uint64_t)chunk, (uint64_t)n_in - base);
+    for (int level = 0; n_items; ++level) {
+      const int q = level & 1;
+      for (uint32_t t = 0; t < n_items; t += 256) {
+        const uint32_t s = t + threadIdx.x;
+        bool have = false, cont = false;
+        int32_t cseg = -1 - lane, v = 0, cv = 0;
+        int rh = 0;
+        uint64_t okey = ~0ull, ob = ~0ull;
+        if (s < n_items) {
+          int hh;
+          if (level == 0) {
+            const int2 a = __ldcs(reinterpret_cast<const int2*>(act + base + s));
+            v = a.x;
+            hh = a.y;
+            cv = lvh.l1 ? __ldg(comp + v) : gat(comp + v);
+          } else {
+            const int2 a = s_qa[q ^ 1][s];
+            v = a.x;
+            hh = a.y;
+            cv = s_qc[q ^ 1][s];
+          }
+          KDB_DCHECK(cv >= 0 && v >= row_begin && v < N, 8u);
+          const int64_t i = (int64_t)v - row_begin;
+          const RowScan r = scan_ell<false, 4, false, GM, true>(LE + ell_row(i), ell_ps(ell_rows), nbr + i * ld,
+                                                                dist + i * ld, k, eps, v, cv, hh, N, comp, 0, reads, lvh);
+          rh = r.h;
+          if (r.cont) cont = true;
+          else if (r.found) {
+            have = true;
+            cseg = cv;
+            okey = r.best;
+            ob = ((uint64_t)r.bestb << 32) | (uint32_t)r.bestc;
+          }
+        }
+        const unsigned mc = __ballot_sync(0xffffffffu, cont);
+        if (mc && level + 1 < kLevels) {
+          uint32_t b = 0;
+          if (lane == 0) b = atomicAdd(&s_nq[level], (uint32_t)__popc(mc));
+          b = __shfl_sync(0xffffffffu, b, 0);
+          if (cont) {
+            const uint32_t j = b + __popc(mc & lt);
+            s_qa[q][j] = make_int2(v, rh);
+            s_qc[q][j] = cv;
+          }
+        }
+        const unsigned mf = __ballot_sync(0xffffffffu, have);
+        if (mf) {
+          uint32_t b = 0;
+          if (lane == 0) b = atomicAdd(&s_n, (uint32_t)__popc(mf));
+          b = __shfl_sync(0xffffffffu, b, 0);
+          if (have) s_rec[b + __popc(mf & lt)] = Rec{v, rh};
+        }
+        warp_min_pair128(KB, have, cseg, okey, ob);
+      }
+      __syncthreads();
+      n_items = level + 1 < kLevels ? s_nq[level] : 0u;
     }
     __syncthreads();
     if (threadIdx.x == 0) s_base = s_n ? atomicAdd(n_out, s_n) : 0u;

@@ -308,7 +308,7 @@ def c4_small_graph():
     return nbr, dist, eps, oracle_run(nbr, dist, 50, eps)
 
 
-@pytest.mark.parametrize("knob", ["KDB_QUAD", "KDB_REFILL", "KDB_LEAN", "KDB_FASTSCAN", "KDB_TILE"])
+@pytest.mark.parametrize("knob", ["KDB_LVL", "KDB_QUAD", "KDB_REFILL", "KDB_LEAN", "KDB_FASTSCAN", "KDB_TILE"])
 def test_light_round_variants_kept_off(knob, c4_small_graph, monkeypatch):
     """The light-round variants that were measured slower and are off by default
     (DESIGN.md section 16 and its options table) stay parity-green on the path the

@@ -43,6 +43,10 @@ def _run(config, scale, live_window=None, order="inertial"):
     assert f"{np.float32(W['eps']).view(np.uint32):08x}" == gold["eps_bits"]
     N = W["N"]
     g = kdb.Graph(W["nbr"], W["dist"], n_total=N, exact=True)
+    # KDB_* variables of the environment (tools/ A/B scripts: a knob's full-size parity); none by default
+    knobs = kdb.options_from_env()
+    if knobs:
+        print("knobs:", knobs)
     bits, r, lab = kdb.kdbscan(g, W["M"], W["eps"])
     torch.cuda.synchronize()
     full = dict(core=kdb.unpack_core(bits, N).numpy(), comp=r.comp.cpu().numpy(), labels=lab.cpu().numpy(),
