@@ -881,7 +881,25 @@ kdb_status rows_phase(Mst& m, float eps_run) {
           const bool quad = !refill && cas && !pipe && !lean && gm != kGmRuntime && !frz && opt_int("KDB_QUAD", 0) != 0;
           // level-synchronous chunk scan (k_light_lvl): the same one-view CAS case
           const bool lvl = !refill && cas && !pipe && !lean && gm != kGmRuntime && !frz && opt_int("KDB_LVL", 0) != 0;
-          if (lvl) {
+          if (lvl && opt_int("KDB_LVL", 0) == 3) {  // pooled variant with the branch-free chunk scan
+            if (gm == kGmL1)
+              LAUNCH((k_light_pool<kGmL1, true>), grid_for(na_ub[r]), kThreads, st, R.LE, R.n_rows, R.nbr, R.dist, ld, k,
+                     eps_run, R.row_begin, N, comp, R.act[cur], na_ub[r], R.act[cur ^ 1], nout, &R.ctr->grab, KB,
+                     &L.ctr->entries, nin, l2hint, row_chunk(na_ub[r]));
+            else
+              LAUNCH((k_light_pool<kGmHint, true>), grid_for(na_ub[r]), kThreads, st, R.LE, R.n_rows, R.nbr, R.dist, ld, k,
+                     eps_run, R.row_begin, N, comp, R.act[cur], na_ub[r], R.act[cur ^ 1], nout, &R.ctr->grab, KB,
+                     &L.ctr->entries, nin, l2hint, row_chunk(na_ub[r]));
+          } else if (lvl && opt_int("KDB_LVL", 0) == 2) {  // pooled variant (k_light_pool)
+            if (gm == kGmL1)
+              LAUNCH(k_light_pool<kGmL1>, grid_for(na_ub[r]), kThreads, st, R.LE, R.n_rows, R.nbr, R.dist, ld, k,
+                     eps_run, R.row_begin, N, comp, R.act[cur], na_ub[r], R.act[cur ^ 1], nout, &R.ctr->grab, KB,
+                     &L.ctr->entries, nin, l2hint, row_chunk(na_ub[r]));
+            else
+              LAUNCH(k_light_pool<kGmHint>, grid_for(na_ub[r]), kThreads, st, R.LE, R.n_rows, R.nbr, R.dist, ld, k,
+                     eps_run, R.row_begin, N, comp, R.act[cur], na_ub[r], R.act[cur ^ 1], nout, &R.ctr->grab, KB,
+                     &L.ctr->entries, nin, l2hint, row_chunk(na_ub[r]));
+          } else if (lvl) {
             if (gm == kGmL1)
               LAUNCH(k_light_lvl<kGmL1>, grid_for(na_ub[r]), kThreads, st, R.LE, R.n_rows, R.nbr, R.dist, ld, k,
                      eps_run, R.row_begin, N, comp, R.act[cur], na_ub[r], R.act[cur ^ 1], nout, &R.ctr->grab, KB,

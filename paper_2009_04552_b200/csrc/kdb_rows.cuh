@@ -747,7 +747,7 @@ __device__ __forceinline__ RowScan scan_ell(const int4* __restrict__ le, int64_t
 // competes by (key, b); the first other weight ends the scan.  Only a row's
 // final head matters here (r.h = the minimum's column, else k), so the dead
 // prefix is not tracked entry by entry.
-template <int GM>
+template <int GM, bool ONE = false>
 __device__ __forceinline__ RowScan scan_ell_fast(const int4* __restrict__ le, int64_t ps,
                                                  const int32_t* __restrict__ nr, const float* __restrict__ dr, int k,
                                                  float eps, int32_t v, int32_t cv, int h, int64_t N,
@@ -798,6 +798,8 @@ __device__ __forceinline__ RowScan scan_ell_fast(const int4* __restrict__ le, in
       done = done || stop0 || end;
     }
     if (done) break;
+    // ONE (k_light_pool): one chunk per visit unless a minimum's tie group runs on
+    if (ONE && !found && c0 + 4 < kend) return RowScan{false, c0 + 4, best, bestb, bestc, -1, true};
   }
   if (!done && k > kW) {
     // the candidate prefix (or the minimum's tie group) runs past the ELL (rare)
@@ -1519,6 +1521,116 @@ __global__ void __launch_bounds__(256, KDB_LVL_MINB) k_light_lvl(const int4* __r
       }
       __syncthreads();
       n_items = level + 1 < kLevels ? s_nq[level] : 0u;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) s_base = s_n ? atomicAdd(n_out, s_n) : 0u;
+    __syncthreads();
+    for (uint32_t j = threadIdx.x; j < s_n; j += blockDim.x)
+      __stcs(reinterpret_cast<int2*>(act_out + s_base + j), *reinterpret_cast<const int2*>(s_rec + j));
+    __syncthreads();
+  }
+  for (int o = 16; o > 0; o >>= 1) reads += __shfl_xor_sync(0xffffffffu, reads, o);
+  if ((threadIdx.x & 31) == 0 && reads) atomicAdd(n_entries, reads);
+}
+
+// k_light_lvl with a POOL instead of levels: every block step scans one ELL
+// chunk of up to `chunk` rows -- the rows the previous step left unfinished
+// (kept in shared memory with their component and next column) plus as many
+// new records from the round's cursor as fill the step.  Deep levels then run
+// with full warps too (k_light_lvl's level 2 / 3 keep 5 / 2 of a block's 8
+// warps busy).  `grab` counts RECORDS here, not chunks.
+template <int GM, bool FAST = false>
+__global__ void __launch_bounds__(256, KDB_LVL_MINB) k_light_pool(const int4* __restrict__ LE, int64_t ell_rows,
+                                                    const int32_t* __restrict__ nbr, const float* __restrict__ dist,
+                                                    int32_t ld, int32_t k, float eps, int64_t row_begin, int64_t N,
+                                                    const int32_t* __restrict__ comp, const Rec* __restrict__ act,
+                                                    uint32_t n_in, Rec* __restrict__ act_out,
+                                                    uint32_t* __restrict__ n_out, uint32_t* __restrict__ grab,
+                                                    ulonglong2* __restrict__ KB,
+                                                    unsigned long long* __restrict__ n_entries,
+                                                    const uint32_t* __restrict__ n_in_p, int l2hint, int chunk) {
+  if (n_in_p) n_in = *n_in_p;
+  LocalView lvh{};
+  if (l2hint & 1) lvh.pol = l2_evict_last_policy();
+  lvh.l1 = (l2hint >> 1) & 1;
+  __shared__ __align__(16) Rec s_rec[kChunk];
+  __shared__ __align__(8) int2 s_qa[2][kChunk];  // (v, next column)
+  __shared__ int32_t s_qc[2][kChunk];            // comp[v]
+  __shared__ uint32_t s_n, s_in, s_base, s_np[2];
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  unsigned long long reads = 0;
+  if (threadIdx.x < 2) s_np[threadIdx.x] = 0;
+  __syncthreads();
+  bool dry = false;  // the cursor ran past the list (block-uniform)
+  for (int p = 0;; p ^= 1) {
+    const uint32_t np = s_np[p];
+    const uint32_t want = dry ? 0u : (uint32_t)chunk - np;
+    if (threadIdx.x == 0) {
+      s_in = want ? atomicAdd(grab, want) : n_in;
+      s_n = 0;
+      s_np[p ^ 1] = 0;
+    }
+    __syncthreads();
+    const uint32_t b = s_in;
+    const uint32_t avail = b < n_in ? min(want, n_in - b) : 0u;
+    if (avail < want || !want) dry = true;
+    const uint32_t n_items = np + avail;
+    if (n_items == 0) break;
+    for (uint32_t t = 0; t < n_items; t += 256) {
+      const uint32_t s = t + threadIdx.x;
+      bool have = false, cont = false;
+      int32_t cseg = -1 - lane, v = 0, cv = 0;
+      int rh = 0;
+      uint64_t okey = ~0ull, ob = ~0ull;
+      if (s < n_items) {
+        int hh;
+        if (s >= np) {
+          const int2 a = __ldcs(reinterpret_cast<const int2*>(act + b + (s - np)));
+          v = a.x;
+          hh = a.y;
+          cv = lvh.l1 ? __ldg(comp + v) : gat(comp + v);
+        } else {
+          const int2 a = s_qa[p][s];
+          v = a.x;
+          hh = a.y;
+          cv = s_qc[p][s];
+        }
+        KDB_DCHECK(cv >= 0 && v >= row_begin && v < N, 8u);
+        const int64_t i = (int64_t)v - row_begin;
+        const RowScan r = FAST
+            ? scan_ell_fast<GM, true>(LE + ell_row(i), ell_ps(ell_rows), nbr + i * ld, dist + i * ld, k, eps, v, cv, hh, N,
+                                      comp, reads, lvh)
+            : scan_ell<false, 4, false, GM, true>(LE + ell_row(i), ell_ps(ell_rows), nbr + i * ld, dist + i * ld, k, eps,
+                                                  v, cv, hh, N, comp, 0, reads, lvh);
+        rh = r.h;
+        if (r.cont) cont = true;
+        else if (r.found) {
+          have = true;
+          cseg = cv;
+          okey = r.best;
+          ob = ((uint64_t)r.bestb << 32) | (uint32_t)r.bestc;
+        }
+      }
+      const unsigned mc = __ballot_sync(0xffffffffu, cont);
+      if (mc) {
+        uint32_t bq = 0;
+        if (lane == 0) bq = atomicAdd(&s_np[p ^ 1], (uint32_t)__popc(mc));
+        bq = __shfl_sync(0xffffffffu, bq, 0);
+        if (cont) {
+          const uint32_t j = bq + __popc(mc & lt);
+          s_qa[p ^ 1][j] = make_int2(v, rh);
+          s_qc[p ^ 1][j] = cv;
+        }
+      }
+      const unsigned mf = __ballot_sync(0xffffffffu, have);
+      if (mf) {
+        uint32_t bf = 0;
+        if (lane == 0) bf = atomicAdd(&s_n, (uint32_t)__popc(mf));
+        bf = __shfl_sync(0xffffffffu, bf, 0);
+        if (have) s_rec[bf + __popc(mf & lt)] = Rec{v, rh};
+      }
+      warp_min_pair128(KB, have, cseg, okey, ob);
     }
     __syncthreads();
     if (threadIdx.x == 0) s_base = s_n ? atomicAdd(n_out, s_n) : 0u;

@@ -308,13 +308,13 @@ def c4_small_graph():
     return nbr, dist, eps, oracle_run(nbr, dist, 50, eps)
 
 
-@pytest.mark.parametrize("knob", ["KDB_LVL", "KDB_QUAD", "KDB_REFILL", "KDB_LEAN", "KDB_FASTSCAN", "KDB_TILE"])
+@pytest.mark.parametrize("knob", ["KDB_LVL", "KDB_LVL=2", "KDB_LVL=3", "KDB_QUAD", "KDB_REFILL", "KDB_LEAN", "KDB_FASTSCAN", "KDB_TILE"])
 def test_light_round_variants_kept_off(knob, c4_small_graph, monkeypatch):
     """The light-round variants that were measured slower and are off by default
     (DESIGN.md section 16 and its options table) stay parity-green on the path the
     bench runs (one rank, exact graph, light split): the C4 recipe at 128K points,
     and small clustered point sets with duplicate points (ties, w = 0)."""
-    _kdb_opt(knob, "1")
+    _kdb_opt(knob.split("=")[0], knob.split("=")[1] if "=" in knob else "1")
     nbr, dist, eps, exp = c4_small_graph
     assert_parity(run_gpu(nbr, dist, 50, eps, exact=True), exp)
     _kdb_opt("KDB_LIGHT", "6")
