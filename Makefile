@@ -25,6 +25,11 @@ paper_2009_04552_b200/lib/libkdb_ellplanes.so: paper_2009_04552_b200/csrc/kdb.cu
 	@mkdir -p $(dir $@)
 	$(NVCC) $(NVFLAGS) -DKDB_ELL_PLANES=1 -o $@ $< -ldl
 
+# A/B builds: slim light-round hot loop (KDB_SLIM = 1, 2, 3: see kdb_rows.cuh)
+paper_2009_04552_b200/lib/libkdb_slim%.so: paper_2009_04552_b200/csrc/kdb.cu $(wildcard paper_2009_04552_b200/csrc/kdb_*.cuh) include/kdb.h
+	@mkdir -p $(dir $@)
+	$(NVCC) $(NVFLAGS) -DKDB_SLIM=$* -o $@ $< -ldl
+
 $(KNNG_SO): paper_2009_04552_b200/csrc/knng.cu include/knng.h
 	@mkdir -p $(dir $@)
 	$(NVCC) $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -shared -Iinclude -o $@ $<

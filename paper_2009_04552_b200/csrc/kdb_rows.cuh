@@ -202,8 +202,18 @@ __device__ __forceinline__ void load_chunk(const int32_t* nr, const float* dr, i
   }
 }
 
+#ifndef KDB_SLIM
+#define KDB_SLIM 1  // 1 (default) = loop-carried scan flags in full registers instead of packed bytes (54 -> 15 PRMT
+#endif              // in k_light_round, C4 light rounds 10.17 -> 10.08 ms); A/B builds libkdb_slim<n>.so: 0 = bool flags;
+                    // 2 = + scan_ell's tail out of line (11.9 ms: the call pins the scan state); 3 = + record loop not
+                    // unrolled (12.1 ms)
+#if KDB_SLIM
+typedef int scan_flag_t;
+#else
+typedef bool scan_flag_t;
+#endif
 struct RowScan {
-  bool found;
+  scan_flag_t found;
   int h;          // new head: the first leaving entry, or k when exhausted
   uint64_t best;  // minimum key of the group
   uint32_t bestb;
@@ -644,6 +654,34 @@ __global__ void k_reuse_rows(const int4* __restrict__ LE, const uint32_t* __rest
 // GW: component gathers are issued GW entries at a time; once the minimum is
 // found only entries of its weight (decided from the loaded w) are gathered,
 // so a smaller GW trades memory-level parallelism for L2 sector traffic.
+// The rare tail of scan_ell (the candidate prefix or the minimum's tie group runs
+// past the kW ELL columns into the graph row), out of line under KDB_SLIM so the
+// light-round kernels' hot loop stays small (2,768 SASS instructions with it inline;
+// ncu: ~7% of stall samples are no_instruction).
+template <bool DIRECT, int GM>
+__device__ __noinline__ void scan_ell_tail(RowScan& r, uint32_t wstar, const int32_t* __restrict__ nr,
+                                           const float* __restrict__ dr, int k, float eps, int32_t v, int32_t cv, int h,
+                                           int64_t N, const int32_t* __restrict__ comp, int all_core,
+                                           unsigned long long& reads, const LocalView& lv) {
+  if (!r.found) {
+    r = scan_row<false, DIRECT>(nr, dr, k, eps, v, cv, max(h, kW), N, comp, all_core, reads, lv);
+    r.bidx = -1;
+    return;
+  }
+  for (int c = kW; c < k; ++c) {
+    const float wc = __ldcg(dr + c);
+    if (mono_bits(wc) != wstar || !(wc <= eps)) break;
+    const int32_t Jc = __ldcg(nr + c);
+    ++reads;
+    if (Jc < 0 || Jc >= N || Jc == v) continue;
+    const int32_t cc = comp_of_m<GM>(comp, Jc, DIRECT && all_core, lv);
+    if (cc < 0 || (!DIRECT && cc == cv)) continue;
+    const uint64_t kk = pack_key(wstar, (uint32_t)min(v, Jc));
+    const uint32_t bb = (uint32_t)max(v, Jc);
+    if (kk < r.best || (kk == r.best && bb < r.bestb)) { r.best = kk; r.bestb = bb; r.bestc = cc; r.bidx = -1; }
+  }
+}
+
 template <bool DIRECT, int GW = 4, bool PIPE = false, int GM = kGmRuntime, bool ONE = false>
 __device__ __forceinline__ RowScan scan_ell(const int4* __restrict__ le, int64_t ps, const int32_t* __restrict__ nr,
                                             const float* __restrict__ dr, int k, float eps, int32_t v, int32_t cv,
@@ -653,7 +691,7 @@ __device__ __forceinline__ RowScan scan_ell(const int4* __restrict__ le, int64_t
   uint32_t wstar = 0;
   const int kend = min(k, kW);
   int c0 = h & ~3;
-  bool done = false;
+  scan_flag_t done = false;
   // PIPE: the next chunk's load is issued with the current one, so a row whose
   // chunk holds no leaving entry does not wait a second load latency (chosen per
   // input: pays when many rows scan past their first chunk, see rows_phase)
@@ -712,6 +750,13 @@ __device__ __forceinline__ RowScan scan_ell(const int4* __restrict__ le, int64_t
     // ONE (k_light_lvl): one chunk per visit unless a minimum's tie group runs on
     if (ONE && !done && !r.found && c0 < kend) { r.h = c0; r.cont = true; return r; }
   }
+#if KDB_SLIM >= 2
+  if (!done && k > kW) {
+    const bool was_found = r.found;
+    scan_ell_tail<DIRECT, GM>(r, wstar, nr, dr, k, eps, v, cv, h, N, comp, all_core, reads, lv);
+    if (!was_found) return r;
+  }
+#else
   if (!done && k > kW) {
     // the candidate prefix (or the minimum's tie group) runs past the ELL
     if (!r.found) {
@@ -733,6 +778,7 @@ __device__ __forceinline__ RowScan scan_ell(const int4* __restrict__ le, int64_t
       if (kk < r.best || (kk == r.best && bb < r.bestb)) { r.best = kk; r.bestb = bb; r.bestc = cc; r.bidx = -1; }
     }
   }
+#endif
   if (!r.found) r.h = k;
   return r;
 }
@@ -1020,6 +1066,9 @@ __global__ void __launch_bounds__(256) k_light_round(const int4* __restrict__ LE
     __syncthreads();
     const uint64_t base = (uint64_t)s_chunk * chunk;
     if (base >= n_in) break;
+#if KDB_SLIM >= 3
+#pragma unroll 1
+#endif
     for (int t = 0; t < chunk; t += 256) {
       const uint64_t s = base + t + threadIdx.x;
       // CAS: the warp's offers are min-reduced over runs of lanes offering to
